@@ -1,0 +1,386 @@
+"""Benchmark of the B200 hot path (BASELINE config 2 by default).
+
+A "step" = one F(u), one J(u)v and one J(u)^T w apply over the full config-2
+field (E = 2^22 elements, N = 7, 29,360,128 DOF, fp64), inputs resident in
+HBM.  value = 3 * DOF / step time ("apply-DOF/s" summed over the three
+operators).  Each field is 235 MB, larger than the 126 MB L2, so no flush is
+needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference algorithm's CPU implementation (the numpy
+port in oracle/, bit-identical to semopt 0.1.0 on the golden fixtures) on the
+host cores, on a bounded sample of the same workload.
+Under torchrun (N > 1) every rank runs its own independent config-2 problem
+(weak scaling, no data-path collective); timing is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BYTES_PER_DOF = {"F": 16, "J": 24, "JT": 24}
+METRIC = "fp64 DOF/s for F(u), J*v and J^T*w applies (summed), BASELINE config 2"
+
+
+def flop_per_dof(N, op):
+    n = N + 1
+    per_elem = 4 * n * n + 3 * n + N + 1 if op == "F" else 6 * n * n + 5 * n + N + 1
+    return per_elem / N
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-sweep", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+# ----------------------------------------------------------------------------- CPU arm
+
+
+def cpu_reference_step_sample(E_sample, reps, seed):
+    """Time the reference algorithm (oracle port) on E_sample elements of config 2."""
+    import numpy as np
+
+    from oracle import semref as R
+    from paper_1806_01422_b200 import configs
+
+    c = configs.CFG2
+    h = (c["xb"] - c["xa"]) / c["E"]
+    mesh = R.Mesh1D(0.0, E_sample * h, E_sample, c["N"], True)   # same h, N, nu as config 2
+    op = R.BurgersOracle(mesh, c["nu"])
+    u, v, w = configs.operator_inputs(mesh.ndof, seed)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        op.rhs(u)
+        op.jac(u, v)
+        op.jact(u, w)
+        times.append(time.perf_counter() - t0)
+    del np
+    return mesh.ndof, times
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    E_sample = 1 << 18
+    ndof, times = cpu_reference_step_sample(E_sample, args.warmup + args.steps, seed=12)
+    timed = times[args.warmup:]
+    total = sum(timed)
+    value = 3 * ndof * len(timed) / total
+    cores = host_cores()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "DOF/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * total / len(timed), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded U(-1,1), N(0,1) per node)",
+        "config": {"workload": "BASELINE config 2 (1D Burgers, N=7, nu=0.01, periodic [-1,1])",
+                   "E": 1 << 22, "N": 7, "sample_E": E_sample, "sample_dof": ndof},
+        "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": cores, "kind": "port",
+                         "sample": f"F+J+J^T on E=2^18 of config 2 (same h, N, nu), "
+                                   f"numpy/OpenBLAS port of semopt ops.py, {cores} host threads"},
+        "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons via NVML while the timed region runs."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._thread = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as exc:  # pragma: no cover - depends on the box
+            self.nvml = None
+            self.err = str(exc)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM))
+                mask = self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if mask & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:  # pragma: no cover
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nvml is not None:
+            self._thread = threading.Thread(target=self._run, daemon=True)
+            self._thread.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._thread is not None:
+            self._thread.join()
+
+    def summary(self):
+        if self.nvml is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": self.err}
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic():
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            return json.load(fh)
+    return {}
+
+
+def timed_ops(op, ud, vd, wd, outs, steps, stream):
+    """Run `steps` steps of (F, J, J^T) with per-launch CUDA events on the launching stream."""
+    import torch
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+    with torch.cuda.stream(stream):
+        for s in range(steps):
+            e = ev[s]
+            e[0].record(stream)
+            op.launch_rhs(ud, outs[0])
+            e[1].record(stream)
+            op.launch_jac(ud, vd, outs[1])
+            e[2].record(stream)
+            op.launch_jact(ud, wd, outs[2])
+            e[3].record(stream)
+    stream.synchronize()
+    per = {"F": [], "J": [], "JT": []}
+    for e in ev:
+        per["F"].append(e[0].elapsed_time(e[1]))
+        per["J"].append(e[1].elapsed_time(e[2]))
+        per["JT"].append(e[2].elapsed_time(e[3]))
+    total = ev[0][0].elapsed_time(ev[-1][3])
+    return total, per
+
+
+def sweep_ratio(op, torch, steps=8):
+    """Forward RK4 sweep vs discrete-adjoint sweep on the config-2 field (store-all)."""
+    from paper_1806_01422_b200 import adjoint, checkpoint, timeloop
+    ts = timeloop.TsConfig(scheme="rk4", t0=0.0, t_end=steps * 1e-6, dt=1e-6)
+    u0 = torch.sin(torch.linspace(0, 6.283185307179586, op.ndof, dtype=torch.float64,
+                                  device=op.device))
+    timeloop.integrate(op, u0, ts)  # warm-up
+    torch.cuda.synchronize()
+    a, b, c, d = (torch.cuda.Event(enable_timing=True) for _ in range(4))
+    a.record()
+    fwd = timeloop.integrate(op, u0, ts)
+    b.record()
+    sched = checkpoint.plan_store_all(fwd.n_steps)
+    j, lam = adjoint.terminal_condition(op.grid, fwd.u_final, 0.5 * u0, op=op)
+    c.record()
+    adjoint.sweep(op, ts, fwd, sched, lam)
+    d.record()
+    torch.cuda.synchronize()
+    f_ms, a_ms = a.elapsed_time(b), c.elapsed_time(d)
+    return {"scheme": "rk4", "steps": steps, "forward_ms": f_ms, "adjoint_ms": a_ms,
+            "adjoint_over_forward": a_ms / f_ms}
+
+
+def run_gpu_arm(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_1806_01422_b200 import configs
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    c = configs.CFG2
+    op = configs.cfg_operator(c, device=dev)
+    op.sync_checks = False
+    ndof = op.ndof
+    u, v, w = configs.operator_inputs(ndof, c["seed"] + rank)
+    ud, vd, wd = (torch.from_numpy(a).to(dev) for a in (u, v, w))
+    outs = [op.empty() for _ in range(3)]
+    stream = torch.cuda.current_stream(dev)
+
+    # warm-up
+    timed_ops(op, ud, vd, wd, outs, max(1, args.warmup), stream)
+    if op.flags():
+        raise RuntimeError("non-finite flag raised on config-2 inputs")
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        total_ms, per = timed_ops(op, ud, vd, wd, outs, args.steps, stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+        dist.barrier()
+    ms_step = total_ms / args.steps
+    value = 3 * ndof * world / (ms_step * 1e-3)
+
+    # e2e through the public API with pinned host buffers, copies inside the timed region
+    uh, vh, wh = (torch.from_numpy(a).pin_memory() for a in (u, v, w))
+    oh = [torch.empty(ndof, dtype=torch.float64).pin_memory() for _ in range(3)]
+    e2e_steps = max(2, min(5, args.steps))
+
+    def e2e_step():
+        du = uh.to(dev, non_blocking=True)
+        dv = vh.to(dev, non_blocking=True)
+        dw = wh.to(dev, non_blocking=True)
+        f = op.apply_rhs(du)
+        jv = op.apply_jacobian(du, dv)
+        jt = op.apply_jacobian_transpose(du, dw)
+        oh[0].copy_(f, non_blocking=True)
+        oh[1].copy_(jv, non_blocking=True)
+        oh[2].copy_(jt, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for _ in range(e2e_steps):
+        e2e_step()
+    s1.record()
+    torch.cuda.synchronize()
+    e2e_ms = s0.elapsed_time(s1) / e2e_steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = 3 * ndof * world / (e2e_ms * 1e-3)
+    if op.flags():
+        raise RuntimeError("non-finite flag raised in e2e")
+
+    sweep = None
+    if not args.no_sweep:
+        sweep = sweep_ratio(op, torch)
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = load_peaks()
+    per_op = {}
+    for k, lst in per.items():
+        avg_ms = sum(lst) / len(lst)
+        gbs = BYTES_PER_DOF[k] * ndof / (avg_ms * 1e-3) / 1e9
+        per_op[k] = {"avg_us": 1e3 * avg_ms, "dof_per_s": ndof / (avg_ms * 1e-3),
+                     "achieved_gbs": gbs, "hbm_frac": gbs / peak,
+                     "fp64_tflops": flop_per_dof(c["N"], "F" if k == "F" else "J") * ndof
+                     / (avg_ms * 1e-3) / 1e12}
+    dom = max(per_op, key=lambda k: per_op[k]["avg_us"])
+    traffic = load_traffic().get({"F": "rhs", "J": "jac", "JT": "jact"}[dom])
+    cpu = None
+    if not args.no_cpu_baseline:
+        ndof_s, times = cpu_reference_step_sample(1 << 20, 3, seed=12)
+        cpu_v = 3 * ndof_s / min(times)
+        cores = host_cores()
+        cpu = {"value": cpu_v, "unit": "DOF/s", "cores": cores, "kind": "port",
+               "sample": f"F+J+J^T once each on E=2^20 of config 2 (same h, N, nu; {ndof_s} DOF), "
+                         f"min of 3 reps, numpy/OpenBLAS port of semopt ops.py, {cores} threads"}
+    line = {
+        "metric": METRIC, "value": value, "unit": "DOF/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded u~U(-1,1), v,w~N(0,1) per node)",
+        "config": {"workload": "BASELINE config 2: 1D Burgers, E=2^22, N=7, nu=0.01, periodic [-1,1]",
+                   "E": c["E"], "N": c["N"], "dof": ndof, "per_rank_problem": "independent",
+                   "l2": "inputs 235 MB/field > 126 MB L2, no flush",
+                   "parallelism": f"replicas x{world}"},
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": per_op[dom]["achieved_gbs"],
+                     "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                     "frac": per_op[dom]["hbm_frac"], "traffic": traffic,
+                     "algorithmic_bytes_per_launch": BYTES_PER_DOF[dom] * ndof},
+        "per_op": per_op,
+        "ratios": {"JT_over_J": per_op["JT"]["avg_us"] / per_op["J"]["avg_us"],
+                   "JT_over_F": per_op["JT"]["avg_us"] / per_op["F"]["avg_us"],
+                   "sweep": sweep},
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "DOF/s", "h2d_bytes_per_step": 3 * 8 * ndof,
+                "d2h_bytes_per_step": 3 * 8 * ndof, "ms_per_step": e2e_ms,
+                "path": "SemOperator.apply_* on pinned host->device copies, results copied back"},
+        "gpu_launches": 3 * args.steps,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    del np
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

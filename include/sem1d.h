@@ -1,0 +1,123 @@
+/*
+ * sem1d.h -- C ABI of the B200 (sm_100a) 1D GLL spectral-element Burgers hot path.
+ *
+ * This is the drop-in boundary.  The reference (semopt 0.1.0, pure Python) has
+ * no FFI: its plugin surface is the duck-typed operator object that the time
+ * loop and the adjoint sweep call.  Each entry point below
+ * replaces one reference call site:
+ *
+ *   sem1d_plan_create  <- SemOperator.__init__          ops.py:91-124
+ *                         (D, Dw, K, M^-1 built on the host, grid.py:126-146)
+ *   sem1d_rhs          <- SemOperator.apply_rhs          ops.py:232-236
+ *   sem1d_jac          <- SemOperator.apply_jacobian     ops.py:238-244
+ *   sem1d_jact         <- SemOperator.apply_jacobian_transpose  ops.py:246-257
+ *   sem1d_rk_stage     <- one stage of step_rk3 / rk3_stages  timeloop.py:111-130
+ *                         (F apply fused with the stage linear combination)
+ *   sem1d_adj_stage    <- one stage of adjoint_step_rk3       adjoint.py:54-61
+ *                         (J^T apply fused with the stage-adjoint recurrence)
+ *   sem1d_terminal     <- terminal_condition                 adjoint.py:33-47
+ *   sem1d_scatter / sem1d_gather <- Grid.scatter / Grid.gather  grid.py:165-182
+ *
+ * Conventions (mirror the reference contract, ops.py:216-230):
+ *  - every array is fp64 in DEVICE memory owned by the caller; nothing is
+ *    allocated inside a compute call; inputs are never written;
+ *  - fields are `batch` consecutive vectors of `ndof` doubles
+ *    (ndof = E*N periodic, E*N+1 homogeneous Dirichlet, grid.py:61-63);
+ *  - calls are stream ordered (`stream` is a cudaStream_t, NULL = legacy default);
+ *  - non-finite inputs do not abort the kernel: they OR a bit into *flag
+ *    (device int), which the host maps to NumericFailure / StepFailure;
+ *  - return value: 0 ok, SEM1D_EINVAL bad argument, SEM1D_ECUDA launch error
+ *    (message via sem1d_last_error()).
+ */
+#ifndef SEM1D_H
+#define SEM1D_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SEM1D_OK 0
+#define SEM1D_EINVAL (-1)
+#define SEM1D_ECUDA (-2)
+
+/* bits OR-ed into *flag */
+#define SEM1D_FLAG_STATE_NONFINITE 1   /* first input (state u) had NaN/Inf  -> NumericFailure */
+#define SEM1D_FLAG_INPUT2_NONFINITE 2  /* second input (v / z) had NaN/Inf  -> NumericFailure */
+#define SEM1D_FLAG_STEP_NONFINITE 4    /* a new RK state is non-finite      -> StepFailure   */
+
+#define SEM1D_MAX_DEGREE 32
+#define SEM1D_MAX_TERMS 5
+
+typedef struct sem1d_plan sem1d_plan;
+
+/* Library identity. */
+int sem1d_version(void);
+const char* sem1d_last_error(void);
+int sem1d_max_degree(void);
+
+/* Operator plan = SemOperator(grid_1d(xa, xb, E, N, bc), PdeCoefficients(nu)).
+ * K, Dw: (N+1)x(N+1) row-major host arrays (ops.py:104-106).
+ * mass_pattern, minv_pattern: N+2 host doubles each, the assembled mass
+ * diagonal (grid.py:128-131) and its reciprocal (ops.py:116) by position:
+ *   [0]      element-interface node (local index 0),
+ *   [i]      interior local node i, 1 <= i <= N-1,
+ *   [N]      first global node of a Dirichlet grid,
+ *   [N+1]    last global node of a Dirichlet grid.
+ * A uniform mesh needs nothing else; no (ndof,) M^-1 array is ever read.
+ * The constants are copied into the plan (kernel-parameter space). */
+int sem1d_plan_create(int64_t n_elements, int degree, int periodic, double nu,
+                      const double* K, const double* Dw, const double* mass_pattern,
+                      const double* minv_pattern, int64_t batch, sem1d_plan** out);
+int sem1d_plan_destroy(sem1d_plan* plan);
+int64_t sem1d_plan_ndof(const sem1d_plan* plan);
+
+/* f = M^-1 Q^T F_e(Q u) (masked).  ops.py:232-236 */
+int sem1d_rhs(const sem1d_plan* plan, const double* u, double* f, int* flag, void* stream);
+/* out = M^-1 Q^T J_e(Qu) Q v (masked).  ops.py:238-244 */
+int sem1d_jac(const sem1d_plan* plan, const double* u, const double* v, double* out,
+              int* flag, void* stream);
+/* out = Q^T J_e^T(Qu) Q mask(M^-1 z) (masked).  ops.py:246-257 */
+int sem1d_jact(const sem1d_plan* plan, const double* u, const double* z, double* out,
+               int* flag, void* stream);
+
+/* One explicit-RK stage, F fused with its linear combination:
+ *   k      = F(U_in)                                  (written to k_out if non-NULL)
+ *   Y      = base + dt * sum_j coef[j] * K_j          (association of timeloop.py:114-127:
+ *                                                      one term -> base + (dt*coef)*K,
+ *                                                      several -> base + dt*((c0 K0 + c1 K1) + ...))
+ * where K_j = terms[j], or the freshly computed k when terms[j] == NULL.
+ * If check_step != 0 a non-finite Y sets SEM1D_FLAG_STEP_NONFINITE (timeloop.py:100-103,129). */
+int sem1d_rk_stage(const sem1d_plan* plan, const double* U_in, double* k_out,
+                   const double* base, int nterms, const double* const* terms,
+                   const double* coef, double dt, double* Y, int check_step,
+                   int* flag, void* stream);
+
+/* One stage of the discrete-adjoint recurrence (adjoint.py:54-61, generalised):
+ *   z      = b * lam + sum_j a[j] * l_j                (left to right)
+ *   l      = dt * J^T(U) z                             (written to l_out if non-NULL)
+ *   lam_out = ((lam + L_0) + L_1) + ...                (only if lam_out != NULL)
+ * where L_j = acc_terms[j], or the fresh l when acc_terms[j] == NULL. */
+int sem1d_adj_stage(const sem1d_plan* plan, const double* U, const double* lam, double b,
+                    int nl, const double* const* l_terms, const double* a,
+                    double dt, double* l_out,
+                    int nacc, const double* const* acc_terms, double* lam_out,
+                    int* flag, void* stream);
+
+/* Terminal condition (adjoint.py:33-47): d = uN - ud, lam = mask(2 M d),
+ * J_out[b] = d^T M d per batch member (deterministic two-level reduction;
+ * `work` must hold sem1d_terminal_work_size(plan) doubles). */
+int64_t sem1d_terminal_work_size(const sem1d_plan* plan);
+int sem1d_terminal(const sem1d_plan* plan, const double* uN, const double* ud, double* lam,
+                   double* J_out, double* work, void* stream);
+
+/* Assembly maps (grid.py:165-182): local blocks are (batch, E, N+1). */
+int sem1d_scatter(const sem1d_plan* plan, const double* u, double* local, void* stream);
+int sem1d_gather(const sem1d_plan* plan, const double* local, double* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SEM1D_H */

@@ -1,0 +1,399 @@
+"""CPU oracle for the 1D GLL spectral-element Burgers hot path.
+
+TEST INFRASTRUCTURE ONLY.  This module is the checker, never the product:
+only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its
+``cpu_baseline`` leg and ``--impl reference`` arm) may import it.  The
+product package ``paper_1806_01422_b200`` must never import anything from
+``oracle/``; its compute path runs only through the sm_100a C-ABI library.
+
+It is a numpy restatement of the reference algorithm (``semopt`` 0.1.0 under
+``/root/reference/pkg/src/semopt``), one function per reference function,
+each citing the file:line it follows.  The arithmetic deliberately uses the
+same numpy primitives and the same evaluation order as the reference
+(fancy-index scatter, BLAS ``x @ A.T`` contractions, ``bincount`` gather), so
+that on the same machine it reproduces the reference bit for bit.
+
+Parity pin: ``tests/golden/make_golden.py`` imports the real reference in the
+build container and writes ``tests/golden/*.npz``; ``tests/test_oracle.py``
+checks this module against those fixtures (bit-exact for GLL/D/K, maps,
+mass, operator applies, RK3 sweeps and schedules).  RK4 does not exist in the
+reference (``timeloop.py:63-64`` accepts euler/rk3/cn); the RK4 pieces here are
+a restatement of the reference stage pattern (``timeloop.py:111-130``) and
+stage-adjoint recurrence (``adjoint.py:54-61``) with the classic tableau,
+pinned by central finite differences instead of golden vectors.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+# --------------------------------------------------------------------------
+# basis (reference basis.py)
+# --------------------------------------------------------------------------
+
+NEWTON_TOL = 1e-14      # basis.py:19
+NEWTON_MAXIT = 100      # basis.py:20
+
+
+def legendre_pair(deg, x):
+    """P_deg and P'_deg by the 3-term recurrence (basis.py:48-66)."""
+    x = np.asarray(x, dtype=float)
+    p0, d0 = np.ones_like(x), np.zeros_like(x)
+    if deg == 0:
+        return p0, d0
+    p1, d1 = x.copy(), np.ones_like(x)
+    for k in range(1, deg):
+        p2 = ((2 * k + 1) * x * p1 - k * p0) / (k + 1)
+        d2 = ((2 * k + 1) * (p1 + x * d1) - k * d0) / (k + 1)
+        p0, p1, d0, d1 = p1, p2, d1, d2
+    return p1, d1
+
+
+def gll_nodes_weights(deg):
+    """GLL nodes and weights (basis.py:69-117): damped Newton on P'_N from
+    Chebyshev-Lobatto guesses, then exact symmetrisation."""
+    n = int(deg)
+    if n < 1:
+        raise ValueError("degree must be >= 1")
+    xs = np.empty(n + 1)
+    xs[0], xs[n] = -1.0, 1.0
+    if n >= 2:
+        x = -np.cos(np.pi * np.arange(1, n) / n)
+        cap = 0.5 * (np.pi / n)
+        for _ in range(NEWTON_MAXIT):
+            p, dp = legendre_pair(n, x)
+            ddp = (2.0 * x * dp - n * (n + 1) * p) / (1.0 - x * x)
+            step = np.clip(dp / ddp, -cap, cap)
+            x = x - step
+            if np.max(np.abs(step)) <= NEWTON_TOL:
+                break
+        else:
+            raise ArithmeticError("GLL Newton did not converge")
+        xs[1:n] = x
+    xs = 0.5 * (xs - xs[::-1])
+    xs[0], xs[n] = -1.0, 1.0
+    pn, _ = legendre_pair(n, xs)
+    wts = 2.0 / (n * (n + 1) * pn * pn)
+    wts = 0.5 * (wts + wts[::-1])
+    return xs, wts
+
+
+def diff_matrix(xs):
+    """Barycentric differentiation matrix, diagonal = -row sum (basis.py:120-134)."""
+    xs = np.asarray(xs, dtype=float)
+    dx = xs[:, None] - xs[None, :]
+    np.fill_diagonal(dx, 1.0)
+    bw = 1.0 / np.prod(dx, axis=1)
+    d = (bw[None, :] / bw[:, None]) / dx
+    np.fill_diagonal(d, 0.0)
+    np.fill_diagonal(d, -np.sum(d, axis=1))
+    return d
+
+
+# --------------------------------------------------------------------------
+# 1D mesh (reference grid.py, 1D subset)
+# --------------------------------------------------------------------------
+
+
+class Mesh1D:
+    """Uniform 1D mesh with the reference assembly maps (grid.py:30-189)."""
+
+    def __init__(self, xa, xb, E, N, periodic=True):
+        self.xa, self.xb, self.E, self.N = float(xa), float(xb), int(E), int(N)
+        self.periodic = bool(periodic)
+        self.h = (self.xb - self.xa) / self.E                       # grid.py:57-58
+        self.ndof = E * N if periodic else E * N + 1                # grid.py:61-63
+        self.xi, self.rho = gll_nodes_weights(N)
+        self.D = diff_matrix(self.xi)
+        e = np.arange(E)[:, None]
+        i = np.arange(N + 1)[None, :]
+        tab = e * N + i                                             # grid.py:65-72
+        if periodic:
+            tab = tab % self.ndof
+        self.table = np.ascontiguousarray(tab)
+        self.multiplicity = self.assemble(np.ones((E, N + 1)))      # grid.py:126-127
+        self.mass = self.assemble(np.broadcast_to((self.h / 2.0) * self.rho, (E, N + 1)))
+        self.maskv = np.ones(self.ndof)                             # grid.py:135-143
+        if not periodic:
+            self.maskv[0] = 0.0
+            self.maskv[-1] = 0.0
+
+    def assemble(self, local):
+        """Q^T: bincount direct-stiffness summation (grid.py:157-161)."""
+        return np.bincount(self.table.ravel(), weights=np.ascontiguousarray(local).ravel(),
+                           minlength=self.ndof)
+
+    def localize(self, u):
+        """Q: global -> (E, N+1) element copies (grid.py:165-169)."""
+        return np.asarray(u, dtype=float)[self.table]
+
+    def apply_mask(self, u):
+        return u if self.periodic else u * self.maskv              # grid.py:184-189
+
+    def coordinates(self):
+        """Node coordinates (grid.py:74-84)."""
+        out = np.empty(self.ndof)
+        for e in range(self.E):
+            a = self.xa + e * self.h
+            out[self.table[e]] = a + self.h * (self.xi + 1.0) / 2.0
+        if self.periodic:
+            out[0] = self.xa
+        return out
+
+
+# --------------------------------------------------------------------------
+# operators (reference ops.py, 1D Burgers)
+# --------------------------------------------------------------------------
+
+
+class BurgersOracle:
+    """F(u), J(u)v, J(u)^T z exactly as ops.py:161-257 evaluates them in 1D."""
+
+    def __init__(self, mesh, nu):
+        self.mesh, self.nu = mesh, float(nu)
+        m = mesh
+        self.Dw = m.D * m.rho[:, None]                              # ops.py:104
+        k = (2.0 / m.h) * (m.D.T * m.rho) @ m.D                     # ops.py:105
+        self.K = 0.5 * (k + k.T)                                    # ops.py:106
+        self.minv = 1.0 / m.mass                                    # ops.py:116
+        self.counts = {"rhs": 0, "jac": 0, "jact": 0}
+
+    @staticmethod
+    def _finite(x):
+        x = np.asarray(x, dtype=float)
+        if not np.isfinite(x).all():                                # ops.py:222-223
+            raise ArithmeticError("non-finite input")
+        return x
+
+    def rhs(self, u):
+        """ops.py:161-174 + 226-236."""
+        u = self._finite(u)
+        self.counts["rhs"] += 1
+        ul = self.mesh.localize(u)
+        acc = ul @ self.K.T
+        acc *= -self.nu
+        acc -= ul * (ul @ self.Dw.T)
+        out = self.mesh.assemble(acc)
+        out *= self.minv
+        return self.mesh.apply_mask(out)
+
+    def jac(self, u, v):
+        """ops.py:176-193 + 238-244."""
+        u, v = self._finite(u), self._finite(v)
+        self.counts["jac"] += 1
+        ul, vl = self.mesh.localize(u), self.mesh.localize(v)
+        acc = vl @ self.K.T
+        acc *= -self.nu
+        acc -= vl * (ul @ self.Dw.T)
+        acc -= ul * (vl @ self.Dw.T)
+        out = self.mesh.assemble(acc)
+        out *= self.minv
+        return self.mesh.apply_mask(out)
+
+    def jact(self, u, z):
+        """ops.py:195-212 + 246-257 (M^-1 first, then element transpose)."""
+        u, z = self._finite(u), self._finite(z)
+        self.counts["jact"] += 1
+        zm = self.mesh.apply_mask(z * self.minv)
+        ul, zl = self.mesh.localize(u), self.mesh.localize(zm)
+        acc = zl @ self.K.T
+        acc *= -self.nu
+        acc -= zl * (ul @ self.Dw.T)
+        acc -= (ul * zl) @ self.Dw
+        return self.mesh.apply_mask(self.mesh.assemble(acc))
+
+    def dense_jacobian(self, u):
+        """Column-by-column J (ops.py:259-273); small grids only."""
+        n = self.mesh.ndof
+        cols = np.empty((n, n))
+        e = np.zeros(n)
+        for k in range(n):
+            e[k] = 1.0
+            cols[:, k] = self.jac(u, e)
+            e[k] = 0.0
+        return cols
+
+
+# --------------------------------------------------------------------------
+# explicit RK (reference timeloop.py; RK4 restated, see module docstring)
+# --------------------------------------------------------------------------
+
+# Butcher tableaux: (A rows, b).  RK3 = timeloop.py:24-25.
+TABLEAUX = {
+    "euler": (((),), (1.0,)),
+    "rk3": (((), (0.5,), (-1.0, 2.0)), (1.0 / 6.0, 2.0 / 3.0, 1.0 / 6.0)),
+    "rk4": (((), (0.5,), (0.0, 0.5), (0.0, 0.0, 1.0)),
+            (1.0 / 6.0, 1.0 / 3.0, 1.0 / 3.0, 1.0 / 6.0)),
+}
+
+
+def _combine(u, dt, coefs, ks):
+    """u + dt * (sum_j a_j k_j) with the reference association.
+
+    One nonzero term: u + (dt * a) * k           (timeloop.py:114, 123)
+    Several terms:    u + dt * ((a1 k1 + a2 k2) + ...)  (timeloop.py:116, 125, 127)
+    Zero coefficients are dropped.
+    """
+    terms = [(a, k) for a, k in zip(coefs, ks) if a != 0.0]
+    if len(terms) == 1:
+        a, k = terms[0]
+        return u + (dt * a) * k
+    s = terms[0][0] * terms[0][1]
+    for a, k in terms[1:]:
+        s = s + a * k
+    return u + dt * s
+
+
+def rk_stages(op, u, dt, scheme):
+    """Stage states U_1..U_s and slopes k_1..k_{s-1} (timeloop.py:111-117)."""
+    A, _ = TABLEAUX[scheme]
+    Us, ks = [u], []
+    for i in range(1, len(A)):
+        ks.append(op.rhs(Us[-1]))
+        Us.append(_combine(u, dt, A[i], ks))
+    return Us, ks
+
+
+def rk_step(op, u, dt, scheme):
+    """One explicit step (timeloop.py:106-130); returns u_new."""
+    A, b = TABLEAUX[scheme]
+    if scheme == "euler":
+        return u + dt * op.rhs(u)                                   # timeloop.py:108
+    Us, ks = rk_stages(op, u, dt, scheme)
+    ks.append(op.rhs(Us[-1]))
+    unew = _combine(u, dt, b, ks)
+    if not np.isfinite(unew).all():
+        raise FloatingPointError("step failure")                    # timeloop.py:129
+    return unew
+
+
+def adjoint_rk_step(op, u, lam, dt, scheme):
+    """Transpose of one step, stages recomputed (adjoint.py:50-61, generalised):
+    l_i = dt J^T(U_i)(b_i lam + sum_{j>i} a_ji l_j);  lam' = lam + l_1 + ... + l_s."""
+    A, b = TABLEAUX[scheme]
+    if scheme == "euler":
+        return lam + dt * op.jact(u, lam)                           # adjoint.py:50-51
+    Us, _ = rk_stages(op, u, dt, scheme)
+    s = len(b)
+    ls = [None] * s
+    for i in range(s - 1, -1, -1):
+        z = b[i] * lam
+        for j in range(i + 1, s):
+            a = A[j][i] if i < len(A[j]) else 0.0
+            if a != 0.0:
+                z = z + a * ls[j]
+        ls[i] = dt * op.jact(Us[i], z)
+    out = lam
+    for i in range(s):
+        out = out + ls[i]
+    return out
+
+
+def step_sizes(t0, t_end, dt):
+    """Fixed-dt step list with the final-step clip (timeloop.py:221-234, 264-278)."""
+    tiny = 1e-9 * dt
+    t, dts, ts = t0, [], [t0]
+    while t < t_end - tiny:
+        rem = t_end - t
+        clipped = rem - dt <= tiny
+        h = rem if clipped else dt
+        t = t_end if clipped else t + h
+        dts.append(h)
+        ts.append(t)
+    return np.asarray(ts), np.asarray(dts)
+
+
+def forward(op, u0, t0, t_end, dt, scheme):
+    """Fixed-dt forward sweep storing every state (timeloop.py:237-329)."""
+    _, dts = step_sizes(t0, t_end, dt)
+    traj = [np.asarray(u0, dtype=float).copy()]
+    u = traj[0]
+    for h in dts:
+        u = rk_step(op, u, h, scheme)
+        traj.append(u)
+    return traj, dts
+
+
+def terminal(mesh, uN, ud):
+    """J = d^T M d, lam_N = 2 M d (adjoint.py:33-47)."""
+    d = np.asarray(uN, dtype=float) - np.asarray(ud, dtype=float)
+    md = mesh.mass * d
+    j = float(np.dot(d, md))
+    return j, mesh.apply_mask(2.0 * md)
+
+
+def evaluate(op, u0, ud, t0, t_end, dt, scheme):
+    """Objective + gradient via store-all forward and adjoint sweep (problems.py:184-199)."""
+    traj, dts = forward(op, u0, t0, t_end, dt, scheme)
+    j, lam = terminal(op.mesh, traj[-1], ud)
+    for n in range(len(dts) - 1, -1, -1):
+        lam = adjoint_rk_step(op, traj[n], lam, dts[n], scheme)
+    return j, lam, traj[-1]
+
+
+# --------------------------------------------------------------------------
+# checkpoint DP (reference checkpoint.py:93-235), used to cross-check schedules
+# --------------------------------------------------------------------------
+
+
+def binomial_recompute_table(m, s):
+    """Minimal total forward evaluations for (m, s) by the reference DP
+    (checkpoint.py:101-135), computed bottom-up."""
+    f_max = s - 1
+    B = np.zeros((m + 1, f_max + 1), dtype=np.int64)
+    T = np.zeros((m + 1, f_max + 1), dtype=np.int64)
+    for l in range(m + 1):
+        for f in range(f_max + 1):
+            if l <= 1:
+                B[l, f] = 0
+            else:
+                best = l * (l - 1) // 2
+                if f >= 1:
+                    for k in range(1, l):
+                        best = min(best, k + B[l - k, f - 1] + B[k, f])
+                B[l, f] = best
+            if l == 0:
+                T[l, f] = 0
+            elif l == 1:
+                T[l, f] = 1
+            else:
+                best = l + B[l, f]
+                if f >= 1:
+                    for k in range(1, l):
+                        best = min(best, k + T[l - k, f - 1] + B[k, f])
+                T[l, f] = best
+    return int(T[m, f_max])
+
+
+# --------------------------------------------------------------------------
+# seeded inputs shared by oracle and GPU
+# --------------------------------------------------------------------------
+
+
+def seeded_fields(ndof, seed):
+    """u ~ U(-1,1), v ~ N(0,1), w ~ N(0,1), drawn per global node in node order."""
+    rng = np.random.default_rng(seed)
+    u = rng.uniform(-1.0, 1.0, ndof)
+    v = rng.standard_normal(ndof)
+    w = rng.standard_normal(ndof)
+    return u, v, w
+
+
+def timer_threads():
+    import os
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+
+def finite_difference_gradient(fun, u0, direction, eps=1e-4):
+    """Central FD of J along a direction (cli.py:237-270 methodology)."""
+    jp = fun(u0 + eps * direction)
+    jm = fun(u0 - eps * direction)
+    return (jp - jm) / (2.0 * eps)
+
+
+__all__ = [
+    "BurgersOracle", "Mesh1D", "TABLEAUX", "adjoint_rk_step", "binomial_recompute_table",
+    "diff_matrix", "evaluate", "finite_difference_gradient", "forward", "gll_nodes_weights",
+    "legendre_pair", "rk_stages", "rk_step", "seeded_fields", "step_sizes", "terminal",
+    "timer_threads",
+]

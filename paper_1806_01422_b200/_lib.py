@@ -1,0 +1,100 @@
+"""ctypes binding of ``libsemb200.so`` (the C ABI in ``include/sem1d.h``).
+
+The library is built in-tree by ``make -C paper_1806_01422_b200/csrc`` (or
+``__graft_entry__.build()``).  There is no fallback: if the library is
+missing, or no CUDA device is present, every compute entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libsemb200.so")
+
+SEM1D_FLAG_STATE_NONFINITE = 1
+SEM1D_FLAG_INPUT2_NONFINITE = 2
+SEM1D_FLAG_STEP_NONFINITE = 4
+MAX_TERMS = 5
+
+c_int, c_int64, c_double, c_void_p = ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
+c_dp = ctypes.POINTER(ctypes.c_double)
+
+# name -> (restype, argtypes); exactly the declarations of include/sem1d.h
+SIGNATURES = {
+    "sem1d_version": (c_int, []),
+    "sem1d_last_error": (ctypes.c_char_p, []),
+    "sem1d_max_degree": (c_int, []),
+    "sem1d_plan_create": (c_int, [c_int64, c_int, c_int, c_double, c_void_p, c_void_p, c_void_p,
+                                  c_void_p, c_int64, ctypes.POINTER(c_void_p)]),
+    "sem1d_plan_destroy": (c_int, [c_void_p]),
+    "sem1d_plan_ndof": (c_int64, [c_void_p]),
+    "sem1d_rhs": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "sem1d_jac": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "sem1d_jact": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "sem1d_rk_stage": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p,
+                               c_double, c_void_p, c_int, c_void_p, c_void_p]),
+    "sem1d_adj_stage": (c_int, [c_void_p, c_void_p, c_void_p, c_double, c_int, c_void_p, c_void_p,
+                                c_double, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "sem1d_terminal_work_size": (c_int64, [c_void_p]),
+    "sem1d_terminal": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "sem1d_scatter": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "sem1d_gather": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+class LibraryMissing(RuntimeError):
+    """libsemb200.so is not built or cannot be loaded (no CPU fallback exists)."""
+
+
+def load():
+    """Load (once) and return the ctypes handle; raises LibraryMissing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise LibraryMissing(
+                f"{LIB_PATH} not found: build it with `make -C {os.path.join(_HERE, 'csrc')} -j` "
+                "or __graft_entry__.build(); there is no CPU fallback")
+        try:
+            lib = ctypes.CDLL(LIB_PATH)
+        except OSError as exc:  # pragma: no cover - environment specific
+            raise LibraryMissing(f"cannot load {LIB_PATH}: {exc}") from exc
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def last_error():
+    return load().sem1d_last_error().decode("utf-8", "replace")
+
+
+def check(rc, what):
+    if rc != 0:
+        raise RuntimeError(f"{what} failed ({rc}): {last_error()}")
+
+
+def ptr_array(ptrs):
+    """ctypes array of device pointers (None -> NULL)."""
+    arr = (c_void_p * max(1, len(ptrs)))()
+    for i, p in enumerate(ptrs):
+        arr[i] = p
+    return arr
+
+
+def dbl_array(vals):
+    arr = (c_double * max(1, len(vals)))()
+    for i, v in enumerate(vals):
+        arr[i] = float(v)
+    return arr

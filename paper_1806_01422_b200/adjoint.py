@@ -1,0 +1,192 @@
+"""Discrete-adjoint backward sweep on the B200 (reference ``semopt/adjoint.py``).
+
+One adjoint step of an s-stage explicit scheme is 2s-1 fused launches: s-1
+``sem1d_rk_stage`` kernels recompute the stage states from the checkpointed
+u_n (adjoint.py:56), then s ``sem1d_adj_stage`` kernels run the stage-adjoint
+recurrence of adjoint.py:58-61, generalised to any tableau,
+
+    l_i = dt J^T(U_i) (b_i lam + sum_{j>i} a_ji l_j),   lam' = lam + l_1 + ... + l_s,
+
+each forming its J^T input while staging the slab and folding dt and the
+final accumulation into its epilogue.  ``sweep`` interprets the reference
+checkpoint schedules (checkpoint.py) over device-resident slots.
+"""
+
+from __future__ import annotations
+
+from . import _lib
+from .checkpoint import Advance, AdjointStep, Done, Restore, Store
+from .errors import CheckpointError, NumericFailure, ValidationError
+from .timeloop import TABLEAUX, _require_explicit, check_step_flags, engine_for
+
+
+def terminal_condition(grid, u_final, u_ref, op=None):
+    """(J, lam_N) with J = d^T M d, lam_N = mask(2 M d), d = u_final - u_ref (adjoint.py:33-47).
+
+    Runs as one fused reduction kernel pair on the device (needs ``op`` or an
+    operator cached on the grid)."""
+    import torch
+    op = op or getattr(grid, "_default_op", None)
+    if op is None:
+        raise ValidationError("terminal_condition on the B200 path needs the operator (op=...)")
+    uN, host = op.field(u_final, "misfit")
+    ud, _ = op.field(u_ref, "misfit")
+    lam = op.empty()
+    J = torch.empty(op.batch, dtype=torch.float64, device=op.device)
+    op.launch_terminal(uN, ud, lam, J)
+    if op.batch == 1:
+        j = float(J.item())
+        return j, (lam.cpu().numpy() if host else lam)
+    return J, lam
+
+
+class AdjointEngine:
+    """Device scratch + launch plan for one backward step of a tableau."""
+
+    def __init__(self, op, scheme):
+        self.op, self.scheme = op, scheme
+        A, b = TABLEAUX[scheme]
+        self.A, self.b, self.s = A, b, len(b)
+        self.fwd = engine_for(op, scheme)
+        self.U = [op.empty() for _ in range(self.s - 1)]
+        self.L = {i: op.empty() for i in range(1, self.s)}
+        # z-combination terms of stage i: (a_ji, j) for j > i with a_ji != 0
+        self.zterms = []
+        for i in range(self.s):
+            terms = []
+            for j in range(i + 1, self.s):
+                a = A[j][i] if i < len(A[j]) else 0.0
+                if a != 0.0:
+                    terms.append((j, float(a)))
+            self.zterms.append(terms)
+
+    def step(self, u_n, lam, dt, lam_out):
+        """lam_out = transpose of the step map at u_n applied to lam (no host sync)."""
+        op, s = self.op, self.s
+        Us = self.fwd.stages(u_n, dt, self.U) if s > 1 else [u_n]
+        for i in range(s - 1, -1, -1):
+            lts = [self.L[j] for j, _ in self.zterms[i]]
+            acs = [a for _, a in self.zterms[i]]
+            if i > 0:
+                op.launch_adj_stage(Us[i], lam, self.b[i], lts, acs, dt, self.L[i], None, None)
+            else:
+                acc = [None] + [self.L[j] for j in range(1, s)]
+                op.launch_adj_stage(Us[0], lam, self.b[0], lts, acs, dt, None, acc, lam_out)
+        op.counters["jact"] += s
+
+
+def adjoint_engine_for(op, scheme):
+    cache = op.__dict__.setdefault("_adj_engines", {})
+    e = cache.get(scheme)
+    if e is None:
+        e = AdjointEngine(op, scheme)
+        cache[scheme] = e
+    return e
+
+
+def _check_adjoint_flags(op):
+    v = op.flags()
+    if v & _lib.SEM1D_FLAG_STATE_NONFINITE:
+        raise NumericFailure("state contains NaN/Inf")
+    if v & _lib.SEM1D_FLAG_INPUT2_NONFINITE:
+        raise NumericFailure("cotangent contains NaN/Inf")
+
+
+def adjoint_step(op, u_n, lam, t, dt, scheme, out=None):
+    out = op.empty() if out is None else out
+    adjoint_engine_for(op, scheme).step(u_n, lam, dt, out)
+    _check_adjoint_flags(op)
+    return out
+
+
+def sweep(op, cfg, fwd, schedule, lam_terminal, check_every=1):
+    """Backward sweep over a recorded trajectory (adjoint.py:72-158).
+
+    Schedule semantics, CheckpointError conditions and ``last_sweep_stats``
+    follow the reference; states are device tensors, a Store keeps a
+    reference (states are never mutated in place), an Advance re-runs the
+    recorded dts through the same fused stage kernels (bitwise replay).
+    """
+    _require_explicit(cfg)
+    m = fwd.n_steps
+    if schedule.n_steps != m:
+        raise ValidationError(f"schedule covers {schedule.n_steps} steps, trajectory has {m}")
+    lam_t, host = op.field(lam_terminal, "cotangent")
+    lam = lam_t.clone()
+    if m == 0:
+        return lam.cpu().numpy() if host else lam
+    dts = fwd.dts
+    stats = {"newton_iters": 0, "gmres_iters": 0, "recomputed": 0}
+    fwd_engine = engine_for(op, cfg.scheme)
+    adj = adjoint_engine_for(op, cfg.scheme)
+
+    slots, preloaded = {}, True
+    for step, slot in schedule.forward_stores.items():
+        if step in fwd.snapshots:
+            slots[slot] = (step, fwd.snapshots[step])
+        else:
+            preloaded = False
+    if preloaded:
+        actions = schedule.actions[schedule.backward_start:]
+        current = None
+    else:
+        if 0 not in fwd.snapshots:
+            raise CheckpointError("trajectory does not retain the initial state")
+        slots = {}
+        actions = schedule.actions
+        current = (0, fwd.snapshots[0])
+
+    succ = (m, fwd.u_final)
+    next_adj = m - 1
+    spare = op.empty()
+    since_check = 0
+    op.flags()
+    for act in actions:
+        if isinstance(act, Restore):
+            if act.slot not in slots or slots[act.slot][0] != act.step:
+                raise CheckpointError(f"restore of step {act.step}: slot not populated")
+            current = slots[act.slot]
+        elif isinstance(act, Store):
+            if current is None or current[0] != act.step:
+                raise CheckpointError(f"store at step {act.step}: state not in hand")
+            slots[act.slot] = current
+        elif isinstance(act, Advance):
+            if current is None or current[0] != act.start:
+                raise CheckpointError(f"advance from step {act.start}: state not in hand")
+            u = current[1]
+            for n in range(act.start, act.stop):
+                nxt = op.empty()
+                fwd_engine.step(u, dts[n], nxt)
+                u = nxt
+            check_step_flags(op)
+            stats["recomputed"] += act.stop - act.start
+            current = (act.stop, u)
+        elif isinstance(act, AdjointStep):
+            n = act.step
+            if n != next_adj:
+                raise CheckpointError(f"adjoint step {n} out of order")
+            if current is None or current[0] != n:
+                raise CheckpointError(f"adjoint step {n}: forward state missing")
+            if not (succ[0] == n + 1 or n + 1 == m):
+                raise CheckpointError(f"adjoint step {n}: successor state missing")
+            adj.step(current[1], lam, dts[n], spare)
+            lam, spare = spare, lam
+            since_check += 1
+            if since_check >= check_every:
+                _check_adjoint_flags(op)
+                since_check = 0
+            succ = current
+            next_adj -= 1
+        elif isinstance(act, Done):
+            break
+    _check_adjoint_flags(op)
+    if next_adj != -1:
+        raise CheckpointError(f"sweep incomplete: stopped before adjoint step {next_adj}")
+    op.last_sweep_stats = stats
+    return lam.cpu().numpy() if host else lam
+
+
+def gradient(op, cfg, fwd, schedule, u_ref):
+    """terminal_condition + sweep (adjoint.py:161-164)."""
+    j, lam = terminal_condition(op.grid, fwd.u_final, u_ref, op=op)
+    return j, sweep(op, cfg, fwd, schedule, lam)

@@ -1,0 +1,68 @@
+"""The BASELINE.json workloads as builders.
+
+Inputs are seeded numpy PCG64 draws per global node in node order, created on
+the host and shared unchanged by the oracle (tests / bench CPU leg) and the
+device path.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import timeloop
+from .grid import DIRICHLET0, PERIODIC, grid_1d
+from .ops import PdeCoefficients, SemOperator
+from .problems import AssimilationProblem
+
+CFG1 = dict(xa=-1.0, xb=1.0, E=16, N=9, nu=0.01, steps=20, dt=1e-4, seed=1806)
+CFG2 = dict(xa=-1.0, xb=1.0, E=1 << 22, N=7, nu=0.01, seed=2)
+CFG3 = dict(xa=-1.0, xb=1.0, E=1 << 18, N=31, nu=1e-3, seed=3)
+# config 4: dt = 5e-5 is unstable on [-1, 1] (rho(J) = 3.85e6, SURVEY.md finding 4);
+# [0, 20] gives rho = 3.85e4 and an RK4 limit of ~7e-5.
+CFG4 = dict(xa=0.0, xb=20.0, B=4096, E=256, N=15, nu=0.01, steps=1000, dt=5e-5, seed=4)
+
+
+def cfg1_inputs(grid, seed=CFG1["seed"]):
+    """u0 = sin(pi x) + 0.01 N(0,1); target IC = sin(pi x) + 0.5 sin(2 pi x) (BASELINE config 1)."""
+    x = grid.node_coordinates()[0]
+    rng = np.random.default_rng(seed)
+    u0 = grid.mask(np.sin(np.pi * x) + 0.01 * rng.standard_normal(grid.nglobal))
+    obs0 = grid.mask(np.sin(np.pi * x) + 0.5 * np.sin(2.0 * np.pi * x))
+    return u0, obs0
+
+
+def cfg1_problem(bc=PERIODIC, scheme="rk4", checkpoint_slots=None, device=None, target=None):
+    c = CFG1
+    grid = grid_1d(c["xa"], c["xb"], c["E"], c["N"], bc)
+    op = SemOperator(grid, PdeCoefficients(c["nu"]), device=device)
+    ts = timeloop.TsConfig(scheme=scheme, t0=0.0, t_end=c["steps"] * c["dt"], dt=c["dt"])
+    u0, obs0 = cfg1_inputs(grid)
+    if target is None:
+        target = timeloop.integrate(op, obs0, ts, store_steps=None).u_final
+    return AssimilationProblem(name=f"cfg1-{bc}-{scheme}", grid=grid, op=op, ts=ts,
+                               u_target=target, u_guess=u0, checkpoint_slots=checkpoint_slots)
+
+
+def operator_inputs(ndof, seed):
+    """u ~ U(-1,1), v ~ N(0,1), w ~ N(0,1) per node (BASELINE configs 2/3)."""
+    rng = np.random.default_rng(seed)
+    u = rng.uniform(-1.0, 1.0, ndof)
+    v = rng.standard_normal(ndof)
+    w = rng.standard_normal(ndof)
+    return u, v, w
+
+
+def fourier_fields(grid, batch, n_modes, seed):
+    """Per problem: sum_k a_k sin(2 pi k (x - xa) / L), a_k ~ U(-1, 1) (BASELINE configs 4/5)."""
+    ax = grid.axis
+    x = grid.node_coordinates()[0]
+    rng = np.random.default_rng(seed)
+    amps = rng.uniform(-1.0, 1.0, (batch, n_modes))
+    k = np.arange(1, n_modes + 1)
+    phase = 2.0 * np.pi * np.outer(k, (x - ax.xa) / ax.length)   # (modes, ndof)
+    return amps @ np.sin(phase)
+
+
+def cfg_operator(cfg, device=None, batch=1, bc=PERIODIC):
+    grid = grid_1d(cfg["xa"], cfg["xb"], cfg["E"], cfg["N"], bc)
+    return SemOperator(grid, PdeCoefficients(cfg["nu"]), device=device, batch=batch)

@@ -1,0 +1,368 @@
+// sem1d_capi.cu -- the extern "C" boundary (include/sem1d.h): plans, argument
+// validation, dispatch by degree, and the small non-templated kernels
+// (terminal condition, scatter, gather).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "sem1d_launch.cuh"
+
+using namespace sem1d;
+
+namespace sem1d {
+#define SEM_DECL(NN) \
+  extern template cudaError_t launch_apply<NN>(const PlanView&, int, const Args&, cudaStream_t);
+SEM_DECL(1) SEM_DECL(2) SEM_DECL(3) SEM_DECL(4) SEM_DECL(5) SEM_DECL(6) SEM_DECL(7) SEM_DECL(8)
+SEM_DECL(9) SEM_DECL(10) SEM_DECL(11) SEM_DECL(12) SEM_DECL(13) SEM_DECL(14) SEM_DECL(15)
+SEM_DECL(16) SEM_DECL(17) SEM_DECL(18) SEM_DECL(19) SEM_DECL(20) SEM_DECL(21) SEM_DECL(22)
+SEM_DECL(23) SEM_DECL(24) SEM_DECL(25) SEM_DECL(26) SEM_DECL(27) SEM_DECL(28) SEM_DECL(29)
+SEM_DECL(30) SEM_DECL(31) SEM_DECL(32)
+#undef SEM_DECL
+}  // namespace sem1d
+
+struct sem1d_plan {
+  int N;
+  int64_t E, ndof, batch;
+  int periodic;
+  double nu;
+  std::vector<double> packed;  // Consts<N> image
+  std::vector<double> mass, minv;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  return fail(SEM1D_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+PlanView view(const sem1d_plan* p) {
+  PlanView v;
+  v.consts = p->packed.data();
+  v.geo.E = p->E;
+  v.geo.ndof = p->ndof;
+  v.geo.periodic = p->periodic;
+  v.batch = p->batch;
+  return v;
+}
+
+cudaError_t dispatch(const sem1d_plan* p, int kind, const Args& a, cudaStream_t s) {
+  const PlanView v = view(p);
+  switch (p->N) {
+#define SEM_CASE(NN) \
+  case NN: return launch_apply<NN>(v, kind, a, s);
+    SEM_CASE(1) SEM_CASE(2) SEM_CASE(3) SEM_CASE(4) SEM_CASE(5) SEM_CASE(6) SEM_CASE(7)
+    SEM_CASE(8) SEM_CASE(9) SEM_CASE(10) SEM_CASE(11) SEM_CASE(12) SEM_CASE(13) SEM_CASE(14)
+    SEM_CASE(15) SEM_CASE(16) SEM_CASE(17) SEM_CASE(18) SEM_CASE(19) SEM_CASE(20) SEM_CASE(21)
+    SEM_CASE(22) SEM_CASE(23) SEM_CASE(24) SEM_CASE(25) SEM_CASE(26) SEM_CASE(27) SEM_CASE(28)
+    SEM_CASE(29) SEM_CASE(30) SEM_CASE(31) SEM_CASE(32)
+#undef SEM_CASE
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+bool valid_plan(const sem1d_plan* p) { return p != nullptr && p->N >= 1 && p->N <= SEM1D_MAX_DEGREE; }
+
+Args blank_args() {
+  Args a;
+  std::memset(&a, 0, sizeof(a));
+  return a;
+}
+
+int fill_combo(Combo& c, int n, const double* const* ptrs, const double* coef, bool need_coef,
+               const char* what) {
+  if (n < 0 || n > SEM1D_MAX_TERMS) return fail(SEM1D_EINVAL, std::string(what) + ": bad term count");
+  if (n > 0 && ptrs == nullptr) return fail(SEM1D_EINVAL, std::string(what) + ": null term list");
+  if (n > 0 && need_coef && coef == nullptr) return fail(SEM1D_EINVAL, std::string(what) + ": null coefficients");
+  c.n = n;
+  for (int j = 0; j < n; ++j) {
+    c.ptr[j] = ptrs[j];
+    c.coef[j] = need_coef ? coef[j] : 1.0;
+  }
+  return SEM1D_OK;
+}
+
+// ---------------------------------------------------------------- small kernels
+
+struct Pattern {
+  double mass[SEM1D_MAX_DEGREE + 2];
+  int N;
+};
+
+__device__ __forceinline__ double pat_at(const Pattern& P, int64_t g, const Geo& G) {
+  if (!G.periodic) {
+    if (g == 0) return P.mass[P.N];
+    if (g == G.E * P.N) return P.mass[P.N + 1];
+  }
+  return P.mass[g % P.N];
+}
+
+constexpr int RED_TPB = 256;
+constexpr int RED_ITEMS = 16;
+
+__device__ double block_sum_fixed(double v, double* sh) {
+  // fixed-shape tree: deterministic for a given blockDim
+  sh[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = RED_TPB / 2; s > 0; s >>= 1) {
+    if ((int)threadIdx.x < s) sh[threadIdx.x] = sh[threadIdx.x] + sh[threadIdx.x + s];
+    __syncthreads();
+  }
+  return sh[0];
+}
+
+// d = uN - ud; md = M d; lam = mask(2 md); partial sums of d*md   (adjoint.py:39-47)
+__global__ void __launch_bounds__(RED_TPB)
+    terminal_kernel(const Pattern P, const Geo G, const double* __restrict__ uN,
+                    const double* __restrict__ ud, double* __restrict__ lam,
+                    double* __restrict__ work, int nblk) {
+  __shared__ double sh[RED_TPB];
+  const int64_t bofs = (int64_t)blockIdx.y * G.ndof;
+  const int64_t start = (int64_t)blockIdx.x * RED_TPB * RED_ITEMS;
+  double acc = 0.0;
+  for (int it = 0; it < RED_ITEMS; ++it) {
+    const int64_t g = start + (int64_t)it * RED_TPB + threadIdx.x;
+    if (g < G.ndof) {
+      const double d = __dsub_rn(uN[bofs + g], ud[bofs + g]);
+      const double md = __dmul_rn(pat_at(P, g, G), d);
+      double l = __dmul_rn(2.0, md);
+      if (!G.periodic && (g == 0 || g == G.E * P.N)) l = __dmul_rn(l, 0.0);
+      lam[bofs + g] = l;
+      acc = __dadd_rn(acc, __dmul_rn(d, md));
+    }
+  }
+  const double s = block_sum_fixed(acc, sh);
+  if (threadIdx.x == 0) work[(int64_t)blockIdx.y * nblk + blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(RED_TPB)
+    terminal_finish(const double* __restrict__ work, int nblk, double* __restrict__ J_out) {
+  __shared__ double sh[RED_TPB];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < nblk; i += RED_TPB) acc = __dadd_rn(acc, work[(int64_t)blockIdx.x * nblk + i]);
+  const double s = block_sum_fixed(acc, sh);
+  if (threadIdx.x == 0) J_out[blockIdx.x] = s;
+}
+
+// local[b, e, i] = u[b, (e*N + i) mod ndof]                      (grid.py:165-169)
+__global__ void scatter_kernel(const Geo G, int N, const double* __restrict__ u,
+                               double* __restrict__ local) {
+  const int n = N + 1;
+  const int64_t total = G.E * n;
+  const int64_t bofs_u = (int64_t)blockIdx.y * G.ndof, bofs_l = (int64_t)blockIdx.y * total;
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = k / n;
+    const int i = (int)(k - e * n);
+    int64_t g = e * N + i;
+    if (g >= G.ndof) g -= G.ndof;
+    local[bofs_l + k] = u[bofs_u + g];
+  }
+}
+
+// out[g] = (0 + first contribution) + second contribution         (grid.py:157-161)
+__global__ void gather_kernel(const Geo G, int N, const double* __restrict__ local,
+                              double* __restrict__ out) {
+  const int n = N + 1;
+  const int64_t bofs_o = (int64_t)blockIdx.y * G.ndof, bofs_l = (int64_t)blockIdx.y * G.E * n;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < G.ndof;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = g / N;
+    const int i = (int)(g - e * N);
+    double v;
+    if (i != 0) {
+      v = __dadd_rn(0.0, local[bofs_l + e * n + i]);
+    } else if (G.periodic) {
+      // bincount visits table positions in ravel order
+      const int64_t eprev = (e == 0) ? G.E - 1 : e - 1;
+      const double a = local[bofs_l + e * n];
+      const double b = local[bofs_l + eprev * n + N];
+      v = (e == 0) ? __dadd_rn(__dadd_rn(0.0, a), b) : __dadd_rn(__dadd_rn(0.0, b), a);
+    } else {
+      if (e == 0) {
+        v = __dadd_rn(0.0, local[bofs_l]);
+      } else if (e == G.E) {
+        v = __dadd_rn(0.0, local[bofs_l + (e - 1) * n + N]);
+      } else {
+        v = __dadd_rn(__dadd_rn(0.0, local[bofs_l + (e - 1) * n + N]), local[bofs_l + e * n]);
+      }
+    }
+    out[bofs_o + g] = v;
+  }
+}
+
+unsigned grid_for(int64_t work, int tpb) {
+  int64_t b = (work + tpb - 1) / tpb;
+  if (b > 148 * 32) b = 148 * 32;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sem1d_version(void) { return 1; }
+const char* sem1d_last_error(void) { return g_err.c_str(); }
+int sem1d_max_degree(void) { return SEM1D_MAX_DEGREE; }
+
+int sem1d_plan_create(int64_t n_elements, int degree, int periodic, double nu, const double* K,
+                      const double* Dw, const double* mass_pattern, const double* minv_pattern,
+                      int64_t batch, sem1d_plan** out) {
+  if (out == nullptr) return fail(SEM1D_EINVAL, "plan_create: null output");
+  *out = nullptr;
+  if (degree < 1 || degree > SEM1D_MAX_DEGREE)
+    return fail(SEM1D_EINVAL, "plan_create: degree must be in [1, " +
+                                  std::to_string(SEM1D_MAX_DEGREE) + "]");
+  if (n_elements < 1) return fail(SEM1D_EINVAL, "plan_create: need at least one element");
+  if (periodic && n_elements * degree < 2)
+    return fail(SEM1D_EINVAL, "plan_create: periodic axis needs E*N >= 2");
+  if (batch < 1 || batch > 65535) return fail(SEM1D_EINVAL, "plan_create: batch must be in [1, 65535]");
+  if (!K || !Dw || !mass_pattern || !minv_pattern) return fail(SEM1D_EINVAL, "plan_create: null constant");
+  if (!std::isfinite(nu) || nu < 0.0) return fail(SEM1D_EINVAL, "plan_create: viscosity must be >= 0");
+  const int n = degree + 1;
+  const int64_t nb = (n_elements + 127) / 128;
+  if (nb > 2147483647LL) return fail(SEM1D_EINVAL, "plan_create: too many elements");
+  sem1d_plan* p = new (std::nothrow) sem1d_plan();
+  if (!p) return fail(SEM1D_EINVAL, "plan_create: out of host memory");
+  p->N = degree;
+  p->E = n_elements;
+  p->periodic = periodic ? 1 : 0;
+  p->ndof = n_elements * degree + (periodic ? 0 : 1);
+  p->batch = batch;
+  p->nu = nu;
+  p->mass.assign(mass_pattern, mass_pattern + degree + 2);
+  p->minv.assign(minv_pattern, minv_pattern + degree + 2);
+  // Consts<N> image: K[n*n], Dw[n*n], minv[N+2], mass[N+2], nu
+  p->packed.reserve(2 * n * n + 2 * (degree + 2) + 1);
+  p->packed.insert(p->packed.end(), K, K + n * n);
+  p->packed.insert(p->packed.end(), Dw, Dw + n * n);
+  p->packed.insert(p->packed.end(), minv_pattern, minv_pattern + degree + 2);
+  p->packed.insert(p->packed.end(), mass_pattern, mass_pattern + degree + 2);
+  p->packed.push_back(nu);
+  *out = p;
+  return SEM1D_OK;
+}
+
+int sem1d_plan_destroy(sem1d_plan* plan) {
+  delete plan;
+  return SEM1D_OK;
+}
+
+int64_t sem1d_plan_ndof(const sem1d_plan* plan) { return plan ? plan->ndof : -1; }
+
+static int run_apply(const sem1d_plan* p, int kind, const Args& a, void* stream, const char* name) {
+  cudaError_t e = dispatch(p, kind, a, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, name);
+  return SEM1D_OK;
+}
+
+int sem1d_rhs(const sem1d_plan* plan, const double* u, double* f, int* flag, void* stream) {
+  if (!valid_plan(plan) || !u || !f || !flag) return fail(SEM1D_EINVAL, "sem1d_rhs: bad argument");
+  Args a = blank_args();
+  a.u = u; a.out = f; a.flag = flag;
+  return run_apply(plan, 0, a, stream, "sem1d_rhs");
+}
+
+int sem1d_jac(const sem1d_plan* plan, const double* u, const double* v, double* out, int* flag,
+              void* stream) {
+  if (!valid_plan(plan) || !u || !v || !out || !flag) return fail(SEM1D_EINVAL, "sem1d_jac: bad argument");
+  Args a = blank_args();
+  a.u = u; a.w = v; a.out = out; a.flag = flag;
+  return run_apply(plan, 1, a, stream, "sem1d_jac");
+}
+
+int sem1d_jact(const sem1d_plan* plan, const double* u, const double* z, double* out, int* flag,
+               void* stream) {
+  if (!valid_plan(plan) || !u || !z || !out || !flag) return fail(SEM1D_EINVAL, "sem1d_jact: bad argument");
+  Args a = blank_args();
+  a.u = u; a.w = z; a.out = out; a.flag = flag;
+  return run_apply(plan, 2, a, stream, "sem1d_jact");
+}
+
+int sem1d_rk_stage(const sem1d_plan* plan, const double* U_in, double* k_out, const double* base,
+                   int nterms, const double* const* terms, const double* coef, double dt, double* Y,
+                   int check_step, int* flag, void* stream) {
+  if (!valid_plan(plan) || !U_in || !base || !Y || !flag || nterms < 1)
+    return fail(SEM1D_EINVAL, "sem1d_rk_stage: bad argument");
+  Args a = blank_args();
+  a.u = U_in; a.out = k_out; a.flag = flag; a.base = base; a.dt = dt; a.Y = Y;
+  a.check = check_step ? 1 : 0;
+  int rc = fill_combo(a.epi, nterms, terms, coef, true, "sem1d_rk_stage");
+  if (rc) return rc;
+  return run_apply(plan, 3, a, stream, "sem1d_rk_stage");
+}
+
+int sem1d_adj_stage(const sem1d_plan* plan, const double* U, const double* lam, double b, int nl,
+                    const double* const* l_terms, const double* acoef, double dt, double* l_out,
+                    int nacc, const double* const* acc_terms, double* lam_out, int* flag,
+                    void* stream) {
+  if (!valid_plan(plan) || !U || !lam || !flag) return fail(SEM1D_EINVAL, "sem1d_adj_stage: bad argument");
+  Args a = blank_args();
+  a.u = U; a.w = lam; a.b = b; a.out = l_out; a.flag = flag; a.base = lam; a.dt = dt; a.Y = lam_out;
+  int rc = fill_combo(a.zin, nl, l_terms, acoef, true, "sem1d_adj_stage(z)");
+  if (rc) return rc;
+  if (lam_out) {
+    rc = fill_combo(a.epi, nacc, acc_terms, nullptr, false, "sem1d_adj_stage(acc)");
+    if (rc) return rc;
+  }
+  return run_apply(plan, 4, a, stream, "sem1d_adj_stage");
+}
+
+int64_t sem1d_terminal_work_size(const sem1d_plan* plan) {
+  if (!valid_plan(plan)) return -1;
+  const int64_t per = RED_TPB * RED_ITEMS;
+  return plan->batch * ((plan->ndof + per - 1) / per);
+}
+
+int sem1d_terminal(const sem1d_plan* plan, const double* uN, const double* ud, double* lam,
+                   double* J_out, double* work, void* stream) {
+  if (!valid_plan(plan) || !uN || !ud || !lam || !J_out || !work)
+    return fail(SEM1D_EINVAL, "sem1d_terminal: bad argument");
+  Pattern P;
+  std::memset(&P, 0, sizeof(P));
+  P.N = plan->N;
+  for (int i = 0; i < plan->N + 2; ++i) P.mass[i] = plan->mass[i];
+  const Geo G = view(plan).geo;
+  const int64_t per = RED_TPB * RED_ITEMS;
+  const int nblk = (int)((plan->ndof + per - 1) / per);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  terminal_kernel<<<dim3(nblk, (unsigned)plan->batch), RED_TPB, 0, s>>>(P, G, uN, ud, lam, work, nblk);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "sem1d_terminal");
+  terminal_finish<<<(unsigned)plan->batch, RED_TPB, 0, s>>>(work, nblk, J_out);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(e, "sem1d_terminal(finish)");
+  return SEM1D_OK;
+}
+
+int sem1d_scatter(const sem1d_plan* plan, const double* u, double* local, void* stream) {
+  if (!valid_plan(plan) || !u || !local) return fail(SEM1D_EINVAL, "sem1d_scatter: bad argument");
+  const Geo G = view(plan).geo;
+  scatter_kernel<<<dim3(grid_for(plan->E * (plan->N + 1), 256), (unsigned)plan->batch), 256, 0,
+                   static_cast<cudaStream_t>(stream)>>>(G, plan->N, u, local);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SEM1D_OK : cuda_fail(e, "sem1d_scatter");
+}
+
+int sem1d_gather(const sem1d_plan* plan, const double* local, double* out, void* stream) {
+  if (!valid_plan(plan) || !local || !out) return fail(SEM1D_EINVAL, "sem1d_gather: bad argument");
+  const Geo G = view(plan).geo;
+  gather_kernel<<<dim3(grid_for(plan->ndof, 256), (unsigned)plan->batch), 256, 0,
+                  static_cast<cudaStream_t>(stream)>>>(G, plan->N, local, out);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SEM1D_OK : cuda_fail(e, "sem1d_gather");
+}
+
+}  // extern "C"

@@ -1,0 +1,232 @@
+"""1D uniform GLL mesh metadata and assembly maps (reference ``semopt/grid.py``).
+
+Design for the B200 path: the reference materialises an (E, N+1) int64
+local->global table and (ndof,) multiplicity / mass / mask arrays
+(``grid.py:65-72,112-146``) -- 2.15 GB of table alone at E = 2^25.  A uniform
+1D mesh needs none of them: element e owns the contiguous node range
+[e*N, e*N+N] (mod ndof when periodic), the mass diagonal is a per-local-index
+pattern, and the Dirichlet mask touches two nodes.  The kernels use the
+closed forms; the full arrays exist here only as lazily built host
+properties so the reference's attribute surface (and the bit-exact tests
+against it) keep working.
+
+3D grids (``grid.py:113-122,239-244``) are outside the B200 hot path
+ and are rejected with ValidationError.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from functools import cached_property
+
+import numpy as np
+
+from .basis import gll_rule
+from .errors import ValidationError
+
+PERIODIC = "periodic"
+DIRICHLET0 = "dirichlet0"
+
+
+@dataclass(frozen=True)
+class Axis:
+    """Extent, element count, degree and boundary kind of the single axis."""
+
+    xa: float
+    xb: float
+    elements: int
+    degree: int
+    bc: str = PERIODIC
+
+    def __post_init__(self):
+        # same admissibility rules as grid.py:40-50
+        if self.xb <= self.xa:
+            raise ValidationError(f"axis extent is empty: [{self.xa}, {self.xb}]")
+        if self.elements < 1:
+            raise ValidationError("need at least one element per axis")
+        if self.degree < 1:
+            raise ValidationError("polynomial degree must be >= 1")
+        if self.bc not in (PERIODIC, DIRICHLET0):
+            raise ValidationError(f"unknown boundary kind {self.bc!r}")
+        if self.bc == PERIODIC and self.elements * self.degree < 2:
+            raise ValidationError("periodic axis needs E*N >= 2 (degenerate wrap)")
+
+    @property
+    def length(self):
+        return self.xb - self.xa
+
+    @property
+    def element_length(self):
+        return (self.xb - self.xa) / self.elements
+
+    @property
+    def npts(self):
+        return self.elements * self.degree + (0 if self.bc == PERIODIC else 1)
+
+    def local_to_global(self):
+        """(E, N+1) table e*N + i (mod npts if periodic) -- test/inspection only."""
+        tab = (np.arange(self.elements)[:, None] * self.degree
+               + np.arange(self.degree + 1)[None, :])
+        return tab % self.npts if self.bc == PERIODIC else tab
+
+    def coordinates(self):
+        """Node coordinates, vectorised closed form of grid.py:74-84: each node takes
+        the value written last by the reference loop (the right element at interfaces)."""
+        xi = gll_rule(self.degree).nodes
+        h, E, N = self.element_length, self.elements, self.degree
+        left = self.xa + np.arange(E) * h
+        loc = left[:, None] + h * (xi + 1.0) / 2.0
+        out = np.empty(self.npts)
+        out[:E * N] = loc[:, :N].ravel()
+        if self.bc == PERIODIC:
+            out[0] = self.xa
+        else:
+            out[E * N] = loc[E - 1, N]
+        return out
+
+
+class Grid:
+    """1D mesh + assembly metadata.  Build through :func:`grid_1d`/:func:`build_grid`."""
+
+    def __init__(self, axes):
+        axes = tuple(axes)
+        if len(axes) != 1:
+            raise ValidationError(
+                "only 1D grids are on the B200 hot path (3D sum-factorised grids are out of scope)")
+        ax = axes[0]
+        self.axes = axes
+        self.axis = ax
+        self.dim = 1
+        self.ncomp = 1
+        self.bases = (gll_rule(ax.degree),)
+        self.shape = (ax.npts,)
+        self.nscalar = ax.npts
+        self.nglobal = ax.npts
+        self.nelem = ax.elements
+        self.local_shape = (ax.degree + 1,)
+        self.periodic = ax.bc == PERIODIC
+        self.has_mask = not self.periodic
+        self.h = ax.element_length
+        # per-position mass pattern (see include/sem1d.h): [0] interface,
+        # [1..N-1] interior, [N] first / [N+1] last node of a Dirichlet grid.
+        # bincount sums (0 + a) + b at an interface (grid.py:157-161); a + b is
+        # commutative, so every position is reproduced bit for bit.
+        rho = self.bases[0].weights
+        m_loc = (self.h / 2.0) * rho
+        N = ax.degree
+        pat = np.empty(N + 2)
+        pat[1:N] = m_loc[1:N]
+        if self.periodic or ax.elements > 1:
+            pat[0] = m_loc[N] + m_loc[0]
+        else:
+            pat[0] = m_loc[0]
+        pat[N] = m_loc[0]
+        pat[N + 1] = m_loc[N]
+        if N == 1 and self.periodic and ax.elements == 1:  # excluded by Axis, kept explicit
+            raise ValidationError("degenerate periodic grid")
+        self.mass_pattern = pat
+        self.minv_pattern = 1.0 / pat   # ops.py:116 (1.0 / mass)
+        if np.any(pat <= 0.0):
+            raise ValidationError("assembled mass diagonal is not positive")
+
+    # -- lazily materialised reference attributes (test / inspection only) --------
+
+    @cached_property
+    def table(self):
+        t = np.ascontiguousarray(self.axis.local_to_global())
+        t.setflags(write=False)
+        return t
+
+    def _expand(self, pat):
+        E, N = self.axis.elements, self.axis.degree
+        out = np.empty(self.nglobal)
+        out[:E * N] = np.tile(pat[:N], E)
+        if not self.periodic:
+            out[0] = pat[N]
+            out[E * N] = pat[N + 1]
+        out.setflags(write=False)
+        return out
+
+    @cached_property
+    def mass_scalar(self):
+        return self._expand(self.mass_pattern)
+
+    @cached_property
+    def multiplicity(self):
+        E, N = self.axis.elements, self.axis.degree
+        pat = np.ones(N + 2)
+        pat[0] = 2.0 if (self.periodic or E > 1) else 1.0
+        return self._expand(pat)
+
+    @cached_property
+    def mask_scalar(self):
+        m = np.ones(self.nglobal)
+        if not self.periodic:
+            m[0] = 0.0
+            m[-1] = 0.0
+        m.setflags(write=False)
+        return m
+
+    # -- maps on device fields (C ABI) ------------------------------------------
+
+    def scatter(self, u):
+        """Global -> (1, E, N+1) element copies (grid.py:165-169), on the device."""
+        from . import ops
+        return ops._grid_scatter(self, u)
+
+    def gather(self, local):
+        """Adjoint of scatter (grid.py:171-182), on the device."""
+        from . import ops
+        return ops._grid_gather(self, local)
+
+    def mask(self, u):
+        """Zero the Dirichlet end nodes (grid.py:184-189); works on numpy or torch."""
+        if not self.has_mask:
+            return u
+        if isinstance(u, np.ndarray):
+            self._check_host(u)
+            return u * self.mask_scalar
+        out = u.clone()
+        out[..., 0] = out[..., 0] * 0.0
+        out[..., -1] = out[..., -1] * 0.0
+        return out
+
+    def mass(self):
+        return self.mass_scalar
+
+    def _check_host(self, u):
+        u = np.asarray(u, dtype=float)
+        if u.shape != (self.nglobal,):
+            raise ValidationError(f"field has shape {u.shape}, expected ({self.nglobal},)")
+        return u
+
+    # -- geometry -------------------------------------------------------------
+
+    def node_coordinates(self):
+        return (self.axis.coordinates(),)
+
+    def evaluate(self, fn):
+        """Sample x -> fn(x) at the nodes, masked (grid.py:209-222)."""
+        vals = np.asarray(fn(self.node_coordinates()[0]), dtype=float).ravel()
+        return self.mask(vals)
+
+    def l2_norm(self, u):
+        """sqrt(u^T M u) (grid.py:224-227)."""
+        if isinstance(u, np.ndarray):
+            u = self._check_host(u)
+            return float(np.sqrt(np.dot(u, self.mass_scalar * u)))
+        import torch
+        m = torch.as_tensor(self.mass_scalar, device=u.device)
+        return float(torch.sqrt(torch.dot(u, m * u)))
+
+
+def build_grid(axes):
+    return Grid(axes)
+
+
+def grid_1d(xa, xb, elements, degree, bc=PERIODIC):
+    return Grid([Axis(xa, xb, elements, degree, bc)])
+
+
+def grid_3d(*args, **kwargs):
+    raise ValidationError("3D grids are outside the B200 hot path (SURVEY.md section 8(f), 'next')")

@@ -1,0 +1,318 @@
+"""Matrix-free Burgers operator on the B200 (reference ``semopt/ops.py``).
+
+``SemOperator`` keeps the reference's duck-typed plugin surface
+(``apply_rhs``, ``apply_jacobian``, ``apply_jacobian_transpose``, ``densify``,
+``counters``, ``grid``, ``coef``, ``max_matrix_dim``; ops.py:84-273) but every
+apply is ONE fused sm_100a kernel launched through the C ABI
+(``include/sem1d.h``): scatter, the element contractions, the nonlinear and
+viscous terms, the gather, M^-1 and the Dirichlet mask never leave the SM.
+
+Fields are fp64 torch tensors on the operator's CUDA device.  numpy inputs
+are accepted for drop-in use: they are copied to the device and the result is
+copied back (that host round trip is what ``bench.py`` reports as ``e2e``).
+There is no CPU fallback: without the library or a GPU the constructor raises.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .errors import NumericFailure, ValidationError
+
+BURGERS = "burgers"
+LINEAR = "linear"
+NONE = "none"
+
+_DENSIFY_LIMIT = 5000
+
+
+class PdeCoefficients:
+    """Viscosity and advection kind (ops.py:42-60).  Only Burgers advection is on
+    the B200 hot path; 'linear' / 'none' are SURVEY 8(f) "next" items."""
+
+    def __init__(self, nu, advection=BURGERS, speed=None):
+        if not np.isfinite(nu) or nu < 0.0:
+            raise ValidationError(f"viscosity must be >= 0, got {nu!r}")
+        if advection not in (BURGERS, LINEAR, NONE):
+            raise ValidationError(f"unknown advection kind {advection!r}")
+        if advection != BURGERS:
+            raise ValidationError(
+                f"advection {advection!r} is not on the B200 hot path (only 'burgers')")
+        self.nu = float(nu)
+        self.advection = advection
+        self.speed = None
+
+    def __repr__(self):
+        return f"PdeCoefficients(nu={self.nu}, advection={self.advection!r})"
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_handle(device):
+    torch = _torch()
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class _Plan:
+    """Owns one sem1d_plan* (C ABI)."""
+
+    def __init__(self, grid, nu, K, Dw, batch):
+        lib = _lib.load()
+        ax = grid.axis
+        K = np.ascontiguousarray(K, dtype=np.float64)
+        Dw = np.ascontiguousarray(Dw, dtype=np.float64)
+        mp = np.ascontiguousarray(grid.mass_pattern, dtype=np.float64)
+        mi = np.ascontiguousarray(grid.minv_pattern, dtype=np.float64)
+        handle = _lib.c_void_p()
+        rc = lib.sem1d_plan_create(ax.elements, ax.degree, 1 if grid.periodic else 0, float(nu),
+                                   K.ctypes.data, Dw.ctypes.data, mp.ctypes.data, mi.ctypes.data,
+                                   int(batch), _lib.ctypes.byref(handle))
+        if rc != 0:
+            msg = _lib.last_error()
+            raise ValidationError(msg)
+        self.handle = handle
+        self._lib = lib
+        self.ndof = lib.sem1d_plan_ndof(handle)
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                self._lib.sem1d_plan_destroy(h)
+            except Exception:  # pragma: no cover - interpreter teardown
+                pass
+            self.handle = None
+
+
+class SemOperator:
+    """Matrix-free SEM operator bundle for one (grid, coefficients) pair.
+
+    ``batch`` > 1 makes every field a (batch, ndof) stack of independent
+    problems sharing grid and viscosity (BASELINE config 4).
+    """
+
+    def __init__(self, grid, coef, device=None, batch=1, sync_checks=True):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise RuntimeError("SemOperator needs a CUDA device (the B200 path has no CPU fallback)")
+        if grid.dim != 1:
+            raise ValidationError("only 1D grids are supported on the B200 path")
+        self.grid = grid
+        self.coef = coef
+        self.batch = int(batch)
+        self.device = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        ax, b = grid.axis, grid.bases[0]
+        w = b.weights
+        # constants exactly as ops.py:103-107
+        self._dw = b.diff * w[:, None]
+        k = (2.0 / ax.element_length) * (b.diff.T * w) @ b.diff
+        self._kmat = 0.5 * (k + k.T)
+        self._minv = grid.minv_pattern
+        self.max_matrix_dim = ax.degree + 1
+        if ax.degree > _lib.load().sem1d_max_degree():
+            raise ValidationError(f"degree {ax.degree} exceeds the kernel limit")
+        self._plan = _Plan(grid, coef.nu, self._kmat, self._dw, self.batch)
+        self.ndof = grid.nglobal
+        self.shape = (self.ndof,) if self.batch == 1 else (self.batch, self.ndof)
+        self._flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._work = torch.empty(max(1, _lib.load().sem1d_terminal_work_size(self._plan.handle)),
+                                 dtype=torch.float64, device=self.device)
+        self.counters = {"rhs": 0, "jac": 0, "jact": 0}
+        self.sync_checks = sync_checks
+        self.last_sweep_stats = {}
+
+    # -- field plumbing -------------------------------------------------------
+
+    def field(self, x, name="field"):
+        """Validate and place an input; returns (tensor on device, came_from_host)."""
+        torch = _torch()
+        host = not isinstance(x, torch.Tensor)
+        t = torch.as_tensor(np.asarray(x, dtype=np.float64) if host else x)
+        if tuple(t.shape) != self.shape:
+            raise ValidationError(f"{name} has shape {tuple(t.shape)}, expected {self.shape}")
+        if t.dtype != torch.float64:
+            raise ValidationError(f"{name} must be float64, got {t.dtype}")
+        if t.device != self.device:
+            t = t.to(self.device, non_blocking=False)
+        return t.contiguous(), host
+
+    def empty(self):
+        torch = _torch()
+        return torch.empty(self.shape, dtype=torch.float64, device=self.device)
+
+    def _stream(self):
+        return _stream_handle(self.device)
+
+    def flags(self, reset=True):
+        """Read (and clear) the device non-finite flags -- one host sync."""
+        v = int(self._flag.item())
+        if v and reset:
+            self._flag.zero_()
+        return v
+
+    def raise_for_flags(self, names=("state", "tangent")):
+        v = self.flags()
+        if v & _lib.SEM1D_FLAG_STATE_NONFINITE:
+            raise NumericFailure(f"{names[0]} contains NaN/Inf")
+        if v & _lib.SEM1D_FLAG_INPUT2_NONFINITE:
+            raise NumericFailure(f"{names[1]} contains NaN/Inf")
+        return v
+
+    @staticmethod
+    def _isfinite_all(t):
+        torch = _torch()
+        return bool(torch.isfinite(t).all().item())
+
+    @staticmethod
+    def _out(t, host):
+        return t.cpu().numpy() if host else t
+
+    # -- raw launches (no validation, no sync): used by the engines -------------
+
+    def launch_rhs(self, u, out):
+        _lib.check(_lib.load().sem1d_rhs(self._plan.handle, u.data_ptr(), out.data_ptr(),
+                                         self._flag.data_ptr(), self._stream()), "sem1d_rhs")
+
+    def launch_jac(self, u, v, out):
+        _lib.check(_lib.load().sem1d_jac(self._plan.handle, u.data_ptr(), v.data_ptr(),
+                                         out.data_ptr(), self._flag.data_ptr(), self._stream()),
+                   "sem1d_jac")
+
+    def launch_jact(self, u, z, out):
+        _lib.check(_lib.load().sem1d_jact(self._plan.handle, u.data_ptr(), z.data_ptr(),
+                                          out.data_ptr(), self._flag.data_ptr(), self._stream()),
+                   "sem1d_jact")
+
+    def launch_rk_stage(self, U_in, k_out, base, terms, coefs, dt, Y, check):
+        ptrs = _lib.ptr_array([None if t is None else t.data_ptr() for t in terms])
+        cf = _lib.dbl_array(coefs)
+        _lib.check(_lib.load().sem1d_rk_stage(
+            self._plan.handle, U_in.data_ptr(), None if k_out is None else k_out.data_ptr(),
+            base.data_ptr(), len(terms), ptrs, cf, float(dt), Y.data_ptr(), 1 if check else 0,
+            self._flag.data_ptr(), self._stream()), "sem1d_rk_stage")
+
+    def launch_adj_stage(self, U, lam, b, l_terms, a_coefs, dt, l_out, acc_terms, lam_out):
+        lp = _lib.ptr_array([t.data_ptr() for t in l_terms])
+        ac = _lib.dbl_array(a_coefs)
+        accp = _lib.ptr_array([None if t is None else t.data_ptr() for t in (acc_terms or [])])
+        _lib.check(_lib.load().sem1d_adj_stage(
+            self._plan.handle, U.data_ptr(), lam.data_ptr(), float(b), len(l_terms), lp, ac,
+            float(dt), None if l_out is None else l_out.data_ptr(),
+            len(acc_terms or []), accp, None if lam_out is None else lam_out.data_ptr(),
+            self._flag.data_ptr(), self._stream()), "sem1d_adj_stage")
+
+    def launch_terminal(self, uN, ud, lam, J_out):
+        _lib.check(_lib.load().sem1d_terminal(self._plan.handle, uN.data_ptr(), ud.data_ptr(),
+                                              lam.data_ptr(), J_out.data_ptr(),
+                                              self._work.data_ptr(), self._stream()),
+                   "sem1d_terminal")
+
+    # -- reference surface ------------------------------------------------------
+
+    def apply_rhs(self, u):
+        """f(u) = M^-1 gather(F_e(scatter(u))) (ops.py:232-236)."""
+        ut, host = self.field(u, "state")
+        self.counters["rhs"] += 1
+        out = self.empty()
+        self.launch_rhs(ut, out)
+        if self.sync_checks:
+            self.raise_for_flags(("state", "state"))
+        return self._out(out, host)
+
+    def apply_jacobian(self, u, w):
+        """J(u) w (ops.py:238-244)."""
+        ut, host = self.field(u, "state")
+        wt, _ = self.field(w, "tangent")
+        self.counters["jac"] += 1
+        out = self.empty()
+        self.launch_jac(ut, wt, out)
+        if self.sync_checks:
+            self.raise_for_flags(("state", "tangent"))
+        return self._out(out, host)
+
+    def apply_jacobian_transpose(self, u, z):
+        """(M^-1 J)^T z = gather(J_e^T scatter(M^-1 z)) (ops.py:246-257)."""
+        ut, host = self.field(u, "state")
+        zt, _ = self.field(z, "cotangent")
+        self.counters["jact"] += 1
+        out = self.empty()
+        self.launch_jact(ut, zt, out)
+        if self.sync_checks:
+            self.raise_for_flags(("state", "cotangent"))
+        return self._out(out, host)
+
+    def densify(self, u):
+        """Dense J by columns (ops.py:259-273); verification only, n <= 5000."""
+        torch = _torch()
+        n = self.grid.nglobal
+        if n > _DENSIFY_LIMIT:
+            raise ValidationError(f"densify refused: {n} unknowns exceeds limit {_DENSIFY_LIMIT}")
+        if self.batch != 1:
+            raise ValidationError("densify needs batch == 1")
+        ut, host = self.field(u, "state")
+        cols = torch.empty((n, n), dtype=torch.float64, device=self.device)
+        e = torch.zeros(n, dtype=torch.float64, device=self.device)
+        col = self.empty()
+        for k in range(n):
+            e[k] = 1.0
+            self.launch_jac(ut, e, col)
+            cols[:, k] = col
+            e[k] = 0.0
+        self.counters["jac"] += n
+        self.raise_for_flags(("state", "tangent"))
+        return self._out(cols, host)
+
+
+# -- grid maps on the device (used by Grid.scatter / Grid.gather) ----------------
+
+_GEOM_PLANS = {}
+
+
+def _geom_plan(grid, batch):
+    key = (id(grid), batch)
+    p = _GEOM_PLANS.get(key)
+    if p is None:
+        n = grid.axis.degree + 1
+        z = np.zeros((n, n))
+        p = _Plan(grid, 0.0, z, z, batch)
+        _GEOM_PLANS[key] = (grid, p)   # keep grid alive while its plan is cached
+        return p
+    return p[1]
+
+
+def _grid_scatter(grid, u):
+    torch = _torch()
+    host = not isinstance(u, torch.Tensor)
+    t = torch.as_tensor(np.asarray(u, dtype=np.float64)) if host else u
+    if tuple(t.shape) != (grid.nglobal,):
+        raise ValidationError(f"field has shape {tuple(t.shape)}, expected ({grid.nglobal},)")
+    if not t.is_cuda:
+        t = t.cuda()
+    t = t.contiguous().to(torch.float64)
+    out = torch.empty((1, grid.nelem, grid.axis.degree + 1), dtype=torch.float64, device=t.device)
+    p = _geom_plan(grid, 1)
+    _lib.check(_lib.load().sem1d_scatter(p.handle, t.data_ptr(), out.data_ptr(),
+                                         _stream_handle(t.device)), "sem1d_scatter")
+    return out.cpu().numpy() if host else out
+
+
+def _grid_gather(grid, local):
+    torch = _torch()
+    host = not isinstance(local, torch.Tensor)
+    t = torch.as_tensor(np.asarray(local, dtype=np.float64)) if host else local
+    want = (1, grid.nelem, grid.axis.degree + 1)
+    if tuple(t.shape) != want:
+        raise ValidationError(f"local block shape {tuple(t.shape)} does not match grid {want}")
+    if not t.is_cuda:
+        t = t.cuda()
+    t = t.contiguous().to(torch.float64)
+    out = torch.empty(grid.nglobal, dtype=torch.float64, device=t.device)
+    p = _geom_plan(grid, 1)
+    _lib.check(_lib.load().sem1d_gather(p.handle, t.data_ptr(), out.data_ptr(),
+                                        _stream_handle(t.device)), "sem1d_gather")
+    return out.cpu().numpy() if host else out

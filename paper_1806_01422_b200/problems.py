@@ -1,0 +1,127 @@
+"""Assimilation problems: objective + gradient on the B200 (reference ``semopt/problems.py``).
+
+``AssimilationProblem.evaluate(u0) -> (J, dJ/du0)`` keeps the reference
+contract (problems.py:161-205): one forward integration storing exactly the
+schedule's checkpoints, the terminal seed, one backward sweep.  J follows the
+reference convention J = d^T M d (adjoint.py:33-47); BASELINE.json quotes
+0.5 ||d||_M^2, which is ``0.5 * J`` with gradient ``0.5 * g``.
+
+Builders for the BASELINE configurations live in ``configs.py``; the
+reference's ``burgers1d`` problem (Dirichlet Burgers on [-2, 2], Cole-Hopf
+target) is kept here.  advdiff1d / diffusion1d / burgers3d need operators
+outside the B200 hot path and raise ValidationError.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import adjoint, checkpoint, timeloop
+from .errors import ValidationError
+from .grid import DIRICHLET0, grid_1d
+from .ops import BURGERS, PdeCoefficients, SemOperator
+
+
+def burgers1d_exact(x, t, nu):
+    """Cole-Hopf solution (problems.py:35-39)."""
+    x = np.asarray(x, dtype=float)
+    decay = np.exp(-nu * t * np.pi ** 2)
+    return 2.0 * nu * np.pi * np.sin(np.pi * x) * decay / (2.0 + decay * np.cos(np.pi * x))
+
+
+def burgers1d_guess(x, nu, center=2.0):
+    x = np.asarray(x, dtype=float)
+    return burgers1d_exact(x, 0.0, nu) + np.exp(-4.0 * (x - center) ** 2)
+
+
+@dataclass
+class AssimilationProblem:
+    """Terminal-misfit data assimilation over initial conditions."""
+
+    name: str
+    grid: object
+    op: SemOperator
+    ts: timeloop.TsConfig
+    u_target: object
+    u_guess: object
+    u_exact_ic: object = None
+    exact_solution: object = None
+    checkpoint_slots: int | None = None
+
+    def __post_init__(self):
+        self._target_dev = None
+
+    def schedule_for(self, m):
+        if self.checkpoint_slots is None:
+            return checkpoint.plan_store_all(m)
+        return checkpoint.plan_binomial(m, self.checkpoint_slots)
+
+    def target(self):
+        if self._target_dev is None:
+            self._target_dev, _ = self.op.field(self.u_target, "target")
+        return self._target_dev
+
+    def forward(self, u0, store="all", keep_log=False):
+        return timeloop.integrate(self.op, u0, self.ts, store_steps=store, keep_log=keep_log)
+
+    def evaluate(self, u0):
+        """(J, dJ/du0) = one forward + one adjoint sweep (problems.py:184-199)."""
+        if self.ts.adaptive:
+            raise ValidationError("adaptive stepping is outside the B200 hot path")
+        u0_dev, host = self.op.field(u0, "initial state")
+        m = timeloop.count_steps(self.ts)
+        sched = self.schedule_for(m)
+        fwd = timeloop.integrate(self.op, u0_dev, self.ts, store_steps=sched.forward_stores.keys())
+        if fwd.n_steps != m:  # a StepFailure retry changed the time grid
+            sched = self.schedule_for(fwd.n_steps)
+        j, lam = adjoint.terminal_condition(self.grid, fwd.u_final, self.target(), op=self.op)
+        g = adjoint.sweep(self.op, self.ts, fwd, sched, lam)
+        self.last_forward = fwd
+        if host:
+            g = g.cpu().numpy()
+        return j, g
+
+    def ic_error(self, u0):
+        if self.u_exact_ic is None:
+            raise ValidationError(f"problem {self.name} has no exact initial condition")
+        diff = (u0 - self.u_exact_ic) if isinstance(u0, np.ndarray) else (
+            u0 - self.op.field(self.u_exact_ic)[0])
+        return self.grid.l2_norm(diff)
+
+
+def _ts(scheme, horizon, steps, dt, adaptive, **kw):
+    if dt is None:
+        dt = horizon / steps
+    return timeloop.TsConfig(scheme=scheme, t0=0.0, t_end=horizon, dt=dt, adaptive=adaptive, **kw)
+
+
+def burgers1d_problem(elements=5, degree=8, nu=0.001, horizon=4.0, steps=400, dt=None,
+                      scheme="rk3", adaptive=False, guess_center=2.0, checkpoint_slots=None,
+                      device=None, **ts_kw):
+    """The reference's 1D Burgers case (problems.py:215-232)."""
+    grid = grid_1d(-2.0, 2.0, elements, degree, DIRICHLET0)
+    op = SemOperator(grid, PdeCoefficients(nu, BURGERS), device=device)
+    x = grid.node_coordinates()[0]
+    return AssimilationProblem(
+        name="burgers1d", grid=grid, op=op,
+        ts=_ts(scheme, horizon, steps, dt, adaptive, **ts_kw),
+        u_target=grid.mask(burgers1d_exact(x, horizon, nu)),
+        u_guess=grid.mask(burgers1d_guess(x, nu, guess_center)),
+        u_exact_ic=grid.mask(burgers1d_exact(x, 0.0, nu)),
+        exact_solution=lambda x, t, nu=nu: burgers1d_exact(x, t, nu),
+        checkpoint_slots=checkpoint_slots)
+
+
+def make_problem(kind, **params):
+    from . import configs
+    builders = {"burgers1d": burgers1d_problem, "cfg1": configs.cfg1_problem}
+    if kind not in builders:
+        raise ValidationError(f"unknown problem {kind!r}; on the B200 path choose from "
+                              f"{sorted(builders)}")
+    return builders[kind](**params)
+
+
+def spectral_error_estimate(values, grid):
+    raise ValidationError("the spectral error estimator is outside the B200 hot path")

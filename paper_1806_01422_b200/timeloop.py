@@ -1,0 +1,299 @@
+"""Explicit-RK forward sweep on the B200 (reference ``semopt/timeloop.py``).
+
+Every RK stage is ONE fused kernel (``sem1d_rk_stage``): it applies F to the
+stage input and, in its epilogue, forms the next stage state (or the new
+step state) from the base state and the stored slopes, so a step is s
+launches and the stage temporaries of ``timeloop.py:111-130`` never exist.
+
+Schemes: the reference's ``euler`` and ``rk3`` (Kutta-3, ``timeloop.py:24-27``)
+with the reference's association order, plus ``rk4`` (classic tableau; absent
+from the reference -- see DESIGN.md).  ``cn`` and adaptive control are outside
+the B200 hot path and raise ValidationError at integrate time.
+
+Host control flow (dt clipping, StepFailure retries with dt halving,
+snapshot selection) replicates ``timeloop.py:221-329`` exactly; the non-finite
+checks of ``timeloop.py:100-103`` and ``ops.py:222-223`` come back as device
+flag bits, read once per step.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import IntegrationError, NumericFailure, StepFailure, ValidationError
+
+RK3_A = ((), (0.5,), (-1.0, 2.0))
+RK3_B = (1.0 / 6.0, 2.0 / 3.0, 1.0 / 6.0)
+RK3_BHAT = (0.0, 1.0, 0.0)
+RK3_EMBEDDED_ORDER = 2
+
+TABLEAUX = {
+    "euler": (((),), (1.0,)),
+    "rk3": (RK3_A, RK3_B),
+    "rk4": (((), (0.5,), (0.0, 0.5), (0.0, 0.0, 1.0)), (1.0 / 6.0, 1.0 / 3.0, 1.0 / 3.0, 1.0 / 6.0)),
+}
+
+_RETRY_HALVINGS = 3   # timeloop.py:29
+
+
+@dataclass
+class TsConfig:
+    """Time-stepper configuration (timeloop.py:32-76); ``rk4`` added."""
+
+    scheme: str = "rk3"
+    t0: float = 0.0
+    t_end: float = 1.0
+    dt: float = 0.01
+    adaptive: bool = False
+    tol_a: float = 1e-8
+    tol_r: float = 1e-8
+    alpha_min: float = 0.1
+    alpha_max: float = 5.0
+    beta: float = 0.9
+    max_steps: int = 1_000_000
+    newton_tol: float = 1e-10
+    newton_max: int = 25
+    gmres_tol: float = 1e-10
+    gmres_max: int = 200
+    gmres_restart: int = 30
+    wlte_form: str = "rms"
+
+    def __post_init__(self):
+        self.validate()
+
+    def validate(self):
+        if self.scheme not in ("euler", "rk3", "rk4", "cn"):
+            raise ValidationError(f"unknown scheme {self.scheme!r}")
+        if not self.t_end > self.t0:
+            raise ValidationError("t_end must exceed t0")
+        if not self.dt > 0.0:
+            raise ValidationError("dt must be positive")
+        if not (0.0 < self.alpha_min < 1.0 < self.alpha_max):
+            raise ValidationError("need 0 < alpha_min < 1 < alpha_max")
+        if not (0.0 < self.beta < 1.0):
+            raise ValidationError("need 0 < beta < 1")
+        if self.adaptive and self.scheme != "rk3":
+            raise ValidationError("adaptive stepping requires the embedded rk3 pair")
+        if self.wlte_form not in ("rms", "max"):
+            raise ValidationError(f"unknown wlte form {self.wlte_form!r}")
+
+
+@dataclass
+class ForwardResult:
+    """Recorded trajectory (timeloop.py:79-97); states are device tensors."""
+
+    ts: np.ndarray
+    dts: np.ndarray
+    snapshots: dict
+    u_final: object
+    stats: dict = field(default_factory=dict)
+    step_log: list = field(default_factory=list)
+
+    @property
+    def n_steps(self):
+        return len(self.dts)
+
+
+def _require_explicit(cfg):
+    if cfg.scheme == "cn":
+        raise ValidationError("Crank-Nicolson is outside the B200 hot path (SURVEY.md 8(f))")
+    if cfg.adaptive:
+        raise ValidationError("adaptive stepping is outside the B200 hot path (SURVEY.md 8(f))")
+
+
+def _nonzero_terms(coefs, upto):
+    return [(j, float(coefs[j])) for j in range(min(upto, len(coefs))) if coefs[j] != 0.0]
+
+
+class StepEngine:
+    """Launch plan + device scratch for one explicit step of a tableau.
+
+    Stage kernel i computes k_i = F(U_i) and writes U_{i+1} (or, for the last
+    stage, the new state) = base + dt * sum_j c_j k_j; slopes are stored only
+    when a later combination reads them.
+    """
+
+    def __init__(self, op, scheme):
+        if scheme not in TABLEAUX:
+            raise ValidationError(f"unknown scheme {scheme!r}")
+        self.op, self.scheme = op, scheme
+        A, b = TABLEAUX[scheme]
+        self.A, self.b, self.s = A, b, len(b)
+        s = self.s
+        # combination rows: row i+1 of A for stages, b for the step
+        self.rows = [_nonzero_terms(A[i + 1], i + 1) for i in range(s - 1)]
+        self.rows.append(_nonzero_terms(b, s))
+        need = set()
+        for i, row in enumerate(self.rows):
+            for j, _ in row:
+                if j < i:
+                    need.add(j)
+        self.stored_k = sorted(need)
+        # stage recomputation (adjoint) only needs the A rows
+        need_rec = set()
+        for i, row in enumerate(self.rows[:-1]):
+            for j, _ in row:
+                if j < i:
+                    need_rec.add(j)
+        self.stored_k_recompute = sorted(need_rec)
+        self._k = {}
+        self._ping = None
+
+    def _buf(self, key):
+        t = self._k.get(key)
+        if t is None:
+            t = self.op.empty()
+            self._k[key] = t
+        return t
+
+    def _launch_stage(self, i, U_in, base, dt, Y, check, store):
+        row = self.rows[i]
+        terms = [None if j == i else self._k[("k", j)] for j, _ in row]
+        coefs = [c for _, c in row]
+        k_out = self._buf(("k", i)) if i in store else None
+        self.op.launch_rk_stage(U_in, k_out, base, terms, coefs, dt, Y, check)
+
+    def step(self, u, dt, out):
+        """Launch one full step u -> out (no host sync)."""
+        s = self.s
+        store = set(self.stored_k)
+        for j in store:
+            self._buf(("k", j))
+        U = u
+        for i in range(s):
+            if i == s - 1:
+                self._launch_stage(i, U, u, dt, out, True, store)
+            else:
+                Y = self._buf(("U", i % 2))
+                self._launch_stage(i, U, u, dt, Y, False, store)
+                U = Y
+        self.op.counters["rhs"] += s
+
+    def stages(self, u, dt, bufs):
+        """Recompute stage states U_1..U_{s-1} into bufs[0..s-2]; returns [u, U_1, ...]."""
+        s = self.s
+        store = set(self.stored_k_recompute)
+        for j in store:
+            self._buf(("k", j))
+        Us = [u]
+        for i in range(s - 1):
+            self._launch_stage(i, Us[-1], u, dt, bufs[i], False, store)
+            Us.append(bufs[i])
+        self.op.counters["rhs"] += s - 1
+        return Us
+
+
+def engine_for(op, scheme):
+    cache = op.__dict__.setdefault("_engines", {})
+    e = cache.get(scheme)
+    if e is None:
+        e = StepEngine(op, scheme)
+        cache[scheme] = e
+    return e
+
+
+def check_step_flags(op):
+    """Map device flags of one step to the reference exceptions."""
+    v = op.flags()
+    if v & (_lib.SEM1D_FLAG_STATE_NONFINITE | _lib.SEM1D_FLAG_INPUT2_NONFINITE):
+        raise NumericFailure("state contains NaN/Inf")
+    if v & _lib.SEM1D_FLAG_STEP_NONFINITE:
+        raise StepFailure("state contains NaN/Inf")
+
+
+def step_forward(op, u, t, dt, cfg, stats=None, out=None, check=True):
+    """One step of the configured scheme (timeloop.py:189-195); returns the new state."""
+    _require_explicit(cfg)
+    if out is None:
+        out = op.empty()
+    engine_for(op, cfg.scheme).step(u, dt, out)
+    if check:
+        check_step_flags(op)
+    return out
+
+
+def count_steps(cfg):
+    """Number of fixed-dt steps (timeloop.py:221-234)."""
+    if cfg.adaptive:
+        raise ValidationError("step count of an adaptive run is not known a priori")
+    tiny = 1e-9 * cfg.dt
+    t, n = cfg.t0, 0
+    while t < cfg.t_end - tiny:
+        clipped = (cfg.t_end - t) - cfg.dt <= tiny
+        t = cfg.t_end if clipped else t + cfg.dt
+        n += 1
+        if n > cfg.max_steps:
+            raise ValidationError(f"fixed-dt run exceeds max_steps={cfg.max_steps}")
+    return n
+
+
+def integrate(op, u0, cfg, store_steps="all", keep_log=False):
+    """Integrate t0 -> t_end recording the trajectory (timeloop.py:237-329).
+
+    ``store_steps``: "all", an iterable of step indices, or None (step 0 only).
+    Stored states stay on the device; a StepFailure is retried with dt halved
+    up to three times, exactly like the reference.
+    """
+    _require_explicit(cfg)
+    u, _ = op.field(u0, "initial state")
+    if not bool(op._isfinite_all(u)):
+        raise NumericFailure("initial state contains NaN/Inf")
+    store_all = store_steps == "all"
+    want = None if store_all else ({0} if store_steps is None else {int(s) for s in store_steps})
+    stats = {"steps": 0, "rejects": 0, "retries": 0, "newton_iters": 0, "gmres_iters": 0}
+    snapshots = {}
+    if store_all or 0 in want:
+        snapshots[0] = u.clone()
+    ts, dts = [cfg.t0], []
+    log = [] if keep_log else None
+    t, dt_next = cfg.t0, cfg.dt
+    tiny = 1e-9 * cfg.dt
+    n = attempts = 0
+    engine = engine_for(op, cfg.scheme)
+    op.flags()  # clear stale bits
+    while t < cfg.t_end - tiny:
+        attempts += 1
+        if attempts > cfg.max_steps:
+            raise IntegrationError(f"max_steps={cfg.max_steps} exceeded at t={t:.6g}",
+                                   diagnostics={"t": t, "steps": n, "stats": stats})
+        remaining = cfg.t_end - t
+        clipped = remaining - dt_next <= tiny
+        dt = remaining if clipped else dt_next
+        u_new = op.empty()
+        for retry in range(_RETRY_HALVINGS + 1):
+            try:
+                engine.step(u, dt, u_new)
+                check_step_flags(op)
+                break
+            except StepFailure:
+                stats["retries"] += 1
+                if retry == _RETRY_HALVINGS:
+                    raise
+                dt *= 0.5
+                clipped = False
+        if dt != dt_next and not clipped:
+            dt_next = dt
+        n += 1
+        t = cfg.t_end if clipped else t + dt
+        dts.append(dt)
+        ts.append(t)
+        u = u_new
+        stats["steps"] = n
+        if store_all or n in want:
+            snapshots[n] = u
+        if keep_log:
+            log.append((n, t, dt, 0.0, 1))
+    return ForwardResult(ts=np.asarray(ts), dts=np.asarray(dts), snapshots=snapshots,
+                         u_final=u, stats=stats, step_log=log if keep_log else [])
+
+
+def rk3_stages(op, u, t, dt):
+    """Stage states (U1, U2, U3) of the Kutta-3 step (timeloop.py:111-117)."""
+    e = engine_for(op, "rk3")
+    bufs = [op.empty(), op.empty()]
+    Us = e.stages(u, dt, bufs)
+    check_step_flags(op)
+    return tuple(Us)

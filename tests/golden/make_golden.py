@@ -1,0 +1,195 @@
+"""Generate the golden fixtures from the REAL reference (semopt 0.1.0).
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports ``semopt`` from /root/reference/pkg/src and writes small .npz files
+next to this script.  The fixtures travel with the repo; nothing on the GPU box
+reads /root/reference.  Inputs are seeded numpy PCG64 draws per global node in
+node order.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+def _ref():
+    sys.path.insert(0, REF)
+    import semopt  # noqa: F401
+    from semopt import adjoint, checkpoint, grid, ops, optimize, problems, timeloop
+    return semopt, grid, ops, timeloop, adjoint, checkpoint, problems, optimize
+
+
+def basis_fixture(semopt, ops, grid):
+    out = {}
+    for n in list(range(1, 33)) + [48, 64]:
+        b = semopt.gll_rule(n)
+        out[f"nodes_{n}"] = b.nodes
+        out[f"weights_{n}"] = b.weights
+        out[f"diff_{n}"] = b.diff
+        g = grid.grid_1d(-1.0, 1.0, 16, n)
+        op = ops.SemOperator(g, ops.PdeCoefficients(0.01))
+        out[f"K_{n}"] = op._kmat[0]
+        out[f"Dw_{n}"] = op._dw[0]
+    return out
+
+
+MAP_CASES = [
+    (0.0, 1.0, 2, 2, "periodic"), (-1.0, 1.0, 1, 4, "dirichlet0"), (0.0, 1.0, 2, 1, "periodic"),
+    (-1.0, 1.0, 3, 4, "periodic"), (-1.0, 1.0, 16, 9, "periodic"), (-1.0, 1.0, 16, 9, "dirichlet0"),
+    (-2.0, 2.0, 5, 8, "dirichlet0"), (-1.0, 1.0, 4, 31, "periodic"), (0.0, 20.0, 256, 15, "periodic"),
+    (-1.0, 1.0, 1, 3, "periodic"), (-1.0, 1.0, 7, 1, "dirichlet0"),
+]
+
+
+def maps_fixture(grid):
+    out = {}
+    for k, (xa, xb, e, n, bc) in enumerate(MAP_CASES):
+        g = grid.grid_1d(xa, xb, e, n, bc)
+        out[f"case_{k}"] = np.array([xa, xb, e, n, bc == "periodic"], dtype=float)
+        out[f"table_{k}"] = g.table
+        out[f"mult_{k}"] = g.multiplicity
+        out[f"mass_{k}"] = g.mass_scalar
+        out[f"mask_{k}"] = g.mask_scalar
+        out[f"coords_{k}"] = g.node_coordinates()[0]
+    return out
+
+
+# (xa, xb, E, N, bc, nu, seed)
+OP_CASES = [
+    (-1.0, 1.0, 16, 9, "periodic", 0.01, 0),
+    (-1.0, 1.0, 16, 9, "dirichlet0", 0.01, 1),
+    (-1.0, 1.0, 3, 4, "periodic", 0.01, 2),
+    (-1.0, 1.0, 64, 7, "periodic", 0.01, 3),
+    (-1.0, 1.0, 64, 7, "dirichlet0", 0.01, 4),
+    (0.0, 20.0, 32, 15, "periodic", 0.01, 5),
+    (-1.0, 1.0, 8, 31, "periodic", 1e-3, 6),
+    (-1.0, 1.0, 1, 5, "periodic", 0.05, 7),
+    (-1.0, 1.0, 2, 1, "periodic", 0.1, 8),
+    (-1.0, 1.0, 5, 2, "dirichlet0", 0.1, 9),
+    (-1.0, 1.0, 300, 3, "periodic", 0.02, 10),
+    (-1.0, 1.0, 40, 12, "dirichlet0", 0.005, 11),
+]
+
+
+def ops_fixture(grid, ops):
+    out = {}
+    for k, (xa, xb, e, n, bc, nu, seed) in enumerate(OP_CASES):
+        g = grid.grid_1d(xa, xb, e, n, bc)
+        op = ops.SemOperator(g, ops.PdeCoefficients(nu))
+        rng = np.random.default_rng(seed)
+        u = rng.uniform(-1.0, 1.0, g.nglobal)
+        v = rng.standard_normal(g.nglobal)
+        w = rng.standard_normal(g.nglobal)
+        out[f"case_{k}"] = np.array([xa, xb, e, n, bc == "periodic", nu, seed], dtype=float)
+        out[f"u_{k}"], out[f"v_{k}"], out[f"w_{k}"] = u, v, w
+        out[f"f_{k}"] = op.apply_rhs(u)
+        out[f"jv_{k}"] = op.apply_jacobian(u, v)
+        out[f"jtw_{k}"] = op.apply_jacobian_transpose(u, w)
+    return out
+
+
+def cfg1_inputs(grid, bc):
+    """BASELINE config 1: E=16, N=9, nu=0.01 on [-1,1]; u0 = sin(pi x) + 0.01 N(0,1)."""
+    g = grid.grid_1d(-1.0, 1.0, 16, 9, bc)
+    x = g.node_coordinates()[0]
+    rng = np.random.default_rng(1806)
+    u0 = g.mask(np.sin(np.pi * x) + 0.01 * rng.standard_normal(g.nglobal))
+    u_obs0 = g.mask(np.sin(np.pi * x) + 0.5 * np.sin(2.0 * np.pi * x))
+    return g, u0, u_obs0
+
+
+def sweep_fixture(grid, ops, timeloop, adjoint, checkpoint, problems, optimize):
+    out = {}
+    for bc in ("periodic", "dirichlet0"):
+        for scheme in ("rk3", "euler"):
+            g, u0, uo0 = cfg1_inputs(grid, bc)
+            op = ops.SemOperator(g, ops.PdeCoefficients(0.01))
+            ts = timeloop.TsConfig(scheme=scheme, t0=0.0, t_end=20 * 1e-4, dt=1e-4)
+            target = timeloop.integrate(op, uo0, ts, store_steps=None).u_final
+            prob = problems.AssimilationProblem(name="cfg1", grid=g, op=op, ts=ts,
+                                                u_target=target, u_guess=u0)
+            j, gr = prob.evaluate(u0)
+            key = f"{bc}_{scheme}"
+            out[f"u0_{key}"], out[f"target_{key}"] = u0, target
+            out[f"J_{key}"] = np.array([j])
+            out[f"grad_{key}"] = gr
+            out[f"ufinal_{key}"] = prob.last_forward.u_final
+            out[f"dts_{key}"] = prob.last_forward.dts
+            out[f"counters_{key}"] = np.array([op.counters["rhs"], op.counters["jac"],
+                                               op.counters["jact"]])
+            # binomial checkpointing must give the same gradient
+            prob_b = problems.AssimilationProblem(name="cfg1b", grid=g, op=op, ts=ts,
+                                                  u_target=target, u_guess=u0,
+                                                  checkpoint_slots=4)
+            jb, gb = prob_b.evaluate(u0)
+            out[f"gradbinom_{key}"] = gb
+    # a longer RK3 periodic run (m=100) for schedule transparency
+    g, u0, uo0 = cfg1_inputs(grid, "periodic")
+    op = ops.SemOperator(g, ops.PdeCoefficients(0.01))
+    ts = timeloop.TsConfig(scheme="rk3", t0=0.0, t_end=0.0123, dt=1e-4)  # clipped last step
+    target = timeloop.integrate(op, uo0, ts, store_steps=None).u_final
+    prob = problems.AssimilationProblem(name="cfg1l", grid=g, op=op, ts=ts,
+                                        u_target=target, u_guess=u0, checkpoint_slots=10)
+    j, gr = prob.evaluate(u0)
+    out["long_target"], out["long_J"], out["long_grad"] = target, np.array([j]), gr
+    out["long_dts"] = prob.last_forward.dts
+    # three L-BFGS iterations on cfg1 periodic RK3
+    g, u0, uo0 = cfg1_inputs(grid, "periodic")
+    op = ops.SemOperator(g, ops.PdeCoefficients(0.01))
+    ts = timeloop.TsConfig(scheme="rk3", t0=0.0, t_end=20 * 1e-4, dt=1e-4)
+    target = timeloop.integrate(op, uo0, ts, store_steps=None).u_final
+    prob = problems.AssimilationProblem(name="cfg1o", grid=g, op=op, ts=ts,
+                                        u_target=target, u_guess=u0)
+    res = optimize.minimize(prob.evaluate, u0, optimize.OptimConfig(max_iters=3))
+    out["opt_log"] = np.array([[r[0], r[1], r[2], r[3], r[4]] for r in res.log])
+    out["opt_x"] = res.x
+    return out
+
+
+SCHED_CASES = [(1, 1), (3, 3), (5, 2), (10, 3), (20, 4), (30, 5), (100, 10), (57, 7), (500, 64)]
+
+
+def schedules_fixture(checkpoint):
+    out = {}
+    kinds = {"Store": 0, "Restore": 1, "Advance": 2, "AdjointStep": 3, "Done": 4}
+    for m, s in SCHED_CASES:
+        sch = checkpoint.plan_binomial(m, s)
+        rows = []
+        for a in sch.actions:
+            name = type(a).__name__
+            if name in ("Store", "Restore"):
+                rows.append((kinds[name], a.slot, a.step))
+            elif name == "Advance":
+                rows.append((kinds[name], a.start, a.stop))
+            elif name == "AdjointStep":
+                rows.append((kinds[name], a.step, -1))
+            else:
+                rows.append((kinds[name], -1, -1))
+        out[f"actions_{m}_{s}"] = np.array(rows, dtype=np.int64)
+        out[f"meta_{m}_{s}"] = np.array([sch.recomputed, sch.backward_start, sch.slots])
+        out[f"stores_{m}_{s}"] = np.array(sorted(sch.forward_stores.items()), dtype=np.int64)
+    return out
+
+
+def main():
+    semopt, grid, ops, timeloop, adjoint, checkpoint, problems, optimize = _ref()
+    np.savez_compressed(os.path.join(HERE, "basis.npz"), **basis_fixture(semopt, ops, grid))
+    np.savez_compressed(os.path.join(HERE, "maps.npz"), **maps_fixture(grid))
+    np.savez_compressed(os.path.join(HERE, "ops.npz"), **ops_fixture(grid, ops))
+    np.savez_compressed(os.path.join(HERE, "sweeps.npz"),
+                        **sweep_fixture(grid, ops, timeloop, adjoint, checkpoint, problems, optimize))
+    np.savez_compressed(os.path.join(HERE, "schedules.npz"), **schedules_fixture(checkpoint))
+    print("golden fixtures written to", HERE)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,180 @@
+"""Operator parity on the B200: F, J v, J^T w through the C ABI vs the reference
+fixtures and the oracle.  Tolerances (BASELINE north_star): 1e-12 relative (max-abs,
+normalised by the reference's max) per apply on the BASELINE's rough inputs;
+integer maps and the gather bit-exact."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1806_01422_b200 as sb
+from oracle import semref as R
+from paper_1806_01422_b200 import configs
+from paper_1806_01422_b200.grid import grid_1d
+from semtest_util import golden, rel_err
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def _op(xa, xb, E, N, periodic, nu, batch=1):
+    g = grid_1d(xa, xb, int(E), int(N), "periodic" if periodic else "dirichlet0")
+    return sb.SemOperator(g, sb.PdeCoefficients(nu), device="cuda:0", batch=batch)
+
+
+def test_golden_operator_cases(cuda):
+    g = golden("ops.npz")
+    k = 0
+    while f"case_{k}" in g:
+        xa, xb, E, N, per, nu, _ = g[f"case_{k}"]
+        op = _op(xa, xb, E, N, per, nu)
+        u, v, w = g[f"u_{k}"], g[f"v_{k}"], g[f"w_{k}"]
+        assert rel_err(op.apply_rhs(u), g[f"f_{k}"]) <= TOL, k
+        assert rel_err(op.apply_jacobian(u, v), g[f"jv_{k}"]) <= TOL, k
+        assert rel_err(op.apply_jacobian_transpose(u, w), g[f"jtw_{k}"]) <= TOL, k
+        assert op.counters == {"rhs": 1, "jac": 1, "jact": 1}
+        k += 1
+
+
+@pytest.mark.parametrize("N", list(range(1, 33)))
+@pytest.mark.parametrize("periodic", [True, False])
+def test_every_degree_vs_oracle(cuda, N, periodic):
+    # element counts straddle the CTA tile (256 / 128 elements) to exercise halos and tails
+    E = {1: 700, 2: 300}.get(N, 261 if N <= 8 else 131)
+    nu = 0.01
+    op = _op(-1.0, 1.0, E, N, periodic, nu)
+    ref = R.BurgersOracle(R.Mesh1D(-1.0, 1.0, E, N, periodic), nu)
+    u, v, w = R.seeded_fields(ref.mesh.ndof, 100 + N)
+    assert rel_err(op.apply_rhs(u), ref.rhs(u)) <= TOL
+    assert rel_err(op.apply_jacobian(u, v), ref.jac(u, v)) <= TOL
+    assert rel_err(op.apply_jacobian_transpose(u, w), ref.jact(u, w)) <= TOL
+
+
+@pytest.mark.parametrize("E", [1, 2, 3, 255, 256, 257, 512, 1000])
+def test_tile_edges(cuda, E):
+    for periodic in (True, False):
+        N = 7 if (periodic or E > 0) else 7
+        if periodic and E * N < 2:
+            continue
+        op = _op(0.0, 3.0, E, N, periodic, 0.02)
+        ref = R.BurgersOracle(R.Mesh1D(0.0, 3.0, E, N, periodic), 0.02)
+        u, v, w = R.seeded_fields(ref.mesh.ndof, E)
+        assert rel_err(op.apply_rhs(u), ref.rhs(u)) <= TOL
+        assert rel_err(op.apply_jacobian(u, v), ref.jac(u, v)) <= TOL
+        assert rel_err(op.apply_jacobian_transpose(u, w), ref.jact(u, w)) <= TOL
+
+
+def test_batched_operator_equals_per_problem(cuda):
+    B, E, N = 5, 40, 15
+    op = _op(0.0, 20.0, E, N, True, 0.01, batch=B)
+    ref = R.BurgersOracle(R.Mesh1D(0.0, 20.0, E, N, True), 0.01)
+    rng = np.random.default_rng(5)
+    U = rng.uniform(-1, 1, (B, ref.mesh.ndof))
+    W = rng.standard_normal((B, ref.mesh.ndof))
+    F = op.apply_rhs(U)
+    JT = op.apply_jacobian_transpose(U, W)
+    for b in range(B):
+        assert rel_err(F[b], ref.rhs(U[b])) <= TOL
+        assert rel_err(JT[b], ref.jact(U[b], W[b])) <= TOL
+
+
+def test_scatter_gather_bit_exact(cuda):
+    for per in (True, False):
+        for E, N in [(1, 3), (2, 1), (16, 9), (300, 7)]:
+            if per and E * N < 2:
+                continue
+            grid = grid_1d(-1.0, 1.0, E, N, "periodic" if per else "dirichlet0")
+            m = R.Mesh1D(-1.0, 1.0, E, N, per)
+            rng = np.random.default_rng(E * 31 + N)
+            u = rng.standard_normal(grid.nglobal)
+            loc = rng.standard_normal((1, E, N + 1))
+            assert np.array_equal(grid.scatter(u)[0], m.localize(u))
+            assert np.array_equal(grid.gather(loc), m.assemble(loc[0]))
+            ones = np.ones((1, E, N + 1))
+            assert np.array_equal(grid.gather(ones), grid.multiplicity)
+
+
+def test_nonfinite_inputs_raise(cuda):
+    op = _op(-1.0, 1.0, 16, 9, True, 0.01)
+    u = np.zeros(op.ndof)
+    bad = u.copy()
+    bad[77] = np.nan
+    with pytest.raises(sb.NumericFailure, match="state"):
+        op.apply_rhs(bad)
+    with pytest.raises(sb.NumericFailure, match="tangent"):
+        op.apply_jacobian(u, bad)
+    bad[77] = np.inf
+    with pytest.raises(sb.NumericFailure, match="cotangent"):
+        op.apply_jacobian_transpose(u, bad)
+    op.apply_rhs(u)  # flag was cleared
+    with pytest.raises(sb.ValidationError):
+        op.apply_rhs(np.zeros(op.ndof + 1))
+
+
+def test_operator_properties(cuda):
+    """SPEC.md ops invariants: F(const) = 0, 1^T M f = 0 (periodic), J linear in w,
+    J vs central FD, dot-product identity, densify^T z = J^T z."""
+    op = _op(-1.0, 1.0, 3, 4, True, 0.01)
+    n = op.ndof
+    assert np.max(np.abs(op.apply_rhs(np.full(n, 0.7)))) <= 1e-13
+    rng = np.random.default_rng(11)
+    u = rng.uniform(-1, 1, n)
+    f = op.apply_rhs(u)
+    assert abs(op.grid.mass_scalar @ f) <= 1e-12 * np.abs(op.grid.mass_scalar * f).sum()
+    w = rng.standard_normal(n)
+    eps = 1e-5
+    fd = (op.apply_rhs(u + eps * w) - op.apply_rhs(u - eps * w)) / (2 * eps)
+    assert rel_err(fd, op.apply_jacobian(u, w)) <= 1e-8
+    for per in (True, False):
+        op = _op(-1.0, 1.0, 3, 4, per, 0.01)
+        mask = op.grid.mask_scalar
+        for _ in range(200):
+            u, w, z = (rng.standard_normal(op.ndof) * mask for _ in range(3))
+            lhs = op.apply_jacobian(u, w) @ z
+            rhs = w @ op.apply_jacobian_transpose(u, z)
+            assert abs(lhs - rhs) / (np.linalg.norm(w) * np.linalg.norm(z)) <= 1e-13
+        Jd = op.densify(u)
+        assert rel_err(Jd.T @ z, op.apply_jacobian_transpose(u, z)) <= 1e-12
+
+
+def test_device_tensors_in_device_tensors_out(cuda):
+    op = _op(-1.0, 1.0, 64, 7, True, 0.01)
+    u = torch.rand(op.ndof, dtype=torch.float64, device=cuda)
+    f = op.apply_rhs(u)
+    assert isinstance(f, torch.Tensor) and f.is_cuda
+    assert torch.equal(f, op.apply_rhs(u))  # bitwise reproducible
+
+
+def test_cfg2_full_size_properties(cuda):
+    """BASELINE config 2 at full size (E = 2^22, N = 7): size-independent checks --
+    linearity of J and J^T, the dot-product identity, and oracle parity on a
+    periodic sub-window computed on the host."""
+    c = configs.CFG2
+    op = configs.cfg_operator(c, device="cuda:0")
+    u, v, w = configs.operator_inputs(op.ndof, c["seed"])
+    ud, vd, wd = (torch.from_numpy(a).to(cuda) for a in (u, v, w))
+    f = op.apply_rhs(ud)
+    jv = op.apply_jacobian(ud, vd)
+    jtw = op.apply_jacobian_transpose(ud, wd)
+    assert torch.isfinite(f).all() and torch.isfinite(jv).all() and torch.isfinite(jtw).all()
+    # linearity
+    jv2 = op.apply_jacobian(ud, 2.0 * vd + wd)
+    lin = 2.0 * jv + op.apply_jacobian(ud, wd)
+    assert float((jv2 - lin).abs().max() / lin.abs().max()) <= 1e-12
+    # dot-product identity at full size
+    lhs = float(torch.dot(jv, wd))
+    rhs = float(torch.dot(vd, jtw))
+    assert abs(lhs - rhs) / (float(vd.norm()) * float(wd.norm())) <= 1e-12
+    # oracle on windows of elements: element-local results away from the window edge
+    N, E = c["N"], c["E"]
+    fh, jh = f.cpu().numpy(), jtw.cpu().numpy()
+    h = (c["xb"] - c["xa"]) / E
+    for e0 in (0, E // 2 - 17, E - 64):
+        ne = 64
+        sub = R.BurgersOracle(R.Mesh1D(0.0, ne * h, ne, N, True), c["nu"])
+        idx = (np.arange(e0 * N, (e0 + ne) * N)) % op.ndof
+        fs = sub.rhs(u[idx])
+        js = sub.jact(u[idx], w[idx])
+        inner = slice(N + 1, (ne - 1) * N)   # interior nodes do not see the window wrap
+        assert rel_err(fh[idx][inner], fs[inner]) <= TOL
+        assert rel_err(jh[idx][inner], js[inner]) <= TOL

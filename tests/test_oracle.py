@@ -1,0 +1,151 @@
+"""The oracle (oracle/semref.py) pinned against fixtures made by the REAL reference
+(tests/golden/make_golden.py), plus the SPEC.md known-answer tests."""
+
+import numpy as np
+import pytest
+
+from oracle import semref as R
+from semtest_util import golden
+
+DEGREES = list(range(1, 33)) + [48, 64]
+
+
+@pytest.mark.parametrize("n", DEGREES)
+def test_basis_bit_exact(n):
+    g = golden("basis.npz")
+    x, w = R.gll_nodes_weights(n)
+    assert np.array_equal(x, g[f"nodes_{n}"])
+    assert np.array_equal(w, g[f"weights_{n}"])
+    assert np.array_equal(R.diff_matrix(x), g[f"diff_{n}"])
+    op = R.BurgersOracle(R.Mesh1D(-1.0, 1.0, 16, n), 0.01)
+    assert np.array_equal(op.K, g[f"K_{n}"])
+    assert np.array_equal(op.Dw, g[f"Dw_{n}"])
+
+
+def test_basis_kats():
+    # SPEC.md:43-45,52-54
+    x, w = R.gll_nodes_weights(1)
+    assert np.allclose(x, [-1, 1]) and np.allclose(w, [1, 1])
+    x, w = R.gll_nodes_weights(2)
+    assert np.allclose(x, [-1, 0, 1], atol=1e-15) and np.allclose(w, [1 / 3, 4 / 3, 1 / 3])
+    assert np.allclose(R.diff_matrix(R.gll_nodes_weights(1)[0]), [[-0.5, 0.5], [-0.5, 0.5]])
+    x, w = R.gll_nodes_weights(8)
+    assert abs(np.sum(w * x ** 14) - 2.0 / 15.0) <= 1e-14
+    for n in range(1, 17):
+        x, w = R.gll_nodes_weights(n)
+        for k in range(2 * n):
+            exact = 0.0 if k % 2 else 2.0 / (k + 1)
+            assert abs(np.sum(w * x ** k) - exact) <= 1e-12
+        d = R.diff_matrix(x)
+        for k in range(1, n + 1):
+            assert np.max(np.abs(d @ x ** k - k * x ** (k - 1))) <= 1e-10
+
+
+def _mesh_from_case(c):
+    xa, xb, e, n, per = c[:5]
+    return R.Mesh1D(xa, xb, int(e), int(n), bool(per))
+
+
+def test_maps_bit_exact():
+    g = golden("maps.npz")
+    k = 0
+    while f"case_{k}" in g:
+        m = _mesh_from_case(g[f"case_{k}"])
+        assert np.array_equal(m.table, g[f"table_{k}"])
+        assert np.array_equal(m.multiplicity, g[f"mult_{k}"])
+        assert np.array_equal(m.mass, g[f"mass_{k}"])
+        assert np.array_equal(m.maskv, g[f"mask_{k}"])
+        assert np.array_equal(m.coordinates(), g[f"coords_{k}"])
+        k += 1
+    assert k >= 10
+
+
+def test_ops_bit_exact():
+    g = golden("ops.npz")
+    k = 0
+    while f"case_{k}" in g:
+        c = g[f"case_{k}"]
+        op = R.BurgersOracle(_mesh_from_case(c), c[5])
+        u, v, w = g[f"u_{k}"], g[f"v_{k}"], g[f"w_{k}"]
+        assert np.array_equal(op.rhs(u), g[f"f_{k}"])
+        assert np.array_equal(op.jac(u, v), g[f"jv_{k}"])
+        assert np.array_equal(op.jact(u, w), g[f"jtw_{k}"])
+        k += 1
+
+
+@pytest.mark.parametrize("bc", ["periodic", "dirichlet0"])
+@pytest.mark.parametrize("scheme", ["rk3", "euler"])
+def test_sweep_bit_exact(bc, scheme):
+    g = golden("sweeps.npz")
+    key = f"{bc}_{scheme}"
+    op = R.BurgersOracle(R.Mesh1D(-1.0, 1.0, 16, 9, bc == "periodic"), 0.01)
+    j, grad, uf = R.evaluate(op, g[f"u0_{key}"], g[f"target_{key}"], 0.0, 20 * 1e-4, 1e-4, scheme)
+    assert j == g[f"J_{key}"][0]
+    assert np.array_equal(grad, g[f"grad_{key}"])
+    assert np.array_equal(uf, g[f"ufinal_{key}"])
+    _, dts = R.step_sizes(0.0, 20 * 1e-4, 1e-4)
+    assert np.array_equal(dts, g[f"dts_{key}"])
+    # binomial checkpointing replays identical arithmetic
+    assert np.array_equal(grad, g[f"gradbinom_{key}"])
+
+
+def test_long_sweep_clipped_last_step():
+    g = golden("sweeps.npz")
+    op = R.BurgersOracle(R.Mesh1D(-1.0, 1.0, 16, 9, True), 0.01)
+    u0 = g["u0_periodic_rk3"]
+    j, grad, _ = R.evaluate(op, u0, g["long_target"], 0.0, 0.0123, 1e-4, "rk3")
+    assert j == g["long_J"][0]
+    assert np.array_equal(grad, g["long_grad"])
+    _, dts = R.step_sizes(0.0, 0.0123, 1e-4)
+    assert np.array_equal(dts, g["long_dts"])
+
+
+def test_rk4_restatement_matches_finite_differences():
+    """RK4 is absent from the reference: pin its adjoint by central FD."""
+    g = golden("sweeps.npz")
+    op = R.BurgersOracle(R.Mesh1D(-1.0, 1.0, 16, 9, True), 0.01)
+    u0, tgt = g["u0_periodic_rk3"], g["target_periodic_rk3"]
+    j, grad, _ = R.evaluate(op, u0, tgt, 0.0, 20 * 1e-4, 1e-4, "rk4")
+    rng = np.random.default_rng(7)
+    for _ in range(3):
+        d = rng.standard_normal(u0.size)
+
+        def fun(u):
+            return R.evaluate(op, u, tgt, 0.0, 20 * 1e-4, 1e-4, "rk4")[0]
+
+        fd = R.finite_difference_gradient(fun, u0, d, eps=1e-4)
+        assert abs(fd - grad @ d) <= 1e-7 * max(1.0, abs(fd))
+
+
+def test_rk3_scalar_kat():
+    """u' = -u, dt = 0.1, u0 = 1 -> 0.9048375 (scalar surrogate of the tableau)."""
+
+    class Scalar:
+        def rhs(self, u):
+            return -u
+
+    # SPEC.md:266 quotes 0.9048375 with the bound |u' - e^-0.1| <= 5e-6; Kutta-3 gives
+    # 1 - 0.1 + 0.005 - 1/6000 = 0.904833..., and 0.9048375 is the RK4 value exactly.
+    u = R.rk_step(Scalar(), np.array([1.0]), 0.1, "rk3")
+    assert abs(u[0] - np.exp(-0.1)) <= 5e-6
+    assert abs(u[0] - (1 - 0.1 + 0.005 - 0.1 ** 3 / 6)) < 1e-15
+    u4 = R.rk_step(Scalar(), np.array([1.0]), 0.1, "rk4")
+    assert abs(u4[0] - 0.9048375) < 1e-15
+
+
+def test_dot_product_identity_oracle():
+    rng = np.random.default_rng(3)
+    for per in (True, False):
+        op = R.BurgersOracle(R.Mesh1D(-1.0, 1.0, 3, 4, per), 0.01)
+        for _ in range(50):
+            # Dirichlet tangent/cotangent fields keep zero boundary entries (SPEC.md ops Field)
+            u, w, z = (op.mesh.apply_mask(rng.standard_normal(op.mesh.ndof)) for _ in range(3))
+            lhs = op.jac(u, w) @ z
+            rhs = w @ op.jact(u, z)
+            assert abs(lhs - rhs) / (np.linalg.norm(w) * np.linalg.norm(z)) <= 1e-13
+
+
+def test_binomial_dp_matches_reference_counts():
+    s = golden("schedules.npz")
+    for m, slots in [(10, 3), (20, 4), (30, 5), (100, 10), (57, 7)]:
+        assert R.binomial_recompute_table(m, slots) - m == s[f"meta_{m}_{slots}"][0]
