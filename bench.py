@@ -151,7 +151,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:  # pragma: no cover
                 pass
-            time.sleep(0.02)
+            time.sleep(0.002)
 
     def __enter__(self):
         if self.nvml is not None:
@@ -218,9 +218,12 @@ def timed_ops(op, ud, vd, wd, outs, steps, stream):
 
 
 def sweep_ratio(op, torch, steps=8):
-    """Forward RK4 sweep vs discrete-adjoint sweep on the config-2 field (store-all)."""
+    """Forward RK4 sweep vs discrete-adjoint sweep on the config-2 field (store-all).
+    h = 4.8e-7 on config 2 makes the explicit limit ~5e-14 (rho*h^2 ~ 13 at nu=0.01),
+    so dt = 1e-14: this measures cost, not physics."""
     from paper_1806_01422_b200 import adjoint, checkpoint, timeloop
-    ts = timeloop.TsConfig(scheme="rk4", t0=0.0, t_end=steps * 1e-6, dt=1e-6)
+    dt = 1e-14
+    ts = timeloop.TsConfig(scheme="rk4", t0=0.0, t_end=steps * dt, dt=dt)
     u0 = torch.sin(torch.linspace(0, 6.283185307179586, op.ndof, dtype=torch.float64,
                                   device=op.device))
     timeloop.integrate(op, u0, ts)  # warm-up

@@ -298,6 +298,255 @@ __global__ void __launch_bounds__(Tile<N>::TPB, Tile<N>::MINB)
   if (EPI == EPI_RK && bad_y) atomicOr(A.flag, SEM1D_FLAG_STEP_NONFINITE);
 }
 
+// ============================================================================
+// Persistent, TMA-pipelined variant (odd N; the BASELINE degrees 7/9/15/31).
+//
+// One CTA per SM slot loops over tiles of TPB elements.  Thread 0 issues the
+// slab loads of the tile STAGES-1 iterations ahead as 1D bulk-tensor copies
+// (cp.async.bulk global->shared, completion counted on an mbarrier), so HBM
+// streams continuously while the CTA contracts the current tile; the
+// non-finite checks and the J^T input scaling move into registers.  The
+// first and last tile of every ring (periodic wrap / Dirichlet ends / ragged
+// tail) take a synchronous per-thread load path.
+// ============================================================================
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int N>
+struct TmaTile {
+  static constexpr int TPB = Tile<N>::TPB;
+  static constexpr int SLAB = (TPB + 1) * N + 1;
+  // +1 double for the 16-byte alignment shift, rounded to a 16-byte multiple
+  static constexpr int SLAB_ALLOC = ((SLAB + 1) + 1) & ~1;
+};
+
+// zm = mask(z * M^-1) for local node j of element e (ops.py:252-254), in registers
+template <int N>
+__device__ __forceinline__ double jt_scale(const Consts<N>& C, double z, int j, int64_t e,
+                                           const Geo& G) {
+  int pos = (j == 0 || j == N) ? 0 : j;
+  bool zero = false;
+  if (!G.periodic) {
+    if (j == 0 && e == 0) { pos = N; zero = true; }
+    if (j == N && e == G.E - 1) { pos = N + 1; zero = true; }
+  }
+  double v = __dmul_rn(z, C.minv[pos]);
+  return zero ? __dmul_rn(v, 0.0) : v;
+}
+
+template <int N, int OP, int EPI, int STAGES>
+__global__ void __launch_bounds__(Tile<N>::TPB, Tile<N>::MINB)
+    apply_tma_kernel(const __grid_constant__ Consts<N> C, const Geo G, const Args A,
+                     const int tiles_per_ring, const int total_tiles) {
+  using TT = TmaTile<N>;
+  constexpr int n = N + 1;
+  constexpr int TPB = TT::TPB;
+  constexpr int NIN = (OP == OP_RHS) ? 1 : 2;
+  constexpr int SA = TT::SLAB_ALLOC;
+  extern __shared__ __align__(16) double smem[];
+  double* stage_buf = smem;                          // [STAGES][NIN][SA]
+  double* so = smem + STAGES * NIN * SA;             // [SA]
+  double* slast = so + SA;                           // [TPB + 2]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(slast + TPB + 2);
+  const int tid = threadIdx.x;
+  const bool periodic = G.periodic != 0;
+  const int64_t last_node = G.E * N;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto tile_of = [&](int T, int64_t& bofs, int64_t& e0, int& nel, bool& boundary) {
+    const int b = T / tiles_per_ring;
+    const int tl = T - b * tiles_per_ring;
+    bofs = (int64_t)b * G.ndof;
+    e0 = (int64_t)tl * TPB;
+    nel = (int)min((int64_t)TPB, G.E - e0);
+    boundary = (tl == 0) || (tl == tiles_per_ring - 1);
+  };
+  auto issue = [&](int T, int s) {  // thread 0
+    int64_t bofs, e0;
+    int nel;
+    bool boundary;
+    tile_of(T, bofs, e0, nel, boundary);
+    if (boundary) return;
+    const int64_t gg0 = bofs + (e0 - 1) * N;
+    const int64_t a0 = gg0 & ~(int64_t)1;
+    const int shift = (int)(gg0 - a0);
+    const int cnt = (nel + 1) * N + 1;
+    const uint32_t bytes = (uint32_t)(((cnt + shift) * 8 + 15) & ~15);
+    mbar_expect_tx(&bars[s], NIN * bytes);
+    bulk_g2s(stage_buf + (s * NIN + 0) * SA, A.u + a0, bytes, &bars[s]);
+    if (NIN == 2) bulk_g2s(stage_buf + (s * NIN + 1) * SA, A.w + a0, bytes, &bars[s]);
+  };
+
+  if (tid == 0) {
+    for (int p = 0; p < STAGES - 1; ++p) {
+      const int T = blockIdx.x + p * gridDim.x;
+      if (T < total_tiles) issue(T, p);
+    }
+  }
+
+  bool bad_u = false, bad_w = false, bad_y = false;
+  uint32_t phases = 0;
+  int iter = 0;
+  for (int T = blockIdx.x; T < total_tiles; T += gridDim.x, ++iter) {
+    const int s = iter % STAGES;
+    if (tid == 0) {
+      const int Tn = T + (STAGES - 1) * gridDim.x;
+      if (Tn < total_tiles) issue(Tn, (iter + STAGES - 1) % STAGES);
+    }
+    int64_t bofs, e0;
+    int nel;
+    bool boundary;
+    tile_of(T, bofs, e0, nel, boundary);
+    double* su = stage_buf + (s * NIN + 0) * SA;
+    double* sw = stage_buf + (s * NIN + 1) * SA;
+    int shift;
+    const int64_t g0 = (e0 - 1) * N;
+    if (boundary) {
+      shift = 0;
+      const int cnt = (nel + 1) * N + 1;
+      for (int k = tid; k < cnt; k += TPB) {
+        int64_t g = g0 + k;
+        bool valid = true;
+        if (g < 0) {
+          if (periodic) g += G.ndof; else valid = false;
+        } else if (g >= G.ndof) {
+          g -= G.ndof;
+        }
+        su[k] = valid ? __ldg(A.u + bofs + g) : 0.0;
+        if (NIN == 2) sw[k] = valid ? __ldg(A.w + bofs + g) : 0.0;
+      }
+      __syncthreads();
+    } else {
+      const int64_t gg0 = bofs + g0;
+      shift = (int)(gg0 & 1);
+      while (!mbar_try_wait(&bars[s], (phases >> s) & 1u)) {
+      }
+      phases ^= (1u << s);
+    }
+
+    // ---- contraction (one element per thread) ----
+    {
+      double x[n], y[(OP != OP_RHS) ? n : 1], t[(OP == OP_JACT) ? n : 1];
+      auto load = [&](int base, int64_t e) {
+#pragma unroll
+        for (int j = 0; j < n; ++j) {
+          x[j] = su[shift + base + j];
+          bad_u |= nonfinite(x[j]);
+          if (OP != OP_RHS) {
+            y[j] = sw[shift + base + j];
+            bad_w |= nonfinite(y[j]);
+            if (OP == OP_JACT) y[j] = jt_scale<N>(C, y[j], j, e, G);
+          }
+        }
+        if (OP == OP_JACT) {
+#pragma unroll
+          for (int j = 0; j < n; ++j) t[j] = __dmul_rn(x[j], y[j]);
+        }
+      };
+      if (tid < nel) {
+        load((tid + 1) * N, e0 + tid);
+#pragma unroll
+        for (int i = 0; i < N; ++i) so[tid * N + i] = elem_row<N, OP>(C, x, y, t, i);
+        slast[tid + 1] = elem_row<N, OP>(C, x, y, t, N);
+      }
+      if (tid == 0) {
+        double hl = 0.0;
+        if (periodic || e0 > 0) {
+          load(0, (e0 == 0) ? G.E - 1 : e0 - 1);
+          hl = elem_row<N, OP>(C, x, y, t, N);
+        }
+        slast[0] = hl;
+      }
+    }
+    __syncthreads();
+
+    // ---- gather, M^-1, mask, stage arithmetic; coalesced stores ----
+    const bool last_tile = (e0 + nel == G.E);
+    const int nout = nel * N + ((!periodic && last_tile) ? 1 : 0);
+    const int64_t gbase = e0 * N;
+    for (int k = tid; k < nout; k += TPB) {
+      const int64_t g = gbase + k;
+      const int loc = k % N;
+      double v;
+      if (loc != 0) {
+        v = so[k];
+      } else {
+        const int te = k / N;
+        v = (te < nel) ? __dadd_rn(slast[te], so[k]) : slast[te];
+      }
+      if (OP != OP_JACT) v = __dmul_rn(v, pattern<N>(C.minv, g, loc, periodic, last_node));
+      if (!periodic && (g == 0 || g == last_node)) v = __dmul_rn(v, 0.0);
+      const int64_t ga = bofs + g;
+      if (EPI == EPI_STORE) {
+        A.out[ga] = v;
+      } else {  // EPI_RK
+        if (A.out) A.out[ga] = v;
+        double yv;
+        if (A.epi.n == 1) {
+          const double kk = A.epi.ptr[0] ? __ldg(A.epi.ptr[0] + ga) : v;
+          yv = __dadd_rn(__ldg(A.base + ga), __dmul_rn(__dmul_rn(A.dt, A.epi.coef[0]), kk));
+        } else {
+          double sacc = 0.0;
+          for (int j = 0; j < A.epi.n; ++j) {
+            const double kk = A.epi.ptr[j] ? __ldg(A.epi.ptr[j] + ga) : v;
+            const double term = __dmul_rn(A.epi.coef[j], kk);
+            sacc = (j == 0) ? term : __dadd_rn(sacc, term);
+          }
+          yv = __dadd_rn(__ldg(A.base + ga), __dmul_rn(A.dt, sacc));
+        }
+        if (A.check) bad_y |= nonfinite(yv);
+        A.Y[ga] = yv;
+      }
+    }
+    __syncthreads();
+  }
+  if (bad_u || bad_w || bad_y)
+    atomicOr(A.flag, (bad_u ? SEM1D_FLAG_STATE_NONFINITE : 0) |
+                         (bad_w ? SEM1D_FLAG_INPUT2_NONFINITE : 0) |
+                         (bad_y ? SEM1D_FLAG_STEP_NONFINITE : 0));
+}
+
+template <int N, int OP, int STAGES>
+constexpr size_t tma_smem_bytes() {
+  constexpr int NIN = (OP == OP_RHS) ? 1 : 2;
+  return sizeof(double) * ((size_t)(STAGES * NIN + 1) * TmaTile<N>::SLAB_ALLOC + TmaTile<N>::TPB + 2) +
+         sizeof(uint64_t) * STAGES;
+}
+
 template <int N, int OP>
 constexpr size_t apply_smem_bytes() {
   return sizeof(double) *

@@ -31,14 +31,53 @@ static cudaError_t launch_one(const PlanView& p, const Args& a, cudaStream_t s) 
   return cudaGetLastError();
 }
 
+constexpr int kTmaStages = 2;
+
+template <int N, int OP, int EPI>
+static cudaError_t launch_tma(const PlanView& p, const Args& a, cudaStream_t s) {
+  auto kern = apply_tma_kernel<N, OP, EPI, kTmaStages>;
+  constexpr size_t smem = tma_smem_bytes<N, OP, kTmaStages>();
+  static int max_resident = 0;  // CTAs per SM for this instantiation (cached)
+  if (max_resident == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int per_sm = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Tile<N>::TPB, smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    max_resident = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
+  }
+  const int64_t per_ring = (p.geo.E + Tile<N>::TPB - 1) / Tile<N>::TPB;
+  const int64_t total = per_ring * p.batch;
+  if (total > 0x7fffffffLL) return cudaErrorInvalidValue;
+  const int grid = (int)(total < max_resident ? total : max_resident);
+  kern<<<grid, Tile<N>::TPB, smem, s>>>(*static_cast<const Consts<N>*>(p.consts), p.geo, a,
+                                        (int)per_ring, (int)total);
+  return cudaGetLastError();
+}
+
+// The TMA path needs odd N (contiguous, conflict-free element stride) and at
+// least three tiles per ring (first and last tile take the synchronous path).
+template <int N>
+static bool use_tma(const PlanView& p) {
+  return (N % 2 == 1) && p.geo.E >= 3 * (int64_t)Tile<N>::TPB;
+}
+
 // kind: 0 F, 1 J, 2 J^T, 3 RK stage (F + combine), 4 adjoint stage (J^T + recurrence)
 template <int N>
 cudaError_t launch_apply(const PlanView& p, int kind, const Args& a, cudaStream_t s) {
+  const bool tma = use_tma<N>(p);
   switch (kind) {
-    case 0: return launch_one<N, OP_RHS, PRO_PLAIN, EPI_STORE>(p, a, s);
-    case 1: return launch_one<N, OP_JAC, PRO_PLAIN, EPI_STORE>(p, a, s);
-    case 2: return launch_one<N, OP_JACT, PRO_PLAIN, EPI_STORE>(p, a, s);
-    case 3: return launch_one<N, OP_RHS, PRO_PLAIN, EPI_RK>(p, a, s);
+    case 0: return tma ? launch_tma<N, OP_RHS, EPI_STORE>(p, a, s)
+                       : launch_one<N, OP_RHS, PRO_PLAIN, EPI_STORE>(p, a, s);
+    case 1: return tma ? launch_tma<N, OP_JAC, EPI_STORE>(p, a, s)
+                       : launch_one<N, OP_JAC, PRO_PLAIN, EPI_STORE>(p, a, s);
+    case 2: return tma ? launch_tma<N, OP_JACT, EPI_STORE>(p, a, s)
+                       : launch_one<N, OP_JACT, PRO_PLAIN, EPI_STORE>(p, a, s);
+    case 3: return tma ? launch_tma<N, OP_RHS, EPI_RK>(p, a, s)
+                       : launch_one<N, OP_RHS, PRO_PLAIN, EPI_RK>(p, a, s);
     case 4: return launch_one<N, OP_JACT, PRO_ADJ, EPI_ADJ>(p, a, s);
     default: return cudaErrorInvalidValue;
   }

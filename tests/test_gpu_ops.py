@@ -50,6 +50,31 @@ def test_every_degree_vs_oracle(cuda, N, periodic):
     assert rel_err(op.apply_jacobian_transpose(u, w), ref.jact(u, w)) <= TOL
 
 
+@pytest.mark.parametrize("N", [1, 3, 5, 7, 9, 11, 15, 21, 31])
+@pytest.mark.parametrize("periodic", [True, False])
+def test_tma_pipeline_vs_oracle(cuda, N, periodic):
+    """Odd degrees with >= 3 tiles per ring take the persistent TMA-pipelined kernel;
+    ragged tails, batch > 1 and both boundary kinds."""
+    tpb = 256 if N <= 8 else 128
+    E = 7 * tpb + 37
+    B = 3
+    op = _op(-1.0, 1.0, E, N, periodic, 0.01, batch=B)
+    ref = R.BurgersOracle(R.Mesh1D(-1.0, 1.0, E, N, periodic), 0.01)
+    rng = np.random.default_rng(N)
+    U = rng.uniform(-1, 1, (B, ref.mesh.ndof))
+    V = rng.standard_normal((B, ref.mesh.ndof))
+    W = rng.standard_normal((B, ref.mesh.ndof))
+    F, JV, JT = op.apply_rhs(U), op.apply_jacobian(U, V), op.apply_jacobian_transpose(U, W)
+    for b in range(B):
+        assert rel_err(F[b], ref.rhs(U[b])) <= TOL
+        assert rel_err(JV[b], ref.jac(U[b], V[b])) <= TOL
+        assert rel_err(JT[b], ref.jact(U[b], W[b])) <= TOL
+    bad = U.copy()
+    bad[1, ref.mesh.ndof // 2] = np.nan
+    with pytest.raises(sb.NumericFailure):
+        op.apply_rhs(bad)
+
+
 @pytest.mark.parametrize("E", [1, 2, 3, 255, 256, 257, 512, 1000])
 def test_tile_edges(cuda, E):
     for periodic in (True, False):
@@ -134,7 +159,8 @@ def test_operator_properties(cuda):
             rhs = w @ op.apply_jacobian_transpose(u, z)
             assert abs(lhs - rhs) / (np.linalg.norm(w) * np.linalg.norm(z)) <= 1e-13
         Jd = op.densify(u)
-        assert rel_err(Jd.T @ z, op.apply_jacobian_transpose(u, z)) <= 1e-12
+        # J^T output is masked at Dirichlet ends (ops.py:257): compare on the mask
+        assert rel_err(mask * (Jd.T @ z), op.apply_jacobian_transpose(u, z)) <= 1e-12
 
 
 def test_device_tensors_in_device_tensors_out(cuda):
@@ -164,7 +190,8 @@ def test_cfg2_full_size_properties(cuda):
     # dot-product identity at full size
     lhs = float(torch.dot(jv, wd))
     rhs = float(torch.dot(vd, jtw))
-    assert abs(lhs - rhs) / (float(vd.norm()) * float(wd.norm())) <= 1e-12
+    # ||J|| ~ nu N^4 / h^2 ~ 1e13 here: normalise by the inner product itself
+    assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
     # oracle on windows of elements: element-local results away from the window edge
     N, E = c["N"], c["E"]
     fh, jh = f.cpu().numpy(), jtw.cpu().numpy()
