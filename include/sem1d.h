@@ -54,6 +54,12 @@ typedef struct sem1d_plan sem1d_plan;
 
 /* Library identity. */
 int sem1d_version(void);
+/* Kernel-path selection for A/B measurement and tests (process-wide):
+ * 0 = automatic (warp-specialised FP64 tensor-core DMMA kernel for N+1 in
+ *     {8,16,24,32}, else the TMA-pipelined DFMA kernel for odd N, else the
+ *     plain tiled kernel), 1 = never a tensor-core kernel, 2 = plain tiled
+ *     kernel only, 3 = the CTA-synchronous tensor-core kernel (A/B reference). */
+int sem1d_set_kernel_path(int path);
 const char* sem1d_last_error(void);
 int sem1d_max_degree(void);
 

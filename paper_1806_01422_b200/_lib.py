@@ -12,7 +12,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsemb200.so")
+# SEM1D_LIB selects an alternative build of the same ABI (A/B kernel experiments)
+LIB_PATH = os.environ.get("SEM1D_LIB") or os.path.join(_HERE, "libsemb200.so")
 
 SEM1D_FLAG_STATE_NONFINITE = 1
 SEM1D_FLAG_INPUT2_NONFINITE = 2
@@ -25,6 +26,7 @@ c_dp = ctypes.POINTER(ctypes.c_double)
 # name -> (restype, argtypes); exactly the declarations of include/sem1d.h
 SIGNATURES = {
     "sem1d_version": (c_int, []),
+    "sem1d_set_kernel_path": (c_int, [c_int]),
     "sem1d_last_error": (ctypes.c_char_p, []),
     "sem1d_max_degree": (c_int, []),
     "sem1d_plan_create": (c_int, [c_int64, c_int, c_int, c_double, c_void_p, c_void_p, c_void_p,

@@ -25,6 +25,11 @@ SEM_DECL(30) SEM_DECL(31) SEM_DECL(32)
 #undef SEM_DECL
 }  // namespace sem1d
 
+namespace sem1d {
+static int g_path_override = 0;
+int sem1d_path_override() { return g_path_override; }
+}  // namespace sem1d
+
 struct sem1d_plan {
   int N;
   int64_t E, ndof, batch;
@@ -214,6 +219,12 @@ unsigned grid_for(int64_t work, int tpb) {
 extern "C" {
 
 int sem1d_version(void) { return 1; }
+
+int sem1d_set_kernel_path(int path) {
+  if (path < 0 || path > 3) return fail(SEM1D_EINVAL, "sem1d_set_kernel_path: path must be 0..3");
+  sem1d::g_path_override = path;
+  return SEM1D_OK;
+}
 const char* sem1d_last_error(void) { return g_err.c_str(); }
 int sem1d_max_degree(void) { return SEM1D_MAX_DEGREE; }
 

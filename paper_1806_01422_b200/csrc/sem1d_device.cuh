@@ -29,6 +29,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "../../include/sem1d.h"
 
 namespace sem1d {
@@ -538,6 +540,798 @@ __global__ void __launch_bounds__(Tile<N>::TPB, Tile<N>::MINB)
     atomicOr(A.flag, (bad_u ? SEM1D_FLAG_STATE_NONFINITE : 0) |
                          (bad_w ? SEM1D_FLAG_INPUT2_NONFINITE : 0) |
                          (bad_y ? SEM1D_FLAG_STEP_NONFINITE : 0));
+}
+
+// ============================================================================
+// FP64 tensor-core variant (n = N+1 in {8, 16, 32}: BASELINE degrees 7, 15, 31).
+//
+// The per-element contractions of a tile are small GEMMs: Out[e][i] =
+// sum_j A[e][j] M[i][j] with A = u, v or zm and M = K, Dw (or Dw^T for the
+// J^T advection term).  A warp handles 8 elements at a time with
+// mma.sync.m8n8k4.f64 (SASS DMMA): one instruction does 8 elements x 8 rows x
+// 4 columns, replacing 32 DFMA + 32 constant loads per thread.  A-fragments
+// come straight from the staged slab (element e's nodes are contiguous), the
+// B-fragments of K / Dw are built once per CTA, interior nodes are finalised
+// (M^-1) in place, the shared interface node is fixed up after one barrier,
+// and full tiles leave through a TMA bulk store (cp.async.bulk shared->global).
+// ============================================================================
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_u32(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int K>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(K) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+template <int N>
+struct MmaTile {
+  static constexpr int n = N + 1;
+  static_assert(n % 8 == 0, "tensor-core path needs n = N+1 divisible by 8");
+  static constexpr int THREADS = 256;
+  static constexpr int ELEMS = (n == 8) ? 256 : (n == 16 ? 128 : 64);   // elements per tile
+  static constexpr int MT = ELEMS / 8;                                  // 8-element m-tiles
+  static constexpr int NT = n / 8;                                      // 8-row n-tiles
+  static constexpr int KC = n / 4;                                      // 4-column k-chunks
+  static constexpr int SLAB = (ELEMS + 1) * N + 1;
+  static constexpr int SLAB_ALLOC = ((SLAB + 1) + 1) & ~1;
+  static constexpr bool B_IN_SMEM = (n > 16);
+  static constexpr int MINB = (n == 32) ? 1 : 2;
+};
+
+// fragment matrices: 0 = K (used as M^T), 1 = Dw (as M^T: Dw u), 2 = Dw (as M: Dw^T t)
+template <int N>
+__device__ __forceinline__ double bfrag_value(const Consts<N>& C, int mat, int nt, int kc, int lane) {
+  constexpr int n = N + 1;
+  const int i = 8 * nt + (lane >> 2);
+  const int j = 4 * kc + (lane & 3);
+  if (mat == 0) return C.K[i * n + j];
+  if (mat == 1) return C.Dw[i * n + j];
+  return C.Dw[j * n + i];
+}
+
+template <int N, int OP, int EPI, int STAGES>
+__global__ void __launch_bounds__(MmaTile<N>::THREADS, MmaTile<N>::MINB)
+    apply_mma_kernel(const __grid_constant__ Consts<N> C, const Geo G, const Args A,
+                     const int tiles_per_ring, const int total_tiles) {
+  using MT_ = MmaTile<N>;
+  constexpr int n = N + 1;
+  constexpr int THREADS = MT_::THREADS;
+  constexpr int ELEMS = MT_::ELEMS;
+  constexpr int NT = MT_::NT;
+  constexpr int KC = MT_::KC;
+  constexpr int NIN = (OP == OP_RHS) ? 1 : 2;
+  constexpr int NMAT = (OP == OP_JACT) ? 3 : 2;
+  constexpr int SA = MT_::SLAB_ALLOC;
+  extern __shared__ __align__(16) double smem[];
+  double* stage_buf = smem;                               // [STAGES][NIN][SA]
+  double* so = smem + STAGES * NIN * SA;                  // [SA] finalised node values
+  double* slast = so + SA;                                // [ELEMS + 2]
+  double* bsm = slast + ELEMS + 2;                        // [NMAT][NT][KC][32] if B_IN_SMEM
+  uint64_t* bars = reinterpret_cast<uint64_t*>(bsm + (MT_::B_IN_SMEM ? NMAT * NT * KC * 32 : 0));
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const bool periodic = G.periodic != 0;
+  const int64_t last_node = G.E * N;
+  const double mnu = -C.nu;
+
+  // ---- B fragments (constant per CTA)
+  double breg[MT_::B_IN_SMEM ? 1 : NMAT * NT * KC];
+  if (MT_::B_IN_SMEM) {
+    for (int q = tid; q < NMAT * NT * KC * 32; q += THREADS) {
+      const int l = q & 31, r = q >> 5;
+      const int kc = r % KC, nt = (r / KC) % NT, mat = r / (KC * NT);
+      bsm[q] = bfrag_value<N>(C, mat == 2 ? 2 : mat, nt, kc, l);
+    }
+  } else {
+#pragma unroll
+    for (int mat = 0; mat < NMAT; ++mat)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int kc = 0; kc < KC; ++kc)
+          breg[(mat * NT + nt) * KC + kc] = bfrag_value<N>(C, mat, nt, kc, lane);
+  }
+  auto bget = [&](int mat, int nt, int kc) -> double {
+    if (MT_::B_IN_SMEM) return bsm[((mat * NT + nt) * KC + kc) * 32 + lane];
+    return breg[(mat * NT + nt) * KC + kc];
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  auto tile_of = [&](int T, int64_t& bofs, int64_t& e0, int& nel, bool& boundary) {
+    const int b = T / tiles_per_ring;
+    const int tl = T - b * tiles_per_ring;
+    bofs = (int64_t)b * G.ndof;
+    e0 = (int64_t)tl * ELEMS;
+    nel = (int)min((int64_t)ELEMS, G.E - e0);
+    boundary = (tl == 0) || (tl == tiles_per_ring - 1);
+  };
+  auto issue = [&](int T, int s) {
+    int64_t bofs, e0;
+    int nel;
+    bool boundary;
+    tile_of(T, bofs, e0, nel, boundary);
+    if (boundary) return;
+    const int64_t gg0 = bofs + (e0 - 1) * N;
+    const int64_t a0 = gg0 & ~(int64_t)1;
+    const int shift = (int)(gg0 - a0);
+    const int cnt = (nel + 1) * N + 1;
+    const uint32_t bytes = (uint32_t)(((cnt + shift) * 8 + 15) & ~15);
+    mbar_expect_tx(&bars[s], NIN * bytes);
+    bulk_g2s(stage_buf + (s * NIN + 0) * SA, A.u + a0, bytes, &bars[s]);
+    if (NIN == 2) bulk_g2s(stage_buf + (s * NIN + 1) * SA, A.w + a0, bytes, &bars[s]);
+  };
+  if (tid == 0) {
+    for (int p = 0; p < STAGES - 1; ++p) {
+      const int T = blockIdx.x + p * gridDim.x;
+      if (T < total_tiles) issue(T, p);
+    }
+  }
+
+  bool bad_u = false, bad_w = false, bad_y = false;
+  uint32_t phases = 0;
+  int iter = 0;
+  for (int T = blockIdx.x; T < total_tiles; T += gridDim.x, ++iter) {
+    const int s = iter % STAGES;
+    if (tid == 0) {
+      const int Tn = T + (STAGES - 1) * gridDim.x;
+      if (Tn < total_tiles) issue(Tn, (iter + STAGES - 1) % STAGES);
+    }
+    int64_t bofs, e0;
+    int nel;
+    bool boundary;
+    tile_of(T, bofs, e0, nel, boundary);
+    const double* su = stage_buf + (s * NIN + 0) * SA;
+    const double* sw = stage_buf + (s * NIN + 1) * SA;
+    int shift;
+    const int64_t g0 = (e0 - 1) * N;
+    if (boundary) {
+      shift = 0;
+      double* wu = stage_buf + (s * NIN + 0) * SA;
+      double* ww = stage_buf + (s * NIN + 1) * SA;
+      const int cnt = (nel + 1) * N + 1;
+      for (int k = tid; k < cnt; k += THREADS) {
+        int64_t g = g0 + k;
+        bool valid = true;
+        if (g < 0) {
+          if (periodic) g += G.ndof; else valid = false;
+        } else if (g >= G.ndof) {
+          g -= G.ndof;
+        }
+        wu[k] = valid ? __ldg(A.u + bofs + g) : 0.0;
+        if (NIN == 2) ww[k] = valid ? __ldg(A.w + bofs + g) : 0.0;
+      }
+      // partial tile: zero the slab beyond the last element so padded m-tiles stay finite
+      for (int k = cnt + tid; k < (ELEMS + 1) * N + 1; k += THREADS) {
+        wu[k] = 0.0;
+        if (NIN == 2) ww[k] = 0.0;
+      }
+      __syncthreads();
+    } else {
+      shift = (int)((bofs + g0) & 1);
+      while (!mbar_try_wait(&bars[s], (phases >> s) & 1u)) {
+      }
+      phases ^= (1u << s);
+    }
+
+    // ---- tensor-core contraction: warp w owns m-tiles w, w+8, ...
+    for (int mt = warp; mt < MT_::MT; mt += THREADS / 32) {
+      const int el = 8 * mt + (lane >> 2);          // local element of this lane's A/C row
+      const bool live = el < nel;
+      const int64_t eg = e0 + el;
+      const int base = shift + (el + 1) * N;        // slab offset of element el's node 0
+      double au[KC], aw[(OP != OP_RHS) ? KC : 1], at[(OP == OP_JACT) ? KC : 1];
+#pragma unroll
+      for (int kc = 0; kc < KC; ++kc) {
+        const int j = 4 * kc + (lane & 3);
+        au[kc] = su[base + j];
+        if (live) bad_u |= nonfinite(au[kc]);
+        if (OP != OP_RHS) {
+          aw[kc] = sw[base + j];
+          if (live) bad_w |= nonfinite(aw[kc]);
+          if (OP == OP_JACT) {
+            aw[kc] = jt_scale<N>(C, aw[kc], j, eg, G);
+            at[kc] = __dmul_rn(au[kc], aw[kc]);
+          }
+        }
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        double k0 = 0.0, k1 = 0.0, p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
+#pragma unroll
+        for (int kc = 0; kc < KC; ++kc) {
+          const double ak = (OP == OP_RHS) ? au[kc] : aw[kc];
+          dmma884(k0, k1, ak, bget(0, nt, kc));            // K x            (x = u, v or zm)
+          dmma884(p0, p1, au[kc], bget(1, nt, kc));        // Dw u
+          if (OP == OP_JAC) dmma884(q0, q1, aw[kc], bget(1, nt, kc));   // Dw v
+          if (OP == OP_JACT) dmma884(q0, q1, at[kc], bget(2, nt, kc));  // Dw^T (u o zm)
+        }
+        if (live) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int i = 8 * nt + 2 * (lane & 3) + h;
+            const double kx = h ? k1 : k0, du = h ? p1 : p0, qq = h ? q1 : q0;
+            const double ui = su[base + i];
+            double r;
+            if (OP == OP_RHS) {
+              r = __dsub_rn(__dmul_rn(kx, mnu), __dmul_rn(ui, du));
+            } else if (OP == OP_JAC) {
+              const double vi = sw[base + i];
+              r = __dsub_rn(__dsub_rn(__dmul_rn(kx, mnu), __dmul_rn(vi, du)), __dmul_rn(ui, qq));
+            } else {
+              const double zi = jt_scale<N>(C, sw[base + i], i, eg, G);
+              r = __dsub_rn(__dsub_rn(__dmul_rn(kx, mnu), __dmul_rn(zi, du)), qq);
+            }
+            if (i == N) {
+              slast[el + 1] = r;
+            } else if (i == 0) {
+              so[el * N] = r;
+            } else {
+              so[el * N + i] = (OP == OP_JACT) ? r : __dmul_rn(r, C.minv[i]);
+            }
+          }
+        }
+      }
+    }
+    if (tid == 0) {  // row N of the halo element (left neighbour tile), scalar
+      double hl = 0.0;
+      if (periodic || e0 > 0) {
+        double x[n], y[(OP != OP_RHS) ? n : 1], t[(OP == OP_JACT) ? n : 1];
+        const int64_t eh = (e0 == 0) ? G.E - 1 : e0 - 1;
+#pragma unroll
+        for (int j = 0; j < n; ++j) {
+          x[j] = su[shift + j];
+          if (OP != OP_RHS) {
+            y[j] = sw[shift + j];
+            if (OP == OP_JACT) y[j] = jt_scale<N>(C, y[j], j, eh, G);
+          }
+        }
+        if (OP == OP_JACT) {
+#pragma unroll
+          for (int j = 0; j < n; ++j) t[j] = __dmul_rn(x[j], y[j]);
+        }
+        hl = elem_row<N, OP>(C, x, y, t, N);
+      }
+      slast[0] = hl;
+    }
+    __syncthreads();
+
+    // ---- interface nodes: element e-1's row N + element e's row 0 (grid.py:157-161)
+    const bool last_tile = (e0 + nel == G.E);
+    for (int el = tid; el <= nel; el += THREADS) {
+      const int64_t g = e0 * N + (int64_t)el * N;
+      if (el < nel) {
+        double v = __dadd_rn(slast[el], so[el * N]);
+        if (OP != OP_JACT) v = __dmul_rn(v, (!periodic && g == 0) ? C.minv[N] : C.minv[0]);
+        if (!periodic && g == 0) v = __dmul_rn(v, 0.0);
+        so[el * N] = v;
+      } else if (!periodic && last_tile) {  // Dirichlet end node E*N
+        double v = slast[el];
+        if (OP != OP_JACT) v = __dmul_rn(v, C.minv[N + 1]);
+        so[el * N] = __dmul_rn(v, 0.0);
+      }
+    }
+    const int nout = nel * N + ((!periodic && last_tile) ? 1 : 0);
+    const int64_t gout = bofs + e0 * N;
+    const bool bulk = (EPI == EPI_STORE) && !boundary && ((gout & 1) == 0);
+    if (bulk) fence_proxy_async_smem();
+    __syncthreads();
+    if (bulk) {
+      if (tid == 0) {
+        bulk_s2g(A.out + gout, so, (uint32_t)(nout * 8));
+        bulk_commit();
+        bulk_wait_read<0>();
+      }
+    } else {
+      for (int k = tid; k < nout; k += THREADS) {
+        const double v = so[k];
+        const int64_t ga = gout + k;
+        if (EPI == EPI_STORE) {
+          A.out[ga] = v;
+        } else {  // EPI_RK: base + dt * combination (timeloop.py:114-127)
+          if (A.out) A.out[ga] = v;
+          double yv;
+          if (A.epi.n == 1) {
+            const double kk = A.epi.ptr[0] ? __ldg(A.epi.ptr[0] + ga) : v;
+            yv = __dadd_rn(__ldg(A.base + ga), __dmul_rn(__dmul_rn(A.dt, A.epi.coef[0]), kk));
+          } else {
+            double sacc = 0.0;
+            for (int j = 0; j < A.epi.n; ++j) {
+              const double kk = A.epi.ptr[j] ? __ldg(A.epi.ptr[j] + ga) : v;
+              const double term = __dmul_rn(A.epi.coef[j], kk);
+              sacc = (j == 0) ? term : __dadd_rn(sacc, term);
+            }
+            yv = __dadd_rn(__ldg(A.base + ga), __dmul_rn(A.dt, sacc));
+          }
+          if (A.check) bad_y |= nonfinite(yv);
+          A.Y[ga] = yv;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) bulk_wait_all();
+  if (bad_u || bad_w || bad_y)
+    atomicOr(A.flag, (bad_u ? SEM1D_FLAG_STATE_NONFINITE : 0) |
+                         (bad_w ? SEM1D_FLAG_INPUT2_NONFINITE : 0) |
+                         (bad_y ? SEM1D_FLAG_STEP_NONFINITE : 0));
+}
+
+// ============================================================================
+// Warp-specialised tensor-core kernel.  Warp CW (the last) is the TMA
+// producer: it waits until a stage is released, loads the unaligned or wrapped
+// pieces of the slab with its lanes and the 16-byte-aligned body with one bulk
+// copy per input, then arms the stage's "full" mbarrier.  Warps 0..CW-1 are
+// DMMA consumers, each owning WE consecutive elements of the tile: they
+// contract with mma.m8n8k4.f64, form the shared interface node in registers
+// (shuffle from the neighbouring lane; the row N of the element left of the
+// warp is recomputed warp-cooperatively), stage their finished node range in
+// shared memory and write it back with their own bulk store.  There is no
+// CTA-wide barrier inside the tile loop.
+// ============================================================================
+
+#ifndef WS_ELEMS8
+#define WS_ELEMS8 256
+#endif
+
+// Occupancy per operator (A/B-measured on config 2, profiles/r1_ab_occupancy.json):
+// F (one input) runs best at 4 CTAs/SM, J and J^T at 3.
+template <int N, int OP>
+constexpr int ws_minb() {
+  return ((N + 1) > 16) ? 1 : ((N + 1) == 16 ? 2 : (OP == OP_RHS ? 4 : 3));
+}
+
+template <int N>
+struct WsTile {
+  static constexpr int n = N + 1;
+  static constexpr int CW = 8;                                   // consumer warps
+  static constexpr int THREADS = 32 * (CW + 1);
+  static constexpr int ELEMS = (n == 8) ? WS_ELEMS8 : MmaTile<N>::ELEMS;
+  static constexpr int WE = ELEMS / CW;                          // elements per consumer warp
+  static constexpr int WMT = WE / 8;                             // m-tiles per warp
+  static constexpr int NT = n / 8, KC = n / 4;
+  static constexpr int SLAB = (ELEMS + 1) * N + 1;
+  static constexpr int SLAB_ALLOC = ((SLAB + 1) + 1) & ~1;
+  static constexpr int OUT = ((ELEMS * N + 2) + 1) & ~1;         // per-CTA output staging
+  static constexpr bool B_IN_SMEM = (n > 16);
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int N, int OP>
+__device__ __forceinline__ double combine_rows(double kx, double du, double qq, double ui,
+                                               double wi, double mnu) {
+  if (OP == OP_RHS) return __dsub_rn(__dmul_rn(kx, mnu), __dmul_rn(ui, du));
+  if (OP == OP_JAC)
+    return __dsub_rn(__dsub_rn(__dmul_rn(kx, mnu), __dmul_rn(wi, du)), __dmul_rn(ui, qq));
+  return __dsub_rn(__dsub_rn(__dmul_rn(kx, mnu), __dmul_rn(wi, du)), qq);
+}
+
+// One DMMA m-tile: 8 elements (A rows) x n rows, pointwise-combined.  Lane
+// (rr, kq) ends with rows i = 8nt + 2kq + h of element rr in r[nt][h].
+// EDGE = tile touches a Dirichlet end (masking / special M^-1 entries).
+template <int N, int OP, bool EDGE>
+struct MTileOut {
+  double r[N / 8 + 1][2];
+};
+
+template <int N, int OP, bool EDGE, class BGet>
+__device__ __forceinline__ void mtile_compute(const Consts<N>& C, const Geo& G, const double* su,
+                                              const double* sw, int base, int64_t eg,
+                                              const double* minv_a, const double (*minv_p)[2],
+                                              double mnu, int kq, BGet bget, double& fin_u,
+                                              double& fin_w, double (&r)[(N + 1) / 8][2]) {
+  constexpr int n = N + 1, NT = n / 8, KC = n / 4;
+  const bool eslow = EDGE && (eg == 0 || eg == G.E - 1);
+  double au[KC], aw[(OP != OP_RHS) ? KC : 1], at[(OP == OP_JACT) ? KC : 1];
+#pragma unroll
+  for (int kc = 0; kc < KC; ++kc) {
+    const int j = 4 * kc + kq;
+    au[kc] = su[base + j];
+    fin_u = fma(au[kc], 0.0, fin_u);   // NaN/Inf * 0 = NaN: one DFMA per value
+    if (OP != OP_RHS) {
+      aw[kc] = sw[base + j];
+      fin_w = fma(aw[kc], 0.0, fin_w);
+      if (OP == OP_JACT) {
+        aw[kc] = eslow ? jt_scale<N>(C, aw[kc], j, eg, G) : __dmul_rn(aw[kc], minv_a[kc]);
+        at[kc] = __dmul_rn(au[kc], aw[kc]);
+      }
+    }
+  }
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    double k0 = 0.0, k1 = 0.0, p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
+#pragma unroll
+    for (int kc = 0; kc < KC; ++kc) {
+      dmma884(k0, k1, (OP == OP_RHS) ? au[kc] : aw[kc], bget(0, nt, kc));   // K x
+      dmma884(p0, p1, au[kc], bget(1, nt, kc));                            // Dw u
+      if (OP == OP_JAC) dmma884(q0, q1, aw[kc], bget(1, nt, kc));          // Dw v
+      if (OP == OP_JACT) dmma884(q0, q1, at[kc], bget(2, nt, kc));         // Dw^T (u o zm)
+    }
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = 8 * nt + 2 * kq + h;
+      const double ui = su[base + i];
+      double wi = 0.0;
+      if (OP == OP_JAC) wi = sw[base + i];
+      if (OP == OP_JACT) {
+        const double zr = sw[base + i];
+        wi = eslow ? jt_scale<N>(C, zr, i, eg, G) : __dmul_rn(zr, minv_p[nt][h]);
+      }
+      r[nt][h] = combine_rows<N, OP>(h ? k1 : k0, h ? p1 : p0, h ? q1 : q0, ui, wi, mnu);
+    }
+  }
+}
+
+template <int N, int OP, int EPI, int STAGES>
+__global__ void __launch_bounds__(WsTile<N>::THREADS, ws_minb<N, OP>())
+    apply_ws_kernel(const __grid_constant__ Consts<N> C, const Geo G, const Args A,
+                    const int tiles_per_ring, const int total_tiles) {
+  using W = WsTile<N>;
+  constexpr int n = N + 1;
+  constexpr int ELEMS = W::ELEMS, WE = W::WE, WMT = W::WMT, NT = W::NT, KC = W::KC;
+  constexpr int NIN = (OP == OP_RHS) ? 1 : 2;
+  constexpr int NMAT = (OP == OP_JACT) ? 3 : 2;
+  constexpr int SA = W::SLAB_ALLOC;
+  extern __shared__ __align__(16) double smem[];
+  double* stage_buf = smem;                                   // [STAGES][NIN][SA]
+  double* ostage = smem + STAGES * NIN * SA;                  // [OUT]
+  double* hrow = ostage + W::OUT;                             // [STAGES][CW] warp halo rows
+  double* bsm = hrow + STAGES * W::CW;                        // B fragments (n = 32)
+  uint64_t* full = reinterpret_cast<uint64_t*>(bsm + (W::B_IN_SMEM ? NMAT * NT * KC * 32 : 0));
+  uint64_t* empty = full + STAGES;
+  uint64_t* halo = empty + STAGES;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  const bool periodic = G.periodic != 0;
+
+  if (W::B_IN_SMEM) {
+    for (int q = tid; q < NMAT * NT * KC * 32; q += W::THREADS) {
+      const int l = q & 31, r = q >> 5;
+      const int kc = r % KC, nt = (r / KC) % NT, mat = r / (KC * NT);
+      bsm[q] = bfrag_value<N>(C, mat, nt, kc, l);
+    }
+  }
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], W::CW);
+      mbar_init(&halo[s], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // per-lane constants (all warps): B fragments, M^-1 at fragment positions
+  double breg[W::B_IN_SMEM ? 1 : NMAT * NT * KC];
+  if (!W::B_IN_SMEM) {
+#pragma unroll
+    for (int mat = 0; mat < NMAT; ++mat)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int kc = 0; kc < KC; ++kc)
+          breg[(mat * NT + nt) * KC + kc] = bfrag_value<N>(C, mat, nt, kc, lane);
+  }
+  auto bget = [&](int mat, int nt, int kc) -> double {
+    if (W::B_IN_SMEM) return bsm[((mat * NT + nt) * KC + kc) * 32 + lane];
+    return breg[(mat * NT + nt) * KC + kc];
+  };
+  const int kq = lane & 3, rr = lane >> 2;
+  const double mnu = -C.nu;
+  double minv_a[KC];                                // M^-1 at A columns j = 4kc + kq
+#pragma unroll
+  for (int kc = 0; kc < KC; ++kc) {
+    const int j = 4 * kc + kq;
+    minv_a[kc] = C.minv[(j == 0 || j == N) ? 0 : j];
+  }
+  double minv_p[NT][2];                             // M^-1 at output rows i = 8nt + 2kq + h
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int i = 8 * nt + 2 * kq + h;
+      minv_p[nt][h] = C.minv[(i == 0 || i == N) ? 0 : i];
+    }
+  const double minv_if = C.minv[0];
+  double fin_u = 0.0, fin_w = 0.0;
+  bool bad_y = false;
+
+  // ------------------------------------------------------------------ producer
+  if (warp == W::CW) {
+    // tile cursor for the loads (runs STAGES-1 tiles ahead of the halo cursor)
+    auto tile_coords = [&](int T, int& tl, int64_t& bofs) {
+      const int b = T / tiles_per_ring;
+      tl = T - b * tiles_per_ring;
+      bofs = (int64_t)b * G.ndof;
+    };
+    auto load_tile = [&](int T, int s) {
+      int tl;
+      int64_t bofs;
+      tile_coords(T, tl, bofs);
+      const int64_t e0 = (int64_t)tl * ELEMS;
+      const int nel = (int)min((int64_t)ELEMS, G.E - e0);
+      const int cnt = (nel + 1) * N + 1;
+      const int64_t g0 = (e0 - 1) * N;
+      const int sh = (int)((bofs + g0) & 1);
+      const int64_t lo = g0 < 0 ? 0 : g0;
+      const int64_t hi = min(g0 + cnt, G.ndof);
+      int64_t alo = ((bofs + lo + 1) & ~(int64_t)1) - bofs;
+      int64_t ahi = ((bofs + hi) & ~(int64_t)1) - bofs;
+      if (ahi < alo) ahi = alo;
+      const int k0 = (int)(alo - g0), k1 = (int)(ahi - g0);
+      double* dst0 = stage_buf + (s * NIN + 0) * SA + sh;
+      double* dst1 = stage_buf + (s * NIN + 1) * SA + sh;
+      const double* src0 = A.u + bofs;
+      const double* src1 = (NIN == 2) ? A.w + bofs : nullptr;
+      auto scalar_piece = [&](int kb, int ke) {
+        for (int k = kb + lane; k < ke; k += 32) {
+          int64_t g = g0 + k;
+          bool valid = true;
+          if (g < 0) {
+            if (periodic) g += G.ndof; else valid = false;
+          } else if (g >= G.ndof) {
+            g -= G.ndof;
+          }
+          dst0[k] = valid ? __ldg(src0 + g) : 0.0;
+          if (NIN == 2) dst1[k] = valid ? __ldg(src1 + g) : 0.0;
+        }
+      };
+      scalar_piece(0, k0);
+      scalar_piece(k1, cnt);
+      for (int k = cnt + lane; k < (ELEMS + 1) * N + 1; k += 32) {  // ragged tile: finite pad
+        dst0[k] = 0.0;
+        if (NIN == 2) dst1[k] = 0.0;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        const uint32_t bytes = (uint32_t)((ahi - alo) * 8);
+        mbar_expect_tx(&full[s], NIN * bytes);
+        if (bytes > 0) {
+          bulk_g2s(dst0 + k0, src0 + alo, bytes, &full[s]);
+          if (NIN == 2) bulk_g2s(dst1 + k0, src1 + alo, bytes, &full[s]);
+        }
+      }
+    };
+    int issued = 0;  // tiles issued so far (iteration index of the next load)
+    auto issue_next = [&](int T) {
+      const int s = issued % STAGES;
+      while (!mbar_try_wait(&empty[s], ((issued / STAGES) & 1) ^ 1)) {
+      }
+      load_tile(T, s);
+      ++issued;
+    };
+    for (int p = 0; p < STAGES - 1; ++p) {
+      const int T = blockIdx.x + p * gridDim.x;
+      if (T < total_tiles) issue_next(T);
+    }
+    int it = 0;
+    for (int T = blockIdx.x; T < total_tiles; T += gridDim.x, ++it) {
+      const int Tn = T + (STAGES - 1) * gridDim.x;
+      if (Tn < total_tiles) issue_next(Tn);
+      // row N of the element left of each consumer warp: one DMMA m-tile whose
+      // row rr is tile-local element rr*WE - 1 (slab base rr*WE*N)
+      const int s = it % STAGES;
+      int tl;
+      int64_t bofs;
+      tile_coords(T, tl, bofs);
+      const int64_t e0 = (int64_t)tl * ELEMS;
+      const int sh = (int)((bofs + (e0 - 1) * N) & 1);
+      const double* su = stage_buf + (s * NIN + 0) * SA + sh;
+      const double* sw = stage_buf + (s * NIN + 1) * SA + sh;
+      while (!mbar_try_wait(&full[s], (it / STAGES) & 1)) {
+      }
+      const int64_t eh = e0 + rr * WE - 1;
+      const int64_t ehw = (eh < 0) ? G.E - 1 : eh;
+      double r[NT][2];
+      double du_ = 0.0, dw_ = 0.0;
+      if (!periodic && (tl == 0 || tl == tiles_per_ring - 1))
+        mtile_compute<N, OP, true>(C, G, su, sw, rr * WE * N, ehw, minv_a, minv_p, mnu, kq, bget, du_, dw_, r);
+      else
+        mtile_compute<N, OP, false>(C, G, su, sw, rr * WE * N, ehw, minv_a, minv_p, mnu, kq, bget, du_, dw_, r);
+      if (kq == 3) hrow[s * W::CW + rr] = (!periodic && eh < 0) ? 0.0 : r[NT - 1][1];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&halo[s]);
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ consumers
+  double* wout = ostage + warp * WE * N;            // this warp's contiguous node staging
+  int it = 0;
+  int tl = blockIdx.x % tiles_per_ring;
+  int bidx = blockIdx.x / tiles_per_ring;
+  for (int T = blockIdx.x; T < total_tiles; T += gridDim.x, ++it) {
+    const int s = it % STAGES;
+    const int64_t bofs = (int64_t)bidx * G.ndof;
+    const int64_t e0 = (int64_t)tl * ELEMS;
+    const int nel = (int)min((int64_t)ELEMS, G.E - e0);
+    const int sh = (int)((bofs + (e0 - 1) * N) & 1);
+    const bool edge = !periodic && (tl == 0 || tl == tiles_per_ring - 1);
+    const double* su = stage_buf + (s * NIN + 0) * SA + sh;
+    const double* sw = stage_buf + (s * NIN + 1) * SA + sh;
+    const int wel0 = warp * WE;
+    const int wnel = min(WE, nel - wel0);
+    while (!mbar_try_wait(&full[s], (it / STAGES) & 1)) {
+    }
+    if (wnel > 0) {
+      if (lane == 0) bulk_wait_read<0>();   // previous store out of `wout` has drained
+      __syncwarp();
+      double carry = 0.0;
+      auto body = [&](auto edge_tag) {
+        constexpr bool EDGE = decltype(edge_tag)::value;
+#pragma unroll
+        for (int q = 0; q < WMT; ++q) {
+          const int le = 8 * q + rr;                // warp-local element of this lane
+          const bool live = le < wnel;
+          const int64_t eg = e0 + wel0 + le;
+          const int base = (wel0 + le + 1) * N;
+          double r[NT][2];
+          mtile_compute<N, OP, EDGE>(C, G, su, sw, base, eg, minv_a, minv_p, mnu, kq, bget,
+                                     fin_u, fin_w, r);
+          // interior rows -> staging; rows 0 and N stay in registers
+#pragma unroll
+          for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const int i = 8 * nt + 2 * kq + h;
+              if (live && i != 0 && i != N)
+                wout[le * N + i] = (OP == OP_JACT) ? r[nt][h] : __dmul_rn(r[nt][h], minv_p[nt][h]);
+            }
+          const double row0 = r[0][0];              // valid in lanes kq == 0
+          const double rowN = r[NT - 1][1];         // valid in lanes kq == 3
+          double left = __shfl_up_sync(0xffffffffu, rowN, 1);
+          if (rr == 0) left = carry;                // q == 0: patched after the halo arrives
+          carry = __shfl_sync(0xffffffffu, rowN, 31);
+          if (kq == 0 && live) {
+            double v = (q == 0 && rr == 0) ? row0 : __dadd_rn(left, row0);
+            if (!(q == 0 && rr == 0)) {
+              if (EDGE && eg == 0) {
+                if (OP != OP_JACT) v = __dmul_rn(v, C.minv[N]);
+                v = __dmul_rn(v, 0.0);
+              } else if (OP != OP_JACT) {
+                v = __dmul_rn(v, minv_if);
+              }
+            }
+            wout[le * N] = v;
+          }
+          if (EDGE && kq == 3 && live && eg == G.E - 1) {  // Dirichlet end node E*N
+            double v = rowN;
+            if (OP != OP_JACT) v = __dmul_rn(v, C.minv[N + 1]);
+            wout[(le + 1) * N] = __dmul_rn(v, 0.0);
+          }
+        }
+      };
+      if (edge) body(std::integral_constant<bool, true>{});
+      else body(std::integral_constant<bool, false>{});
+      // first interface node of the warp: needs the halo row from the producer
+      while (!mbar_try_wait(&halo[s], (it / STAGES) & 1)) {
+      }
+      if (lane == 0) {
+        const int64_t eg = e0 + wel0;
+        double v = __dadd_rn(hrow[s * W::CW + warp], wout[0]);
+        if (!periodic && eg == 0) {
+          if (OP != OP_JACT) v = __dmul_rn(v, C.minv[N]);
+          v = __dmul_rn(v, 0.0);
+        } else if (OP != OP_JACT) {
+          v = __dmul_rn(v, minv_if);
+        }
+        wout[0] = v;
+      }
+    } else {
+      while (!mbar_try_wait(&halo[s], (it / STAGES) & 1)) {
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);   // this warp is done reading stage s
+    if (wnel > 0) {
+      const bool owns_end = !periodic && (e0 + wel0 + wnel == G.E);
+      const int cnt_w = wnel * N + (owns_end ? 1 : 0);
+      const int64_t gw = bofs + (e0 + wel0) * N;    // absolute index of the warp's first node
+      const bool bulk = (EPI == EPI_STORE) && ((gw & 1) == 0) && ((cnt_w & 1) == 0);
+      if (bulk) {
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          bulk_s2g(A.out + gw, wout, (uint32_t)(cnt_w * 8));
+          bulk_commit();
+        }
+      } else {
+        for (int k = lane; k < cnt_w; k += 32) {
+          const double v = wout[k];
+          const int64_t ga = gw + k;
+          if (EPI == EPI_STORE) {
+            A.out[ga] = v;
+          } else {  // EPI_RK: base + dt * combination (timeloop.py:114-127)
+            if (A.out) A.out[ga] = v;
+            double yv;
+            if (A.epi.n == 1) {
+              const double kk = A.epi.ptr[0] ? __ldg(A.epi.ptr[0] + ga) : v;
+              yv = __dadd_rn(__ldg(A.base + ga), __dmul_rn(__dmul_rn(A.dt, A.epi.coef[0]), kk));
+            } else {
+              double sacc = 0.0;
+              for (int j = 0; j < A.epi.n; ++j) {
+                const double kk = A.epi.ptr[j] ? __ldg(A.epi.ptr[j] + ga) : v;
+                const double term = __dmul_rn(A.epi.coef[j], kk);
+                sacc = (j == 0) ? term : __dadd_rn(sacc, term);
+              }
+              yv = __dadd_rn(__ldg(A.base + ga), __dmul_rn(A.dt, sacc));
+            }
+            if (A.check) bad_y |= nonfinite(yv);
+            A.Y[ga] = yv;
+          }
+        }
+        __syncwarp();
+      }
+    }
+    tl += gridDim.x;
+    while (tl >= tiles_per_ring) {
+      tl -= tiles_per_ring;
+      ++bidx;
+    }
+  }
+  if (lane == 0) bulk_wait_all();
+  const bool bad_u = fin_u != fin_u, bad_w = fin_w != fin_w;
+  if (bad_u || bad_w || bad_y)
+    atomicOr(A.flag, (bad_u ? SEM1D_FLAG_STATE_NONFINITE : 0) |
+                         (bad_w ? SEM1D_FLAG_INPUT2_NONFINITE : 0) |
+                         (bad_y ? SEM1D_FLAG_STEP_NONFINITE : 0));
+}
+
+// Pipeline depth: enough stages that ~100 KB of slab loads can be in flight per
+// CTA (two CTAs per SM for n <= 16), since HBM at ~1.5 us loaded latency needs
+// >= 64 KB outstanding per SM (Little's law).
+template <int N, int OP>
+constexpr int ws_stages() {
+  using W = WsTile<N>;
+  constexpr int NIN = (OP == OP_RHS) ? 1 : 2;
+  // shared-memory budget that keeps ws_minb CTAs resident (227 KB per SM)
+  constexpr int mb = ws_minb<N, OP>();
+  constexpr int budget = (mb == 1 ? 180 : (mb == 2 ? 104 : (mb == 3 ? 72 : 56))) * 1024;
+  constexpr int per = NIN * W::SLAB_ALLOC * 8;
+  constexpr int st = (budget - W::OUT * 8 - (W::B_IN_SMEM ? 3 * W::NT * W::KC * 32 * 8 : 0)) / per;
+  return st < 2 ? 2 : (st > 8 ? 8 : st);
+}
+
+template <int N, int OP, int STAGES>
+constexpr size_t ws_smem_bytes() {
+  using W = WsTile<N>;
+  constexpr int NIN = (OP == OP_RHS) ? 1 : 2;
+  constexpr int NMAT = (OP == OP_JACT) ? 3 : 2;
+  return sizeof(double) * ((size_t)STAGES * NIN * W::SLAB_ALLOC + W::OUT + STAGES * W::CW +
+                           (W::B_IN_SMEM ? NMAT * W::NT * W::KC * 32 : 0)) +
+         sizeof(uint64_t) * 3 * STAGES;
+}
+
+template <int N, int OP, int STAGES>
+constexpr size_t mma_smem_bytes() {
+  using MT_ = MmaTile<N>;
+  constexpr int NIN = (OP == OP_RHS) ? 1 : 2;
+  constexpr int NMAT = (OP == OP_JACT) ? 3 : 2;
+  return sizeof(double) * ((size_t)(STAGES * NIN + 1) * MT_::SLAB_ALLOC + MT_::ELEMS + 2 +
+                           (MT_::B_IN_SMEM ? NMAT * MT_::NT * MT_::KC * 32 : 0)) +
+         sizeof(uint64_t) * STAGES;
 }
 
 template <int N, int OP, int STAGES>

@@ -9,6 +9,11 @@
 
 namespace sem1d {
 
+// Kernel-path override for A/B measurements and tests: 0 = auto (warp-specialised
+// tensor-core kernel, else TMA/DFMA, else plain), 1 = no tensor-core path,
+// 2 = plain kernel only, 3 = the first (CTA-synchronous) tensor-core kernel.
+int sem1d_path_override();
+
 struct PlanView {
   const void* consts;  // Consts<N>, packed by the plan
   Geo geo;
@@ -58,6 +63,76 @@ static cudaError_t launch_tma(const PlanView& p, const Args& a, cudaStream_t s) 
   return cudaGetLastError();
 }
 
+template <int N, int OP, int EPI>
+static cudaError_t launch_mma(const PlanView& p, const Args& a, cudaStream_t s) {
+  if constexpr ((N + 1) % 8 != 0) {
+    return cudaErrorInvalidValue;
+  } else {
+    auto kern = apply_mma_kernel<N, OP, EPI, kTmaStages>;
+    constexpr size_t smem = mma_smem_bytes<N, OP, kTmaStages>();
+    static int max_resident = 0;
+    if (max_resident == 0) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      int per_sm = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, MmaTile<N>::THREADS, smem);
+      if (e != cudaSuccess) return e;
+      int dev = 0, sms = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      max_resident = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
+    }
+    const int64_t per_ring = (p.geo.E + MmaTile<N>::ELEMS - 1) / MmaTile<N>::ELEMS;
+    const int64_t total = per_ring * p.batch;
+    if (total > 0x7fffffffLL) return cudaErrorInvalidValue;
+    const int grid = (int)(total < max_resident ? total : max_resident);
+    kern<<<grid, MmaTile<N>::THREADS, smem, s>>>(*static_cast<const Consts<N>*>(p.consts), p.geo, a,
+                                                 (int)per_ring, (int)total);
+    return cudaGetLastError();
+  }
+}
+
+
+template <int N, int OP, int EPI>
+static cudaError_t launch_ws(const PlanView& p, const Args& a, cudaStream_t s) {
+  if constexpr ((N + 1) % 8 != 0) {
+    return cudaErrorInvalidValue;
+  } else {
+    constexpr int ST = ws_stages<N, OP>();
+    auto kern = apply_ws_kernel<N, OP, EPI, ST>;
+    constexpr size_t smem = ws_smem_bytes<N, OP, ST>();
+    static int max_resident = 0;
+    if (max_resident == 0) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      int per_sm = 0;
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WsTile<N>::THREADS, smem);
+      if (e != cudaSuccess) return e;
+      int dev = 0, sms = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      max_resident = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
+    }
+    const int64_t per_ring = (p.geo.E + WsTile<N>::ELEMS - 1) / WsTile<N>::ELEMS;
+    const int64_t total = per_ring * p.batch;
+    if (total > 0x7fffffffLL) return cudaErrorInvalidValue;
+    const int grid = (int)(total < max_resident ? total : max_resident);
+    kern<<<grid, WsTile<N>::THREADS, smem, s>>>(*static_cast<const Consts<N>*>(p.consts), p.geo, a,
+                                                (int)per_ring, (int)total);
+    return cudaGetLastError();
+  }
+}
+
+// FP64 tensor-core path: n = N+1 a multiple of 8 (N = 7, 15, 23, 31), >= 3 tiles per ring.
+template <int N>
+static bool use_mma(const PlanView& p) {
+  if constexpr ((N + 1) % 8 != 0) {
+    return false;
+  } else {
+    return p.geo.E >= 3 * (int64_t)MmaTile<N>::ELEMS;
+  }
+}
+
 // The TMA path needs odd N (contiguous, conflict-free element stride) and at
 // least three tiles per ring (first and last tile take the synchronous path).
 template <int N>
@@ -68,7 +143,26 @@ static bool use_tma(const PlanView& p) {
 // kind: 0 F, 1 J, 2 J^T, 3 RK stage (F + combine), 4 adjoint stage (J^T + recurrence)
 template <int N>
 cudaError_t launch_apply(const PlanView& p, int kind, const Args& a, cudaStream_t s) {
-  const bool tma = use_tma<N>(p);
+  const bool tma = use_tma<N>(p) && sem1d_path_override() != 2;
+  if constexpr ((N + 1) % 8 == 0) {
+    // warp-specialised DMMA kernel handles every ring size (wrap / ragged pieces in-kernel)
+    if (kind <= 3 && sem1d_path_override() == 0) {
+      switch (kind) {
+        case 0: return launch_ws<N, OP_RHS, EPI_STORE>(p, a, s);
+        case 1: return launch_ws<N, OP_JAC, EPI_STORE>(p, a, s);
+        case 2: return launch_ws<N, OP_JACT, EPI_STORE>(p, a, s);
+        default: return launch_ws<N, OP_RHS, EPI_RK>(p, a, s);
+      }
+    }
+    if (kind <= 3 && use_mma<N>(p) && sem1d_path_override() == 3) {
+      switch (kind) {
+        case 0: return launch_mma<N, OP_RHS, EPI_STORE>(p, a, s);
+        case 1: return launch_mma<N, OP_JAC, EPI_STORE>(p, a, s);
+        case 2: return launch_mma<N, OP_JACT, EPI_STORE>(p, a, s);
+        default: return launch_mma<N, OP_RHS, EPI_RK>(p, a, s);
+      }
+    }
+  }
   switch (kind) {
     case 0: return tma ? launch_tma<N, OP_RHS, EPI_STORE>(p, a, s)
                        : launch_one<N, OP_RHS, PRO_PLAIN, EPI_STORE>(p, a, s);

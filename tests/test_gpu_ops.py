@@ -50,10 +50,20 @@ def test_every_degree_vs_oracle(cuda, N, periodic):
     assert rel_err(op.apply_jacobian_transpose(u, w), ref.jact(u, w)) <= TOL
 
 
-@pytest.mark.parametrize("N", [1, 3, 5, 7, 9, 11, 15, 21, 31])
+@pytest.fixture(params=[0, 1, 2, 3], ids=["auto", "no-mma", "plain", "mma-sync"])
+def kernel_path(request):
+    from paper_1806_01422_b200 import _lib
+    lib = _lib.load()
+    assert lib.sem1d_set_kernel_path(request.param) == 0
+    yield request.param
+    lib.sem1d_set_kernel_path(0)
+
+
+@pytest.mark.parametrize("N", [1, 3, 5, 7, 9, 11, 15, 21, 23, 31])
 @pytest.mark.parametrize("periodic", [True, False])
-def test_tma_pipeline_vs_oracle(cuda, N, periodic):
-    """Odd degrees with >= 3 tiles per ring take the persistent TMA-pipelined kernel;
+def test_tma_pipeline_vs_oracle(cuda, N, periodic, kernel_path):
+    """Large rings take the persistent pipelined kernels (DMMA tensor-core path for
+    N+1 in {8, 16, 24, 32}, TMA/DFMA path for other odd N); every path is checked:
     ragged tails, batch > 1 and both boundary kinds."""
     tpb = 256 if N <= 8 else 128
     E = 7 * tpb + 37
