@@ -1077,9 +1077,17 @@ __global__ void __launch_bounds__(WsTile<N>::THREADS, ws_minb<N, OP>())
       const int sh = (int)((bofs + g0) & 1);
       const int64_t lo = g0 < 0 ? 0 : g0;
       const int64_t hi = min(g0 + cnt, G.ndof);
-      int64_t alo = ((bofs + lo + 1) & ~(int64_t)1) - bofs;
-      int64_t ahi = ((bofs + hi) & ~(int64_t)1) - bofs;
-      if (ahi < alo) ahi = alo;
+      int64_t alo, ahi;
+      if (g0 >= 0 && g0 + cnt + 1 <= G.ndof) {
+        // interior tile: widen the body outward to 16-byte boundaries (the extra
+        // doubles lie inside this ring), so no lane has to load anything itself
+        alo = ((bofs + g0) & ~(int64_t)1) - bofs;
+        ahi = ((bofs + g0 + cnt + 1) & ~(int64_t)1) - bofs;
+      } else {
+        alo = ((bofs + lo + 1) & ~(int64_t)1) - bofs;
+        ahi = ((bofs + hi) & ~(int64_t)1) - bofs;
+        if (ahi < alo) ahi = alo;
+      }
       const int k0 = (int)(alo - g0), k1 = (int)(ahi - g0);
       double* dst0 = stage_buf + (s * NIN + 0) * SA + sh;
       double* dst1 = stage_buf + (s * NIN + 1) * SA + sh;
@@ -1098,8 +1106,8 @@ __global__ void __launch_bounds__(WsTile<N>::THREADS, ws_minb<N, OP>())
           if (NIN == 2) dst1[k] = valid ? __ldg(src1 + g) : 0.0;
         }
       };
-      scalar_piece(0, k0);
-      scalar_piece(k1, cnt);
+      if (k0 > 0) scalar_piece(0, k0);
+      if (k1 < cnt) scalar_piece(k1, cnt);
       for (int k = cnt + lane; k < (ELEMS + 1) * N + 1; k += 32) {  // ragged tile: finite pad
         dst0[k] = 0.0;
         if (NIN == 2) dst1[k] = 0.0;
@@ -1128,10 +1136,9 @@ __global__ void __launch_bounds__(WsTile<N>::THREADS, ws_minb<N, OP>())
     }
     int it = 0;
     for (int T = blockIdx.x; T < total_tiles; T += gridDim.x, ++it) {
-      const int Tn = T + (STAGES - 1) * gridDim.x;
-      if (Tn < total_tiles) issue_next(Tn);
       // row N of the element left of each consumer warp: one DMMA m-tile whose
-      // row rr is tile-local element rr*WE - 1 (slab base rr*WE*N)
+      // row rr is tile-local element rr*WE - 1 (slab base rr*WE*N).  Done before
+      // the next issue so the consumers' halo wait never sits behind a refill.
       const int s = it % STAGES;
       int tl;
       int64_t bofs;
@@ -1153,6 +1160,8 @@ __global__ void __launch_bounds__(WsTile<N>::THREADS, ws_minb<N, OP>())
       if (kq == 3) hrow[s * W::CW + rr] = (!periodic && eh < 0) ? 0.0 : r[NT - 1][1];
       __syncwarp();
       if (lane == 0) mbar_arrive(&halo[s]);
+      const int Tn = T + (STAGES - 1) * gridDim.x;
+      if (Tn < total_tiles) issue_next(Tn);
     }
     return;
   }
