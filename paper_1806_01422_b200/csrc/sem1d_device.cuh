@@ -894,9 +894,30 @@ __global__ void __launch_bounds__(MmaTile<N>::THREADS, MmaTile<N>::MINB)
 
 // Occupancy per operator (A/B-measured on config 2, profiles/r1_ab_occupancy.json):
 // F (one input) runs best at 4 CTAs/SM, J and J^T at 3.
+#ifndef WS_MINB_F8
+#define WS_MINB_F8 3
+#endif
+#ifndef WS_MINB_J8
+#define WS_MINB_J8 3
+#endif
 template <int N, int OP>
 constexpr int ws_minb() {
-  return ((N + 1) > 16) ? 1 : ((N + 1) == 16 ? 2 : (OP == OP_RHS ? 4 : 3));
+  return ((N + 1) > 16) ? 1 : ((N + 1) == 16 ? 2 : (OP == OP_RHS ? WS_MINB_F8 : WS_MINB_J8));
+}
+
+// ws-kernel B fragments with permuted output columns: DMMA output column
+// c = 8nt + 2kq + h holds element row sigma(c) = 4(2nt + h) + kq, i.e. exactly the
+// node this lane already holds as its A-fragment column for kc = 2nt + h.  The
+// pointwise terms (u_i, v_i, zm_i, M^-1_i) then come from registers, not smem.
+template <int N>
+__device__ __forceinline__ double bfrag_perm(const Consts<N>& C, int mat, int nt, int kc, int lane) {
+  constexpr int n = N + 1;
+  const int c = 8 * nt + (lane >> 2);            // B column = DMMA output column
+  const int i = 4 * (2 * (c >> 3) + (c & 1)) + ((c >> 1) & 3);
+  const int j = 4 * kc + (lane & 3);
+  if (mat == 0) return C.K[i * n + j];
+  if (mat == 1) return C.Dw[i * n + j];
+  return C.Dw[j * n + i];
 }
 
 template <int N>
@@ -970,14 +991,12 @@ __device__ __forceinline__ void mtile_compute(const Consts<N>& C, const Geo& G, 
     }
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int i = 8 * nt + 2 * kq + h;
-      const double ui = su[base + i];
+      // permuted output column (2kq+h of n-tile nt) = node 4(2nt+h)+kq = A column kc'
+      const int kcp = 2 * nt + h;
+      const double ui = au[kcp];
       double wi = 0.0;
-      if (OP == OP_JAC) wi = sw[base + i];
-      if (OP == OP_JACT) {
-        const double zr = sw[base + i];
-        wi = eslow ? jt_scale<N>(C, zr, i, eg, G) : __dmul_rn(zr, minv_p[nt][h]);
-      }
+      if (OP == OP_JAC) wi = aw[kcp];
+      if (OP == OP_JACT) wi = aw[kcp];   // already zm = mask(z M^-1)
       r[nt][h] = combine_rows<N, OP>(h ? k1 : k0, h ? p1 : p0, h ? q1 : q0, ui, wi, mnu);
     }
   }
@@ -1010,7 +1029,7 @@ __global__ void __launch_bounds__(WsTile<N>::THREADS, ws_minb<N, OP>())
     for (int q = tid; q < NMAT * NT * KC * 32; q += W::THREADS) {
       const int l = q & 31, r = q >> 5;
       const int kc = r % KC, nt = (r / KC) % NT, mat = r / (KC * NT);
-      bsm[q] = bfrag_value<N>(C, mat, nt, kc, l);
+      bsm[q] = bfrag_perm<N>(C, mat, nt, kc, l);
     }
   }
   if (tid == 0) {
@@ -1032,7 +1051,7 @@ __global__ void __launch_bounds__(WsTile<N>::THREADS, ws_minb<N, OP>())
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int kc = 0; kc < KC; ++kc)
-          breg[(mat * NT + nt) * KC + kc] = bfrag_value<N>(C, mat, nt, kc, lane);
+          breg[(mat * NT + nt) * KC + kc] = bfrag_perm<N>(C, mat, nt, kc, lane);
   }
   auto bget = [&](int mat, int nt, int kc) -> double {
     if (W::B_IN_SMEM) return bsm[((mat * NT + nt) * KC + kc) * 32 + lane];
@@ -1204,9 +1223,9 @@ __global__ void __launch_bounds__(WsTile<N>::THREADS, ws_minb<N, OP>())
           for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              const int i = 8 * nt + 2 * kq + h;
+              const int i = 4 * (2 * nt + h) + kq;     // permuted row (= A column)
               if (live && i != 0 && i != N)
-                wout[le * N + i] = (OP == OP_JACT) ? r[nt][h] : __dmul_rn(r[nt][h], minv_p[nt][h]);
+                wout[le * N + i] = (OP == OP_JACT) ? r[nt][h] : __dmul_rn(r[nt][h], minv_a[2 * nt + h]);
             }
           const double row0 = r[0][0];              // valid in lanes kq == 0
           const double rowN = r[NT - 1][1];         // valid in lanes kq == 3
@@ -1317,7 +1336,7 @@ constexpr int ws_stages() {
   constexpr int NIN = (OP == OP_RHS) ? 1 : 2;
   // shared-memory budget that keeps ws_minb CTAs resident (227 KB per SM)
   constexpr int mb = ws_minb<N, OP>();
-  constexpr int budget = (mb == 1 ? 180 : (mb == 2 ? 104 : (mb == 3 ? 72 : 56))) * 1024;
+  constexpr int budget = (mb == 1 ? 180 : (mb == 2 ? 104 : (mb == 3 ? 72 : (mb == 4 ? 54 : 44)))) * 1024;
   constexpr int per = NIN * W::SLAB_ALLOC * 8;
   constexpr int st = (budget - W::OUT * 8 - (W::B_IN_SMEM ? 3 * W::NT * W::KC * 32 * 8 : 0)) / per;
   return st < 2 ? 2 : (st > 8 ? 8 : st);
