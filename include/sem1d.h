@@ -111,6 +111,19 @@ int sem1d_adj_stage(const sem1d_plan* plan, const double* U, const double* lam, 
                     int nacc, const double* const* acc_terms, double* lam_out,
                     int* flag, void* stream);
 
+/* Ring-resident forward sweep for many small independent problems (BASELINE
+ * config 4): one CTA per ring integrates `nsteps` explicit steps of `scheme`
+ * (0 euler, 1 rk3, 2 rk4; timeloop.py:106-130) with step sizes dts[0..nsteps)
+ * (device), entirely in shared memory, writing state n of problem b to
+ * traj[n][b][:] (step-major, so traj[n] is a contiguous batch; traj may be
+ * NULL) and the last state to u_final.  flags[b] gets
+ * SEM1D_FLAG_STEP_NONFINITE if any new state of problem b was non-finite
+ * (the reference's StepFailure, timeloop.py:129; no dt retry in the batched
+ * sweep -- the host re-runs failing problems).  Periodic rings with N+1 a
+ * multiple of 8 and E a multiple of 8 (E <= 256) only. */
+int sem1d_ens_forward(const sem1d_plan* plan, const double* u0, double* traj, double* u_final,
+                      const double* dts, int nsteps, int scheme, int* flags, void* stream);
+
 /* Terminal condition (adjoint.py:33-47): d = uN - ud, lam = mask(2 M d),
  * J_out[b] = d^T M d per batch member (deterministic two-level reduction;
  * `work` must hold sem1d_terminal_work_size(plan) doubles). */

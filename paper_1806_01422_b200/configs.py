@@ -66,3 +66,22 @@ def fourier_fields(grid, batch, n_modes, seed):
 def cfg_operator(cfg, device=None, batch=1, bc=PERIODIC):
     grid = grid_1d(cfg["xa"], cfg["xb"], cfg["E"], cfg["N"], bc)
     return SemOperator(grid, PdeCoefficients(cfg["nu"]), device=device, batch=batch)
+
+
+def cfg4_problem(B=None, steps=None, scheme="rk4", device=None, seed=CFG4["seed"]):
+    """BASELINE config 4: B periodic rings (E=256, N=15, nu=0.01) on [0, 20]; u0 and the
+    observation IC are sums of 4 seeded Fourier modes (different seeds); observations come
+    from a forward run.  ``B``/``steps`` override the sizes for tests."""
+    import torch
+    c = CFG4
+    B = c["B"] if B is None else B
+    steps = c["steps"] if steps is None else steps
+    grid = grid_1d(c["xa"], c["xb"], c["E"], c["N"], PERIODIC)
+    op = SemOperator(grid, PdeCoefficients(c["nu"]), device=device, batch=B)
+    ts = timeloop.TsConfig(scheme=scheme, t0=0.0, t_end=steps * c["dt"], dt=c["dt"])
+    u0 = fourier_fields(grid, B, 4, seed)
+    obs0 = fourier_fields(grid, B, 4, seed + 1000)
+    target = timeloop.integrate_ensemble(op, torch.from_numpy(obs0).to(op.device), ts,
+                                         store_trajectory=False).u_final
+    return AssimilationProblem(name=f"cfg4-{scheme}", grid=grid, op=op, ts=ts, u_target=target,
+                               u_guess=u0)

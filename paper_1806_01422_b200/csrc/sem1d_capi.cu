@@ -16,7 +16,8 @@ using namespace sem1d;
 
 namespace sem1d {
 #define SEM_DECL(NN) \
-  extern template cudaError_t launch_apply<NN>(const PlanView&, int, const Args&, cudaStream_t);
+  extern template cudaError_t launch_apply<NN>(const PlanView&, int, const Args&, cudaStream_t); \
+  extern template cudaError_t launch_ens_forward<NN>(const PlanView&, const EnsArgs&, cudaStream_t);
 SEM_DECL(1) SEM_DECL(2) SEM_DECL(3) SEM_DECL(4) SEM_DECL(5) SEM_DECL(6) SEM_DECL(7) SEM_DECL(8)
 SEM_DECL(9) SEM_DECL(10) SEM_DECL(11) SEM_DECL(12) SEM_DECL(13) SEM_DECL(14) SEM_DECL(15)
 SEM_DECL(16) SEM_DECL(17) SEM_DECL(18) SEM_DECL(19) SEM_DECL(20) SEM_DECL(21) SEM_DECL(22)
@@ -75,6 +76,44 @@ cudaError_t dispatch(const sem1d_plan* p, int kind, const Args& a, cudaStream_t 
 #undef SEM_CASE
     default: return cudaErrorInvalidValue;
   }
+}
+
+cudaError_t dispatch_ens_forward(const sem1d_plan* p, const EnsArgs& a, cudaStream_t s) {
+  const PlanView v = view(p);
+  switch (p->N) {
+#define SEM_CASE(NN) \
+  case NN: return launch_ens_forward<NN>(v, a, s);
+    SEM_CASE(1) SEM_CASE(2) SEM_CASE(3) SEM_CASE(4) SEM_CASE(5) SEM_CASE(6) SEM_CASE(7)
+    SEM_CASE(8) SEM_CASE(9) SEM_CASE(10) SEM_CASE(11) SEM_CASE(12) SEM_CASE(13) SEM_CASE(14)
+    SEM_CASE(15) SEM_CASE(16) SEM_CASE(17) SEM_CASE(18) SEM_CASE(19) SEM_CASE(20) SEM_CASE(21)
+    SEM_CASE(22) SEM_CASE(23) SEM_CASE(24) SEM_CASE(25) SEM_CASE(26) SEM_CASE(27) SEM_CASE(28)
+    SEM_CASE(29) SEM_CASE(30) SEM_CASE(31) SEM_CASE(32)
+#undef SEM_CASE
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// Butcher tableaux of the schemes on the path (timeloop.py:24-27; RK4 classic)
+bool make_tableau(int scheme, Tableau& t) {
+  std::memset(&t, 0, sizeof(t));
+  if (scheme == 0) {            // euler
+    t.s = 1; t.b[0] = 1.0;
+  } else if (scheme == 1) {     // rk3 (Kutta-3)
+    t.s = 3;
+    t.a[1][0] = 0.5;
+    t.a[2][0] = -1.0; t.a[2][1] = 2.0;
+    t.b[0] = 1.0 / 6.0; t.b[1] = 2.0 / 3.0; t.b[2] = 1.0 / 6.0;
+    t.keep[0] = 1;
+  } else if (scheme == 2) {     // rk4
+    t.s = 4;
+    t.a[1][0] = 0.5; t.a[2][1] = 0.5; t.a[3][2] = 1.0;
+    t.b[0] = 1.0 / 6.0; t.b[1] = 1.0 / 3.0; t.b[2] = 1.0 / 3.0; t.b[3] = 1.0 / 6.0;
+  } else {
+    return false;
+  }
+  for (int i = 1; i < t.s; ++i)
+    for (int j = 0; j < i; ++j) t.nterm[i] += (t.a[i][j] != 0.0);
+  return true;
 }
 
 bool valid_plan(const sem1d_plan* p) { return p != nullptr && p->N >= 1 && p->N <= SEM1D_MAX_DEGREE; }
@@ -329,6 +368,22 @@ int sem1d_adj_stage(const sem1d_plan* plan, const double* U, const double* lam, 
     if (rc) return rc;
   }
   return run_apply(plan, 4, a, stream, "sem1d_adj_stage");
+}
+
+int sem1d_ens_forward(const sem1d_plan* plan, const double* u0, double* traj, double* u_final,
+                      const double* dts, int nsteps, int scheme, int* flags, void* stream) {
+  if (!valid_plan(plan) || !u0 || !u_final || !dts || !flags || nsteps < 0)
+    return fail(SEM1D_EINVAL, "sem1d_ens_forward: bad argument");
+  EnsArgs a;
+  std::memset(&a, 0, sizeof(a));
+  if (!make_tableau(scheme, a.tab)) return fail(SEM1D_EINVAL, "sem1d_ens_forward: unknown scheme");
+  a.u0 = u0; a.traj = traj; a.u_final = u_final; a.dts = dts; a.nsteps = nsteps; a.flags = flags;
+  cudaError_t e = dispatch_ens_forward(plan, a, static_cast<cudaStream_t>(stream));
+  if (e == cudaErrorNotSupported)
+    return fail(SEM1D_EINVAL, "sem1d_ens_forward: needs periodic rings, N+1 in {8,16,24,32}, "
+                              "E a multiple of 8 (E <= 256) that fit in shared memory");
+  if (e != cudaSuccess) return cuda_fail(e, "sem1d_ens_forward");
+  return SEM1D_OK;
 }
 
 int64_t sem1d_terminal_work_size(const sem1d_plan* plan) {

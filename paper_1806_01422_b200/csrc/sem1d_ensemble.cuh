@@ -1,0 +1,221 @@
+// sem1d_ensemble.cuh -- ring-resident sweeps (BASELINE config 4: many small
+// independent problems).  One CTA owns one periodic/Dirichlet ring whose
+// fields fit in shared memory and runs every RK step of the forward sweep
+// there; only the trajectory leaves the SM (one bulk store per step), so a
+// 1000-step forward sweep costs 8 bytes per DOF per step of HBM traffic and
+// is FP64-tensor-core bound.  The backward sweep (sem1d_ens_adjoint) streams
+// the trajectory back in the same way.
+//
+// Mapping: 8 consumer warps; a warp owns ring elements in m-tiles of 8
+// (DMMA m8n8k4.f64, permuted output columns as in apply_ws_kernel), lane
+// (rr, kq) owns nodes 4kc + kq of element rr for kc = 0..KC-1 except node N,
+// which is the right neighbour's node 0.  Interface node 0 = row N of the
+// left element (shfl within the warp, shared-memory exchange across warps,
+// ring wrap from the last warp) + row 0 of the element.
+#pragma once
+
+#include "sem1d_device.cuh"
+
+namespace sem1d {
+
+struct Tableau {
+  double a[4][4];    // a[i][j], j < i
+  double b[4];
+  int s;             // stages (1..4)
+  int keep[4];       // keep[j] != 0: k_j must be stored for a later combination row
+  int nterm[4];      // nonzero terms of row i (i >= 1)
+};
+
+struct EnsArgs {
+  const double* u0;      // (batch, ndof)
+  double* traj;          // (nsteps+1, batch, ndof), step-major, or nullptr
+  double* u_final;       // (batch, ndof)
+  const double* dts;     // (nsteps) device
+  int nsteps;
+  int* flags;            // (batch) per-problem flag bits
+  Tableau tab;
+};
+
+template <int N>
+struct EnsCfg {
+  static constexpr int n = N + 1;
+  static constexpr int W = 8;                 // consumer warps
+  static constexpr int THREADS = 32 * W;
+  static constexpr int NT = n / 8, KC = n / 4;
+};
+
+// One operator application over the whole ring held in shared memory.
+// src: node values (ndof + 1 entries; entry ndof mirrors node 0 if periodic).
+// Output: kv[q][kc] = (M^-1-scaled) F at the nodes owned by this lane, for
+// m-tile q of this warp (node 4kc+kq of element 8*(warp + q*W) + rr ... see body).
+template <int N, int WMT_MAX, class BGet>
+__device__ __forceinline__ void ring_rhs(const Consts<N>& C, const Geo& G, const double* src,
+                                         double* xfer, BGet bget, const double* minv_a,
+                                         double mnu, int warp, int lane,
+                                         double (&kv)[WMT_MAX][(N + 1) / 4], double& fin) {
+  constexpr int KC = (N + 1) / 4, NT = (N + 1) / 8, W = EnsCfg<N>::W;
+  const int kq = lane & 3, rr = lane >> 2;
+  const int E = (int)G.E;
+  const int mt_total = E / 8;
+  double carry = 0.0;
+  double row0_first = 0.0;
+#pragma unroll
+  for (int q = 0; q < WMT_MAX; ++q) {
+    const int mt = warp * WMT_MAX + q;        // contiguous m-tiles per warp
+    if (mt >= mt_total) break;
+    const int e = 8 * mt + rr;
+    const int base = e * N;
+    double au[KC];
+#pragma unroll
+    for (int kc = 0; kc < KC; ++kc) {
+      au[kc] = src[base + 4 * kc + kq];
+      fin = fma(au[kc], 0.0, fin);
+    }
+    double r[NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      double k0 = 0.0, k1 = 0.0, p0 = 0.0, p1 = 0.0;
+#pragma unroll
+      for (int kc = 0; kc < KC; ++kc) {
+        dmma884(k0, k1, au[kc], bget(0, nt, kc));
+        dmma884(p0, p1, au[kc], bget(1, nt, kc));
+      }
+      r[nt][0] = __dsub_rn(__dmul_rn(k0, mnu), __dmul_rn(au[2 * nt], p0));
+      r[nt][1] = __dsub_rn(__dmul_rn(k1, mnu), __dmul_rn(au[2 * nt + 1], p1));
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) kv[q][2 * nt + h] = __dmul_rn(r[nt][h], minv_a[2 * nt + h]);
+    const double row0 = r[0][0];
+    const double rowN = r[NT - 1][1];
+    double left = __shfl_up_sync(0xffffffffu, rowN, 1);
+    if (rr == 0) left = carry;
+    carry = __shfl_sync(0xffffffffu, rowN, 31);
+    if (q == 0) row0_first = row0;           // lane 0 patches it after the exchange
+    if (kq == 0) kv[q][0] = __dmul_rn(__dadd_rn(left, row0), minv_a[0]);
+  }
+  if (lane == 31 && warp * WMT_MAX < mt_total) xfer[warp] = carry;   // row N of the warp's last element
+  __syncthreads();
+  if (lane == 0 && warp * WMT_MAX < mt_total) {
+    // left neighbour of the warp's first element: previous warp (ring wrap from the last)
+    const int wl = (warp == 0) ? (mt_total - 1) / WMT_MAX : warp - 1;
+    double v = __dadd_rn(xfer[wl], row0_first);
+    kv[0][0] = __dmul_rn(v, minv_a[0]);
+  }
+  (void)W;
+}
+
+// Forward sweep of one ring per CTA: periodic rings, E a multiple of 8 with
+// E/8 <= 8 * WMT_MAX.  Trajectory state n+1 is written after step n.
+template <int N, int WMT_MAX>
+__global__ void __launch_bounds__(EnsCfg<N>::THREADS, 1)
+    ens_forward_kernel(const __grid_constant__ Consts<N> C, const Geo G, const EnsArgs A) {
+  constexpr int n = N + 1, KC = EnsCfg<N>::KC, NT = EnsCfg<N>::NT;
+  constexpr int THREADS = EnsCfg<N>::THREADS;
+  extern __shared__ __align__(16) double smem[];
+  const int ndof = (int)G.ndof;
+  const int pad = (ndof + 2 + 1) & ~1;        // ndof + mirror node, 16-byte multiple
+  double* su = smem;                          // base state u_n
+  double* sU = su + pad;                      // current stage input
+  double* sk = sU + pad;                      // stored slope k_0 (RK3 only)
+  double* xfer = sk + pad;                    // [8] warp exchange
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kq = lane & 3, rr = lane >> 2;
+  const int64_t b = blockIdx.x;
+  const double* u0 = A.u0 + b * G.ndof;
+  const double mnu = -C.nu;
+
+  double breg[2 * NT * KC];
+#pragma unroll
+  for (int mat = 0; mat < 2; ++mat)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int kc = 0; kc < KC; ++kc) breg[(mat * NT + nt) * KC + kc] = bfrag_perm<N>(C, mat, nt, kc, lane);
+  auto bget = [&](int mat, int nt, int kc) -> double { return breg[(mat * NT + nt) * KC + kc]; };
+  double minv_a[KC];
+#pragma unroll
+  for (int kc = 0; kc < KC; ++kc) {
+    const int j = 4 * kc + kq;
+    minv_a[kc] = C.minv[(j == 0 || j == N) ? 0 : j];
+  }
+
+  for (int k = tid; k < ndof; k += THREADS) su[k] = u0[k];
+  if (tid == 0) su[ndof] = u0[0];
+  __syncthreads();
+  const int64_t nb = gridDim.x;
+  if (A.traj) {
+    double* t0 = A.traj + b * G.ndof;
+    for (int k = tid; k < ndof; k += THREADS) t0[k] = su[k];
+  }
+
+  const int mt_total = (int)G.E / 8;
+  double fin = 0.0;
+  bool bad_step = false;
+  double acc[WMT_MAX][KC];
+  double kv[WMT_MAX][KC];
+  for (int step = 0; step < A.nsteps; ++step) {
+    const double dt = A.dts[step];
+    for (int i = 0; i < A.tab.s; ++i) {
+      const double* src = (i == 0) ? su : sU;
+      ring_rhs<N, WMT_MAX>(C, G, src, xfer, bget, minv_a, mnu, warp, lane, kv, fin);
+      // (ring_rhs ended with a barrier: every warp is done reading src)
+#pragma unroll
+      for (int q = 0; q < WMT_MAX; ++q) {
+        const int mt = warp * WMT_MAX + q;
+        if (mt >= mt_total) break;
+        const int e = 8 * mt + rr;
+#pragma unroll
+        for (int kc = 0; kc < KC; ++kc) {
+          const int j = 4 * kc + kq;
+          if (j == N) continue;               // node N belongs to the next element
+          const int g = e * N + j;
+          const double kk = kv[q][kc];
+          // acc = b0 k0 + b1 k1 + ... left to right (timeloop.py:127)
+          const double term = __dmul_rn(A.tab.b[i], kk);
+          acc[q][kc] = (i == 0) ? term : __dadd_rn(acc[q][kc], term);
+          if (i + 1 < A.tab.s) {
+            double y;
+            if (A.tab.nterm[i + 1] == 1) {
+              // single term: u + (dt * a) * k  (timeloop.py:114)
+              y = __dadd_rn(su[g], __dmul_rn(__dmul_rn(dt, A.tab.a[i + 1][i]), kk));
+            } else {
+              // u + dt * (a0 k0 + a1 k1)  (timeloop.py:116)
+              double sacc = __dmul_rn(A.tab.a[i + 1][0], (i == 0) ? kk : sk[g]);
+              for (int jj = 1; jj <= i; ++jj)
+                sacc = __dadd_rn(sacc, __dmul_rn(A.tab.a[i + 1][jj], (jj == i) ? kk : sk[g]));
+              y = __dadd_rn(su[g], __dmul_rn(dt, sacc));
+            }
+            sU[g] = y;
+            if (g == 0) sU[ndof] = y;
+            if (i == 0 && A.tab.keep[0]) sk[g] = kk;
+          } else {
+            const double un = __dadd_rn(su[g], __dmul_rn(dt, acc[q][kc]));
+            bad_step |= !isfinite(un);
+            su[g] = un;
+            if (g == 0) su[ndof] = un;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    if (A.traj) {
+      double* tn = A.traj + ((int64_t)(step + 1) * nb + b) * G.ndof;
+      for (int k = tid; k < ndof; k += THREADS) tn[k] = su[k];
+    }
+  }
+  double* uf = A.u_final + b * G.ndof;
+  for (int k = tid; k < ndof; k += THREADS) uf[k] = su[k];
+  const bool bad_in = fin != fin;
+  if (bad_in || bad_step)
+    atomicOr(&A.flags[b], (bad_in ? SEM1D_FLAG_STATE_NONFINITE : 0) | (bad_step ? SEM1D_FLAG_STEP_NONFINITE : 0));
+  (void)n;
+}
+
+template <int N>
+constexpr size_t ens_smem_bytes(int ndof) {
+  return sizeof(double) * (3 * (size_t)((ndof + 2 + 1) & ~1) + 8);
+}
+
+}  // namespace sem1d

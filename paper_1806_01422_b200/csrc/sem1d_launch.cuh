@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include "sem1d_device.cuh"
+#include "sem1d_ensemble.cuh"
 
 namespace sem1d {
 
@@ -179,5 +180,24 @@ cudaError_t launch_apply(const PlanView& p, int kind, const Args& a, cudaStream_
 
 template <int N>
 constexpr size_t consts_size() { return sizeof(Consts<N>); }
+
+// Ring-resident ensemble forward sweep (one CTA per ring).
+template <int N>
+cudaError_t launch_ens_forward(const PlanView& p, const EnsArgs& a, cudaStream_t s) {
+  if constexpr ((N + 1) % 8 != 0) {
+    return cudaErrorNotSupported;
+  } else {
+    constexpr int WMT = 4;
+    if (!p.geo.periodic || p.geo.E % 8 != 0 || p.geo.E / 8 > 8 * WMT) return cudaErrorNotSupported;
+    const size_t smem = ens_smem_bytes<N>((int)p.geo.ndof);
+    if (smem > 220 * 1024) return cudaErrorNotSupported;
+    auto kern = ens_forward_kernel<N, WMT>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)p.batch, EnsCfg<N>::THREADS, smem, s>>>(*static_cast<const Consts<N>*>(p.consts),
+                                                             p.geo, a);
+    return cudaGetLastError();
+  }
+}
 
 }  // namespace sem1d

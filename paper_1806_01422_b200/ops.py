@@ -212,6 +212,13 @@ class SemOperator:
                                               self._work.data_ptr(), self._stream()),
                    "sem1d_terminal")
 
+    def launch_ens_forward(self, u0, traj, u_final, dts_dev, nsteps, scheme, flags):
+        code = {"euler": 0, "rk3": 1, "rk4": 2}[scheme]
+        _lib.check(_lib.load().sem1d_ens_forward(
+            self._plan.handle, u0.data_ptr(), None if traj is None else traj.data_ptr(),
+            u_final.data_ptr(), dts_dev.data_ptr(), int(nsteps), code, flags.data_ptr(),
+            self._stream()), "sem1d_ens_forward")
+
     # -- reference surface ------------------------------------------------------
 
     def apply_rhs(self, u):

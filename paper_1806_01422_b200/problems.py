@@ -49,6 +49,7 @@ class AssimilationProblem:
     u_exact_ic: object = None
     exact_solution: object = None
     checkpoint_slots: int | None = None
+    use_ensemble: bool = True   # batch > 1: ring-resident forward sweep when supported
 
     def __post_init__(self):
         self._target_dev = None
@@ -73,7 +74,15 @@ class AssimilationProblem:
         u0_dev, host = self.op.field(u0, "initial state")
         m = timeloop.count_steps(self.ts)
         sched = self.schedule_for(m)
-        fwd = timeloop.integrate(self.op, u0_dev, self.ts, store_steps=sched.forward_stores.keys())
+        if self.op.batch > 1 and self.checkpoint_slots is None and self.use_ensemble:
+            # many small rings: ring-resident forward sweep, trajectory in HBM
+            fwd = timeloop.integrate_ensemble(self.op, u0_dev, self.ts)
+            if fwd.stats["failed"]:
+                from .errors import StepFailure
+                raise StepFailure(f"non-finite state in problems {fwd.stats['failed'][:8]}")
+        else:
+            fwd = timeloop.integrate(self.op, u0_dev, self.ts,
+                                     store_steps=sched.forward_stores.keys())
         if fwd.n_steps != m:  # a StepFailure retry changed the time grid
             sched = self.schedule_for(fwd.n_steps)
         j, lam = adjoint.terminal_condition(self.grid, fwd.u_final, self.target(), op=self.op)

@@ -297,3 +297,48 @@ def rk3_stages(op, u, t, dt):
     Us = e.stages(u, dt, bufs)
     check_step_flags(op)
     return tuple(Us)
+
+
+def fixed_step_sizes(cfg):
+    """The dt sequence of a fixed-dt run (timeloop.py:264-278, no failures)."""
+    tiny = 1e-9 * cfg.dt
+    t, dts = cfg.t0, []
+    while t < cfg.t_end - tiny:
+        remaining = cfg.t_end - t
+        clipped = remaining - cfg.dt <= tiny
+        dt = remaining if clipped else cfg.dt
+        t = cfg.t_end if clipped else t + dt
+        dts.append(dt)
+        if len(dts) > cfg.max_steps:
+            raise ValidationError(f"fixed-dt run exceeds max_steps={cfg.max_steps}")
+    return dts
+
+
+def integrate_ensemble(op, u0, cfg, store_trajectory=True):
+    """Forward sweep of a batch of independent rings, one CTA per ring, every step in
+    shared memory (sem1d_ens_forward).  Same dt sequence and step arithmetic as
+    :func:`integrate`; a problem whose state goes non-finite is reported in
+    ``stats["failed"]`` (the batched sweep does not retry with halved dt)."""
+    import torch
+    _require_explicit(cfg)
+    u, _ = op.field(u0, "initial state")
+    if not op._isfinite_all(u):
+        raise NumericFailure("initial state contains NaN/Inf")
+    dts = fixed_step_sizes(cfg)
+    m = len(dts)
+    dts_dev = torch.tensor(dts, dtype=torch.float64, device=op.device)
+    traj = None
+    if store_trajectory:
+        traj = torch.empty((m + 1,) + tuple(u.shape), dtype=torch.float64, device=op.device)
+    u_final = op.empty()
+    flags = torch.zeros(op.batch, dtype=torch.int32, device=op.device)
+    op.launch_ens_forward(u.contiguous(), traj, u_final, dts_dev, m, cfg.scheme, flags)
+    fl = flags.cpu()
+    failed = [int(i) for i in torch.nonzero(fl).flatten()]
+    snapshots = {n: traj[n] for n in range(m + 1)} if traj is not None else {0: u.clone()}
+    ts = np.concatenate([[cfg.t0], cfg.t0 + np.cumsum(dts)]) if m else np.asarray([cfg.t0])
+    if m:
+        ts[-1] = cfg.t_end
+    stats = {"steps": m, "rejects": 0, "retries": 0, "failed": failed}
+    return ForwardResult(ts=ts, dts=np.asarray(dts), snapshots=snapshots, u_final=u_final,
+                         stats=stats)

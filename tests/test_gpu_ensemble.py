@@ -1,0 +1,58 @@
+"""Ring-resident ensemble sweeps (BASELINE config 4) vs the oracle and vs the
+stage-kernel integrator, per problem, within the 1e-9 sweep tolerance."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1806_01422_b200 as sb
+from oracle import semref as R
+from paper_1806_01422_b200 import configs, timeloop
+from paper_1806_01422_b200.grid import grid_1d
+from semtest_util import rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("scheme", ["rk4", "rk3", "euler"])
+@pytest.mark.parametrize("E,N", [(256, 15), (64, 7), (32, 31), (16, 15)])
+def test_ensemble_forward_vs_oracle(cuda, scheme, E, N):
+    B, steps, dt = 5, 25, 5e-5
+    grid = grid_1d(0.0, 20.0, E, N)
+    op = sb.SemOperator(grid, sb.PdeCoefficients(0.01), device="cuda:0", batch=B)
+    u0 = configs.fourier_fields(grid, B, 4, seed=E + N)
+    ts = sb.TsConfig(scheme=scheme, t0=0.0, t_end=steps * dt, dt=dt)
+    fwd = timeloop.integrate_ensemble(op, u0, ts)
+    assert fwd.n_steps == steps and not fwd.stats["failed"]
+    ref = R.BurgersOracle(R.Mesh1D(0.0, 20.0, E, N, True), 0.01)
+    for b in (0, B - 1):
+        traj, _ = R.forward(ref, u0[b], 0.0, steps * dt, dt, scheme)
+        for n in (1, steps // 2, steps):
+            assert rel_err(fwd.snapshots[n][b].cpu().numpy(), traj[n]) <= 1e-12
+        assert rel_err(fwd.u_final[b].cpu().numpy(), traj[-1]) <= 1e-12
+    # same arithmetic as the stage-kernel integrator, to rounding of the apply order
+    fwd2 = timeloop.integrate(op, u0, ts)
+    assert float((fwd2.u_final - fwd.u_final).abs().max() / fwd.u_final.abs().max()) <= 1e-12
+
+
+def test_ensemble_failure_is_reported(cuda):
+    grid = grid_1d(0.0, 20.0, 256, 15)
+    op = sb.SemOperator(grid, sb.PdeCoefficients(0.01), device="cuda:0", batch=3)
+    u0 = configs.fourier_fields(grid, 3, 4, seed=1)
+    u0[1] *= 1e140
+    fwd = timeloop.integrate_ensemble(op, u0, sb.TsConfig(scheme="rk4", t_end=20 * 5e-5, dt=5e-5))
+    assert 1 in fwd.stats["failed"] and 0 not in fwd.stats["failed"]
+
+
+def test_cfg4_batched_gradient_vs_oracle(cuda):
+    """config 4 structure at reduced B / steps: batched evaluate() per problem vs oracle."""
+    prob = configs.cfg4_problem(B=4, steps=40, device="cuda:0")
+    u0 = prob.u_guess
+    J, g = prob.evaluate(u0)
+    c = configs.CFG4
+    ref = R.BurgersOracle(R.Mesh1D(c["xa"], c["xb"], c["E"], c["N"], True), c["nu"])
+    target = prob.target().cpu().numpy()
+    for b in range(4):
+        j_ref, g_ref, _ = R.evaluate(ref, u0[b], target[b], 0.0, 40 * c["dt"], c["dt"], "rk4")
+        assert abs(float(J[b]) - j_ref) <= 1e-9 * abs(j_ref)
+        assert rel_err(g[b], g_ref) <= 1e-9
