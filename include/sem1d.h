@@ -124,6 +124,15 @@ int sem1d_adj_stage(const sem1d_plan* plan, const double* U, const double* lam, 
 int sem1d_ens_forward(const sem1d_plan* plan, const double* u0, double* traj, double* u_final,
                       const double* dts, int nsteps, int scheme, int* flags, void* stream);
 
+/* Ring-resident backward sweep matching sem1d_ens_forward (adjoint.py:54-61
+ * generalised to the tableau): for n = nsteps-1..0 it reloads u_n from the
+ * step-major trajectory, recomputes the stage states in shared memory and runs
+ * the stage-adjoint recurrence; lam_out[b] = dJ/du0 for the terminal seeds
+ * lam_in[b] (sem1d_terminal).  Same ring restrictions as sem1d_ens_forward. */
+int sem1d_ens_adjoint(const sem1d_plan* plan, const double* traj, const double* lam_in,
+                      double* lam_out, const double* dts, int nsteps, int scheme, int* flags,
+                      void* stream);
+
 /* Terminal condition (adjoint.py:33-47): d = uN - ud, lam = mask(2 M d),
  * J_out[b] = d^T M d per batch member (deterministic two-level reduction;
  * `work` must hold sem1d_terminal_work_size(plan) doubles). */

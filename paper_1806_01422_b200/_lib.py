@@ -42,6 +42,8 @@ SIGNATURES = {
                                 c_double, c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p]),
     "sem1d_ens_forward": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int,
                                   c_void_p, c_void_p]),
+    "sem1d_ens_adjoint": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int,
+                                  c_void_p, c_void_p]),
     "sem1d_terminal_work_size": (c_int64, [c_void_p]),
     "sem1d_terminal": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "sem1d_scatter": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),

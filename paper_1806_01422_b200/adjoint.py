@@ -190,3 +190,26 @@ def gradient(op, cfg, fwd, schedule, u_ref):
     """terminal_condition + sweep (adjoint.py:161-164)."""
     j, lam = terminal_condition(op.grid, fwd.u_final, u_ref, op=op)
     return j, sweep(op, cfg, fwd, schedule, lam)
+
+
+def ensemble_sweep(op, cfg, fwd, lam_terminal):
+    """Backward sweep of a batch of rings over a trajectory from
+    ``timeloop.integrate_ensemble`` -- one CTA per ring, every step in shared memory
+    (sem1d_ens_adjoint).  Same recurrence as :func:`sweep` with store-all; the stage
+    adjoints are accumulated as lam + (l_s + ... + l_1) instead of ((lam + l_1) + ...)."""
+    import torch
+    traj = getattr(fwd, "trajectory", None)
+    if traj is None:
+        raise ValidationError("ensemble_sweep needs the stored trajectory of integrate_ensemble")
+    lam_in, host = op.field(lam_terminal, "cotangent")
+    lam_out = op.empty()
+    flags = torch.zeros(op.batch, dtype=torch.int32, device=op.device)
+    op.launch_ens_adjoint(traj, lam_in.contiguous(), lam_out, fwd.dts_device, fwd.n_steps,
+                          cfg.scheme, flags)
+    if int(flags.max()):
+        raise NumericFailure("cotangent contains NaN/Inf")
+    s = len(TABLEAUX[cfg.scheme][1])
+    op.counters["rhs"] += (s - 1) * fwd.n_steps
+    op.counters["jact"] += s * fwd.n_steps
+    op.last_sweep_stats = {"newton_iters": 0, "gmres_iters": 0, "recomputed": 0}
+    return lam_out.cpu().numpy() if host else lam_out

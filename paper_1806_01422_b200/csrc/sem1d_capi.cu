@@ -17,7 +17,8 @@ using namespace sem1d;
 namespace sem1d {
 #define SEM_DECL(NN) \
   extern template cudaError_t launch_apply<NN>(const PlanView&, int, const Args&, cudaStream_t); \
-  extern template cudaError_t launch_ens_forward<NN>(const PlanView&, const EnsArgs&, cudaStream_t);
+  extern template cudaError_t launch_ens_forward<NN>(const PlanView&, const EnsArgs&, cudaStream_t); \
+  extern template cudaError_t launch_ens_adjoint<NN>(const PlanView&, const EnsAdjArgs&, cudaStream_t);
 SEM_DECL(1) SEM_DECL(2) SEM_DECL(3) SEM_DECL(4) SEM_DECL(5) SEM_DECL(6) SEM_DECL(7) SEM_DECL(8)
 SEM_DECL(9) SEM_DECL(10) SEM_DECL(11) SEM_DECL(12) SEM_DECL(13) SEM_DECL(14) SEM_DECL(15)
 SEM_DECL(16) SEM_DECL(17) SEM_DECL(18) SEM_DECL(19) SEM_DECL(20) SEM_DECL(21) SEM_DECL(22)
@@ -83,6 +84,21 @@ cudaError_t dispatch_ens_forward(const sem1d_plan* p, const EnsArgs& a, cudaStre
   switch (p->N) {
 #define SEM_CASE(NN) \
   case NN: return launch_ens_forward<NN>(v, a, s);
+    SEM_CASE(1) SEM_CASE(2) SEM_CASE(3) SEM_CASE(4) SEM_CASE(5) SEM_CASE(6) SEM_CASE(7)
+    SEM_CASE(8) SEM_CASE(9) SEM_CASE(10) SEM_CASE(11) SEM_CASE(12) SEM_CASE(13) SEM_CASE(14)
+    SEM_CASE(15) SEM_CASE(16) SEM_CASE(17) SEM_CASE(18) SEM_CASE(19) SEM_CASE(20) SEM_CASE(21)
+    SEM_CASE(22) SEM_CASE(23) SEM_CASE(24) SEM_CASE(25) SEM_CASE(26) SEM_CASE(27) SEM_CASE(28)
+    SEM_CASE(29) SEM_CASE(30) SEM_CASE(31) SEM_CASE(32)
+#undef SEM_CASE
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t dispatch_ens_adjoint(const sem1d_plan* p, const EnsAdjArgs& a, cudaStream_t s) {
+  const PlanView v = view(p);
+  switch (p->N) {
+#define SEM_CASE(NN) \
+  case NN: return launch_ens_adjoint<NN>(v, a, s);
     SEM_CASE(1) SEM_CASE(2) SEM_CASE(3) SEM_CASE(4) SEM_CASE(5) SEM_CASE(6) SEM_CASE(7)
     SEM_CASE(8) SEM_CASE(9) SEM_CASE(10) SEM_CASE(11) SEM_CASE(12) SEM_CASE(13) SEM_CASE(14)
     SEM_CASE(15) SEM_CASE(16) SEM_CASE(17) SEM_CASE(18) SEM_CASE(19) SEM_CASE(20) SEM_CASE(21)
@@ -383,6 +399,23 @@ int sem1d_ens_forward(const sem1d_plan* plan, const double* u0, double* traj, do
     return fail(SEM1D_EINVAL, "sem1d_ens_forward: needs periodic rings, N+1 in {8,16,24,32}, "
                               "E a multiple of 8 (E <= 256) that fit in shared memory");
   if (e != cudaSuccess) return cuda_fail(e, "sem1d_ens_forward");
+  return SEM1D_OK;
+}
+
+int sem1d_ens_adjoint(const sem1d_plan* plan, const double* traj, const double* lam_in,
+                      double* lam_out, const double* dts, int nsteps, int scheme, int* flags,
+                      void* stream) {
+  if (!valid_plan(plan) || !traj || !lam_in || !lam_out || !dts || !flags || nsteps < 0)
+    return fail(SEM1D_EINVAL, "sem1d_ens_adjoint: bad argument");
+  EnsAdjArgs a;
+  std::memset(&a, 0, sizeof(a));
+  if (!make_tableau(scheme, a.tab)) return fail(SEM1D_EINVAL, "sem1d_ens_adjoint: unknown scheme");
+  a.traj = traj; a.lam_in = lam_in; a.lam_out = lam_out; a.dts = dts; a.nsteps = nsteps; a.flags = flags;
+  cudaError_t e = dispatch_ens_adjoint(plan, a, static_cast<cudaStream_t>(stream));
+  if (e == cudaErrorNotSupported)
+    return fail(SEM1D_EINVAL, "sem1d_ens_adjoint: needs periodic rings, N+1 in {8,16,24,32}, "
+                              "E a multiple of 8 (E <= 256) that fit in shared memory");
+  if (e != cudaSuccess) return cuda_fail(e, "sem1d_ens_adjoint");
   return SEM1D_OK;
 }
 

@@ -213,6 +213,206 @@ __global__ void __launch_bounds__(EnsCfg<N>::THREADS, 1)
   (void)n;
 }
 
+// J^T over the ring held in shared memory: usrc = linearisation point, zsrc =
+// zm = mask(z M^-1) already scaled (ops.py:252-254).  Output (no M^-1, ops.py:256):
+// jv[q][kc] at the nodes owned by this lane, interface nodes summed.
+template <int N, int WMT_MAX, class BGet>
+__device__ __forceinline__ void ring_jact(const Consts<N>& C, const Geo& G, const double* usrc,
+                                          const double* zsrc, double* xfer, BGet bget,
+                                          double mnu, int warp, int lane,
+                                          double (&jv)[WMT_MAX][(N + 1) / 4]) {
+  constexpr int KC = (N + 1) / 4, NT = (N + 1) / 8;
+  const int kq = lane & 3, rr = lane >> 2;
+  const int mt_total = (int)G.E / 8;
+  double carry = 0.0, row0_first = 0.0;
+#pragma unroll
+  for (int q = 0; q < WMT_MAX; ++q) {
+    const int mt = warp * WMT_MAX + q;
+    if (mt >= mt_total) break;
+    const int base = (8 * mt + rr) * N;
+    double au[KC], az[KC], at[KC];
+#pragma unroll
+    for (int kc = 0; kc < KC; ++kc) {
+      au[kc] = usrc[base + 4 * kc + kq];
+      az[kc] = zsrc[base + 4 * kc + kq];
+      at[kc] = __dmul_rn(au[kc], az[kc]);
+    }
+    double r[NT][2];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) {
+      double k0 = 0.0, k1 = 0.0, p0 = 0.0, p1 = 0.0, t0 = 0.0, t1 = 0.0;
+#pragma unroll
+      for (int kc = 0; kc < KC; ++kc) {
+        dmma884(k0, k1, az[kc], bget(0, nt, kc));   // K zm
+        dmma884(p0, p1, au[kc], bget(1, nt, kc));   // Dw u
+        dmma884(t0, t1, at[kc], bget(2, nt, kc));   // Dw^T (u o zm)
+      }
+      r[nt][0] = __dsub_rn(__dsub_rn(__dmul_rn(k0, mnu), __dmul_rn(az[2 * nt], p0)), t0);
+      r[nt][1] = __dsub_rn(__dsub_rn(__dmul_rn(k1, mnu), __dmul_rn(az[2 * nt + 1], p1)), t1);
+    }
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) jv[q][2 * nt + h] = r[nt][h];
+    const double row0 = r[0][0], rowN = r[NT - 1][1];
+    double left = __shfl_up_sync(0xffffffffu, rowN, 1);
+    if (rr == 0) left = carry;
+    carry = __shfl_sync(0xffffffffu, rowN, 31);
+    if (q == 0) row0_first = row0;
+    if (kq == 0) jv[q][0] = __dadd_rn(left, row0);
+  }
+  if (lane == 31 && warp * WMT_MAX < mt_total) xfer[warp] = carry;
+  __syncthreads();
+  if (lane == 0 && warp * WMT_MAX < mt_total) {
+    const int wl = (warp == 0) ? (mt_total - 1) / WMT_MAX : warp - 1;
+    jv[0][0] = __dadd_rn(xfer[wl], row0_first);
+  }
+}
+
+struct EnsAdjArgs {
+  const double* traj;     // (nsteps+1, batch, ndof) step-major forward trajectory
+  const double* lam_in;   // (batch, ndof) terminal seed
+  double* lam_out;        // (batch, ndof) dJ/du0
+  const double* dts;
+  int nsteps;
+  int* flags;
+  Tableau tab;
+};
+
+// Backward sweep of one ring per CTA (adjoint.py:54-61 generalised, every step in
+// shared memory): stage states recomputed from the stored u_n (s-1 F applies), then
+// l_i = dt J^T(U_i)(b_i lam + sum_{j>i} a_ji l_j) for i = s-1..0 and
+// lam <- lam + (l_{s-1} + ... + l_0).
+template <int N, int WMT_MAX>
+__global__ void __launch_bounds__(EnsCfg<N>::THREADS, 1)
+    ens_adjoint_kernel(const __grid_constant__ Consts<N> C, const Geo G, const EnsAdjArgs A) {
+  constexpr int KC = EnsCfg<N>::KC, NT = EnsCfg<N>::NT;
+  constexpr int THREADS = EnsCfg<N>::THREADS;
+  extern __shared__ __align__(16) double smem[];
+  const int ndof = (int)G.ndof;
+  const int pad = (ndof + 2 + 1) & ~1;
+  const int S = A.tab.s;
+  double* su = smem;                          // u_n (= U_0)
+  double* sUs = su + pad;                     // U_1 .. U_{S-1}: S-1 arrays
+  double* sk = sUs + 3 * pad;                 // k_0 (RK3 recompute) / an older l (RK3 chain)
+  double* sz = sk + pad;                      // zm for the current J^T
+  double* slam = sz + pad;                    // lam (owner-only)
+  double* xfer = slam + pad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kq = lane & 3, rr = lane >> 2;
+  const int64_t b = blockIdx.x, nb = gridDim.x;
+  const double mnu = -C.nu;
+  auto Uarr = [&](int i) -> double* { return i == 0 ? su : sUs + (i - 1) * pad; };
+
+  double breg[3 * NT * KC];
+#pragma unroll
+  for (int mat = 0; mat < 3; ++mat)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int kc = 0; kc < KC; ++kc) breg[(mat * NT + nt) * KC + kc] = bfrag_perm<N>(C, mat, nt, kc, lane);
+  auto bget = [&](int mat, int nt, int kc) -> double { return breg[(mat * NT + nt) * KC + kc]; };
+  double minv_a[KC];
+#pragma unroll
+  for (int kc = 0; kc < KC; ++kc) {
+    const int j = 4 * kc + kq;
+    minv_a[kc] = C.minv[(j == 0 || j == N) ? 0 : j];
+  }
+  const int mt_total = (int)G.E / 8;
+  const double* lin = A.lam_in + b * G.ndof;
+  for (int k = tid; k < ndof; k += THREADS) slam[k] = lin[k];
+  double fin = 0.0;
+  double kv[WMT_MAX][KC], lnext[WMT_MAX][KC], lacc[WMT_MAX][KC];
+
+  for (int step = A.nsteps - 1; step >= 0; --step) {
+    const double dt = A.dts[step];
+    const double* un = A.traj + ((int64_t)step * nb + b) * G.ndof;
+    __syncthreads();   // previous step's readers of su / sUs are done
+    for (int k = tid; k < ndof; k += THREADS) su[k] = un[k];
+    if (tid == 0) su[ndof] = un[0];
+    __syncthreads();
+    // ---- stage states U_1..U_{S-1} (timeloop.rk3_stages, adjoint.py:56)
+    for (int i = 0; i + 1 < S; ++i) {
+      ring_rhs<N, WMT_MAX>(C, G, Uarr(i), xfer, bget, minv_a, mnu, warp, lane, kv, fin);
+      double* dst = Uarr(i + 1);
+#pragma unroll
+      for (int q = 0; q < WMT_MAX; ++q) {
+        const int mt = warp * WMT_MAX + q;
+        if (mt >= mt_total) break;
+#pragma unroll
+        for (int kc = 0; kc < KC; ++kc) {
+          const int j = 4 * kc + kq;
+          if (j == N) continue;
+          const int g = (8 * mt + rr) * N + j;
+          const double kk = kv[q][kc];
+          double y;
+          if (A.tab.nterm[i + 1] == 1) {
+            y = __dadd_rn(su[g], __dmul_rn(__dmul_rn(dt, A.tab.a[i + 1][i]), kk));
+          } else {
+            double sacc = __dmul_rn(A.tab.a[i + 1][0], (i == 0) ? kk : sk[g]);
+            for (int jj = 1; jj <= i; ++jj)
+              sacc = __dadd_rn(sacc, __dmul_rn(A.tab.a[i + 1][jj], (jj == i) ? kk : sk[g]));
+            y = __dadd_rn(su[g], __dmul_rn(dt, sacc));
+          }
+          dst[g] = y;
+          if (g == 0) dst[ndof] = y;
+          if (i == 0 && A.tab.keep[0]) sk[g] = kk;
+        }
+      }
+      __syncthreads();
+    }
+    // ---- stage-adjoint chain, i = S-1 .. 0
+    for (int i = S - 1; i >= 0; --i) {
+#pragma unroll
+      for (int q = 0; q < WMT_MAX; ++q) {
+        const int mt = warp * WMT_MAX + q;
+        if (mt >= mt_total) break;
+#pragma unroll
+        for (int kc = 0; kc < KC; ++kc) {
+          const int j = 4 * kc + kq;
+          if (j == N) continue;
+          const int g = (8 * mt + rr) * N + j;
+          // z = b_i lam + a_{i+1,i} l_{i+1} + a_{i+2,i} l_{i+2} (adjoint.py:58-60)
+          double z = __dmul_rn(A.tab.b[i], slam[g]);
+          if (i + 1 < S && A.tab.a[i + 1][i] != 0.0) z = __dadd_rn(z, __dmul_rn(A.tab.a[i + 1][i], lnext[q][kc]));
+          if (i + 2 < S && A.tab.a[i + 2][i] != 0.0) z = __dadd_rn(z, __dmul_rn(A.tab.a[i + 2][i], sk[g]));
+          fin = fma(z, 0.0, fin);
+          const double zm = __dmul_rn(z, minv_a[kc]);
+          sz[g] = zm;
+          if (g == 0) sz[ndof] = zm;
+        }
+      }
+      __syncthreads();
+      ring_jact<N, WMT_MAX>(C, G, Uarr(i), sz, xfer, bget, mnu, warp, lane, kv);
+#pragma unroll
+      for (int q = 0; q < WMT_MAX; ++q) {
+        const int mt = warp * WMT_MAX + q;
+        if (mt >= mt_total) break;
+#pragma unroll
+        for (int kc = 0; kc < KC; ++kc) {
+          const int j = 4 * kc + kq;
+          if (j == N) continue;
+          const int g = (8 * mt + rr) * N + j;
+          const double l = __dmul_rn(dt, kv[q][kc]);
+          lacc[q][kc] = (i == S - 1) ? l : __dadd_rn(lacc[q][kc], l);
+          if (i + 1 < S && S == 3) sk[g] = lnext[q][kc];   // RK3: keep l_{i+1} for z_{i-1}
+          lnext[q][kc] = l;
+          if (i == 0) slam[g] = __dadd_rn(slam[g], lacc[q][kc]);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  double* lo = A.lam_out + b * G.ndof;
+  for (int k = tid; k < ndof; k += THREADS) lo[k] = slam[k];
+  if (fin != fin) atomicOr(&A.flags[b], SEM1D_FLAG_INPUT2_NONFINITE);
+}
+
+template <int N>
+constexpr size_t ens_adj_smem_bytes(int ndof) {
+  return sizeof(double) * (7 * (size_t)((ndof + 2 + 1) & ~1) + 8);
+}
+
 template <int N>
 constexpr size_t ens_smem_bytes(int ndof) {
   return sizeof(double) * (3 * (size_t)((ndof + 2 + 1) & ~1) + 8);

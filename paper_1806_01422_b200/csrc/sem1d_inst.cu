@@ -8,4 +8,5 @@
 namespace sem1d {
 template cudaError_t launch_apply<SEM_N>(const PlanView&, int, const Args&, cudaStream_t);
 template cudaError_t launch_ens_forward<SEM_N>(const PlanView&, const EnsArgs&, cudaStream_t);
+template cudaError_t launch_ens_adjoint<SEM_N>(const PlanView&, const EnsAdjArgs&, cudaStream_t);
 }

@@ -181,6 +181,25 @@ cudaError_t launch_apply(const PlanView& p, int kind, const Args& a, cudaStream_
 template <int N>
 constexpr size_t consts_size() { return sizeof(Consts<N>); }
 
+// Ring-resident ensemble backward sweep (one CTA per ring).
+template <int N>
+cudaError_t launch_ens_adjoint(const PlanView& p, const EnsAdjArgs& a, cudaStream_t s) {
+  if constexpr ((N + 1) % 8 != 0) {
+    return cudaErrorNotSupported;
+  } else {
+    constexpr int WMT = 4;
+    if (!p.geo.periodic || p.geo.E % 8 != 0 || p.geo.E / 8 > 8 * WMT) return cudaErrorNotSupported;
+    const size_t smem = ens_adj_smem_bytes<N>((int)p.geo.ndof);
+    if (smem > 226 * 1024) return cudaErrorNotSupported;
+    auto kern = ens_adjoint_kernel<N, WMT>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)p.batch, EnsCfg<N>::THREADS, smem, s>>>(*static_cast<const Consts<N>*>(p.consts),
+                                                             p.geo, a);
+    return cudaGetLastError();
+  }
+}
+
 // Ring-resident ensemble forward sweep (one CTA per ring).
 template <int N>
 cudaError_t launch_ens_forward(const PlanView& p, const EnsArgs& a, cudaStream_t s) {

@@ -219,6 +219,13 @@ class SemOperator:
             u_final.data_ptr(), dts_dev.data_ptr(), int(nsteps), code, flags.data_ptr(),
             self._stream()), "sem1d_ens_forward")
 
+    def launch_ens_adjoint(self, traj, lam_in, lam_out, dts_dev, nsteps, scheme, flags):
+        code = {"euler": 0, "rk3": 1, "rk4": 2}[scheme]
+        _lib.check(_lib.load().sem1d_ens_adjoint(
+            self._plan.handle, traj.data_ptr(), lam_in.data_ptr(), lam_out.data_ptr(),
+            dts_dev.data_ptr(), int(nsteps), code, flags.data_ptr(), self._stream()),
+            "sem1d_ens_adjoint")
+
     # -- reference surface ------------------------------------------------------
 
     def apply_rhs(self, u):

@@ -86,7 +86,10 @@ class AssimilationProblem:
         if fwd.n_steps != m:  # a StepFailure retry changed the time grid
             sched = self.schedule_for(fwd.n_steps)
         j, lam = adjoint.terminal_condition(self.grid, fwd.u_final, self.target(), op=self.op)
-        g = adjoint.sweep(self.op, self.ts, fwd, sched, lam)
+        if getattr(fwd, "trajectory", None) is not None:
+            g = adjoint.ensemble_sweep(self.op, self.ts, fwd, lam)
+        else:
+            g = adjoint.sweep(self.op, self.ts, fwd, sched, lam)
         self.last_forward = fwd
         if host:
             g = g.cpu().numpy()

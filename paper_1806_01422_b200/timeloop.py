@@ -340,5 +340,8 @@ def integrate_ensemble(op, u0, cfg, store_trajectory=True):
     if m:
         ts[-1] = cfg.t_end
     stats = {"steps": m, "rejects": 0, "retries": 0, "failed": failed}
-    return ForwardResult(ts=ts, dts=np.asarray(dts), snapshots=snapshots, u_final=u_final,
-                         stats=stats)
+    res = ForwardResult(ts=ts, dts=np.asarray(dts), snapshots=snapshots, u_final=u_final,
+                        stats=stats)
+    res.trajectory = traj          # (m+1, batch, ndof) step-major, for ensemble_sweep
+    res.dts_device = dts_dev
+    return res
