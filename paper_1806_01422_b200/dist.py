@@ -1,0 +1,329 @@
+"""Element-sharded operator for multi-GPU runs (BASELINE config 5).
+
+Partition: rank r of P owns the contiguous element block [e_lo, e_hi) and the
+global nodes [e_lo*N, e_hi*N) (plus node E*N on the last rank of a Dirichlet
+grid).  Each rank stores its fields on an EXTENDED chain: its elements plus
+one ghost element on each side that has a neighbour (no ghost at a global
+Dirichlet end; two on the left, see Partition), laid out as a local Dirichlet grid with the GLOBAL element
+length h.  The unchanged fused kernels then compute, on every rank, both
+contributions to each owned interface node -- including node e_lo*N, whose
+left contribution comes from the recomputed ghost element -- so a sharded
+apply is bit-identical to the single-GPU apply (the interface sum has the same
+two terms; K and M^-1 are built from the same h).
+
+Communication per operator input: one ghost refresh -- send the first N+1
+owned nodes to the left neighbour and the last 2N owned nodes to the right
+neighbour (torch.distributed P2P: NCCL over NVLink on GPUs, gloo on CPU for
+the tests).  Dot products (the objective, L-BFGS) all-reduce the owned parts.
+The stage kernels run unchanged on extended fields; before each stage the
+inputs the kernel reads across element boundaries (U, and lam / l_j for the
+adjoint) are refreshed in one batched exchange.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _lib
+from .errors import ValidationError
+from .grid import DIRICHLET0, PERIODIC, Axis, Grid
+
+
+class Partition:
+    """Contiguous element blocks; ghost elements where a neighbour exists."""
+
+    def __init__(self, E, N, P, rank, periodic):
+        if P < 1 or not (0 <= rank < P):
+            raise ValidationError(f"bad rank {rank} of {P}")
+        if E < 3 * P:
+            raise ValidationError(f"need at least 3 elements per rank (E={E}, P={P})")
+        self.E, self.N, self.P, self.rank, self.periodic = E, N, P, rank, bool(periodic)
+        self.e_lo = (rank * E) // P
+        self.e_hi = ((rank + 1) * E) // P
+        self.E_loc = self.e_hi - self.e_lo
+        last_dirichlet = (not self.periodic) and rank == P - 1
+        self.n_own = self.E_loc * N + (1 if last_dirichlet else 0)
+        # two ghost elements on the left: J^T masks and M^-1-scales its INPUT at the
+        # chain's end node (ops.py:252-254), so element e_lo-1 (which contributes to the
+        # owned node e_lo*N) must not touch the chain end; one on the right suffices
+        # because node e_hi*N is not owned.
+        self.gl = 2 if (self.periodic or rank > 0) else 0
+        self.gr = 1 if (self.periodic or rank < P - 1) else 0
+        if P == 1:
+            self.gl = self.gr = 0
+        self.E_ext = self.E_loc + self.gl + self.gr
+        self.own0 = self.gl * N                       # owned range start in the ext chain
+        self.ext_ndof = self.E_ext * N + 1
+        self.left = (rank - 1) % P if self.gl else None
+        self.right = (rank + 1) % P if self.gr else None
+        self.g_lo = self.e_lo * N                     # global index of the first owned node
+
+    def owned_slice(self):
+        return slice(self.own0, self.own0 + self.n_own)
+
+
+class HaloExchange:
+    """Ghost refresh of extended fields through torch.distributed point-to-point ops."""
+
+    def __init__(self, part, group=None):
+        self.p, self.group = part, group
+
+    def refresh(self, fields):
+        """Fill the ghost nodes of every extended field in ``fields`` (batched)."""
+        import torch
+        import torch.distributed as dist
+        p = self.p
+        if p.P == 1 or not fields:
+            return
+        N = p.N
+        o0, no = p.own0, p.n_own
+        k = len(fields)
+        ops = []
+        send_l = send_r = recv_l = recv_r = None
+        dev = fields[0].device
+        L = p.gl * N
+        if p.left is not None:      # my first N+1 owned nodes -> left neighbour's right ghost
+            send_l = torch.stack([f[o0:o0 + N + 1] for f in fields]).contiguous()
+            recv_l = torch.empty((k, L), dtype=torch.float64, device=dev)
+        if p.right is not None:     # my last 2N owned nodes -> right neighbour's left ghosts
+            send_r = torch.stack([f[o0 + no - 2 * N:o0 + no] for f in fields]).contiguous()
+            recv_r = torch.empty((k, N + 1), dtype=torch.float64, device=dev)
+        # fixed order (send_left, send_right, recv_right, recv_left) pairs the messages
+        # correctly even when left and right neighbour are the same rank (P = 2)
+        if send_l is not None:
+            ops.append(dist.P2POp(dist.isend, send_l, p.left, self.group, tag=1))
+        if send_r is not None:
+            ops.append(dist.P2POp(dist.isend, send_r, p.right, self.group, tag=2))
+        if recv_r is not None:
+            ops.append(dist.P2POp(dist.irecv, recv_r, p.right, self.group, tag=1))
+        if recv_l is not None:
+            ops.append(dist.P2POp(dist.irecv, recv_l, p.left, self.group, tag=2))
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+        for i, f in enumerate(fields):
+            if recv_l is not None:
+                f[0:L] = recv_l[i]
+            if recv_r is not None:
+                f[o0 + no:o0 + no + N + 1] = recv_r[i]
+
+
+def shard_grid(global_grid, part):
+    """The extended local chain of a partition as a Dirichlet grid with the global h
+    (a single rank keeps the global grid itself, periodic wrap included)."""
+    if part.P == 1:
+        return global_grid
+    ax = global_grid.axis
+    h = global_grid.h
+    xa = ax.xa + (part.e_lo - part.gl) * h
+    xb = xa + part.E_ext * h
+    return Grid([Axis(xa, xb, part.E_ext, ax.degree, DIRICHLET0)], element_length=h)
+
+
+class ShardedOperator:
+    """Drop-in for ``SemOperator`` on one rank of an element-sharded grid.
+
+    Fields are EXTENDED tensors (``ext_ndof`` entries, ghost nodes included);
+    ``field()`` accepts either the owned part (``n_own``) or an extended tensor,
+    ``public()`` returns the owned part.  ``local_factory(grid, coef)`` builds the
+    rank-local operator (the CUDA SemOperator by default; the CPU tests pass a
+    test double with the same launch interface)."""
+
+    def __init__(self, global_grid, coef, rank, world, group=None, local_factory=None, device=None):
+        self.global_grid = global_grid
+        self.coef = coef
+        self.part = Partition(global_grid.axis.elements, global_grid.axis.degree, world, rank,
+                              global_grid.periodic)
+        self.grid = shard_grid(global_grid, self.part)
+        if local_factory is None:
+            from .ops import SemOperator
+
+            def local_factory(g, c):
+                return SemOperator(g, c, device=device)
+        self.local = local_factory(self.grid, coef)
+        self.device = self.local.device
+        self.batch = 1
+        self.ndof = self.part.ext_ndof
+        self.shape = (self.ndof,)
+        self.halo = HaloExchange(self.part, group)
+        self.group = group
+        self.counters = self.local.counters
+        self.sync_checks = True
+        self.last_sweep_stats = {}
+        self.max_matrix_dim = self.local.max_matrix_dim
+        # owned-node mass pattern for the objective (global positions)
+        m = global_grid.mass_pattern
+        N = self.part.N
+        g = self.part.g_lo + np.arange(self.part.n_own)
+        pos = g % N
+        mass = m[pos].copy()
+        if not global_grid.periodic:
+            mass[g == 0] = m[N]
+            mass[g == global_grid.axis.elements * N] = m[N + 1]
+        import torch
+        self._mass_own = torch.as_tensor(mass, device=self.device)
+        mask = np.ones(self.part.n_own)
+        if not global_grid.periodic:
+            mask[g == 0] = 0.0
+            mask[g == global_grid.axis.elements * N] = 0.0
+        self._mask_own = torch.as_tensor(mask, device=self.device)
+
+    # -- fields -------------------------------------------------------------
+
+    def empty(self):
+        import torch
+        return torch.zeros(self.shape, dtype=torch.float64, device=self.device)
+
+    def field(self, x, name="field"):
+        import torch
+        host = not isinstance(x, torch.Tensor)
+        t = torch.as_tensor(np.asarray(x, dtype=np.float64) if host else x)
+        if t.dtype != torch.float64:
+            raise ValidationError(f"{name} must be float64, got {t.dtype}")
+        t = t.to(self.device)
+        if tuple(t.shape) == (self.part.n_own,):
+            e = self.empty()
+            e[self.part.owned_slice()] = t
+            self.halo.refresh([e])
+            return e, host
+        if tuple(t.shape) == self.shape:
+            return t.contiguous(), host
+        raise ValidationError(f"{name} has shape {tuple(t.shape)}, expected ({self.part.n_own},) "
+                              f"owned or {self.shape} extended")
+
+    def public(self, t):
+        return t[self.part.owned_slice()]
+
+    def _isfinite_all(self, t):
+        import torch
+        ok = torch.tensor([0.0 if bool(torch.isfinite(self.public(t)).all()) else 1.0],
+                          device=self.device)
+        self._allreduce(ok, "max")
+        return float(ok.item()) == 0.0
+
+    def _allreduce(self, t, op="sum"):
+        import torch.distributed as dist
+        if self.part.P > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX,
+                            group=self.group)
+        return t
+
+    def flags(self, reset=True):
+        """Device flags OR-ed over ranks, so every rank raises the same exception."""
+        import torch
+        v = self.local.flags(reset=reset)
+        t = torch.tensor([float(v)], device=self.device)
+        if self.part.P > 1:
+            bits = torch.tensor([float(v & b) > 0 for b in (1, 2, 4)], dtype=torch.float64,
+                                device=self.device)
+            self._allreduce(bits, "max")
+            v = sum(b for b, on in zip((1, 2, 4), bits.tolist()) if on)
+        del t
+        return int(v)
+
+    def dot(self, a, b):
+        """Global inner product of extended (or owned) fields: owned parts, all-reduced."""
+        import torch
+        a = self.public(a) if a.shape[-1] == self.ndof else a
+        b = self.public(b) if b.shape[-1] == self.ndof else b
+        t = torch.dot(a.reshape(-1), b.reshape(-1)).reshape(1)
+        return float(self._allreduce(t, "sum").item())
+
+    # -- launches: refresh what the kernel reads across element boundaries ------
+
+    def launch_rhs(self, u, out):
+        self.halo.refresh([u])
+        self.local.launch_rhs(u, out)
+
+    def launch_jac(self, u, v, out):
+        self.halo.refresh([u, v])
+        self.local.launch_jac(u, v, out)
+
+    def launch_jact(self, u, z, out):
+        self.halo.refresh([u, z])
+        self.local.launch_jact(u, z, out)
+
+    def launch_rk_stage(self, U_in, k_out, base, terms, coefs, dt, Y, check):
+        self.halo.refresh([U_in])
+        self.local.launch_rk_stage(U_in, k_out, base, terms, coefs, dt, Y, check)
+
+    def launch_adj_stage(self, U, lam, b, l_terms, a_coefs, dt, l_out, acc_terms, lam_out):
+        self.halo.refresh([U, lam] + list(l_terms))
+        self.local.launch_adj_stage(U, lam, b, l_terms, a_coefs, dt, l_out, acc_terms, lam_out)
+
+    def launch_terminal(self, uN, ud, lam, J_out):
+        """Objective on owned nodes, all-reduced; lam = mask(2 M d) (adjoint.py:39-47)."""
+        sl = self.part.owned_slice()
+        d = uN[sl] - ud[sl]
+        md = self._mass_own * d
+        lam.zero_()
+        lam[sl] = (2.0 * md) * self._mask_own
+        j = (d * md).sum().reshape(1)
+        J_out.copy_(self._allreduce(j, "sum"))
+
+    # -- reference surface ----------------------------------------------------
+
+    def apply_rhs(self, u):
+        ut, host = self.field(u, "state")
+        self.counters["rhs"] += 1
+        out = self.empty()
+        self.launch_rhs(ut, out)
+        self._raise(("state", "state"))
+        return self._ret(out, host)
+
+    def apply_jacobian(self, u, w):
+        ut, host = self.field(u, "state")
+        wt, _ = self.field(w, "tangent")
+        self.counters["jac"] += 1
+        out = self.empty()
+        self.launch_jac(ut, wt, out)
+        self._raise(("state", "tangent"))
+        return self._ret(out, host)
+
+    def apply_jacobian_transpose(self, u, z):
+        ut, host = self.field(u, "state")
+        zt, _ = self.field(z, "cotangent")
+        self.counters["jact"] += 1
+        out = self.empty()
+        self.launch_jact(ut, zt, out)
+        self._raise(("state", "cotangent"))
+        return self._ret(out, host)
+
+    def _raise(self, names):
+        from .errors import NumericFailure
+        v = self.flags()
+        if v & _lib.SEM1D_FLAG_STATE_NONFINITE:
+            raise NumericFailure(f"{names[0]} contains NaN/Inf")
+        if v & _lib.SEM1D_FLAG_INPUT2_NONFINITE:
+            raise NumericFailure(f"{names[1]} contains NaN/Inf")
+
+    def _ret(self, t, host):
+        o = self.public(t)
+        return o.cpu().numpy() if host else o
+
+
+def sharded_dot(op):
+    """The ``dot`` callable for :func:`optimize.minimize` on sharded fields."""
+    return op.dot
+
+
+def init_from_env(backend=None):
+    """torch.distributed init from torchrun's environment (MASTER_ADDR must be 127.0.0.1
+    on these boxes).  Returns (rank, world, local_rank)."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and not dist.is_initialized():
+        if backend is None:
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+    return rank, world, local
+
+
+__all__ = ["HaloExchange", "Partition", "ShardedOperator", "init_from_env", "shard_grid",
+           "sharded_dot", "PERIODIC"]

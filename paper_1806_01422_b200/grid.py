@@ -88,7 +88,9 @@ class Axis:
 class Grid:
     """1D mesh + assembly metadata.  Build through :func:`grid_1d`/:func:`build_grid`."""
 
-    def __init__(self, axes):
+    def __init__(self, axes, element_length=None):
+        """``element_length`` overrides (xb - xa) / E: a shard of a larger mesh must use
+        the global h bit for bit (K, M^-1 depend on it), whatever its local extent."""
         axes = tuple(axes)
         if len(axes) != 1:
             raise ValidationError(
@@ -106,7 +108,7 @@ class Grid:
         self.local_shape = (ax.degree + 1,)
         self.periodic = ax.bc == PERIODIC
         self.has_mask = not self.periodic
-        self.h = ax.element_length
+        self.h = ax.element_length if element_length is None else float(element_length)
         # per-position mass pattern (see include/sem1d.h): [0] interface,
         # [1..N-1] interior, [N] first / [N+1] last node of a Dirichlet grid.
         # bincount sums (0 + a) + b at an interface (grid.py:157-161); a + b is

@@ -110,7 +110,7 @@ class SemOperator:
         w = b.weights
         # constants exactly as ops.py:103-107
         self._dw = b.diff * w[:, None]
-        k = (2.0 / ax.element_length) * (b.diff.T * w) @ b.diff
+        k = (2.0 / grid.h) * (b.diff.T * w) @ b.diff
         self._kmat = 0.5 * (k + k.T)
         self._minv = grid.minv_pattern
         self.max_matrix_dim = ax.degree + 1

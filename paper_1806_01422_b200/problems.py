@@ -91,6 +91,8 @@ class AssimilationProblem:
         else:
             g = adjoint.sweep(self.op, self.ts, fwd, sched, lam)
         self.last_forward = fwd
+        if hasattr(self.op, "public") and tuple(np.shape(u0)) != tuple(g.shape):
+            g = self.op.public(g)       # sharded: owned part back for owned-part input
         if host:
             g = g.cpu().numpy()
         return j, g
