@@ -36,13 +36,17 @@ struct EnsArgs {
   Tableau tab;
 };
 
-template <int N>
+// warps per ring: the forward sweep runs best with 16 warps x 2 m-tiles (128 regs),
+// the backward sweep with 8 warps x 4 m-tiles (A/B on config 4, profiles/)
+template <int N, int WARPS = 8>
 struct EnsCfg {
   static constexpr int n = N + 1;
-  static constexpr int W = 8;                 // consumer warps
+  static constexpr int W = WARPS;
   static constexpr int THREADS = 32 * W;
   static constexpr int NT = n / 8, KC = n / 4;
 };
+constexpr int kEnsFwdWarps = 16;
+constexpr int kEnsAdjWarps = 8;
 
 // One operator application over the whole ring held in shared memory.
 // src: node values (ndof + 1 entries; entry ndof mirrors node 0 if periodic).
@@ -109,17 +113,17 @@ __device__ __forceinline__ void ring_rhs(const Consts<N>& C, const Geo& G, const
 // Forward sweep of one ring per CTA: periodic rings, E a multiple of 8 with
 // E/8 <= 8 * WMT_MAX.  Trajectory state n+1 is written after step n.
 template <int N, int WMT_MAX>
-__global__ void __launch_bounds__(EnsCfg<N>::THREADS, 1)
+__global__ void __launch_bounds__(EnsCfg<N, kEnsFwdWarps>::THREADS, 1)
     ens_forward_kernel(const __grid_constant__ Consts<N> C, const Geo G, const EnsArgs A) {
   constexpr int n = N + 1, KC = EnsCfg<N>::KC, NT = EnsCfg<N>::NT;
-  constexpr int THREADS = EnsCfg<N>::THREADS;
+  constexpr int THREADS = EnsCfg<N, kEnsFwdWarps>::THREADS;
   extern __shared__ __align__(16) double smem[];
   const int ndof = (int)G.ndof;
   const int pad = (ndof + 2 + 1) & ~1;        // ndof + mirror node, 16-byte multiple
   double* su = smem;                          // base state u_n
   double* sU = su + pad;                      // current stage input
   double* sk = sU + pad;                      // stored slope k_0 (RK3 only)
-  double* xfer = sk + pad;                    // [8] warp exchange
+  double* xfer = sk + pad;                    // [W] warp exchange
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kq = lane & 3, rr = lane >> 2;
   const int64_t b = blockIdx.x;
@@ -284,10 +288,10 @@ struct EnsAdjArgs {
 // l_i = dt J^T(U_i)(b_i lam + sum_{j>i} a_ji l_j) for i = s-1..0 and
 // lam <- lam + (l_{s-1} + ... + l_0).
 template <int N, int WMT_MAX>
-__global__ void __launch_bounds__(EnsCfg<N>::THREADS, 1)
+__global__ void __launch_bounds__(EnsCfg<N, kEnsAdjWarps>::THREADS, 1)
     ens_adjoint_kernel(const __grid_constant__ Consts<N> C, const Geo G, const EnsAdjArgs A) {
   constexpr int KC = EnsCfg<N>::KC, NT = EnsCfg<N>::NT;
-  constexpr int THREADS = EnsCfg<N>::THREADS;
+  constexpr int THREADS = EnsCfg<N, kEnsAdjWarps>::THREADS;
   extern __shared__ __align__(16) double smem[];
   const int ndof = (int)G.ndof;
   const int pad = (ndof + 2 + 1) & ~1;
@@ -410,12 +414,12 @@ __global__ void __launch_bounds__(EnsCfg<N>::THREADS, 1)
 
 template <int N>
 constexpr size_t ens_adj_smem_bytes(int ndof) {
-  return sizeof(double) * (7 * (size_t)((ndof + 2 + 1) & ~1) + 8);
+  return sizeof(double) * (7 * (size_t)((ndof + 2 + 1) & ~1) + 32);
 }
 
 template <int N>
 constexpr size_t ens_smem_bytes(int ndof) {
-  return sizeof(double) * (3 * (size_t)((ndof + 2 + 1) & ~1) + 8);
+  return sizeof(double) * (3 * (size_t)((ndof + 2 + 1) & ~1) + 32);
 }
 
 }  // namespace sem1d

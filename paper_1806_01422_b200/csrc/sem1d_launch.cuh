@@ -187,14 +187,15 @@ cudaError_t launch_ens_adjoint(const PlanView& p, const EnsAdjArgs& a, cudaStrea
   if constexpr ((N + 1) % 8 != 0) {
     return cudaErrorNotSupported;
   } else {
-    constexpr int WMT = 4;
-    if (!p.geo.periodic || p.geo.E % 8 != 0 || p.geo.E / 8 > 8 * WMT) return cudaErrorNotSupported;
+    constexpr int W = kEnsAdjWarps;
+    constexpr int WMT = 32 / W;
+    if (!p.geo.periodic || p.geo.E % 8 != 0 || p.geo.E / 8 > W * WMT) return cudaErrorNotSupported;
     const size_t smem = ens_adj_smem_bytes<N>((int)p.geo.ndof);
     if (smem > 226 * 1024) return cudaErrorNotSupported;
     auto kern = ens_adjoint_kernel<N, WMT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)p.batch, EnsCfg<N>::THREADS, smem, s>>>(*static_cast<const Consts<N>*>(p.consts),
+    kern<<<(unsigned)p.batch, EnsCfg<N, W>::THREADS, smem, s>>>(*static_cast<const Consts<N>*>(p.consts),
                                                              p.geo, a);
     return cudaGetLastError();
   }
@@ -206,14 +207,15 @@ cudaError_t launch_ens_forward(const PlanView& p, const EnsArgs& a, cudaStream_t
   if constexpr ((N + 1) % 8 != 0) {
     return cudaErrorNotSupported;
   } else {
-    constexpr int WMT = 4;
-    if (!p.geo.periodic || p.geo.E % 8 != 0 || p.geo.E / 8 > 8 * WMT) return cudaErrorNotSupported;
+    constexpr int W = kEnsFwdWarps;
+    constexpr int WMT = 32 / W;
+    if (!p.geo.periodic || p.geo.E % 8 != 0 || p.geo.E / 8 > W * WMT) return cudaErrorNotSupported;
     const size_t smem = ens_smem_bytes<N>((int)p.geo.ndof);
     if (smem > 220 * 1024) return cudaErrorNotSupported;
     auto kern = ens_forward_kernel<N, WMT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)p.batch, EnsCfg<N>::THREADS, smem, s>>>(*static_cast<const Consts<N>*>(p.consts),
+    kern<<<(unsigned)p.batch, EnsCfg<N, W>::THREADS, smem, s>>>(*static_cast<const Consts<N>*>(p.consts),
                                                              p.geo, a);
     return cudaGetLastError();
   }

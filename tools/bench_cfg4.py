@@ -12,7 +12,7 @@ from paper_1806_01422_b200 import adjoint, configs, timeloop  # noqa: E402
 
 
 def main(B=4096, steps=1000, cpu_sample=2):
-    B, steps = int(B), int(steps)
+    B, steps, cpu_sample = int(B), int(steps), int(cpu_sample)
     prob = configs.cfg4_problem(B=B, steps=steps, device="cuda:0")
     op = prob.op
     u0 = torch.from_numpy(prob.u_guess).cuda()
