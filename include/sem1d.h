@@ -119,8 +119,10 @@ int sem1d_adj_stage(const sem1d_plan* plan, const double* U, const double* lam, 
  * NULL) and the last state to u_final.  flags[b] gets
  * SEM1D_FLAG_STEP_NONFINITE if any new state of problem b was non-finite
  * (the reference's StepFailure, timeloop.py:129; no dt retry in the batched
- * sweep -- the host re-runs failing problems).  Periodic rings with N+1 a
- * multiple of 8 and E a multiple of 8 (E <= 256) only. */
+ * sweep -- the host re-runs failing problems).  Rings must fit one CTA:
+ * E*(N+1) <= 1024 (any degree, periodic or Dirichlet; one thread per element
+ * row), or periodic with N+1 a multiple of 8 and E a multiple of 8, E <= 256
+ * (FP64 tensor-core ring kernel). */
 int sem1d_ens_forward(const sem1d_plan* plan, const double* u0, double* traj, double* u_final,
                       const double* dts, int nsteps, int scheme, int* flags, void* stream);
 

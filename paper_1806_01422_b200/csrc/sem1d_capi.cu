@@ -396,8 +396,8 @@ int sem1d_ens_forward(const sem1d_plan* plan, const double* u0, double* traj, do
   a.u0 = u0; a.traj = traj; a.u_final = u_final; a.dts = dts; a.nsteps = nsteps; a.flags = flags;
   cudaError_t e = dispatch_ens_forward(plan, a, static_cast<cudaStream_t>(stream));
   if (e == cudaErrorNotSupported)
-    return fail(SEM1D_EINVAL, "sem1d_ens_forward: needs periodic rings, N+1 in {8,16,24,32}, "
-                              "E a multiple of 8 (E <= 256) that fit in shared memory");
+    return fail(SEM1D_EINVAL, "sem1d_ens_forward: ring too large for one CTA (needs E*(N+1) <= 1024, "
+                              "or periodic, N+1 in {8,16,24,32}, E a multiple of 8, E <= 256)");
   if (e != cudaSuccess) return cuda_fail(e, "sem1d_ens_forward");
   return SEM1D_OK;
 }
@@ -413,8 +413,8 @@ int sem1d_ens_adjoint(const sem1d_plan* plan, const double* traj, const double* 
   a.traj = traj; a.lam_in = lam_in; a.lam_out = lam_out; a.dts = dts; a.nsteps = nsteps; a.flags = flags;
   cudaError_t e = dispatch_ens_adjoint(plan, a, static_cast<cudaStream_t>(stream));
   if (e == cudaErrorNotSupported)
-    return fail(SEM1D_EINVAL, "sem1d_ens_adjoint: needs periodic rings, N+1 in {8,16,24,32}, "
-                              "E a multiple of 8 (E <= 256) that fit in shared memory");
+    return fail(SEM1D_EINVAL, "sem1d_ens_adjoint: ring too large for one CTA (needs E*(N+1) <= 1024, "
+                              "or periodic, N+1 in {8,16,24,32}, E a multiple of 8, E <= 256)");
   if (e != cudaSuccess) return cuda_fail(e, "sem1d_ens_adjoint");
   return SEM1D_OK;
 }

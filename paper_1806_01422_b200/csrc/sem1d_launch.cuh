@@ -7,6 +7,7 @@
 
 #include "sem1d_device.cuh"
 #include "sem1d_ensemble.cuh"
+#include "sem1d_smallring.cuh"
 
 namespace sem1d {
 
@@ -181,44 +182,74 @@ cudaError_t launch_apply(const PlanView& p, int kind, const Args& a, cudaStream_
 template <int N>
 constexpr size_t consts_size() { return sizeof(Consts<N>); }
 
-// Ring-resident ensemble backward sweep (one CTA per ring).
+// Small rings (E*(N+1) <= 1024): one thread per (element, row), any degree and
+// boundary kind, whole sweep per launch.
 template <int N>
-cudaError_t launch_ens_adjoint(const PlanView& p, const EnsAdjArgs& a, cudaStream_t s) {
-  if constexpr ((N + 1) % 8 != 0) {
-    return cudaErrorNotSupported;
-  } else {
-    constexpr int W = kEnsAdjWarps;
-    constexpr int WMT = 32 / W;
-    if (!p.geo.periodic || p.geo.E % 8 != 0 || p.geo.E / 8 > W * WMT) return cudaErrorNotSupported;
-    const size_t smem = ens_adj_smem_bytes<N>((int)p.geo.ndof);
-    if (smem > 226 * 1024) return cudaErrorNotSupported;
-    auto kern = ens_adjoint_kernel<N, WMT>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+static cudaError_t launch_small(const PlanView& p, const EnsArgs* fa, const EnsAdjArgs* aa,
+                                cudaStream_t s) {
+  const int n = N + 1;
+  const int64_t threads = ((p.geo.E * n + 31) / 32) * 32;
+  if (threads > 1024) return cudaErrorNotSupported;
+  SmallGeo sg;
+  sg.E = (int)p.geo.E; sg.N = N; sg.ndof = (int)p.geo.ndof; sg.periodic = p.geo.periodic;
+  const Consts<N>& C = *static_cast<const Consts<N>*>(p.consts);
+  if (fa) {
+    const size_t smem = small_fwd_smem(N, sg.ndof, sg.E);
+    if (smem > 220 * 1024) return cudaErrorNotSupported;
+    cudaError_t e = cudaFuncSetAttribute(small_forward_kernel<N>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    kern<<<(unsigned)p.batch, EnsCfg<N, W>::THREADS, smem, s>>>(*static_cast<const Consts<N>*>(p.consts),
-                                                             p.geo, a);
-    return cudaGetLastError();
+    small_forward_kernel<N><<<(unsigned)p.batch, (unsigned)threads, smem, s>>>(C, sg, *fa);
+  } else {
+    const size_t smem = small_adj_smem(N, sg.ndof, sg.E);
+    if (smem > 220 * 1024) return cudaErrorNotSupported;
+    cudaError_t e = cudaFuncSetAttribute(small_adjoint_kernel<N>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    small_adjoint_kernel<N><<<(unsigned)p.batch, (unsigned)threads, smem, s>>>(C, sg, *aa);
   }
+  return cudaGetLastError();
 }
 
-// Ring-resident ensemble forward sweep (one CTA per ring).
+// Ring-resident backward sweep: DMMA ring kernel for n % 8 == 0 periodic rings of
+// <= 256 elements, else the small-ring kernel when E*(N+1) <= 1024.
+template <int N>
+cudaError_t launch_ens_adjoint(const PlanView& p, const EnsAdjArgs& a, cudaStream_t s) {
+  if constexpr ((N + 1) % 8 == 0) {
+    constexpr int W = kEnsAdjWarps;
+    constexpr int WMT = 32 / W;
+    const size_t smem = ens_adj_smem_bytes<N>((int)p.geo.ndof);
+    if (p.geo.periodic && p.geo.E % 8 == 0 && p.geo.E / 8 <= W * WMT && smem <= 226 * 1024 &&
+        p.geo.E * (N + 1) > 1024) {
+      auto kern = ens_adjoint_kernel<N, WMT>;
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      kern<<<(unsigned)p.batch, EnsCfg<N, W>::THREADS, smem, s>>>(
+          *static_cast<const Consts<N>*>(p.consts), p.geo, a);
+      return cudaGetLastError();
+    }
+  }
+  return launch_small<N>(p, nullptr, &a, s);
+}
+
+// Ring-resident forward sweep (same selection as the backward sweep).
 template <int N>
 cudaError_t launch_ens_forward(const PlanView& p, const EnsArgs& a, cudaStream_t s) {
-  if constexpr ((N + 1) % 8 != 0) {
-    return cudaErrorNotSupported;
-  } else {
+  if constexpr ((N + 1) % 8 == 0) {
     constexpr int W = kEnsFwdWarps;
     constexpr int WMT = 32 / W;
-    if (!p.geo.periodic || p.geo.E % 8 != 0 || p.geo.E / 8 > W * WMT) return cudaErrorNotSupported;
     const size_t smem = ens_smem_bytes<N>((int)p.geo.ndof);
-    if (smem > 220 * 1024) return cudaErrorNotSupported;
-    auto kern = ens_forward_kernel<N, WMT>;
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    kern<<<(unsigned)p.batch, EnsCfg<N, W>::THREADS, smem, s>>>(*static_cast<const Consts<N>*>(p.consts),
-                                                             p.geo, a);
-    return cudaGetLastError();
+    if (p.geo.periodic && p.geo.E % 8 == 0 && p.geo.E / 8 <= W * WMT && smem <= 220 * 1024 &&
+        p.geo.E * (N + 1) > 1024) {
+      auto kern = ens_forward_kernel<N, WMT>;
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      kern<<<(unsigned)p.batch, EnsCfg<N, W>::THREADS, smem, s>>>(
+          *static_cast<const Consts<N>*>(p.consts), p.geo, a);
+      return cudaGetLastError();
+    }
   }
+  return launch_small<N>(p, &a, nullptr, s);
 }
 
 }  // namespace sem1d

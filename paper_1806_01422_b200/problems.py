@@ -74,13 +74,18 @@ class AssimilationProblem:
         u0_dev, host = self.op.field(u0, "initial state")
         m = timeloop.count_steps(self.ts)
         sched = self.schedule_for(m)
-        if self.op.batch > 1 and self.checkpoint_slots is None and self.use_ensemble:
-            # many small rings: ring-resident forward sweep, trajectory in HBM
+        fwd = None
+        if (self.use_ensemble and self.checkpoint_slots is None
+                and hasattr(self.op, "launch_ens_forward")
+                and timeloop.ring_resident_supported(self.op)):
+            # the ring fits one CTA: whole forward sweep in one launch, trajectory in HBM
             fwd = timeloop.integrate_ensemble(self.op, u0_dev, self.ts)
             if fwd.stats["failed"]:
-                from .errors import StepFailure
-                raise StepFailure(f"non-finite state in problems {fwd.stats['failed'][:8]}")
-        else:
+                if self.op.batch > 1:
+                    from .errors import StepFailure
+                    raise StepFailure(f"non-finite state in problems {fwd.stats['failed'][:8]}")
+                fwd = None   # re-run stepwise: exact reference retry / exception semantics
+        if fwd is None:
             fwd = timeloop.integrate(self.op, u0_dev, self.ts,
                                      store_steps=sched.forward_stores.keys())
         if fwd.n_steps != m:  # a StepFailure retry changed the time grid

@@ -314,6 +314,15 @@ def fixed_step_sizes(cfg):
     return dts
 
 
+def ring_resident_supported(op):
+    """Whether the whole ring fits one CTA (mirrors launch_ens_forward in csrc)."""
+    ax = op.grid.axis
+    E, n = ax.elements, ax.degree + 1
+    if E * n <= 1024:
+        return True
+    return bool(op.grid.periodic and n % 8 == 0 and E % 8 == 0 and E <= 256)
+
+
 def integrate_ensemble(op, u0, cfg, store_trajectory=True):
     """Forward sweep of a batch of independent rings, one CTA per ring, every step in
     shared memory (sem1d_ens_forward).  Same dt sequence and step arithmetic as
@@ -333,6 +342,7 @@ def integrate_ensemble(op, u0, cfg, store_trajectory=True):
     u_final = op.empty()
     flags = torch.zeros(op.batch, dtype=torch.int32, device=op.device)
     op.launch_ens_forward(u.contiguous(), traj, u_final, dts_dev, m, cfg.scheme, flags)
+    op.counters["rhs"] += len(TABLEAUX[cfg.scheme][1]) * m
     fl = flags.cpu()
     failed = [int(i) for i in torch.nonzero(fl).flatten()]
     snapshots = {n: traj[n] for n in range(m + 1)} if traj is not None else {0: u.clone()}

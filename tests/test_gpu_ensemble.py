@@ -79,3 +79,30 @@ def test_ensemble_adjoint_vs_stage_sweep(cuda, scheme, E, N):
         j_ref, g_ref, _ = R.evaluate(ref, u0[b], ud[b], 0.0, steps * dt, dt, scheme)
         assert abs(float(J[b]) - j_ref) <= 1e-9 * abs(j_ref)
         assert rel_err(g_ens[b].cpu().numpy(), g_ref) <= 1e-9
+
+
+@pytest.mark.parametrize("scheme", ["rk4", "rk3", "euler"])
+@pytest.mark.parametrize("bc", ["periodic", "dirichlet0"])
+@pytest.mark.parametrize("E,N", [(16, 9), (5, 2), (40, 12), (3, 31)])
+def test_small_ring_sweeps_vs_oracle(cuda, scheme, bc, E, N):
+    """Small rings (E*(N+1) <= 1024, any degree / boundary kind): one launch per sweep."""
+    from paper_1806_01422_b200 import adjoint
+    B, steps, dt = 3, 15, 1e-5       # explicit limit ~3e-5 for E=40, N=12 on [-1, 1]
+    grid = grid_1d(-1.0, 1.0, E, N, bc)
+    op = sb.SemOperator(grid, sb.PdeCoefficients(0.01), device="cuda:0", batch=B)
+    rng = np.random.default_rng(E * N)
+    x = grid.node_coordinates()[0]
+    u0 = np.stack([grid.mask(np.sin(np.pi * x) + 0.05 * rng.standard_normal(grid.nglobal))
+                   for _ in range(B)])
+    ud = np.stack([grid.mask(np.sin(np.pi * x + 0.3)) for _ in range(B)])
+    ts = sb.TsConfig(scheme=scheme, t0=0.0, t_end=steps * dt, dt=dt)
+    fwd = timeloop.integrate_ensemble(op, u0, ts)
+    assert not fwd.stats["failed"]
+    J, lam = adjoint.terminal_condition(grid, fwd.u_final, torch.from_numpy(ud).cuda(), op=op)
+    g = adjoint.ensemble_sweep(op, ts, fwd, lam)
+    ref = R.BurgersOracle(R.Mesh1D(-1.0, 1.0, E, N, bc == "periodic"), 0.01)
+    for b in range(B):
+        j_ref, g_ref, uf = R.evaluate(ref, u0[b], ud[b], 0.0, steps * dt, dt, scheme)
+        assert rel_err(fwd.u_final[b].cpu().numpy(), uf) <= 1e-12
+        assert abs(float(J[b]) - j_ref) <= 1e-9 * abs(j_ref)
+        assert rel_err(g[b].cpu().numpy(), g_ref) <= 1e-9
