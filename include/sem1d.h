@@ -135,6 +135,21 @@ int sem1d_ens_adjoint(const sem1d_plan* plan, const double* traj, const double* 
                       double* lam_out, const double* dts, int nsteps, int scheme, int* flags,
                       void* stream);
 
+/* Temporally blocked steps for large periodic rings (batch 1, N+1 in
+ * {8,16,24,32}, at least two 256/128-element tiles): ONE launch per explicit
+ * step u -> u_new (all stages of timeloop.py:111-130 in shared memory, 16 B/DOF
+ * of HBM traffic) and ONE launch per adjoint step lam -> lam_out (stage states
+ * recomputed from u, stage-adjoint chain of adjoint.py:54-61 in shared memory,
+ * 24 B/DOF).  Each CTA recomputes s (forward) or 2s-1 (adjoint) ghost elements
+ * per side of its tile.  Outputs must not alias inputs.  Flags as for
+ * sem1d_rk_stage / sem1d_adj_stage.  sem1d_step_supported(plan) tells whether
+ * the plan qualifies. */
+int sem1d_step_supported(const sem1d_plan* plan);
+int sem1d_rk_step(const sem1d_plan* plan, const double* u, double* u_new, double dt, int scheme,
+                  int* flag, void* stream);
+int sem1d_adj_step(const sem1d_plan* plan, const double* u, const double* lam, double* lam_out,
+                   double dt, int scheme, int* flag, void* stream);
+
 /* Terminal condition (adjoint.py:33-47): d = uN - ud, lam = mask(2 M d),
  * J_out[b] = d^T M d per batch member (deterministic two-level reduction;
  * `work` must hold sem1d_terminal_work_size(plan) doubles). */

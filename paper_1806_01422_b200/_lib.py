@@ -44,6 +44,10 @@ SIGNATURES = {
                                   c_void_p, c_void_p]),
     "sem1d_ens_adjoint": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int,
                                   c_void_p, c_void_p]),
+    "sem1d_step_supported": (c_int, [c_void_p]),
+    "sem1d_rk_step": (c_int, [c_void_p, c_void_p, c_void_p, c_double, c_int, c_void_p, c_void_p]),
+    "sem1d_adj_step": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int, c_void_p,
+                               c_void_p]),
     "sem1d_terminal_work_size": (c_int64, [c_void_p]),
     "sem1d_terminal": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "sem1d_scatter": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),

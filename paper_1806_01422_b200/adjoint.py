@@ -48,8 +48,8 @@ class AdjointEngine:
         A, b = TABLEAUX[scheme]
         self.A, self.b, self.s = A, b, len(b)
         self.fwd = engine_for(op, scheme)
-        self.U = [op.empty() for _ in range(self.s - 1)]
-        self.L = {i: op.empty() for i in range(1, self.s)}
+        self._U = None
+        self._L = None
         # z-combination terms of stage i: (a_ji, j) for j > i with a_ji != 0
         self.zterms = []
         for i in range(self.s):
@@ -60,9 +60,27 @@ class AdjointEngine:
                     terms.append((j, float(a)))
             self.zterms.append(terms)
 
+    @property
+    def U(self):   # per-stage scratch, allocated only if the per-stage path runs
+        if self._U is None:
+            self._U = [self.op.empty() for _ in range(self.s - 1)]
+        return self._U
+
+    @property
+    def L(self):
+        if self._L is None:
+            self._L = {i: self.op.empty() for i in range(1, self.s)}
+        return self._L
+
     def step(self, u_n, lam, dt, lam_out):
         """lam_out = transpose of the step map at u_n applied to lam (no host sync)."""
         op, s = self.op, self.s
+        fused = getattr(op, "step_fused_supported", None)
+        if fused is not None and fused():
+            op.launch_adj_step(u_n, lam, lam_out, dt, self.scheme)
+            op.counters["rhs"] += s - 1
+            op.counters["jact"] += s
+            return
         Us = self.fwd.stages(u_n, dt, self.U) if s > 1 else [u_n]
         for i in range(s - 1, -1, -1):
             lts = [self.L[j] for j, _ in self.zterms[i]]

@@ -18,7 +18,8 @@ namespace sem1d {
 #define SEM_DECL(NN) \
   extern template cudaError_t launch_apply<NN>(const PlanView&, int, const Args&, cudaStream_t); \
   extern template cudaError_t launch_ens_forward<NN>(const PlanView&, const EnsArgs&, cudaStream_t); \
-  extern template cudaError_t launch_ens_adjoint<NN>(const PlanView&, const EnsAdjArgs&, cudaStream_t);
+  extern template cudaError_t launch_ens_adjoint<NN>(const PlanView&, const EnsAdjArgs&, cudaStream_t); \
+  extern template cudaError_t launch_tile_step<NN>(const PlanView&, int, TileStepArgs, cudaStream_t);
 SEM_DECL(1) SEM_DECL(2) SEM_DECL(3) SEM_DECL(4) SEM_DECL(5) SEM_DECL(6) SEM_DECL(7) SEM_DECL(8)
 SEM_DECL(9) SEM_DECL(10) SEM_DECL(11) SEM_DECL(12) SEM_DECL(13) SEM_DECL(14) SEM_DECL(15)
 SEM_DECL(16) SEM_DECL(17) SEM_DECL(18) SEM_DECL(19) SEM_DECL(20) SEM_DECL(21) SEM_DECL(22)
@@ -99,6 +100,21 @@ cudaError_t dispatch_ens_adjoint(const sem1d_plan* p, const EnsAdjArgs& a, cudaS
   switch (p->N) {
 #define SEM_CASE(NN) \
   case NN: return launch_ens_adjoint<NN>(v, a, s);
+    SEM_CASE(1) SEM_CASE(2) SEM_CASE(3) SEM_CASE(4) SEM_CASE(5) SEM_CASE(6) SEM_CASE(7)
+    SEM_CASE(8) SEM_CASE(9) SEM_CASE(10) SEM_CASE(11) SEM_CASE(12) SEM_CASE(13) SEM_CASE(14)
+    SEM_CASE(15) SEM_CASE(16) SEM_CASE(17) SEM_CASE(18) SEM_CASE(19) SEM_CASE(20) SEM_CASE(21)
+    SEM_CASE(22) SEM_CASE(23) SEM_CASE(24) SEM_CASE(25) SEM_CASE(26) SEM_CASE(27) SEM_CASE(28)
+    SEM_CASE(29) SEM_CASE(30) SEM_CASE(31) SEM_CASE(32)
+#undef SEM_CASE
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t dispatch_tile(const sem1d_plan* p, int kind, const TileStepArgs& a, cudaStream_t s) {
+  const PlanView v = view(p);
+  switch (p->N) {
+#define SEM_CASE(NN) \
+  case NN: return launch_tile_step<NN>(v, kind, a, s);
     SEM_CASE(1) SEM_CASE(2) SEM_CASE(3) SEM_CASE(4) SEM_CASE(5) SEM_CASE(6) SEM_CASE(7)
     SEM_CASE(8) SEM_CASE(9) SEM_CASE(10) SEM_CASE(11) SEM_CASE(12) SEM_CASE(13) SEM_CASE(14)
     SEM_CASE(15) SEM_CASE(16) SEM_CASE(17) SEM_CASE(18) SEM_CASE(19) SEM_CASE(20) SEM_CASE(21)
@@ -416,6 +432,42 @@ int sem1d_ens_adjoint(const sem1d_plan* plan, const double* traj, const double* 
     return fail(SEM1D_EINVAL, "sem1d_ens_adjoint: ring too large for one CTA (needs E*(N+1) <= 1024, "
                               "or periodic, N+1 in {8,16,24,32}, E a multiple of 8, E <= 256)");
   if (e != cudaSuccess) return cuda_fail(e, "sem1d_ens_adjoint");
+  return SEM1D_OK;
+}
+
+int sem1d_step_supported(const sem1d_plan* plan) {
+  if (!valid_plan(plan)) return 0;
+  const int te = ((plan->N + 1) == 8) ? 256 : ((plan->N + 1) == 32 ? 64 : 128);
+  return (plan->periodic && plan->batch == 1 && (plan->N + 1) % 8 == 0 && plan->E >= 2 * te) ? 1 : 0;
+}
+
+int sem1d_rk_step(const sem1d_plan* plan, const double* u, double* u_new, double dt, int scheme,
+                  int* flag, void* stream) {
+  if (!valid_plan(plan) || !u || !u_new || !flag || u == u_new)
+    return fail(SEM1D_EINVAL, "sem1d_rk_step: bad argument (u_new must not alias u)");
+  TileStepArgs a;
+  std::memset(&a, 0, sizeof(a));
+  if (!make_tableau(scheme, a.tab)) return fail(SEM1D_EINVAL, "sem1d_rk_step: unknown scheme");
+  a.u = u; a.out = u_new; a.flag = flag; a.dt = dt;
+  cudaError_t e = dispatch_tile(plan, 0, a, static_cast<cudaStream_t>(stream));
+  if (e == cudaErrorNotSupported)
+    return fail(SEM1D_EINVAL, "sem1d_rk_step: needs a periodic batch-1 ring, N+1 in {8,16,24,32}, E >= 2 tiles");
+  if (e != cudaSuccess) return cuda_fail(e, "sem1d_rk_step");
+  return SEM1D_OK;
+}
+
+int sem1d_adj_step(const sem1d_plan* plan, const double* u, const double* lam, double* lam_out,
+                   double dt, int scheme, int* flag, void* stream) {
+  if (!valid_plan(plan) || !u || !lam || !lam_out || !flag || lam == lam_out)
+    return fail(SEM1D_EINVAL, "sem1d_adj_step: bad argument (lam_out must not alias lam)");
+  TileStepArgs a;
+  std::memset(&a, 0, sizeof(a));
+  if (!make_tableau(scheme, a.tab)) return fail(SEM1D_EINVAL, "sem1d_adj_step: unknown scheme");
+  a.u = u; a.lam = lam; a.out = lam_out; a.flag = flag; a.dt = dt;
+  cudaError_t e = dispatch_tile(plan, 1, a, static_cast<cudaStream_t>(stream));
+  if (e == cudaErrorNotSupported)
+    return fail(SEM1D_EINVAL, "sem1d_adj_step: needs a periodic batch-1 ring, N+1 in {8,16,24,32}, E >= 2 tiles");
+  if (e != cudaSuccess) return cuda_fail(e, "sem1d_adj_step");
   return SEM1D_OK;
 }
 

@@ -52,7 +52,7 @@ constexpr int kEnsAdjWarps = 8;
 // src: node values (ndof + 1 entries; entry ndof mirrors node 0 if periodic).
 // Output: kv[q][kc] = (M^-1-scaled) F at the nodes owned by this lane, for
 // m-tile q of this warp (node 4kc+kq of element 8*(warp + q*W) + rr ... see body).
-template <int N, int WMT_MAX, class BGet>
+template <int N, int WMT_MAX, class BGet, bool WRAP = true>
 __device__ __forceinline__ void ring_rhs(const Consts<N>& C, const Geo& G, const double* src,
                                          double* xfer, BGet bget, const double* minv_a,
                                          double mnu, int warp, int lane,
@@ -102,9 +102,10 @@ __device__ __forceinline__ void ring_rhs(const Consts<N>& C, const Geo& G, const
   if (lane == 31 && warp * WMT_MAX < mt_total) xfer[warp] = carry;   // row N of the warp's last element
   __syncthreads();
   if (lane == 0 && warp * WMT_MAX < mt_total) {
-    // left neighbour of the warp's first element: previous warp (ring wrap from the last)
-    const int wl = (warp == 0) ? (mt_total - 1) / WMT_MAX : warp - 1;
-    double v = __dadd_rn(xfer[wl], row0_first);
+    // left neighbour of the warp's first element: previous warp (ring wrap from the last;
+    // an open chain's first node stays incomplete -- it lies in the ghost margin)
+    const int wl = (warp == 0) ? (WRAP ? (mt_total - 1) / WMT_MAX : -1) : warp - 1;
+    const double v = wl >= 0 ? __dadd_rn(xfer[wl], row0_first) : row0_first;
     kv[0][0] = __dmul_rn(v, minv_a[0]);
   }
   (void)W;
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(EnsCfg<N, kEnsFwdWarps>::THREADS, 1)
 // J^T over the ring held in shared memory: usrc = linearisation point, zsrc =
 // zm = mask(z M^-1) already scaled (ops.py:252-254).  Output (no M^-1, ops.py:256):
 // jv[q][kc] at the nodes owned by this lane, interface nodes summed.
-template <int N, int WMT_MAX, class BGet>
+template <int N, int WMT_MAX, class BGet, bool WRAP = true>
 __device__ __forceinline__ void ring_jact(const Consts<N>& C, const Geo& G, const double* usrc,
                                           const double* zsrc, double* xfer, BGet bget,
                                           double mnu, int warp, int lane,
@@ -268,8 +269,8 @@ __device__ __forceinline__ void ring_jact(const Consts<N>& C, const Geo& G, cons
   if (lane == 31 && warp * WMT_MAX < mt_total) xfer[warp] = carry;
   __syncthreads();
   if (lane == 0 && warp * WMT_MAX < mt_total) {
-    const int wl = (warp == 0) ? (mt_total - 1) / WMT_MAX : warp - 1;
-    jv[0][0] = __dadd_rn(xfer[wl], row0_first);
+    const int wl = (warp == 0) ? (WRAP ? (mt_total - 1) / WMT_MAX : -1) : warp - 1;
+    jv[0][0] = wl >= 0 ? __dadd_rn(xfer[wl], row0_first) : row0_first;
   }
 }
 
@@ -416,6 +417,336 @@ template <int N>
 constexpr size_t ens_adj_smem_bytes(int ndof) {
   return sizeof(double) * (7 * (size_t)((ndof + 2 + 1) & ~1) + 32);
 }
+
+// ============================================================================
+// Temporally blocked steps for LARGE periodic rings.  A CTA takes a tile of TE
+// = 8*W*WMT consecutive elements, of which the outer H on each side are ghost
+// elements recomputed from the neighbouring tiles' data: H = s for a forward
+// step (the valid range shrinks by one element per stage), H = 2s-1 for an
+// adjoint step (s-1 stage recomputes + s transposed applies).  Everything
+// between the tile load and the store of the central TE-2H elements stays in
+// shared memory, so one RK step moves 16 B/DOF and one adjoint step 24 B/DOF
+// (plus the ghost margin) instead of one HBM round trip per stage.
+// ============================================================================
+
+struct TileStepArgs {
+  const double* u;        // state u_n (forward input / adjoint linearisation point)
+  const double* lam;      // adjoint: lam_{n+1}
+  double* out;            // forward: u_{n+1}; adjoint: lam_n
+  int* flag;
+  double dt;
+  int H;                  // ghost elements per side
+  int ntiles;             // ceil(E / (TE - 2H))
+  Tableau tab;
+};
+
+// Tile loader shared by the step kernels: interior tiles arrive by one bulk
+// copy (issued one tile ahead, completion on an mbarrier); tiles whose node
+// range wraps around the ring end are loaded synchronously by the whole CTA.
+struct TileLoad {
+  int64_t g0;      // first node (mod ndof)
+  int sh;          // 16-byte alignment shift of the smem copy
+  bool bulk;       // loaded by cp.async.bulk
+};
+
+__device__ __forceinline__ TileLoad tile_load_plan(int t, int T, int H, int N, int LEN, int64_t ndof) {
+  TileLoad L;
+  int64_t g0 = (((int64_t)t * T - H) * N) % ndof;
+  if (g0 < 0) g0 += ndof;
+  L.g0 = g0;
+  L.sh = (int)(g0 & 1);
+  const int64_t a0 = g0 - L.sh;
+  const int64_t bytes = ((int64_t)(LEN + L.sh) * 8 + 15) & ~15LL;
+  L.bulk = (a0 * 8 + bytes <= ndof * 8);
+  if (!L.bulk) L.sh = 0;
+  return L;
+}
+
+__device__ __forceinline__ void tile_issue(const TileLoad& L, int LEN, const double* src, double* dst,
+                                           uint64_t* bar, int nsrc, const double* src2, double* dst2) {
+  const int64_t a0 = L.g0 - L.sh;
+  const uint32_t bytes = (uint32_t)((((int64_t)(LEN + L.sh)) * 8 + 15) & ~15LL);
+  mbar_expect_tx(bar, nsrc * bytes);
+  bulk_g2s(dst, src + a0, bytes, bar);
+  if (nsrc == 2) bulk_g2s(dst2, src2 + a0, bytes, bar);
+}
+
+template <int N, int W, int WMT>
+__global__ void __launch_bounds__(32 * W, 1)
+    tile_step_kernel(const __grid_constant__ Consts<N> C, const Geo G, const TileStepArgs A) {
+  constexpr int KC = (N + 1) / 4, NT = (N + 1) / 8;
+  constexpr int TE = 8 * W * WMT;
+  constexpr int LEN = TE * N + 1;
+  constexpr int PAD = ((LEN + 2) + 1) & ~1;
+  extern __shared__ __align__(16) double smem[];
+  double* sbuf = smem;                        // [2][PAD] double-buffered tile loads (base u)
+  double* sU = sbuf + 2 * PAD;                // stage input / new state
+  double* sk = sU + PAD;                      // k_0 (RK3)
+  double* xfer = sk + PAD;                    // [W]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(xfer + 32);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kq = lane & 3, rr = lane >> 2;
+  const int T = TE - 2 * A.H;
+  const int64_t ndof = G.ndof;
+  const double mnu = -C.nu;
+  Geo Gt = G;
+  Gt.E = TE;
+  double breg[2 * NT * KC];
+#pragma unroll
+  for (int mat = 0; mat < 2; ++mat)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int kc = 0; kc < KC; ++kc) breg[(mat * NT + nt) * KC + kc] = bfrag_perm<N>(C, mat, nt, kc, lane);
+  auto bget = [&](int mat, int nt, int kc) -> double { return breg[(mat * NT + nt) * KC + kc]; };
+  double minv_a[KC];
+#pragma unroll
+  for (int kc = 0; kc < KC; ++kc) {
+    const int j = 4 * kc + kq;
+    minv_a[kc] = C.minv[(j == 0 || j == N) ? 0 : j];
+  }
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0 && blockIdx.x < A.ntiles) {
+    const TileLoad L = tile_load_plan(blockIdx.x, T, A.H, N, LEN, ndof);
+    if (L.bulk) tile_issue(L, LEN, A.u, sbuf, &bar[0], 1, nullptr, nullptr);
+  }
+  double fin = 0.0;
+  bool bad = false;
+  uint32_t phase = 0;
+  double kv[WMT][KC], acc[WMT][KC];
+  int it = 0;
+  for (int t = blockIdx.x; t < A.ntiles; t += gridDim.x, ++it) {
+    const int b = it & 1;
+    double* sb = sbuf + b * PAD;
+    const TileLoad L = tile_load_plan(t, T, A.H, N, LEN, ndof);
+    if (L.bulk) {
+      while (!mbar_try_wait(&bar[b], (phase >> b) & 1u)) {
+      }
+      phase ^= (1u << b);
+    } else {
+      for (int k = tid; k < LEN; k += 32 * W) {
+        int64_t g = L.g0 + k;
+        while (g >= ndof) g -= ndof;
+        sb[k] = __ldg(A.u + g);
+      }
+      __syncthreads();
+    }
+    // prefetch the next tile into the other buffer (free: its tile ended with a barrier)
+    if (tid == 0 && t + (int)gridDim.x < A.ntiles) {
+      const TileLoad Ln = tile_load_plan(t + gridDim.x, T, A.H, N, LEN, ndof);
+      if (Ln.bulk) tile_issue(Ln, LEN, A.u, sbuf + (b ^ 1) * PAD, &bar[b ^ 1], 1, nullptr, nullptr);
+    }
+    const double* su = sb + L.sh;
+    if (tid == 0) sU[LEN - 1] = su[LEN - 1];   // the chain's last node is never owned
+    for (int st = 0; st < A.tab.s; ++st) {
+      const double* src = (st == 0) ? su : sU;
+      ring_rhs<N, WMT, decltype(bget), false>(C, Gt, src, xfer, bget, minv_a, mnu, warp, lane, kv, fin);
+#pragma unroll
+      for (int q = 0; q < WMT; ++q) {
+        const int e = 8 * (warp * WMT + q) + rr;
+#pragma unroll
+        for (int kc = 0; kc < KC; ++kc) {
+          const int j = 4 * kc + kq;
+          if (j == N) continue;
+          const int g = e * N + j;
+          const double kk = kv[q][kc];
+          const double term = __dmul_rn(A.tab.b[st], kk);
+          acc[q][kc] = (st == 0) ? term : __dadd_rn(acc[q][kc], term);
+          if (st + 1 < A.tab.s) {
+            double y;
+            if (A.tab.nterm[st + 1] == 1) {
+              y = __dadd_rn(su[g], __dmul_rn(__dmul_rn(A.dt, A.tab.a[st + 1][st]), kk));
+            } else {
+              double sacc = __dmul_rn(A.tab.a[st + 1][0], (st == 0) ? kk : sk[g]);
+              for (int jj = 1; jj <= st; ++jj)
+                sacc = __dadd_rn(sacc, __dmul_rn(A.tab.a[st + 1][jj], (jj == st) ? kk : sk[g]));
+              y = __dadd_rn(su[g], __dmul_rn(A.dt, sacc));
+            }
+            sU[g] = y;
+            if (st == 0 && A.tab.keep[0]) sk[g] = kk;
+          } else {
+            const double un = __dadd_rn(su[g], __dmul_rn(A.dt, acc[q][kc]));
+            if (e >= A.H && e < A.H + T) bad |= !isfinite(un);
+            sU[g] = un;                         // every warp is past its last read of sU
+          }
+        }
+      }
+      __syncthreads();
+    }
+    const int64_t e_out0 = (int64_t)t * T;
+    const int nout_el = (int)min((int64_t)T, G.E - e_out0);
+    for (int k = tid; k < nout_el * N; k += 32 * W) A.out[e_out0 * N + k] = sU[A.H * N + k];
+    __syncthreads();
+  }
+  if (fin != fin || bad)
+    atomicOr(A.flag, (fin != fin ? SEM1D_FLAG_STATE_NONFINITE : 0) | (bad ? SEM1D_FLAG_STEP_NONFINITE : 0));
+}
+
+template <int N, int W, int WMT>
+__global__ void __launch_bounds__(32 * W, 1)
+    tile_adj_kernel(const __grid_constant__ Consts<N> C, const Geo G, const TileStepArgs A) {
+  constexpr int KC = (N + 1) / 4, NT = (N + 1) / 8;
+  constexpr int TE = 8 * W * WMT;
+  constexpr int LEN = TE * N + 1;
+  constexpr int PAD = ((LEN + 2) + 1) & ~1;
+  extern __shared__ __align__(16) double smem[];
+  double* sbu = smem;                         // [2][PAD] u_n loads (= U_0)
+  double* sbl = sbu + 2 * PAD;                // [2][PAD] lam loads (accumulated in place)
+  double* sUs = sbl + 2 * PAD;                // U_1 .. U_3
+  double* sk = sUs + 3 * PAD;
+  double* sz = sk + PAD;
+  double* xfer = sz + PAD;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(xfer + 32);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int kq = lane & 3, rr = lane >> 2;
+  const int T = TE - 2 * A.H;
+  const int S = A.tab.s;
+  const int64_t ndof = G.ndof;
+  const double mnu = -C.nu;
+  Geo Gt = G;
+  Gt.E = TE;
+  double* su = sbu;
+  double* slam = sbl;
+  auto Uarr = [&](int i) -> double* { return i == 0 ? su : sUs + (i - 1) * PAD; };
+  double breg[3 * NT * KC];
+#pragma unroll
+  for (int mat = 0; mat < 3; ++mat)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+      for (int kc = 0; kc < KC; ++kc) breg[(mat * NT + nt) * KC + kc] = bfrag_perm<N>(C, mat, nt, kc, lane);
+  auto bget = [&](int mat, int nt, int kc) -> double { return breg[(mat * NT + nt) * KC + kc]; };
+  double minv_a[KC];
+#pragma unroll
+  for (int kc = 0; kc < KC; ++kc) {
+    const int j = 4 * kc + kq;
+    minv_a[kc] = C.minv[(j == 0 || j == N) ? 0 : j];
+  }
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0 && blockIdx.x < A.ntiles) {
+    const TileLoad L = tile_load_plan(blockIdx.x, T, A.H, N, LEN, ndof);
+    if (L.bulk) tile_issue(L, LEN, A.u, sbu, &bar[0], 2, A.lam, sbl);
+  }
+  double fin = 0.0;
+  uint32_t phase = 0;
+  double kv[WMT][KC], lnext[WMT][KC], lacc[WMT][KC];
+  int it = 0;
+  for (int t = blockIdx.x; t < A.ntiles; t += gridDim.x, ++it) {
+    const int bsel = it & 1;
+    const TileLoad L = tile_load_plan(t, T, A.H, N, LEN, ndof);
+    if (L.bulk) {
+      while (!mbar_try_wait(&bar[bsel], (phase >> bsel) & 1u)) {
+      }
+      phase ^= (1u << bsel);
+    } else {
+      for (int k = tid; k < LEN; k += 32 * W) {
+        int64_t g = L.g0 + k;
+        while (g >= ndof) g -= ndof;
+        sbu[bsel * PAD + k] = __ldg(A.u + g);
+        sbl[bsel * PAD + k] = __ldg(A.lam + g);
+      }
+      __syncthreads();
+    }
+    if (tid == 0 && t + (int)gridDim.x < A.ntiles) {
+      const TileLoad Ln = tile_load_plan(t + gridDim.x, T, A.H, N, LEN, ndof);
+      if (Ln.bulk) tile_issue(Ln, LEN, A.u, sbu + (bsel ^ 1) * PAD, &bar[bsel ^ 1], 2, A.lam,
+                              sbl + (bsel ^ 1) * PAD);
+    }
+    su = sbu + bsel * PAD + L.sh;
+    slam = sbl + bsel * PAD + L.sh;
+    if (tid == 0)
+      for (int i = 1; i < S; ++i) Uarr(i)[LEN - 1] = su[LEN - 1];   // never-owned last node
+    for (int i = 0; i + 1 < S; ++i) {
+      ring_rhs<N, WMT, decltype(bget), false>(C, Gt, Uarr(i), xfer, bget, minv_a, mnu, warp, lane, kv, fin);
+      double* dst = Uarr(i + 1);
+#pragma unroll
+      for (int q = 0; q < WMT; ++q) {
+        const int e = 8 * (warp * WMT + q) + rr;
+#pragma unroll
+        for (int kc = 0; kc < KC; ++kc) {
+          const int j = 4 * kc + kq;
+          if (j == N) continue;
+          const int g = e * N + j;
+          const double kk = kv[q][kc];
+          double y;
+          if (A.tab.nterm[i + 1] == 1) {
+            y = __dadd_rn(su[g], __dmul_rn(__dmul_rn(A.dt, A.tab.a[i + 1][i]), kk));
+          } else {
+            double sacc = __dmul_rn(A.tab.a[i + 1][0], (i == 0) ? kk : sk[g]);
+            for (int jj = 1; jj <= i; ++jj)
+              sacc = __dadd_rn(sacc, __dmul_rn(A.tab.a[i + 1][jj], (jj == i) ? kk : sk[g]));
+            y = __dadd_rn(su[g], __dmul_rn(A.dt, sacc));
+          }
+          dst[g] = y;
+          if (i == 0 && A.tab.keep[0]) sk[g] = kk;
+        }
+      }
+      __syncthreads();
+    }
+    for (int i = S - 1; i >= 0; --i) {
+#pragma unroll
+      for (int q = 0; q < WMT; ++q) {
+        const int e = 8 * (warp * WMT + q) + rr;
+#pragma unroll
+        for (int kc = 0; kc < KC; ++kc) {
+          const int j = 4 * kc + kq;
+          if (j == N) continue;
+          const int g = e * N + j;
+          double z = __dmul_rn(A.tab.b[i], slam[g]);
+          if (i + 1 < S && A.tab.a[i + 1][i] != 0.0) z = __dadd_rn(z, __dmul_rn(A.tab.a[i + 1][i], lnext[q][kc]));
+          if (i + 2 < S && A.tab.a[i + 2][i] != 0.0) z = __dadd_rn(z, __dmul_rn(A.tab.a[i + 2][i], sk[g]));
+          if (e >= A.H && e < A.H + T) fin = fma(z, 0.0, fin);
+          sz[g] = __dmul_rn(z, minv_a[kc]);
+        }
+      }
+      if (tid == 0) sz[TE * N] = 0.0;         // last node of the open chain (ghost margin)
+      __syncthreads();
+      ring_jact<N, WMT, decltype(bget), false>(C, Gt, Uarr(i), sz, xfer, bget, mnu, warp, lane, kv);
+#pragma unroll
+      for (int q = 0; q < WMT; ++q) {
+        const int e = 8 * (warp * WMT + q) + rr;
+#pragma unroll
+        for (int kc = 0; kc < KC; ++kc) {
+          const int j = 4 * kc + kq;
+          if (j == N) continue;
+          const int g = e * N + j;
+          const double l = __dmul_rn(A.dt, kv[q][kc]);
+          lacc[q][kc] = (i == S - 1) ? l : __dadd_rn(lacc[q][kc], l);
+          if (i + 1 < S && S == 3) sk[g] = lnext[q][kc];
+          lnext[q][kc] = l;
+          if (i == 0) slam[g] = __dadd_rn(slam[g], lacc[q][kc]);
+        }
+      }
+      __syncthreads();
+    }
+    const int64_t e_out0 = (int64_t)t * T;
+    const int nout_el = (int)min((int64_t)T, G.E - e_out0);
+    for (int k = tid; k < nout_el * N; k += 32 * W) A.out[e_out0 * N + k] = slam[A.H * N + k];
+    __syncthreads();
+  }
+  if (fin != fin) atomicOr(A.flag, SEM1D_FLAG_INPUT2_NONFINITE);
+}
+
+template <int N>
+struct TileCfg {
+  // TE = 256 elements for N = 7, 128 for N = 15/23, 64 for N = 31 (9 adjoint slabs fit 227 KB)
+  static constexpr int W = (N + 1) == 32 ? 8 : 16;
+  static constexpr int WMT = (N + 1) == 8 ? 2 : 1;
+  static constexpr int TE = 8 * W * WMT;
+  static constexpr int PAD = ((TE * N + 1 + 2) + 1) & ~1;
+  static constexpr size_t fwd_smem = sizeof(double) * (4 * (size_t)PAD + 32) + 2 * sizeof(uint64_t);
+  static constexpr size_t adj_smem = sizeof(double) * (9 * (size_t)PAD + 32) + 2 * sizeof(uint64_t);
+};
 
 template <int N>
 constexpr size_t ens_smem_bytes(int ndof) {

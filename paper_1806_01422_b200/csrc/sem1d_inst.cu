@@ -9,4 +9,5 @@ namespace sem1d {
 template cudaError_t launch_apply<SEM_N>(const PlanView&, int, const Args&, cudaStream_t);
 template cudaError_t launch_ens_forward<SEM_N>(const PlanView&, const EnsArgs&, cudaStream_t);
 template cudaError_t launch_ens_adjoint<SEM_N>(const PlanView&, const EnsAdjArgs&, cudaStream_t);
+template cudaError_t launch_tile_step<SEM_N>(const PlanView&, int, TileStepArgs, cudaStream_t);
 }

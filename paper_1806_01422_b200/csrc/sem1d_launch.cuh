@@ -5,6 +5,8 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "sem1d_device.cuh"
 #include "sem1d_ensemble.cuh"
 #include "sem1d_smallring.cuh"
@@ -250,6 +252,49 @@ cudaError_t launch_ens_forward(const PlanView& p, const EnsArgs& a, cudaStream_t
     }
   }
   return launch_small<N>(p, &a, nullptr, s);
+}
+
+// Temporally blocked RK step / adjoint step for large periodic rings (batch 1).
+// kind 0: forward step (H = s), 1: adjoint step (H = 2s - 1).
+template <int N>
+cudaError_t launch_tile_step(const PlanView& p, int kind, TileStepArgs a, cudaStream_t s) {
+  if constexpr ((N + 1) % 8 != 0) {
+    return cudaErrorNotSupported;
+  } else {
+    using TC = TileCfg<N>;
+    if (!p.geo.periodic || p.batch != 1 || p.geo.E < 2 * TC::TE) return cudaErrorNotSupported;
+    a.H = (kind == 0) ? a.tab.s : 2 * a.tab.s - 1;
+    const int T = TC::TE - 2 * a.H;
+    a.ntiles = (int)((p.geo.E + T - 1) / T);
+    const size_t smem = kind == 0 ? TC::fwd_smem : TC::adj_smem;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (kind == 0) {
+      auto kern = tile_step_kernel<N, TC::W, TC::WMT>;
+      static int per_sm = 0;
+      if (per_sm == 0) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * TC::W, smem);
+        if (per_sm < 1) per_sm = 1;
+      }
+      const int grid = (int)std::min<int64_t>(a.ntiles, (int64_t)per_sm * sms);
+      kern<<<grid, 32 * TC::W, smem, s>>>(*static_cast<const Consts<N>*>(p.consts), p.geo, a);
+    } else {
+      auto kern = tile_adj_kernel<N, TC::W, TC::WMT>;
+      static int per_sm = 0;
+      if (per_sm == 0) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * TC::W, smem);
+        if (per_sm < 1) per_sm = 1;
+      }
+      const int grid = (int)std::min<int64_t>(a.ntiles, (int64_t)per_sm * sms);
+      kern<<<grid, 32 * TC::W, smem, s>>>(*static_cast<const Consts<N>*>(p.consts), p.geo, a);
+    }
+    return cudaGetLastError();
+  }
 }
 
 }  // namespace sem1d

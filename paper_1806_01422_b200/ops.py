@@ -226,6 +226,26 @@ class SemOperator:
             dts_dev.data_ptr(), int(nsteps), code, flags.data_ptr(), self._stream()),
             "sem1d_ens_adjoint")
 
+    _SCHEME_CODES = {"euler": 0, "rk3": 1, "rk4": 2}
+
+    def step_fused_supported(self):
+        """Whole-step fused kernels apply (periodic batch-1 ring, n % 8 == 0, >= 2 tiles)."""
+        if not hasattr(self, "_step_ok"):
+            self._step_ok = bool(_lib.load().sem1d_step_supported(self._plan.handle))
+        return self._step_ok and getattr(self, "use_fused_steps", True)
+
+    def launch_rk_step(self, u, u_new, dt, scheme):
+        _lib.check(_lib.load().sem1d_rk_step(self._plan.handle, u.data_ptr(), u_new.data_ptr(),
+                                             float(dt), self._SCHEME_CODES[scheme],
+                                             self._flag.data_ptr(), self._stream()),
+                   "sem1d_rk_step")
+
+    def launch_adj_step(self, u, lam, lam_out, dt, scheme):
+        _lib.check(_lib.load().sem1d_adj_step(self._plan.handle, u.data_ptr(), lam.data_ptr(),
+                                              lam_out.data_ptr(), float(dt),
+                                              self._SCHEME_CODES[scheme], self._flag.data_ptr(),
+                                              self._stream()), "sem1d_adj_step")
+
     # -- reference surface ------------------------------------------------------
 
     def apply_rhs(self, u):

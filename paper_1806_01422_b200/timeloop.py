@@ -157,7 +157,13 @@ class StepEngine:
         self.op.launch_rk_stage(U_in, k_out, base, terms, coefs, dt, Y, check)
 
     def step(self, u, dt, out):
-        """Launch one full step u -> out (no host sync)."""
+        """Launch one full step u -> out (no host sync): one temporally blocked launch
+        when the ring qualifies, else one fused launch per stage."""
+        fused = getattr(self.op, "step_fused_supported", None)
+        if fused is not None and fused():
+            self.op.launch_rk_step(u, out, dt, self.scheme)
+            self.op.counters["rhs"] += self.s
+            return
         s = self.s
         store = set(self.stored_k)
         for j in store:
