@@ -280,6 +280,42 @@ class SemOperator:
             self.raise_for_flags(("state", "cotangent"))
         return self._out(out, host)
 
+    def apply_host(self, u, v=None, w=None, kinds=None, chunks=8):
+        """F(u), J(u) v, J(u)^T w on HOST fields (pinned CPU tensors or numpy), streamed
+        through the GPU in element chunks with copy/compute overlap (see HostStreamer).
+        Returns a dict {"rhs", "jac", "jact"} of pinned CPU tensors (numpy for numpy
+        input); raises NumericFailure like apply_* on non-finite input."""
+        import torch
+        if self.batch != 1:
+            raise ValidationError("apply_host needs batch == 1")
+        host_np = not isinstance(u, torch.Tensor)
+
+        def prep(x, name):
+            if x is None:
+                return None
+            t = torch.as_tensor(np.asarray(x, dtype=np.float64)) if not isinstance(x, torch.Tensor) else x
+            if tuple(t.shape) != self.shape or t.dtype != torch.float64 or t.is_cuda:
+                raise ValidationError(f"{name} must be a float64 host field of shape {self.shape}")
+            return t
+        u, v, w = prep(u, "state"), prep(v, "tangent"), prep(w, "cotangent")
+        if kinds is None:
+            kinds = ["rhs"] + (["jac"] if v is not None else []) + (["jact"] if w is not None else [])
+        key = ("_streamer", chunks)
+        st = self.__dict__.get(key)
+        if st is None:
+            st = HostStreamer(self, chunks)
+            self.__dict__[key] = st
+        outs = st.run(tuple(kinds), u, v, w)
+        torch.cuda.current_stream(self.device).synchronize()
+        fl = int(st.flag.item())
+        if fl & _lib.SEM1D_FLAG_STATE_NONFINITE:
+            raise NumericFailure("state contains NaN/Inf")
+        if fl & _lib.SEM1D_FLAG_INPUT2_NONFINITE:
+            raise NumericFailure("tangent contains NaN/Inf" if "jac" in kinds else "cotangent contains NaN/Inf")
+        if host_np:
+            return {k: t.numpy() for k, t in outs.items()}
+        return outs
+
     def densify(self, u):
         """Dense J by columns (ops.py:259-273); verification only, n <= 5000."""
         torch = _torch()
@@ -300,6 +336,121 @@ class SemOperator:
         self.counters["jac"] += n
         self.raise_for_flags(("state", "tangent"))
         return self._out(cols, host)
+
+
+# -- streaming applies on host-resident fields -------------------------------------
+
+
+class HostStreamer:
+    """F / J v / J^T w on HOST fields, streamed through the GPU in element chunks.
+
+    The ring is cut into C element blocks with the sharded ghost-element geometry of
+    ``dist.Partition`` (each chunk recomputes its neighbours' boundary elements, so the
+    result is bit-identical to the whole-ring apply).  Chunk i+1's host->device copies,
+    chunk i's kernels and chunk i-1's device->host copies run on three streams, so a
+    step costs max(H2D, D2H) instead of H2D + compute + D2H.  Inputs should be pinned
+    CPU tensors (numpy arrays are staged through pinned buffers)."""
+
+    def __init__(self, op, chunks=8):
+        import torch
+
+        from .dist import Partition, shard_grid
+        g = op.grid
+        E = g.axis.elements
+        chunks = max(2, min(int(chunks), E // 3))
+        self.op, self.C = op, chunks
+        self.parts = [Partition(E, g.axis.degree, chunks, c, g.periodic) for c in range(chunks)]
+        self.ops = []
+        cache = {}
+        for p in self.parts:
+            key = (p.E_ext, p.gl, p.gr, p.rank == 0, p.rank == chunks - 1)
+            sg = shard_grid(g, p)
+            # grids differ only in their extent; the plan depends on (E_ext, N, bc, h)
+            k2 = (p.E_ext,)
+            if k2 not in cache:
+                cache[k2] = SemOperator(sg, op.coef, device=op.device, sync_checks=False)
+            self.ops.append(cache[k2])
+            del key
+        self.flag = torch.zeros(1, dtype=torch.int32, device=op.device)
+        for o in cache.values():
+            o._flag = self.flag             # one flag word for the whole streamed apply
+        self.maxext = max(p.ext_ndof for p in self.parts)
+        self.ndof = g.nglobal
+        dev = op.device
+        self.s_h2d = torch.cuda.Stream(dev)
+        self.s_cmp = torch.cuda.Stream(dev)
+        self.s_d2h = torch.cuda.Stream(dev)
+        self.slots = [{} for _ in range(2)]
+
+    def _buf(self, slot, name):
+        import torch
+        b = self.slots[slot].get(name)
+        if b is None:
+            b = torch.empty(self.maxext, dtype=torch.float64, device=self.op.device)
+            self.slots[slot][name] = b
+        return b
+
+    def _ranges(self, p):
+        """(dst offset, src start, length) pieces of the chunk's ext range in the ring."""
+        start = p.g_lo - p.gl * p.N
+        n = p.ext_ndof
+        out, off = [], 0
+        while off < n:
+            g = (start + off) % self.ndof
+            ln = min(n - off, self.ndof - g)
+            out.append((off, g, ln))
+            off += ln
+        return out
+
+    def run(self, kinds, u, v=None, w=None, outs=None):
+        """kinds: subset of ("rhs", "jac", "jact"); returns {kind: host tensor}."""
+        import torch
+        sync_copy = not u.is_pinned()   # pageable input: the copy engine cannot overlap it
+        ins = {"u": u, "v": v, "w": w}
+        if outs is None:
+            outs = {k: torch.empty(self.ndof, dtype=torch.float64, pin_memory=True) for k in kinds}
+        need = ["u"] + (["v"] if "jac" in kinds else []) + (["w"] if "jact" in kinds else [])
+        ev_in = [torch.cuda.Event() for _ in range(self.C)]
+        ev_out = [torch.cuda.Event() for _ in range(self.C)]
+        ev_free = [torch.cuda.Event() for _ in range(self.C)]
+        cur = torch.cuda.current_stream(self.op.device)
+        self.s_h2d.wait_stream(cur)
+        self.flag.zero_()
+        for c, p in enumerate(self.parts):
+            slot = c % 2
+            op = self.ops[c]
+            with torch.cuda.stream(self.s_h2d):
+                if c >= 2:
+                    self.s_h2d.wait_event(ev_free[c - 2])      # slot's previous D2H done
+                for name in need:
+                    dst = self._buf(slot, name)
+                    for off, g, ln in self._ranges(p):
+                        dst[off:off + ln].copy_(ins[name][g:g + ln], non_blocking=not sync_copy)
+                ev_in[c].record(self.s_h2d)
+            with torch.cuda.stream(self.s_cmp):
+                self.s_cmp.wait_event(ev_in[c])
+                n = p.ext_ndof
+                ub = self._buf(slot, "u")[:n]
+                for k in kinds:
+                    ob = self._buf(slot, "o_" + k)[:n]
+                    if k == "rhs":
+                        op.launch_rhs(ub, ob)
+                    elif k == "jac":
+                        op.launch_jac(ub, self._buf(slot, "v")[:n], ob)
+                    else:
+                        op.launch_jact(ub, self._buf(slot, "w")[:n], ob)
+                ev_out[c].record(self.s_cmp)
+            with torch.cuda.stream(self.s_d2h):
+                self.s_d2h.wait_event(ev_out[c])
+                sl = p.owned_slice()
+                for k in kinds:
+                    outs[k][p.g_lo:p.g_lo + p.n_own].copy_(self._buf(slot, "o_" + k)[sl],
+                                                           non_blocking=True)
+                ev_free[c].record(self.s_d2h)
+        cur.wait_stream(self.s_d2h)
+        cur.wait_stream(self.s_cmp)
+        self.op.counters.update({k: self.op.counters[k] + 1 for k in kinds})
+        return outs
 
 
 # -- grid maps on the device (used by Grid.scatter / Grid.gather) ----------------

@@ -215,3 +215,22 @@ def test_cfg2_full_size_properties(cuda):
         inner = slice(N + 1, (ne - 1) * N)   # interior nodes do not see the window wrap
         assert rel_err(fh[idx][inner], fs[inner]) <= TOL
         assert rel_err(jh[idx][inner], js[inner]) <= TOL
+
+
+@pytest.mark.parametrize("E,N,bc", [(4096, 7, "periodic"), (1000, 15, "dirichlet0"), (600, 9, "periodic")])
+def test_host_streaming_apply(cuda, E, N, bc):
+    """apply_host: chunked H2D / compute / D2H overlap == device applies (same kernels)."""
+    op = _op(-1.0, 1.0, E, N, bc == "periodic", 0.01)
+    u, v, w = R.seeded_fields(op.ndof, E)
+    uh, vh, wh = (torch.from_numpy(a).pin_memory() for a in (u, v, w))
+    out = op.apply_host(uh, vh, wh)
+    ud, vd, wd = (torch.from_numpy(a).cuda() for a in (u, v, w))
+    for k, ref in (("rhs", op.apply_rhs(ud)), ("jac", op.apply_jacobian(ud, vd)),
+                   ("jact", op.apply_jacobian_transpose(ud, wd))):
+        assert rel_err(out[k].numpy(), ref.cpu().numpy()) <= 1e-14
+    npout = op.apply_host(u, kinds=["rhs"])
+    assert np.array_equal(npout["rhs"], out["rhs"].numpy())
+    bad = u.copy()
+    bad[E] = np.nan
+    with pytest.raises(sb.NumericFailure):
+        op.apply_host(bad)
