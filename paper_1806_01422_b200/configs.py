@@ -20,6 +20,12 @@ CFG3 = dict(xa=-1.0, xb=1.0, E=1 << 18, N=31, nu=1e-3, seed=3)
 # config 4: dt = 5e-5 is unstable on [-1, 1] (rho(J) = 3.85e6, SURVEY.md finding 4);
 # [0, 20] gives rho = 3.85e4 and an RK4 limit of ~7e-5.
 CFG4 = dict(xa=0.0, xb=20.0, B=4096, E=256, N=15, nu=0.01, steps=1000, dt=5e-5, seed=4)
+# config 5 gives neither domain nor dt: h = 1/64 (domain length 2^25 / 64) gives
+# rho(J) ~ 5.4e3 at nu = 1e-3, N = 7 (oracle dense Jacobian at the same h), so RK4 is
+# stable to dt ~ 5e-4; dt = 2e-4, 500 steps.  Binomial checkpointing with s = 40 slots
+# (75 GB of 1.88 GB states on one 180 GB B200, leaving room for the L-BFGS vectors).
+CFG5 = dict(h=1.0 / 64.0, E=1 << 25, N=7, nu=1e-3, steps=500, dt=2e-4, slots=40, modes=32,
+            seed=5, lbfgs_iters=10)
 
 
 def cfg1_inputs(grid, seed=CFG1["seed"]):
@@ -63,6 +69,26 @@ def fourier_fields(grid, batch, n_modes, seed):
     return amps @ np.sin(phase)
 
 
+def fourier_field_device(grid, n_modes, seed, device):
+    """One seeded smooth Fourier field sum_k a_k sin(2 pi k (x - xa) / L), a_k ~ U(-1, 1),
+    evaluated on the device from the closed-form node coordinates (config 5 sizes make
+    the host outer product of fourier_fields prohibitive)."""
+    import torch
+    ax = grid.axis
+    rng = np.random.default_rng(seed)
+    amps = rng.uniform(-1.0, 1.0, n_modes)
+    N, E = ax.degree, ax.elements
+    xi = torch.as_tensor(grid.bases[0].nodes[:N], device=device)
+    e = torch.arange(E, dtype=torch.float64, device=device)
+    x = (e[:, None] * grid.h + grid.h * (xi[None, :] + 1.0) / 2.0).reshape(-1)
+    if not grid.periodic:
+        x = torch.cat([x, torch.tensor([E * grid.h], dtype=torch.float64, device=device)])
+    out = torch.zeros_like(x)
+    for k in range(1, n_modes + 1):
+        out += float(amps[k - 1]) * torch.sin((2.0 * np.pi * k / ax.length) * x)
+    return out
+
+
 def cfg_operator(cfg, device=None, batch=1, bc=PERIODIC):
     grid = grid_1d(cfg["xa"], cfg["xb"], cfg["E"], cfg["N"], bc)
     return SemOperator(grid, PdeCoefficients(cfg["nu"]), device=device, batch=batch)
@@ -85,3 +111,22 @@ def cfg4_problem(B=None, steps=None, scheme="rk4", device=None, seed=CFG4["seed"
                                          store_trajectory=False).u_final
     return AssimilationProblem(name=f"cfg4-{scheme}", grid=grid, op=op, ts=ts, u_target=target,
                                u_guess=u0)
+
+
+def cfg5_problem(E=None, steps=None, slots=None, device=None, seed=CFG5["seed"]):
+    """BASELINE config 5 (single-GPU form): periodic ring of E elements (h = 1/64, N = 7,
+    nu = 1e-3); u0 = 32-mode smooth Fourier field, target = forward run of a perturbed u0."""
+    import torch
+    c = CFG5
+    E = c["E"] if E is None else E
+    steps = c["steps"] if steps is None else steps
+    slots = c["slots"] if slots is None else slots
+    grid = grid_1d(0.0, E * c["h"], E, c["N"], PERIODIC)
+    op = SemOperator(grid, PdeCoefficients(c["nu"]), device=device)
+    ts = timeloop.TsConfig(scheme="rk4", t0=0.0, t_end=steps * c["dt"], dt=c["dt"])
+    u0_t = fourier_field_device(grid, c["modes"], seed, op.device) / 8.0
+    pert = fourier_field_device(grid, c["modes"], seed + 77, op.device) / 40.0
+    target = timeloop.integrate(op, u0_t + pert, ts, store_steps=None).u_final
+    del pert
+    return AssimilationProblem(name="cfg5", grid=grid, op=op, ts=ts, u_target=target,
+                               u_guess=u0_t, checkpoint_slots=slots)

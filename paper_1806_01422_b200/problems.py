@@ -53,6 +53,7 @@ class AssimilationProblem:
 
     def __post_init__(self):
         self._target_dev = None
+        self.last_forward = None
 
     def schedule_for(self, m):
         if self.checkpoint_slots is None:
@@ -71,6 +72,7 @@ class AssimilationProblem:
         """(J, dJ/du0) = one forward + one adjoint sweep (problems.py:184-199)."""
         if self.ts.adaptive:
             raise ValidationError("adaptive stepping is outside the B200 hot path")
+        self.last_forward = None   # release the previous trajectory / checkpoints first
         u0_dev, host = self.op.field(u0, "initial state")
         m = timeloop.count_steps(self.ts)
         sched = self.schedule_for(m)
