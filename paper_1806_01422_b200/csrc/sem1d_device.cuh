@@ -891,6 +891,9 @@ __global__ void __launch_bounds__(MmaTile<N>::THREADS, MmaTile<N>::MINB)
 #ifndef WS_ELEMS8
 #define WS_ELEMS8 256
 #endif
+#ifndef WS_CW32
+#define WS_CW32 16
+#endif
 
 // Occupancy per operator (A/B-measured on config 2, profiles/r1_ab_occupancy.json):
 // F (one input) runs best at 4 CTAs/SM, J and J^T at 3.
@@ -923,9 +926,10 @@ __device__ __forceinline__ double bfrag_perm(const Consts<N>& C, int mat, int nt
 template <int N>
 struct WsTile {
   static constexpr int n = N + 1;
-  static constexpr int CW = 8;                                   // consumer warps
+  // consumer warps: 16 for n = 32 (FP64-bound, latency hidden by more warps), else 8
+  static constexpr int CW = (n == 32) ? WS_CW32 : 8;
   static constexpr int THREADS = 32 * (CW + 1);
-  static constexpr int ELEMS = (n == 8) ? WS_ELEMS8 : MmaTile<N>::ELEMS;
+  static constexpr int ELEMS = (n == 8) ? WS_ELEMS8 : (n == 32 ? 8 * CW : MmaTile<N>::ELEMS);
   static constexpr int WE = ELEMS / CW;                          // elements per consumer warp
   static constexpr int WMT = WE / 8;                             // m-tiles per warp
   static constexpr int NT = n / 8, KC = n / 4;
@@ -1168,15 +1172,19 @@ __global__ void __launch_bounds__(WsTile<N>::THREADS, ws_minb<N, OP>())
       const double* sw = stage_buf + (s * NIN + 1) * SA + sh;
       while (!mbar_try_wait(&full[s], (it / STAGES) & 1)) {
       }
-      const int64_t eh = e0 + rr * WE - 1;
-      const int64_t ehw = (eh < 0) ? G.E - 1 : eh;
-      double r[NT][2];
-      double du_ = 0.0, dw_ = 0.0;
-      if (!periodic && (tl == 0 || tl == tiles_per_ring - 1))
-        mtile_compute<N, OP, true>(C, G, su, sw, rr * WE * N, ehw, minv_a, minv_p, mnu, kq, bget, du_, dw_, r);
-      else
-        mtile_compute<N, OP, false>(C, G, su, sw, rr * WE * N, ehw, minv_a, minv_p, mnu, kq, bget, du_, dw_, r);
-      if (kq == 3) hrow[s * W::CW + rr] = (!periodic && eh < 0) ? 0.0 : r[NT - 1][1];
+#pragma unroll 1
+      for (int hm = 0; hm < W::CW / 8; ++hm) {      // one halo m-tile per 8 consumer warps
+        const int wq = hm * 8 + rr;                 // consumer warp whose left neighbour this is
+        const int64_t eh = e0 + wq * WE - 1;
+        const int64_t ehw = (eh < 0) ? G.E - 1 : eh;
+        double r[NT][2];
+        double du_ = 0.0, dw_ = 0.0;
+        if (!periodic && (tl == 0 || tl == tiles_per_ring - 1))
+          mtile_compute<N, OP, true>(C, G, su, sw, wq * WE * N, ehw, minv_a, minv_p, mnu, kq, bget, du_, dw_, r);
+        else
+          mtile_compute<N, OP, false>(C, G, su, sw, wq * WE * N, ehw, minv_a, minv_p, mnu, kq, bget, du_, dw_, r);
+        if (kq == 3) hrow[s * W::CW + wq] = (!periodic && eh < 0) ? 0.0 : r[NT - 1][1];
+      }
       __syncwarp();
       if (lane == 0) mbar_arrive(&halo[s]);
       const int Tn = T + (STAGES - 1) * gridDim.x;

@@ -10,6 +10,9 @@ from paper_1806_01422_b200 import configs  # noqa: E402
 
 
 def main(cfg="2", reps=20):
+    from paper_1806_01422_b200 import _lib
+    path = int(os.environ.get("SEM1D_PATH", "0"))   # 0 auto (DMMA), 1 DFMA/TMA, 2 plain
+    _lib.load().sem1d_set_kernel_path(path)
     c = {"2": configs.CFG2, "3": configs.CFG3}[cfg]
     op = configs.cfg_operator(c, device="cuda:0")
     u, v, w = configs.operator_inputs(op.ndof, c["seed"])
@@ -28,7 +31,8 @@ def main(cfg="2", reps=20):
         torch.cuda.synchronize()
         res[name] = round(1e3 * s.elapsed_time(e) / int(reps), 2)
     assert op.flags() == 0
-    print(json.dumps({"lib": os.path.basename(os.environ.get("SEM1D_LIB", "default")), "cfg": cfg, "us": res}))
+    print(json.dumps({"lib": os.path.basename(os.environ.get("SEM1D_LIB", "default")), "cfg": cfg,
+                      "path": {0: "dmma-ws", 1: "dfma-tma", 2: "plain-dfma"}[path], "us": res}))
 
 
 if __name__ == "__main__":
