@@ -429,6 +429,13 @@ constexpr size_t ens_adj_smem_bytes(int ndof) {
 // (plus the ghost margin) instead of one HBM round trip per stage.
 // ============================================================================
 
+#ifndef TILE_MINB8
+#define TILE_MINB8 1
+#endif
+#ifndef TILE_ADJ_MINB
+#define TILE_ADJ_MINB 1
+#endif
+
 struct TileStepArgs {
   const double* u;        // state u_n (forward input / adjoint linearisation point)
   const double* lam;      // adjoint: lam_{n+1}
@@ -471,8 +478,12 @@ __device__ __forceinline__ void tile_issue(const TileLoad& L, int LEN, const dou
   if (nsrc == 2) bulk_g2s(dst2, src2 + a0, bytes, bar);
 }
 
+// resident CTAs per SM (A/B: a 64-register cap for two CTAs made the n = 8 step 2x slower)
+template <int N>
+constexpr int tile_minb() { return (N + 1) == 8 ? TILE_MINB8 : 1; }
+
 template <int N, int W, int WMT>
-__global__ void __launch_bounds__(32 * W, 1)
+__global__ void __launch_bounds__(32 * W, tile_minb<N>())
     tile_step_kernel(const __grid_constant__ Consts<N> C, const Geo G, const TileStepArgs A) {
   constexpr int KC = (N + 1) / 4, NT = (N + 1) / 8;
   constexpr int TE = 8 * W * WMT;
@@ -588,7 +599,7 @@ __global__ void __launch_bounds__(32 * W, 1)
 }
 
 template <int N, int W, int WMT>
-__global__ void __launch_bounds__(32 * W, 1)
+__global__ void __launch_bounds__(32 * W, TILE_ADJ_MINB)
     tile_adj_kernel(const __grid_constant__ Consts<N> C, const Geo G, const TileStepArgs A) {
   constexpr int KC = (N + 1) / 4, NT = (N + 1) / 8;
   constexpr int TE = 8 * W * WMT;
