@@ -234,3 +234,35 @@ def test_host_streaming_apply(cuda, E, N, bc):
     bad[E] = np.nan
     with pytest.raises(sb.NumericFailure):
         op.apply_host(bad)
+
+
+def test_max_size_config5_apply(cuda):
+    """Largest BASELINE field (config 5: E = 2^25, N = 7, 235M DOF, 1.9 GB per field):
+    size-independent properties on device-generated inputs plus oracle windows."""
+    from paper_1806_01422_b200 import configs
+    c = configs.CFG5
+    g = grid_1d(0.0, c["E"] * c["h"], c["E"], c["N"])
+    op = sb.SemOperator(g, sb.PdeCoefficients(c["nu"]), device="cuda:0")
+    gen = torch.Generator(device="cuda").manual_seed(55)
+    u = torch.rand(op.ndof, dtype=torch.float64, device=cuda, generator=gen) * 2 - 1
+    v = torch.randn(op.ndof, dtype=torch.float64, device=cuda, generator=gen)
+    f = op.apply_rhs(u)
+    jv = op.apply_jacobian(u, v)
+    jtv = op.apply_jacobian_transpose(u, v)
+    assert bool(torch.isfinite(f).all() and torch.isfinite(jv).all() and torch.isfinite(jtv).all())
+    # dot-product identity <J v, v> = <v, J^T v> at 235M DOF
+    lhs, rhs = float(torch.dot(jv, v)), float(torch.dot(v, jtv))
+    assert abs(lhs - rhs) <= 1e-11 * abs(lhs)
+    # periodic conservation 1^T M f = 0 (SPEC ops invariants), relative to sum |M f|
+    m = torch.as_tensor(g.mass_pattern[np.arange(g.axis.degree)], device=cuda).repeat(c["E"])
+    mf = m * f
+    assert abs(float(mf.sum())) <= 1e-10 * float(mf.abs().sum())
+    # oracle windows away from the window edges
+    N = c["N"]
+    uh, fh = u.cpu().numpy(), f.cpu().numpy()
+    for e0 in (0, c["E"] // 3, c["E"] - 64):
+        ne = 64
+        sub = R.BurgersOracle(R.Mesh1D(0.0, ne * c["h"], ne, N, True), c["nu"])
+        idx = np.arange(e0 * N, (e0 + ne) * N) % op.ndof
+        inner = slice(N + 1, (ne - 1) * N)
+        assert rel_err(fh[idx][inner], sub.rhs(uh[idx])[inner]) <= 1e-12
