@@ -432,6 +432,9 @@ constexpr size_t ens_adj_smem_bytes(int ndof) {
 #ifndef TILE_MINB8
 #define TILE_MINB8 1
 #endif
+#ifndef TILE_WMT8
+#define TILE_WMT8 4
+#endif
 #ifndef TILE_ADJ_MINB
 #define TILE_ADJ_MINB 1
 #endif
@@ -750,13 +753,19 @@ __global__ void __launch_bounds__(32 * W, TILE_ADJ_MINB)
 
 template <int N>
 struct TileCfg {
-  // TE = 256 elements for N = 7, 128 for N = 15/23, 64 for N = 31 (9 adjoint slabs fit 227 KB)
+  // forward: TE = 512 elements for N = 7 (4 m-tiles per warp: more independent DMMA chains
+  // per barrier), 128 for N = 15/23, 64 for N = 31; adjoint: 256 / 128 / 64 (nine slabs
+  // must fit 227 KB)
   static constexpr int W = (N + 1) == 32 ? 8 : 16;
-  static constexpr int WMT = (N + 1) == 8 ? 2 : 1;
-  static constexpr int TE = 8 * W * WMT;
-  static constexpr int PAD = ((TE * N + 1 + 2) + 1) & ~1;
-  static constexpr size_t fwd_smem = sizeof(double) * (4 * (size_t)PAD + 32) + 2 * sizeof(uint64_t);
-  static constexpr size_t adj_smem = sizeof(double) * (9 * (size_t)PAD + 32) + 2 * sizeof(uint64_t);
+  static constexpr int WMT_F = (N + 1) == 8 ? TILE_WMT8 : 1;
+  static constexpr int WMT_A = (N + 1) == 8 ? 2 : 1;
+  static constexpr int TE_F = 8 * W * WMT_F;
+  static constexpr int TE_A = 8 * W * WMT_A;
+  static constexpr int PAD_F = ((TE_F * N + 1 + 2) + 1) & ~1;
+  static constexpr int PAD_A = ((TE_A * N + 1 + 2) + 1) & ~1;
+  static constexpr size_t fwd_smem = sizeof(double) * (4 * (size_t)PAD_F + 32) + 2 * sizeof(uint64_t);
+  static constexpr size_t adj_smem = sizeof(double) * (9 * (size_t)PAD_A + 32) + 2 * sizeof(uint64_t);
+  static constexpr int TE_MAX = TE_F > TE_A ? TE_F : TE_A;
 };
 
 template <int N>

@@ -262,16 +262,16 @@ cudaError_t launch_tile_step(const PlanView& p, int kind, TileStepArgs a, cudaSt
     return cudaErrorNotSupported;
   } else {
     using TC = TileCfg<N>;
-    if (!p.geo.periodic || p.batch != 1 || p.geo.E < 2 * TC::TE) return cudaErrorNotSupported;
+    if (!p.geo.periodic || p.batch != 1 || p.geo.E < 2 * TC::TE_MAX) return cudaErrorNotSupported;
     a.H = (kind == 0) ? a.tab.s : 2 * a.tab.s - 1;
-    const int T = TC::TE - 2 * a.H;
+    const int T = (kind == 0 ? TC::TE_F : TC::TE_A) - 2 * a.H;
     a.ntiles = (int)((p.geo.E + T - 1) / T);
     const size_t smem = kind == 0 ? TC::fwd_smem : TC::adj_smem;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (kind == 0) {
-      auto kern = tile_step_kernel<N, TC::W, TC::WMT>;
+      auto kern = tile_step_kernel<N, TC::W, TC::WMT_F>;
       static int per_sm = 0;
       if (per_sm == 0) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -282,7 +282,7 @@ cudaError_t launch_tile_step(const PlanView& p, int kind, TileStepArgs a, cudaSt
       const int grid = (int)std::min<int64_t>(a.ntiles, (int64_t)per_sm * sms);
       kern<<<grid, 32 * TC::W, smem, s>>>(*static_cast<const Consts<N>*>(p.consts), p.geo, a);
     } else {
-      auto kern = tile_adj_kernel<N, TC::W, TC::WMT>;
+      auto kern = tile_adj_kernel<N, TC::W, TC::WMT_A>;
       static int per_sm = 0;
       if (per_sm == 0) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

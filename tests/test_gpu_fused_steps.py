@@ -27,7 +27,7 @@ def _problem(E, N, nu, dt, steps, scheme, seed):
 
 
 @pytest.mark.parametrize("scheme", ["rk4", "rk3", "euler"])
-@pytest.mark.parametrize("E,N,dt", [(549, 7, 2e-6), (301, 15, 2e-7), (260, 31, 1e-8)])
+@pytest.mark.parametrize("E,N,dt", [(1061, 7, 2e-6), (301, 15, 2e-7), (260, 31, 1e-8)])
 def test_fused_step_sweeps(cuda, scheme, E, N, dt):
     steps = 6
     g, op, u0, ud, ts = _problem(E, N, 1e-3, dt, steps, scheme, E)
@@ -51,11 +51,11 @@ def test_fused_step_sweeps(cuda, scheme, E, N, dt):
 
 
 def test_fused_step_flags(cuda):
-    g, op, u0, ud, ts = _problem(549, 7, 1e-3, 2e-6, 3, "rk4", 1)
+    g, op, u0, ud, ts = _problem(1061, 7, 1e-3, 2e-6, 3, "rk4", 1)
     u0[100] = np.nan
     with pytest.raises(sb.NumericFailure):
         timeloop.integrate(op, u0, ts)
     # a blow-up inside the step -> StepFailure retries, then gives up like the reference
-    g, op, u0, ud, ts = _problem(549, 7, 1e-3, 0.5, 3, "rk4", 1)
+    g, op, u0, ud, ts = _problem(1061, 7, 1e-3, 0.5, 3, "rk4", 1)
     with pytest.raises(sb.NumericFailure):
         timeloop.integrate(op, 1e150 * u0, ts)
