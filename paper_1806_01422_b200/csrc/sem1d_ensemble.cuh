@@ -435,6 +435,9 @@ constexpr size_t ens_adj_smem_bytes(int ndof) {
 #ifndef TILE_WMT8
 #define TILE_WMT8 4
 #endif
+#ifndef TILE_WA8
+#define TILE_WA8 16
+#endif
 #ifndef TILE_ADJ_MINB
 #define TILE_ADJ_MINB 1
 #endif
@@ -757,10 +760,11 @@ struct TileCfg {
   // per barrier), 128 for N = 15/23, 64 for N = 31; adjoint: 256 / 128 / 64 (nine slabs
   // must fit 227 KB)
   static constexpr int W = (N + 1) == 32 ? 8 : 16;
+  static constexpr int W_A = (N + 1) == 8 ? TILE_WA8 : W;     // adjoint warps
   static constexpr int WMT_F = (N + 1) == 8 ? TILE_WMT8 : 1;
-  static constexpr int WMT_A = (N + 1) == 8 ? 2 : 1;
+  static constexpr int WMT_A = (N + 1) == 8 ? 256 / (8 * W_A) : 1;
   static constexpr int TE_F = 8 * W * WMT_F;
-  static constexpr int TE_A = 8 * W * WMT_A;
+  static constexpr int TE_A = 8 * W_A * WMT_A;
   static constexpr int PAD_F = ((TE_F * N + 1 + 2) + 1) & ~1;
   static constexpr int PAD_A = ((TE_A * N + 1 + 2) + 1) & ~1;
   static constexpr size_t fwd_smem = sizeof(double) * (4 * (size_t)PAD_F + 32) + 2 * sizeof(uint64_t);

@@ -282,16 +282,16 @@ cudaError_t launch_tile_step(const PlanView& p, int kind, TileStepArgs a, cudaSt
       const int grid = (int)std::min<int64_t>(a.ntiles, (int64_t)per_sm * sms);
       kern<<<grid, 32 * TC::W, smem, s>>>(*static_cast<const Consts<N>*>(p.consts), p.geo, a);
     } else {
-      auto kern = tile_adj_kernel<N, TC::W, TC::WMT_A>;
+      auto kern = tile_adj_kernel<N, TC::W_A, TC::WMT_A>;
       static int per_sm = 0;
       if (per_sm == 0) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * TC::W, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * TC::W_A, smem);
         if (per_sm < 1) per_sm = 1;
       }
       const int grid = (int)std::min<int64_t>(a.ntiles, (int64_t)per_sm * sms);
-      kern<<<grid, 32 * TC::W, smem, s>>>(*static_cast<const Consts<N>*>(p.consts), p.geo, a);
+      kern<<<grid, 32 * TC::W_A, smem, s>>>(*static_cast<const Consts<N>*>(p.consts), p.geo, a);
     }
     return cudaGetLastError();
   }
