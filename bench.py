@@ -47,6 +47,10 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-sweep", action="store_true")
+    # test-only: exercise the sharded path with every rank on cuda:0 and a gloo exchange
+    # (safe on one GPU: no kernel waits on another rank)
+    p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
+    p.add_argument("--same-device", action="store_true")
     return p.parse_args()
 
 
@@ -258,9 +262,11 @@ def run_gpu_arm(args):
     from paper_1806_01422_b200 import configs
 
     rank, world, local = dist_env()
+    if args.same_device:
+        local = 0
     if world > 1:
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+        dist.init_process_group(args.dist_backend)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     c = configs.CFG2
@@ -297,7 +303,7 @@ def run_gpu_arm(args):
         total_ms, per = timed_ops(op, ud, vd, wd, outs, args.steps, stream)
     torch.cuda.synchronize()
     if world > 1:
-        t = torch.tensor([total_ms], device=dev)
+        t = torch.tensor([total_ms], device=dev if args.dist_backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
         dist.barrier()
@@ -337,7 +343,7 @@ def run_gpu_arm(args):
     torch.cuda.synchronize()
     e2e_ms = s0.elapsed_time(s1) / e2e_steps
     if world > 1:
-        t = torch.tensor([e2e_ms], device=dev)
+        t = torch.tensor([e2e_ms], device=dev if args.dist_backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e_value = 3 * ndof * world / (e2e_ms * 1e-3)

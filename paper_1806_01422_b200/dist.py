@@ -98,8 +98,21 @@ class HaloExchange:
             ops.append(dist.P2POp(dist.irecv, recv_r, p.right, self.group, tag=1))
         if recv_l is not None:
             ops.append(dist.P2POp(dist.irecv, recv_l, p.left, self.group, tag=2))
+        staged = dev.type == "cuda" and dist.get_backend(self.group) == "gloo"
+        if staged:   # gloo moves CPU tensors only: stage through host memory
+            ops = [dist.P2POp(o.op, o.tensor.cpu() if o.op is dist.isend else
+                              torch.empty(o.tensor.shape, dtype=o.tensor.dtype), o.peer, self.group,
+                              tag=o.tag) for o in ops]
+            recv_cpu = [o.tensor for o in ops if o.op is dist.irecv]
         for r in dist.batch_isend_irecv(ops):
             r.wait()
+        if staged:
+            k_r = 0
+            if recv_r is not None:
+                recv_r.copy_(recv_cpu[k_r])
+                k_r += 1
+            if recv_l is not None:
+                recv_l.copy_(recv_cpu[k_r])
         for i, f in enumerate(fields):
             if recv_l is not None:
                 f[0:L] = recv_l[i]
@@ -203,8 +216,13 @@ class ShardedOperator:
     def _allreduce(self, t, op="sum"):
         import torch.distributed as dist
         if self.part.P > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX,
-                            group=self.group)
+            rop = dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX
+            if t.is_cuda and dist.get_backend(self.group) == "gloo":
+                c = t.cpu()
+                dist.all_reduce(c, op=rop, group=self.group)
+                t.copy_(c)
+            else:
+                dist.all_reduce(t, op=rop, group=self.group)
         return t
 
     def flags(self, reset=True):
