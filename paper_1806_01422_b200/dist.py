@@ -5,7 +5,9 @@ global nodes [e_lo*N, e_hi*N) (plus node E*N on the last rank of a Dirichlet
 grid).  Each rank stores its fields on an EXTENDED chain: its elements plus
 one ghost element on each side that has a neighbour (no ghost at a global
 Dirichlet end; two on the left, see Partition), laid out as a local Dirichlet grid with the GLOBAL element
-length h.  The unchanged fused kernels then compute, on every rank, both
+length h.  On periodic global rings each rank instead keeps ghost ZONES of 8
+elements per side on a periodic local chain, so the single-launch RK step and
+adjoint step kernels run after ONE exchange per step (Partition docstring).  The unchanged fused kernels then compute, on every rank, both
 contributions to each owned interface node -- including node e_lo*N, whose
 left contribution comes from the recomputed ghost element -- so a sharded
 apply is bit-identical to the single-GPU apply (the interface sum has the same
@@ -30,13 +32,22 @@ from .grid import DIRICHLET0, PERIODIC, Axis, Grid
 
 
 class Partition:
-    """Contiguous element blocks; ghost elements where a neighbour exists."""
+    """Contiguous element blocks; ghost elements where a neighbour exists.
 
-    def __init__(self, E, N, P, rank, periodic):
+    ``zone`` = 0: the minimal Dirichlet-chain layout (2 ghost elements left, 1 right).
+    ``zone`` = G > 0 (periodic global rings only): G ghost elements on each side and the
+    extended chain is itself treated as a PERIODIC ring -- the wrap-around garbage of a
+    step reaches at most 2s-1 elements into the chain, i.e. stays in the ghost zone when
+    G >= 2s-1, so the single-launch step kernels run unchanged after one exchange."""
+
+    def __init__(self, E, N, P, rank, periodic, zone=0):
         if P < 1 or not (0 <= rank < P):
             raise ValidationError(f"bad rank {rank} of {P}")
         if E < 3 * P:
             raise ValidationError(f"need at least 3 elements per rank (E={E}, P={P})")
+        if zone and not periodic:
+            raise ValidationError("ghost zones need a periodic global ring")
+        self.zone = int(zone) if P > 1 else 0
         self.E, self.N, self.P, self.rank, self.periodic = E, N, P, rank, bool(periodic)
         self.e_lo = (rank * E) // P
         self.e_hi = ((rank + 1) * E) // P
@@ -49,11 +60,15 @@ class Partition:
         # because node e_hi*N is not owned.
         self.gl = 2 if (self.periodic or rank > 0) else 0
         self.gr = 1 if (self.periodic or rank < P - 1) else 0
+        if self.zone:
+            if self.E_loc < self.zone:
+                raise ValidationError(f"ghost zone {self.zone} exceeds the {self.E_loc}-element block")
+            self.gl = self.gr = self.zone
         if P == 1:
             self.gl = self.gr = 0
         self.E_ext = self.E_loc + self.gl + self.gr
         self.own0 = self.gl * N                       # owned range start in the ext chain
-        self.ext_ndof = self.E_ext * N + 1
+        self.ext_ndof = self.E_ext * N + (0 if self.zone else 1)
         self.left = (rank - 1) % P if self.gl else None
         self.right = (rank + 1) % P if self.gr else None
         self.g_lo = self.e_lo * N                     # global index of the first owned node
@@ -81,13 +96,19 @@ class HaloExchange:
         ops = []
         send_l = send_r = recv_l = recv_r = None
         dev = fields[0].device
-        L = p.gl * N
-        if p.left is not None:      # my first N+1 owned nodes -> left neighbour's right ghost
-            send_l = torch.stack([f[o0:o0 + N + 1] for f in fields]).contiguous()
+        L = p.gl * N                       # left ghost nodes I receive
+        R = p.gr * N + (0 if p.zone else 1)  # right ghost nodes I receive
+        # what the neighbours receive from me: every rank that has a left (right)
+        # neighbour has the same left (right) ghost width -- 2N (N+1) for Dirichlet chains,
+        # zone*N in ghost-zone mode -- so the sizes are the neighbours', not mine
+        to_left = p.zone * N if p.zone else N + 1
+        to_right = p.zone * N if p.zone else 2 * N
+        if p.left is not None:      # my first nodes -> left neighbour's right ghost
+            send_l = torch.stack([f[o0:o0 + to_left] for f in fields]).contiguous()
             recv_l = torch.empty((k, L), dtype=torch.float64, device=dev)
-        if p.right is not None:     # my last 2N owned nodes -> right neighbour's left ghosts
-            send_r = torch.stack([f[o0 + no - 2 * N:o0 + no] for f in fields]).contiguous()
-            recv_r = torch.empty((k, N + 1), dtype=torch.float64, device=dev)
+        if p.right is not None:     # my last nodes -> right neighbour's left ghost
+            send_r = torch.stack([f[o0 + no - to_right:o0 + no] for f in fields]).contiguous()
+            recv_r = torch.empty((k, R), dtype=torch.float64, device=dev)
         # fixed order (send_left, send_right, recv_right, recv_left) pairs the messages
         # correctly even when left and right neighbour are the same rank (P = 2)
         if send_l is not None:
@@ -117,19 +138,20 @@ class HaloExchange:
             if recv_l is not None:
                 f[0:L] = recv_l[i]
             if recv_r is not None:
-                f[o0 + no:o0 + no + N + 1] = recv_r[i]
+                f[o0 + no:o0 + no + R] = recv_r[i]
 
 
 def shard_grid(global_grid, part):
-    """The extended local chain of a partition as a Dirichlet grid with the global h
-    (a single rank keeps the global grid itself, periodic wrap included)."""
+    """The extended local chain of a partition with the global h: a Dirichlet chain, or a
+    periodic one in ghost-zone mode (a single rank keeps the global grid itself)."""
     if part.P == 1:
         return global_grid
     ax = global_grid.axis
     h = global_grid.h
     xa = ax.xa + (part.e_lo - part.gl) * h
     xb = xa + part.E_ext * h
-    return Grid([Axis(xa, xb, part.E_ext, ax.degree, DIRICHLET0)], element_length=h)
+    bc = PERIODIC if part.zone else DIRICHLET0
+    return Grid([Axis(xa, xb, part.E_ext, ax.degree, bc)], element_length=h)
 
 
 class ShardedOperator:
@@ -141,11 +163,14 @@ class ShardedOperator:
     rank-local operator (the CUDA SemOperator by default; the CPU tests pass a
     test double with the same launch interface)."""
 
-    def __init__(self, global_grid, coef, rank, world, group=None, local_factory=None, device=None):
+    def __init__(self, global_grid, coef, rank, world, group=None, local_factory=None, device=None,
+                 zone=None):
         self.global_grid = global_grid
         self.coef = coef
+        if zone is None:   # periodic rings: ghost zones wide enough for a fused RK4 adjoint step
+            zone = 8 if global_grid.periodic else 0
         self.part = Partition(global_grid.axis.elements, global_grid.axis.degree, world, rank,
-                              global_grid.periodic)
+                              global_grid.periodic, zone=zone)
         self.grid = shard_grid(global_grid, self.part)
         if local_factory is None:
             from .ops import SemOperator
@@ -267,6 +292,20 @@ class ShardedOperator:
     def launch_adj_stage(self, U, lam, b, l_terms, a_coefs, dt, l_out, acc_terms, lam_out):
         self.halo.refresh([U, lam] + list(l_terms))
         self.local.launch_adj_stage(U, lam, b, l_terms, a_coefs, dt, l_out, acc_terms, lam_out)
+
+    # -- whole-step launches (ghost-zone mode): one exchange per step ----------------
+
+    def step_fused_supported(self):
+        f = getattr(self.local, "step_fused_supported", None)
+        return bool(self.part.zone >= 7 and f is not None and f())
+
+    def launch_rk_step(self, u, u_new, dt, scheme):
+        self.halo.refresh([u])
+        self.local.launch_rk_step(u, u_new, dt, scheme)
+
+    def launch_adj_step(self, u, lam, lam_out, dt, scheme):
+        self.halo.refresh([u, lam])
+        self.local.launch_adj_step(u, lam, lam_out, dt, scheme)
 
     def launch_terminal(self, uN, ud, lam, J_out):
         """Objective on owned nodes, all-reduced; lam = mask(2 M d) (adjoint.py:39-47)."""

@@ -23,13 +23,23 @@ def _worker(rank, world, port, bc, q):
                       WORLD_SIZE=str(world))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
+        _work(rank, world, bc, q)
+    except Exception as exc:  # report instead of dying silently (the parent would time out)
+        import traceback
+        q.put((rank, {"exception: " + "".join(traceback.format_exception(exc))[-1500:]: False}))
+    finally:
+        dist.destroy_process_group()
+
+
+def _work(rank, world, bc, q):
+    if True:
         from cpu_local_op import CpuLocalOp
         from oracle import semref as R
         import paper_1806_01422_b200 as sb
         from paper_1806_01422_b200 import dist as sd, timeloop
         from paper_1806_01422_b200.grid import grid_1d
 
-        E, N, nu = 24, 9, 0.01
+        E, N, nu = 24, 9, 0.01   # >= 8 elements (one ghost zone) per rank up to world 3
         g = grid_1d(-1.0, 1.0, E, N, bc)
         op = sd.ShardedOperator(g, sb.PdeCoefficients(nu), rank, world,
                                 local_factory=CpuLocalOp)
@@ -63,8 +73,6 @@ def _worker(rank, world, port, bc, q):
         # step-count / time grid identical on every rank
         res["steps"] = prob.last_forward.n_steps == timeloop.count_steps(ts)
         q.put((rank, res))
-    finally:
-        dist.destroy_process_group()
 
 
 @pytest.mark.parametrize("world", [2, 3])
@@ -76,7 +84,7 @@ def test_sharded_matches_global(world, bc):
     procs = [ctx.Process(target=_worker, args=(r, world, port, bc, q)) for r in range(world)]
     for p in procs:
         p.start()
-    out = [q.get(timeout=240) for _ in range(world)]
+    out = [q.get(timeout=120) for _ in range(world)]
     for p in procs:
         p.join(timeout=60)
     for rank, res in sorted(out):
