@@ -1,6 +1,10 @@
-"""BASELINE config 5 on ONE GPU: E = 2^25 elements (N = 7, 235M DOF), 500 RK4 steps per
-gradient with binomial checkpointing (s = 64 slots in HBM), L-BFGS on device vectors.
-Prints one JSON line: per-evaluate forward/adjoint times and the optimisation log."""
+"""BASELINE config 5: E = 2^25 elements (N = 7, 235M DOF), 500 RK4 steps per gradient with
+binomial checkpointing (s slots in HBM), L-BFGS on device vectors.  One GPU, or element-
+sharded under torchrun (ghost-zone mode: one NCCL exchange per step, all-reduced dots).
+
+  python tools/bench_cfg5.py [E] [steps] [slots] [iters]
+  torchrun --nproc-per-node 8 --master-addr 127.0.0.1 tools/bench_cfg5.py
+Prints one JSON line (rank 0): per-evaluate time (max over ranks) and the optimisation log."""
 import json
 import os
 import sys
@@ -10,46 +14,81 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_1806_01422_b200 as sb  # noqa: E402
-from paper_1806_01422_b200 import configs  # noqa: E402
+from paper_1806_01422_b200 import configs, timeloop  # noqa: E402
 
 
 def main(E=None, steps=None, slots=None, iters=None):
+    import torch.distributed as dist
+
+    from paper_1806_01422_b200 import dist as sd
+    from paper_1806_01422_b200.grid import grid_1d
     c = configs.CFG5
     E = int(E or c["E"])
     steps = int(steps or c["steps"])
     slots = int(slots or c["slots"])
     iters = int(iters if iters is not None else c["lbfgs_iters"])
+    backend = os.environ.get("SEM1D_DIST_BACKEND")
+    rank, world, local = sd.init_from_env(backend)
+    if os.environ.get("SEM1D_SAME_DEVICE"):
+        local = 0
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
     t0 = time.perf_counter()
-    prob = configs.cfg5_problem(E=E, steps=steps, slots=slots, device="cuda:0")
+    g = grid_1d(0.0, E * c["h"], E, c["N"])
+    coef = sb.PdeCoefficients(c["nu"])
+    if world == 1:
+        prob = configs.cfg5_problem(E=E, steps=steps, slots=slots, device=dev)
+        op = prob.op
+        dot = sb.optimize.default_dot
+    else:
+        op = sd.ShardedOperator(g, coef, rank, world, device=dev)
+        ts = timeloop.TsConfig(scheme="rk4", t0=0.0, t_end=steps * c["dt"], dt=c["dt"])
+        sl = slice(op.part.g_lo, op.part.g_lo + op.part.n_own)
+        u0 = configs.fourier_field_device(g, c["modes"], c["seed"], dev)[sl] / 8.0
+        pert = configs.fourier_field_device(g, c["modes"], c["seed"] + 77, dev)[sl] / 40.0
+        target = timeloop.integrate(op, op.field(u0 + pert)[0], ts, store_steps=None).u_final
+        prob = sb.AssimilationProblem(name="cfg5-sharded", grid=op.grid, op=op, ts=ts,
+                                      u_target=target, u_guess=op.field(u0)[0],
+                                      checkpoint_slots=slots)
+        dot = op.dot
     torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
     times = []
 
     def fun(x):
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         a = time.perf_counter()
-        j, g = prob.evaluate(x)
+        j, gr = prob.evaluate(x)
         torch.cuda.synchronize()
-        times.append(time.perf_counter() - a)
-        return j, g
+        t = torch.tensor([time.perf_counter() - a], dtype=torch.float64,
+                         device=dev if backend != "gloo" else "cpu")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        times.append(float(t.item()))
+        return j, gr
 
     t0 = time.perf_counter()
-    # stop at the reference default gtol (1e-8 relative): past convergence every line
-    # search would burn its 25-evaluation budget at round-off level
-    res = sb.minimize(fun, prob.u_guess, sb.OptimConfig(max_iters=iters, gtol=1e-8))
+    res = sb.minimize(fun, prob.u_guess, sb.OptimConfig(max_iters=iters, gtol=1e-8), dot=dot)
     torch.cuda.synchronize()
     opt_s = time.perf_counter() - t0
-    ndof = prob.grid.nglobal
-    sched = prob.schedule_for(steps)
-    out = {"workload": "BASELINE config 5 (single GPU)", "E": E, "N": c["N"], "dof": ndof,
-           "steps": steps, "slots": slots, "recomputed_steps": sched.recomputed,
-           "setup_s": setup_s, "lbfgs_iterations": res.iterations, "status": res.status,
-           "evaluations": len(times), "evaluate_s_mean": sum(times) / len(times),
-           "evaluate_s_min": min(times), "optimize_s": opt_s,
-           "dof_steps_per_s_forward_equiv": ndof * steps / min(times),
-           "J_log": [r[1] for r in res.log], "gnorm_log": [r[2] for r in res.log],
-           "kernels": "fused whole-step" if prob.op.step_fused_supported() else "per-stage"}
-    print(json.dumps(out))
+    if rank == 0:
+        out = {"workload": "BASELINE config 5", "n_gpus": world, "E": E, "N": c["N"],
+               "dof": E * c["N"], "steps": steps, "slots": slots,
+               "recomputed_steps": prob.schedule_for(steps).recomputed, "setup_s": setup_s,
+               "lbfgs_iterations": res.iterations, "status": res.status,
+               "evaluations": len(times), "evaluate_s_min": min(times),
+               "evaluate_s_mean": sum(times) / len(times), "optimize_s": opt_s,
+               "dof_steps_per_s_forward_equiv": E * c["N"] * steps / min(times),
+               "J_log": [r[1] for r in res.log], "gnorm_log": [r[2] for r in res.log],
+               "kernels": "fused whole-step" if op.step_fused_supported() else "per-stage",
+               "sharding": "single GPU" if world == 1 else
+                           f"{world} ranks, ghost zones of {op.part.zone} elements"}
+        print(json.dumps(out))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":
