@@ -106,3 +106,22 @@ def test_small_ring_sweeps_vs_oracle(cuda, scheme, bc, E, N):
         assert rel_err(fwd.u_final[b].cpu().numpy(), uf) <= 1e-12
         assert abs(float(J[b]) - j_ref) <= 1e-9 * abs(j_ref)
         assert rel_err(g[b].cpu().numpy(), g_ref) <= 1e-9
+
+
+def test_cfg4_full_scale_gradients_vs_oracle(cuda):
+    """BASELINE config 4 at full size (B = 4096, 1000 RK4 steps, 126 GB trajectory in HBM):
+    J and grad J of sampled problems vs the oracle's full 1000-step evaluate (1e-9)."""
+    torch.cuda.empty_cache()
+    prob = configs.cfg4_problem(device="cuda:0")
+    J, g = prob.evaluate(prob.u_guess)
+    assert prob.last_forward.trajectory.shape[0] == 1001
+    c = configs.CFG4
+    ref = R.BurgersOracle(R.Mesh1D(c["xa"], c["xb"], c["E"], c["N"], True), c["nu"])
+    target = prob.target().cpu().numpy()
+    for b in (0, 2047, 4095):
+        j_ref, g_ref, _ = R.evaluate(ref, prob.u_guess[b], target[b], 0.0,
+                                     c["steps"] * c["dt"], c["dt"], "rk4")
+        assert abs(float(J[b]) - j_ref) <= 1e-9 * abs(j_ref)
+        assert rel_err(g[b], g_ref) <= 1e-9
+    del prob, J, g
+    torch.cuda.empty_cache()
