@@ -18,6 +18,14 @@
 
 namespace sem1d {
 
+#ifndef SEM1D_FIN_INT
+#define SEM1D_FIN_INT 1
+#endif
+// non-finite test without a dependency chain: exponent field all ones (Inf / NaN)
+__device__ __forceinline__ unsigned nonfinite_bit(double x) {
+  return ((unsigned)__double2hiint(x) & 0x7ff00000u) == 0x7ff00000u ? 1u : 0u;
+}
+
 struct Tableau {
   double a[4][4];    // a[i][j], j < i
   double b[4];
@@ -56,7 +64,7 @@ template <int N, int WMT_MAX, class BGet, bool WRAP = true>
 __device__ __forceinline__ void ring_rhs(const Consts<N>& C, const Geo& G, const double* src,
                                          double* xfer, BGet bget, const double* minv_a,
                                          double mnu, int warp, int lane,
-                                         double (&kv)[WMT_MAX][(N + 1) / 4], double& fin) {
+                                         double (&kv)[WMT_MAX][(N + 1) / 4], unsigned& fin) {
   constexpr int KC = (N + 1) / 4, NT = (N + 1) / 8, W = EnsCfg<N>::W;
   const int kq = lane & 3, rr = lane >> 2;
   const int E = (int)G.E;
@@ -73,7 +81,11 @@ __device__ __forceinline__ void ring_rhs(const Consts<N>& C, const Geo& G, const
 #pragma unroll
     for (int kc = 0; kc < KC; ++kc) {
       au[kc] = src[base + 4 * kc + kq];
-      fin = fma(au[kc], 0.0, fin);
+#if SEM1D_FIN_INT
+      fin |= nonfinite_bit(au[kc]);
+#else
+      fin |= (au[kc] - au[kc] != 0.0) ? 1u : 0u;
+#endif
     }
     double r[NT][2];
 #pragma unroll
@@ -156,7 +168,7 @@ __global__ void __launch_bounds__(EnsCfg<N, kEnsFwdWarps>::THREADS, 1)
   }
 
   const int mt_total = (int)G.E / 8;
-  double fin = 0.0;
+  unsigned fin = 0u;
   bool bad_step = false;
   double acc[WMT_MAX][KC];
   double kv[WMT_MAX][KC];
@@ -212,7 +224,7 @@ __global__ void __launch_bounds__(EnsCfg<N, kEnsFwdWarps>::THREADS, 1)
   }
   double* uf = A.u_final + b * G.ndof;
   for (int k = tid; k < ndof; k += THREADS) uf[k] = su[k];
-  const bool bad_in = fin != fin;
+  const bool bad_in = fin != 0u;
   if (bad_in || bad_step)
     atomicOr(&A.flags[b], (bad_in ? SEM1D_FLAG_STATE_NONFINITE : 0) | (bad_step ? SEM1D_FLAG_STEP_NONFINITE : 0));
   (void)n;
@@ -326,7 +338,7 @@ __global__ void __launch_bounds__(EnsCfg<N, kEnsAdjWarps>::THREADS, 1)
   const int mt_total = (int)G.E / 8;
   const double* lin = A.lam_in + b * G.ndof;
   for (int k = tid; k < ndof; k += THREADS) slam[k] = lin[k];
-  double fin = 0.0;
+  unsigned fin = 0u;
   double kv[WMT_MAX][KC], lnext[WMT_MAX][KC], lacc[WMT_MAX][KC];
 
   for (int step = A.nsteps - 1; step >= 0; --step) {
@@ -381,7 +393,7 @@ __global__ void __launch_bounds__(EnsCfg<N, kEnsAdjWarps>::THREADS, 1)
           double z = __dmul_rn(A.tab.b[i], slam[g]);
           if (i + 1 < S && A.tab.a[i + 1][i] != 0.0) z = __dadd_rn(z, __dmul_rn(A.tab.a[i + 1][i], lnext[q][kc]));
           if (i + 2 < S && A.tab.a[i + 2][i] != 0.0) z = __dadd_rn(z, __dmul_rn(A.tab.a[i + 2][i], sk[g]));
-          fin = fma(z, 0.0, fin);
+          fin |= nonfinite_bit(z);
           const double zm = __dmul_rn(z, minv_a[kc]);
           sz[g] = zm;
           if (g == 0) sz[ndof] = zm;
@@ -410,7 +422,7 @@ __global__ void __launch_bounds__(EnsCfg<N, kEnsAdjWarps>::THREADS, 1)
   }
   double* lo = A.lam_out + b * G.ndof;
   for (int k = tid; k < ndof; k += THREADS) lo[k] = slam[k];
-  if (fin != fin) atomicOr(&A.flags[b], SEM1D_FLAG_INPUT2_NONFINITE);
+  if (fin) atomicOr(&A.flags[b], SEM1D_FLAG_INPUT2_NONFINITE);
 }
 
 template <int N>
@@ -532,7 +544,7 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
     const TileLoad L = tile_load_plan(blockIdx.x, T, A.H, N, LEN, ndof);
     if (L.bulk) tile_issue(L, LEN, A.u, sbuf, &bar[0], 1, nullptr, nullptr);
   }
-  double fin = 0.0;
+  unsigned fin = 0u;
   bool bad = false;
   uint32_t phase = 0;
   double kv[WMT][KC], acc[WMT][KC];
@@ -563,6 +575,10 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
     for (int st = 0; st < A.tab.s; ++st) {
       const double* src = (st == 0) ? su : sU;
       ring_rhs<N, WMT, decltype(bget), false>(C, Gt, src, xfer, bget, minv_a, mnu, warp, lane, kv, fin);
+      const double tb = A.tab.b[st];
+      const bool last = (st + 1 == A.tab.s);
+      const bool one = !last && A.tab.nterm[st + 1] == 1;
+      const double c1 = last ? 0.0 : __dmul_rn(A.dt, A.tab.a[st + 1][st]);
 #pragma unroll
       for (int q = 0; q < WMT; ++q) {
         const int e = 8 * (warp * WMT + q) + rr;
@@ -572,12 +588,12 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
           if (j == N) continue;
           const int g = e * N + j;
           const double kk = kv[q][kc];
-          const double term = __dmul_rn(A.tab.b[st], kk);
+          const double term = __dmul_rn(tb, kk);
           acc[q][kc] = (st == 0) ? term : __dadd_rn(acc[q][kc], term);
-          if (st + 1 < A.tab.s) {
+          if (!last) {
             double y;
-            if (A.tab.nterm[st + 1] == 1) {
-              y = __dadd_rn(su[g], __dmul_rn(__dmul_rn(A.dt, A.tab.a[st + 1][st]), kk));
+            if (one) {
+              y = __dadd_rn(su[g], __dmul_rn(c1, kk));
             } else {
               double sacc = __dmul_rn(A.tab.a[st + 1][0], (st == 0) ? kk : sk[g]);
               for (int jj = 1; jj <= st; ++jj)
@@ -600,8 +616,8 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
     for (int k = tid; k < nout_el * N; k += 32 * W) A.out[e_out0 * N + k] = sU[A.H * N + k];
     __syncthreads();
   }
-  if (fin != fin || bad)
-    atomicOr(A.flag, (fin != fin ? SEM1D_FLAG_STATE_NONFINITE : 0) | (bad ? SEM1D_FLAG_STEP_NONFINITE : 0));
+  if (fin || bad)
+    atomicOr(A.flag, (fin ? SEM1D_FLAG_STATE_NONFINITE : 0) | (bad ? SEM1D_FLAG_STEP_NONFINITE : 0));
 }
 
 template <int N, int W, int WMT>
@@ -654,7 +670,7 @@ __global__ void __launch_bounds__(32 * W, TILE_ADJ_MINB)
     const TileLoad L = tile_load_plan(blockIdx.x, T, A.H, N, LEN, ndof);
     if (L.bulk) tile_issue(L, LEN, A.u, sbu, &bar[0], 2, A.lam, sbl);
   }
-  double fin = 0.0;
+  unsigned fin = 0u;
   uint32_t phase = 0;
   double kv[WMT][KC], lnext[WMT][KC], lacc[WMT][KC];
   int it = 0;
@@ -722,7 +738,7 @@ __global__ void __launch_bounds__(32 * W, TILE_ADJ_MINB)
           double z = __dmul_rn(A.tab.b[i], slam[g]);
           if (i + 1 < S && A.tab.a[i + 1][i] != 0.0) z = __dadd_rn(z, __dmul_rn(A.tab.a[i + 1][i], lnext[q][kc]));
           if (i + 2 < S && A.tab.a[i + 2][i] != 0.0) z = __dadd_rn(z, __dmul_rn(A.tab.a[i + 2][i], sk[g]));
-          if (e >= A.H && e < A.H + T) fin = fma(z, 0.0, fin);
+          if (e >= A.H && e < A.H + T) fin |= nonfinite_bit(z);
           sz[g] = __dmul_rn(z, minv_a[kc]);
         }
       }
@@ -751,7 +767,7 @@ __global__ void __launch_bounds__(32 * W, TILE_ADJ_MINB)
     for (int k = tid; k < nout_el * N; k += 32 * W) A.out[e_out0 * N + k] = slam[A.H * N + k];
     __syncthreads();
   }
-  if (fin != fin) atomicOr(A.flag, SEM1D_FLAG_INPUT2_NONFINITE);
+  if (fin) atomicOr(A.flag, SEM1D_FLAG_INPUT2_NONFINITE);
 }
 
 template <int N>
