@@ -437,7 +437,7 @@ int sem1d_ens_adjoint(const sem1d_plan* plan, const double* traj, const double* 
 
 int sem1d_step_supported(const sem1d_plan* plan) {
   if (!valid_plan(plan)) return 0;
-  const int te = ((plan->N + 1) == 8) ? 8 * 16 * TILE_WMT8 : ((plan->N + 1) == 32 ? 64 : 128);
+  const int te = ((plan->N + 1) == 8) ? 8 * TILE_WF8 * TILE_WMT8 : ((plan->N + 1) == 32 ? 64 : 128);
   return (plan->periodic && plan->batch == 1 && (plan->N + 1) % 8 == 0 && plan->E >= 2 * te) ? 1 : 0;
 }
 

@@ -442,16 +442,22 @@ constexpr size_t ens_adj_smem_bytes(int ndof) {
 // ============================================================================
 
 #ifndef TILE_MINB8
-#define TILE_MINB8 1
+#define TILE_MINB8 2
 #endif
 #ifndef TILE_WMT8
 #define TILE_WMT8 4
 #endif
 #ifndef TILE_WA8
-#define TILE_WA8 16
+#define TILE_WA8 4
 #endif
-#ifndef TILE_ADJ_MINB
-#define TILE_ADJ_MINB 1
+#ifndef TILE_WF8
+#define TILE_WF8 8
+#endif
+#ifndef TILE_WMTA8
+#define TILE_WMTA8 4
+#endif
+#ifndef TILE_ADJ_MINB8
+#define TILE_ADJ_MINB8 3
 #endif
 
 struct TileStepArgs {
@@ -499,6 +505,8 @@ __device__ __forceinline__ void tile_issue(const TileLoad& L, int LEN, const dou
 // resident CTAs per SM (A/B: a 64-register cap for two CTAs made the n = 8 step 2x slower)
 template <int N>
 constexpr int tile_minb() { return (N + 1) == 8 ? TILE_MINB8 : 1; }
+template <int N>
+constexpr int tile_adj_minb() { return (N + 1) == 8 ? TILE_ADJ_MINB8 : 1; }
 
 template <int N, int W, int WMT>
 __global__ void __launch_bounds__(32 * W, tile_minb<N>())
@@ -621,7 +629,7 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
 }
 
 template <int N, int W, int WMT>
-__global__ void __launch_bounds__(32 * W, TILE_ADJ_MINB)
+__global__ void __launch_bounds__(32 * W, tile_adj_minb<N>())
     tile_adj_kernel(const __grid_constant__ Consts<N> C, const Geo G, const TileStepArgs A) {
   constexpr int KC = (N + 1) / 4, NT = (N + 1) / 8;
   constexpr int TE = 8 * W * WMT;
@@ -772,13 +780,15 @@ __global__ void __launch_bounds__(32 * W, TILE_ADJ_MINB)
 
 template <int N>
 struct TileCfg {
-  // forward: TE = 512 elements for N = 7 (4 m-tiles per warp: more independent DMMA chains
-  // per barrier), 128 for N = 15/23, 64 for N = 31; adjoint: 256 / 128 / 64 (nine slabs
-  // must fit 227 KB)
-  static constexpr int W = (N + 1) == 32 ? 8 : 16;
-  static constexpr int W_A = (N + 1) == 8 ? TILE_WA8 : W;     // adjoint warps
+  // forward: TE = 256 elements for N = 7 (8 warps x 4 m-tiles, 2 CTAs per SM: the second
+  // CTA's DMMA fills the first one's barrier waits; A/B 0.48 vs 0.54 ms per RK4 step at
+  // 16 x 4 x 1), 128 for N = 15/23, 64 for N = 31; adjoint: 128 for N = 7 (4 warps x 4
+  // m-tiles, 3 CTAs per SM; 1.155 vs 1.190 ms at 16 x 2 x 1), 128 / 64 otherwise (nine
+  // slabs must fit the shared memory of the resident CTAs)
+  static constexpr int W = (N + 1) == 32 ? 8 : ((N + 1) == 8 ? TILE_WF8 : 16);
+  static constexpr int W_A = (N + 1) == 8 ? TILE_WA8 : ((N + 1) == 32 ? 8 : 16);  // adjoint warps
   static constexpr int WMT_F = (N + 1) == 8 ? TILE_WMT8 : 1;
-  static constexpr int WMT_A = (N + 1) == 8 ? 256 / (8 * W_A) : 1;
+  static constexpr int WMT_A = (N + 1) == 8 ? TILE_WMTA8 : 1;
   static constexpr int TE_F = 8 * W * WMT_F;
   static constexpr int TE_A = 8 * W_A * WMT_A;
   static constexpr int PAD_F = ((TE_F * N + 1 + 2) + 1) & ~1;
