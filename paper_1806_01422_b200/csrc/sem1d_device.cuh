@@ -90,7 +90,19 @@ struct Tile {
   __device__ static __forceinline__ int sidx(int k) { return PAD ? k + k / N : k; }
 };
 
+// non-finite test without a DFMA dependency chain: exponent field all ones (Inf / NaN).
+// Integer pipe, so it does not compete with DMMA for the FP64 pipe.
+__device__ __forceinline__ unsigned nonfinite_bit(double x) {
+  return ((unsigned)__double2hiint(x) & 0x7ff00000u) == 0x7ff00000u ? 1u : 0u;
+}
+#ifndef SEM1D_NONFINITE_INT
+#define SEM1D_NONFINITE_INT 1
+#endif
+#if SEM1D_NONFINITE_INT
+__device__ __forceinline__ bool nonfinite(double v) { return nonfinite_bit(v) != 0u; }
+#else
 __device__ __forceinline__ bool nonfinite(double v) { return !isfinite(v); }
+#endif
 
 // One output row i of the element operator.  x = u, y = v or zm, t = u o zm.
 template <int N, int OP>
@@ -888,6 +900,19 @@ __global__ void __launch_bounds__(MmaTile<N>::THREADS, MmaTile<N>::MINB)
 // CTA-wide barrier inside the tile loop.
 // ============================================================================
 
+#ifndef WS_FIN_INT
+#define WS_FIN_INT 1
+#endif
+#if WS_FIN_INT
+typedef unsigned ws_fin_t;
+#define WS_FIN_ACC(acc, x) (acc) |= nonfinite_bit(x)
+#define WS_FIN_BAD(acc) ((acc) != 0u)
+#else
+typedef double ws_fin_t;
+#define WS_FIN_ACC(acc, x) (acc) = fma((x), 0.0, (acc))
+#define WS_FIN_BAD(acc) ((acc) != (acc))
+#endif
+
 #ifndef WS_ELEMS8
 #define WS_ELEMS8 256
 #endif
@@ -903,6 +928,17 @@ __global__ void __launch_bounds__(MmaTile<N>::THREADS, MmaTile<N>::MINB)
 #ifndef WS_MINB_J8
 #define WS_MINB_J8 3
 #endif
+// output staging buffers: 2 lets a warp compute tile t+1 while the bulk store of
+// tile t still reads its staging (F has the shared memory to spare)
+#ifndef WS_OUTB_F
+#define WS_OUTB_F 2
+#endif
+#ifndef WS_OUTB_J
+#define WS_OUTB_J 1
+#endif
+template <int OP>
+constexpr int ws_outb() { return OP == OP_RHS ? WS_OUTB_F : WS_OUTB_J; }
+
 template <int N, int OP>
 constexpr int ws_minb() {
   return ((N + 1) > 16) ? 1 : ((N + 1) == 16 ? 2 : (OP == OP_RHS ? WS_MINB_F8 : WS_MINB_J8));
@@ -964,8 +1000,8 @@ template <int N, int OP, bool EDGE, class BGet>
 __device__ __forceinline__ void mtile_compute(const Consts<N>& C, const Geo& G, const double* su,
                                               const double* sw, int base, int64_t eg,
                                               const double* minv_a, const double (*minv_p)[2],
-                                              double mnu, int kq, BGet bget, double& fin_u,
-                                              double& fin_w, double (&r)[(N + 1) / 8][2]) {
+                                              double mnu, int kq, BGet bget, ws_fin_t& fin_u,
+                                              ws_fin_t& fin_w, double (&r)[(N + 1) / 8][2]) {
   constexpr int n = N + 1, NT = n / 8, KC = n / 4;
   const bool eslow = EDGE && (eg == 0 || eg == G.E - 1);
   double au[KC], aw[(OP != OP_RHS) ? KC : 1], at[(OP == OP_JACT) ? KC : 1];
@@ -973,10 +1009,10 @@ __device__ __forceinline__ void mtile_compute(const Consts<N>& C, const Geo& G, 
   for (int kc = 0; kc < KC; ++kc) {
     const int j = 4 * kc + kq;
     au[kc] = su[base + j];
-    fin_u = fma(au[kc], 0.0, fin_u);   // NaN/Inf * 0 = NaN: one DFMA per value
+    WS_FIN_ACC(fin_u, au[kc]);
     if (OP != OP_RHS) {
       aw[kc] = sw[base + j];
-      fin_w = fma(aw[kc], 0.0, fin_w);
+      WS_FIN_ACC(fin_w, aw[kc]);
       if (OP == OP_JACT) {
         aw[kc] = eslow ? jt_scale<N>(C, aw[kc], j, eg, G) : __dmul_rn(aw[kc], minv_a[kc]);
         at[kc] = __dmul_rn(au[kc], aw[kc]);
@@ -1018,8 +1054,9 @@ __global__ void __launch_bounds__(WsTile<N>::THREADS, ws_minb<N, OP>())
   constexpr int SA = W::SLAB_ALLOC;
   extern __shared__ __align__(16) double smem[];
   double* stage_buf = smem;                                   // [STAGES][NIN][SA]
-  double* ostage = smem + STAGES * NIN * SA;                  // [OUT]
-  double* hrow = ostage + W::OUT;                             // [STAGES][CW] warp halo rows
+  constexpr int OUTB = ws_outb<OP>();
+  double* ostage = smem + STAGES * NIN * SA;                  // [OUTB][OUT]
+  double* hrow = ostage + OUTB * W::OUT;                      // [STAGES][CW] warp halo rows
   double* bsm = hrow + STAGES * W::CW;                        // B fragments (n = 32)
   uint64_t* full = reinterpret_cast<uint64_t*>(bsm + (W::B_IN_SMEM ? NMAT * NT * KC * 32 : 0));
   uint64_t* empty = full + STAGES;
@@ -1078,7 +1115,7 @@ __global__ void __launch_bounds__(WsTile<N>::THREADS, ws_minb<N, OP>())
       minv_p[nt][h] = C.minv[(i == 0 || i == N) ? 0 : i];
     }
   const double minv_if = C.minv[0];
-  double fin_u = 0.0, fin_w = 0.0;
+  ws_fin_t fin_u = 0, fin_w = 0;
   bool bad_y = false;
 
   // ------------------------------------------------------------------ producer
@@ -1178,7 +1215,7 @@ __global__ void __launch_bounds__(WsTile<N>::THREADS, ws_minb<N, OP>())
         const int64_t eh = e0 + wq * WE - 1;
         const int64_t ehw = (eh < 0) ? G.E - 1 : eh;
         double r[NT][2];
-        double du_ = 0.0, dw_ = 0.0;
+        ws_fin_t du_ = 0, dw_ = 0;
         if (!periodic && (tl == 0 || tl == tiles_per_ring - 1))
           mtile_compute<N, OP, true>(C, G, su, sw, wq * WE * N, ehw, minv_a, minv_p, mnu, kq, bget, du_, dw_, r);
         else
@@ -1194,7 +1231,6 @@ __global__ void __launch_bounds__(WsTile<N>::THREADS, ws_minb<N, OP>())
   }
 
   // ------------------------------------------------------------------ consumers
-  double* wout = ostage + warp * WE * N;            // this warp's contiguous node staging
   int it = 0;
   int tl = blockIdx.x % tiles_per_ring;
   int bidx = blockIdx.x / tiles_per_ring;
@@ -1209,10 +1245,11 @@ __global__ void __launch_bounds__(WsTile<N>::THREADS, ws_minb<N, OP>())
     const double* sw = stage_buf + (s * NIN + 1) * SA + sh;
     const int wel0 = warp * WE;
     const int wnel = min(WE, nel - wel0);
+    double* wout = ostage + (it % OUTB) * W::OUT + warp * WE * N;   // this warp's node staging
     while (!mbar_try_wait(&full[s], (it / STAGES) & 1)) {
     }
     if (wnel > 0) {
-      if (lane == 0) bulk_wait_read<0>();   // previous store out of `wout` has drained
+      if (lane == 0) bulk_wait_read<OUTB - 1>();   // the store out of this buffer has drained
       __syncwarp();
       double carry = 0.0;
       auto body = [&](auto edge_tag) {
@@ -1319,6 +1356,9 @@ __global__ void __launch_bounds__(WsTile<N>::THREADS, ws_minb<N, OP>())
           }
         }
         __syncwarp();
+        // an empty group keeps one commit per tile, so wait_group.read<OUTB-1> above
+        // always refers to the store out of the buffer about to be reused
+        if (OUTB > 1 && lane == 0) bulk_commit();
       }
     }
     tl += gridDim.x;
@@ -1328,7 +1368,7 @@ __global__ void __launch_bounds__(WsTile<N>::THREADS, ws_minb<N, OP>())
     }
   }
   if (lane == 0) bulk_wait_all();
-  const bool bad_u = fin_u != fin_u, bad_w = fin_w != fin_w;
+  const bool bad_u = WS_FIN_BAD(fin_u), bad_w = WS_FIN_BAD(fin_w);
   if (bad_u || bad_w || bad_y)
     atomicOr(A.flag, (bad_u ? SEM1D_FLAG_STATE_NONFINITE : 0) |
                          (bad_w ? SEM1D_FLAG_INPUT2_NONFINITE : 0) |
@@ -1346,7 +1386,7 @@ constexpr int ws_stages() {
   constexpr int mb = ws_minb<N, OP>();
   constexpr int budget = (mb == 1 ? 180 : (mb == 2 ? 104 : (mb == 3 ? 72 : (mb == 4 ? 54 : 44)))) * 1024;
   constexpr int per = NIN * W::SLAB_ALLOC * 8;
-  constexpr int st = (budget - W::OUT * 8 - (W::B_IN_SMEM ? 3 * W::NT * W::KC * 32 * 8 : 0)) / per;
+  constexpr int st = (budget - ws_outb<OP>() * W::OUT * 8 - (W::B_IN_SMEM ? 3 * W::NT * W::KC * 32 * 8 : 0)) / per;
   return st < 2 ? 2 : (st > 8 ? 8 : st);
 }
 
@@ -1355,7 +1395,7 @@ constexpr size_t ws_smem_bytes() {
   using W = WsTile<N>;
   constexpr int NIN = (OP == OP_RHS) ? 1 : 2;
   constexpr int NMAT = (OP == OP_JACT) ? 3 : 2;
-  return sizeof(double) * ((size_t)STAGES * NIN * W::SLAB_ALLOC + W::OUT + STAGES * W::CW +
+  return sizeof(double) * ((size_t)STAGES * NIN * W::SLAB_ALLOC + ws_outb<OP>() * W::OUT + STAGES * W::CW +
                            (W::B_IN_SMEM ? NMAT * W::NT * W::KC * 32 : 0)) +
          sizeof(uint64_t) * 3 * STAGES;
 }

@@ -21,10 +21,6 @@ namespace sem1d {
 #ifndef SEM1D_FIN_INT
 #define SEM1D_FIN_INT 1
 #endif
-// non-finite test without a dependency chain: exponent field all ones (Inf / NaN)
-__device__ __forceinline__ unsigned nonfinite_bit(double x) {
-  return ((unsigned)__double2hiint(x) & 0x7ff00000u) == 0x7ff00000u ? 1u : 0u;
-}
 
 struct Tableau {
   double a[4][4];    // a[i][j], j < i
