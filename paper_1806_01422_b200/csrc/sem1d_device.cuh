@@ -959,13 +959,17 @@ __device__ __forceinline__ double bfrag_perm(const Consts<N>& C, int mat, int nt
   return C.Dw[j * n + i];
 }
 
-template <int N>
+#ifndef WS_ELEMS8_J
+#define WS_ELEMS8_J WS_ELEMS8
+#endif
+template <int N, int OP = OP_RHS>
 struct WsTile {
   static constexpr int n = N + 1;
   // consumer warps: 16 for n = 32 (FP64-bound, latency hidden by more warps), else 8
   static constexpr int CW = (n == 32) ? WS_CW32 : 8;
   static constexpr int THREADS = 32 * (CW + 1);
-  static constexpr int ELEMS = (n == 8) ? WS_ELEMS8 : (n == 32 ? 8 * CW : MmaTile<N>::ELEMS);
+  static constexpr int ELEMS =
+      (n == 8) ? (OP == OP_RHS ? WS_ELEMS8 : WS_ELEMS8_J) : (n == 32 ? 8 * CW : MmaTile<N>::ELEMS);
   static constexpr int WE = ELEMS / CW;                          // elements per consumer warp
   static constexpr int WMT = WE / 8;                             // m-tiles per warp
   static constexpr int NT = n / 8, KC = n / 4;
@@ -1043,10 +1047,10 @@ __device__ __forceinline__ void mtile_compute(const Consts<N>& C, const Geo& G, 
 }
 
 template <int N, int OP, int EPI, int STAGES>
-__global__ void __launch_bounds__(WsTile<N>::THREADS, ws_minb<N, OP>())
+__global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
     apply_ws_kernel(const __grid_constant__ Consts<N> C, const Geo G, const Args A,
                     const int tiles_per_ring, const int total_tiles) {
-  using W = WsTile<N>;
+  using W = WsTile<N, OP>;
   constexpr int n = N + 1;
   constexpr int ELEMS = W::ELEMS, WE = W::WE, WMT = W::WMT, NT = W::NT, KC = W::KC;
   constexpr int NIN = (OP == OP_RHS) ? 1 : 2;
@@ -1380,7 +1384,7 @@ __global__ void __launch_bounds__(WsTile<N>::THREADS, ws_minb<N, OP>())
 // >= 64 KB outstanding per SM (Little's law).
 template <int N, int OP>
 constexpr int ws_stages() {
-  using W = WsTile<N>;
+  using W = WsTile<N, OP>;
   constexpr int NIN = (OP == OP_RHS) ? 1 : 2;
   // shared-memory budget that keeps ws_minb CTAs resident (227 KB per SM)
   constexpr int mb = ws_minb<N, OP>();
@@ -1392,7 +1396,7 @@ constexpr int ws_stages() {
 
 template <int N, int OP, int STAGES>
 constexpr size_t ws_smem_bytes() {
-  using W = WsTile<N>;
+  using W = WsTile<N, OP>;
   constexpr int NIN = (OP == OP_RHS) ? 1 : 2;
   constexpr int NMAT = (OP == OP_JACT) ? 3 : 2;
   return sizeof(double) * ((size_t)STAGES * NIN * W::SLAB_ALLOC + ws_outb<OP>() * W::OUT + STAGES * W::CW +

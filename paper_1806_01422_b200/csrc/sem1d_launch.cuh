@@ -110,18 +110,18 @@ static cudaError_t launch_ws(const PlanView& p, const Args& a, cudaStream_t s) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       int per_sm = 0;
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WsTile<N>::THREADS, smem);
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WsTile<N, OP>::THREADS, smem);
       if (e != cudaSuccess) return e;
       int dev = 0, sms = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       max_resident = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
     }
-    const int64_t per_ring = (p.geo.E + WsTile<N>::ELEMS - 1) / WsTile<N>::ELEMS;
+    const int64_t per_ring = (p.geo.E + WsTile<N, OP>::ELEMS - 1) / WsTile<N, OP>::ELEMS;
     const int64_t total = per_ring * p.batch;
     if (total > 0x7fffffffLL) return cudaErrorInvalidValue;
     const int grid = (int)(total < max_resident ? total : max_resident);
-    kern<<<grid, WsTile<N>::THREADS, smem, s>>>(*static_cast<const Consts<N>*>(p.consts), p.geo, a,
+    kern<<<grid, WsTile<N, OP>::THREADS, smem, s>>>(*static_cast<const Consts<N>*>(p.consts), p.geo, a,
                                                 (int)per_ring, (int)total);
     return cudaGetLastError();
   }
