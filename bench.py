@@ -320,8 +320,7 @@ def run_gpu_arm(args):
     def e2e_step():
         if streaming:
             # public streaming API: element-chunked H2D / kernels / D2H overlap
-            r = op.apply_host(uh, vh, wh)
-            oh[0], oh[1], oh[2] = r["rhs"], r["jac"], r["jact"]
+            op.apply_host(uh, vh, wh, out={"rhs": oh[0], "jac": oh[1], "jact": oh[2]})
             return
         du = uh.to(dev, non_blocking=True)
         dv = vh.to(dev, non_blocking=True)

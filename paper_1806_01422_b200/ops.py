@@ -280,11 +280,13 @@ class SemOperator:
             self.raise_for_flags(("state", "cotangent"))
         return self._out(out, host)
 
-    def apply_host(self, u, v=None, w=None, kinds=None, chunks=8):
+    def apply_host(self, u, v=None, w=None, kinds=None, chunks=8, out=None, slots=3):
         """F(u), J(u) v, J(u)^T w on HOST fields (pinned CPU tensors or numpy), streamed
         through the GPU in element chunks with copy/compute overlap (see HostStreamer).
         Returns a dict {"rhs", "jac", "jact"} of pinned CPU tensors (numpy for numpy
-        input); raises NumericFailure like apply_* on non-finite input."""
+        input); ``out`` may supply some of them (float64 host tensors of the field's
+        shape, pinned for overlap).  Raises NumericFailure like apply_* on non-finite
+        input."""
         import torch
         if self.batch != 1:
             raise ValidationError("apply_host needs batch == 1")
@@ -300,12 +302,17 @@ class SemOperator:
         u, v, w = prep(u, "state"), prep(v, "tangent"), prep(w, "cotangent")
         if kinds is None:
             kinds = ["rhs"] + (["jac"] if v is not None else []) + (["jact"] if w is not None else [])
-        key = ("_streamer", chunks)
+        if out:
+            for k, t in out.items():
+                if (not isinstance(t, torch.Tensor) or t.is_cuda or t.dtype != torch.float64
+                        or tuple(t.shape) != self.shape):
+                    raise ValidationError(f"out[{k!r}] must be a float64 host tensor of shape {self.shape}")
+        key = ("_streamer", chunks, slots)
         st = self.__dict__.get(key)
         if st is None:
-            st = HostStreamer(self, chunks)
+            st = HostStreamer(self, chunks, slots)
             self.__dict__[key] = st
-        outs = st.run(tuple(kinds), u, v, w)
+        outs = st.run(tuple(kinds), u, v, w, outs=out)
         torch.cuda.current_stream(self.device).synchronize()
         fl = int(st.flag.item())
         if fl & _lib.SEM1D_FLAG_STATE_NONFINITE:
@@ -351,7 +358,7 @@ class HostStreamer:
     step costs max(H2D, D2H) instead of H2D + compute + D2H.  Inputs should be pinned
     CPU tensors (numpy arrays are staged through pinned buffers)."""
 
-    def __init__(self, op, chunks=8):
+    def __init__(self, op, chunks=8, slots=3):
         import torch
 
         from .dist import Partition, shard_grid
@@ -380,7 +387,11 @@ class HostStreamer:
         self.s_h2d = torch.cuda.Stream(dev)
         self.s_cmp = torch.cuda.Stream(dev)
         self.s_d2h = torch.cuda.Stream(dev)
-        self.slots = [{} for _ in range(2)]
+        # device buffer sets: chunk c reuses set c % S once chunk c - S has left the
+        # device, so S >= 3 keeps the H2D engine from waiting on the D2H of the
+        # chunk just before it
+        self.nslots = max(2, int(slots))
+        self.slots = [{} for _ in range(self.nslots)]
 
     def _buf(self, slot, name):
         import torch
@@ -407,31 +418,37 @@ class HostStreamer:
         import torch
         sync_copy = not u.is_pinned()   # pageable input: the copy engine cannot overlap it
         ins = {"u": u, "v": v, "w": w}
-        if outs is None:
-            outs = {k: torch.empty(self.ndof, dtype=torch.float64, pin_memory=True) for k in kinds}
+        outs = dict(outs or {})
+        for k in kinds:
+            if k not in outs:
+                outs[k] = torch.empty(self.ndof, dtype=torch.float64, pin_memory=True)
         need = ["u"] + (["v"] if "jac" in kinds else []) + (["w"] if "jact" in kinds else [])
-        ev_in = [torch.cuda.Event() for _ in range(self.C)]
-        ev_out = [torch.cuda.Event() for _ in range(self.C)]
+        uses = {"rhs": ("u",), "jac": ("u", "v"), "jact": ("u", "w")}
+        ev_in = [{nm: torch.cuda.Event() for nm in need} for _ in range(self.C)]
+        ev_out = [{k: torch.cuda.Event() for k in kinds} for _ in range(self.C)]
         ev_free = [torch.cuda.Event() for _ in range(self.C)]
         cur = torch.cuda.current_stream(self.op.device)
         self.s_h2d.wait_stream(cur)
         self.flag.zero_()
+        S = self.nslots
         for c, p in enumerate(self.parts):
-            slot = c % 2
+            slot = c % S
             op = self.ops[c]
+            # per-field events: F(chunk c) starts, and its D2H leaves, as soon as u has
+            # arrived, while v and w of the same chunk are still on the H2D engine
             with torch.cuda.stream(self.s_h2d):
-                if c >= 2:
-                    self.s_h2d.wait_event(ev_free[c - 2])      # slot's previous D2H done
+                if c >= S:
+                    self.s_h2d.wait_event(ev_free[c - S])      # slot's previous D2H done
                 for name in need:
                     dst = self._buf(slot, name)
                     for off, g, ln in self._ranges(p):
                         dst[off:off + ln].copy_(ins[name][g:g + ln], non_blocking=not sync_copy)
-                ev_in[c].record(self.s_h2d)
+                    ev_in[c][name].record(self.s_h2d)
             with torch.cuda.stream(self.s_cmp):
-                self.s_cmp.wait_event(ev_in[c])
                 n = p.ext_ndof
                 ub = self._buf(slot, "u")[:n]
                 for k in kinds:
+                    self.s_cmp.wait_event(ev_in[c][uses[k][-1]])   # fields arrive in `need` order
                     ob = self._buf(slot, "o_" + k)[:n]
                     if k == "rhs":
                         op.launch_rhs(ub, ob)
@@ -439,11 +456,11 @@ class HostStreamer:
                         op.launch_jac(ub, self._buf(slot, "v")[:n], ob)
                     else:
                         op.launch_jact(ub, self._buf(slot, "w")[:n], ob)
-                ev_out[c].record(self.s_cmp)
+                    ev_out[c][k].record(self.s_cmp)
             with torch.cuda.stream(self.s_d2h):
-                self.s_d2h.wait_event(ev_out[c])
                 sl = p.owned_slice()
                 for k in kinds:
+                    self.s_d2h.wait_event(ev_out[c][k])
                     outs[k][p.g_lo:p.g_lo + p.n_own].copy_(self._buf(slot, "o_" + k)[sl],
                                                            non_blocking=True)
                 ev_free[c].record(self.s_d2h)

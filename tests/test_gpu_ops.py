@@ -230,6 +230,11 @@ def test_host_streaming_apply(cuda, E, N, bc):
         assert rel_err(out[k].numpy(), ref.cpu().numpy()) <= 1e-14
     npout = op.apply_host(u, kinds=["rhs"])
     assert np.array_equal(npout["rhs"], out["rhs"].numpy())
+    for slots in (2, 4):       # caller-provided outputs, other buffer-set counts
+        given = {k: torch.full((op.ndof,), 7.0, dtype=torch.float64).pin_memory() for k in out}
+        r = op.apply_host(uh, vh, wh, out=given, slots=slots, chunks=5)
+        for k in out:
+            assert r[k] is given[k] and torch.equal(given[k], out[k])
     bad = u.copy()
     bad[E] = np.nan
     with pytest.raises(sb.NumericFailure):

@@ -1,4 +1,4 @@
-"""Chunk-count sweep of SemOperator.apply_host on config 2, plus raw PCIe H2D / D2H / duplex."""
+"""Slot / chunk-count sweep of SemOperator.apply_host on config 2, plus raw PCIe H2D / D2H / duplex."""
 import json
 import os
 import sys
@@ -41,9 +41,13 @@ def main():
         torch.cuda.current_stream().wait_stream(s1)
         torch.cuda.current_stream().wait_stream(s2)
     res["duplex_GBs_each_way"] = op.ndof * 8 / t_ms(duplex) / 1e6
-    for ch in (4, 8, 16, 32, 64):
-        ms = t_ms(lambda: op.apply_host(uh, vh, wh, chunks=ch), reps=3)
-        res[f"apply_host_chunks{ch}_ms"] = ms
+    outs = {k: torch.empty(op.ndof, dtype=torch.float64).pin_memory() for k in ("rhs", "jac", "jact")}
+    for sl in (2, 3):
+        for ch in (4, 6, 8, 12):
+            ms = t_ms(lambda: op.apply_host(uh, vh, wh, chunks=ch, slots=sl, out=outs), reps=3)
+            res[f"apply_host_slots{sl}_chunks{ch}_ms"] = ms
+    ms = t_ms(lambda: op.apply_host(uh, vh, wh), reps=3)
+    res["apply_host_default_fresh_outputs_ms"] = ms
     print(json.dumps(res))
 
 
