@@ -637,7 +637,6 @@ __global__ void __launch_bounds__(MmaTile<N>::THREADS, MmaTile<N>::MINB)
   const int lane = tid & 31;
   const int warp = tid >> 5;
   const bool periodic = G.periodic != 0;
-  const int64_t last_node = G.E * N;
   const double mnu = -C.nu;
 
   // ---- B fragments (constant per CTA)
@@ -1051,7 +1050,6 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
     apply_ws_kernel(const __grid_constant__ Consts<N> C, const Geo G, const Args A,
                     const int tiles_per_ring, const int total_tiles) {
   using W = WsTile<N, OP>;
-  constexpr int n = N + 1;
   constexpr int ELEMS = W::ELEMS, WE = W::WE, WMT = W::WMT, NT = W::NT, KC = W::KC;
   constexpr int NIN = (OP == OP_RHS) ? 1 : 2;
   constexpr int NMAT = (OP == OP_JACT) ? 3 : 2;
