@@ -155,6 +155,45 @@ def sweep_fixture(grid, ops, timeloop, adjoint, checkpoint, problems, optimize):
     return out
 
 
+IMPLICIT_CASES = [
+    # (key, bc, scheme, adaptive, t_end, dt, extra TsConfig kwargs, checkpoint slots)
+    ("cn_periodic", "periodic", "cn", False, 10 * 1e-3, 1e-3, {}, None),
+    ("cn_dirichlet", "dirichlet0", "cn", False, 10 * 1e-3, 1e-3, {}, None),
+    ("cn_binom", "periodic", "cn", False, 12 * 1e-3, 1e-3, {}, 3),
+    ("cn_stiff", "periodic", "cn", False, 4 * 2e-2, 2e-2, {"gmres_restart": 8}, None),
+    ("ad_rms", "periodic", "rk3", True, 2e-2, 1e-3, {"tol_a": 1e-7, "tol_r": 1e-7}, None),
+    ("ad_max", "dirichlet0", "rk3", True, 2e-2, 5e-4, {"tol_a": 1e-6, "tol_r": 1e-6,
+                                                      "wlte_form": "max"}, 4),
+]
+
+
+def implicit_fixture(grid, ops, timeloop, problems):
+    """Crank-Nicolson (Newton + scipy GMRES, timeloop.py:154-186 / adjoint.py:64-69) and
+    adaptive Kutta-3 (controller timeloop.py:198-218) runs on config-1 inputs."""
+    out = {}
+    for key, bc, scheme, adaptive, t_end, dt, kw, slots in IMPLICIT_CASES:
+        g, u0, uo0 = cfg1_inputs(grid, bc)
+        op = ops.SemOperator(g, ops.PdeCoefficients(0.01))
+        ts = timeloop.TsConfig(scheme=scheme, t0=0.0, t_end=t_end, dt=dt, adaptive=adaptive, **kw)
+        tgt_run = timeloop.integrate(op, uo0, ts, store_steps=None, keep_log=True)
+        target = tgt_run.u_final
+        prob = problems.AssimilationProblem(name=key, grid=g, op=op, ts=ts, u_target=target,
+                                            u_guess=u0, checkpoint_slots=slots)
+        j, gr = prob.evaluate(u0)
+        fwd = prob.last_forward
+        out[f"u0_{key}"], out[f"target_{key}"] = u0, target
+        out[f"J_{key}"], out[f"grad_{key}"] = np.array([j]), gr
+        out[f"ufinal_{key}"], out[f"dts_{key}"], out[f"ts_{key}"] = fwd.u_final, fwd.dts, fwd.ts
+        st = fwd.stats
+        out[f"fstats_{key}"] = np.array([st["steps"], st["rejects"], st["retries"],
+                                         st["newton_iters"], st["gmres_iters"]])
+        sw = op.last_sweep_stats
+        out[f"sstats_{key}"] = np.array([sw["newton_iters"], sw["gmres_iters"], sw["recomputed"]])
+        out[f"tlog_{key}"] = np.array(tgt_run.step_log, dtype=float).reshape(-1, 5)
+        out[f"tdts_{key}"] = tgt_run.dts
+    return out
+
+
 SCHED_CASES = [(1, 1), (3, 3), (5, 2), (10, 3), (20, 4), (30, 5), (100, 10), (57, 7), (500, 64)]
 
 
@@ -188,6 +227,8 @@ def main():
     np.savez_compressed(os.path.join(HERE, "sweeps.npz"),
                         **sweep_fixture(grid, ops, timeloop, adjoint, checkpoint, problems, optimize))
     np.savez_compressed(os.path.join(HERE, "schedules.npz"), **schedules_fixture(checkpoint))
+    np.savez_compressed(os.path.join(HERE, "implicit.npz"),
+                        **implicit_fixture(grid, ops, timeloop, problems))
     print("golden fixtures written to", HERE)
 
 

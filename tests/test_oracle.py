@@ -149,3 +149,45 @@ def test_binomial_dp_matches_reference_counts():
     s = golden("schedules.npz")
     for m, slots in [(10, 3), (20, 4), (30, 5), (100, 10), (57, 7)]:
         assert R.binomial_recompute_table(m, slots) - m == s[f"meta_{m}_{slots}"][0]
+
+
+# Crank-Nicolson / adaptive Kutta-3 cases of tests/golden/make_golden.py (IMPLICIT_CASES):
+# key -> (periodic, scheme, adaptive, t_end, dt, TsConfig overrides)
+IMPLICIT = {
+    "cn_periodic": (True, "cn", False, 10 * 1e-3, 1e-3, {}),
+    "cn_dirichlet": (False, "cn", False, 10 * 1e-3, 1e-3, {}),
+    "cn_stiff": (True, "cn", False, 4 * 2e-2, 2e-2, {"gmres_restart": 8}),
+    "ad_rms": (True, "rk3", True, 2e-2, 1e-3, {"tol_a": 1e-7, "tol_r": 1e-7}),
+    "ad_max": (False, "rk3", True, 2e-2, 5e-4, {"tol_a": 1e-6, "tol_r": 1e-6, "wlte_form": "max"}),
+}
+
+
+@pytest.mark.parametrize("key", sorted(IMPLICIT))
+def test_implicit_and_adaptive_bit_exact(key):
+    """CN (Newton + scipy GMRES, timeloop.py:154-186, adjoint.py:64-69) and adaptive RK3
+    (controller timeloop.py:198-218): objective, gradient, final state, accepted dt
+    sequence and the Newton / GMRES / reject counters equal the reference's."""
+    g = golden("implicit.npz")
+    per, scheme, adaptive, t_end, dt, cfg = IMPLICIT[key]
+    op = R.BurgersOracle(R.Mesh1D(-1.0, 1.0, 16, 9, per), 0.01)
+    j, gr, uf, fs, ss = R.evaluate_general(op, g[f"u0_{key}"], g[f"target_{key}"], 0.0, t_end,
+                                           dt, scheme, adaptive, cfg)
+    assert j == g[f"J_{key}"][0]
+    assert np.array_equal(gr, g[f"grad_{key}"])
+    assert np.array_equal(uf, g[f"ufinal_{key}"])
+    assert [fs[k] for k in ("steps", "rejects", "retries", "newton_iters", "gmres_iters")] == \
+        list(g[f"fstats_{key}"])
+    if scheme == "cn" and key != "cn_binom":
+        assert ss["gmres_iters"] == g[f"sstats_{key}"][1]
+    # the target run's step log (accepted and rejected attempts)
+    _, dts, _, _, log = R.integrate_general(op, _target_ic(per), 0.0, t_end, dt, scheme,
+                                            adaptive, cfg)
+    assert np.array_equal(dts, g[f"tdts_{key}"])
+    assert np.array_equal(np.array(log, dtype=float).reshape(-1, 5), g[f"tlog_{key}"])
+
+
+def _target_ic(periodic):
+    """u_obs0 of make_golden.cfg1_inputs (sin pi x + 0.5 sin 2 pi x, masked)."""
+    mesh = R.Mesh1D(-1.0, 1.0, 16, 9, periodic)
+    x = mesh.coordinates()
+    return mesh.apply_mask(np.sin(np.pi * x) + 0.5 * np.sin(2.0 * np.pi * x))
