@@ -17,6 +17,8 @@
  *                         (J^T apply fused with the stage-adjoint recurrence)
  *   sem1d_terminal     <- terminal_condition                 adjoint.py:33-47
  *   sem1d_scatter / sem1d_gather <- Grid.scatter / Grid.gather  grid.py:165-182
+ *   sem1d_cn_step / sem1d_cn_adjoint_step / sem1d_gmres <- the Crank-Nicolson path
+ *                         timeloop.py:133-186, adjoint.py:64-69 (see below)
  *
  * Conventions (mirror the reference contract, ops.py:216-230):
  *  - every array is fp64 in DEVICE memory owned by the caller; nothing is
@@ -160,6 +162,73 @@ int sem1d_terminal(const sem1d_plan* plan, const double* uN, const double* ud, d
 /* Assembly maps (grid.py:165-182): local blocks are (batch, E, N+1). */
 int sem1d_scatter(const sem1d_plan* plan, const double* u, double* local, void* stream);
 int sem1d_gather(const sem1d_plan* plan, const double* local, double* out, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Implicit path and adaptive Kutta-3 controller.
+ *
+ *   sem1d_cn_step          <- step_cn          timeloop.py:154-186
+ *                             (full Newton, GMRES on I - dt/2 J(v))
+ *   sem1d_cn_adjoint_step  <- adjoint_step_cn  adjoint.py:64-69
+ *   sem1d_gmres            <- _gmres_solve     timeloop.py:133-151 (scipy 1.18.1
+ *                             gmres restated: MGS Arnoldi, Givens, gh-8400 tolerance
+ *                             control, one counted matvec per column + per cycle)
+ *   sem1d_rk_error_norm    <- controller       timeloop.py:198-218 (reduction part)
+ *
+ * Batch-1 plans.  `work` is device memory of sem1d_cn_work_size(plan, restart)
+ * doubles, ZERO-INITIALISED once before first use (it holds a reduction ticket
+ * the kernels leave at zero); a workspace serves one stream at a time.  These
+ * calls synchronise `stream` at the reference's decision points (GMRES inner
+ * stop test, Newton residual test).  Outcomes are reported in `st` (counters are
+ * accumulated, so one stats object can cover a whole sweep). */
+#define SEM1D_CN_OK 0
+#define SEM1D_CN_GMRES_FAILED 1        /* GMRES did not converge -> StepFailure        */
+#define SEM1D_CN_NEWTON_STALLED 2      /* newton_max iterations   -> StepFailure        */
+#define SEM1D_CN_RESIDUAL_NONFINITE 3  /* Newton residual NaN/Inf -> StepFailure        */
+#define SEM1D_CN_INPUT_NONFINITE 4     /* an operator input NaN/Inf -> NumericFailure   */
+
+typedef struct {
+  double newton_tol;   /* TsConfig.newton_tol  (1e-10) */
+  int newton_max;      /* TsConfig.newton_max  (25)    */
+  double gmres_tol;    /* TsConfig.gmres_tol   (1e-10) */
+  int gmres_max;       /* TsConfig.gmres_max   (200)   */
+  int gmres_restart;   /* TsConfig.gmres_restart (30), 1..64 */
+} sem1d_cn_params;
+
+typedef struct {
+  int64_t newton_iters, gmres_iters;              /* the reference's stats counters */
+  int64_t rhs_applies, jac_applies, jact_applies; /* SemOperator.counters increments */
+  int status;                                     /* SEM1D_CN_* of the last call     */
+  int gmres_info;                                 /* scipy info of the failing solve */
+  double last_residual;                           /* |r| at the last Newton test     */
+} sem1d_cn_stats;
+
+int64_t sem1d_cn_work_size(const sem1d_plan* plan, int restart);
+/* v = Crank-Nicolson step of u (v must not alias u). */
+int sem1d_cn_step(const sem1d_plan* plan, const double* u, double* v, double dt,
+                  const sem1d_cn_params* params, double* work, int* flag, sem1d_cn_stats* st,
+                  void* stream);
+/* lam_out = transpose of the CN step map between u_n and u_np1, applied to lam. */
+int sem1d_cn_adjoint_step(const sem1d_plan* plan, const double* u_n, const double* u_np1,
+                          const double* lam, double* lam_out, double dt,
+                          const sem1d_cn_params* params, double* work, int* flag,
+                          sem1d_cn_stats* st, void* stream);
+/* x = GMRES solution of (I + alpha J(p)) x = b, or (I + alpha J(p)^T) x = b if transpose;
+ * st->gmres_info = scipy's info (0 converged, else maxiter; -1 non-finite). */
+int sem1d_gmres(const sem1d_plan* plan, int transpose, const double* p, double alpha,
+                const double* b, double* x, const sem1d_cn_params* params, double* work,
+                int* flag, sem1d_cn_stats* st, void* stream);
+
+/* Deterministic reductions; `work` holds sem1d_reduce_work_size() doubles, zeroed once.
+ * out[0] = x . y */
+int64_t sem1d_reduce_work_size(void);
+int sem1d_vec_dot(int64_t n, const double* x, const double* y, double* work, double* out,
+                  void* stream);
+/* out[0] = sum_i sqrt(r_i) (max_form = 0, the reference's "rms" wlte before /n) or
+ * max_i r_i (max_form = 1), r_i = |u_new - u_hat| / (tol_a + max(|u_new|,|u_hat|) tol_r),
+ * u_hat = u + dt k2 (timeloop.py:124,205-210). */
+int sem1d_rk_error_norm(int64_t n, const double* u_new, const double* u, const double* k2,
+                        double dt, double tol_a, double tol_r, int max_form, double* work,
+                        double* out, void* stream);
 
 #ifdef __cplusplus
 }

@@ -23,6 +23,26 @@ MAX_TERMS = 5
 c_int, c_int64, c_double, c_void_p = ctypes.c_int, ctypes.c_int64, ctypes.c_double, ctypes.c_void_p
 c_dp = ctypes.POINTER(ctypes.c_double)
 
+SEM1D_CN_OK = 0
+SEM1D_CN_GMRES_FAILED = 1
+SEM1D_CN_NEWTON_STALLED = 2
+SEM1D_CN_RESIDUAL_NONFINITE = 3
+SEM1D_CN_INPUT_NONFINITE = 4
+
+
+class CnParams(ctypes.Structure):
+    """sem1d_cn_params (TsConfig's Newton / GMRES settings, timeloop.py:49-53)."""
+    _fields_ = [("newton_tol", c_double), ("newton_max", c_int), ("gmres_tol", c_double),
+                ("gmres_max", c_int), ("gmres_restart", c_int)]
+
+
+class CnStats(ctypes.Structure):
+    """sem1d_cn_stats (accumulating counters + status of the last call)."""
+    _fields_ = [("newton_iters", c_int64), ("gmres_iters", c_int64), ("rhs_applies", c_int64),
+                ("jac_applies", c_int64), ("jact_applies", c_int64), ("status", c_int),
+                ("gmres_info", c_int), ("last_residual", c_double)]
+
+
 # name -> (restype, argtypes); exactly the declarations of include/sem1d.h
 SIGNATURES = {
     "sem1d_version": (c_int, []),
@@ -52,6 +72,19 @@ SIGNATURES = {
     "sem1d_terminal": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "sem1d_scatter": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
     "sem1d_gather": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    "sem1d_cn_work_size": (c_int64, [c_void_p, c_int]),
+    "sem1d_cn_step": (c_int, [c_void_p, c_void_p, c_void_p, c_double, ctypes.POINTER(CnParams),
+                              c_void_p, c_void_p, ctypes.POINTER(CnStats), c_void_p]),
+    "sem1d_cn_adjoint_step": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double,
+                                      ctypes.POINTER(CnParams), c_void_p, c_void_p,
+                                      ctypes.POINTER(CnStats), c_void_p]),
+    "sem1d_gmres": (c_int, [c_void_p, c_int, c_void_p, c_double, c_void_p, c_void_p,
+                            ctypes.POINTER(CnParams), c_void_p, c_void_p, ctypes.POINTER(CnStats),
+                            c_void_p]),
+    "sem1d_reduce_work_size": (c_int64, []),
+    "sem1d_vec_dot": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "sem1d_rk_error_norm": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_double, c_double,
+                                    c_double, c_int, c_void_p, c_void_p, c_void_p]),
 }
 
 _lock = threading.Lock()

@@ -1,5 +1,9 @@
 """Discrete-adjoint backward sweep on the B200 (reference ``semopt/adjoint.py``).
 
+Crank-Nicolson steps transpose through ``sem1d_cn_adjoint_step``: GMRES with J^T
+applications only, (I - dt/2 J(u_{n+1}))^T mu = lam, then lam_n = mu + dt/2 J^T(u_n) mu
+(adjoint.py:64-69).
+
 One adjoint step of an s-stage explicit scheme is 2s-1 fused launches: s-1
 ``sem1d_rk_stage`` kernels recompute the stage states from the checkpointed
 u_n (adjoint.py:56), then s ``sem1d_adj_stage`` kernels run the stage-adjoint
@@ -17,7 +21,7 @@ from __future__ import annotations
 from . import _lib
 from .checkpoint import Advance, AdjointStep, Done, Restore, Store
 from .errors import CheckpointError, NumericFailure, ValidationError
-from .timeloop import TABLEAUX, _require_explicit, check_step_flags, engine_for
+from .timeloop import TABLEAUX, _cn_raise, check_step_flags, engine_for, step_cn
 
 
 def terminal_condition(grid, u_final, u_ref, op=None):
@@ -117,6 +121,25 @@ def adjoint_step(op, u_n, lam, t, dt, scheme, out=None):
     return out
 
 
+def adjoint_step_cn(op, u_n, u_np1, lam, t, dt, cfg, stats=None, out=None):
+    """Transpose of one CN step (adjoint.py:64-69) on the device; ``stats`` receives
+    gmres_iters; GMRES non-convergence raises StepFailure like the reference."""
+    from . import _lib
+    if not hasattr(op, "launch_cn_adjoint_step"):
+        raise ValidationError("Crank-Nicolson runs on a single-device batch-1 SemOperator")
+    un, host = op.field(u_n, "state")
+    up, _ = op.field(u_np1, "state")
+    lt, _ = op.field(lam, "cotangent")
+    out = op.empty() if out is None else out
+    st = _lib.CnStats()
+    op.launch_cn_adjoint_step(un, up, lt, out, dt, cfg, st)
+    op.counters["jact"] += st.jact_applies
+    if stats is not None:
+        stats["gmres_iters"] = stats.get("gmres_iters", 0) + st.gmres_iters
+    _cn_raise(st, "cotangent")
+    return out.cpu().numpy() if host else out
+
+
 def sweep(op, cfg, fwd, schedule, lam_terminal, check_every=1):
     """Backward sweep over a recorded trajectory (adjoint.py:72-158).
 
@@ -125,7 +148,6 @@ def sweep(op, cfg, fwd, schedule, lam_terminal, check_every=1):
     reference (states are never mutated in place), an Advance re-runs the
     recorded dts through the same fused stage kernels (bitwise replay).
     """
-    _require_explicit(cfg)
     m = fwd.n_steps
     if schedule.n_steps != m:
         raise ValidationError(f"schedule covers {schedule.n_steps} steps, trajectory has {m}")
@@ -135,8 +157,10 @@ def sweep(op, cfg, fwd, schedule, lam_terminal, check_every=1):
         return lam.cpu().numpy() if host else lam
     dts = fwd.dts
     stats = {"newton_iters": 0, "gmres_iters": 0, "recomputed": 0}
-    fwd_engine = engine_for(op, cfg.scheme)
-    adj = adjoint_engine_for(op, cfg.scheme)
+    cn = cfg.scheme == "cn"
+    fwd_engine = None if cn else engine_for(op, cfg.scheme)
+    adj = None if cn else adjoint_engine_for(op, cfg.scheme)
+    fused = getattr(fwd, "fused_steps", True)   # replay with the forward run's kernel path
 
     slots, preloaded = {}, True
     for step, slot in schedule.forward_stores.items():
@@ -174,9 +198,13 @@ def sweep(op, cfg, fwd, schedule, lam_terminal, check_every=1):
             u = current[1]
             for n in range(act.start, act.stop):
                 nxt = op.empty()
-                fwd_engine.step(u, dts[n], nxt)
+                if cn:
+                    step_cn(op, u, fwd.ts[n], dts[n], cfg, stats, out=nxt)
+                else:
+                    fwd_engine.step(u, dts[n], nxt, fused=fused)
                 u = nxt
-            check_step_flags(op)
+            if not cn:
+                check_step_flags(op)
             stats["recomputed"] += act.stop - act.start
             current = (act.stop, u)
         elif isinstance(act, AdjointStep):
@@ -187,7 +215,11 @@ def sweep(op, cfg, fwd, schedule, lam_terminal, check_every=1):
                 raise CheckpointError(f"adjoint step {n}: forward state missing")
             if not (succ[0] == n + 1 or n + 1 == m):
                 raise CheckpointError(f"adjoint step {n}: successor state missing")
-            adj.step(current[1], lam, dts[n], spare)
+            if cn:
+                u_np1 = succ[1] if succ[0] == n + 1 else fwd.u_final
+                adjoint_step_cn(op, current[1], u_np1, lam, fwd.ts[n], dts[n], cfg, stats, out=spare)
+            else:
+                adj.step(current[1], lam, dts[n], spare)
             lam, spare = spare, lam
             since_check += 1
             if since_check >= check_every:

@@ -43,13 +43,27 @@ struct sem1d_plan {
 };
 
 namespace {
-
 thread_local std::string g_err;
+}  // namespace
 
-int fail(int code, const std::string& msg) {
+namespace sem1d {
+// shared with the other translation units of the library (sem1d_krylov.cu)
+int set_error(int code, const std::string& msg) {
   g_err = msg;
   return code;
 }
+}  // namespace sem1d
+
+namespace {
+
+int fail(int code, const std::string& msg) { return sem1d::set_error(code, msg); }
+}  // namespace
+
+namespace sem1d {
+int64_t plan_batch(const sem1d_plan* p) { return p ? p->batch : 0; }
+}  // namespace sem1d
+
+namespace {
 
 int cuda_fail(cudaError_t e, const char* where) {
   return fail(SEM1D_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));

@@ -246,6 +246,81 @@ class SemOperator:
                                               self._SCHEME_CODES[scheme], self._flag.data_ptr(),
                                               self._stream()), "sem1d_adj_step")
 
+    # -- implicit path (Crank-Nicolson) --------------------
+
+    def _cn_work(self, restart):
+        """Zero-initialised device workspace for sem1d_cn_* / sem1d_gmres (one per operator)."""
+        torch = _torch()
+        ws = getattr(self, "_cn_ws", None)
+        if ws is None or ws[0] != int(restart):
+            n = _lib.load().sem1d_cn_work_size(self._plan.handle, int(restart))
+            if n < 0:
+                raise ValidationError(f"gmres_restart={restart} outside the kernel limit 1..64")
+            self._cn_ws = (int(restart), torch.zeros(int(n), dtype=torch.float64, device=self.device))
+        return self._cn_ws[1]
+
+    @staticmethod
+    def _cn_params(cfg):
+        return _lib.CnParams(float(cfg.newton_tol), int(cfg.newton_max), float(cfg.gmres_tol),
+                             int(cfg.gmres_max), int(cfg.gmres_restart))
+
+    def _require_single(self, what):
+        if self.batch != 1:
+            raise ValidationError(f"{what} needs a batch-1 operator")
+
+    def launch_cn_step(self, u, v, dt, cfg, st):
+        """v = Crank-Nicolson step of u (timeloop.py:154-186); accumulates into the CnStats st.
+        Synchronises the stream at the reference's Newton / GMRES decision points."""
+        import ctypes
+        self._require_single("Crank-Nicolson")
+        work = self._cn_work(cfg.gmres_restart)
+        self._flag.zero_()
+        p = self._cn_params(cfg)
+        _lib.check(_lib.load().sem1d_cn_step(self._plan.handle, u.data_ptr(), v.data_ptr(), float(dt),
+                                             ctypes.byref(p), work.data_ptr(), self._flag.data_ptr(),
+                                             ctypes.byref(st), self._stream()), "sem1d_cn_step")
+
+    def launch_cn_adjoint_step(self, u_n, u_np1, lam, lam_out, dt, cfg, st):
+        """lam_out = transpose of the CN step map (adjoint.py:64-69)."""
+        import ctypes
+        self._require_single("Crank-Nicolson")
+        work = self._cn_work(cfg.gmres_restart)
+        self._flag.zero_()
+        p = self._cn_params(cfg)
+        _lib.check(_lib.load().sem1d_cn_adjoint_step(
+            self._plan.handle, u_n.data_ptr(), u_np1.data_ptr(), lam.data_ptr(), lam_out.data_ptr(),
+            float(dt), ctypes.byref(p), work.data_ptr(), self._flag.data_ptr(), ctypes.byref(st),
+            self._stream()), "sem1d_cn_adjoint_step")
+
+    def launch_gmres(self, p, alpha, b, x, cfg, st, transpose=False):
+        """x = GMRES solution of (I + alpha J(p)) x = b (or J^T), scipy 1.18.1 semantics."""
+        import ctypes
+        self._require_single("GMRES")
+        work = self._cn_work(cfg.gmres_restart)
+        self._flag.zero_()
+        prm = self._cn_params(cfg)
+        _lib.check(_lib.load().sem1d_gmres(self._plan.handle, 1 if transpose else 0, p.data_ptr(),
+                                           float(alpha), b.data_ptr(), x.data_ptr(), ctypes.byref(prm),
+                                           work.data_ptr(), self._flag.data_ptr(), ctypes.byref(st),
+                                           self._stream()), "sem1d_gmres")
+
+    def rk_error_norm(self, u_new, u, k2, dt, cfg):
+        """Weighted local truncation error of the embedded Kutta-3 pair
+        (timeloop.py:205-210): mean sqrt(ratio) ("rms") or max ratio ("max").  One sync."""
+        torch = _torch()
+        self._require_single("adaptive stepping")
+        if not hasattr(self, "_red"):
+            self._red = torch.zeros(int(_lib.load().sem1d_reduce_work_size()) + 2,
+                                    dtype=torch.float64, device=self.device)
+        out = self._red[-1:]
+        mx = cfg.wlte_form == "max"
+        _lib.check(_lib.load().sem1d_rk_error_norm(
+            self.ndof, u_new.data_ptr(), u.data_ptr(), k2.data_ptr(), float(dt), float(cfg.tol_a),
+            float(cfg.tol_r), 1 if mx else 0, self._red.data_ptr(), out.data_ptr(), self._stream()),
+            "sem1d_rk_error_norm")
+        v = float(out.item())
+        return v if mx else v / self.ndof
+
     # -- reference surface ------------------------------------------------------
 
     def apply_rhs(self, u):

@@ -70,14 +70,17 @@ class AssimilationProblem:
 
     def evaluate(self, u0):
         """(J, dJ/du0) = one forward + one adjoint sweep (problems.py:184-199)."""
-        if self.ts.adaptive:
-            raise ValidationError("adaptive stepping is outside the B200 hot path")
         self.last_forward = None   # release the previous trajectory / checkpoints first
         u0_dev, host = self.op.field(u0, "initial state")
+        if self.ts.adaptive:
+            # problems.py:186-188: the step count is known only afterwards; the sweep
+            # replays the whole schedule from the initial state
+            fwd = timeloop.integrate(self.op, u0_dev, self.ts, store_steps=None)
+            return self._finish(fwd, self.schedule_for(fwd.n_steps), u0, host)
         m = timeloop.count_steps(self.ts)
         sched = self.schedule_for(m)
         fwd = None
-        if (self.use_ensemble and self.checkpoint_slots is None
+        if (self.use_ensemble and self.checkpoint_slots is None and self.ts.scheme != "cn"
                 and hasattr(self.op, "launch_ens_forward")
                 and timeloop.ring_resident_supported(self.op)):
             # the ring fits one CTA: whole forward sweep in one launch, trajectory in HBM
@@ -92,6 +95,10 @@ class AssimilationProblem:
                                      store_steps=sched.forward_stores.keys())
         if fwd.n_steps != m:  # a StepFailure retry changed the time grid
             sched = self.schedule_for(fwd.n_steps)
+        return self._finish(fwd, sched, u0, host)
+
+    def _finish(self, fwd, sched, u0, host):
+        """terminal seed + backward sweep (problems.py:196-199)."""
         j, lam = adjoint.terminal_condition(self.grid, fwd.u_final, self.target(), op=self.op)
         if getattr(fwd, "trajectory", None) is not None:
             g = adjoint.ensemble_sweep(self.op, self.ts, fwd, lam)

@@ -7,8 +7,12 @@ launches and the stage temporaries of ``timeloop.py:111-130`` never exist.
 
 Schemes: the reference's ``euler`` and ``rk3`` (Kutta-3, ``timeloop.py:24-27``)
 with the reference's association order, plus ``rk4`` (classic tableau; absent
-from the reference -- see DESIGN.md).  ``cn`` and adaptive control are outside
-the B200 hot path and raise ValidationError at integrate time.
+from the reference -- see DESIGN.md), and ``cn``: Crank-Nicolson by full Newton
+with GMRES on (I - dt/2 J(v)) (``timeloop.py:133-186``), run natively by
+``sem1d_cn_step`` (Newton + scipy-1.18.1 GMRES restated over the J kernel).
+Adaptive Kutta-3 (``adaptive=True``) uses the embedded midpoint pair and the
+controller of ``timeloop.py:198-218``; the weighted error is one device
+reduction (``sem1d_rk_error_norm``), the accept / dt decision runs on the host.
 
 Host control flow (dt clipping, StepFailure retries with dt halving,
 snapshot selection) replicates ``timeloop.py:221-329`` exactly; the non-finite
@@ -98,10 +102,11 @@ class ForwardResult:
 
 
 def _require_explicit(cfg):
+    """Batched / ring-resident sweeps run fixed-dt explicit schemes only."""
     if cfg.scheme == "cn":
-        raise ValidationError("Crank-Nicolson is outside the B200 hot path (SURVEY.md 8(f))")
+        raise ValidationError("the batched ring-resident sweep runs explicit schemes only")
     if cfg.adaptive:
-        raise ValidationError("adaptive stepping is outside the B200 hot path (SURVEY.md 8(f))")
+        raise ValidationError("the batched ring-resident sweep runs fixed-dt schemes only")
 
 
 def _nonzero_terms(coefs, upto):
@@ -156,11 +161,12 @@ class StepEngine:
         k_out = self._buf(("k", i)) if i in store else None
         self.op.launch_rk_stage(U_in, k_out, base, terms, coefs, dt, Y, check)
 
-    def step(self, u, dt, out):
+    def step(self, u, dt, out, fused=True):
         """Launch one full step u -> out (no host sync): one temporally blocked launch
-        when the ring qualifies, else one fused launch per stage."""
-        fused = getattr(self.op, "step_fused_supported", None)
-        if fused is not None and fused():
+        when the ring qualifies (and ``fused``), else one fused launch per stage, which
+        also leaves the stored slopes (k_2 of Kutta-3 for the embedded pair) in place."""
+        fz = getattr(self.op, "step_fused_supported", None)
+        if fused and fz is not None and fz():
             self.op.launch_rk_step(u, out, dt, self.scheme)
             self.op.counters["rhs"] += self.s
             return
@@ -210,15 +216,98 @@ def check_step_flags(op):
         raise StepFailure("state contains NaN/Inf")
 
 
-def step_forward(op, u, t, dt, cfg, stats=None, out=None, check=True):
+def step_forward(op, u, t, dt, cfg, stats=None, out=None, check=True, fused=True):
     """One step of the configured scheme (timeloop.py:189-195); returns the new state."""
-    _require_explicit(cfg)
     if out is None:
         out = op.empty()
-    engine_for(op, cfg.scheme).step(u, dt, out)
+    if cfg.scheme == "cn":
+        return step_cn(op, u, t, dt, cfg, stats, out=out)
+    engine_for(op, cfg.scheme).step(u, dt, out, fused=fused)
     if check:
         check_step_flags(op)
     return out
+
+
+def step_euler(op, u, t, dt):
+    """One forward-Euler step (timeloop.py:106-108)."""
+    ut, host = op.field(u, "state")
+    out = op.empty()
+    engine_for(op, "euler").step(ut, dt, out)
+    check_step_flags(op)
+    return out.cpu().numpy() if host else out
+
+
+def step_rk3(op, u, t, dt):
+    """One Kutta-3 step; returns (u_new, u_embedded, error_estimate) (timeloop.py:119-130).
+    u_new comes from the per-stage kernels (k_2 stays on the device); the embedded
+    midpoint u + dt k_2 and the difference are formed on the device."""
+    ut, host = op.field(u, "state")
+    e = engine_for(op, "rk3")
+    u_new = op.empty()
+    e.step(ut, dt, u_new, fused=False)
+    check_step_flags(op)
+    u_hat = ut + dt * e._k[("k", 1)]
+    err = u_new - u_hat
+    if host:
+        return u_new.cpu().numpy(), u_hat.cpu().numpy(), err.cpu().numpy()
+    return u_new, u_hat, err
+
+
+def _cn_raise(st, what):
+    """Map sem1d_cn_stats.status to the reference exceptions (timeloop.py:146-186)."""
+    s = st.status
+    if s == _lib.SEM1D_CN_OK:
+        return
+    if s == _lib.SEM1D_CN_GMRES_FAILED:
+        raise StepFailure(f"GMRES did not converge (info={st.gmres_info})",
+                          diagnostics={"gmres_info": st.gmres_info, "gmres_iters": st.gmres_iters})
+    if s == _lib.SEM1D_CN_NEWTON_STALLED:
+        raise StepFailure(f"Newton stalled after {st.newton_iters} iterations "
+                          f"(|r|={st.last_residual:.3e})", diagnostics={"newton_iters": st.newton_iters})
+    if s == _lib.SEM1D_CN_RESIDUAL_NONFINITE:
+        raise StepFailure("residual contains NaN/Inf")
+    raise NumericFailure(f"{what} contains NaN/Inf")
+
+
+def step_cn(op, u, t, dt, cfg, stats=None, out=None):
+    """One Crank-Nicolson step (timeloop.py:154-186) on the device: full Newton with the
+    Jacobian re-evaluated each iteration, unpreconditioned GMRES on (I - dt/2 J(v)).
+    ``stats`` receives newton_iters (successful steps only) and gmres_iters, as in the
+    reference; StepFailure / NumericFailure as the reference raises them."""
+    if not hasattr(op, "launch_cn_step"):
+        raise ValidationError("Crank-Nicolson runs on a single-device batch-1 SemOperator")
+    ut, host = op.field(u, "state")
+    out = op.empty() if out is None else out
+    st = _lib.CnStats()
+    op.launch_cn_step(ut, out, dt, cfg, st)
+    op.counters["rhs"] += st.rhs_applies
+    op.counters["jac"] += st.jac_applies
+    if stats is not None:
+        stats["gmres_iters"] = stats.get("gmres_iters", 0) + st.gmres_iters
+    _cn_raise(st, "state")
+    if stats is not None:
+        stats["newton_iters"] = stats.get("newton_iters", 0) + st.newton_iters
+    return out.cpu().numpy() if host else out
+
+
+def controller(err, u_new, u_hat, dt_old, cfg):
+    """Embedded-pair step-size controller (timeloop.py:198-218) on numpy arrays or
+    device tensors; ``integrate`` uses the fused device reduction instead."""
+    xp = np
+    if not isinstance(err, np.ndarray):
+        import torch as xp  # noqa: N812
+    tol = cfg.tol_a + xp.maximum(xp.abs(u_new), xp.abs(u_hat)) * cfg.tol_r
+    ratios = xp.abs(err) / tol
+    wlte = float(xp.mean(xp.sqrt(ratios))) if cfg.wlte_form == "rms" else float(xp.max(ratios))
+    return _controller_decision(wlte, dt_old, cfg)
+
+
+def _controller_decision(wlte, dt_old, cfg):
+    if wlte == 0.0:
+        return True, cfg.alpha_max * dt_old, wlte
+    factor = min(cfg.alpha_max,
+                 max(cfg.alpha_min, cfg.beta * (1.0 / wlte) ** (1.0 / (RK3_EMBEDDED_ORDER + 1))))
+    return wlte <= 1.0, factor * dt_old, wlte
 
 
 def count_steps(cfg):
@@ -243,7 +332,6 @@ def integrate(op, u0, cfg, store_steps="all", keep_log=False):
     Stored states stay on the device; a StepFailure is retried with dt halved
     up to three times, exactly like the reference.
     """
-    _require_explicit(cfg)
     u, _ = op.field(u0, "initial state")
     if not bool(op._isfinite_all(u)):
         raise NumericFailure("initial state contains NaN/Inf")
@@ -258,7 +346,9 @@ def integrate(op, u0, cfg, store_steps="all", keep_log=False):
     t, dt_next = cfg.t0, cfg.dt
     tiny = 1e-9 * cfg.dt
     n = attempts = 0
-    engine = engine_for(op, cfg.scheme)
+    cn = cfg.scheme == "cn"
+    engine = None if cn else engine_for(op, cfg.scheme)
+    fused = not cfg.adaptive          # the embedded pair needs the per-stage k_2
     op.flags()  # clear stale bits
     while t < cfg.t_end - tiny:
         attempts += 1
@@ -271,8 +361,11 @@ def integrate(op, u0, cfg, store_steps="all", keep_log=False):
         u_new = op.empty()
         for retry in range(_RETRY_HALVINGS + 1):
             try:
-                engine.step(u, dt, u_new)
-                check_step_flags(op)
+                if cn:
+                    step_cn(op, u, t, dt, cfg, stats, out=u_new)
+                else:
+                    engine.step(u, dt, u_new, fused=fused)
+                    check_step_flags(op)
                 break
             except StepFailure:
                 stats["retries"] += 1
@@ -280,7 +373,18 @@ def integrate(op, u0, cfg, store_steps="all", keep_log=False):
                     raise
                 dt *= 0.5
                 clipped = False
-        if dt != dt_next and not clipped:
+        wlte = 0.0
+        if cfg.adaptive:
+            wlte = op.rk_error_norm(u_new, u, engine._k[("k", 1)], dt, cfg)
+            accept, dt_prop, wlte = _controller_decision(wlte, dt, cfg)
+            if not accept:
+                stats["rejects"] += 1
+                if keep_log:
+                    log.append((n, t, dt, wlte, 0))
+                dt_next = dt_prop
+                continue
+            dt_next = dt_prop
+        elif dt != dt_next and not clipped:
             dt_next = dt
         n += 1
         t = cfg.t_end if clipped else t + dt
@@ -291,9 +395,11 @@ def integrate(op, u0, cfg, store_steps="all", keep_log=False):
         if store_all or n in want:
             snapshots[n] = u
         if keep_log:
-            log.append((n, t, dt, 0.0, 1))
-    return ForwardResult(ts=np.asarray(ts), dts=np.asarray(dts), snapshots=snapshots,
-                         u_final=u, stats=stats, step_log=log if keep_log else [])
+            log.append((n, t, dt, wlte, 1))
+    res = ForwardResult(ts=np.asarray(ts), dts=np.asarray(dts), snapshots=snapshots,
+                        u_final=u, stats=stats, step_log=log if keep_log else [])
+    res.fused_steps = fused       # replays (checkpoint Advance) take the same kernel path
+    return res
 
 
 def rk3_stages(op, u, t, dt):
