@@ -44,8 +44,9 @@ int64_t plan_batch(const sem1d_plan* p);           // sem1d_capi.cu
 
 namespace {
 
-constexpr int KT = 512;                 // threads per CTA
-constexpr int KB = 296;                 // CTAs per reduction launch (2 per SM), fixed
+constexpr int KT = 256;                 // threads per CTA
+constexpr int KB = 4 * 148;             // CTAs per reduction launch: one resident wave (4 per SM), fixed
+constexpr int KU = 4;                   // grid-strided elements per thread with loads issued together
 constexpr int RED_DOUBLES = 2 * KB + 2; // partials (2 slots) + ticket
 constexpr int MAX_RESTART = 64;
 
@@ -100,8 +101,10 @@ __device__ __forceinline__ void grid_reduce(double (&v)[R], double* work, double
   __threadfence();
   double w[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r)
-    w[r] = (threadIdx.x < KB) ? __ldcg(work + r * KB + threadIdx.x) : 0.0;
+  for (int r = 0; r < R; ++r) {          // fixed order: thread t combines partials t, t+KT, ...
+    w[r] = __ldcg(work + r * KB + threadIdx.x);
+    for (int k = threadIdx.x + KT; k < KB; k += KT) w[r] = red_op<MAX>(w[r], __ldcg(work + r * KB + k));
+  }
   __syncthreads();                       // sred reuse
   block_reduce<R, MAX>(w, sred);
   if (threadIdx.x == 0) {
@@ -117,44 +120,68 @@ __device__ __forceinline__ bool nonfin(double x) {
 
 // ------------------------------------------------------------------ kernels
 
-__global__ void __launch_bounds__(KT) k_dot(int64_t n, const double* x, const double* y, double* work,
+// Grid-strided element loop with KU loads in flight per thread: LOAD(u, i) fills the
+// registers of slot u, STEP(u, i) consumes them (all loads of a batch precede its stores,
+// so aliasing between outputs and inputs cannot serialise them).
+#define KR_LOOP(n, LOAD, STEP)                                                          \
+  {                                                                                     \
+    const int64_t S_ = (int64_t)gridDim.x * KT;                                         \
+    int64_t i0_ = blockIdx.x * (int64_t)KT + threadIdx.x;                               \
+    for (; i0_ + (KU - 1) * S_ < (n); i0_ += KU * S_) {                                 \
+      _Pragma("unroll") for (int u = 0; u < KU; ++u) { const int64_t i = i0_ + u * S_; (void)i; LOAD } \
+      _Pragma("unroll") for (int u = 0; u < KU; ++u) { const int64_t i = i0_ + u * S_; (void)i; STEP } \
+    }                                                                                   \
+    for (; i0_ < (n); i0_ += S_) {                                                      \
+      const int u = 0;                                                                  \
+      const int64_t i = i0_;                                                            \
+      (void)i;                                                                          \
+      LOAD STEP                                                                         \
+    }                                                                                   \
+  }
+
+__global__ void __launch_bounds__(KT, 4) k_dot(int64_t n, const double* x, const double* y, double* work,
                                             double* out) {
   double v[1] = {0.0};
-  for (int64_t i = blockIdx.x * (int64_t)KT + threadIdx.x; i < n; i += (int64_t)KB * KT)
-    v[0] = __dadd_rn(v[0], __dmul_rn(x[i], y[i]));
+  double a[KU], b[KU];
+  KR_LOOP(n, { a[u] = __ldg(x + i); b[u] = __ldg(y + i); },
+          { v[0] = __dadd_rn(v[0], __dmul_rn(a[u], b[u])); })
   grid_reduce<1, false>(v, work, out);
 }
 
 // w = x + alpha t;  out[0] = w.w, out[1] = z.w (z may be NULL)
-__global__ void __launch_bounds__(KT) k_shift_dot2(int64_t n, const double* x, const double* t, double alpha,
+__global__ void __launch_bounds__(KT, 4) k_shift_dot2(int64_t n, const double* x, const double* t, double alpha,
                                                    double* w, const double* z, double* work, double* out) {
   double v[2] = {0.0, 0.0};
-  for (int64_t i = blockIdx.x * (int64_t)KT + threadIdx.x; i < n; i += (int64_t)KB * KT) {
-    const double wi = __dadd_rn(x[i], __dmul_rn(alpha, t[i]));
-    w[i] = wi;
-    v[0] = __dadd_rn(v[0], __dmul_rn(wi, wi));
-    if (z) v[1] = __dadd_rn(v[1], __dmul_rn(z[i], wi));
-  }
+  double a[KU], b[KU], c[KU];
+  KR_LOOP(n, { a[u] = x[i]; b[u] = t[i]; c[u] = z ? z[i] : 0.0; },
+          {
+            const double wi = __dadd_rn(a[u], __dmul_rn(alpha, b[u]));
+            w[i] = wi;
+            v[0] = __dadd_rn(v[0], __dmul_rn(wi, wi));
+            v[1] = __dadd_rn(v[1], __dmul_rn(c[u], wi));
+          })
   grid_reduce<2, false>(v, work, out);
 }
 
 // y -= a[0] * x (modified Gram-Schmidt update);  out[0] = z.y_new (z == y: |y_new|^2)
-__global__ void __launch_bounds__(KT) k_axpy_dot(int64_t n, const double* a, const double* x, double* y,
+__global__ void __launch_bounds__(KT, 4) k_axpy_dot(int64_t n, const double* a, const double* x, double* y,
                                                  const double* z, double* work, double* out) {
   const double av = __ldcg(a);
+  const bool self = (z == y);
   double v[1] = {0.0};
-  for (int64_t i = blockIdx.x * (int64_t)KT + threadIdx.x; i < n; i += (int64_t)KB * KT) {
-    const double yi = __dsub_rn(y[i], __dmul_rn(av, x[i]));
-    y[i] = yi;
-    const double zi = (z == y) ? yi : z[i];
-    v[0] = __dadd_rn(v[0], __dmul_rn(zi, yi));
-  }
+  double xa[KU], ya[KU], za[KU];
+  KR_LOOP(n, { xa[u] = __ldg(x + i); ya[u] = y[i]; za[u] = self ? 0.0 : __ldg(z + i); },
+          {
+            const double yi = __dsub_rn(ya[u], __dmul_rn(av, xa[u]));
+            y[i] = yi;
+            v[0] = __dadd_rn(v[0], __dmul_rn(self ? yi : za[u], yi));
+          })
   grid_reduce<1, false>(v, work, out);
 }
 
-__global__ void __launch_bounds__(KT) k_scale(int64_t n, const double* x, double s, double* y) {
-  for (int64_t i = blockIdx.x * (int64_t)KT + threadIdx.x; i < n; i += (int64_t)gridDim.x * KT)
-    y[i] = __dmul_rn(x[i], s);
+__global__ void __launch_bounds__(KT, 4) k_scale(int64_t n, const double* x, double s, double* y) {
+  double a[KU];
+  KR_LOOP(n, { a[u] = x[i]; }, { y[i] = __dmul_rn(a[u], s); })
 }
 
 struct Coefs {
@@ -162,7 +189,7 @@ struct Coefs {
 };
 
 // x += sum_k c_k V_k   (scipy: x += y @ v[:col+1, :])
-__global__ void __launch_bounds__(KT) k_lincomb(int64_t n, int m, const Coefs c, const double* V,
+__global__ void __launch_bounds__(KT, 4) k_lincomb(int64_t n, int m, const Coefs c, const double* V,
                                                 int64_t ld, double* x) {
   for (int64_t i = blockIdx.x * (int64_t)KT + threadIdx.x; i < n; i += (int64_t)gridDim.x * KT) {
     double acc = __dmul_rn(c.c[0], V[i]);
@@ -172,59 +199,65 @@ __global__ void __launch_bounds__(KT) k_lincomb(int64_t n, int m, const Coefs c,
 }
 
 // r = b - (x + alpha t);  out[0] = r.r   (scipy: r = b - matvec(x))
-__global__ void __launch_bounds__(KT) k_residual(int64_t n, const double* b, const double* x, const double* t,
+__global__ void __launch_bounds__(KT, 4) k_residual(int64_t n, const double* b, const double* x, const double* t,
                                                  double alpha, double* r, double* work, double* out) {
   double v[1] = {0.0};
-  for (int64_t i = blockIdx.x * (int64_t)KT + threadIdx.x; i < n; i += (int64_t)KB * KT) {
-    const double ri = __dsub_rn(b[i], __dadd_rn(x[i], __dmul_rn(alpha, t[i])));
-    r[i] = ri;
-    v[0] = __dadd_rn(v[0], __dmul_rn(ri, ri));
-  }
+  double ba[KU], xa[KU], ta[KU];
+  KR_LOOP(n, { ba[u] = __ldg(b + i); xa[u] = __ldg(x + i); ta[u] = __ldg(t + i); },
+          {
+            const double ri = __dsub_rn(ba[u], __dadd_rn(xa[u], __dmul_rn(alpha, ta[u])));
+            r[i] = ri;
+            v[0] = __dadd_rn(v[0], __dmul_rn(ri, ri));
+          })
   grid_reduce<1, false>(v, work, out);
 }
 
 // nr = -((v - u) - h (fu + fv))  (timeloop.py:168 with the sign of the GMRES rhs -r);
 // out[0] = |r|^2; a non-finite r sets flag bit 1
-__global__ void __launch_bounds__(KT) k_cn_residual(int64_t n, const double* v, const double* u,
+__global__ void __launch_bounds__(KT, 4) k_cn_residual(int64_t n, const double* v, const double* u_,
                                                     const double* fu, const double* fv, double h, double* nr,
                                                     double* work, double* out, int* flag) {
   double acc[1] = {0.0};
   bool bad = false;
-  for (int64_t i = blockIdx.x * (int64_t)KT + threadIdx.x; i < n; i += (int64_t)KB * KT) {
-    const double ri = __dsub_rn(__dsub_rn(v[i], u[i]), __dmul_rn(h, __dadd_rn(fu[i], fv[i])));
-    bad |= nonfin(ri);
-    nr[i] = -ri;
-    acc[0] = __dadd_rn(acc[0], __dmul_rn(ri, ri));
-  }
+  double va[KU], ua[KU], fa[KU], ga[KU];
+  KR_LOOP(n, { va[u] = __ldg(v + i); ua[u] = __ldg(u_ + i); fa[u] = __ldg(fu + i); ga[u] = __ldg(fv + i); },
+          {
+            const double ri = __dsub_rn(__dsub_rn(va[u], ua[u]), __dmul_rn(h, __dadd_rn(fa[u], ga[u])));
+            bad |= nonfin(ri);
+            nr[i] = -ri;
+            acc[0] = __dadd_rn(acc[0], __dmul_rn(ri, ri));
+          })
   if (bad) atomicOr(flag, 1);
   grid_reduce<1, false>(acc, work, out);
 }
 
-__global__ void __launch_bounds__(KT) k_add(int64_t n, const double* x, const double* y, double* out) {
-  for (int64_t i = blockIdx.x * (int64_t)KT + threadIdx.x; i < n; i += (int64_t)gridDim.x * KT)
-    out[i] = __dadd_rn(x[i], y[i]);
+__global__ void __launch_bounds__(KT, 4) k_add(int64_t n, const double* x, const double* y, double* out) {
+  double a[KU], b[KU];
+  KR_LOOP(n, { a[u] = x[i]; b[u] = y[i]; }, { out[i] = __dadd_rn(a[u], b[u]); })
 }
 
 // Embedded-pair error (timeloop.py:205-210): u_hat = u + dt k2, err = u_new - u_hat,
 // tol = tol_a + max(|u_new|, |u_hat|) tol_r, ratio = |err| / tol;
 // out[0] = sum sqrt(ratio) (form 0, "rms": the reference's mean of square roots) or max ratio
 template <bool MAX>
-__global__ void __launch_bounds__(KT) k_rk_error(int64_t n, const double* un, const double* u, const double* k2,
+__global__ void __launch_bounds__(KT, 4) k_rk_error(int64_t n, const double* un, const double* u_, const double* k2,
                                                  double dt, double ta, double tr, double* work, double* out) {
   double v[1] = {0.0};
-  for (int64_t i = blockIdx.x * (int64_t)KT + threadIdx.x; i < n; i += (int64_t)KB * KT) {
-    const double uh = __dadd_rn(u[i], __dmul_rn(dt, k2[i]));
-    const double e = __dsub_rn(un[i], uh);
-    const double tol = __dadd_rn(ta, __dmul_rn(fmax(fabs(un[i]), fabs(uh)), tr));
-    const double ratio = __ddiv_rn(fabs(e), tol);
-    v[0] = MAX ? fmax(v[0], ratio) : __dadd_rn(v[0], __dsqrt_rn(ratio));
-  }
+  double na[KU], ua[KU], ka[KU];
+  KR_LOOP(n, { na[u] = __ldg(un + i); ua[u] = __ldg(u_ + i); ka[u] = __ldg(k2 + i); },
+          {
+            const double uh = __dadd_rn(ua[u], __dmul_rn(dt, ka[u]));
+            const double e = __dsub_rn(na[u], uh);
+            const double tol = __dadd_rn(ta, __dmul_rn(fmax(fabs(na[u]), fabs(uh)), tr));
+            const double ratio = __ddiv_rn(fabs(e), tol);
+            v[0] = MAX ? fmax(v[0], ratio) : __dadd_rn(v[0], __dsqrt_rn(ratio));
+          })
   grid_reduce<1, MAX>(v, work, out);
 }
 
 int ew_grid(int64_t n) {
   const int64_t b = (n + KT - 1) / KT;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(b, 4 * 148));
+  return (int)std::max<int64_t>(1, std::min<int64_t>(b, KB));
 }
 
 // ------------------------------------------------------------------ host drivers
