@@ -26,6 +26,7 @@ from .errors import ValidationError
 
 PERIODIC = "periodic"
 DIRICHLET0 = "dirichlet0"
+SNAPSHOT_MAGIC = "semopt-field v1"    # grid.py:27
 
 
 @dataclass(frozen=True)
@@ -232,3 +233,72 @@ def grid_1d(xa, xb, elements, degree, bc=PERIODIC):
 
 def grid_3d(*args, **kwargs):
     raise ValidationError("3D grids are outside the B200 hot path (SURVEY.md section 8(f), 'next')")
+
+
+# -- field snapshots (reference grid.py:250-305) ---------------------------------
+#
+# Format: an ASCII header (magic line, "dim", "ncomp", one "axis" line per axis with
+# elements / degree / repr'd extent / bc, "count", "end-header"), then `count`
+# little-endian float64 values.  Files written here are byte-identical to the
+# reference's for the same grid and values, and either side reads the other's.
+
+
+def _host_values(grid, values):
+    """Field -> contiguous host float64 array of shape (nglobal,) (device tensors copied)."""
+    if not isinstance(values, np.ndarray) and hasattr(values, "detach"):
+        values = values.detach().cpu().numpy()
+    v = np.asarray(values, dtype=float)
+    if v.shape != (grid.nglobal,):
+        raise ValidationError(f"field has shape {v.shape}, expected ({grid.nglobal},)")
+    return v
+
+
+def save_field(path, grid, values):
+    """Write a field snapshot (grid.py:253-270)."""
+    v = _host_values(grid, values)
+    lines = [SNAPSHOT_MAGIC, f"dim {grid.dim}", f"ncomp {grid.ncomp}"]
+    for k, ax in enumerate(grid.axes):
+        lines.append(f"axis {k} elements {ax.elements} degree {ax.degree} "
+                     f"extent {ax.xa!r} {ax.xb!r} bc {ax.bc}")
+    lines += [f"count {grid.nglobal}", "end-header"]
+    with open(path, "wb") as fh:
+        fh.write(("\n".join(lines) + "\n").encode("ascii"))
+        fh.write(v.astype("<f8", copy=False).tobytes())
+
+
+def load_field(path):
+    """Read a snapshot (grid.py:273-305); returns (grid, values).  3D snapshots parse but
+    their grid is outside the B200 path (ValidationError from Grid)."""
+    with open(path, "rb") as fh:
+        blob = fh.read()
+    marker = b"end-header\n"
+    cut = blob.find(marker)
+    if cut < 0 or not blob.startswith(SNAPSHOT_MAGIC.encode("ascii")):
+        raise ValidationError(f"{path}: not a semopt field snapshot")
+    meta, axes_kv = {}, {}
+    for line in blob[:cut].decode("ascii").splitlines()[1:]:
+        parts = line.split()
+        if not parts:
+            continue
+        if parts[0] == "axis":
+            axes_kv[int(parts[1])] = parts[2:]
+        else:
+            meta[parts[0]] = parts[1:]
+    try:
+        dim, count = int(meta["dim"][0]), int(meta["count"][0])
+        axes = []
+        for k in range(dim):
+            f = axes_kv[k]
+            ext = f.index("extent")
+            axes.append(Axis(xa=float(f[ext + 1]), xb=float(f[ext + 2]),
+                             elements=int(f[f.index("elements") + 1]),
+                             degree=int(f[f.index("degree") + 1]), bc=f[f.index("bc") + 1]))
+    except (KeyError, ValueError, IndexError) as exc:
+        raise ValidationError(f"{path}: malformed snapshot header ({exc})") from exc
+    grid = Grid(axes)
+    if grid.nglobal != count:
+        raise ValidationError(f"{path}: header count {count} != grid {grid.nglobal}")
+    payload = blob[cut + len(marker):]
+    if len(payload) < 8 * count:
+        raise ValidationError(f"{path}: payload holds {len(payload) // 8} values, header says {count}")
+    return grid, np.frombuffer(payload, dtype="<f8", count=count).astype(float)

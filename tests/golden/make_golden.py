@@ -194,6 +194,43 @@ def implicit_fixture(grid, ops, timeloop, problems):
     return out
 
 
+CLI_RUNS = {
+    # name -> argv of the reference CLI (outputs land in a temp dir)
+    "schedule": ["schedule", "--steps", "30", "--checkpoint-slots", "5", "--output", "{d}/sched.csv"],
+    "forward": ["forward", "--problem", "burgers1d", "--elements", "5", "--degree", "8", "--steps",
+                "40", "--horizon", "0.4", "--output", "{d}/fwd"],
+    "forward_cn": ["forward", "--problem", "burgers1d", "--elements", "5", "--degree", "8", "--steps",
+                   "8", "--horizon", "0.4", "--scheme", "cn", "--output", "{d}/fwdcn"],
+    "gradcheck": ["gradcheck", "--problem", "burgers1d", "--elements", "4", "--degree", "6",
+                  "--steps", "20", "--horizon", "0.2", "--ndirs", "2", "--eps", "1e-4,1e-5",
+                  "--output", "{d}/gc.csv"],
+}
+
+
+def cli_fixture(semopt, grid):
+    """Outputs of the reference CLI (cli.py:208-401) and one snapshot file
+    (grid.py:253-270), as raw bytes."""
+    import tempfile
+    from semopt import cli
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        for name, argv in CLI_RUNS.items():
+            rc = cli.main([a.format(d=d) for a in argv])
+            out[f"rc_{name}"] = np.array([rc])
+        for name, fname in (("schedule", "sched.csv"), ("forward_csv", "fwd.csv"),
+                            ("forward_field", "fwd.field"), ("forward_cn_csv", "fwdcn.csv"),
+                            ("forward_cn_field", "fwdcn.field"), ("gradcheck", "gc.csv")):
+            with open(os.path.join(d, fname), "rb") as fh:
+                out[name] = np.frombuffer(fh.read(), dtype=np.uint8)
+        g = grid.grid_1d(-1.0, 1.0, 3, 4, "dirichlet0")
+        vals = np.sin(np.arange(g.nglobal) * 0.7) * 1e3
+        grid.save_field(os.path.join(d, "snap.field"), g, vals)
+        with open(os.path.join(d, "snap.field"), "rb") as fh:
+            out["snapshot"] = np.frombuffer(fh.read(), dtype=np.uint8)
+        out["snapshot_values"] = vals
+    return out
+
+
 SCHED_CASES = [(1, 1), (3, 3), (5, 2), (10, 3), (20, 4), (30, 5), (100, 10), (57, 7), (500, 64)]
 
 
@@ -229,6 +266,7 @@ def main():
     np.savez_compressed(os.path.join(HERE, "schedules.npz"), **schedules_fixture(checkpoint))
     np.savez_compressed(os.path.join(HERE, "implicit.npz"),
                         **implicit_fixture(grid, ops, timeloop, problems))
+    np.savez_compressed(os.path.join(HERE, "cli.npz"), **cli_fixture(semopt, grid))
     print("golden fixtures written to", HERE)
 
 
