@@ -218,6 +218,166 @@ class BurgersOracle:
 
 
 # --------------------------------------------------------------------------
+# 3D periodic boxes, sum-factorised operators (reference grid.py:112-146,
+# ops.py:63-81,109-115,127-212) -- same numpy primitives and evaluation order
+# --------------------------------------------------------------------------
+
+
+class Mesh3D:
+    """Periodic tensor-product box; one degree N on every axis, E and extent per axis."""
+
+    def __init__(self, extents, elements, N):
+        self.N, self.n = N, N + 1
+        self.ext = [tuple(map(float, e)) for e in extents]
+        self.E = [int(e) for e in elements]
+        self.h = [(b - a) / E for (a, b), E in zip(self.ext, self.E)]
+        self.npts = [E * N for E in self.E]
+        self.nscalar = int(np.prod(self.npts))
+        self.ndof = 3 * self.nscalar
+        self.nelem = int(np.prod(self.E))
+        x, w = gll_nodes_weights(N)
+        self.xi, self.rho = x, w
+        tabs = [((np.arange(E)[:, None] * N + np.arange(self.n)[None, :]) % p)
+                for E, p in zip(self.E, self.npts)]
+        n2, n3 = self.npts[1], self.npts[2]
+        g1 = tabs[0][:, None, None, :, None, None]
+        g2 = tabs[1][None, :, None, None, :, None]
+        g3 = tabs[2][None, None, :, None, None, :]
+        self.table = ((g1 * n2 + g2) * n3 + g3).reshape(self.nelem, self.n, self.n, self.n)
+        self.mvec = [(h / 2.0) * w for h in self.h]                      # ops.py:108
+        m1, m2, m3 = self.mvec
+        blk = m1[:, None, None] * m2[None, :, None] * m3[None, None, :]  # grid.py:150-157
+        self.mass_scalar = self._bincount(np.broadcast_to(blk, (self.nelem,) + (self.n,) * 3))
+        self.mass = np.tile(self.mass_scalar, 3)
+        self.minv = 1.0 / self.mass
+
+    def _bincount(self, local):
+        return np.bincount(self.table.ravel(), weights=np.ascontiguousarray(local).ravel(),
+                           minlength=self.nscalar)
+
+    def scatter(self, u):
+        return np.asarray(u, dtype=float).reshape(3, self.nscalar)[:, self.table]
+
+    def gather(self, local):
+        out = np.empty(self.ndof)
+        for c in range(3):
+            out[c * self.nscalar:(c + 1) * self.nscalar] = self._bincount(local[c])
+        return out
+
+    @staticmethod
+    def apply_mask(u):
+        return u              # periodic boxes only (grid.py:96-99)
+
+    def coordinates(self):
+        """Per-axis node coordinates (grid.py:74-84)."""
+        out = []
+        for (a, b), E, h, p in zip(self.ext, self.E, self.h, self.npts):
+            c = np.empty(p)
+            for e in range(E):
+                idx = (e * self.N + np.arange(self.n)) % p
+                c[idx] = (a + e * h) + h * (self.xi + 1.0) / 2.0
+            c[0] = a
+            out.append(c)
+        return out
+
+
+def _apply_axis3(a, x, axis):
+    """Matrix a along spatial axis (1-based) of (..., n1, n2, n3) blocks (ops.py:63-81)."""
+    if axis == 3:
+        return x @ a.T
+    shape = x.shape
+    if axis == 1:
+        xr = x.reshape(-1, shape[-3], shape[-2] * shape[-1])
+        return np.matmul(a, xr).reshape(shape[:-3] + (a.shape[0], shape[-2], shape[-1]))
+    xr = x.reshape(-1, shape[-2], shape[-1])
+    return np.matmul(a, xr).reshape(shape)
+
+
+class BurgersOracle3D:
+    """F, J, J^T of 3D Burgers (ops.py:160-257) on a Mesh3D."""
+
+    def __init__(self, mesh, nu):
+        self.mesh, self.nu = mesh, float(nu)
+        D = diff_matrix(mesh.xi)
+        w = mesh.rho
+        self.Dw = D * w[:, None]
+        self.K = []
+        for h in mesh.h:
+            k = (2.0 / h) * (D.T * w) @ D
+            self.K.append(0.5 * (k + k.T))
+        m1, m2, m3 = mesh.mvec
+        self.T = [m2[:, None] * m3[None, :], m1[:, None] * m3[None, :], m1[:, None] * m2[None, :]]
+
+    def _tr(self, x, j):
+        t = self.T[j]
+        if j == 0:
+            return x * t
+        if j == 1:
+            return x * t[:, None, :]
+        return x * t[:, :, None]
+
+    def kop(self, x, j):
+        return self._tr(_apply_axis3(self.K[j], x, j + 1), j)
+
+    def dop(self, x, j):
+        return self._tr(_apply_axis3(self.Dw, x, j + 1), j)
+
+    def dop_t(self, x, j):
+        return self._tr(_apply_axis3(self.Dw.T, x, j + 1), j)
+
+    def _elem_rhs(self, ul):
+        out = np.empty_like(ul)
+        for i in range(3):
+            acc = self.kop(ul[i], 0)
+            for j in (1, 2):
+                acc += self.kop(ul[i], j)
+            acc *= -self.nu
+            for j in range(3):
+                acc -= ul[j] * self.dop(ul[i], j)
+            out[i] = acc
+        return out
+
+    def _elem_jac(self, ul, wl):
+        out = np.empty_like(wl)
+        for i in range(3):
+            acc = self.kop(wl[i], 0)
+            for j in (1, 2):
+                acc += self.kop(wl[i], j)
+            acc *= -self.nu
+            for j in range(3):
+                acc -= wl[j] * self.dop(ul[i], j)
+                acc -= ul[j] * self.dop(wl[i], j)
+            out[i] = acc
+        return out
+
+    def _elem_jact(self, ul, zl):
+        out = np.empty_like(zl)
+        for i in range(3):
+            acc = self.kop(zl[i], 0)
+            for j in (1, 2):
+                acc += self.kop(zl[i], j)
+            acc *= -self.nu
+            for j in range(3):
+                acc -= zl[j] * self.dop(ul[j], i)
+                acc -= self.dop_t(ul[j] * zl[i], j)
+            out[i] = acc
+        return out
+
+    def rhs(self, u):
+        m = self.mesh
+        return m.gather(self._elem_rhs(m.scatter(u))) * m.minv
+
+    def jac(self, u, v):
+        m = self.mesh
+        return m.gather(self._elem_jac(m.scatter(u), m.scatter(v))) * m.minv
+
+    def jact(self, u, z):
+        m = self.mesh
+        zm = np.asarray(z, dtype=float) * m.minv
+        return m.gather(self._elem_jact(m.scatter(u), m.scatter(zm)))
+
+
+# --------------------------------------------------------------------------
 # explicit RK (reference timeloop.py; RK4 restated, see module docstring)
 # --------------------------------------------------------------------------
 

@@ -231,6 +231,49 @@ def cli_fixture(semopt, grid):
     return out
 
 
+GRID3D_CASES = [
+    # (extents per axis, elements per axis, degree)
+    (((-2.0, 2.0),) * 3, (2, 2, 2), 3),
+    (((0.0, 1.0), (-1.0, 2.0), (0.0, 2.5)), (2, 3, 2), 4),
+    (((-2.0, 2.0),) * 3, (1, 2, 1), 2),
+]
+
+
+def grid3d_fixture(grid, ops, problems, timeloop):
+    """3D sum-factorised operators (ops.py:71-81,109-115,141-150,160-212) and maps
+    (grid.py:112-146) on small periodic boxes, plus a short burgers3d evaluation."""
+    out = {}
+    for k, (ext, els, deg) in enumerate(GRID3D_CASES):
+        axes = [grid.Axis(e[0], e[1], n, deg, "periodic") for e, n in zip(ext, els)]
+        g = grid.build_grid(axes)
+        op = ops.SemOperator(g, ops.PdeCoefficients(0.05))
+        rng = np.random.default_rng(300 + k)
+        u = rng.uniform(-1.0, 1.0, g.nglobal)
+        v = rng.standard_normal(g.nglobal)
+        w = rng.standard_normal(g.nglobal)
+        out[f"case_{k}"] = np.array([*[x for e in ext for x in e], *els, deg], dtype=float)
+        out[f"table_{k}"] = g.table
+        out[f"mass_{k}"] = g.mass_scalar
+        out[f"u_{k}"], out[f"v_{k}"], out[f"w_{k}"] = u, v, w
+        out[f"F_{k}"] = op.apply_rhs(u)
+        out[f"J_{k}"] = op.apply_jacobian(u, v)
+        out[f"JT_{k}"] = op.apply_jacobian_transpose(u, w)
+        out[f"coords_{k}"] = np.concatenate(g.node_coordinates())
+    for scheme in ("rk3", "cn"):
+        prob = problems.make_problem("burgers3d", elements=2, degree=3, steps=6, horizon=0.03,
+                                     scheme=scheme)
+        j, gr = prob.evaluate(prob.u_guess)
+        out[f"b3d_{scheme}_J"] = np.array([j])
+        out[f"b3d_{scheme}_grad"] = gr
+        out[f"b3d_{scheme}_ufinal"] = prob.last_forward.u_final
+        out[f"b3d_{scheme}_guess"] = prob.u_guess
+        out[f"b3d_{scheme}_target"] = prob.u_target
+        st = prob.last_forward.stats
+        out[f"b3d_{scheme}_stats"] = np.array([st["steps"], st["newton_iters"], st["gmres_iters"],
+                                               prob.op.last_sweep_stats["gmres_iters"]])
+    return out
+
+
 SCHED_CASES = [(1, 1), (3, 3), (5, 2), (10, 3), (20, 4), (30, 5), (100, 10), (57, 7), (500, 64)]
 
 
@@ -267,6 +310,7 @@ def main():
     np.savez_compressed(os.path.join(HERE, "implicit.npz"),
                         **implicit_fixture(grid, ops, timeloop, problems))
     np.savez_compressed(os.path.join(HERE, "cli.npz"), **cli_fixture(semopt, grid))
+    np.savez_compressed(os.path.join(HERE, "grid3d.npz"), **grid3d_fixture(grid, ops, problems, timeloop))
     print("golden fixtures written to", HERE)
 
 

@@ -191,3 +191,45 @@ def _target_ic(periodic):
     mesh = R.Mesh1D(-1.0, 1.0, 16, 9, periodic)
     x = mesh.coordinates()
     return mesh.apply_mask(np.sin(np.pi * x) + 0.5 * np.sin(2.0 * np.pi * x))
+
+
+def _mesh3d_case(g, k):
+    c = g[f"case_{k}"]
+    ext = [(c[0], c[1]), (c[2], c[3]), (c[4], c[5])]
+    return R.Mesh3D(ext, [int(x) for x in c[6:9]], int(c[9]))
+
+
+@pytest.mark.parametrize("k", [0, 1, 2])
+def test_3d_maps_and_ops_bit_exact(k):
+    """3D periodic boxes (grid.py:112-146) and the sum-factorised F, J, J^T
+    (ops.py:63-81,160-257), incl. an anisotropic box with different E per axis."""
+    g = golden("grid3d.npz")
+    m = _mesh3d_case(g, k)
+    o = R.BurgersOracle3D(m, 0.05)
+    assert np.array_equal(m.table, g[f"table_{k}"])
+    assert np.array_equal(m.mass_scalar, g[f"mass_{k}"])
+    assert np.array_equal(np.concatenate(m.coordinates()), g[f"coords_{k}"])
+    u, v, w = g[f"u_{k}"], g[f"v_{k}"], g[f"w_{k}"]
+    assert np.array_equal(o.rhs(u), g[f"F_{k}"])
+    assert np.array_equal(o.jac(u, v), g[f"J_{k}"])
+    assert np.array_equal(o.jact(u, w), g[f"JT_{k}"])
+    # discrete-adjoint identity <J v, w>_ = <v, M^-1-weighted J^T ...>: the transpose is exact
+    lhs = np.dot(o.jac(u, v), w)
+    rhs = np.dot(v, o.jact(u, w))
+    assert abs(lhs - rhs) <= 1e-11 * max(abs(lhs), 1.0)
+
+
+@pytest.mark.parametrize("scheme", ["rk3", "cn"])
+def test_burgers3d_evaluate_bit_exact(scheme):
+    """problems.burgers3d (elements=2, degree=3, 6 steps): J, gradient, final state and
+    Newton / GMRES counters equal the reference's."""
+    g = golden("grid3d.npz")
+    m = R.Mesh3D([(-2.0, 2.0)] * 3, [2, 2, 2], 3)
+    o = R.BurgersOracle3D(m, 0.001)
+    j, gr, uf, fs, ss = R.evaluate_general(o, g[f"b3d_{scheme}_guess"], g[f"b3d_{scheme}_target"],
+                                           0.0, 0.03, 0.03 / 6, scheme)
+    assert j == g[f"b3d_{scheme}_J"][0]
+    assert np.array_equal(gr, g[f"b3d_{scheme}_grad"])
+    assert np.array_equal(uf, g[f"b3d_{scheme}_ufinal"])
+    assert [fs["steps"], fs["newton_iters"], fs["gmres_iters"], ss["gmres_iters"]] == \
+        list(g[f"b3d_{scheme}_stats"])
