@@ -230,6 +230,57 @@ int sem1d_rk_error_norm(int64_t n, const double* u_new, const double* u, const d
                         double dt, double tol_a, double tol_r, int max_form, double* work,
                         double* out, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Stage compositions for operators without fused stage kernels (the 3D path):
+ * the same association orders as sem1d_rk_stage / sem1d_adj_stage.
+ *   Y   = base + (dt c0) T0  |  base + dt ((c0 T0 + c1 T1) + ...)   (timeloop.py:114-127)
+ *   z   = b lam + sum_j a_j l_j                                       (adjoint.py:58-60)
+ *   out = ((x + t0) + t1) + ...                                       (adjoint.py:61)
+ *   y   = s x
+ * `terms` / `coef` are host arrays (of device pointers / values), at most
+ * SEM1D_MAX_TERMS entries. */
+int sem1d_vec_rk_combine(int64_t n, const double* base, double dt, int nterms,
+                         const double* const* terms, const double* coef, double* Y, int check,
+                         int* flag, void* stream);
+int sem1d_vec_adj_combine(int64_t n, const double* lam, double b, int nl,
+                          const double* const* l_terms, const double* a, double* z, void* stream);
+int sem1d_vec_accumulate(int64_t n, const double* x, int nt, const double* const* terms,
+                         double* out, void* stream);
+int sem1d_vec_scale(int64_t n, const double* x, double s, double* y, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * 3D periodic boxes: sum-factorised Burgers operators
+ *   sem3d_rhs   <- SemOperator.apply_rhs                 ops.py:160-174,232-236 (dim 3)
+ *   sem3d_jac   <- SemOperator.apply_jacobian            ops.py:176-193,238-244
+ *   sem3d_jact  <- SemOperator.apply_jacobian_transpose  ops.py:195-212,246-257
+ *   sem3d_terminal <- terminal_condition                 adjoint.py:33-47
+ * Fields: 3 components x P1*P2*P3 scalar nodes, P_a = E_a*N, node (g1,g2,g3) at
+ * (g1*P2 + g2)*P3 + g3 (grid.py:118-127).  One degree N (1..12) on all axes.
+ * Plan constants (host arrays, copied): K3 = 3 stiffness matrices (n x n, one per
+ * axis: ops.py:105-106 with that axis' h), Dw (n x n), T3 = the transverse mass
+ * weights (n x n per direction, ops.py:109-115), and the assembled mass diagonal
+ * and its reciprocal by position class ((N+1)^3 values, index
+ * (c1*(N+1)+c2)*(N+1)+c3 with c = 0 for the wrap node g = 0, g mod N for interior
+ * nodes, N for the other element interfaces -- bincount's summation order differs
+ * between the two interface kinds, grid.py:131-135).  `work` holds
+ * sem3d_work_size(plan) doubles (element-block scratch). */
+typedef struct sem3d_plan sem3d_plan;
+int sem3d_max_degree(void);
+int sem3d_plan_create(const int64_t* elements, int degree, double nu, const double* K3,
+                      const double* Dw, const double* T3, const double* minv_pattern,
+                      const double* mass_pattern, sem3d_plan** out);
+int sem3d_plan_destroy(sem3d_plan* plan);
+int64_t sem3d_plan_ndof(const sem3d_plan* plan);
+int64_t sem3d_work_size(const sem3d_plan* plan);
+int sem3d_rhs(const sem3d_plan* plan, const double* u, double* f, double* work, int* flag,
+              void* stream);
+int sem3d_jac(const sem3d_plan* plan, const double* u, const double* v, double* out,
+              double* work, int* flag, void* stream);
+int sem3d_jact(const sem3d_plan* plan, const double* u, const double* z, double* out,
+               double* work, int* flag, void* stream);
+int sem3d_terminal(const sem3d_plan* plan, const double* uN, const double* ud, double* lam,
+                   double* J, double* work, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -85,6 +85,22 @@ SIGNATURES = {
     "sem1d_vec_dot": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "sem1d_rk_error_norm": (c_int, [c_int64, c_void_p, c_void_p, c_void_p, c_double, c_double,
                                     c_double, c_int, c_void_p, c_void_p, c_void_p]),
+    "sem1d_vec_rk_combine": (c_int, [c_int64, c_void_p, c_double, c_int, c_void_p, c_void_p, c_void_p,
+                                     c_int, c_void_p, c_void_p]),
+    "sem1d_vec_adj_combine": (c_int, [c_int64, c_void_p, c_double, c_int, c_void_p, c_void_p, c_void_p,
+                                      c_void_p]),
+    "sem1d_vec_accumulate": (c_int, [c_int64, c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
+    "sem1d_vec_scale": (c_int, [c_int64, c_void_p, c_double, c_void_p, c_void_p]),
+    "sem3d_max_degree": (c_int, []),
+    "sem3d_plan_create": (c_int, [c_void_p, c_int, c_double, c_void_p, c_void_p, c_void_p, c_void_p,
+                                  c_void_p, ctypes.POINTER(c_void_p)]),
+    "sem3d_plan_destroy": (c_int, [c_void_p]),
+    "sem3d_plan_ndof": (c_int64, [c_void_p]),
+    "sem3d_work_size": (c_int64, [c_void_p]),
+    "sem3d_rhs": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "sem3d_jac": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "sem3d_jact": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "sem3d_terminal": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
 }
 
 _lock = threading.Lock()

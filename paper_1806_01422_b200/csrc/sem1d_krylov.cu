@@ -255,6 +255,65 @@ __global__ void __launch_bounds__(KT, 4) k_rk_error(int64_t n, const double* un,
   grid_reduce<1, MAX>(v, work, out);
 }
 
+// ---- stage compositions for operators without fused stage kernels (3D) ----------
+
+struct Terms {
+  const double* p[SEM1D_MAX_TERMS];
+  double c[SEM1D_MAX_TERMS];
+  int n;
+};
+
+// Y = base + (dt c0) K0 (one term) or base + dt ((c0 K0 + c1 K1) + ...)  -- the association
+// of timeloop.py:114-127 / sem1d_rk_stage; a non-finite Y sets SEM1D_FLAG_STEP_NONFINITE
+__global__ void __launch_bounds__(KT, 4) k_rk_combine(int64_t n, const double* base, double dt, const Terms T,
+                                                      double* Y, int check, int* flag) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)KT + threadIdx.x; i < n; i += (int64_t)gridDim.x * KT) {
+    double y;
+    if (T.n == 1) {
+      y = __dadd_rn(base[i], __dmul_rn(__dmul_rn(dt, T.c[0]), T.p[0][i]));
+    } else {
+      double acc = __dmul_rn(T.c[0], T.p[0][i]);
+      for (int j = 1; j < T.n; ++j) acc = __dadd_rn(acc, __dmul_rn(T.c[j], T.p[j][i]));
+      y = __dadd_rn(base[i], __dmul_rn(dt, acc));
+    }
+    if (check) bad |= nonfin(y);
+    Y[i] = y;
+  }
+  if (bad) atomicOr(flag, SEM1D_FLAG_STEP_NONFINITE);
+}
+
+// z = b lam + sum_j a_j l_j (left to right, adjoint.py:58-60 / sem1d_adj_stage)
+__global__ void __launch_bounds__(KT, 4) k_adj_combine(int64_t n, const double* lam, double b, const Terms T,
+                                                       double* z) {
+  for (int64_t i = blockIdx.x * (int64_t)KT + threadIdx.x; i < n; i += (int64_t)gridDim.x * KT) {
+    double acc = __dmul_rn(b, lam[i]);
+    for (int j = 0; j < T.n; ++j) acc = __dadd_rn(acc, __dmul_rn(T.c[j], T.p[j][i]));
+    z[i] = acc;
+  }
+}
+
+// out = ((x + t0) + t1) + ...   (lam + l_1 + l_2 + ..., adjoint.py:61)
+__global__ void __launch_bounds__(KT, 4) k_accumulate(int64_t n, const double* x, const Terms T, double* out) {
+  for (int64_t i = blockIdx.x * (int64_t)KT + threadIdx.x; i < n; i += (int64_t)gridDim.x * KT) {
+    double acc = x[i];
+    for (int j = 0; j < T.n; ++j) acc = __dadd_rn(acc, T.p[j][i]);
+    out[i] = acc;
+  }
+}
+
+bool make_terms(int nt, const double* const* ptrs, const double* coefs, Terms& T) {
+  if (nt < 0 || nt > SEM1D_MAX_TERMS) return false;
+  std::memset(&T, 0, sizeof(T));
+  T.n = nt;
+  for (int j = 0; j < nt; ++j) {
+    if (!ptrs[j]) return false;
+    T.p[j] = ptrs[j];
+    T.c[j] = coefs ? coefs[j] : 1.0;
+  }
+  return true;
+}
+
 int ew_grid(int64_t n) {
   const int64_t b = (n + KT - 1) / KT;
   return (int)std::max<int64_t>(1, std::min<int64_t>(b, KB));
@@ -643,5 +702,43 @@ int sem1d_rk_error_norm(int64_t n, const double* u_new, const double* u, const d
 }
 
 int64_t sem1d_reduce_work_size(void) { return RED_DOUBLES; }
+
+int sem1d_vec_rk_combine(int64_t n, const double* base, double dt, int nterms, const double* const* terms,
+                         const double* coef, double* Y, int check, int* flag, void* stream) {
+  Terms T;
+  if (n < 1 || !base || !Y || nterms < 1 || !terms || !coef || !make_terms(nterms, terms, coef, T) ||
+      (check && !flag))
+    return fail(SEM1D_EINVAL, "sem1d_vec_rk_combine: bad argument");
+  k_rk_combine<<<ew_grid(n), KT, 0, static_cast<cudaStream_t>(stream)>>>(n, base, dt, T, Y, check, flag);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SEM1D_OK : cuda_fail(e, "sem1d_vec_rk_combine");
+}
+
+int sem1d_vec_adj_combine(int64_t n, const double* lam, double b, int nl, const double* const* l_terms,
+                          const double* a, double* z, void* stream) {
+  Terms T;
+  if (n < 1 || !lam || !z || (nl > 0 && (!l_terms || !a)) || !make_terms(nl, l_terms, a, T))
+    return fail(SEM1D_EINVAL, "sem1d_vec_adj_combine: bad argument");
+  k_adj_combine<<<ew_grid(n), KT, 0, static_cast<cudaStream_t>(stream)>>>(n, lam, b, T, z);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SEM1D_OK : cuda_fail(e, "sem1d_vec_adj_combine");
+}
+
+int sem1d_vec_accumulate(int64_t n, const double* x, int nt, const double* const* terms, double* out,
+                         void* stream) {
+  Terms T;
+  if (n < 1 || !x || !out || (nt > 0 && !terms) || !make_terms(nt, terms, nullptr, T))
+    return fail(SEM1D_EINVAL, "sem1d_vec_accumulate: bad argument");
+  k_accumulate<<<ew_grid(n), KT, 0, static_cast<cudaStream_t>(stream)>>>(n, x, T, out);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SEM1D_OK : cuda_fail(e, "sem1d_vec_accumulate");
+}
+
+int sem1d_vec_scale(int64_t n, const double* x, double s, double* y, void* stream) {
+  if (n < 1 || !x || !y) return fail(SEM1D_EINVAL, "sem1d_vec_scale: bad argument");
+  k_scale<<<ew_grid(n), KT, 0, static_cast<cudaStream_t>(stream)>>>(n, x, s, y);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SEM1D_OK : cuda_fail(e, "sem1d_vec_scale");
+}
 
 }  // extern "C"

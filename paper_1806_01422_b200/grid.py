@@ -10,8 +10,8 @@ closed forms; the full arrays exist here only as lazily built host
 properties so the reference's attribute surface (and the bit-exact tests
 against it) keep working.
 
-3D grids (``grid.py:113-122,239-244``) are outside the B200 hot path
- and are rejected with ValidationError.
+3D periodic boxes (``grid.py:113-122,239-244``) are :class:`Grid3D` (SURVEY.md
+section 8(f) row 2); their operators live in ``ops3d.py``.
 """
 
 from __future__ import annotations
@@ -223,16 +223,149 @@ class Grid:
         return float(torch.sqrt(torch.dot(u, m * u)))
 
 
+class Grid3D:
+    """Periodic 3D box with a 3-component field (reference Grid with three axes,
+    grid.py:112-146).  One degree on all axes (the kernels' constraint); extents and
+    element counts may differ per axis.  The assembly maps are closed forms on the
+    device; the reference's tables / bincount masses exist here only as lazily built
+    host arrays for inspection and the bit-exact tests."""
+
+    def __init__(self, axes):
+        axes = tuple(axes)
+        if len(axes) != 3:
+            raise ValidationError("Grid3D needs three axes")
+        if any(ax.bc != PERIODIC for ax in axes):
+            raise ValidationError("unsupported configuration: 3D grids require periodic axes")
+        if len({ax.degree for ax in axes}) != 1:
+            raise ValidationError("the B200 3D kernels need the same degree on every axis")
+        self.axes = axes
+        self.dim = 3
+        self.ncomp = 3
+        self.N = axes[0].degree
+        self.bases = tuple(gll_rule(ax.degree) for ax in axes)
+        self.shape = tuple(ax.npts for ax in axes)
+        self.nscalar = int(np.prod(self.shape))
+        self.nglobal = 3 * self.nscalar
+        self.nelem = int(np.prod([ax.elements for ax in axes]))
+        self.local_shape = (self.N + 1,) * 3
+        self.periodic = True
+        self.has_mask = False
+        self.h = tuple(ax.element_length for ax in axes)
+        self.mvec = tuple((ax.element_length / 2.0) * b.weights for ax, b in zip(axes, self.bases))
+        self.mass_pattern = self._mass_pattern()
+        self.minv_pattern = 1.0 / self.mass_pattern
+
+    # bincount of the element mass blocks in table order (grid.py:131-135, 150-161) on a
+    # box of min(E_a, 2) elements per axis: it holds every position class (interior node,
+    # wrap node g = 0, other interface) with the same per-node summation order
+    def _mass_pattern(self):
+        N, n = self.N, self.N + 1
+        Es = [min(ax.elements, 2) for ax in self.axes]
+        Ps = [E * N for E in Es]
+        tabs = [((np.arange(E)[:, None] * N + np.arange(n)[None, :]) % P) for E, P in zip(Es, Ps)]
+        g1 = tabs[0][:, None, None, :, None, None]
+        g2 = tabs[1][None, :, None, None, :, None]
+        g3 = tabs[2][None, None, :, None, None, :]
+        table = ((g1 * Ps[1] + g2) * Ps[2] + g3).reshape(-1)
+        m1, m2, m3 = self.mvec
+        blk = m1[:, None, None] * m2[None, :, None] * m3[None, None, :]
+        ne = int(np.prod(Es))
+        mass = np.bincount(table, weights=np.broadcast_to(blk, (ne, n, n, n)).ravel(),
+                           minlength=int(np.prod(Ps))).reshape(Ps)
+        pat = np.empty((N + 1,) * 3)
+        pos = [[0] + list(range(1, N)) + [N if E > 1 else 0] for E in Es]   # class -> node
+        for c1 in range(N + 1):
+            for c2 in range(N + 1):
+                for c3 in range(N + 1):
+                    pat[c1, c2, c3] = mass[pos[0][c1], pos[1][c2], pos[2][c3]]
+        return pat.ravel()
+
+    # -- lazily materialised reference attributes (inspection / tests) ------------
+
+    @cached_property
+    def table(self):
+        N, n = self.N, self.N + 1
+        tabs = [ax.local_to_global() for ax in self.axes]
+        n2, n3 = self.shape[1], self.shape[2]
+        g1 = tabs[0][:, None, None, :, None, None]
+        g2 = tabs[1][None, :, None, None, :, None]
+        g3 = tabs[2][None, None, :, None, None, :]
+        t = np.ascontiguousarray(((g1 * n2 + g2) * n3 + g3).reshape(self.nelem, n, n, n))
+        t.setflags(write=False)
+        return t
+
+    @cached_property
+    def mass_scalar(self):
+        """The assembled mass diagonal by position class (bit-identical to the reference's
+        bincount, tests/test_host.py)."""
+        N = self.N
+        cls = []
+        for P in self.shape:
+            g = np.arange(P)
+            r = g % N
+            cls.append(np.where(r != 0, r, np.where(g == 0, 0, N)))
+        idx = (cls[0][:, None, None] * (N + 1) + cls[1][None, :, None]) * (N + 1) + cls[2][None, None, :]
+        m = self.mass_pattern[idx].ravel()
+        m.setflags(write=False)
+        return m
+
+    def mass(self):
+        return np.tile(self.mass_scalar, 3)
+
+    def mask(self, u):
+        return u                                   # periodic boxes only
+
+    def scatter(self, u):
+        """Global -> (3, nelem, n, n, n) element blocks (grid.py:165-169), host arrays."""
+        u = self._check_host(u)
+        return u.reshape(3, self.nscalar)[:, self.table]
+
+    def gather(self, local):
+        """Adjoint of scatter (grid.py:171-182), host arrays."""
+        out = np.empty(self.nglobal)
+        for c in range(3):
+            out[c * self.nscalar:(c + 1) * self.nscalar] = np.bincount(
+                self.table.ravel(), weights=np.ascontiguousarray(local[c]).ravel(), minlength=self.nscalar)
+        return out
+
+    def _check_host(self, u):
+        u = np.asarray(u, dtype=float)
+        if u.shape != (self.nglobal,):
+            raise ValidationError(f"field has shape {u.shape}, expected ({self.nglobal},)")
+        return u
+
+    def node_coordinates(self):
+        return tuple(ax.coordinates() for ax in self.axes)
+
+    def evaluate(self, fn):
+        """(x1, x2, x3) meshes -> 3 component arrays (grid.py:209-222)."""
+        mesh = np.meshgrid(*self.node_coordinates(), indexing="ij")
+        comps = fn(*mesh)
+        return np.concatenate([np.asarray(c, dtype=float).ravel() for c in comps])
+
+    def l2_norm(self, u):
+        if isinstance(u, np.ndarray):
+            u = self._check_host(u)
+            return float(np.sqrt(np.dot(u, self.mass() * u)))
+        import torch
+        m = torch.as_tensor(self.mass(), device=u.device)
+        return float(torch.sqrt(torch.dot(u, m * u)))
+
+
 def build_grid(axes):
-    return Grid(axes)
+    axes = tuple(axes)
+    return Grid3D(axes) if len(axes) == 3 else Grid(axes)
 
 
 def grid_1d(xa, xb, elements, degree, bc=PERIODIC):
     return Grid([Axis(xa, xb, elements, degree, bc)])
 
 
-def grid_3d(*args, **kwargs):
-    raise ValidationError("3D grids are outside the B200 hot path (SURVEY.md section 8(f), 'next')")
+def grid_3d(extents, elements, degree):
+    """Periodic 3D box (grid.py:239-244); extents is ((xa, xb),)*3 or one (xa, xb) pair."""
+    if len(extents) == 2 and np.isscalar(extents[0]):
+        extents = (extents,) * 3
+    return Grid3D([Axis(e[0], e[1], elements, degree, PERIODIC) for e in extents])
 
 
 # -- field snapshots (reference grid.py:250-305) ---------------------------------

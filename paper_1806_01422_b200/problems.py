@@ -8,8 +8,9 @@ reference convention J = d^T M d (adjoint.py:33-47); BASELINE.json quotes
 
 Builders for the BASELINE configurations live in ``configs.py``; the
 reference's ``burgers1d`` problem (Dirichlet Burgers on [-2, 2], Cole-Hopf
-target) is kept here.  advdiff1d / diffusion1d / burgers3d need operators
-outside the B200 hot path and raise ValidationError.
+target) and the periodic ``burgers3d`` box are kept here.
+advdiff1d / diffusion1d need LINEAR / NONE advection, outside the B200 path, and
+raise ValidationError.
 """
 
 from __future__ import annotations
@@ -20,7 +21,7 @@ import numpy as np
 
 from . import adjoint, checkpoint, timeloop
 from .errors import ValidationError
-from .grid import DIRICHLET0, grid_1d
+from .grid import DIRICHLET0, grid_1d, grid_3d
 from .ops import BURGERS, PdeCoefficients, SemOperator
 
 
@@ -142,9 +143,32 @@ def burgers1d_problem(elements=5, degree=8, nu=0.001, horizon=4.0, steps=400, dt
         checkpoint_slots=checkpoint_slots)
 
 
+def burgers3d_initial(x1, x2, x3):
+    """Product-of-waves initial velocity, cyclic in the components (problems.py:65-72)."""
+    s, c = np.sin, np.cos
+    h = 0.5 * np.pi
+    return (s(h * x1) * c(h * x2) * c(h * x3), s(h * x2) * c(h * x3) * c(h * x1),
+            s(h * x3) * c(h * x1) * c(h * x2))
+
+
+def burgers3d_problem(elements=4, degree=8, nu=0.001, horizon=0.1, steps=50, dt=None, scheme="rk3",
+                      adaptive=False, checkpoint_slots=None, device=None, **ts_kw):
+    """The reference's periodic 3D Burgers case on [-2, 2]^3 (problems.py:257-272): target =
+    the initial condition times exp(-nu T); guess = the initial condition."""
+    from .ops3d import SemOperator3D
+    grid = grid_3d((-2.0, 2.0), elements, degree)
+    op = SemOperator3D(grid, PdeCoefficients(nu, BURGERS), device=device)
+    ic = grid.evaluate(burgers3d_initial)
+    return AssimilationProblem(name="burgers3d", grid=grid, op=op,
+                               ts=_ts(scheme, horizon, steps, dt, adaptive, **ts_kw),
+                               u_target=np.exp(-nu * horizon) * ic, u_guess=ic, u_exact_ic=None,
+                               exact_solution=None, checkpoint_slots=checkpoint_slots)
+
+
 def make_problem(kind, **params):
     from . import configs
-    builders = {"burgers1d": burgers1d_problem, "cfg1": configs.cfg1_problem}
+    builders = {"burgers1d": burgers1d_problem, "burgers3d": burgers3d_problem,
+                "cfg1": configs.cfg1_problem}
     if kind not in builders:
         raise ValidationError(f"unknown problem {kind!r}; on the B200 path choose from "
                               f"{sorted(builders)}")

@@ -57,7 +57,7 @@ def test_schedule_command_matches_reference(tmp_path):
 
 
 def test_exit_codes_and_config(tmp_path):
-    assert cli.main(["forward", "--problem", "burgers3d", "--output", str(tmp_path / "x")]) == 2
+    assert cli.main(["forward", "--problem", "advdiff1d", "--output", str(tmp_path / "x")]) == 2
     assert cli.main(["forward", "--bogus"]) == 2
     assert cli.main(["schedule"]) == 2                              # --steps is required
     cfg = tmp_path / "c.cfg"

@@ -8,6 +8,7 @@ import paper_1806_01422_b200 as sb
 from paper_1806_01422_b200 import checkpoint as C
 from paper_1806_01422_b200 import timeloop as T
 from paper_1806_01422_b200.grid import grid_1d
+from oracle import semref as R
 from semtest_util import golden
 
 DEGREES = list(range(1, 33)) + [48, 64]
@@ -61,8 +62,12 @@ def test_grid_kats_and_validation():
         grid_1d(0.0, 1.0, 1, 1)
     with pytest.raises(sb.ValidationError):
         grid_1d(1.0, 0.0, 4, 4)
-    with pytest.raises(sb.ValidationError):
-        sb.grid_3d((-2.0, 2.0), 2, 4)
+    g3 = sb.grid_3d((-2.0, 2.0), 2, 4)            # 3D periodic box
+    assert g3.nglobal == 3 * 8 ** 3 and g3.ncomp == 3 and not g3.has_mask
+    with pytest.raises(sb.ValidationError):       # 3D grids require periodic axes (grid.py:97-101)
+        sb.build_grid([sb.Axis(-1.0, 1.0, 2, 3, "dirichlet0")] * 3)
+    with pytest.raises(sb.ValidationError):       # one degree on all axes (kernel constraint)
+        sb.build_grid([sb.Axis(-1.0, 1.0, 2, 3), sb.Axis(-1.0, 1.0, 2, 4), sb.Axis(-1.0, 1.0, 2, 3)])
     with pytest.raises(sb.ValidationError):
         sb.PdeCoefficients(-1.0)
     with pytest.raises(sb.ValidationError):
@@ -160,3 +165,19 @@ def test_lbfgs_quadratic_and_reference_log_shape():
     assert all(b2 <= a2 for a2, b2 in zip(js, js[1:]))  # monotone (Wolfe decrease)
     with pytest.raises(sb.LineSearchError):
         sb.line_search(lambda t: (0.0, 0.0, None), 0.0, 1.0)
+
+
+@pytest.mark.parametrize("k", [0, 1, 2])
+def test_grid3d_maps_bit_exact(k):
+    """Grid3D: table, coordinates and the mass diagonal built from (N+1)^3 position
+    classes equal the reference's bincount arrays bit for bit (grid.py:112-146)."""
+    g = golden("grid3d.npz")
+    c = g[f"case_{k}"]
+    ext = [(c[0], c[1]), (c[2], c[3]), (c[4], c[5])]
+    grid = sb.build_grid([sb.Axis(e[0], e[1], int(E), int(c[9])) for e, E in zip(ext, c[6:9])])
+    assert np.array_equal(grid.table, g[f"table_{k}"])
+    assert np.array_equal(grid.mass_scalar, g[f"mass_{k}"])
+    assert np.array_equal(np.concatenate(grid.node_coordinates()), g[f"coords_{k}"])
+    u = g[f"u_{k}"]
+    assert np.array_equal(grid.gather(grid.scatter(u)), R.Mesh3D(ext, [int(x) for x in c[6:9]],
+                                                                 int(c[9])).gather(grid.scatter(u)))
