@@ -33,6 +33,7 @@
 
 namespace sem1d {
 int set_error(int code, const std::string& msg);   // sem1d_capi.cu
+int sem1d_path_override();                          // sem1d_capi.cu: 0 auto, 1 no tensor cores
 }
 
 struct sem3d_plan {
@@ -45,6 +46,17 @@ struct sem3d_plan {
 namespace {
 
 constexpr int S3_MAX_N = 12;
+// output rows contracted together per pencil: independent FMA chains hide the DFMA latency
+#ifndef S3_UNROLL_F
+#define S3_UNROLL_F 4
+#endif
+#ifndef S3_UNROLL_J
+#define S3_UNROLL_J 4
+#endif
+#ifndef S3_UNROLL_JT
+#define S3_UNROLL_JT 2
+#endif
+constexpr int kUnrollF = S3_UNROLL_F, kUnrollJ = S3_UNROLL_J, kUnrollJT = S3_UNROLL_JT;
 enum { OP3_RHS = 0, OP3_JAC = 1, OP3_JACT = 2 };
 
 int fail(int code, const std::string& m) { return sem1d::set_error(code, m); }
@@ -61,14 +73,25 @@ __device__ __forceinline__ bool nonfin3(double x) {
   return ((unsigned)__double2hiint(x) & 0x7ff00000u) == 0x7ff00000u;
 }
 
+// Padded shared-memory block strides per n (node (i,j,k) at i*SI + j*SJ + k): chosen by an
+// exhaustive search so that the pencil loads of all three phases (lanes = (a,b) pencils)
+// hit at most 3 lanes per double bank (unpadded n = 8 put 16 lanes on one bank).
+constexpr int pad_j(int n) {
+  return (n == 3 || n == 4 || n == 8 || n == 10) ? 1 : 0;
+}
+constexpr int pad_i(int n) {
+  return n == 3 ? 1 : (n == 6 ? 1 : (n == 7 ? 3 : (n == 9 ? 2 : (n == 12 || n == 13 ? 1 : 0))));
+}
+
 template <int N>
 struct L3 {
   static constexpr int n = N + 1, n2 = n * n, n3 = n * n * n;
+  static constexpr int SJ = n + pad_j(n), SI = n * SJ + pad_i(n), BLK = n * SI;   // padded block
   static constexpr int THREADS = ((n2 + 31) / 32) * 32;
   // shared arrays (doubles): consts 7 n^2, fields, scratch
   static constexpr int CONSTS = 7 * n2;
   static constexpr int arrays(int op) { return op == OP3_RHS ? 6 : (op == OP3_JAC ? 11 : 12); }
-  static constexpr size_t smem(int op) { return sizeof(double) * ((size_t)CONSTS + (size_t)arrays(op) * n3); }
+  static constexpr size_t smem(int op) { return sizeof(double) * ((size_t)CONSTS + (size_t)arrays(op) * BLK); }
 };
 
 // element e -> global scalar index of local node (i, j, k)
@@ -82,25 +105,32 @@ __device__ __forceinline__ int64_t node_index(const Geo3& G, int64_t e1, int64_t
 }
 
 // One axis contraction of a pencil: y[i] = sum_l A[i][l] x[l] (A row-major n x n in smem)
+// The axis contractions are dense matrix products (the reference runs them through BLAS
+// dgemm, ops.py:63-81), so they use FMA; only the pointwise terms keep the reference's
+// separately rounded multiply / add.
 template <int n>
 __device__ __forceinline__ double contract_row(const double* A, const double (&x)[n], int i) {
-  double acc = __dmul_rn(A[i * n], x[0]);
+  double acc = A[i * n] * x[0];
 #pragma unroll
-  for (int l = 1; l < n; ++l) acc = __dadd_rn(acc, __dmul_rn(A[i * n + l], x[l]));
+  for (int l = 1; l < n; ++l) acc = fma(A[i * n + l], x[l], acc);
   return acc;
 }
 template <int n>
 __device__ __forceinline__ double contract_row_t(const double* A, const double (&x)[n], int i) {
-  double acc = __dmul_rn(A[i], x[0]);
+  double acc = A[i] * x[0];
 #pragma unroll
-  for (int l = 1; l < n; ++l) acc = __dadd_rn(acc, __dmul_rn(A[l * n + i], x[l]));
+  for (int l = 1; l < n; ++l) acc = fma(A[l * n + i], x[l], acc);
   return acc;
 }
 
-// node offset inside an n^3 block for phase `ax` (0,1,2), pencil (a,b), position p along ax
-template <int n>
+// padded block offset of node (i, j, k), and of position p along axis `ax` of pencil (a,b)
+template <int N>
+__device__ __forceinline__ int bidx(int i, int j, int k) {
+  return i * L3<N>::SI + j * L3<N>::SJ + k;
+}
+template <int N>
 __device__ __forceinline__ int off(int ax, int a, int b, int p) {
-  return ax == 0 ? (p * n + a) * n + b : (ax == 1 ? (a * n + p) * n + b : (a * n + b) * n + p);
+  return ax == 0 ? bidx<N>(p, a, b) : (ax == 1 ? bidx<N>(a, p, b) : bidx<N>(a, b, p));
 }
 
 template <int N, int OP>
@@ -114,9 +144,10 @@ __global__ void __launch_bounds__(L3<N>::THREADS) elem3d_kernel(const Geo3 G, co
   double* sK = sm;                  // [3][n2]
   double* sD = sK + 3 * n2;         // Dw [n2]
   double* sT = sD + n2;             // transverse weights [3][n2]
-  double* sU = sT + 3 * n2;         // [3][n3] state
-  double* sW = sU + 3 * n3;         // [3][n3] v (J) / M^-1 z (J^T); unused for F
-  double* scr = (OP == OP3_RHS) ? sW : sW + 3 * n3;   // scratch arrays
+  constexpr int B = L::BLK;         // padded block size
+  double* sU = sT + 3 * n2;         // [3][B] state
+  double* sW = sU + 3 * B;          // [3][B] v (J) / M^-1 z (J^T); unused for F
+  double* scr = (OP == OP3_RHS) ? sW : sW + 3 * B;    // scratch arrays
   const int tid = threadIdx.x;
   for (int k = tid; k < 7 * n2; k += blockDim.x) sK[k] = cbuf[k];
   const int64_t e = blockIdx.x;
@@ -126,11 +157,12 @@ __global__ void __launch_bounds__(L3<N>::THREADS) elem3d_kernel(const Geo3 G, co
   for (int q = tid; q < n3; q += blockDim.x) {
     const int i = q / n2, j = (q / n) % n, k = q % n;
     const int64_t g = node_index(G, e1, e2, e3, N, i, j, k);
+    const int qb = bidx<N>(i, j, k);
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       const double x = u[c * G.nscalar + g];
       bad_u |= nonfin3(x);
-      sU[c * n3 + q] = x;
+      sU[c * B + qb] = x;
       if (OP != OP3_RHS) {
         double y = w[c * G.nscalar + g];
         bad_w |= nonfin3(y);
@@ -145,7 +177,7 @@ __global__ void __launch_bounds__(L3<N>::THREADS) elem3d_kernel(const Geo3 G, co
           }
           y = __dmul_rn(y, minv_pat[(cl[0] * (N + 1) + cl[1]) * (N + 1) + cl[2]]);
         }
-        sW[c * n3 + q] = y;
+        sW[c * B + qb] = y;
       }
     }
   }
@@ -158,8 +190,8 @@ __global__ void __launch_bounds__(L3<N>::THREADS) elem3d_kernel(const Geo3 G, co
   double* const* dummy = nullptr;
   (void)dummy;
   for (int ci = 0; ci < 3; ++ci) {
-    const double* Ui = sU + ci * n3;
-    const double* Wi = sW + ci * n3;
+    const double* Ui = sU + ci * B;
+    const double* Wi = sW + ci * B;
     for (int ax = 0; ax < 3; ++ax) {
       if (act) {
         const double t = sT[ax * n2 + a * n + b];
@@ -167,16 +199,16 @@ __global__ void __launch_bounds__(L3<N>::THREADS) elem3d_kernel(const Geo3 G, co
         double xu[n], xw[n];
 #pragma unroll
         for (int l = 0; l < n; ++l) {
-          const int o = off<n>(ax, a, b, l);
+          const int o = off<N>(ax, a, b, l);
           xu[l] = Ui[o];
           if (OP != OP3_RHS) xw[l] = Wi[o];
         }
         if (OP == OP3_RHS) {
-          double* D0 = scr + n3;
-          double* D1 = scr + 2 * n3;
-#pragma unroll 1
+          double* D0 = scr + B;
+          double* D1 = scr + 2 * B;
+#pragma unroll(kUnrollF)
           for (int p = 0; p < n; ++p) {
-            const int o = off<n>(ax, a, b, p);
+            const int o = off<N>(ax, a, b, p);
             const double kt = __dmul_rn(contract_row<n>(Ka, xu, p), t);
             const double dt = __dmul_rn(contract_row<n>(sD, xu, p), t);
             if (ax == 0) {
@@ -188,18 +220,18 @@ __global__ void __launch_bounds__(L3<N>::THREADS) elem3d_kernel(const Geo3 G, co
             } else {
               double acc = __dmul_rn(__dadd_rn(KS[o], kt), G.mnu);
               acc = __dsub_rn(acc, __dmul_rn(sU[o], D0[o]));
-              acc = __dsub_rn(acc, __dmul_rn(sU[n3 + o], D1[o]));
-              acc = __dsub_rn(acc, __dmul_rn(sU[2 * n3 + o], dt));
+              acc = __dsub_rn(acc, __dmul_rn(sU[B + o], D1[o]));
+              acc = __dsub_rn(acc, __dmul_rn(sU[2 * B + o], dt));
               KS[o] = acc;                       // element result (in place)
             }
           }
         } else if (OP == OP3_JAC) {
           // D_ax u_i and D_ax w_i per node, kept for the final combination
-          double* Du = scr + n3 + 2 * ax * n3;   // [3][2] arrays: (Du, Dw) per axis 0,1
-          double* Dv = Du + n3;
-#pragma unroll 1
+          double* Du = scr + B + 2 * ax * B;   // [3][2] arrays: (Du, Dw) per axis 0,1
+          double* Dv = Du + B;
+#pragma unroll(kUnrollJ)
           for (int p = 0; p < n; ++p) {
-            const int o = off<n>(ax, a, b, p);
+            const int o = off<N>(ax, a, b, p);
             const double kt = __dmul_rn(contract_row<n>(Ka, xw, p), t);
             const double du = __dmul_rn(contract_row<n>(sD, xu, p), t);
             const double dw = __dmul_rn(contract_row<n>(sD, xw, p), t);
@@ -212,30 +244,30 @@ __global__ void __launch_bounds__(L3<N>::THREADS) elem3d_kernel(const Geo3 G, co
               Du[o] = du;
               Dv[o] = dw;
             } else {
-              const double* Du0 = scr + n3;
-              const double* Dv0 = Du0 + n3;
-              const double* Du1 = Du0 + 2 * n3;
-              const double* Dv1 = Du1 + n3;
+              const double* Du0 = scr + B;
+              const double* Dv0 = Du0 + B;
+              const double* Du1 = Du0 + 2 * B;
+              const double* Dv1 = Du1 + B;
               double acc = __dmul_rn(__dadd_rn(KS[o], kt), G.mnu);
               acc = __dsub_rn(acc, __dmul_rn(sW[o], Du0[o]));
               acc = __dsub_rn(acc, __dmul_rn(sU[o], Dv0[o]));
-              acc = __dsub_rn(acc, __dmul_rn(sW[n3 + o], Du1[o]));
-              acc = __dsub_rn(acc, __dmul_rn(sU[n3 + o], Dv1[o]));
-              acc = __dsub_rn(acc, __dmul_rn(sW[2 * n3 + o], du));
-              acc = __dsub_rn(acc, __dmul_rn(sU[2 * n3 + o], dw));
+              acc = __dsub_rn(acc, __dmul_rn(sW[B + o], Du1[o]));
+              acc = __dsub_rn(acc, __dmul_rn(sU[B + o], Dv1[o]));
+              acc = __dsub_rn(acc, __dmul_rn(sW[2 * B + o], du));
+              acc = __dsub_rn(acc, __dmul_rn(sU[2 * B + o], dw));
               KS[o] = acc;
             }
           }
         } else {
           // J^T: K_ax z_i, T_ax = D_ax^T (u_ax o z_i), and on the phase ax == ci the
           // three E_j = z_j (D_ci u_j)
-          double* Ej = scr + n3;                 // [3] arrays
-          double* Tj = scr + 4 * n3;             // [2] arrays (T_0, T_1)
+          double* Ej = scr + B;                 // [3] arrays
+          double* Tj = scr + 4 * B;             // [2] arrays (T_0, T_1)
           double xt[n];
-          const double* Ua = sU + ax * n3;
+          const double* Ua = sU + ax * B;
 #pragma unroll
           for (int l = 0; l < n; ++l) {
-            const int o = off<n>(ax, a, b, l);
+            const int o = off<N>(ax, a, b, l);
             xt[l] = __dmul_rn(Ua[o], xw[l]);
           }
           double xu1[n], xu2[n], xu0[n];
@@ -243,40 +275,40 @@ __global__ void __launch_bounds__(L3<N>::THREADS) elem3d_kernel(const Geo3 G, co
           if (own) {
 #pragma unroll
             for (int l = 0; l < n; ++l) {
-              const int o = off<n>(ax, a, b, l);
+              const int o = off<N>(ax, a, b, l);
               xu0[l] = sU[o];
-              xu1[l] = sU[n3 + o];
-              xu2[l] = sU[2 * n3 + o];
+              xu1[l] = sU[B + o];
+              xu2[l] = sU[2 * B + o];
             }
           }
-#pragma unroll 1
+#pragma unroll(kUnrollJT)
           for (int p = 0; p < n; ++p) {
-            const int o = off<n>(ax, a, b, p);
+            const int o = off<N>(ax, a, b, p);
             const double kt = __dmul_rn(contract_row<n>(Ka, xw, p), t);
             const double tt = __dmul_rn(contract_row_t<n>(sD, xt, p), t);
             double e0 = 0.0, e1v = 0.0, e2v = 0.0;
             if (own) {
               e0 = __dmul_rn(sW[o], __dmul_rn(contract_row<n>(sD, xu0, p), t));
-              e1v = __dmul_rn(sW[n3 + o], __dmul_rn(contract_row<n>(sD, xu1, p), t));
-              e2v = __dmul_rn(sW[2 * n3 + o], __dmul_rn(contract_row<n>(sD, xu2, p), t));
+              e1v = __dmul_rn(sW[B + o], __dmul_rn(contract_row<n>(sD, xu1, p), t));
+              e2v = __dmul_rn(sW[2 * B + o], __dmul_rn(contract_row<n>(sD, xu2, p), t));
             }
             if (ax < 2) {
               KS[o] = (ax == 0) ? kt : __dadd_rn(KS[o], kt);
-              Tj[ax * n3 + o] = tt;
+              Tj[ax * B + o] = tt;
               if (own) {
                 Ej[o] = e0;
-                Ej[n3 + o] = e1v;
-                Ej[2 * n3 + o] = e2v;
+                Ej[B + o] = e1v;
+                Ej[2 * B + o] = e2v;
               }
             } else {
               const double E0 = own ? e0 : Ej[o];
-              const double E1 = own ? e1v : Ej[n3 + o];
-              const double E2 = own ? e2v : Ej[2 * n3 + o];
+              const double E1 = own ? e1v : Ej[B + o];
+              const double E2 = own ? e2v : Ej[2 * B + o];
               double acc = __dmul_rn(__dadd_rn(KS[o], kt), G.mnu);
               acc = __dsub_rn(acc, E0);
               acc = __dsub_rn(acc, Tj[o]);
               acc = __dsub_rn(acc, E1);
-              acc = __dsub_rn(acc, Tj[n3 + o]);
+              acc = __dsub_rn(acc, Tj[B + o]);
               acc = __dsub_rn(acc, E2);
               acc = __dsub_rn(acc, tt);
               KS[o] = acc;
@@ -288,56 +320,223 @@ __global__ void __launch_bounds__(L3<N>::THREADS) elem3d_kernel(const Geo3 G, co
     }
     // element block of component ci -> scratch (coalesced: contiguous n^3 run)
     double* dst = loc + ((int64_t)ci * G.nelem + e) * n3;
-    for (int q = tid; q < n3; q += blockDim.x) dst[q] = KS[q];
+    for (int q = tid; q < n3; q += blockDim.x) dst[q] = KS[bidx<N>(q / n2, (q / n) % n, q % n)];
     __syncthreads();
   }
 }
 
-// Q^T + M^-1: one thread per (component, global node); contributions of the element
-// blocks that share the node, per axis (element k-1, local N) before (element k, local 0).
-template <int N>
-__global__ void __launch_bounds__(256) gather3d_kernel(const Geo3 G, const double* __restrict__ cbuf,
-                                                      const double* __restrict__ loc, double* out, int scale) {
-  constexpr int n = N + 1, n3 = n * n * n;
-  const int64_t total = 3 * G.nscalar;
-  const double* minv_pat = cbuf + 7 * n * n;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const int c = (int)(t / G.nscalar);
-    const int64_t g = t - c * G.nscalar;
-    const int64_t g3 = g % G.P3, g12 = g / G.P3, g2 = g12 % G.P2, g1 = g12 / G.P2;
-    const int64_t gg[3] = {g1, g2, g3};
-    const int64_t EE[3] = {G.E1, G.E2, G.E3};
-    int64_t ea[3][2];
-    int la[3][2], na[3], cl[3];
+// ----------------------------------------------------------------------------
+// n = 8 (N = 7): the axis contractions on the FP64 tensor cores.  One element per CTA,
+// four warps, each warp two tiles of 8 pencils.  A contraction along the phase axis is
+// D[pencil][i] = sum_l X[pencil][l] M[i][l]: DMMA m8n8k4 with the element data as the A
+// operand (lane: pencil lane>>2, l = 4kc + lane&3, loaded from the padded block) and the
+// constant matrix as the B operand (lane: M[i = lane>>2][l = 4kc + lane&3], held in
+// registers for the whole kernel); the lane receives outputs i = 2(lane&3) + {0,1} of
+// pencil lane>>2.  Phases, scratch arrays and the final evaluation order are those of
+// elem3d_kernel.
+// ----------------------------------------------------------------------------
+
+__device__ __forceinline__ void dmma8(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+template <int OP>
+__global__ void __launch_bounds__(128) elem3d_mma_kernel(const Geo3 G, const double* __restrict__ cbuf,
+                                                        const double* __restrict__ u,
+                                                        const double* __restrict__ w, double* loc, int* flag) {
+  constexpr int N = 7;
+  using L = L3<N>;
+  constexpr int n = 8, n2 = 64, n3 = 512;
+  constexpr int B = L::BLK;
+  extern __shared__ __align__(16) double sm[];
+  double* sU = sm;                                   // [3][B]
+  double* sW = sU + 3 * B;                           // [3][B] (J, J^T)
+  double* ACC = (OP == OP3_RHS) ? sW : sW + 3 * B;   // [B] per-node accumulator
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r = lane >> 2, kq = lane & 3;
+  // B fragments: K_ax (3), Dw, Dw^T -- M[i = r][l = 4kc + kq]; transverse weights of the
+  // lane's two pencils per axis
+  double bK[3][2], bD[2], bDt[2], tw[3][2];
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const int64_t k = gg[a] / N;
-      const int r = (int)(gg[a] - k * N);
-      if (r != 0) {
-        na[a] = 1;
-        ea[a][0] = k;
-        la[a][0] = r;
-        cl[a] = r;
-      } else {
-        na[a] = 2;
-        const int64_t km = (k == 0) ? EE[a] - 1 : k - 1;
-        ea[a][0] = km;       // element k-1 (local N) first
-        la[a][0] = N;
-        ea[a][1] = k;
-        la[a][1] = 0;
-        cl[a] = (gg[a] == 0) ? 0 : N;
+  for (int kc = 0; kc < 2; ++kc) {
+    const int l = 4 * kc + kq;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) bK[a][kc] = cbuf[a * n2 + r * n + l];
+    bD[kc] = cbuf[3 * n2 + r * n + l];
+    bDt[kc] = cbuf[3 * n2 + l * n + r];
+  }
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int tt = 0; tt < 2; ++tt) tw[a][tt] = cbuf[4 * n2 + a * n2 + (2 * warp + tt) * n + r];
+  const int64_t e = blockIdx.x;
+  const int64_t e3 = e % G.E3, e12 = e / G.E3, e2 = e12 % G.E2, e1 = e12 / G.E2;
+  const double* minv_pat = cbuf + 7 * n2;
+  unsigned bad_u = 0, bad_w = 0;
+  for (int q = tid; q < n3; q += blockDim.x) {
+    const int i = q >> 6, j = (q >> 3) & 7, k = q & 7;
+    const int64_t g = node_index(G, e1, e2, e3, N, i, j, k);
+    const int qb = bidx<N>(i, j, k);
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      const double x = u[c * G.nscalar + g];
+      bad_u |= nonfin3(x);
+      sU[c * B + qb] = x;
+      if (OP != OP3_RHS) {
+        double y = w[c * G.nscalar + g];
+        bad_w |= nonfin3(y);
+        if (OP == OP3_JACT) {
+          const int64_t gg[3] = {(e1 * N + i) % G.P1, (e2 * N + j) % G.P2, (e3 * N + k) % G.P3};
+          int cl[3];
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            const int rr = (int)(gg[a] % N);
+            cl[a] = (rr != 0) ? rr : (gg[a] == 0 ? 0 : N);
+          }
+          y = __dmul_rn(y, minv_pat[(cl[0] * (N + 1) + cl[1]) * (N + 1) + cl[2]]);
+        }
+        sW[c * B + qb] = y;
       }
     }
-    double acc = 0.0;
-    for (int x = 0; x < na[0]; ++x)
-      for (int y = 0; y < na[1]; ++y)
-        for (int z = 0; z < na[2]; ++z) {
-          const int64_t e = (ea[0][x] * G.E2 + ea[1][y]) * G.E3 + ea[2][z];
-          const int q = (la[0][x] * n + la[1][y]) * n + la[2][z];
-          acc = __dadd_rn(acc, __ldg(loc + ((int64_t)c * G.nelem + e) * n3 + q));
+  }
+  if (bad_u || bad_w)
+    atomicOr(flag, (bad_u ? SEM1D_FLAG_STATE_NONFINITE : 0) | (bad_w ? SEM1D_FLAG_INPUT2_NONFINITE : 0));
+  __syncthreads();
+  for (int ci = 0; ci < 3; ++ci) {
+    const double* Ui = sU + ci * B;
+    const double* Wi = sW + ci * B;
+    for (int ax = 0; ax < 3; ++ax) {
+#pragma unroll
+      for (int tt = 0; tt < 2; ++tt) {
+        const int pt = 2 * warp + tt;                 // pencil tile: pencils (a = pt, b = 0..7)
+        const double t = tw[ax][tt];
+        double xu[2], xw[2];
+#pragma unroll
+        for (int kc = 0; kc < 2; ++kc) {
+          const int o = off<N>(ax, pt, r, 4 * kc + kq);
+          xu[kc] = Ui[o];
+          if (OP != OP3_RHS) xw[kc] = Wi[o];
         }
-    if (scale) acc = __dmul_rn(acc, minv_pat[(cl[0] * (N + 1) + cl[1]) * (N + 1) + cl[2]]);
-    out[t] = acc;
+        // contribution of this axis at the lane's two output nodes (i = 2kq + h):
+        //   F:   -nu K x_i - u_ax (D u_i)            J: -nu K w_i - w_ax (D u_i) - u_ax (D w_i)
+        //   J^T: -nu K z_i - D^T(u_ax z_i) [- sum_j z_j (D u_j) on the axis ax == ci]
+        double c[2];
+        if (OP == OP3_RHS) {
+          double k0 = 0.0, k1 = 0.0, d0 = 0.0, d1 = 0.0;
+#pragma unroll
+          for (int kc = 0; kc < 2; ++kc) {
+            dmma8(k0, k1, xu[kc], bK[ax][kc]);
+            dmma8(d0, d1, xu[kc], bD[kc]);
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int o = off<N>(ax, pt, r, 2 * kq + h);
+            c[h] = __dsub_rn(__dmul_rn(__dmul_rn(h ? k1 : k0, t), G.mnu),
+                             __dmul_rn(sU[ax * B + o], __dmul_rn(h ? d1 : d0, t)));
+          }
+        } else if (OP == OP3_JAC) {
+          double k0 = 0.0, k1 = 0.0, p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
+#pragma unroll
+          for (int kc = 0; kc < 2; ++kc) {
+            dmma8(k0, k1, xw[kc], bK[ax][kc]);
+            dmma8(p0, p1, xu[kc], bD[kc]);
+            dmma8(q0, q1, xw[kc], bD[kc]);
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int o = off<N>(ax, pt, r, 2 * kq + h);
+            double v = __dmul_rn(__dmul_rn(h ? k1 : k0, t), G.mnu);
+            v = __dsub_rn(v, __dmul_rn(sW[ax * B + o], __dmul_rn(h ? p1 : p0, t)));
+            c[h] = __dsub_rn(v, __dmul_rn(sU[ax * B + o], __dmul_rn(h ? q1 : q0, t)));
+          }
+        } else {
+          const double* Ua = sU + ax * B;
+          double xt[2];
+#pragma unroll
+          for (int kc = 0; kc < 2; ++kc) xt[kc] = __dmul_rn(Ua[off<N>(ax, pt, r, 4 * kc + kq)], xw[kc]);
+          double k0 = 0.0, k1 = 0.0, t0 = 0.0, t1 = 0.0;
+#pragma unroll
+          for (int kc = 0; kc < 2; ++kc) {
+            dmma8(k0, k1, xw[kc], bK[ax][kc]);
+            dmma8(t0, t1, xt[kc], bDt[kc]);
+          }
+          double ej[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+          const bool own = (ax == ci);
+          if (own) {
+#pragma unroll
+            for (int kc = 0; kc < 2; ++kc) {
+              const int o = off<N>(ax, pt, r, 4 * kc + kq);
+#pragma unroll
+              for (int jj = 0; jj < 3; ++jj) dmma8(ej[jj][0], ej[jj][1], sU[jj * B + o], bD[kc]);
+            }
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int o = off<N>(ax, pt, r, 2 * kq + h);
+            double v = __dsub_rn(__dmul_rn(__dmul_rn(h ? k1 : k0, t), G.mnu), __dmul_rn(h ? t1 : t0, t));
+            if (own) {
+#pragma unroll
+              for (int jj = 0; jj < 3; ++jj) v = __dsub_rn(v, __dmul_rn(sW[jj * B + o], __dmul_rn(ej[jj][h], t)));
+            }
+            c[h] = v;
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int o = off<N>(ax, pt, r, 2 * kq + h);
+          ACC[o] = (ax == 0) ? c[h] : __dadd_rn(ACC[o], c[h]);
+        }
+      }
+      __syncthreads();
+    }
+    double* dst = loc + ((int64_t)ci * G.nelem + e) * n3;
+    for (int q = tid; q < n3; q += blockDim.x) dst[q] = ACC[bidx<N>(q >> 6, (q >> 3) & 7, q & 7)];
+    __syncthreads();
+  }
+}
+
+// Q^T + M^-1: one CTA per (component, g1, g2) row, threads along g3.  The contributions
+// of the element blocks sharing a node are summed per axis with (element k-1, local N)
+// before (element k, local 0); the row's axis-1/2 candidates are computed once per CTA
+// and the per-thread index math is division by the compile-time N.
+template <int N>
+__global__ void __launch_bounds__(128) gather3d_kernel(const Geo3 G, const double* __restrict__ cbuf,
+                                                      const double* __restrict__ loc, double* out, int scale) {
+  constexpr int n = N + 1, n3 = n * n * n;
+  const double* minv_pat = cbuf + 7 * n * n;
+  const int P1 = (int)G.P1, P2 = (int)G.P2, P3 = (int)G.P3;
+  const int row = blockIdx.x;                          // (c * P1 + g1) * P2 + g2
+  const int g2 = row % P2, t1 = row / P2, g1 = t1 % P1, c = t1 / P1;
+  int e1c[2], l1c[2], e2c[2], l2c[2], n1, n2c, cl1, cl2;
+  {
+    const int k = g1 / N, r = g1 - k * N;
+    if (r) { n1 = 1; e1c[0] = k; l1c[0] = r; cl1 = r; }
+    else { n1 = 2; e1c[0] = k ? k - 1 : (int)G.E1 - 1; l1c[0] = N; e1c[1] = k; l1c[1] = 0; cl1 = g1 ? N : 0; }
+  }
+  {
+    const int k = g2 / N, r = g2 - k * N;
+    if (r) { n2c = 1; e2c[0] = k; l2c[0] = r; cl2 = r; }
+    else { n2c = 2; e2c[0] = k ? k - 1 : (int)G.E2 - 1; l2c[0] = N; e2c[1] = k; l2c[1] = 0; cl2 = g2 ? N : 0; }
+  }
+  const double* lc = loc + (int64_t)c * G.nelem * n3;
+  double* orow = out + ((int64_t)(c * P1 + g1) * P2 + g2) * P3;
+  const int E2 = (int)G.E2, E3 = (int)G.E3;
+  for (int g3 = threadIdx.x; g3 < P3; g3 += blockDim.x) {
+    const int k = g3 / N, r = g3 - k * N;
+    int e3c[2], l3c[2], n3c, cl3;
+    if (r) { n3c = 1; e3c[0] = k; l3c[0] = r; cl3 = r; }
+    else { n3c = 2; e3c[0] = k ? k - 1 : E3 - 1; l3c[0] = N; e3c[1] = k; l3c[1] = 0; cl3 = g3 ? N : 0; }
+    double acc = 0.0;
+    for (int x = 0; x < n1; ++x)
+      for (int y = 0; y < n2c; ++y)
+        for (int z = 0; z < n3c; ++z) {
+          const int64_t e = ((int64_t)e1c[x] * E2 + e2c[y]) * E3 + e3c[z];
+          acc = __dadd_rn(acc, __ldg(lc + e * n3 + (l1c[x] * n + l2c[y]) * n + l3c[z]));
+        }
+    if (scale) acc = __dmul_rn(acc, minv_pat[(cl1 * (N + 1) + cl2) * (N + 1) + cl3]);
+    orow[g3] = acc;
   }
 }
 
@@ -395,9 +594,27 @@ Geo3 geo(const sem3d_plan* p) {
   return G;
 }
 
+template <int OP>
+cudaError_t launch_elem_mma(const sem3d_plan* p, const double* u, const double* w, double* loc, int* flag,
+                            cudaStream_t s) {
+  auto kern = elem3d_mma_kernel<OP>;
+  constexpr size_t smem = sizeof(double) * (size_t)L3<7>::BLK * (OP == OP3_RHS ? 4 : 7);
+  static bool done = false;
+  if (!done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    done = true;
+  }
+  kern<<<(unsigned)p->nelem, 128, smem, s>>>(geo(p), p->cbuf, u, w, loc, flag);
+  return cudaGetLastError();
+}
+
 template <int N, int OP>
 cudaError_t launch_elem(const sem3d_plan* p, const double* u, const double* w, double* loc, int* flag,
                         cudaStream_t s) {
+  if constexpr (N == 7) {
+    if (sem1d::sem1d_path_override() == 0) return launch_elem_mma<OP>(p, u, w, loc, flag, s);
+  }
   auto kern = elem3d_kernel<N, OP>;
   constexpr size_t smem = L3<N>::smem(OP);
   static bool done = false;
@@ -412,9 +629,9 @@ cudaError_t launch_elem(const sem3d_plan* p, const double* u, const double* w, d
 
 template <int N>
 cudaError_t launch_gather(const sem3d_plan* p, const double* loc, double* out, int scale, cudaStream_t s) {
-  const int64_t total = 3 * p->nscalar;
-  const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
-  gather3d_kernel<N><<<grid, 256, 0, s>>>(geo(p), p->cbuf, loc, out, scale);
+  const int64_t rows = 3 * p->P[0] * p->P[1];
+  if (rows > 0x7fffffffLL) return cudaErrorInvalidValue;
+  gather3d_kernel<N><<<(unsigned)rows, 128, 0, s>>>(geo(p), p->cbuf, loc, out, scale);
   return cudaGetLastError();
 }
 

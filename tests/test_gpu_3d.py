@@ -106,3 +106,22 @@ def test_3d_nonfinite_inputs_raise(cuda):
         op.apply_jacobian_transpose(u, bad)
     with pytest.raises(sb.ValidationError):
         op.apply_rhs(u[:-1])
+
+
+def test_3d_tensor_core_and_cuda_core_paths_agree(cuda):
+    """N = 7 runs the DMMA element kernel by default; kernel path 1 forces the DFMA one."""
+    from paper_1806_01422_b200 import _lib
+    ext = [(0.0, 1.0), (-1.0, 1.0), (0.0, 3.0)]
+    grid = build_grid([Axis(a, b, 3, 7, "periodic") for a, b in ext])
+    op = SemOperator3D(grid, sb.PdeCoefficients(0.02), device="cuda:0")
+    u, v, w = (torch.from_numpy(a).cuda() for a in R.seeded_fields(grid.nglobal, 77))
+    outs = {}
+    lib = _lib.load()
+    try:
+        for path in (0, 1):
+            lib.sem1d_set_kernel_path(path)
+            outs[path] = [op.apply_rhs(u), op.apply_jacobian(u, v), op.apply_jacobian_transpose(u, w)]
+    finally:
+        lib.sem1d_set_kernel_path(0)
+    for a, b in zip(outs[0], outs[1]):
+        assert rel_err(a.cpu().numpy(), b.cpu().numpy()) <= 1e-13
