@@ -280,6 +280,19 @@ int sem3d_jact(const sem3d_plan* plan, const double* u, const double* z, double*
                double* work, int* flag, void* stream);
 int sem3d_terminal(const sem3d_plan* plan, const double* uN, const double* ud, double* lam,
                    double* J, double* work, void* stream);
+/* Crank-Nicolson on 3D boxes: the sem1d_cn_* drivers over the 3D operators.  `work` holds
+ * sem3d_cn_work_size(plan, restart) doubles (Krylov workspace + element scratch), zeroed once. */
+int64_t sem3d_cn_work_size(const sem3d_plan* plan, int restart);
+int sem3d_cn_step(const sem3d_plan* plan, const double* u, double* v, double dt,
+                  const sem1d_cn_params* params, double* work, int* flag, sem1d_cn_stats* st,
+                  void* stream);
+int sem3d_cn_adjoint_step(const sem3d_plan* plan, const double* u_n, const double* u_np1,
+                          const double* lam, double* lam_out, double dt,
+                          const sem1d_cn_params* params, double* work, int* flag,
+                          sem1d_cn_stats* st, void* stream);
+int sem3d_gmres(const sem3d_plan* plan, int transpose, const double* p, double alpha,
+                const double* b, double* x, const sem1d_cn_params* params, double* work,
+                int* flag, sem1d_cn_stats* st, void* stream);
 
 #ifdef __cplusplus
 }

@@ -101,6 +101,15 @@ SIGNATURES = {
     "sem3d_jac": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "sem3d_jact": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "sem3d_terminal": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    "sem3d_cn_work_size": (c_int64, [c_void_p, c_int]),
+    "sem3d_cn_step": (c_int, [c_void_p, c_void_p, c_void_p, c_double, ctypes.POINTER(CnParams),
+                              c_void_p, c_void_p, ctypes.POINTER(CnStats), c_void_p]),
+    "sem3d_cn_adjoint_step": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double,
+                                      ctypes.POINTER(CnParams), c_void_p, c_void_p,
+                                      ctypes.POINTER(CnStats), c_void_p]),
+    "sem3d_gmres": (c_int, [c_void_p, c_int, c_void_p, c_double, c_void_p, c_void_p,
+                            ctypes.POINTER(CnParams), c_void_p, c_void_p, ctypes.POINTER(CnStats),
+                            c_void_p]),
 }
 
 _lock = threading.Lock()

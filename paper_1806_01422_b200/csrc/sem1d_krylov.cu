@@ -353,8 +353,29 @@ void lartg(double f, double g, double& c, double& s, double& r) {
   }
 }
 
+// The operator the Krylov drivers run on: a 1D plan (sem1d_*) or a 3D plan (sem3d_*,
+// which also needs its element-block scratch).
+struct OpIf {
+  const void* plan;
+  int is3d;
+  double* work3d;
+  int64_t n;
+  int rhs(const double* u, double* f, int* flag, void* s) const {
+    return is3d ? sem3d_rhs(static_cast<const sem3d_plan*>(plan), u, f, work3d, flag, s)
+                : sem1d_rhs(static_cast<const sem1d_plan*>(plan), u, f, flag, s);
+  }
+  int jac(const double* u, const double* v, double* out, int* flag, void* s) const {
+    return is3d ? sem3d_jac(static_cast<const sem3d_plan*>(plan), u, v, out, work3d, flag, s)
+                : sem1d_jac(static_cast<const sem1d_plan*>(plan), u, v, out, flag, s);
+  }
+  int jact(const double* u, const double* z, double* out, int* flag, void* s) const {
+    return is3d ? sem3d_jact(static_cast<const sem3d_plan*>(plan), u, z, out, work3d, flag, s)
+                : sem1d_jact(static_cast<const sem1d_plan*>(plan), u, z, out, flag, s);
+  }
+};
+
 struct Gmres {
-  const sem1d_plan* plan;
+  const OpIf* plan;
   int op;                 // 0: J(p), 1: J(p)^T
   const double* p;        // linearisation point
   double alpha;           // operator x + alpha * J x
@@ -365,7 +386,7 @@ struct Gmres {
   int64_t matvecs = 0;
 
   int jop(const double* x, double* out) {
-    return op == 0 ? sem1d_jac(plan, p, x, out, flag, v.s) : sem1d_jact(plan, p, x, out, flag, v.s);
+    return op == 0 ? plan->jac(p, x, out, flag, v.s) : plan->jact(p, x, out, flag, v.s);
   }
 };
 
@@ -553,22 +574,12 @@ Layout layout(double* work, int64_t n, int restart) {
   return L;
 }
 
-}  // namespace
-
-extern "C" {
-
-int64_t sem1d_cn_work_size(const sem1d_plan* plan, int restart) {
-  if (!plan || restart < 1 || restart > MAX_RESTART) return -1;
-  const int64_t n = sem1d_plan_ndof(plan);
-  return (int64_t)(restart + 1) * n + 4 * n + RED_DOUBLES + 3 * MAX_RESTART + 16 + 2;
-}
-
-int sem1d_gmres(const sem1d_plan* plan, int transpose, const double* p, double alpha, const double* b,
-                double* x, const sem1d_cn_params* P, double* work, int* flag, sem1d_cn_stats* st,
-                void* stream) {
-  if (!plan || !p || !b || !x || !work || !flag || !st || sem1d::plan_batch(plan) != 1)
-    return fail(SEM1D_EINVAL, "sem1d_gmres: bad argument (batch-1 plan, device pointers)");
-  const int64_t n = sem1d_plan_ndof(plan);
+int gmres_impl(const OpIf& op, int transpose, const double* p, double alpha, const double* b, double* x,
+               const sem1d_cn_params* P, double* work, int* flag, sem1d_cn_stats* st, void* stream) {
+  if (!p || !b || !x || !work || !flag || !st)
+    return fail(SEM1D_EINVAL, "gmres: bad argument (device pointers)");
+  const int64_t n = op.n;
+  const OpIf* plan = &op;
   if (!check_params(P, n)) return fail(SEM1D_EINVAL, "sem1d_gmres: bad parameters (1 <= restart <= 64)");
   const int restart = (int)std::min<int64_t>(P->gmres_restart, n);
   const Layout L = layout(work, n, P->gmres_restart);
@@ -584,11 +595,12 @@ int sem1d_gmres(const sem1d_plan* plan, int transpose, const double* p, double a
   return rc;
 }
 
-int sem1d_cn_step(const sem1d_plan* plan, const double* u, double* v, double dt, const sem1d_cn_params* P,
-                  double* work, int* flag, sem1d_cn_stats* st, void* stream) {
-  if (!plan || !u || !v || u == v || !work || !flag || !st || sem1d::plan_batch(plan) != 1)
-    return fail(SEM1D_EINVAL, "sem1d_cn_step: bad argument (batch-1 plan, v must not alias u)");
-  const int64_t n = sem1d_plan_ndof(plan);
+int cn_step_impl(const OpIf& op, const double* u, double* v, double dt, const sem1d_cn_params* P,
+                 double* work, int* flag, sem1d_cn_stats* st, void* stream) {
+  if (!u || !v || u == v || !work || !flag || !st)
+    return fail(SEM1D_EINVAL, "cn_step: bad argument (v must not alias u)");
+  const int64_t n = op.n;
+  const OpIf* plan = &op;
   if (!check_params(P, n)) return fail(SEM1D_EINVAL, "sem1d_cn_step: bad parameters (1 <= restart <= 64)");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const Layout L = layout(work, n, P->gmres_restart);
@@ -597,7 +609,7 @@ int sem1d_cn_step(const sem1d_plan* plan, const double* u, double* v, double dt,
   int rc, hflag = 0;
   cudaError_t e;
   // fu = f(u) (timeloop.py:166); the input check of apply_rhs raises NumericFailure
-  if ((rc = sem1d_rhs(plan, u, L.fu, flag, stream))) return rc;
+  if ((rc = plan->rhs(u, L.fu, flag, stream))) return rc;
   st->rhs_applies += 1;
   if ((rc = read_flag(vv, flag, &hflag))) return rc;
   if (hflag) { st->status = SEM1D_CN_INPUT_NONFINITE; return SEM1D_OK; }
@@ -609,7 +621,7 @@ int sem1d_cn_step(const sem1d_plan* plan, const double* u, double* v, double dt,
   const double h = 0.5 * dt;
   int iters = 0;
   while (true) {
-    if ((rc = sem1d_rhs(plan, v, L.t, flag, stream))) return rc;          // f(v)
+    if ((rc = plan->rhs(v, L.t, flag, stream))) return rc;          // f(v)
     st->rhs_applies += 1;
     int* rflag = reinterpret_cast<int*>(L.scal + 3 * MAX_RESTART + 8);
     e = cudaMemsetAsync(rflag, 0, sizeof(int), s);
@@ -648,13 +660,13 @@ int sem1d_cn_step(const sem1d_plan* plan, const double* u, double* v, double dt,
   return e == cudaSuccess ? SEM1D_OK : cuda_fail(e, "sem1d_cn_step");
 }
 
-int sem1d_cn_adjoint_step(const sem1d_plan* plan, const double* u_n, const double* u_np1, const double* lam,
-                          double* lam_out, double dt, const sem1d_cn_params* P, double* work, int* flag,
-                          sem1d_cn_stats* st, void* stream) {
-  if (!plan || !u_n || !u_np1 || !lam || !lam_out || lam_out == lam || !work || !flag || !st ||
-      sem1d::plan_batch(plan) != 1)
-    return fail(SEM1D_EINVAL, "sem1d_cn_adjoint_step: bad argument (batch-1 plan, lam_out must not alias lam)");
-  const int64_t n = sem1d_plan_ndof(plan);
+int cn_adjoint_impl(const OpIf& op, const double* u_n, const double* u_np1, const double* lam, double* lam_out,
+                    double dt, const sem1d_cn_params* P, double* work, int* flag, sem1d_cn_stats* st,
+                    void* stream) {
+  if (!u_n || !u_np1 || !lam || !lam_out || lam_out == lam || !work || !flag || !st)
+    return fail(SEM1D_EINVAL, "cn_adjoint_step: bad argument (lam_out must not alias lam)");
+  const int64_t n = op.n;
+  const OpIf* plan = &op;
   if (!check_params(P, n)) return fail(SEM1D_EINVAL, "sem1d_cn_adjoint_step: bad parameters");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const Layout L = layout(work, n, P->gmres_restart);
@@ -675,11 +687,79 @@ int sem1d_cn_adjoint_step(const sem1d_plan* plan, const double* u_n, const doubl
   if (hflag || nonfinite) { st->status = SEM1D_CN_INPUT_NONFINITE; st->gmres_info = -1; return SEM1D_OK; }
   if (info != 0) { st->status = SEM1D_CN_GMRES_FAILED; st->gmres_info = info; return SEM1D_OK; }
   // lam_n = mu + dt/2 J^T(u_n) mu  (adjoint.py:69)
-  if ((rc = sem1d_jact(plan, u_n, L.delta, L.t, flag, stream))) return rc;
+  if ((rc = plan->jact(u_n, L.delta, L.t, flag, stream))) return rc;
   st->jact_applies += 1;
   k_shift_dot2<<<KB, KT, 0, s>>>(n, L.delta, L.t, h, lam_out, nullptr, L.red, L.scal);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? SEM1D_OK : cuda_fail(e, "sem1d_cn_adjoint_step");
+}
+
+}  // namespace
+
+extern "C" {
+
+int64_t sem1d_cn_work_size(const sem1d_plan* plan, int restart) {
+  if (!plan || restart < 1 || restart > MAX_RESTART) return -1;
+  const int64_t n = sem1d_plan_ndof(plan);
+  return (int64_t)(restart + 1) * n + 4 * n + RED_DOUBLES + 3 * MAX_RESTART + 16 + 2;
+}
+
+int sem1d_gmres(const sem1d_plan* plan, int transpose, const double* p, double alpha, const double* b,
+                double* x, const sem1d_cn_params* P, double* work, int* flag, sem1d_cn_stats* st,
+                void* stream) {
+  if (!plan || sem1d::plan_batch(plan) != 1) return fail(SEM1D_EINVAL, "sem1d_gmres: needs a batch-1 plan");
+  return gmres_impl(OpIf{plan, 0, nullptr, sem1d_plan_ndof(plan)}, transpose, p, alpha, b, x, P, work, flag,
+                    st, stream);
+}
+
+int sem1d_cn_step(const sem1d_plan* plan, const double* u, double* v, double dt, const sem1d_cn_params* P,
+                  double* work, int* flag, sem1d_cn_stats* st, void* stream) {
+  if (!plan || sem1d::plan_batch(plan) != 1) return fail(SEM1D_EINVAL, "sem1d_cn_step: needs a batch-1 plan");
+  return cn_step_impl(OpIf{plan, 0, nullptr, sem1d_plan_ndof(plan)}, u, v, dt, P, work, flag, st, stream);
+}
+
+int sem1d_cn_adjoint_step(const sem1d_plan* plan, const double* u_n, const double* u_np1, const double* lam,
+                          double* lam_out, double dt, const sem1d_cn_params* P, double* work, int* flag,
+                          sem1d_cn_stats* st, void* stream) {
+  if (!plan || sem1d::plan_batch(plan) != 1)
+    return fail(SEM1D_EINVAL, "sem1d_cn_adjoint_step: needs a batch-1 plan");
+  return cn_adjoint_impl(OpIf{plan, 0, nullptr, sem1d_plan_ndof(plan)}, u_n, u_np1, lam, lam_out, dt, P, work,
+                         flag, st, stream);
+}
+
+// 3D: `work` = the Krylov workspace for n = ndof, then the element-block scratch
+static int64_t krylov_doubles(int64_t n, int restart) {
+  return (int64_t)(restart + 1) * n + 4 * n + RED_DOUBLES + 3 * MAX_RESTART + 16 + 2;
+}
+
+int64_t sem3d_cn_work_size(const sem3d_plan* plan, int restart) {
+  if (!plan || restart < 1 || restart > MAX_RESTART) return -1;
+  return krylov_doubles(sem3d_plan_ndof(plan), restart) + sem3d_work_size(plan);
+}
+
+static OpIf op3(const sem3d_plan* plan, double* work, int restart) {
+  const int64_t n = sem3d_plan_ndof(plan);
+  return OpIf{plan, 1, work + krylov_doubles(n, restart), n};
+}
+
+int sem3d_gmres(const sem3d_plan* plan, int transpose, const double* p, double alpha, const double* b, double* x,
+                const sem1d_cn_params* P, double* work, int* flag, sem1d_cn_stats* st, void* stream) {
+  if (!plan || !P || !work) return fail(SEM1D_EINVAL, "sem3d_gmres: bad argument");
+  return gmres_impl(op3(plan, work, P->gmres_restart), transpose, p, alpha, b, x, P, work, flag, st, stream);
+}
+
+int sem3d_cn_step(const sem3d_plan* plan, const double* u, double* v, double dt, const sem1d_cn_params* P,
+                  double* work, int* flag, sem1d_cn_stats* st, void* stream) {
+  if (!plan || !P || !work) return fail(SEM1D_EINVAL, "sem3d_cn_step: bad argument");
+  return cn_step_impl(op3(plan, work, P->gmres_restart), u, v, dt, P, work, flag, st, stream);
+}
+
+int sem3d_cn_adjoint_step(const sem3d_plan* plan, const double* u_n, const double* u_np1, const double* lam,
+                          double* lam_out, double dt, const sem1d_cn_params* P, double* work, int* flag,
+                          sem1d_cn_stats* st, void* stream) {
+  if (!plan || !P || !work) return fail(SEM1D_EINVAL, "sem3d_cn_adjoint_step: bad argument");
+  return cn_adjoint_impl(op3(plan, work, P->gmres_restart), u_n, u_np1, lam, lam_out, dt, P, work, flag, st,
+                         stream);
 }
 
 int sem1d_vec_dot(int64_t n, const double* x, const double* y, double* work, double* out, void* stream) {

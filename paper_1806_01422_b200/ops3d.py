@@ -193,6 +193,37 @@ class SemOperator3D:
                                                 _lib.ptr_array([t.data_ptr() for t in acc]),
                                                 lam_out.data_ptr(), s), "sem1d_vec_accumulate")
 
+    # -- Crank-Nicolson (sem3d_cn_*: the native Newton / GMRES drivers over the 3D applies) --
+
+    def _cn_work(self, restart):
+        torch = _torch()
+        ws = getattr(self, "_cn_ws", None)
+        if ws is None or ws[0] != int(restart):
+            n = _lib.load().sem3d_cn_work_size(self._plan.handle, int(restart))
+            if n < 0:
+                raise ValidationError(f"gmres_restart={restart} outside the kernel limit 1..64")
+            self._cn_ws = (int(restart), torch.zeros(int(n), dtype=torch.float64, device=self.device))
+        return self._cn_ws[1]
+
+    def launch_cn_step(self, u, v, dt, cfg, st):
+        from .ops import SemOperator
+        work = self._cn_work(cfg.gmres_restart)
+        self._flag.zero_()
+        p = SemOperator._cn_params(cfg)
+        _lib.check(_lib.load().sem3d_cn_step(self._plan.handle, u.data_ptr(), v.data_ptr(), float(dt),
+                                             ctypes.byref(p), work.data_ptr(), self._flag.data_ptr(),
+                                             ctypes.byref(st), self._stream()), "sem3d_cn_step")
+
+    def launch_cn_adjoint_step(self, u_n, u_np1, lam, lam_out, dt, cfg, st):
+        from .ops import SemOperator
+        work = self._cn_work(cfg.gmres_restart)
+        self._flag.zero_()
+        p = SemOperator._cn_params(cfg)
+        _lib.check(_lib.load().sem3d_cn_adjoint_step(
+            self._plan.handle, u_n.data_ptr(), u_np1.data_ptr(), lam.data_ptr(), lam_out.data_ptr(),
+            float(dt), ctypes.byref(p), work.data_ptr(), self._flag.data_ptr(), ctypes.byref(st),
+            self._stream()), "sem3d_cn_adjoint_step")
+
     def launch_terminal(self, uN, ud, lam, J_out):
         _lib.check(_lib.load().sem3d_terminal(self._plan.handle, uN.data_ptr(), ud.data_ptr(), lam.data_ptr(),
                                               J_out.data_ptr(), self._work.data_ptr(), self._stream()),

@@ -65,7 +65,7 @@ def test_3d_dense_jacobian_matches_oracle(cuda):
     assert rel_err(d, dref) <= 1e-12
 
 
-@pytest.mark.parametrize("scheme", ["rk3"])
+@pytest.mark.parametrize("scheme", ["rk3", "cn"])
 def test_burgers3d_evaluate_matches_reference(cuda, scheme):
     g = golden("grid3d.npz")
     prob = problems.make_problem("burgers3d", elements=2, degree=3, steps=6, horizon=0.03,
@@ -76,6 +76,9 @@ def test_burgers3d_evaluate_matches_reference(cuda, scheme):
     assert abs(j - g[f"b3d_{scheme}_J"][0]) <= 1e-9 * abs(g[f"b3d_{scheme}_J"][0])
     assert rel_err(gr, g[f"b3d_{scheme}_grad"]) <= 1e-9
     assert rel_err(prob.last_forward.u_final.cpu().numpy(), g[f"b3d_{scheme}_ufinal"]) <= 1e-12
+    st = prob.last_forward.stats
+    assert [st["steps"], st["newton_iters"], st["gmres_iters"], prob.op.last_sweep_stats["gmres_iters"]] == \
+        list(g[f"b3d_{scheme}_stats"])
 
 
 def test_burgers3d_gradient_finite_difference_and_binomial(cuda):
