@@ -80,6 +80,12 @@ int sem1d_plan_create(int64_t n_elements, int degree, int periodic, double nu,
                       const double* minv_pattern, int64_t batch, sem1d_plan** out);
 int sem1d_plan_destroy(sem1d_plan* plan);
 int64_t sem1d_plan_ndof(const sem1d_plan* plan);
+/* Advection kind of the plan (ops.py:44-60, 147-212): 0 Burgers (default), 1 linear with
+ * constant speed `speed` (F = M^-1 Q^T(-nu K u - speed Dw u), J v = the same map on v,
+ * J^T z = Q^T(-nu K zm - speed Dw^T zm)), 2 none (diffusion only).  Plans of kind 1 / 2
+ * run sem1d_rhs / sem1d_jac / sem1d_jact through a generic kernel; the fused stage, step and
+ * ensemble entry points accept Burgers plans only (SEM1D_EINVAL otherwise). */
+int sem1d_plan_set_advection(sem1d_plan* plan, int mode, double speed);
 
 /* f = M^-1 Q^T F_e(Q u) (masked).  ops.py:232-236 */
 int sem1d_rhs(const sem1d_plan* plan, const double* u, double* f, int* flag, void* stream);

@@ -217,6 +217,42 @@ class BurgersOracle:
         return cols
 
 
+class AdvectionOracle(BurgersOracle):
+    """The LINEAR (constant speed a) and NONE advection branches of ops.py:147-212 in 1D:
+    F = M^-1 Q^T(-nu K u - a Dw u), J v = F-part on v, J^T z = Q^T(-nu K zm - a Dw^T zm)."""
+
+    def __init__(self, mesh, nu, kind, speed=None):
+        super().__init__(mesh, nu)
+        self.kind = kind
+        self.a = float(np.atleast_1d(speed)[0]) if kind == "linear" else 0.0
+
+    def _lin(self, xl, transpose=False):
+        acc = xl @ self.K.T
+        acc *= -self.nu
+        if self.kind == "linear":
+            acc -= self.a * (xl @ self.Dw if transpose else xl @ self.Dw.T)
+        return acc
+
+    def rhs(self, u):
+        u = self._finite(u)
+        out = self.mesh.assemble(self._lin(self.mesh.localize(u)))
+        out *= self.minv
+        return self.mesh.apply_mask(out)
+
+    def jac(self, u, v):
+        self._finite(u)
+        v = self._finite(v)
+        out = self.mesh.assemble(self._lin(self.mesh.localize(v)))
+        out *= self.minv
+        return self.mesh.apply_mask(out)
+
+    def jact(self, u, z):
+        self._finite(u)
+        z = self._finite(z)
+        zm = self.mesh.apply_mask(z * self.minv)
+        return self.mesh.apply_mask(self.mesh.assemble(self._lin(self.mesh.localize(zm), True)))
+
+
 # --------------------------------------------------------------------------
 # 3D periodic boxes, sum-factorised operators (reference grid.py:112-146,
 # ops.py:63-81,109-115,127-212) -- same numpy primitives and evaluation order

@@ -53,6 +53,7 @@ SIGNATURES = {
                                   c_void_p, c_int64, ctypes.POINTER(c_void_p)]),
     "sem1d_plan_destroy": (c_int, [c_void_p]),
     "sem1d_plan_ndof": (c_int64, [c_void_p]),
+    "sem1d_plan_set_advection": (c_int, [c_void_p, c_int, c_double]),
     "sem1d_rhs": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "sem1d_jac": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     "sem1d_jact": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),

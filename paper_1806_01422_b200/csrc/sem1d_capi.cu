@@ -40,6 +40,9 @@ struct sem1d_plan {
   double nu;
   std::vector<double> packed;  // Consts<N> image
   std::vector<double> mass, minv;
+  int adv = 0;                 // 0 Burgers, 1 linear (constant speed), 2 none (ops.py:147-212)
+  double speed = 0.0;
+  double* dconst = nullptr;    // advection kinds: device K[n*n], Dw[n*n], minv[N+2]
 };
 
 namespace {
@@ -163,6 +166,9 @@ bool make_tableau(int scheme, Tableau& t) {
 }
 
 bool valid_plan(const sem1d_plan* p) { return p != nullptr && p->N >= 1 && p->N <= SEM1D_MAX_DEGREE; }
+// fused stage / step / ensemble kernels implement Burgers advection only; plans with another
+// advection kind compose their stages from F / J^T applies and the vector kernels
+bool valid_burgers(const sem1d_plan* p) { return valid_plan(p) && p->adv == 0; }
 
 Args blank_args() {
   Args a;
@@ -313,6 +319,115 @@ int sem1d_set_kernel_path(int path) {
 const char* sem1d_last_error(void) { return g_err.c_str(); }
 int sem1d_max_degree(void) { return SEM1D_MAX_DEGREE; }
 
+// ---- LINEAR / NONE advection (ops.py:147-212 branches) --------------------------------
+// One thread per (problem, global node): the node's (at most two) element rows
+//   row_i(x) = (K x)_i * (-nu) - a (Dw x)_i          (F, J: x = u resp. v)
+//   row_i(x) = (K x)_i * (-nu) - a (Dw^T x)_i        (J^T:  x = mask(M^-1 z))
+// summed in the reference gather order ((element k-1, local N) + (element k, local 0)),
+// then M^-1 and the Dirichlet mask (F, J) or the mask (J^T).  For these operators J(u)v
+// does not depend on u, which is still checked for NaN/Inf like ops.py:216-223 does.
+namespace {
+__device__ __forceinline__ bool nonfin_adv(double x) {
+  return ((unsigned)__double2hiint(x) & 0x7ff00000u) == 0x7ff00000u;
+}
+
+__device__ __forceinline__ double adv_minv(const double* mi, int N, int64_t g, int64_t ndof, int periodic) {
+  if (!periodic && g == 0) return mi[N];
+  if (!periodic && g == ndof - 1) return mi[N + 1];
+  return mi[g % N];
+}
+
+__global__ void adv_apply_kernel(int N, int64_t E, int64_t ndof, int periodic, double mnu, double a, int mode,
+                                 int op, const double* __restrict__ cst, const double* __restrict__ u,
+                                 const double* __restrict__ w, double* __restrict__ out, int* flag) {
+  extern __shared__ double sc[];
+  const int n = N + 1;
+  for (int k = threadIdx.x; k < 2 * n * n + N + 2; k += blockDim.x) sc[k] = cst[k];
+  __syncthreads();
+  const double* K = sc;
+  const double* Dw = sc + n * n;
+  const double* mi = sc + 2 * n * n;
+  const int64_t b = blockIdx.y;
+  const double* ub = u + b * ndof;
+  const double* xb = (op == 0 ? u : w) + b * ndof;
+  unsigned bad_u = 0, bad_w = 0;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < ndof; g += (int64_t)gridDim.x * blockDim.x) {
+    bad_u |= nonfin_adv(ub[g]);
+    if (op != 0) bad_w |= nonfin_adv(w[b * ndof + g]);
+    const int64_t k = g / N;
+    const int r = (int)(g - k * N);
+    // contributing (element, local row) pairs in gather order
+    int64_t ee[2];
+    int rr[2], cnt = 0;
+    if (r != 0) {
+      ee[0] = k; rr[0] = r; cnt = 1;
+    } else if (periodic) {
+      if (k == 0) { ee[0] = 0; rr[0] = 0; ee[1] = E - 1; rr[1] = N; }
+      else { ee[0] = k - 1; rr[0] = N; ee[1] = k; rr[1] = 0; }
+      cnt = 2;
+    } else {
+      if (k == 0) { ee[0] = 0; rr[0] = 0; cnt = 1; }
+      else if (k == E) { ee[0] = E - 1; rr[0] = N; cnt = 1; }
+      else { ee[0] = k - 1; rr[0] = N; ee[1] = k; rr[1] = 0; cnt = 2; }
+    }
+    double acc = 0.0;
+    for (int c = 0; c < cnt; ++c) {
+      const int64_t base = ee[c] * N;
+      const int i = rr[c];
+      double kx = 0.0, dx = 0.0;
+      for (int j = 0; j < n; ++j) {
+        int64_t gj = base + j;
+        if (periodic && gj >= ndof) gj -= ndof;
+        double x = xb[gj];
+        if (op == 2) {                           // J^T input: mask(z M^-1)
+          x = __dmul_rn(x, adv_minv(mi, N, gj, ndof, periodic));
+          if (!periodic && (gj == 0 || gj == ndof - 1)) x = __dmul_rn(x, 0.0);
+        }
+        kx = fma(K[i * n + j], x, kx);
+        if (mode == 1) dx = fma(op == 2 ? Dw[j * n + i] : Dw[i * n + j], x, dx);
+      }
+      double row = __dmul_rn(kx, mnu);
+      if (mode == 1) row = __dsub_rn(row, __dmul_rn(a, dx));
+      acc = (c == 0) ? row : __dadd_rn(acc, row);
+    }
+    if (op != 2) acc = __dmul_rn(acc, adv_minv(mi, N, g, ndof, periodic));
+    if (!periodic && (g == 0 || g == ndof - 1)) acc = __dmul_rn(acc, 0.0);
+    out[b * ndof + g] = acc;
+  }
+  if (bad_u || bad_w)
+    atomicOr(flag, (bad_u ? SEM1D_FLAG_STATE_NONFINITE : 0) | (bad_w ? SEM1D_FLAG_INPUT2_NONFINITE : 0));
+}
+
+int run_adv(const sem1d_plan* p, int op, const double* u, const double* w, double* out, int* flag, void* stream,
+            const char* name) {
+  const int n = p->N + 1;
+  const size_t smem = sizeof(double) * (2 * n * n + p->N + 2);
+  const int64_t blocks = std::min<int64_t>((p->ndof + 255) / 256, 148 * 8);
+  dim3 grid((unsigned)std::max<int64_t>(1, blocks), (unsigned)p->batch);
+  adv_apply_kernel<<<grid, 256, smem, static_cast<cudaStream_t>(stream)>>>(
+      p->N, p->E, p->ndof, p->periodic, -p->nu, p->speed, p->adv, op, p->dconst, u, w, out, flag);
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? SEM1D_OK : cuda_fail(e, name);
+}
+}  // namespace
+
+int sem1d_plan_set_advection(sem1d_plan* plan, int mode, double speed) {
+  if (!plan || mode < 0 || mode > 2 || !std::isfinite(speed))
+    return fail(SEM1D_EINVAL, "sem1d_plan_set_advection: bad argument (mode 0 burgers, 1 linear, 2 none)");
+  plan->adv = mode;
+  plan->speed = (mode == 1) ? speed : 0.0;
+  if (mode != 0 && !plan->dconst) {
+    const int n = plan->N + 1;
+    std::vector<double> h(2 * n * n + plan->N + 2);
+    std::memcpy(h.data(), plan->packed.data(), sizeof(double) * 2 * n * n);     // K, Dw
+    std::memcpy(h.data() + 2 * n * n, plan->minv.data(), sizeof(double) * (plan->N + 2));
+    cudaError_t e = cudaMalloc(&plan->dconst, sizeof(double) * h.size());
+    if (e == cudaSuccess) e = cudaMemcpy(plan->dconst, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return cuda_fail(e, "sem1d_plan_set_advection");
+  }
+  return SEM1D_OK;
+}
+
 int sem1d_plan_create(int64_t n_elements, int degree, int periodic, double nu, const double* K,
                       const double* Dw, const double* mass_pattern, const double* minv_pattern,
                       int64_t batch, sem1d_plan** out) {
@@ -352,6 +467,7 @@ int sem1d_plan_create(int64_t n_elements, int degree, int periodic, double nu, c
 }
 
 int sem1d_plan_destroy(sem1d_plan* plan) {
+  if (plan && plan->dconst) cudaFree(plan->dconst);
   delete plan;
   return SEM1D_OK;
 }
@@ -366,6 +482,7 @@ static int run_apply(const sem1d_plan* p, int kind, const Args& a, void* stream,
 
 int sem1d_rhs(const sem1d_plan* plan, const double* u, double* f, int* flag, void* stream) {
   if (!valid_plan(plan) || !u || !f || !flag) return fail(SEM1D_EINVAL, "sem1d_rhs: bad argument");
+  if (plan->adv) return run_adv(plan, 0, u, nullptr, f, flag, stream, "sem1d_rhs");
   Args a = blank_args();
   a.u = u; a.out = f; a.flag = flag;
   return run_apply(plan, 0, a, stream, "sem1d_rhs");
@@ -374,6 +491,7 @@ int sem1d_rhs(const sem1d_plan* plan, const double* u, double* f, int* flag, voi
 int sem1d_jac(const sem1d_plan* plan, const double* u, const double* v, double* out, int* flag,
               void* stream) {
   if (!valid_plan(plan) || !u || !v || !out || !flag) return fail(SEM1D_EINVAL, "sem1d_jac: bad argument");
+  if (plan->adv) return run_adv(plan, 1, u, v, out, flag, stream, "sem1d_jac");
   Args a = blank_args();
   a.u = u; a.w = v; a.out = out; a.flag = flag;
   return run_apply(plan, 1, a, stream, "sem1d_jac");
@@ -382,6 +500,7 @@ int sem1d_jac(const sem1d_plan* plan, const double* u, const double* v, double* 
 int sem1d_jact(const sem1d_plan* plan, const double* u, const double* z, double* out, int* flag,
                void* stream) {
   if (!valid_plan(plan) || !u || !z || !out || !flag) return fail(SEM1D_EINVAL, "sem1d_jact: bad argument");
+  if (plan->adv) return run_adv(plan, 2, u, z, out, flag, stream, "sem1d_jact");
   Args a = blank_args();
   a.u = u; a.w = z; a.out = out; a.flag = flag;
   return run_apply(plan, 2, a, stream, "sem1d_jact");
@@ -390,7 +509,7 @@ int sem1d_jact(const sem1d_plan* plan, const double* u, const double* z, double*
 int sem1d_rk_stage(const sem1d_plan* plan, const double* U_in, double* k_out, const double* base,
                    int nterms, const double* const* terms, const double* coef, double dt, double* Y,
                    int check_step, int* flag, void* stream) {
-  if (!valid_plan(plan) || !U_in || !base || !Y || !flag || nterms < 1)
+  if (!valid_burgers(plan) || !U_in || !base || !Y || !flag || nterms < 1)
     return fail(SEM1D_EINVAL, "sem1d_rk_stage: bad argument");
   Args a = blank_args();
   a.u = U_in; a.out = k_out; a.flag = flag; a.base = base; a.dt = dt; a.Y = Y;
@@ -404,7 +523,7 @@ int sem1d_adj_stage(const sem1d_plan* plan, const double* U, const double* lam, 
                     const double* const* l_terms, const double* acoef, double dt, double* l_out,
                     int nacc, const double* const* acc_terms, double* lam_out, int* flag,
                     void* stream) {
-  if (!valid_plan(plan) || !U || !lam || !flag) return fail(SEM1D_EINVAL, "sem1d_adj_stage: bad argument");
+  if (!valid_burgers(plan) || !U || !lam || !flag) return fail(SEM1D_EINVAL, "sem1d_adj_stage: bad argument");
   Args a = blank_args();
   a.u = U; a.w = lam; a.b = b; a.out = l_out; a.flag = flag; a.base = lam; a.dt = dt; a.Y = lam_out;
   int rc = fill_combo(a.zin, nl, l_terms, acoef, true, "sem1d_adj_stage(z)");
@@ -418,7 +537,7 @@ int sem1d_adj_stage(const sem1d_plan* plan, const double* U, const double* lam, 
 
 int sem1d_ens_forward(const sem1d_plan* plan, const double* u0, double* traj, double* u_final,
                       const double* dts, int nsteps, int scheme, int* flags, void* stream) {
-  if (!valid_plan(plan) || !u0 || !u_final || !dts || !flags || nsteps < 0)
+  if (!valid_burgers(plan) || !u0 || !u_final || !dts || !flags || nsteps < 0)
     return fail(SEM1D_EINVAL, "sem1d_ens_forward: bad argument");
   EnsArgs a;
   std::memset(&a, 0, sizeof(a));
@@ -435,7 +554,7 @@ int sem1d_ens_forward(const sem1d_plan* plan, const double* u0, double* traj, do
 int sem1d_ens_adjoint(const sem1d_plan* plan, const double* traj, const double* lam_in,
                       double* lam_out, const double* dts, int nsteps, int scheme, int* flags,
                       void* stream) {
-  if (!valid_plan(plan) || !traj || !lam_in || !lam_out || !dts || !flags || nsteps < 0)
+  if (!valid_burgers(plan) || !traj || !lam_in || !lam_out || !dts || !flags || nsteps < 0)
     return fail(SEM1D_EINVAL, "sem1d_ens_adjoint: bad argument");
   EnsAdjArgs a;
   std::memset(&a, 0, sizeof(a));
@@ -450,14 +569,14 @@ int sem1d_ens_adjoint(const sem1d_plan* plan, const double* traj, const double* 
 }
 
 int sem1d_step_supported(const sem1d_plan* plan) {
-  if (!valid_plan(plan)) return 0;
+  if (!valid_burgers(plan)) return 0;
   const int te = ((plan->N + 1) == 8) ? 8 * TILE_WF8 * TILE_WMT8 : ((plan->N + 1) == 32 ? 64 : 128);
   return (plan->periodic && plan->batch == 1 && (plan->N + 1) % 8 == 0 && plan->E >= 2 * te) ? 1 : 0;
 }
 
 int sem1d_rk_step(const sem1d_plan* plan, const double* u, double* u_new, double dt, int scheme,
                   int* flag, void* stream) {
-  if (!valid_plan(plan) || !u || !u_new || !flag || u == u_new)
+  if (!valid_burgers(plan) || !u || !u_new || !flag || u == u_new)
     return fail(SEM1D_EINVAL, "sem1d_rk_step: bad argument (u_new must not alias u)");
   TileStepArgs a;
   std::memset(&a, 0, sizeof(a));
@@ -472,7 +591,7 @@ int sem1d_rk_step(const sem1d_plan* plan, const double* u, double* u_new, double
 
 int sem1d_adj_step(const sem1d_plan* plan, const double* u, const double* lam, double* lam_out,
                    double dt, int scheme, int* flag, void* stream) {
-  if (!valid_plan(plan) || !u || !lam || !lam_out || !flag || lam == lam_out)
+  if (!valid_burgers(plan) || !u || !lam || !lam_out || !flag || lam == lam_out)
     return fail(SEM1D_EINVAL, "sem1d_adj_step: bad argument (lam_out must not alias lam)");
   TileStepArgs a;
   std::memset(&a, 0, sizeof(a));

@@ -28,23 +28,67 @@ _DENSIFY_LIMIT = 5000
 
 
 class PdeCoefficients:
-    """Viscosity and advection kind (ops.py:42-60).  Only Burgers advection is on
-    the B200 hot path; 'linear' / 'none' are SURVEY 8(f) "next" items."""
+    """Viscosity plus advection kind ('burgers' | 'linear' | 'none') (ops.py:42-60).
+    Burgers runs the fused tensor-core kernels; 'linear' (constant speed) and 'none'
+    run the generic 1D apply kernel with composed stages (sem1d_plan_set_advection)."""
 
     def __init__(self, nu, advection=BURGERS, speed=None):
         if not np.isfinite(nu) or nu < 0.0:
             raise ValidationError(f"viscosity must be >= 0, got {nu!r}")
         if advection not in (BURGERS, LINEAR, NONE):
             raise ValidationError(f"unknown advection kind {advection!r}")
-        if advection != BURGERS:
-            raise ValidationError(
-                f"advection {advection!r} is not on the B200 hot path (only 'burgers')")
         self.nu = float(nu)
         self.advection = advection
-        self.speed = None
+        if advection == LINEAR:
+            if speed is None:
+                raise ValidationError("linear advection needs a speed")
+            self.speed = np.atleast_1d(np.asarray(speed, dtype=float))
+        else:
+            self.speed = None
 
     def __repr__(self):
-        return f"PdeCoefficients(nu={self.nu}, advection={self.advection!r})"
+        return f"PdeCoefficients(nu={self.nu}, advection={self.advection!r}, speed={self.speed})"
+
+
+class ComposedStages:
+    """RK and adjoint stages composed from the F / J^T applies and the library's vector
+    kernels (sem1d_vec_*), with the association orders of sem1d_rk_stage /
+    sem1d_adj_stage -- for operators without fused stage kernels (3D boxes, the
+    linear / none advection kinds).  Needs launch_rhs / launch_jact, _buf, _flag, _stream."""
+
+    def _numel(self):
+        return self.ndof * self.batch
+
+    def _buf(self, key):
+        bufs = self.__dict__.setdefault("_tmp", {})
+        t = bufs.get(key)
+        if t is None:
+            t = self.empty()
+            bufs[key] = t
+        return t
+
+    def compose_rk_stage(self, U_in, k_out, base, terms, coefs, dt, Y, check):
+        k = k_out if k_out is not None else self._buf("k")
+        self.launch_rhs(U_in, k)
+        ptrs = _lib.ptr_array([(k if t is None else t).data_ptr() for t in terms])
+        _lib.check(_lib.load().sem1d_vec_rk_combine(
+            self._numel(), base.data_ptr(), float(dt), len(terms), ptrs, _lib.dbl_array(coefs),
+            Y.data_ptr(), 1 if check else 0, self._flag.data_ptr(), self._stream()), "sem1d_vec_rk_combine")
+
+    def compose_adj_stage(self, U, lam, b, l_terms, a_coefs, dt, l_out, acc_terms, lam_out):
+        lib, s, n = _lib.load(), self._stream(), self._numel()
+        z, jt = self._buf("z"), self._buf("jt")
+        _lib.check(lib.sem1d_vec_adj_combine(n, lam.data_ptr(), float(b), len(l_terms),
+                                             _lib.ptr_array([t.data_ptr() for t in l_terms]),
+                                             _lib.dbl_array(a_coefs), z.data_ptr(), s), "sem1d_vec_adj_combine")
+        self.launch_jact(U, z, jt)
+        lo = l_out if l_out is not None else self._buf("l")
+        _lib.check(lib.sem1d_vec_scale(n, jt.data_ptr(), float(dt), lo.data_ptr(), s), "sem1d_vec_scale")
+        if lam_out is not None:
+            acc = [lo if t is None else t for t in (acc_terms or [])]
+            _lib.check(lib.sem1d_vec_accumulate(n, lam.data_ptr(), len(acc),
+                                                _lib.ptr_array([t.data_ptr() for t in acc]),
+                                                lam_out.data_ptr(), s), "sem1d_vec_accumulate")
 
 
 def _torch():
@@ -88,7 +132,7 @@ class _Plan:
             self.handle = None
 
 
-class SemOperator:
+class SemOperator(ComposedStages):
     """Matrix-free SEM operator bundle for one (grid, coefficients) pair.
 
     ``batch`` > 1 makes every field a (batch, ndof) stack of independent
@@ -117,6 +161,14 @@ class SemOperator:
         if ax.degree > _lib.load().sem1d_max_degree():
             raise ValidationError(f"degree {ax.degree} exceeds the kernel limit")
         self._plan = _Plan(grid, coef.nu, self._kmat, self._dw, self.batch)
+        self._adv = coef.advection != BURGERS
+        if self._adv:
+            if coef.advection == LINEAR and coef.speed.size != grid.ncomp:   # ops.py:95-100
+                raise ValidationError(f"linear advection speed has {coef.speed.size} components, "
+                                      f"grid has {grid.ncomp}")
+            mode, a = (1, float(coef.speed[0])) if coef.advection == LINEAR else (2, 0.0)
+            _lib.check(_lib.load().sem1d_plan_set_advection(self._plan.handle, mode, a),
+                       "sem1d_plan_set_advection")
         self.ndof = grid.nglobal
         self.shape = (self.ndof,) if self.batch == 1 else (self.batch, self.ndof)
         self._flag = torch.zeros(1, dtype=torch.int32, device=self.device)
@@ -189,6 +241,8 @@ class SemOperator:
                    "sem1d_jact")
 
     def launch_rk_stage(self, U_in, k_out, base, terms, coefs, dt, Y, check):
+        if self._adv:
+            return self.compose_rk_stage(U_in, k_out, base, terms, coefs, dt, Y, check)
         ptrs = _lib.ptr_array([None if t is None else t.data_ptr() for t in terms])
         cf = _lib.dbl_array(coefs)
         _lib.check(_lib.load().sem1d_rk_stage(
@@ -197,6 +251,8 @@ class SemOperator:
             self._flag.data_ptr(), self._stream()), "sem1d_rk_stage")
 
     def launch_adj_stage(self, U, lam, b, l_terms, a_coefs, dt, l_out, acc_terms, lam_out):
+        if self._adv:
+            return self.compose_adj_stage(U, lam, b, l_terms, a_coefs, dt, l_out, acc_terms, lam_out)
         lp = _lib.ptr_array([t.data_ptr() for t in l_terms])
         ac = _lib.dbl_array(a_coefs)
         accp = _lib.ptr_array([None if t is None else t.data_ptr() for t in (acc_terms or [])])
@@ -231,7 +287,7 @@ class SemOperator:
     def step_fused_supported(self):
         """Whole-step fused kernels apply (periodic batch-1 ring, n % 8 == 0, >= 2 tiles)."""
         if not hasattr(self, "_step_ok"):
-            self._step_ok = bool(_lib.load().sem1d_step_supported(self._plan.handle))
+            self._step_ok = bool(_lib.load().sem1d_step_supported(self._plan.handle)) and not self._adv
         return self._step_ok and getattr(self, "use_fused_steps", True)
 
     def launch_rk_step(self, u, u_new, dt, scheme):

@@ -20,7 +20,7 @@ import numpy as np
 from . import _lib
 from .errors import NumericFailure, ValidationError
 from .grid import Grid3D
-from .ops import BURGERS, _stream_handle, _torch
+from .ops import BURGERS, ComposedStages, _stream_handle, _torch
 
 
 class _Plan3D:
@@ -50,7 +50,7 @@ class _Plan3D:
             self.handle = None
 
 
-class SemOperator3D:
+class SemOperator3D(ComposedStages):
     """Matrix-free 3D Burgers operator bundle (ops.py:84-257 with dim 3)."""
 
     def __init__(self, grid, coef, device=None):
@@ -106,13 +106,6 @@ class SemOperator3D:
         torch = _torch()
         return torch.empty(self.shape, dtype=torch.float64, device=self.device)
 
-    def _buf(self, key):
-        t = self._tmp.get(key)
-        if t is None:
-            t = self.empty()
-            self._tmp[key] = t
-        return t
-
     def _stream(self):
         return _stream_handle(self.device)
 
@@ -165,33 +158,12 @@ class SemOperator3D:
                    "sem3d_jact")
 
     def launch_rk_stage(self, U_in, k_out, base, terms, coefs, dt, Y, check):
-        """k = F(U_in) (into k_out or scratch), Y = base + dt * combination (sem1d_rk_stage
-        semantics: a None term is the fresh k)."""
-        k = k_out if k_out is not None else self._buf("k")
-        self.launch_rhs(U_in, k)
-        ptrs = _lib.ptr_array([(k if t is None else t).data_ptr() for t in terms])
-        _lib.check(_lib.load().sem1d_vec_rk_combine(
-            self.ndof, base.data_ptr(), float(dt), len(terms), ptrs, _lib.dbl_array(coefs), Y.data_ptr(),
-            1 if check else 0, self._flag.data_ptr(), self._stream()), "sem1d_vec_rk_combine")
+        """k = F(U_in), Y = base + dt * combination (sem1d_rk_stage semantics)."""
+        self.compose_rk_stage(U_in, k_out, base, terms, coefs, dt, Y, check)
 
     def launch_adj_stage(self, U, lam, b, l_terms, a_coefs, dt, l_out, acc_terms, lam_out):
-        """z = b lam + sum a_j l_j; l = dt J^T(U) z; lam_out = ((lam + L_0) + L_1) + ...
-        (sem1d_adj_stage semantics)."""
-        lib, s = _lib.load(), self._stream()
-        z, jt = self._buf("z"), self._buf("jt")
-        _lib.check(lib.sem1d_vec_adj_combine(self.ndof, lam.data_ptr(), float(b), len(l_terms),
-                                             _lib.ptr_array([t.data_ptr() for t in l_terms]),
-                                             _lib.dbl_array(a_coefs), z.data_ptr(), s),
-                   "sem1d_vec_adj_combine")
-        self.launch_jact(U, z, jt)
-        lo = l_out if l_out is not None else self._buf("l")
-        _lib.check(lib.sem1d_vec_scale(self.ndof, jt.data_ptr(), float(dt), lo.data_ptr(), s),
-                   "sem1d_vec_scale")
-        if lam_out is not None:
-            acc = [lo if t is None else t for t in (acc_terms or [])]
-            _lib.check(lib.sem1d_vec_accumulate(self.ndof, lam.data_ptr(), len(acc),
-                                                _lib.ptr_array([t.data_ptr() for t in acc]),
-                                                lam_out.data_ptr(), s), "sem1d_vec_accumulate")
+        """z = b lam + sum a_j l_j; l = dt J^T(U) z; lam_out = ((lam + L_0) + L_1) + ..."""
+        self.compose_adj_stage(U, lam, b, l_terms, a_coefs, dt, l_out, acc_terms, lam_out)
 
     # -- Crank-Nicolson (sem3d_cn_*: the native Newton / GMRES drivers over the 3D applies) --
 

@@ -8,9 +8,9 @@ reference convention J = d^T M d (adjoint.py:33-47); BASELINE.json quotes
 
 Builders for the BASELINE configurations live in ``configs.py``; the
 reference's ``burgers1d`` problem (Dirichlet Burgers on [-2, 2], Cole-Hopf
-target) and the periodic ``burgers3d`` box are kept here.
-advdiff1d / diffusion1d need LINEAR / NONE advection, outside the B200 path, and
-raise ValidationError.
+target), the periodic ``burgers3d`` box, and the linear
+``advdiff1d`` / pure-diffusion ``diffusion1d`` problems are kept here -- every
+problem of the reference's PROBLEM_BUILDERS (problems.py:293-298).
 """
 
 from __future__ import annotations
@@ -22,7 +22,8 @@ import numpy as np
 from . import adjoint, checkpoint, timeloop
 from .errors import ValidationError
 from .grid import DIRICHLET0, grid_1d, grid_3d
-from .ops import BURGERS, PdeCoefficients, SemOperator
+from .grid import PERIODIC
+from .ops import BURGERS, LINEAR, NONE, PdeCoefficients, SemOperator
 
 
 def burgers1d_exact(x, t, nu):
@@ -165,9 +166,62 @@ def burgers3d_problem(elements=4, degree=8, nu=0.001, horizon=0.1, steps=50, dt=
                                exact_solution=None, checkpoint_slots=checkpoint_slots)
 
 
+def advdiff_coefficients(seed, n_modes=5):
+    """Mode amplitudes drawn once per seed from U[0.9, 1] (problems.py:47-50)."""
+    return np.random.default_rng(seed).uniform(0.9, 1.0, n_modes)
+
+
+def advdiff_reference(x, t, coeffs, nu=1e-5, speed=0.1):
+    """sum_j a_j sin(2 pi j (x - a t)) e^{-4 nu pi^2 j^2 t} (problems.py:53-61)."""
+    x = np.asarray(x, dtype=float)
+    out = np.zeros_like(x)
+    for j, aj in enumerate(np.atleast_1d(coeffs), start=1):
+        out += aj * np.sin(2.0 * np.pi * j * (x - speed * t)) * np.exp(-nu * 4.0 * np.pi ** 2 * j ** 2 * t)
+    return out
+
+
+def diffusion1d_exact(x, t, nu):
+    """Two-mode heat solution (problems.py:81-86)."""
+    x = np.asarray(x, dtype=float)
+    return np.sin(2 * np.pi * x) * np.exp(-nu * 4 * np.pi ** 2 * t) + np.cos(
+        4 * np.pi * x) * np.exp(-nu * 16 * np.pi ** 2 * t)
+
+
+def advdiff1d_problem(elements=8, degree=8, nu=1e-5, speed=0.1, horizon=0.01, steps=100, dt=None,
+                      scheme="rk3", adaptive=False, seed=0, guess_seed=1, n_modes=5,
+                      checkpoint_slots=None, device=None, **ts_kw):
+    """Linear advection-diffusion on the periodic unit interval (problems.py:235-254)."""
+    grid = grid_1d(0.0, 1.0, elements, degree, PERIODIC)
+    op = SemOperator(grid, PdeCoefficients(nu, LINEAR, speed=[speed]), device=device)
+    x = grid.node_coordinates()[0]
+    coeffs, gcoeffs = advdiff_coefficients(seed, n_modes), advdiff_coefficients(guess_seed, n_modes)
+    return AssimilationProblem(
+        name="advdiff1d", grid=grid, op=op, ts=_ts(scheme, horizon, steps, dt, adaptive, **ts_kw),
+        u_target=advdiff_reference(x, horizon, coeffs, nu, speed),
+        u_guess=advdiff_reference(x, 0.0, gcoeffs, nu, speed),
+        u_exact_ic=advdiff_reference(x, 0.0, coeffs, nu, speed),
+        exact_solution=lambda x, t, c=coeffs, nu=nu, a=speed: advdiff_reference(x, t, c, nu, a),
+        checkpoint_slots=checkpoint_slots)
+
+
+def diffusion1d_problem(elements=5, degree=8, nu=0.001, horizon=1.0, steps=100, dt=None, scheme="rk3",
+                        adaptive=False, checkpoint_slots=None, device=None, **ts_kw):
+    """Pure diffusion on the periodic unit interval (problems.py:275-290)."""
+    grid = grid_1d(0.0, 1.0, elements, degree, PERIODIC)
+    op = SemOperator(grid, PdeCoefficients(nu, NONE), device=device)
+    x = grid.node_coordinates()[0]
+    return AssimilationProblem(
+        name="diffusion1d", grid=grid, op=op, ts=_ts(scheme, horizon, steps, dt, adaptive, **ts_kw),
+        u_target=diffusion1d_exact(x, horizon, nu), u_guess=diffusion1d_exact(x, 0.0, nu),
+        u_exact_ic=diffusion1d_exact(x, 0.0, nu),
+        exact_solution=lambda x, t, nu=nu: diffusion1d_exact(x, t, nu),
+        checkpoint_slots=checkpoint_slots)
+
+
 def make_problem(kind, **params):
     from . import configs
     builders = {"burgers1d": burgers1d_problem, "burgers3d": burgers3d_problem,
+                "advdiff1d": advdiff1d_problem, "diffusion1d": diffusion1d_problem,
                 "cfg1": configs.cfg1_problem}
     if kind not in builders:
         raise ValidationError(f"unknown problem {kind!r}; on the B200 path choose from "

@@ -428,6 +428,8 @@ def fixed_step_sizes(cfg):
 
 def ring_resident_supported(op):
     """Whether the whole ring fits one CTA (mirrors launch_ens_forward in csrc)."""
+    if getattr(op.coef, "advection", "burgers") != "burgers" or op.grid.dim != 1:
+        return False                     # the ring-resident kernels implement 1D Burgers
     ax = op.grid.axis
     E, n = ax.elements, ax.degree + 1
     if E * n <= 1024:

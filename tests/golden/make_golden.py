@@ -274,6 +274,38 @@ def grid3d_fixture(grid, ops, problems, timeloop):
     return out
 
 
+def advkinds_fixture(grid, ops, problems):
+    """LINEAR / NONE advection (ops.py:147-212 branches) on 1D grids, and the reference's
+    advdiff1d / diffusion1d problems (problems.py:235-290)."""
+    out = {}
+    cases = [("lin_p", "periodic", ops.LINEAR, [0.3]), ("lin_d", "dirichlet0", ops.LINEAR, [-0.7]),
+             ("none_p", "periodic", ops.NONE, None), ("none_d", "dirichlet0", ops.NONE, None)]
+    for key, bc, kind, speed in cases:
+        g = grid.grid_1d(-1.0, 1.0, 6, 5, bc)
+        op = ops.SemOperator(g, ops.PdeCoefficients(0.02, kind, speed=speed))
+        rng = np.random.default_rng(len(key) * 7 + (1 if bc == "periodic" else 2))
+        u, v, w = (rng.standard_normal(g.nglobal) for _ in range(3))
+        if bc == "dirichlet0":
+            u, v = g.mask(u), g.mask(v)
+        out[f"u_{key}"], out[f"v_{key}"], out[f"w_{key}"] = u, v, w
+        out[f"F_{key}"] = op.apply_rhs(u)
+        out[f"J_{key}"] = op.apply_jacobian(u, v)
+        out[f"JT_{key}"] = op.apply_jacobian_transpose(u, w)
+    for name, kw in (("advdiff1d", {"steps": 20, "horizon": 0.004}),
+                     ("diffusion1d", {"steps": 20, "horizon": 0.01}),
+                     ("advdiff1d_cn", {"steps": 5, "horizon": 0.004, "scheme": "cn"})):
+        kind = name.split("_")[0]
+        prob = problems.make_problem(kind, **kw)
+        u0 = 1.1 * prob.u_guess            # diffusion1d's guess is the exact IC (J ~ 1e-20)
+        j, gr = prob.evaluate(u0)
+        out[f"{name}_u0"] = u0
+        out[f"{name}_J"], out[f"{name}_grad"] = np.array([j]), gr
+        out[f"{name}_ufinal"] = prob.last_forward.u_final
+        out[f"{name}_guess"], out[f"{name}_target"] = prob.u_guess, prob.u_target
+        out[f"{name}_exact_ic"] = prob.u_exact_ic
+    return out
+
+
 SCHED_CASES = [(1, 1), (3, 3), (5, 2), (10, 3), (20, 4), (30, 5), (100, 10), (57, 7), (500, 64)]
 
 
@@ -311,6 +343,7 @@ def main():
                         **implicit_fixture(grid, ops, timeloop, problems))
     np.savez_compressed(os.path.join(HERE, "cli.npz"), **cli_fixture(semopt, grid))
     np.savez_compressed(os.path.join(HERE, "grid3d.npz"), **grid3d_fixture(grid, ops, problems, timeloop))
+    np.savez_compressed(os.path.join(HERE, "advkinds.npz"), **advkinds_fixture(grid, ops, problems))
     print("golden fixtures written to", HERE)
 
 

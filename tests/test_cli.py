@@ -57,7 +57,7 @@ def test_schedule_command_matches_reference(tmp_path):
 
 
 def test_exit_codes_and_config(tmp_path):
-    assert cli.main(["forward", "--problem", "advdiff1d", "--output", str(tmp_path / "x")]) == 2
+    assert cli.main(["forward", "--problem", "nosuch", "--output", str(tmp_path / "x")]) == 2
     assert cli.main(["forward", "--bogus"]) == 2
     assert cli.main(["schedule"]) == 2                              # --steps is required
     cfg = tmp_path / "c.cfg"
@@ -66,5 +66,6 @@ def test_exit_codes_and_config(tmp_path):
     cfg.write_text("problem = diffusion1d  # comment\nsteps = 12\nadaptive = true\ndt = 1e-3\n")
     vals = cli._read_config(str(cfg), cli.build_parser())
     assert vals == {"problem": "diffusion1d", "steps": 12, "adaptive": True, "dt": 1e-3}
-    # file entries are defaults; the problem named by the file is outside the B200 path -> 2
+    # file entries are defaults: an invalid grid from the file is a validation error (2)
+    cfg.write_text("elements = 0\n")
     assert cli.main(["forward", "--config", str(cfg), "--output", str(tmp_path / "x")]) == 2

@@ -207,3 +207,38 @@ def test_adaptive_larger_ring_replays_on_oracle(cuda, form, tol):
         if accepted:
             u = un
     assert rel_err(res.u_final.cpu().numpy(), u) <= 1e-11
+
+
+# -- LINEAR / NONE advection (ops.py:147-212 branches; problems advdiff1d / diffusion1d) ------
+
+ADV_CASES = [("lin_p", "periodic", "linear", [0.3]), ("lin_d", "dirichlet0", "linear", [-0.7]),
+             ("none_p", "periodic", "none", None), ("none_d", "dirichlet0", "none", None)]
+
+
+@pytest.mark.parametrize("key,bc,kind,speed", ADV_CASES)
+def test_advection_kinds_ops_match_reference(cuda, key, bc, kind, speed):
+    g = golden("advkinds.npz")
+    grid = grid_1d(-1.0, 1.0, 6, 5, bc)
+    op = sb.SemOperator(grid, sb.PdeCoefficients(0.02, kind, speed=speed), device="cuda:0")
+    u, v, w = g[f"u_{key}"], g[f"v_{key}"], g[f"w_{key}"]
+    assert rel_err(op.apply_rhs(u), g[f"F_{key}"]) <= 1e-12
+    assert rel_err(op.apply_jacobian(u, v), g[f"J_{key}"]) <= 1e-12
+    assert rel_err(op.apply_jacobian_transpose(u, w), g[f"JT_{key}"]) <= 1e-12
+    bad = u.copy()
+    bad[2] = np.inf                     # u is validated even though J does not use it
+    with pytest.raises(sb.NumericFailure):
+        op.apply_jacobian(bad, v)
+
+
+@pytest.mark.parametrize("name,kw", [("advdiff1d", {"steps": 20, "horizon": 0.004}),
+                                     ("diffusion1d", {"steps": 20, "horizon": 0.01}),
+                                     ("advdiff1d_cn", {"steps": 5, "horizon": 0.004, "scheme": "cn"})])
+def test_advdiff_and_diffusion_problems_match_reference(cuda, name, kw):
+    g = golden("advkinds.npz")
+    prob = problems.make_problem(name.split("_")[0], device="cuda:0", **kw)
+    assert rel_err(prob.u_target, g[f"{name}_target"]) <= 1e-15
+    assert rel_err(prob.u_exact_ic, g[f"{name}_exact_ic"]) <= 1e-15
+    j, gr = prob.evaluate(g[f"{name}_u0"])
+    assert abs(j - g[f"{name}_J"][0]) <= 1e-9 * abs(g[f"{name}_J"][0])
+    assert rel_err(gr, g[f"{name}_grad"]) <= 1e-9
+    assert rel_err(prob.last_forward.u_final.cpu().numpy(), g[f"{name}_ufinal"]) <= 1e-12

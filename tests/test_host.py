@@ -70,8 +70,11 @@ def test_grid_kats_and_validation():
         sb.build_grid([sb.Axis(-1.0, 1.0, 2, 3), sb.Axis(-1.0, 1.0, 2, 4), sb.Axis(-1.0, 1.0, 2, 3)])
     with pytest.raises(sb.ValidationError):
         sb.PdeCoefficients(-1.0)
+    assert sb.PdeCoefficients(0.1, "linear", speed=[1.0]).speed.tolist() == [1.0]   # ops.py:44-60
     with pytest.raises(sb.ValidationError):
-        sb.PdeCoefficients(0.1, "linear", speed=[1.0])
+        sb.PdeCoefficients(0.1, "linear")            # linear advection needs a speed
+    with pytest.raises(sb.ValidationError):
+        sb.PdeCoefficients(0.1, "upwind")
     big = grid_1d(-1.0, 1.0, 1 << 25, 7)  # config 5 size: no O(ndof) host arrays built
     assert big.nglobal == (1 << 25) * 7 and "table" not in big.__dict__
 

@@ -233,3 +233,30 @@ def test_burgers3d_evaluate_bit_exact(scheme):
     assert np.array_equal(uf, g[f"b3d_{scheme}_ufinal"])
     assert [fs["steps"], fs["newton_iters"], fs["gmres_iters"], ss["gmres_iters"]] == \
         list(g[f"b3d_{scheme}_stats"])
+
+
+@pytest.mark.parametrize("key,periodic,kind,speed", [("lin_p", True, "linear", [0.3]),
+                                                     ("lin_d", False, "linear", [-0.7]),
+                                                     ("none_p", True, "none", None),
+                                                     ("none_d", False, "none", None)])
+def test_advection_kinds_bit_exact(key, periodic, kind, speed):
+    """LINEAR / NONE branches of ops.py:147-212 restated (AdvectionOracle)."""
+    g = golden("advkinds.npz")
+    o = R.AdvectionOracle(R.Mesh1D(-1.0, 1.0, 6, 5, periodic), 0.02, kind, speed)
+    u, v, w = g[f"u_{key}"], g[f"v_{key}"], g[f"w_{key}"]
+    assert np.array_equal(o.rhs(u), g[f"F_{key}"])
+    assert np.array_equal(o.jac(u, v), g[f"J_{key}"])
+    assert np.array_equal(o.jact(u, w), g[f"JT_{key}"])
+
+
+@pytest.mark.parametrize("name,kind,speed,nu,E,t_end,steps,scheme", [
+    ("advdiff1d", "linear", [0.1], 1e-5, 8, 0.004, 20, "rk3"),
+    ("diffusion1d", "none", None, 1e-3, 5, 0.01, 20, "rk3"),
+    ("advdiff1d_cn", "linear", [0.1], 1e-5, 8, 0.004, 5, "cn")])
+def test_advdiff_diffusion_problems_bit_exact(name, kind, speed, nu, E, t_end, steps, scheme):
+    g = golden("advkinds.npz")
+    o = R.AdvectionOracle(R.Mesh1D(0.0, 1.0, E, 8, True), nu, kind, speed)
+    j, gr, uf, _, _ = R.evaluate_general(o, g[f"{name}_u0"], g[f"{name}_target"], 0.0, t_end,
+                                         t_end / steps, scheme)
+    assert j == g[f"{name}_J"][0]
+    assert np.array_equal(gr, g[f"{name}_grad"]) and np.array_equal(uf, g[f"{name}_ufinal"])
