@@ -139,6 +139,14 @@ class SemOperator(ComposedStages):
     problems sharing grid and viscosity (BASELINE config 4).
     """
 
+    def __new__(cls, grid, coef, *args, **kwargs):
+        # the reference's SemOperator serves 1D and 3D grids (ops.py:84-124): a 3D grid gets
+        # the sum-factorised operator
+        if cls is SemOperator and getattr(grid, "dim", 1) == 3:
+            from .ops3d import SemOperator3D
+            return SemOperator3D(grid, coef, device=kwargs.get("device", args[0] if args else None))
+        return super().__new__(cls)
+
     def __init__(self, grid, coef, device=None, batch=1, sync_checks=True):
         torch = _torch()
         if not torch.cuda.is_available():

@@ -306,6 +306,26 @@ def advkinds_fixture(grid, ops, problems):
     return out
 
 
+def spectral_fixture(grid, problems):
+    """problems.spectral_error_estimate (problems.py:106-155) on three fields."""
+    out = {}
+    cases = {
+        "burgers": (grid.grid_1d(-2.0, 2.0, 5, 8, "dirichlet0"), None),
+        "smooth": (grid.grid_1d(0.0, 1.0, 6, 10, "periodic"), lambda x: np.sin(2 * np.pi * x) + 0.2 * np.cos(6 * np.pi * x)),
+        "rough": (grid.grid_1d(0.0, 1.0, 4, 6, "periodic"), lambda x: np.abs(np.sin(3 * np.pi * x)) ** 0.5),
+    }
+    for key, (g, fn) in cases.items():
+        if fn is None:
+            vals = problems.make_problem("burgers1d").u_target
+        else:
+            vals = fn(g.node_coordinates()[0])
+        rep = problems.spectral_error_estimate(vals, g)
+        out[f"{key}_values"] = vals
+        for f in ("eps", "sigma", "scale", "a_top", "resolved", "under_resolved"):
+            out[f"{key}_{f}"] = np.asarray(getattr(rep, f))
+    return out
+
+
 SCHED_CASES = [(1, 1), (3, 3), (5, 2), (10, 3), (20, 4), (30, 5), (100, 10), (57, 7), (500, 64)]
 
 
@@ -344,6 +364,7 @@ def main():
     np.savez_compressed(os.path.join(HERE, "cli.npz"), **cli_fixture(semopt, grid))
     np.savez_compressed(os.path.join(HERE, "grid3d.npz"), **grid3d_fixture(grid, ops, problems, timeloop))
     np.savez_compressed(os.path.join(HERE, "advkinds.npz"), **advkinds_fixture(grid, ops, problems))
+    np.savez_compressed(os.path.join(HERE, "spectral.npz"), **spectral_fixture(grid, problems))
     print("golden fixtures written to", HERE)
 
 

@@ -128,3 +128,12 @@ def test_3d_tensor_core_and_cuda_core_paths_agree(cuda):
         lib.sem1d_set_kernel_path(0)
     for a, b in zip(outs[0], outs[1]):
         assert rel_err(a.cpu().numpy(), b.cpu().numpy()) <= 1e-13
+
+
+def test_semoperator_dispatches_3d_grids(cuda):
+    """The reference's single SemOperator class serves 3D grids (ops.py:84-124)."""
+    grid = grid_3d((-2.0, 2.0), 2, 3)
+    op = sb.SemOperator(grid, sb.PdeCoefficients(0.05), device="cuda:0")
+    assert isinstance(op, SemOperator3D)
+    g = golden("grid3d.npz")
+    assert rel_err(op.apply_rhs(g["u_0"]), g["F_0"]) <= 1e-12

@@ -184,3 +184,19 @@ def test_grid3d_maps_bit_exact(k):
     u = g[f"u_{k}"]
     assert np.array_equal(grid.gather(grid.scatter(u)), R.Mesh3D(ext, [int(x) for x in c[6:9]],
                                                                  int(c[9])).gather(grid.scatter(u)))
+
+
+@pytest.mark.parametrize("key,bc,E,N,ext", [("burgers", "dirichlet0", 5, 8, (-2.0, 2.0)),
+                                           ("smooth", "periodic", 6, 10, (0.0, 1.0)),
+                                           ("rough", "periodic", 4, 6, (0.0, 1.0))])
+def test_spectral_error_estimate_matches_reference(key, bc, E, N, ext):
+    """problems.spectral_error_estimate (problems.py:106-155): the vectorised closed-form fits
+    equal the reference's per-element np.polyfit to rounding."""
+    from paper_1806_01422_b200.problems import spectral_error_estimate
+    g = golden("spectral.npz")
+    rep = spectral_error_estimate(g[f"{key}_values"], grid_1d(ext[0], ext[1], E, N, bc))
+    for f in ("resolved", "under_resolved"):
+        assert np.array_equal(getattr(rep, f), g[f"{key}_{f}"])
+    for f in ("sigma", "scale", "a_top", "eps"):
+        ref = g[f"{key}_{f}"]
+        assert np.allclose(getattr(rep, f), ref, rtol=1e-9, atol=1e-300), f
