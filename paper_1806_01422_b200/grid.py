@@ -87,7 +87,15 @@ class Axis:
 
 
 class Grid:
-    """1D mesh + assembly metadata.  Build through :func:`grid_1d`/:func:`build_grid`."""
+    """1D mesh + assembly metadata.  Build through :func:`grid_1d`/:func:`build_grid`;
+    ``Grid(axes)`` with three axes returns a :class:`Grid3D` (the reference's Grid serves
+    both, grid.py:88-146)."""
+
+    def __new__(cls, axes, element_length=None):
+        axes = tuple(axes)
+        if cls is Grid and len(axes) == 3:
+            return Grid3D(axes)
+        return super().__new__(cls)
 
     def __init__(self, axes, element_length=None):
         """``element_length`` overrides (xb - xa) / E: a shard of a larger mesh must use
