@@ -46,17 +46,11 @@ struct sem3d_plan {
 namespace {
 
 constexpr int S3_MAX_N = 12;
-// output rows contracted together per pencil: independent FMA chains hide the DFMA latency
-#ifndef S3_UNROLL_F
-#define S3_UNROLL_F 4
+// output rows contracted together per pencil: independent FMA chains
+#ifndef S3_UNROLL
+#define S3_UNROLL 4
 #endif
-#ifndef S3_UNROLL_J
-#define S3_UNROLL_J 4
-#endif
-#ifndef S3_UNROLL_JT
-#define S3_UNROLL_JT 2
-#endif
-constexpr int kUnrollF = S3_UNROLL_F, kUnrollJ = S3_UNROLL_J, kUnrollJT = S3_UNROLL_JT;
+constexpr int kUnrollF = S3_UNROLL;
 enum { OP3_RHS = 0, OP3_JAC = 1, OP3_JACT = 2 };
 
 int fail(int code, const std::string& m) { return sem1d::set_error(code, m); }
@@ -90,7 +84,7 @@ struct L3 {
   static constexpr int THREADS = ((n2 + 31) / 32) * 32;
   // shared arrays (doubles): consts 7 n^2, fields, scratch
   static constexpr int CONSTS = 7 * n2;
-  static constexpr int arrays(int op) { return op == OP3_RHS ? 6 : (op == OP3_JAC ? 11 : 12); }
+  static constexpr int arrays(int op) { return op == OP3_RHS ? 4 : 7; }
   static constexpr size_t smem(int op) { return sizeof(double) * ((size_t)CONSTS + (size_t)arrays(op) * BLK); }
 };
 
@@ -147,7 +141,7 @@ __global__ void __launch_bounds__(L3<N>::THREADS) elem3d_kernel(const Geo3 G, co
   constexpr int B = L::BLK;         // padded block size
   double* sU = sT + 3 * n2;         // [3][B] state
   double* sW = sU + 3 * B;          // [3][B] v (J) / M^-1 z (J^T); unused for F
-  double* scr = (OP == OP3_RHS) ? sW : sW + 3 * B;    // scratch arrays
+  double* ACC = (OP == OP3_RHS) ? sW : sW + 3 * B;    // [B] per-node accumulator
   const int tid = threadIdx.x;
   for (int k = tid; k < 7 * n2; k += blockDim.x) sK[k] = cbuf[k];
   const int64_t e = blockIdx.x;
@@ -186,141 +180,62 @@ __global__ void __launch_bounds__(L3<N>::THREADS) elem3d_kernel(const Geo3 G, co
   __syncthreads();
   const bool act = tid < n2;
   const int a = tid / n, b = tid % n;
-  double* KS = scr;                 // sum_j K_j x_i (accumulated over the phases)
-  double* const* dummy = nullptr;
-  (void)dummy;
   for (int ci = 0; ci < 3; ++ci) {
     const double* Ui = sU + ci * B;
     const double* Wi = sW + ci * B;
     for (int ax = 0; ax < 3; ++ax) {
       if (act) {
+        // each phase adds its axis' whole contribution at the nodes of the pencil (a, b):
+        //   F:   -nu K_ax u_i - u_ax D_ax u_i          J: -nu K_ax w_i - w_ax D_ax u_i - u_ax D_ax w_i
+        //   J^T: -nu K_ax z_i - D_ax^T (u_ax z_i) [- sum_j z_j D_ax u_j on the axis ax == ci]
         const double t = sT[ax * n2 + a * n + b];
         const double* Ka = sK + ax * n2;
-        double xu[n], xw[n];
+        double xu[n], xw[n], xt[n], x0[n], x1[n], x2[n];
 #pragma unroll
         for (int l = 0; l < n; ++l) {
           const int o = off<N>(ax, a, b, l);
           xu[l] = Ui[o];
           if (OP != OP3_RHS) xw[l] = Wi[o];
+          if (OP == OP3_JACT) xt[l] = __dmul_rn(sU[ax * B + o], xw[l]);
         }
-        if (OP == OP3_RHS) {
-          double* D0 = scr + B;
-          double* D1 = scr + 2 * B;
-#pragma unroll(kUnrollF)
-          for (int p = 0; p < n; ++p) {
-            const int o = off<N>(ax, a, b, p);
-            const double kt = __dmul_rn(contract_row<n>(Ka, xu, p), t);
-            const double dt = __dmul_rn(contract_row<n>(sD, xu, p), t);
-            if (ax == 0) {
-              KS[o] = kt;
-              D0[o] = dt;
-            } else if (ax == 1) {
-              KS[o] = __dadd_rn(KS[o], kt);
-              D1[o] = dt;
-            } else {
-              double acc = __dmul_rn(__dadd_rn(KS[o], kt), G.mnu);
-              acc = __dsub_rn(acc, __dmul_rn(sU[o], D0[o]));
-              acc = __dsub_rn(acc, __dmul_rn(sU[B + o], D1[o]));
-              acc = __dsub_rn(acc, __dmul_rn(sU[2 * B + o], dt));
-              KS[o] = acc;                       // element result (in place)
-            }
-          }
-        } else if (OP == OP3_JAC) {
-          // D_ax u_i and D_ax w_i per node, kept for the final combination
-          double* Du = scr + B + 2 * ax * B;   // [3][2] arrays: (Du, Dw) per axis 0,1
-          double* Dv = Du + B;
-#pragma unroll(kUnrollJ)
-          for (int p = 0; p < n; ++p) {
-            const int o = off<N>(ax, a, b, p);
-            const double kt = __dmul_rn(contract_row<n>(Ka, xw, p), t);
-            const double du = __dmul_rn(contract_row<n>(sD, xu, p), t);
-            const double dw = __dmul_rn(contract_row<n>(sD, xw, p), t);
-            if (ax == 0) {
-              KS[o] = kt;
-              Du[o] = du;
-              Dv[o] = dw;
-            } else if (ax == 1) {
-              KS[o] = __dadd_rn(KS[o], kt);
-              Du[o] = du;
-              Dv[o] = dw;
-            } else {
-              const double* Du0 = scr + B;
-              const double* Dv0 = Du0 + B;
-              const double* Du1 = Du0 + 2 * B;
-              const double* Dv1 = Du1 + B;
-              double acc = __dmul_rn(__dadd_rn(KS[o], kt), G.mnu);
-              acc = __dsub_rn(acc, __dmul_rn(sW[o], Du0[o]));
-              acc = __dsub_rn(acc, __dmul_rn(sU[o], Dv0[o]));
-              acc = __dsub_rn(acc, __dmul_rn(sW[B + o], Du1[o]));
-              acc = __dsub_rn(acc, __dmul_rn(sU[B + o], Dv1[o]));
-              acc = __dsub_rn(acc, __dmul_rn(sW[2 * B + o], du));
-              acc = __dsub_rn(acc, __dmul_rn(sU[2 * B + o], dw));
-              KS[o] = acc;
-            }
-          }
-        } else {
-          // J^T: K_ax z_i, T_ax = D_ax^T (u_ax o z_i), and on the phase ax == ci the
-          // three E_j = z_j (D_ci u_j)
-          double* Ej = scr + B;                 // [3] arrays
-          double* Tj = scr + 4 * B;             // [2] arrays (T_0, T_1)
-          double xt[n];
-          const double* Ua = sU + ax * B;
+        const bool own = (OP == OP3_JACT) && (ax == ci);
+        if (own) {
 #pragma unroll
           for (int l = 0; l < n; ++l) {
             const int o = off<N>(ax, a, b, l);
-            xt[l] = __dmul_rn(Ua[o], xw[l]);
+            x0[l] = sU[o];
+            x1[l] = sU[B + o];
+            x2[l] = sU[2 * B + o];
           }
-          double xu1[n], xu2[n], xu0[n];
-          const bool own = (ax == ci);
-          if (own) {
-#pragma unroll
-            for (int l = 0; l < n; ++l) {
-              const int o = off<N>(ax, a, b, l);
-              xu0[l] = sU[o];
-              xu1[l] = sU[B + o];
-              xu2[l] = sU[2 * B + o];
-            }
-          }
-#pragma unroll(kUnrollJT)
-          for (int p = 0; p < n; ++p) {
-            const int o = off<N>(ax, a, b, p);
-            const double kt = __dmul_rn(contract_row<n>(Ka, xw, p), t);
-            const double tt = __dmul_rn(contract_row_t<n>(sD, xt, p), t);
-            double e0 = 0.0, e1v = 0.0, e2v = 0.0;
+        }
+#pragma unroll(kUnrollF)
+        for (int p = 0; p < n; ++p) {
+          const int o = off<N>(ax, a, b, p);
+          double c;
+          if (OP == OP3_RHS) {
+            c = __dsub_rn(__dmul_rn(__dmul_rn(contract_row<n>(Ka, xu, p), t), G.mnu),
+                          __dmul_rn(sU[ax * B + o], __dmul_rn(contract_row<n>(sD, xu, p), t)));
+          } else if (OP == OP3_JAC) {
+            c = __dmul_rn(__dmul_rn(contract_row<n>(Ka, xw, p), t), G.mnu);
+            c = __dsub_rn(c, __dmul_rn(sW[ax * B + o], __dmul_rn(contract_row<n>(sD, xu, p), t)));
+            c = __dsub_rn(c, __dmul_rn(sU[ax * B + o], __dmul_rn(contract_row<n>(sD, xw, p), t)));
+          } else {
+            c = __dsub_rn(__dmul_rn(__dmul_rn(contract_row<n>(Ka, xw, p), t), G.mnu),
+                          __dmul_rn(contract_row_t<n>(sD, xt, p), t));
             if (own) {
-              e0 = __dmul_rn(sW[o], __dmul_rn(contract_row<n>(sD, xu0, p), t));
-              e1v = __dmul_rn(sW[B + o], __dmul_rn(contract_row<n>(sD, xu1, p), t));
-              e2v = __dmul_rn(sW[2 * B + o], __dmul_rn(contract_row<n>(sD, xu2, p), t));
-            }
-            if (ax < 2) {
-              KS[o] = (ax == 0) ? kt : __dadd_rn(KS[o], kt);
-              Tj[ax * B + o] = tt;
-              if (own) {
-                Ej[o] = e0;
-                Ej[B + o] = e1v;
-                Ej[2 * B + o] = e2v;
-              }
-            } else {
-              const double E0 = own ? e0 : Ej[o];
-              const double E1 = own ? e1v : Ej[B + o];
-              const double E2 = own ? e2v : Ej[2 * B + o];
-              double acc = __dmul_rn(__dadd_rn(KS[o], kt), G.mnu);
-              acc = __dsub_rn(acc, E0);
-              acc = __dsub_rn(acc, Tj[o]);
-              acc = __dsub_rn(acc, E1);
-              acc = __dsub_rn(acc, Tj[B + o]);
-              acc = __dsub_rn(acc, E2);
-              acc = __dsub_rn(acc, tt);
-              KS[o] = acc;
+              c = __dsub_rn(c, __dmul_rn(sW[o], __dmul_rn(contract_row<n>(sD, x0, p), t)));
+              c = __dsub_rn(c, __dmul_rn(sW[B + o], __dmul_rn(contract_row<n>(sD, x1, p), t)));
+              c = __dsub_rn(c, __dmul_rn(sW[2 * B + o], __dmul_rn(contract_row<n>(sD, x2, p), t)));
             }
           }
+          ACC[o] = (ax == 0) ? c : __dadd_rn(ACC[o], c);
         }
       }
       __syncthreads();
     }
     // element block of component ci -> scratch (coalesced: contiguous n^3 run)
     double* dst = loc + ((int64_t)ci * G.nelem + e) * n3;
-    for (int q = tid; q < n3; q += blockDim.x) dst[q] = KS[bidx<N>(q / n2, (q / n) % n, q % n)];
+    for (int q = tid; q < n3; q += blockDim.x) dst[q] = ACC[bidx<N>(q / n2, (q / n) % n, q % n)];
     __syncthreads();
   }
 }
