@@ -915,8 +915,17 @@ typedef double ws_fin_t;
 #ifndef WS_ELEMS8
 #define WS_ELEMS8 256
 #endif
+// n = 32: consumer warps per operator (A/B, config 3): F and J run 8 warps x 2 m-tiles
+// with each shared-memory B fragment feeding both (mtile_compute_multi: 60.7 / 80.0 us vs
+// 63.0 / 82.3 us at 16 x 1); J^T keeps 16 x 1 (96.4 vs 94.3 us)
 #ifndef WS_CW32
-#define WS_CW32 16
+#define WS_CW32 8
+#endif
+#ifndef WS_CW32_JT
+#define WS_CW32_JT 16
+#endif
+#ifndef WS_ELEMS32
+#define WS_ELEMS32 128
 #endif
 
 // Occupancy per operator (A/B-measured on config 2, profiles/r1_ab_occupancy.json):
@@ -964,11 +973,11 @@ __device__ __forceinline__ double bfrag_perm(const Consts<N>& C, int mat, int nt
 template <int N, int OP = OP_RHS>
 struct WsTile {
   static constexpr int n = N + 1;
-  // consumer warps: 16 for n = 32 (FP64-bound, latency hidden by more warps), else 8
-  static constexpr int CW = (n == 32) ? WS_CW32 : 8;
+  // consumer warps: n = 32 per operator (see WS_CW32 above), else 8
+  static constexpr int CW = (n == 32) ? (OP == OP_JACT ? WS_CW32_JT : WS_CW32) : 8;
   static constexpr int THREADS = 32 * (CW + 1);
   static constexpr int ELEMS =
-      (n == 8) ? (OP == OP_RHS ? WS_ELEMS8 : WS_ELEMS8_J) : (n == 32 ? 8 * CW : MmaTile<N>::ELEMS);
+      (n == 8) ? (OP == OP_RHS ? WS_ELEMS8 : WS_ELEMS8_J) : (n == 32 ? WS_ELEMS32 : MmaTile<N>::ELEMS);
   static constexpr int WE = ELEMS / CW;                          // elements per consumer warp
   static constexpr int WMT = WE / 8;                             // m-tiles per warp
   static constexpr int NT = n / 8, KC = n / 4;
@@ -1042,6 +1051,65 @@ __device__ __forceinline__ void mtile_compute(const Consts<N>& C, const Geo& G, 
       if (OP == OP_JACT) wi = aw[kcp];   // already zm = mask(z M^-1)
       r[nt][h] = combine_rows<N, OP>(h ? k1 : k0, h ? p1 : p0, h ? q1 : q0, ui, wi, mnu);
     }
+  }
+}
+
+// Q m-tiles of one warp at once (elements base0/eg0 + 8q): the loops over the output
+// n-tiles and k-chunks are outermost, so each B fragment -- read from shared memory when
+// the n x n matrices do not fit the register file (n = 32) -- feeds Q DMMAs instead of one.
+template <int N, int OP, bool EDGE, int Q, class BGet>
+__device__ __forceinline__ void mtile_compute_multi(const Consts<N>& C, const Geo& G, const double* su,
+                                                    const double* sw, int base0, int64_t eg0,
+                                                    const double* minv_a, double mnu, int kq, BGet bget,
+                                                    ws_fin_t& fin_u, ws_fin_t& fin_w,
+                                                    double (&r)[Q][(N + 1) / 8][2]) {
+  constexpr int n = N + 1, NT = n / 8, KC = n / 4;
+  double au[Q][KC], aw[Q][(OP != OP_RHS) ? KC : 1], at[Q][(OP == OP_JACT) ? KC : 1];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const int64_t eg = eg0 + 8 * q;
+    const int base = base0 + 8 * q * N;
+    const bool eslow = EDGE && (eg == 0 || eg == G.E - 1);
+#pragma unroll
+    for (int kc = 0; kc < KC; ++kc) {
+      const int j = 4 * kc + kq;
+      au[q][kc] = su[base + j];
+      WS_FIN_ACC(fin_u, au[q][kc]);
+      if (OP != OP_RHS) {
+        aw[q][kc] = sw[base + j];
+        WS_FIN_ACC(fin_w, aw[q][kc]);
+        if (OP == OP_JACT) {
+          aw[q][kc] = eslow ? jt_scale<N>(C, aw[q][kc], j, eg, G) : __dmul_rn(aw[q][kc], minv_a[kc]);
+          at[q][kc] = __dmul_rn(au[q][kc], aw[q][kc]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    double k[Q][2], p[Q][2], qq[Q][2];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) k[q][0] = k[q][1] = p[q][0] = p[q][1] = qq[q][0] = qq[q][1] = 0.0;
+#pragma unroll
+    for (int kc = 0; kc < KC; ++kc) {
+      const double b0 = bget(0, nt, kc), b1 = bget(1, nt, kc);
+      const double b2 = (OP == OP_JACT) ? bget(2, nt, kc) : 0.0;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        dmma884(k[q][0], k[q][1], (OP == OP_RHS) ? au[q][kc] : aw[q][kc], b0);
+        dmma884(p[q][0], p[q][1], au[q][kc], b1);
+        if (OP == OP_JAC) dmma884(qq[q][0], qq[q][1], aw[q][kc], b1);
+        if (OP == OP_JACT) dmma884(qq[q][0], qq[q][1], at[q][kc], b2);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int kcp = 2 * nt + h;
+        const double wi = (OP == OP_RHS) ? 0.0 : aw[q][kcp];
+        r[q][nt][h] = combine_rows<N, OP>(k[q][h], p[q][h], qq[q][h], au[q][kcp], wi, mnu);
+      }
   }
 }
 
@@ -1256,6 +1324,11 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
       double carry = 0.0;
       auto body = [&](auto edge_tag) {
         constexpr bool EDGE = decltype(edge_tag)::value;
+        constexpr bool MULTI = W::B_IN_SMEM && (WMT > 1);
+        double rq[MULTI ? WMT : 1][NT][2];
+        if constexpr (MULTI)
+          mtile_compute_multi<N, OP, EDGE, WMT>(C, G, su, sw, (wel0 + rr + 1) * N, e0 + wel0 + rr, minv_a,
+                                                mnu, kq, bget, fin_u, fin_w, rq);
 #pragma unroll
         for (int q = 0; q < WMT; ++q) {
           const int le = 8 * q + rr;                // warp-local element of this lane
@@ -1263,8 +1336,16 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
           const int64_t eg = e0 + wel0 + le;
           const int base = (wel0 + le + 1) * N;
           double r[NT][2];
-          mtile_compute<N, OP, EDGE>(C, G, su, sw, base, eg, minv_a, minv_p, mnu, kq, bget,
-                                     fin_u, fin_w, r);
+          if constexpr (MULTI) {
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+              r[nt][0] = rq[q][nt][0];
+              r[nt][1] = rq[q][nt][1];
+            }
+          } else {
+            mtile_compute<N, OP, EDGE>(C, G, su, sw, base, eg, minv_a, minv_p, mnu, kq, bget,
+                                       fin_u, fin_w, r);
+          }
           // interior rows -> staging; rows 0 and N stay in registers
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt)
