@@ -1325,7 +1325,7 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
       auto body = [&](auto edge_tag) {
         constexpr bool EDGE = decltype(edge_tag)::value;
         constexpr bool MULTI = W::B_IN_SMEM && (WMT > 1);
-        double rq[MULTI ? WMT : 1][NT][2];
+        [[maybe_unused]] double rq[MULTI ? WMT : 1][NT][2];
         if constexpr (MULTI)
           mtile_compute_multi<N, OP, EDGE, WMT>(C, G, su, sw, (wel0 + rr + 1) * N, e0 + wel0 + rr, minv_a,
                                                 mnu, kq, bget, fin_u, fin_w, rq);
@@ -1334,7 +1334,7 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
           const int le = 8 * q + rr;                // warp-local element of this lane
           const bool live = le < wnel;
           const int64_t eg = e0 + wel0 + le;
-          const int base = (wel0 + le + 1) * N;
+          [[maybe_unused]] const int base = (wel0 + le + 1) * N;
           double r[NT][2];
           if constexpr (MULTI) {
 #pragma unroll

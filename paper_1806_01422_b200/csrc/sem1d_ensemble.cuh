@@ -18,6 +18,11 @@
 
 namespace sem1d {
 
+// periodic ring kernels (tile steps, ensembles): -nu M^-1 / M^-1 folded into the K / Dw
+// B fragments of the F apply (ring_rhs<PRE>); A/B 0.456 vs 0.480 ms per RK4 step
+#ifndef TILE_PRE
+#define TILE_PRE 1
+#endif
 #ifndef SEM1D_FIN_INT
 #define SEM1D_FIN_INT 1
 #endif
@@ -56,11 +61,14 @@ constexpr int kEnsAdjWarps = 8;
 // src: node values (ndof + 1 entries; entry ndof mirrors node 0 if periodic).
 // Output: kv[q][kc] = (M^-1-scaled) F at the nodes owned by this lane, for
 // m-tile q of this warp (node 4kc+kq of element 8*(warp + q*W) + rr ... see body).
-template <int N, int WMT_MAX, class BGet, bool WRAP = true>
+template <int N, int WMT_MAX, class BGet, bool WRAP = true, bool PRE = false>
 __device__ __forceinline__ void ring_rhs(const Consts<N>& C, const Geo& G, const double* src,
                                          double* xfer, BGet bget, const double* minv_a,
                                          double mnu, int warp, int lane,
                                          double (&kv)[WMT_MAX][(N + 1) / 4], unsigned& fin) {
+  // PRE: the B fragments carry -nu M^-1_i (K) and M^-1_i (Dw) on output row i (periodic
+  // rings: one M^-1 per local row, the interface rows share M^-1_0), so the row value is
+  // already the M^-1-scaled F: two FP64 ops per node fewer on the pipe the DMMAs use
   constexpr int KC = (N + 1) / 4, NT = (N + 1) / 8, W = EnsCfg<N>::W;
   const int kq = lane & 3, rr = lane >> 2;
   const int E = (int)G.E;
@@ -92,20 +100,25 @@ __device__ __forceinline__ void ring_rhs(const Consts<N>& C, const Geo& G, const
         dmma884(k0, k1, au[kc], bget(0, nt, kc));
         dmma884(p0, p1, au[kc], bget(1, nt, kc));
       }
-      r[nt][0] = __dsub_rn(__dmul_rn(k0, mnu), __dmul_rn(au[2 * nt], p0));
-      r[nt][1] = __dsub_rn(__dmul_rn(k1, mnu), __dmul_rn(au[2 * nt + 1], p1));
+      if (PRE) {
+        r[nt][0] = __dsub_rn(k0, __dmul_rn(au[2 * nt], p0));
+        r[nt][1] = __dsub_rn(k1, __dmul_rn(au[2 * nt + 1], p1));
+      } else {
+        r[nt][0] = __dsub_rn(__dmul_rn(k0, mnu), __dmul_rn(au[2 * nt], p0));
+        r[nt][1] = __dsub_rn(__dmul_rn(k1, mnu), __dmul_rn(au[2 * nt + 1], p1));
+      }
     }
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) kv[q][2 * nt + h] = __dmul_rn(r[nt][h], minv_a[2 * nt + h]);
+      for (int h = 0; h < 2; ++h) kv[q][2 * nt + h] = PRE ? r[nt][h] : __dmul_rn(r[nt][h], minv_a[2 * nt + h]);
     const double row0 = r[0][0];
     const double rowN = r[NT - 1][1];
     double left = __shfl_up_sync(0xffffffffu, rowN, 1);
     if (rr == 0) left = carry;
     carry = __shfl_sync(0xffffffffu, rowN, 31);
     if (q == 0) row0_first = row0;           // lane 0 patches it after the exchange
-    if (kq == 0) kv[q][0] = __dmul_rn(__dadd_rn(left, row0), minv_a[0]);
+    if (kq == 0) kv[q][0] = PRE ? __dadd_rn(left, row0) : __dmul_rn(__dadd_rn(left, row0), minv_a[0]);
   }
   if (lane == 31 && warp * WMT_MAX < mt_total) xfer[warp] = carry;   // row N of the warp's last element
   __syncthreads();
@@ -114,9 +127,20 @@ __device__ __forceinline__ void ring_rhs(const Consts<N>& C, const Geo& G, const
     // an open chain's first node stays incomplete -- it lies in the ghost margin)
     const int wl = (warp == 0) ? (WRAP ? (mt_total - 1) / WMT_MAX : -1) : warp - 1;
     const double v = wl >= 0 ? __dadd_rn(xfer[wl], row0_first) : row0_first;
-    kv[0][0] = __dmul_rn(v, minv_a[0]);
+    kv[0][0] = PRE ? v : __dmul_rn(v, minv_a[0]);
   }
   (void)W;
+}
+
+// B fragment of ring_rhs<PRE = true>: output row i of K scaled by -nu M^-1_i, of Dw by M^-1_i
+// (periodic rings: row i < N has M^-1 pattern entry i, rows 0 and N the interface entry 0)
+template <int N>
+__device__ __forceinline__ double bfrag_pre(const Consts<N>& C, int mat, int nt, int kc, int lane) {
+  const int c = 8 * nt + (lane >> 2);
+  const int i = 4 * (2 * (c >> 3) + (c & 1)) + ((c >> 1) & 3);      // permuted output row
+  const double mi = C.minv[(i == 0 || i == N) ? 0 : i];
+  const double b = bfrag_perm<N>(C, mat, nt, kc, lane);
+  return mat == 0 ? __dmul_rn(b, __dmul_rn(-C.nu, mi)) : __dmul_rn(b, mi);
 }
 
 // Forward sweep of one ring per CTA: periodic rings, E a multiple of 8 with
@@ -145,7 +169,7 @@ __global__ void __launch_bounds__(EnsCfg<N, kEnsFwdWarps>::THREADS, 1)
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int kc = 0; kc < KC; ++kc) breg[(mat * NT + nt) * KC + kc] = bfrag_perm<N>(C, mat, nt, kc, lane);
+      for (int kc = 0; kc < KC; ++kc) breg[(mat * NT + nt) * KC + kc] = (TILE_PRE ? bfrag_pre<N>(C, mat, nt, kc, lane) : bfrag_perm<N>(C, mat, nt, kc, lane));
   auto bget = [&](int mat, int nt, int kc) -> double { return breg[(mat * NT + nt) * KC + kc]; };
   double minv_a[KC];
 #pragma unroll
@@ -172,7 +196,8 @@ __global__ void __launch_bounds__(EnsCfg<N, kEnsFwdWarps>::THREADS, 1)
     const double dt = A.dts[step];
     for (int i = 0; i < A.tab.s; ++i) {
       const double* src = (i == 0) ? su : sU;
-      ring_rhs<N, WMT_MAX>(C, G, src, xfer, bget, minv_a, mnu, warp, lane, kv, fin);
+      ring_rhs<N, WMT_MAX, decltype(bget), true, TILE_PRE != 0>(C, G, src, xfer, bget, minv_a, mnu, warp, lane, kv,
+                                                               fin);
       // (ring_rhs ended with a barrier: every warp is done reading src)
 #pragma unroll
       for (int q = 0; q < WMT_MAX; ++q) {
@@ -325,6 +350,19 @@ __global__ void __launch_bounds__(EnsCfg<N, kEnsAdjWarps>::THREADS, 1)
 #pragma unroll
       for (int kc = 0; kc < KC; ++kc) breg[(mat * NT + nt) * KC + kc] = bfrag_perm<N>(C, mat, nt, kc, lane);
   auto bget = [&](int mat, int nt, int kc) -> double { return breg[(mat * NT + nt) * KC + kc]; };
+  // stage recompute (ring_rhs<PRE>): K / Dw fragments with -nu M^-1 / M^-1 folded in
+  double bpre[TILE_PRE ? 2 * NT * KC : 1];
+  if (TILE_PRE) {
+#pragma unroll
+    for (int mat = 0; mat < 2; ++mat)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int kc = 0; kc < KC; ++kc) bpre[(mat * NT + nt) * KC + kc] = bfrag_pre<N>(C, mat, nt, kc, lane);
+  }
+  auto bpget = [&](int mat, int nt, int kc) -> double {
+    return TILE_PRE ? bpre[(mat * NT + nt) * KC + kc] : breg[(mat * NT + nt) * KC + kc];
+  };
   double minv_a[KC];
 #pragma unroll
   for (int kc = 0; kc < KC; ++kc) {
@@ -346,7 +384,8 @@ __global__ void __launch_bounds__(EnsCfg<N, kEnsAdjWarps>::THREADS, 1)
     __syncthreads();
     // ---- stage states U_1..U_{S-1} (timeloop.rk3_stages, adjoint.py:56)
     for (int i = 0; i + 1 < S; ++i) {
-      ring_rhs<N, WMT_MAX>(C, G, Uarr(i), xfer, bget, minv_a, mnu, warp, lane, kv, fin);
+      ring_rhs<N, WMT_MAX, decltype(bpget), true, TILE_PRE != 0>(C, G, Uarr(i), xfer, bpget, minv_a, mnu, warp,
+                                                                lane, kv, fin);
       double* dst = Uarr(i + 1);
 #pragma unroll
       for (int q = 0; q < WMT_MAX; ++q) {
@@ -530,7 +569,7 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-      for (int kc = 0; kc < KC; ++kc) breg[(mat * NT + nt) * KC + kc] = bfrag_perm<N>(C, mat, nt, kc, lane);
+      for (int kc = 0; kc < KC; ++kc) breg[(mat * NT + nt) * KC + kc] = (TILE_PRE ? bfrag_pre<N>(C, mat, nt, kc, lane) : bfrag_perm<N>(C, mat, nt, kc, lane));
   auto bget = [&](int mat, int nt, int kc) -> double { return breg[(mat * NT + nt) * KC + kc]; };
   double minv_a[KC];
 #pragma unroll
@@ -578,7 +617,8 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
     if (tid == 0) sU[LEN - 1] = su[LEN - 1];   // the chain's last node is never owned
     for (int st = 0; st < A.tab.s; ++st) {
       const double* src = (st == 0) ? su : sU;
-      ring_rhs<N, WMT, decltype(bget), false>(C, Gt, src, xfer, bget, minv_a, mnu, warp, lane, kv, fin);
+      ring_rhs<N, WMT, decltype(bget), false, TILE_PRE != 0>(C, Gt, src, xfer, bget, minv_a, mnu, warp, lane, kv,
+                                                            fin);
       const double tb = A.tab.b[st];
       const bool last = (st + 1 == A.tab.s);
       const bool one = !last && A.tab.nterm[st + 1] == 1;
@@ -658,6 +698,19 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N>())
 #pragma unroll
       for (int kc = 0; kc < KC; ++kc) breg[(mat * NT + nt) * KC + kc] = bfrag_perm<N>(C, mat, nt, kc, lane);
   auto bget = [&](int mat, int nt, int kc) -> double { return breg[(mat * NT + nt) * KC + kc]; };
+  // stage recompute (ring_rhs<PRE>): K / Dw fragments with -nu M^-1 / M^-1 folded in
+  double bpre[TILE_PRE ? 2 * NT * KC : 1];
+  if (TILE_PRE) {
+#pragma unroll
+    for (int mat = 0; mat < 2; ++mat)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int kc = 0; kc < KC; ++kc) bpre[(mat * NT + nt) * KC + kc] = bfrag_pre<N>(C, mat, nt, kc, lane);
+  }
+  auto bpget = [&](int mat, int nt, int kc) -> double {
+    return TILE_PRE ? bpre[(mat * NT + nt) * KC + kc] : breg[(mat * NT + nt) * KC + kc];
+  };
   double minv_a[KC];
 #pragma unroll
   for (int kc = 0; kc < KC; ++kc) {
@@ -704,7 +757,8 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N>())
     if (tid == 0)
       for (int i = 1; i < S; ++i) Uarr(i)[LEN - 1] = su[LEN - 1];   // never-owned last node
     for (int i = 0; i + 1 < S; ++i) {
-      ring_rhs<N, WMT, decltype(bget), false>(C, Gt, Uarr(i), xfer, bget, minv_a, mnu, warp, lane, kv, fin);
+      ring_rhs<N, WMT, decltype(bpget), false, TILE_PRE != 0>(C, Gt, Uarr(i), xfer, bpget, minv_a, mnu, warp, lane,
+                                                              kv, fin);
       double* dst = Uarr(i + 1);
 #pragma unroll
       for (int q = 0; q < WMT; ++q) {
