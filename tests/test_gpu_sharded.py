@@ -89,3 +89,25 @@ def test_sharded_fused_steps_match_global(cuda, scheme):
         sl = slice(op.part.g_lo, op.part.g_lo + op.part.n_own)
         assert rel_err(op.public(un).cpu().numpy(), un_g[sl].cpu().numpy()) <= 1e-14
         assert rel_err(op.public(ln).cpu().numpy(), ln_g[sl].cpu().numpy()) <= 1e-13
+
+
+def test_bench_two_ranks_json_line(cuda, tmp_path):
+    """bench.py under torchrun with 2 ranks (the driver's N > 1 launch), here on one GPU with
+    --same-device and a gloo exchange (no kernel waits on another rank): one JSON line from
+    rank 0 with the whole-job value, n_gpus = 2 and the sharded parallelism."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(root, "bench.py"),
+           "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-sweep",
+           "--same-device", "--dist-backend", "gloo"]
+    out = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
+    assert "sharded" in d["config"]["parallelism"]
