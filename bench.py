@@ -30,7 +30,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 BYTES_PER_DOF = {"F": 16, "J": 24, "JT": 24}
-METRIC = "fp64 DOF/s for F(u), J*v and J^T*w applies (summed), BASELINE config 2"
+# BASELINE.json "metric", verbatim.  `value` is the config-2 step (F(u), J(u)v, J(u)^T w once
+# each, BASELINE configs[1]) as 3 * DOF / step time; per_op reports F and J^T alone, roofline
+# the % of HBM bandwidth, ratios the adjoint/forward cost ratios.
+METRIC = "fp64 DOF/s for F(u) and J^T\u00b7w apply; % HBM roofline; adjoint/forward cost ratio"
+VALUE_DEF = "3 * DOF / time of one config-2 step (F(u), J(u)v and J(u)^T w once each)"
 
 
 def flop_per_dof(N, op):
@@ -109,7 +113,7 @@ def run_reference_arm(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / len(timed), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded U(-1,1), N(0,1) per node)",
-        "config": {"workload": "BASELINE config 2 (1D Burgers, N=7, nu=0.01, periodic [-1,1])",
+        "config": {"workload": "BASELINE config 2 (1D Burgers, N=7, nu=0.01, periodic [-1,1])", "value": VALUE_DEF,
                    "E": 1 << 22, "N": 7, "sample_E": E_sample, "sample_dof": ndof},
         "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": cores, "kind": "port",
                          "sample": f"F+J+J^T on E=2^18 of config 2 (same h, N, nu), "
@@ -384,7 +388,7 @@ def run_gpu_arm(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded u~U(-1,1), v,w~N(0,1) per node)",
         "config": {"workload": "BASELINE config 2: 1D Burgers, E=2^22, N=7, nu=0.01, periodic [-1,1]",
-                   "E": c["E"], "N": c["N"], "dof": ndof,
+                   "value": VALUE_DEF, "E": c["E"], "N": c["N"], "dof": ndof,
                    "per_rank_problem": "2^22 elements" + ("" if world == 1 else
                                        " of one element-sharded ring (ghost exchange per input)"),
                    "l2": "inputs 235 MB/field > 126 MB L2, no flush",
