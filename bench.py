@@ -227,33 +227,43 @@ def timed_ops(op, ud, vd, wd, outs, steps, stream):
 
 
 def sweep_ratio(op, torch, steps=8):
-    """Forward RK4 sweep vs discrete-adjoint sweep on the config-2 field (store-all).
-    h = 4.8e-7 on config 2 makes the explicit limit ~5e-14 (rho*h^2 ~ 13 at nu=0.01),
-    so dt = 1e-14: this measures cost, not physics."""
+    """Forward RK4 sweep vs discrete-adjoint sweep on the config-2 field (store-all), with the
+    stage states held in HBM (what evaluate() does when they fit) and with the reference's
+    stage recompute.  h = 4.8e-7 on config 2 makes the explicit limit ~5e-14 (rho*h^2 ~ 13
+    at nu=0.01), so dt = 1e-14: this measures cost, not physics."""
     from paper_1806_01422_b200 import adjoint, checkpoint, timeloop
     dt = 1e-14
     ts = timeloop.TsConfig(scheme="rk4", t0=0.0, t_end=steps * dt, dt=dt)
     u0 = torch.sin(torch.linspace(0, 6.283185307179586, op.ndof, dtype=torch.float64,
                                   device=op.device))
-    fw = timeloop.integrate(op, u0, ts)  # warm-up of both sweeps (allocations, attributes)
-    _, lam = adjoint.terminal_condition(op.grid, fw.u_final, 0.5 * u0, op=op)
-    adjoint.sweep(op, ts, fw, checkpoint.plan_store_all(fw.n_steps), lam)
-    del fw, lam
-    torch.cuda.synchronize()
-    a, b, c, d = (torch.cuda.Event(enable_timing=True) for _ in range(4))
-    a.record()
-    fwd = timeloop.integrate(op, u0, ts)
-    b.record()
-    sched = checkpoint.plan_store_all(fwd.n_steps)
-    j, lam = adjoint.terminal_condition(op.grid, fwd.u_final, 0.5 * u0, op=op)
-    c.record()
-    adjoint.sweep(op, ts, fwd, sched, lam)
-    d.record()
-    torch.cuda.synchronize()
-    f_ms, a_ms = a.elapsed_time(b), c.elapsed_time(d)
+
+    def one(keep):
+        fw = timeloop.integrate(op, u0, ts, keep_stages=keep)   # warm-up (allocations)
+        _, lam = adjoint.terminal_condition(op.grid, fw.u_final, 0.5 * u0, op=op)
+        adjoint.sweep(op, ts, fw, checkpoint.plan_store_all(fw.n_steps), lam)
+        del fw, lam
+        torch.cuda.synchronize()
+        a, b, c, d = (torch.cuda.Event(enable_timing=True) for _ in range(4))
+        a.record()
+        fwd = timeloop.integrate(op, u0, ts, keep_stages=keep)
+        b.record()
+        sched = checkpoint.plan_store_all(fwd.n_steps)
+        _, lam = adjoint.terminal_condition(op.grid, fwd.u_final, 0.5 * u0, op=op)
+        c.record()
+        adjoint.sweep(op, ts, fwd, sched, lam)
+        d.record()
+        torch.cuda.synchronize()
+        del fwd, lam
+        return a.elapsed_time(b), c.elapsed_time(d)
+
+    f_ms, a_ms = one(True)
+    fr_ms, ar_ms = one(False)
     return {"scheme": "rk4", "steps": steps, "forward_ms": f_ms, "adjoint_ms": a_ms,
             "adjoint_over_forward": a_ms / f_ms, "ms_per_forward_step": f_ms / steps,
             "ms_per_adjoint_step": a_ms / steps,
+            "stage_states": "held in HBM by the forward step (no adjoint recompute)",
+            "recompute": {"forward_ms": fr_ms, "adjoint_ms": ar_ms, "adjoint_over_forward": ar_ms / fr_ms,
+                          "ms_per_forward_step": fr_ms / steps, "ms_per_adjoint_step": ar_ms / steps},
             "kernels": "one temporally blocked launch per RK4 step and per adjoint step"
                        if getattr(op, "step_fused_supported", lambda: False)() else "per-stage"}
 

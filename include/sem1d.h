@@ -153,6 +153,17 @@ int sem1d_ens_adjoint(const sem1d_plan* plan, const double* traj, const double* 
  * sem1d_rk_stage / sem1d_adj_stage.  sem1d_step_supported(plan) tells whether
  * the plan qualifies. */
 int sem1d_step_supported(const sem1d_plan* plan);
+/* The same steps with the forward trajectory's stage states held in HBM (north_star item 4):
+ * sem1d_rk_step_stages also writes U_1..U_{s-1} of the step to stages[0..s-2] (ndof each);
+ * sem1d_adj_step_stages reads them instead of recomputing (s ghost elements per tile
+ * instead of 2s-1, no F applies), giving the adjoint of timeloop.py:111-130 /
+ * adjoint.py:54-61 with s J^T stages only. */
+int sem1d_step_stages_supported(const sem1d_plan* plan);   /* the pair below qualifies */
+int sem1d_rk_step_stages(const sem1d_plan* plan, const double* u, double* u_new,
+                         double* const* stages, double dt, int scheme, int* flag, void* stream);
+int sem1d_adj_step_stages(const sem1d_plan* plan, const double* u, const double* const* stages,
+                          const double* lam, double* lam_out, double dt, int scheme, int* flag,
+                          void* stream);
 int sem1d_rk_step(const sem1d_plan* plan, const double* u, double* u_new, double dt, int scheme,
                   int* flag, void* stream);
 int sem1d_adj_step(const sem1d_plan* plan, const double* u, const double* lam, double* lam_out,

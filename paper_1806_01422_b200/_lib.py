@@ -66,6 +66,11 @@ SIGNATURES = {
     "sem1d_ens_adjoint": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int,
                                   c_void_p, c_void_p]),
     "sem1d_step_supported": (c_int, [c_void_p]),
+    "sem1d_step_stages_supported": (c_int, [c_void_p]),
+    "sem1d_rk_step_stages": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int, c_void_p,
+                                     c_void_p]),
+    "sem1d_adj_step_stages": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int,
+                                      c_void_p, c_void_p]),
     "sem1d_rk_step": (c_int, [c_void_p, c_void_p, c_void_p, c_double, c_int, c_void_p, c_void_p]),
     "sem1d_adj_step": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int, c_void_p,
                                c_void_p]),

@@ -76,13 +76,18 @@ class AdjointEngine:
             self._L = {i: self.op.empty() for i in range(1, self.s)}
         return self._L
 
-    def step(self, u_n, lam, dt, lam_out):
-        """lam_out = transpose of the step map at u_n applied to lam (no host sync)."""
+    def step(self, u_n, lam, dt, lam_out, stages=None):
+        """lam_out = transpose of the step map at u_n applied to lam (no host sync).
+        ``stages``: the step's stage states U_1..U_{s-1} stored by the forward run (fused
+        path): no recompute."""
         op, s = self.op, self.s
         fused = getattr(op, "step_fused_supported", None)
         if fused is not None and fused():
-            op.launch_adj_step(u_n, lam, lam_out, dt, self.scheme)
-            op.counters["rhs"] += s - 1
+            if stages is not None and s > 1:
+                op.launch_adj_step_stages(u_n, stages, lam, lam_out, dt, self.scheme)
+            else:
+                op.launch_adj_step(u_n, lam, lam_out, dt, self.scheme)
+                op.counters["rhs"] += s - 1
             op.counters["jact"] += s
             return
         Us = self.fwd.stages(u_n, dt, self.U) if s > 1 else [u_n]
@@ -161,6 +166,7 @@ def sweep(op, cfg, fwd, schedule, lam_terminal, check_every=1):
     fwd_engine = None if cn else engine_for(op, cfg.scheme)
     adj = None if cn else adjoint_engine_for(op, cfg.scheme)
     fused = getattr(fwd, "fused_steps", True)   # replay with the forward run's kernel path
+    stage_snaps = getattr(fwd, "stage_snapshots", None) or {}   # stage states kept in HBM
 
     slots, preloaded = {}, True
     for step, slot in schedule.forward_stores.items():
@@ -219,7 +225,7 @@ def sweep(op, cfg, fwd, schedule, lam_terminal, check_every=1):
                 u_np1 = succ[1] if succ[0] == n + 1 else fwd.u_final
                 adjoint_step_cn(op, current[1], u_np1, lam, fwd.ts[n], dts[n], cfg, stats, out=spare)
             else:
-                adj.step(current[1], lam, dts[n], spare)
+                adj.step(current[1], lam, dts[n], spare, stages=stage_snaps.get(n))
             lam, spare = spare, lam
             since_check += 1
             if since_check >= check_every:

@@ -604,6 +604,57 @@ int sem1d_adj_step(const sem1d_plan* plan, const double* u, const double* lam, d
   return SEM1D_OK;
 }
 
+int sem1d_step_stages_supported(const sem1d_plan* plan) {
+  if (!sem1d_step_supported(plan)) return 0;
+  switch (plan->N) {
+    case 7: return stages_fit<7>() ? 1 : 0;
+    case 15: return stages_fit<15>() ? 1 : 0;
+    case 23: return stages_fit<23>() ? 1 : 0;
+    case 31: return stages_fit<31>() ? 1 : 0;
+    default: return 0;
+  }
+}
+
+int sem1d_rk_step_stages(const sem1d_plan* plan, const double* u, double* u_new, double* const* stages,
+                         double dt, int scheme, int* flag, void* stream) {
+  if (!valid_burgers(plan) || !u || !u_new || !flag || !stages || u == u_new)
+    return fail(SEM1D_EINVAL, "sem1d_rk_step_stages: bad argument");
+  TileStepArgs a;
+  std::memset(&a, 0, sizeof(a));
+  if (!make_tableau(scheme, a.tab)) return fail(SEM1D_EINVAL, "sem1d_rk_step_stages: unknown scheme");
+  if (a.tab.s < 2) return fail(SEM1D_EINVAL, "sem1d_rk_step_stages: a one-stage scheme has no stage states");
+  for (int i = 0; i + 1 < a.tab.s; ++i) {
+    if (!stages[i]) return fail(SEM1D_EINVAL, "sem1d_rk_step_stages: NULL stage buffer");
+    a.stages[i] = stages[i];
+  }
+  a.u = u; a.out = u_new; a.flag = flag; a.dt = dt;
+  cudaError_t e = dispatch_tile(plan, 0, a, static_cast<cudaStream_t>(stream));
+  if (e == cudaErrorNotSupported)
+    return fail(SEM1D_EINVAL, "sem1d_rk_step_stages: needs a periodic batch-1 ring, N+1 in {8,16,24,32}");
+  if (e != cudaSuccess) return cuda_fail(e, "sem1d_rk_step_stages");
+  return SEM1D_OK;
+}
+
+int sem1d_adj_step_stages(const sem1d_plan* plan, const double* u, const double* const* stages,
+                          const double* lam, double* lam_out, double dt, int scheme, int* flag, void* stream) {
+  if (!valid_burgers(plan) || !u || !lam || !lam_out || !flag || !stages || lam == lam_out)
+    return fail(SEM1D_EINVAL, "sem1d_adj_step_stages: bad argument (lam_out must not alias lam)");
+  TileStepArgs a;
+  std::memset(&a, 0, sizeof(a));
+  if (!make_tableau(scheme, a.tab)) return fail(SEM1D_EINVAL, "sem1d_adj_step_stages: unknown scheme");
+  if (a.tab.s < 2) return fail(SEM1D_EINVAL, "sem1d_adj_step_stages: a one-stage scheme has no stage states");
+  for (int i = 0; i + 1 < a.tab.s; ++i) {
+    if (!stages[i]) return fail(SEM1D_EINVAL, "sem1d_adj_step_stages: NULL stage buffer");
+    a.stin[i] = stages[i];
+  }
+  a.u = u; a.lam = lam; a.out = lam_out; a.flag = flag; a.dt = dt;
+  cudaError_t e = dispatch_tile(plan, 1, a, static_cast<cudaStream_t>(stream));
+  if (e == cudaErrorNotSupported)
+    return fail(SEM1D_EINVAL, "sem1d_adj_step_stages: needs a periodic batch-1 ring, N+1 in {8,16,24,32}");
+  if (e != cudaSuccess) return cuda_fail(e, "sem1d_adj_step_stages");
+  return SEM1D_OK;
+}
+
 int64_t sem1d_terminal_work_size(const sem1d_plan* plan) {
   if (!valid_plan(plan)) return -1;
   const int64_t per = RED_TPB * RED_ITEMS;

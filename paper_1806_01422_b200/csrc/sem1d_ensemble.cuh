@@ -56,6 +56,9 @@ struct EnsCfg {
 };
 constexpr int kEnsFwdWarps = 16;
 constexpr int kEnsAdjWarps = 8;
+// n = 32: 8 warps (255 registers per thread; at 16 warps the 128-register cap spilled)
+template <int N>
+constexpr int ens_fwd_warps() { return (N + 1) == 32 ? 8 : kEnsFwdWarps; }
 
 // One operator application over the whole ring held in shared memory.
 // src: node values (ndof + 1 entries; entry ndof mirrors node 0 if periodic).
@@ -146,10 +149,10 @@ __device__ __forceinline__ double bfrag_pre(const Consts<N>& C, int mat, int nt,
 // Forward sweep of one ring per CTA: periodic rings, E a multiple of 8 with
 // E/8 <= 8 * WMT_MAX.  Trajectory state n+1 is written after step n.
 template <int N, int WMT_MAX>
-__global__ void __launch_bounds__(EnsCfg<N, kEnsFwdWarps>::THREADS, 1)
+__global__ void __launch_bounds__(EnsCfg<N, ens_fwd_warps<N>()>::THREADS, 1)
     ens_forward_kernel(const __grid_constant__ Consts<N> C, const Geo G, const EnsArgs A) {
   constexpr int n = N + 1, KC = EnsCfg<N>::KC, NT = EnsCfg<N>::NT;
-  constexpr int THREADS = EnsCfg<N, kEnsFwdWarps>::THREADS;
+  constexpr int THREADS = EnsCfg<N, ens_fwd_warps<N>()>::THREADS;
   extern __shared__ __align__(16) double smem[];
   const int ndof = (int)G.ndof;
   const int pad = (ndof + 2 + 1) & ~1;        // ndof + mirror node, 16-byte multiple
@@ -491,6 +494,15 @@ constexpr size_t ens_adj_smem_bytes(int ndof) {
 #ifndef TILE_WMTA8
 #define TILE_WMTA8 4
 #endif
+#ifndef TILE_WA16
+#define TILE_WA16 8
+#endif
+#ifndef TILE_WL8
+#define TILE_WL8 4
+#endif
+#ifndef TILE_WMTL8
+#define TILE_WMTL8 2
+#endif
 #ifndef TILE_ADJ_MINB8
 #define TILE_ADJ_MINB8 3
 #endif
@@ -504,6 +516,8 @@ struct TileStepArgs {
   int H;                  // ghost elements per side
   int ntiles;             // ceil(E / (TE - 2H))
   Tableau tab;
+  double* stages[3];      // forward: also write the stage states U_1..U_{s-1} (NULL: don't)
+  const double* stin[3];  // adjoint: read U_1..U_{s-1} instead of recomputing them (NULL: recompute)
 };
 
 // Tile loader shared by the step kernels: interior tiles arrive by one bulk
@@ -535,6 +549,24 @@ __device__ __forceinline__ void tile_issue(const TileLoad& L, int LEN, const dou
   mbar_expect_tx(bar, nsrc * bytes);
   bulk_g2s(dst, src + a0, bytes, bar);
   if (nsrc == 2) bulk_g2s(dst2, src2 + a0, bytes, bar);
+}
+
+// first 16-byte aligned double after the two mbarriers (the n = 32 B-fragment table)
+template <int N>
+__device__ __forceinline__ double* bar_smem_end(double* p) {
+  return reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
+}
+
+// n slabs of the same tile range under ONE arrive.expect_tx (a second arm could let the
+// phase complete before all copies are registered)
+__device__ __forceinline__ void tile_issue_n(const TileLoad& L, int LEN, const double* const (&src)[5],
+                                             double* const (&dst)[5], uint64_t* bar, int nsrc) {
+  const int64_t a0 = L.g0 - L.sh;
+  const uint32_t bytes = (uint32_t)((((int64_t)(LEN + L.sh)) * 8 + 15) & ~15LL);
+  mbar_expect_tx(bar, nsrc * bytes);
+#pragma unroll
+  for (int i = 0; i < 5; ++i)            // compile-time bound: the pointer arrays stay in registers
+    if (i < nsrc) bulk_g2s(dst[i], src[i] + a0, bytes, bar);
 }
 
 // resident CTAs per SM (A/B: a 64-register cap for two CTAs made the n = 8 step 2x slower)
@@ -616,6 +648,7 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
     const double* su = sb + L.sh;
     if (tid == 0) sU[LEN - 1] = su[LEN - 1];   // the chain's last node is never owned
     for (int st = 0; st < A.tab.s; ++st) {
+      if (A.stages[0] && tid == 0) bulk_wait_read<0>();   // the previous stage's store has read sU
       const double* src = (st == 0) ? su : sU;
       ring_rhs<N, WMT, decltype(bget), false, TILE_PRE != 0>(C, Gt, src, xfer, bget, minv_a, mnu, warp, lane, kv,
                                                             fin);
@@ -653,13 +686,29 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
           }
         }
       }
+      if (A.stages[0]) fence_proxy_async_smem();   // sU is read by the bulk store below
       __syncthreads();
+      if (A.stages[0] && st + 1 < A.tab.s) {  // stage state U_{st+1} of the owned elements
+        const int64_t e_o = (int64_t)t * T;
+        const int no = (int)min((int64_t)T, G.E - e_o) * N;
+        double* dst = A.stages[st] + e_o * N;
+        const double* src = sU + A.H * N;
+        if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0 && (no & 1) == 0) {
+          if (tid == 0) {                     // one async bulk store; read-drained before sU is rewritten
+            bulk_s2g(dst, src, (uint32_t)(no * 8));
+            bulk_commit();
+          }
+        } else {
+          for (int k = tid; k < no; k += 32 * W) dst[k] = src[k];
+        }
+      }
     }
     const int64_t e_out0 = (int64_t)t * T;
     const int nout_el = (int)min((int64_t)T, G.E - e_out0);
     for (int k = tid; k < nout_el * N; k += 32 * W) A.out[e_out0 * N + k] = sU[A.H * N + k];
     __syncthreads();
   }
+  if (A.stages[0] && tid == 0) bulk_wait_all();
   if (fin || bad)
     atomicOr(A.flag, (fin ? SEM1D_FLAG_STATE_NONFINITE : 0) | (bad ? SEM1D_FLAG_STEP_NONFINITE : 0));
 }
@@ -674,8 +723,11 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N>())
   extern __shared__ __align__(16) double smem[];
   double* sbu = smem;                         // [2][PAD] u_n loads (= U_0)
   double* sbl = sbu + 2 * PAD;                // [2][PAD] lam loads (accumulated in place)
-  double* sUs = sbl + 2 * PAD;                // U_1 .. U_3
-  double* sk = sUs + 3 * PAD;
+  // stage states: recomputed into [3][PAD], or (stored by the forward step) prefetched with
+  // the tile into [2][3][PAD]
+  const bool LD = A.stin[0] != nullptr;
+  double* sUs = sbl + 2 * PAD;
+  double* sk = sUs + (LD ? 6 : 3) * PAD;
   double* sz = sk + PAD;
   double* xfer = sz + PAD;
   uint64_t* bar = reinterpret_cast<uint64_t*>(xfer + 32);
@@ -683,33 +735,57 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N>())
   const int kq = lane & 3, rr = lane >> 2;
   const int T = TE - 2 * A.H;
   const int S = A.tab.s;
+  auto issue = [&](const TileLoad& Lx, int buf) {
+    const double* srcs[5] = {A.u, A.lam, A.stin[0], A.stin[1], A.stin[2]};
+    double* dsts[5] = {sbu + buf * PAD, sbl + buf * PAD, sUs + (buf * 3 + 0) * PAD, sUs + (buf * 3 + 1) * PAD,
+                       sUs + (buf * 3 + 2) * PAD};
+    tile_issue_n(Lx, LEN, srcs, dsts, &bar[buf], LD ? S + 1 : 2);
+  };
   const int64_t ndof = G.ndof;
   const double mnu = -C.nu;
   Geo Gt = G;
   Gt.E = TE;
   double* su = sbu;
   double* slam = sbl;
-  auto Uarr = [&](int i) -> double* { return i == 0 ? su : sUs + (i - 1) * PAD; };
-  double breg[3 * NT * KC];
+  double* sUb = sUs;                          // this tile's stage-state slabs
+  auto Uarr = [&](int i) -> double* { return i == 0 ? su : sUb + (i - 1) * PAD; };
+  // B fragments (K, Dw, Dw^T and, for the stage recompute, K / Dw with -nu M^-1 / M^-1 folded
+  // in): registers up to n = 24; at n = 32 (160 values per lane) shared memory, laid out
+  // per lane -- in registers the compiler re-reads them from kernel-parameter space with
+  // lane-divergent indices (19x slower)
+  constexpr bool BSM = (N + 1) == 32;
+  double breg[BSM ? 1 : 3 * NT * KC];
+  double bpre[(BSM || !TILE_PRE) ? 1 : 2 * NT * KC];
+  double* sB = bar_smem_end<N>(reinterpret_cast<double*>(bar + 2));
+  if constexpr (BSM) {
+    for (int q = tid; q < 5 * NT * KC * 32; q += blockDim.x) {
+      const int l = q & 31, f = q >> 5, kc = f % KC, nt = (f / KC) % NT, mat = f / (KC * NT);
+      sB[q] = mat < 3 ? bfrag_perm<N>(C, mat, nt, kc, l)
+                      : (TILE_PRE ? bfrag_pre<N>(C, mat - 3, nt, kc, l) : bfrag_perm<N>(C, mat - 3, nt, kc, l));
+    }
+  } else {
 #pragma unroll
-  for (int mat = 0; mat < 3; ++mat)
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int kc = 0; kc < KC; ++kc) breg[(mat * NT + nt) * KC + kc] = bfrag_perm<N>(C, mat, nt, kc, lane);
-  auto bget = [&](int mat, int nt, int kc) -> double { return breg[(mat * NT + nt) * KC + kc]; };
-  // stage recompute (ring_rhs<PRE>): K / Dw fragments with -nu M^-1 / M^-1 folded in
-  double bpre[TILE_PRE ? 2 * NT * KC : 1];
-  if (TILE_PRE) {
-#pragma unroll
-    for (int mat = 0; mat < 2; ++mat)
+    for (int mat = 0; mat < 3; ++mat)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int kc = 0; kc < KC; ++kc) bpre[(mat * NT + nt) * KC + kc] = bfrag_pre<N>(C, mat, nt, kc, lane);
+        for (int kc = 0; kc < KC; ++kc) breg[(mat * NT + nt) * KC + kc] = bfrag_perm<N>(C, mat, nt, kc, lane);
+    if (TILE_PRE) {
+#pragma unroll
+      for (int mat = 0; mat < 2; ++mat)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int kc = 0; kc < KC; ++kc) bpre[(mat * NT + nt) * KC + kc] = bfrag_pre<N>(C, mat, nt, kc, lane);
+    }
   }
+  auto bget = [&](int mat, int nt, int kc) -> double {
+    if constexpr (BSM) return sB[((mat * NT + nt) * KC + kc) * 32 + lane];
+    else return breg[(mat * NT + nt) * KC + kc];
+  };
   auto bpget = [&](int mat, int nt, int kc) -> double {
-    return TILE_PRE ? bpre[(mat * NT + nt) * KC + kc] : breg[(mat * NT + nt) * KC + kc];
+    if constexpr (BSM) return sB[(((mat + 3) * NT + nt) * KC + kc) * 32 + lane];
+    else return TILE_PRE ? bpre[(mat * NT + nt) * KC + kc] : breg[(mat * NT + nt) * KC + kc];
   };
   double minv_a[KC];
 #pragma unroll
@@ -725,7 +801,7 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N>())
   __syncthreads();
   if (tid == 0 && blockIdx.x < A.ntiles) {
     const TileLoad L = tile_load_plan(blockIdx.x, T, A.H, N, LEN, ndof);
-    if (L.bulk) tile_issue(L, LEN, A.u, sbu, &bar[0], 2, A.lam, sbl);
+    if (L.bulk) issue(L, 0);
   }
   unsigned fin = 0u;
   uint32_t phase = 0;
@@ -744,19 +820,21 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N>())
         while (g >= ndof) g -= ndof;
         sbu[bsel * PAD + k] = __ldg(A.u + g);
         sbl[bsel * PAD + k] = __ldg(A.lam + g);
+        if (LD)
+          for (int i = 1; i < S; ++i) sUs[(bsel * 3 + i - 1) * PAD + k] = __ldg(A.stin[i - 1] + g);
       }
       __syncthreads();
     }
     if (tid == 0 && t + (int)gridDim.x < A.ntiles) {
       const TileLoad Ln = tile_load_plan(t + gridDim.x, T, A.H, N, LEN, ndof);
-      if (Ln.bulk) tile_issue(Ln, LEN, A.u, sbu + (bsel ^ 1) * PAD, &bar[bsel ^ 1], 2, A.lam,
-                              sbl + (bsel ^ 1) * PAD);
+      if (Ln.bulk) issue(Ln, bsel ^ 1);
     }
     su = sbu + bsel * PAD + L.sh;
     slam = sbl + bsel * PAD + L.sh;
-    if (tid == 0)
+    sUb = LD ? sUs + bsel * 3 * PAD + L.sh : sUs;
+    if (tid == 0 && !LD)
       for (int i = 1; i < S; ++i) Uarr(i)[LEN - 1] = su[LEN - 1];   // never-owned last node
-    for (int i = 0; i + 1 < S; ++i) {
+    for (int i = 0; i + 1 < S && !LD; ++i) {
       ring_rhs<N, WMT, decltype(bpget), false, TILE_PRE != 0>(C, Gt, Uarr(i), xfer, bpget, minv_a, mnu, warp, lane,
                                                               kv, fin);
       double* dst = Uarr(i + 1);
@@ -836,15 +914,27 @@ struct TileCfg {
   // m-tiles, 3 CTAs per SM; 1.155 vs 1.190 ms at 16 x 2 x 1), 128 / 64 otherwise (nine
   // slabs must fit the shared memory of the resident CTAs)
   static constexpr int W = (N + 1) == 32 ? 8 : ((N + 1) == 8 ? TILE_WF8 : 16);
-  static constexpr int W_A = (N + 1) == 8 ? TILE_WA8 : ((N + 1) == 32 ? 8 : 16);  // adjoint warps
+  // adjoint warps: 8 x 2 m-tiles for N = 15/23 (at 16 warps the 128-register cap made the
+  // compiler re-read the B fragments from kernel-parameter space with lane-divergent
+  // indices inside the DMMA loops: 6.9x the forward step)
+  static constexpr int W_A = (N + 1) == 8 ? TILE_WA8 : ((N + 1) == 32 ? 8 : TILE_WA16);
   static constexpr int WMT_F = (N + 1) == 8 ? TILE_WMT8 : 1;
-  static constexpr int WMT_A = (N + 1) == 8 ? TILE_WMTA8 : 1;
+  static constexpr int WMT_A = (N + 1) == 8 ? TILE_WMTA8 : ((N + 1) == 32 ? 1 : 128 / (8 * TILE_WA16));
+  // adjoint step reading stored stage states (fewer DMMAs, 12 slabs): its own warp shape
+  static constexpr int W_L = (N + 1) == 8 ? TILE_WL8 : W_A;
+  static constexpr int WMT_L = (N + 1) == 8 ? TILE_WMTL8 : WMT_A;
+  static constexpr int TE_L = 8 * W_L * WMT_L;
+  static constexpr int PAD_L = ((TE_L * N + 1 + 2) + 1) & ~1;
   static constexpr int TE_F = 8 * W * WMT_F;
   static constexpr int TE_A = 8 * W_A * WMT_A;
   static constexpr int PAD_F = ((TE_F * N + 1 + 2) + 1) & ~1;
   static constexpr int PAD_A = ((TE_A * N + 1 + 2) + 1) & ~1;
   static constexpr size_t fwd_smem = sizeof(double) * (4 * (size_t)PAD_F + 32) + 2 * sizeof(uint64_t);
-  static constexpr size_t adj_smem = sizeof(double) * (9 * (size_t)PAD_A + 32) + 2 * sizeof(uint64_t);
+  static constexpr size_t BFRAG = ((N + 1) == 32) ? sizeof(double) * 5 * ((N + 1) / 8) * ((N + 1) / 4) * 32 + 16 : 0;
+  static constexpr size_t adj_smem = sizeof(double) * (9 * (size_t)PAD_A + 32) + 2 * sizeof(uint64_t) + BFRAG;
+  // adjoint step reading the stored stage states: 12 slabs (u, lam, U_1..U_3 double-buffered,
+  // k, z) at the W_L x WMT_L shape
+  static constexpr size_t adj_smem_ld = sizeof(double) * (12 * (size_t)PAD_L + 32) + 2 * sizeof(uint64_t) + BFRAG;
   static constexpr int TE_MAX = TE_F > TE_A ? TE_F : TE_A;
 };
 

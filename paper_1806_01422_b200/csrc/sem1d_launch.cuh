@@ -184,6 +184,13 @@ cudaError_t launch_apply(const PlanView& p, int kind, const Args& a, cudaStream_
 template <int N>
 constexpr size_t consts_size() { return sizeof(Consts<N>); }
 
+// the stored-stage adjoint step fits shared memory for this degree
+template <int N>
+constexpr bool stages_fit() {
+  if constexpr ((N + 1) % 8 != 0) return false;
+  else return TileCfg<N>::adj_smem_ld <= 227 * 1024;
+}
+
 // Small rings (E*(N+1) <= 1024): one thread per (element, row), any degree and
 // boundary kind, whole sweep per launch.
 template <int N>
@@ -238,7 +245,7 @@ cudaError_t launch_ens_adjoint(const PlanView& p, const EnsAdjArgs& a, cudaStrea
 template <int N>
 cudaError_t launch_ens_forward(const PlanView& p, const EnsArgs& a, cudaStream_t s) {
   if constexpr ((N + 1) % 8 == 0) {
-    constexpr int W = kEnsFwdWarps;
+    constexpr int W = ens_fwd_warps<N>();
     constexpr int WMT = 32 / W;
     const size_t smem = ens_smem_bytes<N>((int)p.geo.ndof);
     if (p.geo.periodic && p.geo.E % 8 == 0 && p.geo.E / 8 <= W * WMT && smem <= 220 * 1024 &&
@@ -263,10 +270,12 @@ cudaError_t launch_tile_step(const PlanView& p, int kind, TileStepArgs a, cudaSt
   } else {
     using TC = TileCfg<N>;
     if (!p.geo.periodic || p.batch != 1 || p.geo.E < 2 * TC::TE_MAX) return cudaErrorNotSupported;
-    a.H = (kind == 0) ? a.tab.s : 2 * a.tab.s - 1;
-    const int T = (kind == 0 ? TC::TE_F : TC::TE_A) - 2 * a.H;
+    // ghost elements: s per side for a step (one per stage), 2s-1 for an adjoint step that
+    // recomputes its stages, s when the forward stored them
+    a.H = (kind == 0 || a.stin[0]) ? a.tab.s : 2 * a.tab.s - 1;
+    const int T = (kind == 0 ? TC::TE_F : (a.stin[0] ? TC::TE_L : TC::TE_A)) - 2 * a.H;
     a.ntiles = (int)((p.geo.E + T - 1) / T);
-    const size_t smem = kind == 0 ? TC::fwd_smem : TC::adj_smem;
+    const size_t smem = kind == 0 ? TC::fwd_smem : (a.stin[0] ? TC::adj_smem_ld : TC::adj_smem);
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -282,16 +291,34 @@ cudaError_t launch_tile_step(const PlanView& p, int kind, TileStepArgs a, cudaSt
       const int grid = (int)std::min<int64_t>(a.ntiles, (int64_t)per_sm * sms);
       kern<<<grid, 32 * TC::W, smem, s>>>(*static_cast<const Consts<N>*>(p.consts), p.geo, a);
     } else {
-      auto kern = tile_adj_kernel<N, TC::W_A, TC::WMT_A>;
-      static int per_sm = 0;
-      if (per_sm == 0) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * TC::W_A, smem);
-        if (per_sm < 1) per_sm = 1;
+      if (a.stin[0]) {
+        if (TC::adj_smem_ld > 227 * 1024) return cudaErrorNotSupported;
+        auto kern = tile_adj_kernel<N, TC::W_L, TC::WMT_L>;
+        static int per_sm = 0;
+        if (per_sm == 0) {
+          cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          if (e != cudaSuccess) return e;
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * TC::W_L, smem);
+          if (per_sm < 1) per_sm = 1;
+        }
+        const int grid = (int)std::min<int64_t>(a.ntiles, (int64_t)per_sm * sms);
+        kern<<<grid, 32 * TC::W_L, smem, s>>>(*static_cast<const Consts<N>*>(p.consts), p.geo, a);
+      } else {
+        auto kern = tile_adj_kernel<N, TC::W_A, TC::WMT_A>;
+        static int per_sm = 0;
+        if (per_sm == 0) {
+          // same instantiation as the stored-stage variant (degrees other than 7): keep the
+          // limit at the larger of the two sizes so neither launch exceeds it
+          constexpr bool same = TC::W_L == TC::W_A && TC::WMT_L == TC::WMT_A;
+          constexpr size_t lim = (same && TC::adj_smem_ld <= 227 * 1024) ? TC::adj_smem_ld : TC::adj_smem;
+          cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim);
+          if (e != cudaSuccess) return e;
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * TC::W_A, smem);
+          if (per_sm < 1) per_sm = 1;
+        }
+        const int grid = (int)std::min<int64_t>(a.ntiles, (int64_t)per_sm * sms);
+        kern<<<grid, 32 * TC::W_A, smem, s>>>(*static_cast<const Consts<N>*>(p.consts), p.geo, a);
       }
-      const int grid = (int)std::min<int64_t>(a.ntiles, (int64_t)per_sm * sms);
-      kern<<<grid, 32 * TC::W_A, smem, s>>>(*static_cast<const Consts<N>*>(p.consts), p.geo, a);
     }
     return cudaGetLastError();
   }

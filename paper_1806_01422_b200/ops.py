@@ -304,6 +304,25 @@ class SemOperator(ComposedStages):
                                              self._flag.data_ptr(), self._stream()),
                    "sem1d_rk_step")
 
+    def step_stages_supported(self):
+        """The fused step pair that keeps the stage states in HBM applies (shared memory fits)."""
+        if not hasattr(self, "_stages_ok"):
+            self._stages_ok = bool(_lib.load().sem1d_step_stages_supported(self._plan.handle)) and not self._adv
+        return self._stages_ok and self.step_fused_supported()
+
+    def launch_rk_step_stages(self, u, u_new, stages, dt, scheme):
+        """One fused step that also writes the stage states U_1..U_{s-1} into `stages`."""
+        _lib.check(_lib.load().sem1d_rk_step_stages(
+            self._plan.handle, u.data_ptr(), u_new.data_ptr(), _lib.ptr_array([t.data_ptr() for t in stages]),
+            float(dt), self._SCHEME_CODES[scheme], self._flag.data_ptr(), self._stream()), "sem1d_rk_step_stages")
+
+    def launch_adj_step_stages(self, u, stages, lam, lam_out, dt, scheme):
+        """One fused adjoint step reading the stored stage states (no recompute)."""
+        _lib.check(_lib.load().sem1d_adj_step_stages(
+            self._plan.handle, u.data_ptr(), _lib.ptr_array([t.data_ptr() for t in stages]), lam.data_ptr(),
+            lam_out.data_ptr(), float(dt), self._SCHEME_CODES[scheme], self._flag.data_ptr(), self._stream()),
+            "sem1d_adj_step_stages")
+
     def launch_adj_step(self, u, lam, lam_out, dt, scheme):
         _lib.check(_lib.load().sem1d_adj_step(self._plan.handle, u.data_ptr(), lam.data_ptr(),
                                               lam_out.data_ptr(), float(dt),

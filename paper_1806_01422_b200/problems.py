@@ -52,6 +52,7 @@ class AssimilationProblem:
     exact_solution: object = None
     checkpoint_slots: int | None = None
     use_ensemble: bool = True   # batch > 1: ring-resident forward sweep when supported
+    keep_stages: object = "auto"  # store-all runs: hold stage states in HBM (no adjoint recompute)
 
     def __post_init__(self):
         self._target_dev = None
@@ -93,8 +94,17 @@ class AssimilationProblem:
                     raise StepFailure(f"non-finite state in problems {fwd.stats['failed'][:8]}")
                 fwd = None   # re-run stepwise: exact reference retry / exception semantics
         if fwd is None:
+            keep = False
+            if self.checkpoint_slots is None and timeloop.stages_supported(self.op, self.ts):
+                if self.keep_stages == "auto":
+                    import torch
+                    s = len(timeloop.TABLEAUX[self.ts.scheme][1])
+                    need = m * (s - 1) * self.op.ndof * 8
+                    keep = need <= 0.5 * torch.cuda.mem_get_info(self.op.device)[0]
+                else:
+                    keep = bool(self.keep_stages)
             fwd = timeloop.integrate(self.op, u0_dev, self.ts,
-                                     store_steps=sched.forward_stores.keys())
+                                     store_steps=sched.forward_stores.keys(), keep_stages=keep)
         if fwd.n_steps != m:  # a StepFailure retry changed the time grid
             sched = self.schedule_for(fwd.n_steps)
         return self._finish(fwd, sched, u0, host)

@@ -161,13 +161,17 @@ class StepEngine:
         k_out = self._buf(("k", i)) if i in store else None
         self.op.launch_rk_stage(U_in, k_out, base, terms, coefs, dt, Y, check)
 
-    def step(self, u, dt, out, fused=True):
+    def step(self, u, dt, out, fused=True, stages_out=None):
         """Launch one full step u -> out (no host sync): one temporally blocked launch
         when the ring qualifies (and ``fused``), else one fused launch per stage, which
-        also leaves the stored slopes (k_2 of Kutta-3 for the embedded pair) in place."""
+        also leaves the stored slopes (k_2 of Kutta-3 for the embedded pair) in place.
+        ``stages_out`` (fused path, s > 1): also write U_1..U_{s-1} there."""
         fz = getattr(self.op, "step_fused_supported", None)
         if fused and fz is not None and fz():
-            self.op.launch_rk_step(u, out, dt, self.scheme)
+            if stages_out is not None and self.s > 1:
+                self.op.launch_rk_step_stages(u, out, stages_out, dt, self.scheme)
+            else:
+                self.op.launch_rk_step(u, out, dt, self.scheme)
             self.op.counters["rhs"] += self.s
             return
         s = self.s
@@ -325,7 +329,15 @@ def count_steps(cfg):
     return n
 
 
-def integrate(op, u0, cfg, store_steps="all", keep_log=False):
+def stages_supported(op, cfg):
+    """Whether a forward run can hold its stage states in HBM for the adjoint (fused
+    whole-step kernels, explicit multi-stage scheme, fixed dt)."""
+    fz = getattr(op, "step_stages_supported", None)
+    return (cfg.scheme in TABLEAUX and len(TABLEAUX[cfg.scheme][1]) > 1 and not cfg.adaptive
+            and fz is not None and fz())
+
+
+def integrate(op, u0, cfg, store_steps="all", keep_log=False, keep_stages=False):
     """Integrate t0 -> t_end recording the trajectory (timeloop.py:237-329).
 
     ``store_steps``: "all", an iterable of step indices, or None (step 0 only).
@@ -349,6 +361,10 @@ def integrate(op, u0, cfg, store_steps="all", keep_log=False):
     cn = cfg.scheme == "cn"
     engine = None if cn else engine_for(op, cfg.scheme)
     fused = not cfg.adaptive          # the embedded pair needs the per-stage k_2
+    # stage states held in HBM for the adjoint (north_star item 4): a step that starts from
+    # a stored state keeps U_1..U_{s-1}; the sweep then skips the stage recompute
+    keep_stages = bool(keep_stages) and stages_supported(op, cfg)
+    stage_snaps = {}
     op.flags()  # clear stale bits
     while t < cfg.t_end - tiny:
         attempts += 1
@@ -364,8 +380,12 @@ def integrate(op, u0, cfg, store_steps="all", keep_log=False):
                 if cn:
                     step_cn(op, u, t, dt, cfg, stats, out=u_new)
                 else:
-                    engine.step(u, dt, u_new, fused=fused)
+                    keep_n = keep_stages and (store_all or n in want)   # the step from a kept state
+                    st_out = [op.empty() for _ in range(engine.s - 1)] if keep_n else None
+                    engine.step(u, dt, u_new, fused=fused, stages_out=st_out)
                     check_step_flags(op)
+                    if keep_n:
+                        stage_snaps[n] = st_out
                 break
             except StepFailure:
                 stats["retries"] += 1
@@ -399,6 +419,7 @@ def integrate(op, u0, cfg, store_steps="all", keep_log=False):
     res = ForwardResult(ts=np.asarray(ts), dts=np.asarray(dts), snapshots=snapshots,
                         u_final=u, stats=stats, step_log=log if keep_log else [])
     res.fused_steps = fused       # replays (checkpoint Advance) take the same kernel path
+    res.stage_snapshots = stage_snaps
     return res
 
 

@@ -59,3 +59,31 @@ def test_fused_step_flags(cuda):
     g, op, u0, ud, ts = _problem(1061, 7, 1e-3, 0.5, 3, "rk4", 1)
     with pytest.raises(sb.NumericFailure):
         timeloop.integrate(op, 1e150 * u0, ts)
+
+
+@pytest.mark.parametrize("scheme,E,N,dt", [("rk4", 1061, 7, 2e-6), ("rk3", 1061, 7, 2e-6),
+                                          ("rk4", 301, 15, 2e-7), ("rk4", 260, 31, 1e-8)])
+def test_stage_states_in_hbm_match_recompute(cuda, scheme, E, N, dt):
+    """integrate(keep_stages=True) + sweep: the adjoint reads the stored stage states instead
+    of recomputing them (sem1d_rk_step_stages / sem1d_adj_step_stages); the gradient equals
+    the recompute path's and evaluate() picks it for store-all runs."""
+    from paper_1806_01422_b200 import adjoint, checkpoint
+    g = grid_1d(0.0, 2.0, E, N)
+    op = sb.SemOperator(g, sb.PdeCoefficients(1e-3), device="cuda:0")
+    assert op.step_fused_supported()
+    x = g.node_coordinates()[0]
+    u0 = torch.from_numpy(np.sin(np.pi * x) + 0.3 * np.cos(3 * np.pi * x)).cuda()
+    ts = timeloop.TsConfig(scheme=scheme, t0=0.0, t_end=12 * dt, dt=dt)
+    assert op.step_stages_supported()
+    grads = {}
+    for keep in (True, False):
+        fwd = timeloop.integrate(op, u0, ts, keep_stages=keep)
+        assert (len(fwd.stage_snapshots) == fwd.n_steps) == keep
+        j, lam = adjoint.terminal_condition(g, fwd.u_final, 0.5 * u0, op=op)
+        grads[keep] = adjoint.sweep(op, ts, fwd, checkpoint.plan_store_all(fwd.n_steps), lam).cpu().numpy()
+    assert rel_err(grads[True], grads[False]) <= 1e-13
+    prob = sb.AssimilationProblem(name="ks", grid=g, op=op, ts=ts, u_target=0.5 * u0.cpu().numpy(),
+                                  u_guess=u0.cpu().numpy())
+    _, ge = prob.evaluate(u0)
+    assert len(prob.last_forward.stage_snapshots) == prob.last_forward.n_steps
+    assert rel_err(ge.cpu().numpy(), grads[False]) <= 1e-13
