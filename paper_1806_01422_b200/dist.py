@@ -273,16 +273,25 @@ class ShardedOperator:
 
     # -- launches: refresh what the kernel reads across element boundaries ------
 
-    def launch_rhs(self, u, out):
-        self.halo.refresh([u])
+    def refresh(self, fields):
+        """One batched ghost exchange for several extended fields; launches on them may then
+        pass refresh=False (e.g. a step applying F(u), J(u)v and J(u)^T w exchanges u, v and w
+        once instead of once per apply)."""
+        self.halo.refresh(list(fields))
+
+    def launch_rhs(self, u, out, refresh=True):
+        if refresh:
+            self.halo.refresh([u])
         self.local.launch_rhs(u, out)
 
-    def launch_jac(self, u, v, out):
-        self.halo.refresh([u, v])
+    def launch_jac(self, u, v, out, refresh=True):
+        if refresh:
+            self.halo.refresh([u, v])
         self.local.launch_jac(u, v, out)
 
-    def launch_jact(self, u, z, out):
-        self.halo.refresh([u, z])
+    def launch_jact(self, u, z, out, refresh=True):
+        if refresh:
+            self.halo.refresh([u, z])
         self.local.launch_jact(u, z, out)
 
     def launch_rk_stage(self, U_in, k_out, base, terms, coefs, dt, Y, check):

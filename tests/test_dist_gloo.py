@@ -70,6 +70,20 @@ def _work(rank, world, bc, q):
         ue, _ = op.field(u[sl])
         we, _ = op.field(w[sl])
         res["dot"] = abs(op.dot(ue, we) - float(u @ w)) <= 1e-12 * abs(float(u @ w))
+        # one batched ghost refresh of (u, v, w), then the applies without their own refresh
+        ve, _ = op.field(v[sl])
+        o1, o2 = op.empty(), op.empty()
+        op.launch_jact(ue, we, o1)
+        ue2, _ = op.field(u[sl])
+        ve2, _ = op.field(v[sl])
+        we2, _ = op.field(w[sl])
+        op.refresh([ue2, ve2, we2])
+        op.launch_jact(ue2, we2, o2, refresh=False)
+        o3, o4 = op.empty(), op.empty()
+        op.launch_jac(ue, ve, o3)
+        op.launch_jac(ue2, ve2, o4, refresh=False)
+        res["batched_refresh"] = bool(np.array_equal(np.asarray(o1), np.asarray(o2))
+                                      and np.array_equal(np.asarray(o3), np.asarray(o4)))
         # step-count / time grid identical on every rank
         res["steps"] = prob.last_forward.n_steps == timeloop.count_steps(ts)
         q.put((rank, res))
