@@ -56,6 +56,14 @@ struct EnsCfg {
 };
 constexpr int kEnsFwdWarps = 16;
 constexpr int kEnsAdjWarps = 8;
+#ifndef ENS_ADJ_W16
+#define ENS_ADJ_W16 1
+#endif
+// backward-sweep warps: 16 at n = 16 with the B fragments in shared memory (ens_adj_bsm)
+template <int N>
+constexpr int ens_adj_warps() { return (ENS_ADJ_W16 && (N + 1) == 16) ? 16 : kEnsAdjWarps; }
+template <int N>
+constexpr bool ens_adj_bsm() { return ens_adj_warps<N>() == 16; }
 // n = 32: 8 warps (255 registers per thread; at 16 warps the 128-register cap spilled)
 template <int N>
 constexpr int ens_fwd_warps() { return (N + 1) == 32 ? 8 : kEnsFwdWarps; }
@@ -325,10 +333,10 @@ struct EnsAdjArgs {
 // l_i = dt J^T(U_i)(b_i lam + sum_{j>i} a_ji l_j) for i = s-1..0 and
 // lam <- lam + (l_{s-1} + ... + l_0).
 template <int N, int WMT_MAX>
-__global__ void __launch_bounds__(EnsCfg<N, kEnsAdjWarps>::THREADS, 1)
+__global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
     ens_adjoint_kernel(const __grid_constant__ Consts<N> C, const Geo G, const EnsAdjArgs A) {
   constexpr int KC = EnsCfg<N>::KC, NT = EnsCfg<N>::NT;
-  constexpr int THREADS = EnsCfg<N, kEnsAdjWarps>::THREADS;
+  constexpr int THREADS = EnsCfg<N, ens_adj_warps<N>()>::THREADS;
   extern __shared__ __align__(16) double smem[];
   const int ndof = (int)G.ndof;
   const int pad = (ndof + 2 + 1) & ~1;
@@ -339,32 +347,48 @@ __global__ void __launch_bounds__(EnsCfg<N, kEnsAdjWarps>::THREADS, 1)
   double* sz = sk + pad;                      // zm for the current J^T
   double* slam = sz + pad;                    // lam (owner-only)
   double* xfer = slam + pad;
+  double* sB = xfer + 32;                     // B-fragment table (ens_adj_bsm), per lane
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kq = lane & 3, rr = lane >> 2;
   const int64_t b = blockIdx.x, nb = gridDim.x;
   const double mnu = -C.nu;
   auto Uarr = [&](int i) -> double* { return i == 0 ? su : sUs + (i - 1) * pad; };
 
-  double breg[3 * NT * KC];
+  // B fragments: registers at 8 warps; at 16 warps (128-register cap) shared memory,
+  // laid out per lane (in registers the compiler re-reads them from parameter space
+  // with lane-divergent indices)
+  constexpr bool BSM = ens_adj_bsm<N>();
+  double breg[BSM ? 1 : 3 * NT * KC];
+  double bpre[(BSM || !TILE_PRE) ? 1 : 2 * NT * KC];
+  if constexpr (BSM) {
+    for (int q = tid; q < 5 * NT * KC * 32; q += THREADS) {
+      const int l = q & 31, f = q >> 5, kc = f % KC, nt = (f / KC) % NT, mat = f / (KC * NT);
+      sB[q] = mat < 3 ? bfrag_perm<N>(C, mat, nt, kc, l)
+                      : (TILE_PRE ? bfrag_pre<N>(C, mat - 3, nt, kc, l) : bfrag_perm<N>(C, mat - 3, nt, kc, l));
+    }
+  } else {
 #pragma unroll
-  for (int mat = 0; mat < 3; ++mat)
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-#pragma unroll
-      for (int kc = 0; kc < KC; ++kc) breg[(mat * NT + nt) * KC + kc] = bfrag_perm<N>(C, mat, nt, kc, lane);
-  auto bget = [&](int mat, int nt, int kc) -> double { return breg[(mat * NT + nt) * KC + kc]; };
-  // stage recompute (ring_rhs<PRE>): K / Dw fragments with -nu M^-1 / M^-1 folded in
-  double bpre[TILE_PRE ? 2 * NT * KC : 1];
-  if (TILE_PRE) {
-#pragma unroll
-    for (int mat = 0; mat < 2; ++mat)
+    for (int mat = 0; mat < 3; ++mat)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int kc = 0; kc < KC; ++kc) bpre[(mat * NT + nt) * KC + kc] = bfrag_pre<N>(C, mat, nt, kc, lane);
+        for (int kc = 0; kc < KC; ++kc) breg[(mat * NT + nt) * KC + kc] = bfrag_perm<N>(C, mat, nt, kc, lane);
+    if (TILE_PRE) {
+#pragma unroll
+      for (int mat = 0; mat < 2; ++mat)
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int kc = 0; kc < KC; ++kc) bpre[(mat * NT + nt) * KC + kc] = bfrag_pre<N>(C, mat, nt, kc, lane);
+    }
   }
+  auto bget = [&](int mat, int nt, int kc) -> double {
+    if constexpr (BSM) return sB[((mat * NT + nt) * KC + kc) * 32 + lane];
+    else return breg[(mat * NT + nt) * KC + kc];
+  };
   auto bpget = [&](int mat, int nt, int kc) -> double {
-    return TILE_PRE ? bpre[(mat * NT + nt) * KC + kc] : breg[(mat * NT + nt) * KC + kc];
+    if constexpr (BSM) return sB[(((mat + 3) * NT + nt) * KC + kc) * 32 + lane];
+    else return TILE_PRE ? bpre[(mat * NT + nt) * KC + kc] : breg[(mat * NT + nt) * KC + kc];
   };
   double minv_a[KC];
 #pragma unroll
@@ -465,7 +489,8 @@ __global__ void __launch_bounds__(EnsCfg<N, kEnsAdjWarps>::THREADS, 1)
 
 template <int N>
 constexpr size_t ens_adj_smem_bytes(int ndof) {
-  return sizeof(double) * (7 * (size_t)((ndof + 2 + 1) & ~1) + 32);
+  constexpr size_t frag = ens_adj_bsm<N>() ? 5 * EnsCfg<N>::NT * EnsCfg<N>::KC * 32 : 0;
+  return sizeof(double) * (7 * (size_t)((ndof + 2 + 1) & ~1) + 32 + frag);
 }
 
 // ============================================================================

@@ -225,10 +225,10 @@ static cudaError_t launch_small(const PlanView& p, const EnsArgs* fa, const EnsA
 template <int N>
 cudaError_t launch_ens_adjoint(const PlanView& p, const EnsAdjArgs& a, cudaStream_t s) {
   if constexpr ((N + 1) % 8 == 0) {
-    constexpr int W = kEnsAdjWarps;
+    constexpr int W = ens_adj_warps<N>();
     constexpr int WMT = 32 / W;
     const size_t smem = ens_adj_smem_bytes<N>((int)p.geo.ndof);
-    if (p.geo.periodic && p.geo.E % 8 == 0 && p.geo.E / 8 <= W * WMT && smem <= 226 * 1024 &&
+    if (p.geo.periodic && p.geo.E % 8 == 0 && p.geo.E / 8 <= W * WMT && smem <= 227 * 1024 &&
         p.geo.E * (N + 1) > 1024) {
       auto kern = ens_adjoint_kernel<N, WMT>;
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
