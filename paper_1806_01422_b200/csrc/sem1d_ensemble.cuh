@@ -56,10 +56,27 @@ struct EnsCfg {
 };
 constexpr int kEnsFwdWarps = 16;
 constexpr int kEnsAdjWarps = 8;
-#ifndef ENS_ADJ_W16
-#define ENS_ADJ_W16 1
+#ifndef TILE_WF16
+#define TILE_WF16 8     // tile forward warps at n = 16 (x 16/W m-tiles; 8 x 2 with ring_elem ILV: 0.178 vs 0.203 ms at 16 x 1)
 #endif
-// backward-sweep warps: 16 at n = 16 with the B fragments in shared memory (ens_adj_bsm)
+#ifndef TILE_WF24
+#define TILE_WF24 8     // n = 24 tile forward: 8 x 2 interleaved (0.146 vs 0.164 ms at 16 x 1)
+#endif
+#ifndef ILV_SIMPLE2
+#define ILV_SIMPLE2 0
+#endif
+#ifndef TILE_ILV
+#define TILE_ILV 1      // tile kernels: interleaved m-tile rows (ring_elem)
+#endif
+#ifndef ENS_ILV
+#define ENS_ILV 1       // ensemble kernels: interleaved rows when E is a multiple of 8*WMT
+#endif
+#ifndef ENS_ADJ_W16
+#define ENS_ADJ_W16 0
+#endif
+// backward-sweep warps: 8 (x 4 interleaved m-tiles at n = 16, B fragments in registers:
+// cfg4 adjoint 764 ms); ENS_ADJ_W16 = 16 warps x 2 with the B fragments in a shared-memory
+// table (ens_adj_bsm; 804 ms: the 128-register cap spills)
 template <int N>
 constexpr int ens_adj_warps() { return (ENS_ADJ_W16 && (N + 1) == 16) ? 16 : kEnsAdjWarps; }
 template <int N>
@@ -68,11 +85,31 @@ constexpr bool ens_adj_bsm() { return ens_adj_warps<N>() == 16; }
 template <int N>
 constexpr int ens_fwd_warps() { return (N + 1) == 32 ? 8 : kEnsFwdWarps; }
 
+// Element held by row rr of a warp's m-tile q.  ILV (interleaved; E a multiple of
+// 8*WMT_MAX, WMT_MAX = 2 or 4): a 64-bit LDS/STS is served per half-warp, whose 16 lanes
+// read rows rr = 4h..4h+3 at nodes 4kc + kq, i.e. doubles N*e + kq.  For odd N they hit 16
+// distinct banks iff the half-warp's 4 elements are congruent mod 4 and distinct mod 16;
+// the contiguous mapping (rows N apart) is a 4-way conflict at N = 15.  WMT_MAX = 4:
+// e = 4 rr + q (16 h + 4 a + q); WMT_MAX = 2: e = 4 a + 2 h + q (a = rr & 3, h = rr >> 2).
+// Each element's arithmetic is unchanged, so results are bit-identical.
+template <int WMT_MAX, bool ILV>
+__device__ __forceinline__ int ring_elem(int warp, int q, int rr) {
+  if constexpr (ILV && WMT_MAX == 2 && !ILV_SIMPLE2) return 16 * warp + 4 * (rr & 3) + 2 * (rr >> 2) + q;
+  else if constexpr (ILV && WMT_MAX > 1) return 8 * WMT_MAX * warp + WMT_MAX * rr + q;
+  else return 8 * (warp * WMT_MAX + q) + rr;
+}
+// Row whose m-tile WMT_MAX-1 holds the left neighbour of (rr, m-tile 0), rr > 0 (ILV)
+template <int WMT_MAX>
+__device__ __forceinline__ int ring_left_row(int rr) {
+  if constexpr (WMT_MAX == 2 && !ILV_SIMPLE2) return rr >= 4 ? rr - 4 : rr + 3;
+  else return rr > 0 ? rr - 1 : 0;
+}
+
 // One operator application over the whole ring held in shared memory.
 // src: node values (ndof + 1 entries; entry ndof mirrors node 0 if periodic).
 // Output: kv[q][kc] = (M^-1-scaled) F at the nodes owned by this lane, for
 // m-tile q of this warp (node 4kc+kq of element 8*(warp + q*W) + rr ... see body).
-template <int N, int WMT_MAX, class BGet, bool WRAP = true, bool PRE = false>
+template <int N, int WMT_MAX, class BGet, bool WRAP = true, bool PRE = false, bool ILV = false>
 __device__ __forceinline__ void ring_rhs(const Consts<N>& C, const Geo& G, const double* src,
                                          double* xfer, BGet bget, const double* minv_a,
                                          double mnu, int warp, int lane,
@@ -86,11 +123,12 @@ __device__ __forceinline__ void ring_rhs(const Consts<N>& C, const Geo& G, const
   const int mt_total = E / 8;
   double carry = 0.0;
   double row0_first = 0.0;
+  double row0s[WMT_MAX], rowNs[WMT_MAX];
 #pragma unroll
   for (int q = 0; q < WMT_MAX; ++q) {
-    const int mt = warp * WMT_MAX + q;        // contiguous m-tiles per warp
+    const int mt = warp * WMT_MAX + q;        // this warp's m-tiles
     if (mt >= mt_total) break;
-    const int e = 8 * mt + rr;
+    const int e = ring_elem<WMT_MAX, ILV>(warp, q, rr);
     const int base = e * N;
     double au[KC];
 #pragma unroll
@@ -125,11 +163,28 @@ __device__ __forceinline__ void ring_rhs(const Consts<N>& C, const Geo& G, const
       for (int h = 0; h < 2; ++h) kv[q][2 * nt + h] = PRE ? r[nt][h] : __dmul_rn(r[nt][h], minv_a[2 * nt + h]);
     const double row0 = r[0][0];
     const double rowN = r[NT - 1][1];
-    double left = __shfl_up_sync(0xffffffffu, rowN, 1);
-    if (rr == 0) left = carry;
-    carry = __shfl_sync(0xffffffffu, rowN, 31);
-    if (q == 0) row0_first = row0;           // lane 0 patches it after the exchange
-    if (kq == 0) kv[q][0] = PRE ? __dadd_rn(left, row0) : __dmul_rn(__dadd_rn(left, row0), minv_a[0]);
+    if (ILV && WMT_MAX > 1) {
+      row0s[q] = row0;
+      rowNs[q] = rowN;
+    } else {
+      double left = __shfl_up_sync(0xffffffffu, rowN, 1);
+      if (rr == 0) left = carry;
+      carry = __shfl_sync(0xffffffffu, rowN, 31);
+      if (q == 0) row0_first = row0;           // lane 0 patches it after the exchange
+      if (kq == 0) kv[q][0] = PRE ? __dadd_rn(left, row0) : __dmul_rn(__dadd_rn(left, row0), minv_a[0]);
+    }
+  }
+  if (ILV && WMT_MAX > 1 && warp * WMT_MAX < mt_total) {
+    // left neighbour of (q, rr): (q-1, rr) in lane 4rr+3; of (0, rr): (WMT_MAX-1, ring_left_row)
+#pragma unroll
+    for (int q = 0; q < WMT_MAX; ++q) {
+      const double left = q > 0 ? __shfl_down_sync(0xffffffffu, rowNs[q - 1], 3)
+                                : __shfl_sync(0xffffffffu, rowNs[WMT_MAX - 1], 4 * ring_left_row<WMT_MAX>(rr) + 3);
+      if (kq == 0 && (q > 0 || rr > 0))
+        kv[q][0] = PRE ? __dadd_rn(left, row0s[q]) : __dmul_rn(__dadd_rn(left, row0s[q]), minv_a[0]);
+    }
+    carry = rowNs[WMT_MAX - 1];
+    row0_first = row0s[0];
   }
   if (lane == 31 && warp * WMT_MAX < mt_total) xfer[warp] = carry;   // row N of the warp's last element
   __syncthreads();
@@ -156,7 +211,7 @@ __device__ __forceinline__ double bfrag_pre(const Consts<N>& C, int mat, int nt,
 
 // Forward sweep of one ring per CTA: periodic rings, E a multiple of 8 with
 // E/8 <= 8 * WMT_MAX.  Trajectory state n+1 is written after step n.
-template <int N, int WMT_MAX>
+template <int N, int WMT_MAX, bool ILV>
 __global__ void __launch_bounds__(EnsCfg<N, ens_fwd_warps<N>()>::THREADS, 1)
     ens_forward_kernel(const __grid_constant__ Consts<N> C, const Geo G, const EnsArgs A) {
   constexpr int n = N + 1, KC = EnsCfg<N>::KC, NT = EnsCfg<N>::NT;
@@ -207,14 +262,14 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_fwd_warps<N>()>::THREADS, 1)
     const double dt = A.dts[step];
     for (int i = 0; i < A.tab.s; ++i) {
       const double* src = (i == 0) ? su : sU;
-      ring_rhs<N, WMT_MAX, decltype(bget), true, TILE_PRE != 0>(C, G, src, xfer, bget, minv_a, mnu, warp, lane, kv,
+      ring_rhs<N, WMT_MAX, decltype(bget), true, TILE_PRE != 0, ILV>(C, G, src, xfer, bget, minv_a, mnu, warp, lane, kv,
                                                                fin);
       // (ring_rhs ended with a barrier: every warp is done reading src)
 #pragma unroll
       for (int q = 0; q < WMT_MAX; ++q) {
         const int mt = warp * WMT_MAX + q;
         if (mt >= mt_total) break;
-        const int e = 8 * mt + rr;
+        const int e = ring_elem<WMT_MAX, ILV>(warp, q, rr);
 #pragma unroll
         for (int kc = 0; kc < KC; ++kc) {
           const int j = 4 * kc + kq;
@@ -265,7 +320,7 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_fwd_warps<N>()>::THREADS, 1)
 // J^T over the ring held in shared memory: usrc = linearisation point, zsrc =
 // zm = mask(z M^-1) already scaled (ops.py:252-254).  Output (no M^-1, ops.py:256):
 // jv[q][kc] at the nodes owned by this lane, interface nodes summed.
-template <int N, int WMT_MAX, class BGet, bool WRAP = true>
+template <int N, int WMT_MAX, class BGet, bool WRAP = true, bool ILV = false>
 __device__ __forceinline__ void ring_jact(const Consts<N>& C, const Geo& G, const double* usrc,
                                           const double* zsrc, double* xfer, BGet bget,
                                           double mnu, int warp, int lane,
@@ -274,11 +329,12 @@ __device__ __forceinline__ void ring_jact(const Consts<N>& C, const Geo& G, cons
   const int kq = lane & 3, rr = lane >> 2;
   const int mt_total = (int)G.E / 8;
   double carry = 0.0, row0_first = 0.0;
+  double row0s[WMT_MAX], rowNs[WMT_MAX];
 #pragma unroll
   for (int q = 0; q < WMT_MAX; ++q) {
     const int mt = warp * WMT_MAX + q;
     if (mt >= mt_total) break;
-    const int base = (8 * mt + rr) * N;
+    const int base = ring_elem<WMT_MAX, ILV>(warp, q, rr) * N;
     double au[KC], az[KC], at[KC];
 #pragma unroll
     for (int kc = 0; kc < KC; ++kc) {
@@ -304,11 +360,26 @@ __device__ __forceinline__ void ring_jact(const Consts<N>& C, const Geo& G, cons
 #pragma unroll
       for (int h = 0; h < 2; ++h) jv[q][2 * nt + h] = r[nt][h];
     const double row0 = r[0][0], rowN = r[NT - 1][1];
-    double left = __shfl_up_sync(0xffffffffu, rowN, 1);
-    if (rr == 0) left = carry;
-    carry = __shfl_sync(0xffffffffu, rowN, 31);
-    if (q == 0) row0_first = row0;
-    if (kq == 0) jv[q][0] = __dadd_rn(left, row0);
+    if (ILV && WMT_MAX > 1) {
+      row0s[q] = row0;
+      rowNs[q] = rowN;
+    } else {
+      double left = __shfl_up_sync(0xffffffffu, rowN, 1);
+      if (rr == 0) left = carry;
+      carry = __shfl_sync(0xffffffffu, rowN, 31);
+      if (q == 0) row0_first = row0;
+      if (kq == 0) jv[q][0] = __dadd_rn(left, row0);
+    }
+  }
+  if (ILV && WMT_MAX > 1 && warp * WMT_MAX < mt_total) {
+#pragma unroll
+    for (int q = 0; q < WMT_MAX; ++q) {
+      const double left = q > 0 ? __shfl_down_sync(0xffffffffu, rowNs[q - 1], 3)
+                                : __shfl_sync(0xffffffffu, rowNs[WMT_MAX - 1], 4 * ring_left_row<WMT_MAX>(rr) + 3);
+      if (kq == 0 && (q > 0 || rr > 0)) jv[q][0] = __dadd_rn(left, row0s[q]);
+    }
+    carry = rowNs[WMT_MAX - 1];
+    row0_first = row0s[0];
   }
   if (lane == 31 && warp * WMT_MAX < mt_total) xfer[warp] = carry;
   __syncthreads();
@@ -332,7 +403,7 @@ struct EnsAdjArgs {
 // shared memory): stage states recomputed from the stored u_n (s-1 F applies), then
 // l_i = dt J^T(U_i)(b_i lam + sum_{j>i} a_ji l_j) for i = s-1..0 and
 // lam <- lam + (l_{s-1} + ... + l_0).
-template <int N, int WMT_MAX>
+template <int N, int WMT_MAX, bool ILV>
 __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
     ens_adjoint_kernel(const __grid_constant__ Consts<N> C, const Geo G, const EnsAdjArgs A) {
   constexpr int KC = EnsCfg<N>::KC, NT = EnsCfg<N>::NT;
@@ -411,7 +482,7 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
     __syncthreads();
     // ---- stage states U_1..U_{S-1} (timeloop.rk3_stages, adjoint.py:56)
     for (int i = 0; i + 1 < S; ++i) {
-      ring_rhs<N, WMT_MAX, decltype(bpget), true, TILE_PRE != 0>(C, G, Uarr(i), xfer, bpget, minv_a, mnu, warp,
+      ring_rhs<N, WMT_MAX, decltype(bpget), true, TILE_PRE != 0, ILV>(C, G, Uarr(i), xfer, bpget, minv_a, mnu, warp,
                                                                 lane, kv, fin);
       double* dst = Uarr(i + 1);
 #pragma unroll
@@ -422,7 +493,7 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
         for (int kc = 0; kc < KC; ++kc) {
           const int j = 4 * kc + kq;
           if (j == N) continue;
-          const int g = (8 * mt + rr) * N + j;
+          const int g = ring_elem<WMT_MAX, ILV>(warp, q, rr) * N + j;
           const double kk = kv[q][kc];
           double y;
           if (A.tab.nterm[i + 1] == 1) {
@@ -450,7 +521,7 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
         for (int kc = 0; kc < KC; ++kc) {
           const int j = 4 * kc + kq;
           if (j == N) continue;
-          const int g = (8 * mt + rr) * N + j;
+          const int g = ring_elem<WMT_MAX, ILV>(warp, q, rr) * N + j;
           // z = b_i lam + a_{i+1,i} l_{i+1} + a_{i+2,i} l_{i+2} (adjoint.py:58-60)
           double z = __dmul_rn(A.tab.b[i], slam[g]);
           if (i + 1 < S && A.tab.a[i + 1][i] != 0.0) z = __dadd_rn(z, __dmul_rn(A.tab.a[i + 1][i], lnext[q][kc]));
@@ -462,7 +533,7 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
         }
       }
       __syncthreads();
-      ring_jact<N, WMT_MAX>(C, G, Uarr(i), sz, xfer, bget, mnu, warp, lane, kv);
+      ring_jact<N, WMT_MAX, decltype(bget), true, ILV>(C, G, Uarr(i), sz, xfer, bget, mnu, warp, lane, kv);
 #pragma unroll
       for (int q = 0; q < WMT_MAX; ++q) {
         const int mt = warp * WMT_MAX + q;
@@ -471,7 +542,7 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
         for (int kc = 0; kc < KC; ++kc) {
           const int j = 4 * kc + kq;
           if (j == N) continue;
-          const int g = (8 * mt + rr) * N + j;
+          const int g = ring_elem<WMT_MAX, ILV>(warp, q, rr) * N + j;
           const double l = __dmul_rn(dt, kv[q][kc]);
           lacc[q][kc] = (i == S - 1) ? l : __dadd_rn(lacc[q][kc], l);
           if (i + 1 < S && S == 3) sk[g] = lnext[q][kc];   // RK3: keep l_{i+1} for z_{i-1}
@@ -675,7 +746,7 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
     for (int st = 0; st < A.tab.s; ++st) {
       if (A.stages[0] && tid == 0) bulk_wait_read<0>();   // the previous stage's store has read sU
       const double* src = (st == 0) ? su : sU;
-      ring_rhs<N, WMT, decltype(bget), false, TILE_PRE != 0>(C, Gt, src, xfer, bget, minv_a, mnu, warp, lane, kv,
+      ring_rhs<N, WMT, decltype(bget), false, TILE_PRE != 0, TILE_ILV != 0>(C, Gt, src, xfer, bget, minv_a, mnu, warp, lane, kv,
                                                             fin);
       const double tb = A.tab.b[st];
       const bool last = (st + 1 == A.tab.s);
@@ -683,7 +754,7 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
       const double c1 = last ? 0.0 : __dmul_rn(A.dt, A.tab.a[st + 1][st]);
 #pragma unroll
       for (int q = 0; q < WMT; ++q) {
-        const int e = 8 * (warp * WMT + q) + rr;
+        const int e = ring_elem<WMT, TILE_ILV != 0>(warp, q, rr);
 #pragma unroll
         for (int kc = 0; kc < KC; ++kc) {
           const int j = 4 * kc + kq;
@@ -860,12 +931,12 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N>())
     if (tid == 0 && !LD)
       for (int i = 1; i < S; ++i) Uarr(i)[LEN - 1] = su[LEN - 1];   // never-owned last node
     for (int i = 0; i + 1 < S && !LD; ++i) {
-      ring_rhs<N, WMT, decltype(bpget), false, TILE_PRE != 0>(C, Gt, Uarr(i), xfer, bpget, minv_a, mnu, warp, lane,
+      ring_rhs<N, WMT, decltype(bpget), false, TILE_PRE != 0, TILE_ILV != 0>(C, Gt, Uarr(i), xfer, bpget, minv_a, mnu, warp, lane,
                                                               kv, fin);
       double* dst = Uarr(i + 1);
 #pragma unroll
       for (int q = 0; q < WMT; ++q) {
-        const int e = 8 * (warp * WMT + q) + rr;
+        const int e = ring_elem<WMT, TILE_ILV != 0>(warp, q, rr);
 #pragma unroll
         for (int kc = 0; kc < KC; ++kc) {
           const int j = 4 * kc + kq;
@@ -890,7 +961,7 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N>())
     for (int i = S - 1; i >= 0; --i) {
 #pragma unroll
       for (int q = 0; q < WMT; ++q) {
-        const int e = 8 * (warp * WMT + q) + rr;
+        const int e = ring_elem<WMT, TILE_ILV != 0>(warp, q, rr);
 #pragma unroll
         for (int kc = 0; kc < KC; ++kc) {
           const int j = 4 * kc + kq;
@@ -905,10 +976,10 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N>())
       }
       if (tid == 0) sz[TE * N] = 0.0;         // last node of the open chain (ghost margin)
       __syncthreads();
-      ring_jact<N, WMT, decltype(bget), false>(C, Gt, Uarr(i), sz, xfer, bget, mnu, warp, lane, kv);
+      ring_jact<N, WMT, decltype(bget), false, TILE_ILV != 0>(C, Gt, Uarr(i), sz, xfer, bget, mnu, warp, lane, kv);
 #pragma unroll
       for (int q = 0; q < WMT; ++q) {
-        const int e = 8 * (warp * WMT + q) + rr;
+        const int e = ring_elem<WMT, TILE_ILV != 0>(warp, q, rr);
 #pragma unroll
         for (int kc = 0; kc < KC; ++kc) {
           const int j = 4 * kc + kq;
@@ -935,15 +1006,16 @@ template <int N>
 struct TileCfg {
   // forward: TE = 256 elements for N = 7 (8 warps x 4 m-tiles, 2 CTAs per SM: the second
   // CTA's DMMA fills the first one's barrier waits; A/B 0.48 vs 0.54 ms per RK4 step at
-  // 16 x 4 x 1), 128 for N = 15/23, 64 for N = 31; adjoint: 128 for N = 7 (4 warps x 4
+  // 16 x 4 x 1), 128 for N = 15/23 (N = 15: 8 warps x 2 interleaved m-tiles), 64 for N = 31;
+  // adjoint: 128 for N = 7 (4 warps x 4
   // m-tiles, 3 CTAs per SM; 1.155 vs 1.190 ms at 16 x 2 x 1), 128 / 64 otherwise (nine
   // slabs must fit the shared memory of the resident CTAs)
-  static constexpr int W = (N + 1) == 32 ? 8 : ((N + 1) == 8 ? TILE_WF8 : 16);
+  static constexpr int W = (N + 1) == 32 ? 8 : ((N + 1) == 8 ? TILE_WF8 : ((N + 1) == 16 ? TILE_WF16 : TILE_WF24));
   // adjoint warps: 8 x 2 m-tiles for N = 15/23 (at 16 warps the 128-register cap made the
   // compiler re-read the B fragments from kernel-parameter space with lane-divergent
   // indices inside the DMMA loops: 6.9x the forward step)
   static constexpr int W_A = (N + 1) == 8 ? TILE_WA8 : ((N + 1) == 32 ? 8 : TILE_WA16);
-  static constexpr int WMT_F = (N + 1) == 8 ? TILE_WMT8 : 1;
+  static constexpr int WMT_F = (N + 1) == 8 ? TILE_WMT8 : ((N + 1) == 32 ? 1 : 16 / W);
   static constexpr int WMT_A = (N + 1) == 8 ? TILE_WMTA8 : ((N + 1) == 32 ? 1 : 128 / (8 * TILE_WA16));
   // adjoint step reading stored stage states (fewer DMMAs, 12 slabs): its own warp shape
   static constexpr int W_L = (N + 1) == 8 ? TILE_WL8 : W_A;

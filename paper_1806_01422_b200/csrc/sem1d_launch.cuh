@@ -230,7 +230,7 @@ cudaError_t launch_ens_adjoint(const PlanView& p, const EnsAdjArgs& a, cudaStrea
     const size_t smem = ens_adj_smem_bytes<N>((int)p.geo.ndof);
     if (p.geo.periodic && p.geo.E % 8 == 0 && p.geo.E / 8 <= W * WMT && smem <= 227 * 1024 &&
         p.geo.E * (N + 1) > 1024) {
-      auto kern = ens_adjoint_kernel<N, WMT>;
+      auto kern = (ENS_ILV && p.geo.E % (8 * WMT) == 0) ? ens_adjoint_kernel<N, WMT, true> : ens_adjoint_kernel<N, WMT, false>;
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       kern<<<(unsigned)p.batch, EnsCfg<N, W>::THREADS, smem, s>>>(
@@ -250,7 +250,7 @@ cudaError_t launch_ens_forward(const PlanView& p, const EnsArgs& a, cudaStream_t
     const size_t smem = ens_smem_bytes<N>((int)p.geo.ndof);
     if (p.geo.periodic && p.geo.E % 8 == 0 && p.geo.E / 8 <= W * WMT && smem <= 220 * 1024 &&
         p.geo.E * (N + 1) > 1024) {
-      auto kern = ens_forward_kernel<N, WMT>;
+      auto kern = (ENS_ILV && p.geo.E % (8 * WMT) == 0) ? ens_forward_kernel<N, WMT, true> : ens_forward_kernel<N, WMT, false>;
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       kern<<<(unsigned)p.batch, EnsCfg<N, W>::THREADS, smem, s>>>(

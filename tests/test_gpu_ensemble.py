@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("scheme", ["rk4", "rk3", "euler"])
-@pytest.mark.parametrize("E,N", [(256, 15), (64, 7), (32, 31), (16, 15)])
+@pytest.mark.parametrize("E,N", [(256, 15), (64, 7), (32, 31), (16, 15), (72, 15), (40, 31)])
 def test_ensemble_forward_vs_oracle(cuda, scheme, E, N):
     B, steps, dt = 5, 25, 5e-5
     grid = grid_1d(0.0, 20.0, E, N)
@@ -59,7 +59,7 @@ def test_cfg4_batched_gradient_vs_oracle(cuda):
 
 
 @pytest.mark.parametrize("scheme", ["rk4", "rk3", "euler"])
-@pytest.mark.parametrize("E,N", [(256, 15), (64, 7), (32, 31)])
+@pytest.mark.parametrize("E,N", [(256, 15), (64, 7), (32, 31), (72, 15), (40, 31)])
 def test_ensemble_adjoint_vs_stage_sweep(cuda, scheme, E, N):
     """Ring-resident backward sweep == stage-kernel sweep == oracle (1e-9)."""
     from paper_1806_01422_b200 import adjoint, checkpoint

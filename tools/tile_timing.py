@@ -1,9 +1,9 @@
-"""Fused RK4 step / adjoint step timings (recompute and stored-stage variants) for N = 7, 15, 31."""
+"""Fused RK4 step / adjoint step timings (recompute and stored-stage variants) for N = 7, 15, 23, 31."""
 import json, sys, torch
 sys.path.insert(0, '.')
 import paper_1806_01422_b200 as sb
 from paper_1806_01422_b200.grid import grid_1d
-for N, E in ((7, 1 << 20), (15, 1 << 19), (31, 1 << 18)):
+for N, E in ((7, 1 << 20), (15, 1 << 19), (23, 1 << 18), (31, 1 << 18)):
     g = grid_1d(0.0, E / 64.0, E, N)
     op = sb.SemOperator(g, sb.PdeCoefficients(1e-3), device="cuda:0")
     u = torch.sin(torch.linspace(0, 50, op.ndof, dtype=torch.float64, device="cuda"))
