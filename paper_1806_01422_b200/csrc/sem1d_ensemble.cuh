@@ -209,6 +209,23 @@ __device__ __forceinline__ double bfrag_pre(const Consts<N>& C, int mat, int nt,
   return mat == 0 ? __dmul_rn(b, __dmul_rn(-C.nu, mi)) : __dmul_rn(b, mi);
 }
 
+// B fragments of ring_jact<PREJ = true> (tile adjoint steps): dt and M^-1 folded in, so the
+// stage input z enters unscaled and the row value is already the stage's l contribution:
+// K column j by -nu dt M^-1_j, Dw row i (the z o (Dw u) term) by dt M^-1_i, Dw^T column j
+// by dt M^-1_j (periodic rings: the interface rows/columns take the pattern entry 0)
+template <int N>
+__device__ __forceinline__ double bfrag_adj(const Consts<N>& C, int mat, int nt, int kc, int lane, double dt) {
+  const int c = 8 * nt + (lane >> 2);
+  const int i = 4 * (2 * (c >> 3) + (c & 1)) + ((c >> 1) & 3);      // permuted output row
+  const int j = 4 * kc + (lane & 3);                                  // input node
+  const double mi = C.minv[(i == 0 || i == N) ? 0 : i];
+  const double mj = C.minv[(j == 0 || j == N) ? 0 : j];
+  const double b = bfrag_perm<N>(C, mat, nt, kc, lane);
+  if (mat == 0) return __dmul_rn(b, __dmul_rn(__dmul_rn(-C.nu, dt), mj));
+  if (mat == 1) return __dmul_rn(b, __dmul_rn(dt, mi));
+  return __dmul_rn(b, __dmul_rn(dt, mj));
+}
+
 // Forward sweep of one ring per CTA: periodic rings, E a multiple of 8 with
 // E/8 <= 8 * WMT_MAX.  Trajectory state n+1 is written after step n.
 template <int N, int WMT_MAX, bool ILV>
@@ -320,7 +337,9 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_fwd_warps<N>()>::THREADS, 1)
 // J^T over the ring held in shared memory: usrc = linearisation point, zsrc =
 // zm = mask(z M^-1) already scaled (ops.py:252-254).  Output (no M^-1, ops.py:256):
 // jv[q][kc] at the nodes owned by this lane, interface nodes summed.
-template <int N, int WMT_MAX, class BGet, bool WRAP = true, bool ILV = false>
+// PREJ: fragments from bfrag_adj, zsrc holds the unscaled stage input z, and the output is
+// dt * J^T(M^-1 z) (the M^-1 and dt products ride on the DMMAs)
+template <int N, int WMT_MAX, class BGet, bool WRAP = true, bool ILV = false, bool PREJ = false>
 __device__ __forceinline__ void ring_jact(const Consts<N>& C, const Geo& G, const double* usrc,
                                           const double* zsrc, double* xfer, BGet bget,
                                           double mnu, int warp, int lane,
@@ -352,8 +371,8 @@ __device__ __forceinline__ void ring_jact(const Consts<N>& C, const Geo& G, cons
         dmma884(p0, p1, au[kc], bget(1, nt, kc));   // Dw u
         dmma884(t0, t1, at[kc], bget(2, nt, kc));   // Dw^T (u o zm)
       }
-      r[nt][0] = __dsub_rn(__dsub_rn(__dmul_rn(k0, mnu), __dmul_rn(az[2 * nt], p0)), t0);
-      r[nt][1] = __dsub_rn(__dsub_rn(__dmul_rn(k1, mnu), __dmul_rn(az[2 * nt + 1], p1)), t1);
+      r[nt][0] = __dsub_rn(__dsub_rn(PREJ ? k0 : __dmul_rn(k0, mnu), __dmul_rn(az[2 * nt], p0)), t0);
+      r[nt][1] = __dsub_rn(__dsub_rn(PREJ ? k1 : __dmul_rn(k1, mnu), __dmul_rn(az[2 * nt + 1], p1)), t1);
     }
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
@@ -668,10 +687,39 @@ __device__ __forceinline__ void tile_issue_n(const TileLoad& L, int LEN, const d
 // resident CTAs per SM (A/B: a 64-register cap for two CTAs made the n = 8 step 2x slower)
 template <int N>
 constexpr int tile_minb() { return (N + 1) == 8 ? TILE_MINB8 : 1; }
-template <int N>
-constexpr int tile_adj_minb() { return (N + 1) == 8 ? TILE_ADJ_MINB8 : 1; }
+#ifndef TILE_ADJ_LD_MINB8
+#define TILE_ADJ_LD_MINB8 5
+#endif
+template <int N, int MODE = 0>
+constexpr int tile_adj_minb() { return (N + 1) == 8 ? (MODE == 1 ? TILE_ADJ_LD_MINB8 : TILE_ADJ_MINB8) : 1; }
 
-template <int N, int W, int WMT>
+// Compile-time Butcher tableaux of the tile-step kernels (same values as make_tableau:
+// 0 euler, 1 Kutta-3 of timeloop.py:24-27, 2 classic RK4): with the stage count and
+// coefficients constant the stage loops unroll and every tableau branch folds away
+// (a runtime tableau made integer/branch instructions half of the adjoint step's issue)
+template <int SCH>
+struct TabC {
+  static constexpr int s = SCH == 0 ? 1 : (SCH == 1 ? 3 : 4);
+  __host__ __device__ static constexpr double a(int i, int j) {
+    return SCH == 1 ? ((i == 1 && j == 0) ? 0.5 : (i == 2 && j == 0) ? -1.0 : (i == 2 && j == 1) ? 2.0 : 0.0)
+         : SCH == 2 ? (((i == 1 && j == 0) || (i == 2 && j == 1)) ? 0.5 : (i == 3 && j == 2) ? 1.0 : 0.0)
+                    : 0.0;
+  }
+  __host__ __device__ static constexpr double b(int i) {
+    return SCH == 0 ? 1.0
+         : SCH == 1 ? (i == 1 ? 2.0 / 3.0 : 1.0 / 6.0)
+                    : ((i == 0 || i == 3) ? 1.0 / 6.0 : 1.0 / 3.0);
+  }
+  __host__ __device__ static constexpr int nterm(int i) {
+    int n = 0;
+    for (int j = 0; j < i; ++j) n += a(i, j) != 0.0;
+    return n;
+  }
+  __host__ __device__ static constexpr int keep(int j) { return (SCH == 1 && j == 0) ? 1 : 0; }
+};
+
+// MODE 0: plain step; 1: also store the stage states U_1..U_{s-1} (north_star item 4)
+template <int N, int W, int WMT, int SCH, int MODE>
 __global__ void __launch_bounds__(32 * W, tile_minb<N>())
     tile_step_kernel(const __grid_constant__ Consts<N> C, const Geo G, const TileStepArgs A) {
   constexpr int KC = (N + 1) / 4, NT = (N + 1) / 8;
@@ -687,6 +735,8 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kq = lane & 3, rr = lane >> 2;
   const int T = TE - 2 * A.H;
+  using TB = TabC<SCH>;                       // compile-time tableau: stage loops unroll
+  constexpr bool STG = MODE == 1;
   const int64_t ndof = G.ndof;
   const double mnu = -C.nu;
   Geo Gt = G;
@@ -743,15 +793,16 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
     }
     const double* su = sb + L.sh;
     if (tid == 0) sU[LEN - 1] = su[LEN - 1];   // the chain's last node is never owned
-    for (int st = 0; st < A.tab.s; ++st) {
-      if (A.stages[0] && tid == 0) bulk_wait_read<0>();   // the previous stage's store has read sU
+#pragma unroll
+    for (int st = 0; st < TB::s; ++st) {
+      if (STG && tid == 0) bulk_wait_read<0>();   // the previous stage's store has read sU
       const double* src = (st == 0) ? su : sU;
       ring_rhs<N, WMT, decltype(bget), false, TILE_PRE != 0, TILE_ILV != 0>(C, Gt, src, xfer, bget, minv_a, mnu, warp, lane, kv,
                                                             fin);
-      const double tb = A.tab.b[st];
-      const bool last = (st + 1 == A.tab.s);
-      const bool one = !last && A.tab.nterm[st + 1] == 1;
-      const double c1 = last ? 0.0 : __dmul_rn(A.dt, A.tab.a[st + 1][st]);
+      const double tb = TB::b(st);
+      const bool last = (st + 1 == TB::s);
+      const bool one = !last && TB::nterm(st + 1) == 1;
+      const double c1 = last ? 0.0 : __dmul_rn(A.dt, TB::a(st + 1, st));
 #pragma unroll
       for (int q = 0; q < WMT; ++q) {
         const int e = ring_elem<WMT, TILE_ILV != 0>(warp, q, rr);
@@ -768,13 +819,14 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
             if (one) {
               y = __dadd_rn(su[g], __dmul_rn(c1, kk));
             } else {
-              double sacc = __dmul_rn(A.tab.a[st + 1][0], (st == 0) ? kk : sk[g]);
+              double sacc = __dmul_rn(TB::a(st + 1, 0), (st == 0) ? kk : sk[g]);
+#pragma unroll
               for (int jj = 1; jj <= st; ++jj)
-                sacc = __dadd_rn(sacc, __dmul_rn(A.tab.a[st + 1][jj], (jj == st) ? kk : sk[g]));
+                sacc = __dadd_rn(sacc, __dmul_rn(TB::a(st + 1, jj), (jj == st) ? kk : sk[g]));
               y = __dadd_rn(su[g], __dmul_rn(A.dt, sacc));
             }
             sU[g] = y;
-            if (st == 0 && A.tab.keep[0]) sk[g] = kk;
+            if (st == 0 && TB::keep(0)) sk[g] = kk;
           } else {
             const double un = __dadd_rn(su[g], __dmul_rn(A.dt, acc[q][kc]));
             if (e >= A.H && e < A.H + T) bad |= !isfinite(un);
@@ -782,9 +834,9 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
           }
         }
       }
-      if (A.stages[0]) fence_proxy_async_smem();   // sU is read by the bulk store below
+      if (STG) fence_proxy_async_smem();   // sU is read by the bulk store below
       __syncthreads();
-      if (A.stages[0] && st + 1 < A.tab.s) {  // stage state U_{st+1} of the owned elements
+      if (STG && st + 1 < TB::s) {  // stage state U_{st+1} of the owned elements
         const int64_t e_o = (int64_t)t * T;
         const int no = (int)min((int64_t)T, G.E - e_o) * N;
         double* dst = A.stages[st] + e_o * N;
@@ -804,13 +856,15 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
     for (int k = tid; k < nout_el * N; k += 32 * W) A.out[e_out0 * N + k] = sU[A.H * N + k];
     __syncthreads();
   }
-  if (A.stages[0] && tid == 0) bulk_wait_all();
+  if (STG && tid == 0) bulk_wait_all();
   if (fin || bad)
     atomicOr(A.flag, (fin ? SEM1D_FLAG_STATE_NONFINITE : 0) | (bad ? SEM1D_FLAG_STEP_NONFINITE : 0));
 }
 
-template <int N, int W, int WMT>
-__global__ void __launch_bounds__(32 * W, tile_adj_minb<N>())
+// MODE 0: stage states recomputed (H = 2s-1); 1: read from the forward run's stored
+// states (H = s)
+template <int N, int W, int WMT, int SCH, int MODE>
+__global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
     tile_adj_kernel(const __grid_constant__ Consts<N> C, const Geo G, const TileStepArgs A) {
   constexpr int KC = (N + 1) / 4, NT = (N + 1) / 8;
   constexpr int TE = 8 * W * WMT;
@@ -821,7 +875,8 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N>())
   double* sbl = sbu + 2 * PAD;                // [2][PAD] lam loads (accumulated in place)
   // stage states: recomputed into [3][PAD], or (stored by the forward step) prefetched with
   // the tile into [2][3][PAD]
-  const bool LD = A.stin[0] != nullptr;
+  constexpr bool LD = MODE == 1;
+  using TB = TabC<SCH>;                       // compile-time tableau: stage loops unroll
   double* sUs = sbl + 2 * PAD;
   double* sk = sUs + (LD ? 6 : 3) * PAD;
   double* sz = sk + PAD;
@@ -830,7 +885,7 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N>())
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kq = lane & 3, rr = lane >> 2;
   const int T = TE - 2 * A.H;
-  const int S = A.tab.s;
+  constexpr int S = TB::s;
   auto issue = [&](const TileLoad& Lx, int buf) {
     const double* srcs[5] = {A.u, A.lam, A.stin[0], A.stin[1], A.stin[2]};
     double* dsts[5] = {sbu + buf * PAD, sbl + buf * PAD, sUs + (buf * 3 + 0) * PAD, sUs + (buf * 3 + 1) * PAD,
@@ -856,7 +911,7 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N>())
   if constexpr (BSM) {
     for (int q = tid; q < 5 * NT * KC * 32; q += blockDim.x) {
       const int l = q & 31, f = q >> 5, kc = f % KC, nt = (f / KC) % NT, mat = f / (KC * NT);
-      sB[q] = mat < 3 ? bfrag_perm<N>(C, mat, nt, kc, l)
+      sB[q] = mat < 3 ? bfrag_adj<N>(C, mat, nt, kc, l, A.dt)
                       : (TILE_PRE ? bfrag_pre<N>(C, mat - 3, nt, kc, l) : bfrag_perm<N>(C, mat - 3, nt, kc, l));
     }
   } else {
@@ -865,7 +920,7 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N>())
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int kc = 0; kc < KC; ++kc) breg[(mat * NT + nt) * KC + kc] = bfrag_perm<N>(C, mat, nt, kc, lane);
+        for (int kc = 0; kc < KC; ++kc) breg[(mat * NT + nt) * KC + kc] = bfrag_adj<N>(C, mat, nt, kc, lane, A.dt);
     if (TILE_PRE) {
 #pragma unroll
       for (int mat = 0; mat < 2; ++mat)
@@ -930,6 +985,7 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N>())
     sUb = LD ? sUs + bsel * 3 * PAD + L.sh : sUs;
     if (tid == 0 && !LD)
       for (int i = 1; i < S; ++i) Uarr(i)[LEN - 1] = su[LEN - 1];   // never-owned last node
+#pragma unroll
     for (int i = 0; i + 1 < S && !LD; ++i) {
       ring_rhs<N, WMT, decltype(bpget), false, TILE_PRE != 0, TILE_ILV != 0>(C, Gt, Uarr(i), xfer, bpget, minv_a, mnu, warp, lane,
                                                               kv, fin);
@@ -944,39 +1000,49 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N>())
           const int g = e * N + j;
           const double kk = kv[q][kc];
           double y;
-          if (A.tab.nterm[i + 1] == 1) {
-            y = __dadd_rn(su[g], __dmul_rn(__dmul_rn(A.dt, A.tab.a[i + 1][i]), kk));
+          if (TB::nterm(i + 1) == 1) {
+            y = __dadd_rn(su[g], __dmul_rn(__dmul_rn(A.dt, TB::a(i + 1, i)), kk));
           } else {
-            double sacc = __dmul_rn(A.tab.a[i + 1][0], (i == 0) ? kk : sk[g]);
+            double sacc = __dmul_rn(TB::a(i + 1, 0), (i == 0) ? kk : sk[g]);
+#pragma unroll
             for (int jj = 1; jj <= i; ++jj)
-              sacc = __dadd_rn(sacc, __dmul_rn(A.tab.a[i + 1][jj], (jj == i) ? kk : sk[g]));
+              sacc = __dadd_rn(sacc, __dmul_rn(TB::a(i + 1, jj), (jj == i) ? kk : sk[g]));
             y = __dadd_rn(su[g], __dmul_rn(A.dt, sacc));
           }
           dst[g] = y;
-          if (i == 0 && A.tab.keep[0]) sk[g] = kk;
+          if (i == 0 && TB::keep(0)) sk[g] = kk;
         }
       }
       __syncthreads();
     }
-    for (int i = S - 1; i >= 0; --i) {
+    // z of stage i (unscaled; M^-1 rides on the J^T fragments): b_i lam + sum_{j>i} a_ji l_j
+    // with l_{i+1} in lnext and (Kutta-3) l_{i+2} in sk
+    auto zval = [&](int i, int g, int q, int kc) -> double {
+      double z = __dmul_rn(TB::b(i), slam[g]);
+      if (i + 1 < S && TB::a(i + 1, i) != 0.0) z = __dadd_rn(z, __dmul_rn(TB::a(i + 1, i), lnext[q][kc]));
+      if (i + 2 < S && TB::a(i + 2, i) != 0.0) z = __dadd_rn(z, __dmul_rn(TB::a(i + 2, i), sk[g]));
+      return z;
+    };
 #pragma unroll
-      for (int q = 0; q < WMT; ++q) {
-        const int e = ring_elem<WMT, TILE_ILV != 0>(warp, q, rr);
+    for (int q = 0; q < WMT; ++q) {
+      const int e = ring_elem<WMT, TILE_ILV != 0>(warp, q, rr);
 #pragma unroll
-        for (int kc = 0; kc < KC; ++kc) {
-          const int j = 4 * kc + kq;
-          if (j == N) continue;
-          const int g = e * N + j;
-          double z = __dmul_rn(A.tab.b[i], slam[g]);
-          if (i + 1 < S && A.tab.a[i + 1][i] != 0.0) z = __dadd_rn(z, __dmul_rn(A.tab.a[i + 1][i], lnext[q][kc]));
-          if (i + 2 < S && A.tab.a[i + 2][i] != 0.0) z = __dadd_rn(z, __dmul_rn(A.tab.a[i + 2][i], sk[g]));
-          if (e >= A.H && e < A.H + T) fin |= nonfinite_bit(z);
-          sz[g] = __dmul_rn(z, minv_a[kc]);
-        }
+      for (int kc = 0; kc < KC; ++kc) {
+        const int j = 4 * kc + kq;
+        if (j == N) continue;
+        const int g = e * N + j;
+        const double z = zval(S - 1, g, q, kc);
+        if (e >= A.H && e < A.H + T) fin |= nonfinite_bit(z);
+        sz[g] = z;
       }
-      if (tid == 0) sz[TE * N] = 0.0;         // last node of the open chain (ghost margin)
-      __syncthreads();
-      ring_jact<N, WMT, decltype(bget), false, TILE_ILV != 0>(C, Gt, Uarr(i), sz, xfer, bget, mnu, warp, lane, kv);
+    }
+    if (tid == 0) sz[TE * N] = 0.0;           // last node of the open chain (ghost margin)
+    __syncthreads();
+    // per stage: J^T apply (its internal barrier ends every read of sz), then accumulate l_i
+    // and form z_{i-1} in the same pass -- two barriers per stage
+#pragma unroll
+    for (int i = S - 1; i >= 0; --i) {
+      ring_jact<N, WMT, decltype(bget), false, TILE_ILV != 0, true>(C, Gt, Uarr(i), sz, xfer, bget, mnu, warp, lane, kv);
 #pragma unroll
       for (int q = 0; q < WMT; ++q) {
         const int e = ring_elem<WMT, TILE_ILV != 0>(warp, q, rr);
@@ -985,11 +1051,17 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N>())
           const int j = 4 * kc + kq;
           if (j == N) continue;
           const int g = e * N + j;
-          const double l = __dmul_rn(A.dt, kv[q][kc]);
+          const double l = kv[q][kc];           // already dt * J^T(M^-1 z)
           lacc[q][kc] = (i == S - 1) ? l : __dadd_rn(lacc[q][kc], l);
           if (i + 1 < S && S == 3) sk[g] = lnext[q][kc];
           lnext[q][kc] = l;
-          if (i == 0) slam[g] = __dadd_rn(slam[g], lacc[q][kc]);
+          if (i == 0) {
+            slam[g] = __dadd_rn(slam[g], lacc[q][kc]);
+          } else {
+            const double z = zval(i - 1, g, q, kc);
+            if (e >= A.H && e < A.H + T) fin |= nonfinite_bit(z);
+            sz[g] = z;
+          }
         }
       }
       __syncthreads();

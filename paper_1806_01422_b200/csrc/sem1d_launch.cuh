@@ -261,8 +261,47 @@ cudaError_t launch_ens_forward(const PlanView& p, const EnsArgs& a, cudaStream_t
   return launch_small<N>(p, &a, nullptr, s);
 }
 
+// One tile-step kernel instantiation: occupancy queried once (static per instantiation),
+// grid = min(tiles, resident CTAs).
+template <int N, auto KERN>
+cudaError_t launch_tile_one(const PlanView& p, const TileStepArgs& a, int threads, size_t smem,
+                            size_t smem_limit, cudaStream_t s) {
+  static int per_sm = 0;
+  static int sms = 0;
+  if (per_sm == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_limit);
+    if (e != cudaSuccess) return e;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, KERN, threads, smem);
+    if (per_sm < 1) per_sm = 1;
+  }
+  const int grid = (int)std::min<int64_t>(a.ntiles, (int64_t)per_sm * sms);
+  KERN<<<grid, threads, smem, s>>>(*static_cast<const Consts<N>*>(p.consts), p.geo, a);
+  return cudaGetLastError();
+}
+
+template <int N, int SCH>
+cudaError_t launch_tile_sch(const PlanView& p, int kind, const TileStepArgs& a, cudaStream_t s) {
+  using TC = TileCfg<N>;
+  if (kind == 0) {
+    if (a.stages[0]) return launch_tile_one<N, tile_step_kernel<N, TC::W, TC::WMT_F, SCH, 1>>(p, a, 32 * TC::W, TC::fwd_smem, TC::fwd_smem, s);
+    return launch_tile_one<N, tile_step_kernel<N, TC::W, TC::WMT_F, SCH, 0>>(p, a, 32 * TC::W, TC::fwd_smem, TC::fwd_smem, s);
+  }
+  if (a.stin[0]) {
+    if constexpr (SCH == 0 || TC::adj_smem_ld > 227 * 1024) {
+      return cudaErrorNotSupported;
+    } else {
+      return launch_tile_one<N, tile_adj_kernel<N, TC::W_L, TC::WMT_L, SCH, 1>>(p, a, 32 * TC::W_L, TC::adj_smem_ld, TC::adj_smem_ld, s);
+    }
+  }
+  return launch_tile_one<N, tile_adj_kernel<N, TC::W_A, TC::WMT_A, SCH, 0>>(p, a, 32 * TC::W_A, TC::adj_smem, TC::adj_smem, s);
+}
+
 // Temporally blocked RK step / adjoint step for large periodic rings (batch 1).
-// kind 0: forward step (H = s), 1: adjoint step (H = 2s - 1).
+// kind 0: forward step (H = s), 1: adjoint step (H = 2s - 1, or s from stored stage states).
+// The tableau (euler / Kutta-3 / RK4) is a template parameter of the kernels.
 template <int N>
 cudaError_t launch_tile_step(const PlanView& p, int kind, TileStepArgs a, cudaStream_t s) {
   if constexpr ((N + 1) % 8 != 0) {
@@ -275,52 +314,12 @@ cudaError_t launch_tile_step(const PlanView& p, int kind, TileStepArgs a, cudaSt
     a.H = (kind == 0 || a.stin[0]) ? a.tab.s : 2 * a.tab.s - 1;
     const int T = (kind == 0 ? TC::TE_F : (a.stin[0] ? TC::TE_L : TC::TE_A)) - 2 * a.H;
     a.ntiles = (int)((p.geo.E + T - 1) / T);
-    const size_t smem = kind == 0 ? TC::fwd_smem : (a.stin[0] ? TC::adj_smem_ld : TC::adj_smem);
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (kind == 0) {
-      auto kern = tile_step_kernel<N, TC::W, TC::WMT_F>;
-      static int per_sm = 0;
-      if (per_sm == 0) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * TC::W, smem);
-        if (per_sm < 1) per_sm = 1;
-      }
-      const int grid = (int)std::min<int64_t>(a.ntiles, (int64_t)per_sm * sms);
-      kern<<<grid, 32 * TC::W, smem, s>>>(*static_cast<const Consts<N>*>(p.consts), p.geo, a);
-    } else {
-      if (a.stin[0]) {
-        if (TC::adj_smem_ld > 227 * 1024) return cudaErrorNotSupported;
-        auto kern = tile_adj_kernel<N, TC::W_L, TC::WMT_L>;
-        static int per_sm = 0;
-        if (per_sm == 0) {
-          cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-          if (e != cudaSuccess) return e;
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * TC::W_L, smem);
-          if (per_sm < 1) per_sm = 1;
-        }
-        const int grid = (int)std::min<int64_t>(a.ntiles, (int64_t)per_sm * sms);
-        kern<<<grid, 32 * TC::W_L, smem, s>>>(*static_cast<const Consts<N>*>(p.consts), p.geo, a);
-      } else {
-        auto kern = tile_adj_kernel<N, TC::W_A, TC::WMT_A>;
-        static int per_sm = 0;
-        if (per_sm == 0) {
-          // same instantiation as the stored-stage variant (degrees other than 7): keep the
-          // limit at the larger of the two sizes so neither launch exceeds it
-          constexpr bool same = TC::W_L == TC::W_A && TC::WMT_L == TC::WMT_A;
-          constexpr size_t lim = (same && TC::adj_smem_ld <= 227 * 1024) ? TC::adj_smem_ld : TC::adj_smem;
-          cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lim);
-          if (e != cudaSuccess) return e;
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * TC::W_A, smem);
-          if (per_sm < 1) per_sm = 1;
-        }
-        const int grid = (int)std::min<int64_t>(a.ntiles, (int64_t)per_sm * sms);
-        kern<<<grid, 32 * TC::W_A, smem, s>>>(*static_cast<const Consts<N>*>(p.consts), p.geo, a);
-      }
+    switch (a.tab.s) {
+      case 1: return launch_tile_sch<N, 0>(p, kind, a, s);
+      case 3: return launch_tile_sch<N, 1>(p, kind, a, s);
+      case 4: return launch_tile_sch<N, 2>(p, kind, a, s);
+      default: return cudaErrorInvalidValue;
     }
-    return cudaGetLastError();
   }
 }
 
