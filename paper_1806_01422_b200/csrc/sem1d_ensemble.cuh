@@ -209,7 +209,8 @@ __device__ __forceinline__ double bfrag_pre(const Consts<N>& C, int mat, int nt,
   return mat == 0 ? __dmul_rn(b, __dmul_rn(-C.nu, mi)) : __dmul_rn(b, mi);
 }
 
-// B fragments of ring_jact<PREJ = true> (tile adjoint steps): dt and M^-1 folded in, so the
+// B fragments of ring_jact<PREJ = true> (tile adjoint steps; the ensemble adjoint passes dt = 1
+// since its dt varies per step): dt and M^-1 folded in, so the
 // stage input z enters unscaled and the row value is already the stage's l contribution:
 // K column j by -nu dt M^-1_j, Dw row i (the z o (Dw u) term) by dt M^-1_i, Dw^T column j
 // by dt M^-1_j (periodic rings: the interface rows/columns take the pattern entry 0)
@@ -226,9 +227,34 @@ __device__ __forceinline__ double bfrag_adj(const Consts<N>& C, int mat, int nt,
   return __dmul_rn(b, __dmul_rn(dt, mj));
 }
 
+// Compile-time Butcher tableaux of the sweep kernels (same values as make_tableau:
+// 0 euler, 1 Kutta-3 of timeloop.py:24-27, 2 classic RK4): with the stage count and
+// coefficients constant the stage loops unroll and every tableau branch folds away
+// (a runtime tableau made integer/branch instructions half of the adjoint step's issue)
+template <int SCH>
+struct TabC {
+  static constexpr int s = SCH == 0 ? 1 : (SCH == 1 ? 3 : 4);
+  __host__ __device__ static constexpr double a(int i, int j) {
+    return SCH == 1 ? ((i == 1 && j == 0) ? 0.5 : (i == 2 && j == 0) ? -1.0 : (i == 2 && j == 1) ? 2.0 : 0.0)
+         : SCH == 2 ? (((i == 1 && j == 0) || (i == 2 && j == 1)) ? 0.5 : (i == 3 && j == 2) ? 1.0 : 0.0)
+                    : 0.0;
+  }
+  __host__ __device__ static constexpr double b(int i) {
+    return SCH == 0 ? 1.0
+         : SCH == 1 ? (i == 1 ? 2.0 / 3.0 : 1.0 / 6.0)
+                    : ((i == 0 || i == 3) ? 1.0 / 6.0 : 1.0 / 3.0);
+  }
+  __host__ __device__ static constexpr int nterm(int i) {
+    int n = 0;
+    for (int j = 0; j < i; ++j) n += a(i, j) != 0.0;
+    return n;
+  }
+  __host__ __device__ static constexpr int keep(int j) { return (SCH == 1 && j == 0) ? 1 : 0; }
+};
+
 // Forward sweep of one ring per CTA: periodic rings, E a multiple of 8 with
 // E/8 <= 8 * WMT_MAX.  Trajectory state n+1 is written after step n.
-template <int N, int WMT_MAX, bool ILV>
+template <int N, int WMT_MAX, bool ILV, int SCH>
 __global__ void __launch_bounds__(EnsCfg<N, ens_fwd_warps<N>()>::THREADS, 1)
     ens_forward_kernel(const __grid_constant__ Consts<N> C, const Geo G, const EnsArgs A) {
   constexpr int n = N + 1, KC = EnsCfg<N>::KC, NT = EnsCfg<N>::NT;
@@ -245,6 +271,7 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_fwd_warps<N>()>::THREADS, 1)
   const int64_t b = blockIdx.x;
   const double* u0 = A.u0 + b * G.ndof;
   const double mnu = -C.nu;
+  using TB = TabC<SCH>;                       // compile-time tableau: stage loop unrolls
 
   double breg[2 * NT * KC];
 #pragma unroll
@@ -277,7 +304,8 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_fwd_warps<N>()>::THREADS, 1)
   double kv[WMT_MAX][KC];
   for (int step = 0; step < A.nsteps; ++step) {
     const double dt = A.dts[step];
-    for (int i = 0; i < A.tab.s; ++i) {
+#pragma unroll
+    for (int i = 0; i < TB::s; ++i) {
       const double* src = (i == 0) ? su : sU;
       ring_rhs<N, WMT_MAX, decltype(bget), true, TILE_PRE != 0, ILV>(C, G, src, xfer, bget, minv_a, mnu, warp, lane, kv,
                                                                fin);
@@ -294,26 +322,27 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_fwd_warps<N>()>::THREADS, 1)
           const int g = e * N + j;
           const double kk = kv[q][kc];
           // acc = b0 k0 + b1 k1 + ... left to right (timeloop.py:127)
-          const double term = __dmul_rn(A.tab.b[i], kk);
+          const double term = __dmul_rn(TB::b(i), kk);
           acc[q][kc] = (i == 0) ? term : __dadd_rn(acc[q][kc], term);
-          if (i + 1 < A.tab.s) {
+          if (i + 1 < TB::s) {
             double y;
-            if (A.tab.nterm[i + 1] == 1) {
+            if (TB::nterm(i + 1) == 1) {
               // single term: u + (dt * a) * k  (timeloop.py:114)
-              y = __dadd_rn(su[g], __dmul_rn(__dmul_rn(dt, A.tab.a[i + 1][i]), kk));
+              y = __dadd_rn(su[g], __dmul_rn(__dmul_rn(dt, TB::a(i + 1, i)), kk));
             } else {
               // u + dt * (a0 k0 + a1 k1)  (timeloop.py:116)
-              double sacc = __dmul_rn(A.tab.a[i + 1][0], (i == 0) ? kk : sk[g]);
+              double sacc = __dmul_rn(TB::a(i + 1, 0), (i == 0) ? kk : sk[g]);
+#pragma unroll
               for (int jj = 1; jj <= i; ++jj)
-                sacc = __dadd_rn(sacc, __dmul_rn(A.tab.a[i + 1][jj], (jj == i) ? kk : sk[g]));
+                sacc = __dadd_rn(sacc, __dmul_rn(TB::a(i + 1, jj), (jj == i) ? kk : sk[g]));
               y = __dadd_rn(su[g], __dmul_rn(dt, sacc));
             }
             sU[g] = y;
             if (g == 0) sU[ndof] = y;
-            if (i == 0 && A.tab.keep[0]) sk[g] = kk;
+            if (i == 0 && TB::keep(0)) sk[g] = kk;
           } else {
             const double un = __dadd_rn(su[g], __dmul_rn(dt, acc[q][kc]));
-            bad_step |= !isfinite(un);
+            bad_step |= nonfinite_bit(un) != 0u;
             su[g] = un;
             if (g == 0) su[ndof] = un;
           }
@@ -422,7 +451,7 @@ struct EnsAdjArgs {
 // shared memory): stage states recomputed from the stored u_n (s-1 F applies), then
 // l_i = dt J^T(U_i)(b_i lam + sum_{j>i} a_ji l_j) for i = s-1..0 and
 // lam <- lam + (l_{s-1} + ... + l_0).
-template <int N, int WMT_MAX, bool ILV>
+template <int N, int WMT_MAX, bool ILV, int SCH>
 __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
     ens_adjoint_kernel(const __grid_constant__ Consts<N> C, const Geo G, const EnsAdjArgs A) {
   constexpr int KC = EnsCfg<N>::KC, NT = EnsCfg<N>::NT;
@@ -430,7 +459,8 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
   extern __shared__ __align__(16) double smem[];
   const int ndof = (int)G.ndof;
   const int pad = (ndof + 2 + 1) & ~1;
-  const int S = A.tab.s;
+  using TB = TabC<SCH>;                       // compile-time tableau: stage loops unroll
+  constexpr int S = TB::s;
   double* su = smem;                          // u_n (= U_0)
   double* sUs = su + pad;                     // U_1 .. U_{S-1}: S-1 arrays
   double* sk = sUs + 3 * pad;                 // k_0 (RK3 recompute) / an older l (RK3 chain)
@@ -453,7 +483,7 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
   if constexpr (BSM) {
     for (int q = tid; q < 5 * NT * KC * 32; q += THREADS) {
       const int l = q & 31, f = q >> 5, kc = f % KC, nt = (f / KC) % NT, mat = f / (KC * NT);
-      sB[q] = mat < 3 ? bfrag_perm<N>(C, mat, nt, kc, l)
+      sB[q] = mat < 3 ? bfrag_adj<N>(C, mat, nt, kc, l, 1.0)
                       : (TILE_PRE ? bfrag_pre<N>(C, mat - 3, nt, kc, l) : bfrag_perm<N>(C, mat - 3, nt, kc, l));
     }
   } else {
@@ -462,7 +492,7 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
-        for (int kc = 0; kc < KC; ++kc) breg[(mat * NT + nt) * KC + kc] = bfrag_perm<N>(C, mat, nt, kc, lane);
+        for (int kc = 0; kc < KC; ++kc) breg[(mat * NT + nt) * KC + kc] = bfrag_adj<N>(C, mat, nt, kc, lane, 1.0);
     if (TILE_PRE) {
 #pragma unroll
       for (int mat = 0; mat < 2; ++mat)
@@ -500,6 +530,7 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
     if (tid == 0) su[ndof] = un[0];
     __syncthreads();
     // ---- stage states U_1..U_{S-1} (timeloop.rk3_stages, adjoint.py:56)
+#pragma unroll
     for (int i = 0; i + 1 < S; ++i) {
       ring_rhs<N, WMT_MAX, decltype(bpget), true, TILE_PRE != 0, ILV>(C, G, Uarr(i), xfer, bpget, minv_a, mnu, warp,
                                                                 lane, kv, fin);
@@ -515,44 +546,51 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
           const int g = ring_elem<WMT_MAX, ILV>(warp, q, rr) * N + j;
           const double kk = kv[q][kc];
           double y;
-          if (A.tab.nterm[i + 1] == 1) {
-            y = __dadd_rn(su[g], __dmul_rn(__dmul_rn(dt, A.tab.a[i + 1][i]), kk));
+          if (TB::nterm(i + 1) == 1) {
+            y = __dadd_rn(su[g], __dmul_rn(__dmul_rn(dt, TB::a(i + 1, i)), kk));
           } else {
-            double sacc = __dmul_rn(A.tab.a[i + 1][0], (i == 0) ? kk : sk[g]);
+            double sacc = __dmul_rn(TB::a(i + 1, 0), (i == 0) ? kk : sk[g]);
+#pragma unroll
             for (int jj = 1; jj <= i; ++jj)
-              sacc = __dadd_rn(sacc, __dmul_rn(A.tab.a[i + 1][jj], (jj == i) ? kk : sk[g]));
+              sacc = __dadd_rn(sacc, __dmul_rn(TB::a(i + 1, jj), (jj == i) ? kk : sk[g]));
             y = __dadd_rn(su[g], __dmul_rn(dt, sacc));
           }
           dst[g] = y;
           if (g == 0) dst[ndof] = y;
-          if (i == 0 && A.tab.keep[0]) sk[g] = kk;
+          if (i == 0 && TB::keep(0)) sk[g] = kk;
         }
       }
       __syncthreads();
     }
-    // ---- stage-adjoint chain, i = S-1 .. 0
-    for (int i = S - 1; i >= 0; --i) {
+    // ---- stage-adjoint chain, i = S-1 .. 0 (M^-1 and -nu ride on the J^T fragments, so z
+    // enters unscaled); z_i = b_i lam + a_{i+1,i} l_{i+1} + a_{i+2,i} l_{i+2} (adjoint.py:58-60)
+    auto zval = [&](int i, int g, int q, int kc) -> double {
+      double z = __dmul_rn(TB::b(i), slam[g]);
+      if (i + 1 < S && TB::a(i + 1, i) != 0.0) z = __dadd_rn(z, __dmul_rn(TB::a(i + 1, i), lnext[q][kc]));
+      if (i + 2 < S && TB::a(i + 2, i) != 0.0) z = __dadd_rn(z, __dmul_rn(TB::a(i + 2, i), sk[g]));
+      return z;
+    };
 #pragma unroll
-      for (int q = 0; q < WMT_MAX; ++q) {
-        const int mt = warp * WMT_MAX + q;
-        if (mt >= mt_total) break;
+    for (int q = 0; q < WMT_MAX; ++q) {
+      const int mt = warp * WMT_MAX + q;
+      if (mt >= mt_total) break;
 #pragma unroll
-        for (int kc = 0; kc < KC; ++kc) {
-          const int j = 4 * kc + kq;
-          if (j == N) continue;
-          const int g = ring_elem<WMT_MAX, ILV>(warp, q, rr) * N + j;
-          // z = b_i lam + a_{i+1,i} l_{i+1} + a_{i+2,i} l_{i+2} (adjoint.py:58-60)
-          double z = __dmul_rn(A.tab.b[i], slam[g]);
-          if (i + 1 < S && A.tab.a[i + 1][i] != 0.0) z = __dadd_rn(z, __dmul_rn(A.tab.a[i + 1][i], lnext[q][kc]));
-          if (i + 2 < S && A.tab.a[i + 2][i] != 0.0) z = __dadd_rn(z, __dmul_rn(A.tab.a[i + 2][i], sk[g]));
-          fin |= nonfinite_bit(z);
-          const double zm = __dmul_rn(z, minv_a[kc]);
-          sz[g] = zm;
-          if (g == 0) sz[ndof] = zm;
-        }
+      for (int kc = 0; kc < KC; ++kc) {
+        const int j = 4 * kc + kq;
+        if (j == N) continue;
+        const int g = ring_elem<WMT_MAX, ILV>(warp, q, rr) * N + j;
+        const double z = zval(S - 1, g, q, kc);
+        fin |= nonfinite_bit(z);
+        sz[g] = z;
+        if (g == 0) sz[ndof] = z;
       }
-      __syncthreads();
-      ring_jact<N, WMT_MAX, decltype(bget), true, ILV>(C, G, Uarr(i), sz, xfer, bget, mnu, warp, lane, kv);
+    }
+    __syncthreads();
+    // per stage: J^T apply (its internal barrier ends every read of sz), then accumulate
+    // l_i and form z_{i-1} in one pass -- two barriers per stage
+#pragma unroll
+    for (int i = S - 1; i >= 0; --i) {
+      ring_jact<N, WMT_MAX, decltype(bget), true, ILV, true>(C, G, Uarr(i), sz, xfer, bget, mnu, warp, lane, kv);
 #pragma unroll
       for (int q = 0; q < WMT_MAX; ++q) {
         const int mt = warp * WMT_MAX + q;
@@ -566,7 +604,14 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
           lacc[q][kc] = (i == S - 1) ? l : __dadd_rn(lacc[q][kc], l);
           if (i + 1 < S && S == 3) sk[g] = lnext[q][kc];   // RK3: keep l_{i+1} for z_{i-1}
           lnext[q][kc] = l;
-          if (i == 0) slam[g] = __dadd_rn(slam[g], lacc[q][kc]);
+          if (i == 0) {
+            slam[g] = __dadd_rn(slam[g], lacc[q][kc]);
+          } else {
+            const double z = zval(i - 1, g, q, kc);
+            fin |= nonfinite_bit(z);
+            sz[g] = z;
+            if (g == 0) sz[ndof] = z;
+          }
         }
       }
       __syncthreads();
@@ -692,31 +737,6 @@ constexpr int tile_minb() { return (N + 1) == 8 ? TILE_MINB8 : 1; }
 #endif
 template <int N, int MODE = 0>
 constexpr int tile_adj_minb() { return (N + 1) == 8 ? (MODE == 1 ? TILE_ADJ_LD_MINB8 : TILE_ADJ_MINB8) : 1; }
-
-// Compile-time Butcher tableaux of the tile-step kernels (same values as make_tableau:
-// 0 euler, 1 Kutta-3 of timeloop.py:24-27, 2 classic RK4): with the stage count and
-// coefficients constant the stage loops unroll and every tableau branch folds away
-// (a runtime tableau made integer/branch instructions half of the adjoint step's issue)
-template <int SCH>
-struct TabC {
-  static constexpr int s = SCH == 0 ? 1 : (SCH == 1 ? 3 : 4);
-  __host__ __device__ static constexpr double a(int i, int j) {
-    return SCH == 1 ? ((i == 1 && j == 0) ? 0.5 : (i == 2 && j == 0) ? -1.0 : (i == 2 && j == 1) ? 2.0 : 0.0)
-         : SCH == 2 ? (((i == 1 && j == 0) || (i == 2 && j == 1)) ? 0.5 : (i == 3 && j == 2) ? 1.0 : 0.0)
-                    : 0.0;
-  }
-  __host__ __device__ static constexpr double b(int i) {
-    return SCH == 0 ? 1.0
-         : SCH == 1 ? (i == 1 ? 2.0 / 3.0 : 1.0 / 6.0)
-                    : ((i == 0 || i == 3) ? 1.0 / 6.0 : 1.0 / 3.0);
-  }
-  __host__ __device__ static constexpr int nterm(int i) {
-    int n = 0;
-    for (int j = 0; j < i; ++j) n += a(i, j) != 0.0;
-    return n;
-  }
-  __host__ __device__ static constexpr int keep(int j) { return (SCH == 1 && j == 0) ? 1 : 0; }
-};
 
 // MODE 0: plain step; 1: also store the stage states U_1..U_{s-1} (north_star item 4)
 template <int N, int W, int WMT, int SCH, int MODE>

@@ -230,7 +230,10 @@ cudaError_t launch_ens_adjoint(const PlanView& p, const EnsAdjArgs& a, cudaStrea
     const size_t smem = ens_adj_smem_bytes<N>((int)p.geo.ndof);
     if (p.geo.periodic && p.geo.E % 8 == 0 && p.geo.E / 8 <= W * WMT && smem <= 227 * 1024 &&
         p.geo.E * (N + 1) > 1024) {
-      auto kern = (ENS_ILV && p.geo.E % (8 * WMT) == 0) ? ens_adjoint_kernel<N, WMT, true> : ens_adjoint_kernel<N, WMT, false>;
+      const bool ilv = ENS_ILV && p.geo.E % (8 * WMT) == 0;
+      auto kern = a.tab.s == 4 ? (ilv ? ens_adjoint_kernel<N, WMT, true, 2> : ens_adjoint_kernel<N, WMT, false, 2>)
+                : a.tab.s == 3 ? (ilv ? ens_adjoint_kernel<N, WMT, true, 1> : ens_adjoint_kernel<N, WMT, false, 1>)
+                               : (ilv ? ens_adjoint_kernel<N, WMT, true, 0> : ens_adjoint_kernel<N, WMT, false, 0>);
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       kern<<<(unsigned)p.batch, EnsCfg<N, W>::THREADS, smem, s>>>(
@@ -250,7 +253,10 @@ cudaError_t launch_ens_forward(const PlanView& p, const EnsArgs& a, cudaStream_t
     const size_t smem = ens_smem_bytes<N>((int)p.geo.ndof);
     if (p.geo.periodic && p.geo.E % 8 == 0 && p.geo.E / 8 <= W * WMT && smem <= 220 * 1024 &&
         p.geo.E * (N + 1) > 1024) {
-      auto kern = (ENS_ILV && p.geo.E % (8 * WMT) == 0) ? ens_forward_kernel<N, WMT, true> : ens_forward_kernel<N, WMT, false>;
+      const bool ilv = ENS_ILV && p.geo.E % (8 * WMT) == 0;
+      auto kern = a.tab.s == 4 ? (ilv ? ens_forward_kernel<N, WMT, true, 2> : ens_forward_kernel<N, WMT, false, 2>)
+                : a.tab.s == 3 ? (ilv ? ens_forward_kernel<N, WMT, true, 1> : ens_forward_kernel<N, WMT, false, 1>)
+                               : (ilv ? ens_forward_kernel<N, WMT, true, 0> : ens_forward_kernel<N, WMT, false, 0>);
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       kern<<<(unsigned)p.batch, EnsCfg<N, W>::THREADS, smem, s>>>(
