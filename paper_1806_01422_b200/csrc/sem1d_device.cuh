@@ -915,14 +915,14 @@ typedef double ws_fin_t;
 #ifndef WS_ELEMS8
 #define WS_ELEMS8 256
 #endif
-// n = 32: consumer warps per operator (A/B, config 3): F and J run 8 warps x 2 m-tiles
-// with each shared-memory B fragment feeding both (mtile_compute_multi: 60.7 / 80.0 us vs
-// 63.0 / 82.3 us at 16 x 1); J^T keeps 16 x 1 (96.4 vs 94.3 us)
+// n = 32: consumer warps per operator (A/B, config 3): 8 warps x 2 interleaved m-tiles with
+// each shared-memory B fragment feeding both (mtile_compute_multi): F / J 55.4 / 73.8 us
+// (63.0 / 82.3 at 16 x 1), J^T 90.1 us (97.4 at 16 x 1, which spilled at the 96-register cap)
 #ifndef WS_CW32
 #define WS_CW32 8
 #endif
 #ifndef WS_CW32_JT
-#define WS_CW32_JT 16
+#define WS_CW32_JT 8
 #endif
 #ifndef WS_ELEMS32
 #define WS_ELEMS32 128
@@ -1054,12 +1054,33 @@ __device__ __forceinline__ void mtile_compute(const Consts<N>& C, const Geo& G, 
   }
 }
 
-// Q m-tiles of one warp at once (elements base0/eg0 + 8q): the loops over the output
+#ifndef WS_ILV
+#define WS_ILV 1
+#endif
+// Warp-local element held by row rr of m-tile q (apply_ws_kernel).  ILV (WMT = 2 or 4):
+// interleaved rows, so the 64-bit slab loads/stores of a half-warp (rows 4h..4h+3, nodes
+// N*e + kq) hit 16 distinct banks for odd N -- the half-warp's elements are congruent mod 4
+// and distinct mod 16 (the contiguous mapping puts rows N apart: 4-way conflicts at N = 31).
+// Same mapping as ring_elem of the sweep kernels.
+template <int WMT, bool ILV>
+__device__ __forceinline__ int ws_le(int q, int rr) {
+  if constexpr (ILV && WMT == 2) return 4 * (rr & 3) + 2 * (rr >> 2) + q;
+  else if constexpr (ILV && WMT == 4) return 4 * rr + q;
+  else return 8 * q + rr;
+}
+// ILV: row of m-tile WMT-1 holding the left neighbour of (rr > 0, m-tile 0)
+template <int WMT>
+__device__ __forceinline__ int ws_left_row(int rr) {
+  if constexpr (WMT == 2) return rr >= 4 ? rr - 4 : rr + 3;
+  else return rr > 0 ? rr - 1 : 0;
+}
+
+// Q m-tiles of one warp at once (elements wbase/weg + ws_le(q, rr)): the loops over the output
 // n-tiles and k-chunks are outermost, so each B fragment -- read from shared memory when
 // the n x n matrices do not fit the register file (n = 32) -- feeds Q DMMAs instead of one.
-template <int N, int OP, bool EDGE, int Q, class BGet>
+template <int N, int OP, bool EDGE, int Q, bool ILV, class BGet>
 __device__ __forceinline__ void mtile_compute_multi(const Consts<N>& C, const Geo& G, const double* su,
-                                                    const double* sw, int base0, int64_t eg0,
+                                                    const double* sw, int wbase, int64_t weg, int rr,
                                                     const double* minv_a, double mnu, int kq, BGet bget,
                                                     ws_fin_t& fin_u, ws_fin_t& fin_w,
                                                     double (&r)[Q][(N + 1) / 8][2]) {
@@ -1067,8 +1088,9 @@ __device__ __forceinline__ void mtile_compute_multi(const Consts<N>& C, const Ge
   double au[Q][KC], aw[Q][(OP != OP_RHS) ? KC : 1], at[Q][(OP == OP_JACT) ? KC : 1];
 #pragma unroll
   for (int q = 0; q < Q; ++q) {
-    const int64_t eg = eg0 + 8 * q;
-    const int base = base0 + 8 * q * N;
+    const int le = ws_le<Q, ILV>(q, rr);
+    const int64_t eg = weg + le;
+    const int base = wbase + le * N;
     const bool eslow = EDGE && (eg == 0 || eg == G.E - 1);
 #pragma unroll
     for (int kc = 0; kc < KC; ++kc) {
@@ -1325,27 +1347,42 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
       auto body = [&](auto edge_tag) {
         constexpr bool EDGE = decltype(edge_tag)::value;
         constexpr bool MULTI = W::B_IN_SMEM && (WMT > 1);
-        [[maybe_unused]] double rq[MULTI ? WMT : 1][NT][2];
-        if constexpr (MULTI)
-          mtile_compute_multi<N, OP, EDGE, WMT>(C, G, su, sw, (wel0 + rr + 1) * N, e0 + wel0 + rr, minv_a,
-                                                mnu, kq, bget, fin_u, fin_w, rq);
+        // interleaved rows: A/B (config 2 / 3) F 86.5 -> 85.3 us, J 111.9 -> 111.0 (n = 8);
+        // F 59.9 -> 55.4, J 77.9 -> 73.8 (n = 32); J^T at n = 8 measured slower (126.9 vs 112.2)
+        constexpr bool ILVW = WS_ILV && (WMT == 2 || WMT == 4) && !(OP == OP_JACT && N == 7);
+        double rq[WMT][NT][2];
+        if constexpr (MULTI) {
+          mtile_compute_multi<N, OP, EDGE, WMT, ILVW>(C, G, su, sw, (wel0 + 1) * N, e0 + wel0, rr, minv_a,
+                                                      mnu, kq, bget, fin_u, fin_w, rq);
+        } else {
+#pragma unroll
+          for (int q = 0; q < WMT; ++q) {
+            const int le = ws_le<WMT, ILVW>(q, rr);
+            mtile_compute<N, OP, EDGE>(C, G, su, sw, (wel0 + le + 1) * N, e0 + wel0 + le, minv_a, minv_p, mnu, kq,
+                                       bget, fin_u, fin_w, rq[q]);
+          }
+        }
+        // interface value of element le's node 0 (v = left row N + own row 0, or row 0 alone
+        // for the warp's first element until the halo arrives): M^-1 / Dirichlet mask, staged
+        auto put_row0 = [&](int le, bool first, double left, double row0) {
+          const int64_t eg = e0 + wel0 + le;
+          double v = first ? row0 : __dadd_rn(left, row0);
+          if (!first) {
+            if (EDGE && eg == 0) {
+              if (OP != OP_JACT) v = __dmul_rn(v, C.minv[N]);
+              v = __dmul_rn(v, 0.0);
+            } else if (OP != OP_JACT) {
+              v = __dmul_rn(v, minv_if);
+            }
+          }
+          wout[le * N] = v;
+        };
 #pragma unroll
         for (int q = 0; q < WMT; ++q) {
-          const int le = 8 * q + rr;                // warp-local element of this lane
+          const int le = ws_le<WMT, ILVW>(q, rr);    // warp-local element of this lane
           const bool live = le < wnel;
           const int64_t eg = e0 + wel0 + le;
-          [[maybe_unused]] const int base = (wel0 + le + 1) * N;
-          double r[NT][2];
-          if constexpr (MULTI) {
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-              r[nt][0] = rq[q][nt][0];
-              r[nt][1] = rq[q][nt][1];
-            }
-          } else {
-            mtile_compute<N, OP, EDGE>(C, G, su, sw, base, eg, minv_a, minv_p, mnu, kq, bget,
-                                       fin_u, fin_w, r);
-          }
+          const double (&r)[NT][2] = rq[q];
           // interior rows -> staging; rows 0 and N stay in registers
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt)
@@ -1355,27 +1392,29 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
               if (live && i != 0 && i != N)
                 wout[le * N + i] = (OP == OP_JACT) ? r[nt][h] : __dmul_rn(r[nt][h], minv_a[2 * nt + h]);
             }
-          const double row0 = r[0][0];              // valid in lanes kq == 0
-          const double rowN = r[NT - 1][1];         // valid in lanes kq == 3
-          double left = __shfl_up_sync(0xffffffffu, rowN, 1);
-          if (rr == 0) left = carry;                // q == 0: patched after the halo arrives
-          carry = __shfl_sync(0xffffffffu, rowN, 31);
-          if (kq == 0 && live) {
-            double v = (q == 0 && rr == 0) ? row0 : __dadd_rn(left, row0);
-            if (!(q == 0 && rr == 0)) {
-              if (EDGE && eg == 0) {
-                if (OP != OP_JACT) v = __dmul_rn(v, C.minv[N]);
-                v = __dmul_rn(v, 0.0);
-              } else if (OP != OP_JACT) {
-                v = __dmul_rn(v, minv_if);
-              }
-            }
-            wout[le * N] = v;
+          if constexpr (!ILVW) {
+            const double row0 = r[0][0];              // valid in lanes kq == 0
+            const double rowN = r[NT - 1][1];         // valid in lanes kq == 3
+            double left = __shfl_up_sync(0xffffffffu, rowN, 1);
+            if (rr == 0) left = carry;                // q == 0: patched after the halo arrives
+            carry = __shfl_sync(0xffffffffu, rowN, 31);
+            if (kq == 0 && live) put_row0(le, q == 0 && rr == 0, left, row0);
           }
           if (EDGE && kq == 3 && live && eg == G.E - 1) {  // Dirichlet end node E*N
-            double v = rowN;
+            double v = r[NT - 1][1];
             if (OP != OP_JACT) v = __dmul_rn(v, C.minv[N + 1]);
             wout[(le + 1) * N] = __dmul_rn(v, 0.0);
+          }
+        }
+        if constexpr (ILVW) {
+          // left neighbour of (q, rr): (q-1, rr) in lane 4rr+3; of (0, rr > 0): m-tile WMT-1
+          // of row ws_left_row(rr); (0, 0) is the warp's first element (halo)
+#pragma unroll
+          for (int q = 0; q < WMT; ++q) {
+            const double left = q > 0 ? __shfl_down_sync(0xffffffffu, rq[q - 1][NT - 1][1], 3)
+                                      : __shfl_sync(0xffffffffu, rq[WMT - 1][NT - 1][1], 4 * ws_left_row<WMT>(rr) + 3);
+            const int le = ws_le<WMT, ILVW>(q, rr);
+            if (kq == 0 && le < wnel) put_row0(le, q == 0 && rr == 0, left, rq[q][0][0]);
           }
         }
       };
