@@ -1057,6 +1057,11 @@ __device__ __forceinline__ void mtile_compute(const Consts<N>& C, const Geo& G, 
 #ifndef WS_ILV
 #define WS_ILV 1
 #endif
+// n = 32: output n-tiles per accumulation group in mtile_compute_multi (A/B on config 3:
+// 1 / 2 / 4 -> J^T 90.0 / 88.3 / 88.0 us, F and J flat within 0.3%; 4 slowed J to 75.8 us)
+#ifndef WS_NTG
+#define WS_NTG 2
+#endif
 // Warp-local element held by row rr of m-tile q (apply_ws_kernel).  ILV (WMT = 2 or 4):
 // interleaved rows, so the 64-bit slab loads/stores of a half-warp (rows 4h..4h+3, nodes
 // N*e + kq) hit 16 distinct banks for odd N -- the half-warp's elements are congruent mod 4
@@ -1107,31 +1112,42 @@ __device__ __forceinline__ void mtile_compute_multi(const Consts<N>& C, const Ge
       }
     }
   }
+  // NTG output n-tiles at a time: NTG x Q x (2 or 3) independent accumulator chains per warp
+  // hide the DMMA -> DMMA latency of the k-chunk chains
+  constexpr int NTG = (NT % WS_NTG == 0) ? WS_NTG : 1;
 #pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    double k[Q][2], p[Q][2], qq[Q][2];
+  for (int nt0 = 0; nt0 < NT; nt0 += NTG) {
+    double k[NTG][Q][2], p[NTG][Q][2], qq[NTG][Q][2];
 #pragma unroll
-    for (int q = 0; q < Q; ++q) k[q][0] = k[q][1] = p[q][0] = p[q][1] = qq[q][0] = qq[q][1] = 0.0;
+    for (int g = 0; g < NTG; ++g)
+#pragma unroll
+      for (int q = 0; q < Q; ++q) k[g][q][0] = k[g][q][1] = p[g][q][0] = p[g][q][1] = qq[g][q][0] = qq[g][q][1] = 0.0;
 #pragma unroll
     for (int kc = 0; kc < KC; ++kc) {
-      const double b0 = bget(0, nt, kc), b1 = bget(1, nt, kc);
-      const double b2 = (OP == OP_JACT) ? bget(2, nt, kc) : 0.0;
 #pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        dmma884(k[q][0], k[q][1], (OP == OP_RHS) ? au[q][kc] : aw[q][kc], b0);
-        dmma884(p[q][0], p[q][1], au[q][kc], b1);
-        if (OP == OP_JAC) dmma884(qq[q][0], qq[q][1], aw[q][kc], b1);
-        if (OP == OP_JACT) dmma884(qq[q][0], qq[q][1], at[q][kc], b2);
+      for (int g = 0; g < NTG; ++g) {
+        const int nt = nt0 + g;
+        const double b0 = bget(0, nt, kc), b1 = bget(1, nt, kc);
+        const double b2 = (OP == OP_JACT) ? bget(2, nt, kc) : 0.0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          dmma884(k[g][q][0], k[g][q][1], (OP == OP_RHS) ? au[q][kc] : aw[q][kc], b0);
+          dmma884(p[g][q][0], p[g][q][1], au[q][kc], b1);
+          if (OP == OP_JAC) dmma884(qq[g][q][0], qq[g][q][1], aw[q][kc], b1);
+          if (OP == OP_JACT) dmma884(qq[g][q][0], qq[g][q][1], at[q][kc], b2);
+        }
       }
     }
 #pragma unroll
-    for (int q = 0; q < Q; ++q)
+    for (int g = 0; g < NTG; ++g)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int kcp = 2 * nt + h;
-        const double wi = (OP == OP_RHS) ? 0.0 : aw[q][kcp];
-        r[q][nt][h] = combine_rows<N, OP>(k[q][h], p[q][h], qq[q][h], au[q][kcp], wi, mnu);
-      }
+      for (int q = 0; q < Q; ++q)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int kcp = 2 * (nt0 + g) + h;
+          const double wi = (OP == OP_RHS) ? 0.0 : aw[q][kcp];
+          r[q][nt0 + g][h] = combine_rows<N, OP>(k[g][q][h], p[g][q][h], qq[g][q][h], au[q][kcp], wi, mnu);
+        }
   }
 }
 
