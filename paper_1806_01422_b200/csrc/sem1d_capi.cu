@@ -6,6 +6,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -43,6 +44,12 @@ struct sem1d_plan {
   int adv = 0;                 // 0 Burgers, 1 linear (constant speed), 2 none (ops.py:147-212)
   double speed = 0.0;
   double* dconst = nullptr;    // advection kinds: device K[n*n], Dw[n*n], minv[N+2]
+  // tensor-core apply kernels (N+1 % 8 == 0): the permuted B-fragment table
+  // [K, Dw, Dw^T][n/8][n/4][32 lanes] in device memory, built on first use, so a kernel
+  // prologue is a coalesced copy instead of lane-divergent kernel-parameter reads
+  mutable double* dfrag = nullptr;
+  mutable std::once_flag frag_once;
+  mutable cudaError_t frag_err = cudaSuccess;
 };
 
 namespace {
@@ -72,9 +79,43 @@ int cuda_fail(cudaError_t e, const char* where) {
   return fail(SEM1D_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
+// Host image of bfrag_perm (sem1d_device.cuh) for every (mat, nt, kc, lane): a permutation of
+// K / Dw entries, so the device table is bit-identical to the in-kernel construction.
+cudaError_t ensure_frag(const sem1d_plan* p) {
+  const int n = p->N + 1;
+  if (n % 8 != 0) return cudaSuccess;
+  std::call_once(p->frag_once, [p, n]() {
+    const int NT = n / 8, KC = n / 4;
+    const double* K = p->packed.data();
+    const double* Dw = K + n * n;
+    std::vector<double> h((size_t)3 * NT * KC * 32);
+    for (int mat = 0; mat < 3; ++mat)
+      for (int nt = 0; nt < NT; ++nt)
+        for (int kc = 0; kc < KC; ++kc)
+          for (int l = 0; l < 32; ++l) {
+            const int c = 8 * nt + (l >> 2);
+            const int i = 4 * (2 * (c >> 3) + (c & 1)) + ((c >> 1) & 3);
+            const int j = 4 * kc + (l & 3);
+            h[(((size_t)mat * NT + nt) * KC + kc) * 32 + l] =
+                mat == 0 ? K[i * n + j] : (mat == 1 ? Dw[i * n + j] : Dw[j * n + i]);
+          }
+    double* d = nullptr;
+    cudaError_t e = cudaMalloc(&d, sizeof(double) * h.size());
+    if (e == cudaSuccess) e = cudaMemcpy(d, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess && d) {
+      cudaFree(d);
+      d = nullptr;
+    }
+    p->frag_err = e;
+    p->dfrag = d;
+  });
+  return p->frag_err;
+}
+
 PlanView view(const sem1d_plan* p) {
   PlanView v;
   v.consts = p->packed.data();
+  v.frag = p->dfrag;
   v.geo.E = p->E;
   v.geo.ndof = p->ndof;
   v.geo.periodic = p->periodic;
@@ -83,6 +124,8 @@ PlanView view(const sem1d_plan* p) {
 }
 
 cudaError_t dispatch(const sem1d_plan* p, int kind, const Args& a, cudaStream_t s) {
+  cudaError_t fe = ensure_frag(p);
+  if (fe != cudaSuccess) return fe;
   const PlanView v = view(p);
   switch (p->N) {
 #define SEM_CASE(NN) \
@@ -468,6 +511,7 @@ int sem1d_plan_create(int64_t n_elements, int degree, int periodic, double nu, c
 
 int sem1d_plan_destroy(sem1d_plan* plan) {
   if (plan && plan->dconst) cudaFree(plan->dconst);
+  if (plan && plan->dfrag) cudaFree(plan->dfrag);
   delete plan;
   return SEM1D_OK;
 }

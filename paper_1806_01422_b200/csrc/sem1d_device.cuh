@@ -1154,7 +1154,7 @@ __device__ __forceinline__ void mtile_compute_multi(const Consts<N>& C, const Ge
 template <int N, int OP, int EPI, int STAGES>
 __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
     apply_ws_kernel(const __grid_constant__ Consts<N> C, const Geo G, const Args A,
-                    const int tiles_per_ring, const int total_tiles) {
+                    const int tiles_per_ring, const int total_tiles, const double* __restrict__ frag) {
   using W = WsTile<N, OP>;
   constexpr int ELEMS = W::ELEMS, WE = W::WE, WMT = W::WMT, NT = W::NT, KC = W::KC;
   constexpr int NIN = (OP == OP_RHS) ? 1 : 2;
@@ -1174,11 +1174,18 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
   const int warp = tid >> 5;
   const bool periodic = G.periodic != 0;
 
+  // B fragments: a coalesced copy of the plan's device table (bfrag_perm order; J^T's Dw^T
+  // table follows Dw's), else built from kernel-parameter space (lane-divergent reads: 13% of
+  // the stall samples of the config-3 F kernel)
   if (W::B_IN_SMEM) {
     for (int q = tid; q < NMAT * NT * KC * 32; q += W::THREADS) {
-      const int l = q & 31, r = q >> 5;
-      const int kc = r % KC, nt = (r / KC) % NT, mat = r / (KC * NT);
-      bsm[q] = bfrag_perm<N>(C, mat, nt, kc, l);
+      if (frag) {
+        bsm[q] = __ldg(frag + q);
+      } else {
+        const int l = q & 31, r = q >> 5;
+        const int kc = r % KC, nt = (r / KC) % NT, mat = r / (KC * NT);
+        bsm[q] = bfrag_perm<N>(C, mat, nt, kc, l);
+      }
     }
   }
   if (tid == 0) {
@@ -1200,7 +1207,8 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
       for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
         for (int kc = 0; kc < KC; ++kc)
-          breg[(mat * NT + nt) * KC + kc] = bfrag_perm<N>(C, mat, nt, kc, lane);
+          breg[(mat * NT + nt) * KC + kc] =
+              frag ? __ldg(frag + ((mat * NT + nt) * KC + kc) * 32 + lane) : bfrag_perm<N>(C, mat, nt, kc, lane);
   }
   auto bget = [&](int mat, int nt, int kc) -> double {
     if (W::B_IN_SMEM) return bsm[((mat * NT + nt) * KC + kc) * 32 + lane];

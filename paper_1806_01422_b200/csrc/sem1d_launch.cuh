@@ -20,6 +20,7 @@ int sem1d_path_override();
 
 struct PlanView {
   const void* consts;  // Consts<N>, packed by the plan
+  const double* frag;  // n % 8 == 0: device B-fragment table (bfrag_perm order), or null
   Geo geo;
   int64_t batch;
 };
@@ -122,7 +123,7 @@ static cudaError_t launch_ws(const PlanView& p, const Args& a, cudaStream_t s) {
     if (total > 0x7fffffffLL) return cudaErrorInvalidValue;
     const int grid = (int)(total < max_resident ? total : max_resident);
     kern<<<grid, WsTile<N, OP>::THREADS, smem, s>>>(*static_cast<const Consts<N>*>(p.consts), p.geo, a,
-                                                (int)per_ring, (int)total);
+                                                (int)per_ring, (int)total, p.frag);
     return cudaGetLastError();
   }
 }
