@@ -1174,27 +1174,126 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
   const int warp = tid >> 5;
   const bool periodic = G.periodic != 0;
 
-  // B fragments: a coalesced copy of the plan's device table (bfrag_perm order; J^T's Dw^T
-  // table follows Dw's), else built from kernel-parameter space (lane-divergent reads: 13% of
-  // the stall samples of the config-3 F kernel)
-  if (W::B_IN_SMEM) {
-    for (int q = tid; q < NMAT * NT * KC * 32; q += W::THREADS) {
-      if (frag) {
-        bsm[q] = __ldg(frag + q);
-      } else {
-        const int l = q & 31, r = q >> 5;
-        const int kc = r % KC, nt = (r / KC) % NT, mat = r / (KC * NT);
-        bsm[q] = bfrag_perm<N>(C, mat, nt, kc, l);
+  // tile cursor for the loads (runs STAGES-1 tiles ahead of the halo cursor)
+  auto tile_coords = [&](int T, int& tl, int64_t& bofs) {
+    const int b = T / tiles_per_ring;
+    tl = T - b * tiles_per_ring;
+    bofs = (int64_t)b * G.ndof;
+  };
+  auto load_tile = [&](int T, int s) {
+    int tl;
+    int64_t bofs;
+    tile_coords(T, tl, bofs);
+    const int64_t e0 = (int64_t)tl * ELEMS;
+    const int nel = (int)min((int64_t)ELEMS, G.E - e0);
+    const int cnt = (nel + 1) * N + 1;
+    const int64_t g0 = (e0 - 1) * N;
+    const int sh = (int)((bofs + g0) & 1);
+    const int64_t lo = g0 < 0 ? 0 : g0;
+    const int64_t hi = min(g0 + cnt, G.ndof);
+    int64_t alo, ahi;
+    if (g0 >= 0 && g0 + cnt + 1 <= G.ndof) {
+      // interior tile: widen the body outward to 16-byte boundaries (the extra
+      // doubles lie inside this ring), so no lane has to load anything itself
+      alo = ((bofs + g0) & ~(int64_t)1) - bofs;
+      ahi = ((bofs + g0 + cnt + 1) & ~(int64_t)1) - bofs;
+    } else {
+      alo = ((bofs + lo + 1) & ~(int64_t)1) - bofs;
+      ahi = ((bofs + hi) & ~(int64_t)1) - bofs;
+      if (ahi < alo) ahi = alo;
+    }
+    const int k0 = (int)(alo - g0), k1 = (int)(ahi - g0);
+    double* dst0 = stage_buf + (s * NIN + 0) * SA + sh;
+    double* dst1 = stage_buf + (s * NIN + 1) * SA + sh;
+    const double* src0 = A.u + bofs;
+    const double* src1 = (NIN == 2) ? A.w + bofs : nullptr;
+    auto scalar_piece = [&](int kb, int ke) {
+      for (int k = kb + lane; k < ke; k += 32) {
+        int64_t g = g0 + k;
+        bool valid = true;
+        if (g < 0) {
+          if (periodic) g += G.ndof; else valid = false;
+        } else if (g >= G.ndof) {
+          g -= G.ndof;
+        }
+        dst0[k] = valid ? __ldg(src0 + g) : 0.0;
+        if (NIN == 2) dst1[k] = valid ? __ldg(src1 + g) : 0.0;
+      }
+    };
+    if (k0 > 0) scalar_piece(0, k0);
+    if (k1 < cnt) scalar_piece(k1, cnt);
+    for (int k = cnt + lane; k < (ELEMS + 1) * N + 1; k += 32) {  // ragged tile: finite pad
+      dst0[k] = 0.0;
+      if (NIN == 2) dst1[k] = 0.0;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      const uint32_t bytes = (uint32_t)((ahi - alo) * 8);
+      mbar_expect_tx(&full[s], NIN * bytes);
+      if (bytes > 0) {
+        bulk_g2s(dst0 + k0, src0 + alo, bytes, &full[s]);
+        if (NIN == 2) bulk_g2s(dst1 + k0, src1 + alo, bytes, &full[s]);
       }
     }
-  }
-  if (tid == 0) {
+  };
+  int issued = 0;  // tiles issued so far (iteration index of the next load)
+  auto issue_next = [&](int T) {
+    const int s = issued % STAGES;
+    while (!mbar_try_wait(&empty[s], ((issued / STAGES) & 1) ^ 1)) {
+    }
+    load_tile(T, s);
+    ++issued;
+  };
+  // the producer initialises the barriers; with the fragment table in shared memory (n = 32,
+  // a 16-24 KB copy) it also puts the first STAGES-1 tile loads in flight before the CTA-wide
+  // prologue, hiding their HBM latency behind it (config 3: F/J/J^T -5%; at n = 8, whose
+  // prologue is short, the early issue measured 2% slower for F)
+  constexpr bool EARLY = W::B_IN_SMEM;
+  auto issue_first = [&]() {
+    for (int p = 0; p < STAGES - 1; ++p) {
+      const int T = blockIdx.x + p * gridDim.x;
+      if (T < total_tiles) issue_next(T);
+    }
+  };
+  if (EARLY ? (warp == W::CW && lane == 0) : tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], W::CW);
       mbar_init(&halo[s], 1);
     }
     fence_mbar_init();
+  }
+  if constexpr (EARLY) {
+    if (warp == W::CW) {
+      __syncwarp();
+      issue_first();
+    }
+  }
+  // B fragments: a coalesced copy of the plan's device table (bfrag_perm order; J^T's Dw^T
+  // table follows Dw's), else built from kernel-parameter space (lane-divergent reads: 13% of
+  // the stall samples of the config-3 F kernel)
+  if (W::B_IN_SMEM) {
+    constexpr int TOT = NMAT * NT * KC * 32, PER = (TOT + W::THREADS - 1) / W::THREADS;
+    if (frag) {                    // every load in flight before the first store
+      double t[PER];
+#pragma unroll
+      for (int r = 0; r < PER; ++r) {
+        const int q = tid + r * W::THREADS;
+        t[r] = q < TOT ? __ldg(frag + q) : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < PER; ++r) {
+        const int q = tid + r * W::THREADS;
+        if (q < TOT) bsm[q] = t[r];
+      }
+    }
+    for (int q = tid; q < TOT && !frag; q += W::THREADS) {
+      {
+        const int l = q & 31, r = q >> 5;
+        const int kc = r % KC, nt = (r / KC) % NT, mat = r / (KC * NT);
+        bsm[q] = bfrag_perm<N>(C, mat, nt, kc, l);
+      }
+    }
   }
   __syncthreads();
 
@@ -1236,80 +1335,7 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
 
   // ------------------------------------------------------------------ producer
   if (warp == W::CW) {
-    // tile cursor for the loads (runs STAGES-1 tiles ahead of the halo cursor)
-    auto tile_coords = [&](int T, int& tl, int64_t& bofs) {
-      const int b = T / tiles_per_ring;
-      tl = T - b * tiles_per_ring;
-      bofs = (int64_t)b * G.ndof;
-    };
-    auto load_tile = [&](int T, int s) {
-      int tl;
-      int64_t bofs;
-      tile_coords(T, tl, bofs);
-      const int64_t e0 = (int64_t)tl * ELEMS;
-      const int nel = (int)min((int64_t)ELEMS, G.E - e0);
-      const int cnt = (nel + 1) * N + 1;
-      const int64_t g0 = (e0 - 1) * N;
-      const int sh = (int)((bofs + g0) & 1);
-      const int64_t lo = g0 < 0 ? 0 : g0;
-      const int64_t hi = min(g0 + cnt, G.ndof);
-      int64_t alo, ahi;
-      if (g0 >= 0 && g0 + cnt + 1 <= G.ndof) {
-        // interior tile: widen the body outward to 16-byte boundaries (the extra
-        // doubles lie inside this ring), so no lane has to load anything itself
-        alo = ((bofs + g0) & ~(int64_t)1) - bofs;
-        ahi = ((bofs + g0 + cnt + 1) & ~(int64_t)1) - bofs;
-      } else {
-        alo = ((bofs + lo + 1) & ~(int64_t)1) - bofs;
-        ahi = ((bofs + hi) & ~(int64_t)1) - bofs;
-        if (ahi < alo) ahi = alo;
-      }
-      const int k0 = (int)(alo - g0), k1 = (int)(ahi - g0);
-      double* dst0 = stage_buf + (s * NIN + 0) * SA + sh;
-      double* dst1 = stage_buf + (s * NIN + 1) * SA + sh;
-      const double* src0 = A.u + bofs;
-      const double* src1 = (NIN == 2) ? A.w + bofs : nullptr;
-      auto scalar_piece = [&](int kb, int ke) {
-        for (int k = kb + lane; k < ke; k += 32) {
-          int64_t g = g0 + k;
-          bool valid = true;
-          if (g < 0) {
-            if (periodic) g += G.ndof; else valid = false;
-          } else if (g >= G.ndof) {
-            g -= G.ndof;
-          }
-          dst0[k] = valid ? __ldg(src0 + g) : 0.0;
-          if (NIN == 2) dst1[k] = valid ? __ldg(src1 + g) : 0.0;
-        }
-      };
-      if (k0 > 0) scalar_piece(0, k0);
-      if (k1 < cnt) scalar_piece(k1, cnt);
-      for (int k = cnt + lane; k < (ELEMS + 1) * N + 1; k += 32) {  // ragged tile: finite pad
-        dst0[k] = 0.0;
-        if (NIN == 2) dst1[k] = 0.0;
-      }
-      __syncwarp();
-      if (lane == 0) {
-        const uint32_t bytes = (uint32_t)((ahi - alo) * 8);
-        mbar_expect_tx(&full[s], NIN * bytes);
-        if (bytes > 0) {
-          bulk_g2s(dst0 + k0, src0 + alo, bytes, &full[s]);
-          if (NIN == 2) bulk_g2s(dst1 + k0, src1 + alo, bytes, &full[s]);
-        }
-      }
-    };
-    int issued = 0;  // tiles issued so far (iteration index of the next load)
-    auto issue_next = [&](int T) {
-      const int s = issued % STAGES;
-      while (!mbar_try_wait(&empty[s], ((issued / STAGES) & 1) ^ 1)) {
-      }
-      load_tile(T, s);
-      ++issued;
-    };
-    for (int p = 0; p < STAGES - 1; ++p) {
-      const int T = blockIdx.x + p * gridDim.x;
-      if (T < total_tiles) issue_next(T);
-    }
+    if constexpr (!EARLY) issue_first();
     int it = 0;
     for (int T = blockIdx.x; T < total_tiles; T += gridDim.x, ++it) {
       // row N of the element left of each consumer warp: one DMMA m-tile whose
