@@ -987,6 +987,15 @@ struct WsTile {
   static constexpr bool B_IN_SMEM = (n > 16);
 };
 
+// Programmatic dependent launch (the apply kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): a kernel may start its prologue while
+// the previous kernel in the stream drains; griddep_wait() blocks until that kernel has
+// completed and its memory is visible, so it precedes every global access of the data path.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -1173,6 +1182,8 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
   const int lane = tid & 31;
   const int warp = tid >> 5;
   const bool periodic = G.periodic != 0;
+  // the next kernel may be scheduled as soon as SM resources free up (its data path waits)
+  griddep_launch_dependents();
 
   // tile cursor for the loads (runs STAGES-1 tiles ahead of the halo cursor)
   auto tile_coords = [&](int T, int& tl, int64_t& bofs) {
@@ -1250,6 +1261,7 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
   // prologue is short, the early issue measured 2% slower for F)
   constexpr bool EARLY = W::B_IN_SMEM;
   auto issue_first = [&]() {
+    griddep_wait();              // inputs may come from the previous kernel in the stream
     for (int p = 0; p < STAGES - 1; ++p) {
       const int T = blockIdx.x + p * gridDim.x;
       if (T < total_tiles) issue_next(T);

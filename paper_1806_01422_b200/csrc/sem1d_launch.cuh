@@ -18,6 +18,10 @@ namespace sem1d {
 // 2 = plain kernel only, 3 = the first (CTA-synchronous) tensor-core kernel.
 int sem1d_path_override();
 
+#ifndef WS_PDL
+#define WS_PDL 1
+#endif
+
 struct PlanView {
   const void* consts;  // Consts<N>, packed by the plan
   const double* frag;  // n % 8 == 0: device B-fragment table (bfrag_perm order), or null
@@ -122,9 +126,20 @@ static cudaError_t launch_ws(const PlanView& p, const Args& a, cudaStream_t s) {
     const int64_t total = per_ring * p.batch;
     if (total > 0x7fffffffLL) return cudaErrorInvalidValue;
     const int grid = (int)(total < max_resident ? total : max_resident);
-    kern<<<grid, WsTile<N, OP>::THREADS, smem, s>>>(*static_cast<const Consts<N>*>(p.consts), p.geo, a,
-                                                (int)per_ring, (int)total, p.frag);
-    return cudaGetLastError();
+    // programmatic dependent launch: the prologue (barrier init, fragment table) overlaps the
+    // previous kernel's drain; the producer's griddep_wait() orders the data path after it
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(WsTile<N, OP>::THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = WS_PDL;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, *static_cast<const Consts<N>*>(p.consts), p.geo, a, (int)per_ring,
+                              (int)total, p.frag);
   }
 }
 
