@@ -298,11 +298,23 @@ class SemOperator(ComposedStages):
             self._step_ok = bool(_lib.load().sem1d_step_supported(self._plan.handle)) and not self._adv
         return self._step_ok and getattr(self, "use_fused_steps", True)
 
-    def launch_rk_step(self, u, u_new, dt, scheme):
+    def launch_rk_step(self, u, u_new, dt, scheme, flag=None):
+        """One fused step; ``flag``: device address of the int32 flag word to OR into
+        (default the operator's own -- ``integrate`` passes per-step slots when it runs ahead)."""
         _lib.check(_lib.load().sem1d_rk_step(self._plan.handle, u.data_ptr(), u_new.data_ptr(),
                                              float(dt), self._SCHEME_CODES[scheme],
-                                             self._flag.data_ptr(), self._stream()),
+                                             flag or self._flag.data_ptr(), self._stream()),
                    "sem1d_rk_step")
+
+    supports_flag_slots = True
+
+    def flag_slots(self, k):
+        """A zeroed device int32 array of (at least) k per-step flag words (cached)."""
+        t = getattr(self, "_flag_slots_t", None)
+        if t is None or t.numel() < k:
+            t = _torch().zeros(k, dtype=_torch().int32, device=self.device)
+            self._flag_slots_t = t
+        return t
 
     def step_stages_supported(self):
         """The fused step pair that keeps the stage states in HBM applies (shared memory fits)."""
@@ -310,11 +322,12 @@ class SemOperator(ComposedStages):
             self._stages_ok = bool(_lib.load().sem1d_step_stages_supported(self._plan.handle)) and not self._adv
         return self._stages_ok and self.step_fused_supported()
 
-    def launch_rk_step_stages(self, u, u_new, stages, dt, scheme):
+    def launch_rk_step_stages(self, u, u_new, stages, dt, scheme, flag=None):
         """One fused step that also writes the stage states U_1..U_{s-1} into `stages`."""
         _lib.check(_lib.load().sem1d_rk_step_stages(
             self._plan.handle, u.data_ptr(), u_new.data_ptr(), _lib.ptr_array([t.data_ptr() for t in stages]),
-            float(dt), self._SCHEME_CODES[scheme], self._flag.data_ptr(), self._stream()), "sem1d_rk_step_stages")
+            float(dt), self._SCHEME_CODES[scheme], flag or self._flag.data_ptr(), self._stream()),
+            "sem1d_rk_step_stages")
 
     def launch_adj_step_stages(self, u, stages, lam, lam_out, dt, scheme):
         """One fused adjoint step reading the stored stage states (no recompute)."""

@@ -41,6 +41,10 @@ TABLEAUX = {
 }
 
 _RETRY_HALVINGS = 3   # timeloop.py:29
+# fixed-dt runs on the fused step kernels verify their flags once per _SPEC_WINDOW steps;
+# without stored snapshots the held states are capped at _SPEC_BYTES
+_SPEC_WINDOW = 16
+_SPEC_BYTES = 8e9
 
 
 @dataclass
@@ -161,17 +165,19 @@ class StepEngine:
         k_out = self._buf(("k", i)) if i in store else None
         self.op.launch_rk_stage(U_in, k_out, base, terms, coefs, dt, Y, check)
 
-    def step(self, u, dt, out, fused=True, stages_out=None):
+    def step(self, u, dt, out, fused=True, stages_out=None, flag=None):
         """Launch one full step u -> out (no host sync): one temporally blocked launch
         when the ring qualifies (and ``fused``), else one fused launch per stage, which
         also leaves the stored slopes (k_2 of Kutta-3 for the embedded pair) in place.
-        ``stages_out`` (fused path, s > 1): also write U_1..U_{s-1} there."""
+        ``stages_out`` (fused path, s > 1): also write U_1..U_{s-1} there.  ``flag``
+        (fused path): device address of the step's own flag word."""
         fz = getattr(self.op, "step_fused_supported", None)
         if fused and fz is not None and fz():
+            kw = {} if flag is None else {"flag": flag}
             if stages_out is not None and self.s > 1:
-                self.op.launch_rk_step_stages(u, out, stages_out, dt, self.scheme)
+                self.op.launch_rk_step_stages(u, out, stages_out, dt, self.scheme, **kw)
             else:
-                self.op.launch_rk_step(u, out, dt, self.scheme)
+                self.op.launch_rk_step(u, out, dt, self.scheme, **kw)
             self.op.counters["rhs"] += self.s
             return
         s = self.s
@@ -366,15 +372,81 @@ def integrate(op, u0, cfg, store_steps="all", keep_log=False, keep_stages=False)
     keep_stages = bool(keep_stages) and stages_supported(op, cfg)
     stage_snaps = {}
     op.flags()  # clear stale bits
+    # Running ahead (fixed-dt explicit schemes on the fused step kernels): up to `window` steps
+    # are launched without a host sync, each OR-ing its non-finite bits into its own flag
+    # word; the window is then verified with ONE device->host read.  A flagged step j rolls
+    # the run back to the state before j (trajectory, counters and log included) and step j is
+    # re-run synchronously, so StepFailure retries / NumericFailure behave exactly as in the
+    # per-step-checked loop.  Without stored snapshots the window's states are held for the
+    # rollback, so the window is sized to the free-memory budget.
+    fz = getattr(op, "step_fused_supported", None)
+    spec = (not cn and fused and getattr(op, "supports_flag_slots", False) and fz is not None and fz())
+    window = 0
+    if spec:
+        field_bytes = 8 * int(op.empty().numel())
+        window = _SPEC_WINDOW if store_all else max(0, min(_SPEC_WINDOW, int(_SPEC_BYTES // field_bytes)))
+        spec = window >= 2
+    if spec:
+        slots = op.flag_slots(window)
+        slots.zero_()
+        slot0 = slots.data_ptr()
+    pending = []            # rollback records of the launched, unverified steps
+    sync_next = False       # re-run the next step with a per-step check (after a rollback)
+
+    def verify():
+        """Check the pending window; on a flagged step roll back to it.  True if rolled back."""
+        nonlocal n, t, dt_next, attempts, u, sync_next
+        vals = slots[:len(pending)].cpu().tolist()
+        slots.zero_()
+        bad = next((i for i, v in enumerate(vals) if v), None)
+        if bad is None:
+            pending.clear()
+            return False
+        n, t, dt_next, attempts, u, nlog = pending[bad]
+        for rec in pending[bad:]:
+            snapshots.pop(rec[0] + 1, None)
+            stage_snaps.pop(rec[0], None)
+        del ts[n + 1:]
+        del dts[n:]
+        if keep_log:
+            del log[nlog:]
+        stats["steps"] = n
+        pending.clear()
+        sync_next = True
+        return True
+
     while t < cfg.t_end - tiny:
         attempts += 1
         if attempts > cfg.max_steps:
+            if spec and pending and verify():
+                continue
             raise IntegrationError(f"max_steps={cfg.max_steps} exceeded at t={t:.6g}",
                                    diagnostics={"t": t, "steps": n, "stats": stats})
         remaining = cfg.t_end - t
         clipped = remaining - dt_next <= tiny
         dt = remaining if clipped else dt_next
         u_new = op.empty()
+        if spec and not sync_next:
+            keep_n = keep_stages and (store_all or n in want)
+            st_out = [op.empty() for _ in range(engine.s - 1)] if keep_n else None
+            pending.append((n, t, dt_next, attempts - 1, u, len(log) if keep_log else 0))
+            engine.step(u, dt, u_new, fused=True, stages_out=st_out, flag=slot0 + 4 * (len(pending) - 1))
+            if keep_n:
+                stage_snaps[n] = st_out
+            n += 1
+            t = cfg.t_end if clipped else t + dt
+            dts.append(dt)
+            ts.append(t)
+            u = u_new
+            stats["steps"] = n
+            if store_all or n in want:
+                snapshots[n] = u
+            if keep_log:
+                log.append((n, t, dt, 0.0, 1))
+            if len(pending) == window or not t < cfg.t_end - tiny:
+                verify()
+            continue
+        sync_next = False
         for retry in range(_RETRY_HALVINGS + 1):
             try:
                 if cn:

@@ -87,3 +87,78 @@ def test_stage_states_in_hbm_match_recompute(cuda, scheme, E, N, dt):
     _, ge = prob.evaluate(u0)
     assert len(prob.last_forward.stage_snapshots) == prob.last_forward.n_steps
     assert rel_err(ge.cpu().numpy(), grads[False]) <= 1e-13
+
+
+def _inject_failures(op, u0, t0, fail_rule):
+    """Wrap the fused step launches: a step starting at time T (tracked through the states'
+    sums) whose dt exceeds fail_rule[T] reports a non-finite step result through whichever
+    flag word it was given -- a deterministic failure, the same whether the step runs ahead
+    or is checked at once."""
+    from paper_1806_01422_b200 import _lib
+    time_of = {float(torch.as_tensor(u0, device="cuda:0").sum()): t0}
+    orig_plain, orig_st = op.launch_rk_step, op.launch_rk_step_stages
+
+    def mark(u, u_new, dt, flag):
+        t = time_of[float(u.sum())]
+        time_of[float(u_new.sum())] = t + dt
+        rule = next((v for k, v in fail_rule.items() if abs(k - t) < 1e-12), None)
+        if rule is not None and dt > rule:
+            if flag is None:
+                op._flag.fill_(_lib.SEM1D_FLAG_STEP_NONFINITE)
+            else:
+                tt = op._flag_slots_t
+                tt[(flag - tt.data_ptr()) // 4] = _lib.SEM1D_FLAG_STEP_NONFINITE
+
+    def plain(u, u_new, dt, scheme, flag=None):
+        orig_plain(u, u_new, dt, scheme, flag=flag)
+        mark(u, u_new, dt, flag)
+
+    def staged(u, u_new, stages, dt, scheme, flag=None):
+        orig_st(u, u_new, stages, dt, scheme, flag=flag)
+        mark(u, u_new, dt, flag)
+
+    op.launch_rk_step, op.launch_rk_step_stages = plain, staged
+
+
+@pytest.mark.parametrize("store", ["all", "some"])
+@pytest.mark.parametrize("keep", [False, True])
+def test_run_ahead_rollback_matches_per_step_checks(cuda, store, keep):
+    """integrate() launches fixed-dt fused steps ahead and verifies their per-step flag words
+    once per window; a flagged step rolls the run back and is re-run with the per-step check.
+    With the same (deterministic) step failures -- the step from t = 1e-5 fails at dt and
+    passes at dt/2, the ones from 2e-5 and 3e-5 fail at dt/2 and dt/4 -- the result
+    (time grid, trajectory, stage snapshots, counters, retries, log) is identical to the loop
+    that checks every step."""
+    steps = 40
+    out = {}
+    for mode in ("ahead", "sync"):
+        g, op, u0, ud, ts = _problem(1061, 7, 1e-3, 2e-6, steps, "rk4", 3)
+        if mode == "sync":
+            op.supports_flag_slots = False
+        _inject_failures(op, u0, 0.0, {1e-5: 1.5e-6, 2e-5: 0.75e-6, 3e-5: 0.3e-6})
+        st = "all" if store == "all" else [0, 7, 19, 33]
+        out[mode] = timeloop.integrate(op, u0, ts, store_steps=st, keep_log=True, keep_stages=keep)
+    a, b = out["ahead"], out["sync"]
+    assert np.array_equal(a.ts, b.ts) and np.array_equal(a.dts, b.dts)
+    assert a.stats == b.stats and a.stats["retries"] == 3
+    assert a.step_log == b.step_log
+    assert sorted(a.snapshots) == sorted(b.snapshots)
+    for k in a.snapshots:
+        assert torch.equal(a.snapshots[k], b.snapshots[k])
+    assert torch.equal(a.u_final, b.u_final)
+    assert sorted(a.stage_snapshots) == sorted(b.stage_snapshots)
+    for k in a.stage_snapshots:
+        for x, y in zip(a.stage_snapshots[k], b.stage_snapshots[k]):
+            assert torch.equal(x, y)
+
+
+def test_run_ahead_raises_like_per_step_checks(cuda):
+    """A step that fails at every dt exhausts the halvings: StepFailure from the run-ahead
+    loop as from the per-step-checked one."""
+    for mode in ("ahead", "sync"):
+        g, op, u0, ud, ts = _problem(1061, 7, 1e-3, 2e-6, 30, "rk4", 3)
+        if mode == "sync":
+            op.supports_flag_slots = False
+        _inject_failures(op, u0, 0.0, {9 * 2e-6: 0.0})
+        with pytest.raises(sb.StepFailure):
+            timeloop.integrate(op, u0, ts)
