@@ -754,8 +754,9 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
   uint64_t* bar = reinterpret_cast<uint64_t*>(xfer + 32);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kq = lane & 3, rr = lane >> 2;
-  const int T = TE - 2 * A.H;
   using TB = TabC<SCH>;                       // compile-time tableau: stage loops unroll
+  constexpr int H = TB::s;                    // ghost elements per side (= the launcher's A.H)
+  constexpr int T = TE - 2 * H;
   constexpr bool STG = MODE == 1;
   const int64_t ndof = G.ndof;
   const double mnu = -C.nu;
@@ -781,8 +782,10 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
     fence_mbar_init();
   }
   __syncthreads();
+  griddep_launch_dependents();               // PDL: the next step's prologue may start
+  griddep_wait();                             // ... and this step's data path waits for ours
   if (tid == 0 && blockIdx.x < A.ntiles) {
-    const TileLoad L = tile_load_plan(blockIdx.x, T, A.H, N, LEN, ndof);
+    const TileLoad L = tile_load_plan(blockIdx.x, T, H, N, LEN, ndof);
     if (L.bulk) tile_issue(L, LEN, A.u, sbuf, &bar[0], 1, nullptr, nullptr);
   }
   unsigned fin = 0u;
@@ -793,7 +796,7 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
   for (int t = blockIdx.x; t < A.ntiles; t += gridDim.x, ++it) {
     const int b = it & 1;
     double* sb = sbuf + b * PAD;
-    const TileLoad L = tile_load_plan(t, T, A.H, N, LEN, ndof);
+    const TileLoad L = tile_load_plan(t, T, H, N, LEN, ndof);
     if (L.bulk) {
       while (!mbar_try_wait(&bar[b], (phase >> b) & 1u)) {
       }
@@ -808,7 +811,7 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
     }
     // prefetch the next tile into the other buffer (free: its tile ended with a barrier)
     if (tid == 0 && t + (int)gridDim.x < A.ntiles) {
-      const TileLoad Ln = tile_load_plan(t + gridDim.x, T, A.H, N, LEN, ndof);
+      const TileLoad Ln = tile_load_plan(t + gridDim.x, T, H, N, LEN, ndof);
       if (Ln.bulk) tile_issue(Ln, LEN, A.u, sbuf + (b ^ 1) * PAD, &bar[b ^ 1], 1, nullptr, nullptr);
     }
     const double* su = sb + L.sh;
@@ -849,7 +852,7 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
             if (st == 0 && TB::keep(0)) sk[g] = kk;
           } else {
             const double un = __dadd_rn(su[g], __dmul_rn(A.dt, acc[q][kc]));
-            if (e >= A.H && e < A.H + T) bad |= !isfinite(un);
+            if (e >= H && e < H + T) bad |= !isfinite(un);
             sU[g] = un;                         // every warp is past its last read of sU
           }
         }
@@ -860,7 +863,7 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
         const int64_t e_o = (int64_t)t * T;
         const int no = (int)min((int64_t)T, G.E - e_o) * N;
         double* dst = A.stages[st] + e_o * N;
-        const double* src = sU + A.H * N;
+        const double* src = sU + H * N;
         if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0 && (no & 1) == 0) {
           if (tid == 0) {                     // one async bulk store; read-drained before sU is rewritten
             bulk_s2g(dst, src, (uint32_t)(no * 8));
@@ -873,7 +876,7 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
     }
     const int64_t e_out0 = (int64_t)t * T;
     const int nout_el = (int)min((int64_t)T, G.E - e_out0);
-    for (int k = tid; k < nout_el * N; k += 32 * W) A.out[e_out0 * N + k] = sU[A.H * N + k];
+    for (int k = tid; k < nout_el * N; k += 32 * W) A.out[e_out0 * N + k] = sU[H * N + k];
     __syncthreads();
   }
   if (STG && tid == 0) bulk_wait_all();
@@ -904,8 +907,9 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
   uint64_t* bar = reinterpret_cast<uint64_t*>(xfer + 32);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kq = lane & 3, rr = lane >> 2;
-  const int T = TE - 2 * A.H;
   constexpr int S = TB::s;
+  constexpr int H = LD ? S : 2 * S - 1;       // ghost elements per side (= the launcher's A.H)
+  constexpr int T = TE - 2 * H;
   auto issue = [&](const TileLoad& Lx, int buf) {
     const double* srcs[5] = {A.u, A.lam, A.stin[0], A.stin[1], A.stin[2]};
     double* dsts[5] = {sbu + buf * PAD, sbl + buf * PAD, sUs + (buf * 3 + 0) * PAD, sUs + (buf * 3 + 1) * PAD,
@@ -970,8 +974,10 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
     fence_mbar_init();
   }
   __syncthreads();
+  griddep_launch_dependents();               // PDL: the next step's prologue may start
+  griddep_wait();                             // ... and this step's data path waits for ours
   if (tid == 0 && blockIdx.x < A.ntiles) {
-    const TileLoad L = tile_load_plan(blockIdx.x, T, A.H, N, LEN, ndof);
+    const TileLoad L = tile_load_plan(blockIdx.x, T, H, N, LEN, ndof);
     if (L.bulk) issue(L, 0);
   }
   unsigned fin = 0u;
@@ -980,7 +986,7 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
   int it = 0;
   for (int t = blockIdx.x; t < A.ntiles; t += gridDim.x, ++it) {
     const int bsel = it & 1;
-    const TileLoad L = tile_load_plan(t, T, A.H, N, LEN, ndof);
+    const TileLoad L = tile_load_plan(t, T, H, N, LEN, ndof);
     if (L.bulk) {
       while (!mbar_try_wait(&bar[bsel], (phase >> bsel) & 1u)) {
       }
@@ -997,7 +1003,7 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
       __syncthreads();
     }
     if (tid == 0 && t + (int)gridDim.x < A.ntiles) {
-      const TileLoad Ln = tile_load_plan(t + gridDim.x, T, A.H, N, LEN, ndof);
+      const TileLoad Ln = tile_load_plan(t + gridDim.x, T, H, N, LEN, ndof);
       if (Ln.bulk) issue(Ln, bsel ^ 1);
     }
     su = sbu + bsel * PAD + L.sh;
@@ -1052,7 +1058,7 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
         if (j == N) continue;
         const int g = e * N + j;
         const double z = zval(S - 1, g, q, kc);
-        if (e >= A.H && e < A.H + T) fin |= nonfinite_bit(z);
+        if (e >= H && e < H + T) fin |= nonfinite_bit(z);
         sz[g] = z;
       }
     }
@@ -1079,7 +1085,7 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
             slam[g] = __dadd_rn(slam[g], lacc[q][kc]);
           } else {
             const double z = zval(i - 1, g, q, kc);
-            if (e >= A.H && e < A.H + T) fin |= nonfinite_bit(z);
+            if (e >= H && e < H + T) fin |= nonfinite_bit(z);
             sz[g] = z;
           }
         }
@@ -1088,7 +1094,7 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
     }
     const int64_t e_out0 = (int64_t)t * T;
     const int nout_el = (int)min((int64_t)T, G.E - e_out0);
-    for (int k = tid; k < nout_el * N; k += 32 * W) A.out[e_out0 * N + k] = slam[A.H * N + k];
+    for (int k = tid; k < nout_el * N; k += 32 * W) A.out[e_out0 * N + k] = slam[H * N + k];
     __syncthreads();
   }
   if (fin) atomicOr(A.flag, SEM1D_FLAG_INPUT2_NONFINITE);

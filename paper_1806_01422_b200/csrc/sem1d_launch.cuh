@@ -300,8 +300,19 @@ cudaError_t launch_tile_one(const PlanView& p, const TileStepArgs& a, int thread
     if (per_sm < 1) per_sm = 1;
   }
   const int grid = (int)std::min<int64_t>(a.ntiles, (int64_t)per_sm * sms);
-  KERN<<<grid, threads, smem, s>>>(*static_cast<const Consts<N>*>(p.consts), p.geo, a);
-  return cudaGetLastError();
+  // programmatic dependent launch (consecutive steps of a sweep): the prologue overlaps the
+  // previous step's drain; the kernel's griddep_wait() precedes its data path
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = WS_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, KERN, *static_cast<const Consts<N>*>(p.consts), p.geo, a);
 }
 
 template <int N, int SCH>
