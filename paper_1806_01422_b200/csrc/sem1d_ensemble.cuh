@@ -646,13 +646,13 @@ constexpr size_t ens_adj_smem_bytes(int ndof) {
 #define TILE_WMT8 4
 #endif
 #ifndef TILE_WA8
-#define TILE_WA8 4
+#define TILE_WA8 8      // recompute adjoint at n = 8: 8 warps x 2 m-tiles (0.653 vs 0.682 ms at 4 x 4)
 #endif
 #ifndef TILE_WF8
 #define TILE_WF8 8
 #endif
 #ifndef TILE_WMTA8
-#define TILE_WMTA8 4
+#define TILE_WMTA8 2
 #endif
 #ifndef TILE_WA16
 #define TILE_WA16 8
@@ -1105,8 +1105,8 @@ struct TileCfg {
   // forward: TE = 256 elements for N = 7 (8 warps x 4 m-tiles, 2 CTAs per SM: the second
   // CTA's DMMA fills the first one's barrier waits; A/B 0.48 vs 0.54 ms per RK4 step at
   // 16 x 4 x 1), 128 for N = 15/23 (N = 15: 8 warps x 2 interleaved m-tiles), 64 for N = 31;
-  // adjoint: 128 for N = 7 (4 warps x 4
-  // m-tiles, 3 CTAs per SM; 1.155 vs 1.190 ms at 16 x 2 x 1), 128 / 64 otherwise (nine
+  // adjoint: 128 for N = 7 (8 warps x 2 m-tiles, 3 CTAs per SM; with the compile-time
+  // tableaux 0.653 ms vs 0.682 at 4 x 4 x 3 and 0.735 at 4 x 2), 128 / 64 otherwise (nine
   // slabs must fit the shared memory of the resident CTAs)
   static constexpr int W = (N + 1) == 32 ? 8 : ((N + 1) == 8 ? TILE_WF8 : ((N + 1) == 16 ? TILE_WF16 : TILE_WF24));
   // adjoint warps: 8 x 2 m-tiles for N = 15/23 (at 16 warps the 128-register cap made the
