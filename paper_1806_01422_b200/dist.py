@@ -308,9 +308,25 @@ class ShardedOperator:
         f = getattr(self.local, "step_fused_supported", None)
         return bool(self.part.zone >= 7 and f is not None and f())
 
-    def launch_rk_step(self, u, u_new, dt, scheme):
+    def launch_rk_step(self, u, u_new, dt, scheme, flag=None):
         self.halo.refresh([u])
-        self.local.launch_rk_step(u, u_new, dt, scheme)
+        if flag is None:
+            self.local.launch_rk_step(u, u_new, dt, scheme)
+        else:
+            self.local.launch_rk_step(u, u_new, dt, scheme, flag=flag)
+
+    # run-ahead integrate (timeloop.integrate): per-step flag words of the local operator,
+    # verified with one all-reduce per window so every rank rolls back at the same step
+    @property
+    def supports_flag_slots(self):
+        return bool(getattr(self.local, "supports_flag_slots", False))
+
+    def flag_slots(self, k):
+        return self.local.flag_slots(k)
+
+    def reduce_flag_words(self, words):
+        """Max over ranks of the window's flag words (nonzero = the step failed somewhere)."""
+        return self._allreduce(words.clone(), "max")
 
     def launch_adj_step(self, u, lam, lam_out, dt, scheme):
         self.halo.refresh([u, lam])

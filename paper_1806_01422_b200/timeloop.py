@@ -396,7 +396,9 @@ def integrate(op, u0, cfg, store_steps="all", keep_log=False, keep_stages=False)
     def verify():
         """Check the pending window; on a flagged step roll back to it.  True if rolled back."""
         nonlocal n, t, dt_next, attempts, u, sync_next
-        vals = slots[:len(pending)].cpu().tolist()
+        words = slots[:len(pending)]
+        red = getattr(op, "reduce_flag_words", None)      # sharded: agree across ranks
+        vals = (red(words) if red is not None else words).cpu().tolist()
         slots.zero_()
         bad = next((i for i, v in enumerate(vals) if v), None)
         if bad is None:

@@ -111,3 +111,31 @@ def test_bench_two_ranks_json_line(cuda, tmp_path):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
     assert "sharded" in d["config"]["parallelism"]
+
+
+def test_sharded_evaluate_two_ranks_matches_single(cuda):
+    """Config-5 tool at small size: L-BFGS on evaluate() (run-ahead fused forward steps with
+    per-step flag words verified by a cross-rank max, binomial checkpointing, fused adjoint
+    steps) on 2 element-sharded ranks (one GPU, gloo exchange) gives the objective and
+    gradient-norm history of the single-GPU run."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    tool = os.path.join(root, "tools", "bench_cfg5.py")
+    args = ["16384", "24", "4", "1"]
+    one = subprocess.run([sys.executable, tool] + args, cwd=root, capture_output=True, text=True,
+                         timeout=600)
+    assert one.returncode == 0, one.stderr[-2000:]
+    env = dict(os.environ, SEM1D_DIST_BACKEND="gloo", SEM1D_SAME_DEVICE="1")
+    two = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                          "29541", tool] + args, cwd=root, capture_output=True, text=True,
+                         timeout=600, env=env)
+    assert two.returncode == 0, two.stderr[-2000:]
+    a, b = (json.loads([ln for ln in o.stdout.splitlines() if ln.startswith("{")][-1]) for o in (one, two))
+    assert b["n_gpus"] == 2
+    assert len(a["J_log"]) == len(b["J_log"]) >= 2
+    for x, y in zip(a["J_log"] + a["gnorm_log"], b["J_log"] + b["gnorm_log"]):
+        assert abs(x - y) <= 1e-9 * max(abs(x), 1e-300)
