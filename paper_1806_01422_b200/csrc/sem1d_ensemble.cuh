@@ -368,11 +368,13 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_fwd_warps<N>()>::THREADS, 1)
 // jv[q][kc] at the nodes owned by this lane, interface nodes summed.
 // PREJ: fragments from bfrag_adj, zsrc holds the unscaled stage input z, and the output is
 // dt * J^T(M^-1 z) (the M^-1 and dt products ride on the DMMAs)
-template <int N, int WMT_MAX, class BGet, bool WRAP = true, bool ILV = false, bool PREJ = false>
+// ZS: the stage input is zs * zsrc (the first transposed stage reads b_{s-1} lam straight
+// from the lam slab)
+template <int N, int WMT_MAX, class BGet, bool WRAP = true, bool ILV = false, bool PREJ = false, bool ZS = false>
 __device__ __forceinline__ void ring_jact(const Consts<N>& C, const Geo& G, const double* usrc,
                                           const double* zsrc, double* xfer, BGet bget,
                                           double mnu, int warp, int lane,
-                                          double (&jv)[WMT_MAX][(N + 1) / 4]) {
+                                          double (&jv)[WMT_MAX][(N + 1) / 4], double zs = 1.0) {
   constexpr int KC = (N + 1) / 4, NT = (N + 1) / 8;
   const int kq = lane & 3, rr = lane >> 2;
   const int mt_total = (int)G.E / 8;
@@ -387,7 +389,7 @@ __device__ __forceinline__ void ring_jact(const Consts<N>& C, const Geo& G, cons
 #pragma unroll
     for (int kc = 0; kc < KC; ++kc) {
       au[kc] = usrc[base + 4 * kc + kq];
-      az[kc] = zsrc[base + 4 * kc + kq];
+      az[kc] = ZS ? __dmul_rn(zs, zsrc[base + 4 * kc + kq]) : zsrc[base + 4 * kc + kq];
       at[kc] = __dmul_rn(au[kc], az[kc]);
     }
     double r[NT][2];
@@ -733,7 +735,7 @@ __device__ __forceinline__ void tile_issue_n(const TileLoad& L, int LEN, const d
 template <int N>
 constexpr int tile_minb() { return (N + 1) == 8 ? TILE_MINB8 : 1; }
 #ifndef TILE_ADJ_LD_MINB8
-#define TILE_ADJ_LD_MINB8 5
+#define TILE_ADJ_LD_MINB8 6
 #endif
 template <int N, int MODE = 0>
 constexpr int tile_adj_minb() { return (N + 1) == 8 ? (MODE == 1 ? TILE_ADJ_LD_MINB8 : TILE_ADJ_MINB8) : 1; }
@@ -900,14 +902,17 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
   // the tile into [2][3][PAD]
   constexpr bool LD = MODE == 1;
   using TB = TabC<SCH>;                       // compile-time tableau: stage loops unroll
+  constexpr int S = TB::s;
+  // LD: z of stage i-1 goes into the (dead) stage-state slab U_i and the first stage reads
+  // b_{s-1} lam from the lam slab, so there is no z slab; k (Kutta-3's older l) only for s = 3
+  // -- 10 slabs for RK4, 6 CTAs/SM
   double* sUs = sbl + 2 * PAD;
   double* sk = sUs + (LD ? 6 : 3) * PAD;
-  double* sz = sk + PAD;
-  double* xfer = sz + PAD;
+  double* sz = sk + ((LD && S != 3) ? 0 : PAD);
+  double* xfer = LD ? sz : sz + PAD;
   uint64_t* bar = reinterpret_cast<uint64_t*>(xfer + 32);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kq = lane & 3, rr = lane >> 2;
-  constexpr int S = TB::s;
   constexpr int H = LD ? S : 2 * S - 1;       // ghost elements per side (= the launcher's A.H)
   constexpr int T = TE - 2 * H;
   auto issue = [&](const TileLoad& Lx, int buf) {
@@ -1059,16 +1064,26 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
         const int g = e * N + j;
         const double z = zval(S - 1, g, q, kc);
         if (e >= H && e < H + T) fin |= nonfinite_bit(z);
-        sz[g] = z;
+        if (!LD) sz[g] = z;
       }
     }
-    if (tid == 0) sz[TE * N] = 0.0;           // last node of the open chain (ghost margin)
-    __syncthreads();
+    if (!LD) {
+      if (tid == 0) sz[TE * N] = 0.0;         // last node of the open chain (ghost margin)
+      __syncthreads();
+    }
     // per stage: J^T apply (its internal barrier ends every read of sz), then accumulate l_i
     // and form z_{i-1} in the same pass -- two barriers per stage
 #pragma unroll
     for (int i = S - 1; i >= 0; --i) {
-      ring_jact<N, WMT, decltype(bget), false, TILE_ILV != 0, true>(C, Gt, Uarr(i), sz, xfer, bget, mnu, warp, lane, kv);
+      constexpr bool Z0 = false;
+      if (LD && i == S - 1)
+        ring_jact<N, WMT, decltype(bget), false, TILE_ILV != 0, true, true>(C, Gt, Uarr(i), slam, xfer, bget, mnu, warp,
+                                                                         lane, kv, TB::b(S - 1));
+      else
+        ring_jact<N, WMT, decltype(bget), false, TILE_ILV != 0, true>(C, Gt, Uarr(i), LD ? Uarr(i + 1) : sz, xfer, bget,
+                                                                   mnu, warp, lane, kv);
+      (void)Z0;
+      double* zdst = LD ? Uarr(i) : sz;         // LD: U_i is dead once its J^T has run
 #pragma unroll
       for (int q = 0; q < WMT; ++q) {
         const int e = ring_elem<WMT, TILE_ILV != 0>(warp, q, rr);
@@ -1086,10 +1101,11 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
           } else {
             const double z = zval(i - 1, g, q, kc);
             if (e >= H && e < H + T) fin |= nonfinite_bit(z);
-            sz[g] = z;
+            zdst[g] = z;
           }
         }
       }
+      if (LD && i > 0 && tid == 0) zdst[TE * N] = 0.0;   // last node of the open chain
       __syncthreads();
     }
     const int64_t e_out0 = (int64_t)t * T;
@@ -1115,7 +1131,7 @@ struct TileCfg {
   static constexpr int W_A = (N + 1) == 8 ? TILE_WA8 : ((N + 1) == 32 ? 8 : TILE_WA16);
   static constexpr int WMT_F = (N + 1) == 8 ? TILE_WMT8 : ((N + 1) == 32 ? 1 : 16 / W);
   static constexpr int WMT_A = (N + 1) == 8 ? TILE_WMTA8 : ((N + 1) == 32 ? 1 : 128 / (8 * TILE_WA16));
-  // adjoint step reading stored stage states (fewer DMMAs, 12 slabs): its own warp shape
+  // adjoint step reading stored stage states (fewer DMMAs, 10-11 slabs): its own warp shape
   static constexpr int W_L = (N + 1) == 8 ? TILE_WL8 : W_A;
   static constexpr int WMT_L = (N + 1) == 8 ? TILE_WMTL8 : WMT_A;
   static constexpr int TE_L = 8 * W_L * WMT_L;
@@ -1127,9 +1143,14 @@ struct TileCfg {
   static constexpr size_t fwd_smem = sizeof(double) * (4 * (size_t)PAD_F + 32) + 2 * sizeof(uint64_t);
   static constexpr size_t BFRAG = ((N + 1) == 32) ? sizeof(double) * 5 * ((N + 1) / 8) * ((N + 1) / 4) * 32 + 16 : 0;
   static constexpr size_t adj_smem = sizeof(double) * (9 * (size_t)PAD_A + 32) + 2 * sizeof(uint64_t) + BFRAG;
-  // adjoint step reading the stored stage states: 12 slabs (u, lam, U_1..U_3 double-buffered,
-  // k, z) at the W_L x WMT_L shape
-  static constexpr size_t adj_smem_ld = sizeof(double) * (12 * (size_t)PAD_L + 32) + 2 * sizeof(uint64_t) + BFRAG;
+  // adjoint step reading the stored stage states at the W_L x WMT_L shape: u, lam, U_1..U_3
+  // double-buffered (+ k for Kutta-3); z lives in the dead U slabs, so RK4 needs 10 slabs
+  // (6 CTAs/SM) -- the bound below (11) covers every scheme
+  static constexpr size_t adj_smem_ld = sizeof(double) * (11 * (size_t)PAD_L + 32) + 2 * sizeof(uint64_t) + BFRAG;
+  template <int SCH>
+  static constexpr size_t adj_smem_ld_s() {
+    return sizeof(double) * ((SCH == 1 ? 11 : 10) * (size_t)PAD_L + 32) + 2 * sizeof(uint64_t) + BFRAG;
+  }
   static constexpr int TE_MAX = TE_F > TE_A ? TE_F : TE_A;
 };
 

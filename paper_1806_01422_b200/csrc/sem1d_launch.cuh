@@ -326,7 +326,8 @@ cudaError_t launch_tile_sch(const PlanView& p, int kind, const TileStepArgs& a, 
     if constexpr (SCH == 0 || TC::adj_smem_ld > 227 * 1024) {
       return cudaErrorNotSupported;
     } else {
-      return launch_tile_one<N, tile_adj_kernel<N, TC::W_L, TC::WMT_L, SCH, 1>>(p, a, 32 * TC::W_L, TC::adj_smem_ld, TC::adj_smem_ld, s);
+      constexpr size_t sm = TC::template adj_smem_ld_s<SCH>();
+      return launch_tile_one<N, tile_adj_kernel<N, TC::W_L, TC::WMT_L, SCH, 1>>(p, a, 32 * TC::W_L, sm, sm, s);
     }
   }
   return launch_tile_one<N, tile_adj_kernel<N, TC::W_A, TC::WMT_A, SCH, 0>>(p, a, 32 * TC::W_A, TC::adj_smem, TC::adj_smem, s);
