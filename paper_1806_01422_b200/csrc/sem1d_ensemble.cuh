@@ -45,8 +45,8 @@ struct EnsArgs {
   Tableau tab;
 };
 
-// warps per ring: the forward sweep runs best with 16 warps x 2 m-tiles (128 regs),
-// the backward sweep with 8 warps x 4 m-tiles (A/B on config 4, profiles/)
+// warps per ring: forward 8 warps x 4 m-tiles at 2 rings per SM (see ENS_FWD_WARPS),
+// the backward sweep 8 warps x 4 m-tiles (A/B on config 4, profiles/)
 template <int N, int WARPS = 8>
 struct EnsCfg {
   static constexpr int n = N + 1;
@@ -54,7 +54,16 @@ struct EnsCfg {
   static constexpr int THREADS = 32 * W;
   static constexpr int NT = n / 8, KC = n / 4;
 };
-constexpr int kEnsFwdWarps = 16;
+// forward sweep: 8 warps x 4 interleaved m-tiles with 2 rings (CTAs) per SM, so one ring's
+// stage barriers overlap the other's DMMAs (config 4 forward 213.4 -> 205.9 ms against
+// 16 warps x 2 with one ring per SM)
+#ifndef ENS_FWD_WARPS
+#define ENS_FWD_WARPS 8
+#endif
+#ifndef ENS_FWD_MINB
+#define ENS_FWD_MINB 2
+#endif
+constexpr int kEnsFwdWarps = ENS_FWD_WARPS;
 constexpr int kEnsAdjWarps = 8;
 #ifndef TILE_WF16
 #define TILE_WF16 8     // tile forward warps at n = 16 (x 16/W m-tiles; 8 x 2 with ring_elem ILV: 0.178 vs 0.203 ms at 16 x 1)
@@ -255,7 +264,7 @@ struct TabC {
 // Forward sweep of one ring per CTA: periodic rings, E a multiple of 8 with
 // E/8 <= 8 * WMT_MAX.  Trajectory state n+1 is written after step n.
 template <int N, int WMT_MAX, bool ILV, int SCH>
-__global__ void __launch_bounds__(EnsCfg<N, ens_fwd_warps<N>()>::THREADS, 1)
+__global__ void __launch_bounds__(EnsCfg<N, ens_fwd_warps<N>()>::THREADS, ((N + 1) == 32 ? 1 : ENS_FWD_MINB))
     ens_forward_kernel(const __grid_constant__ Consts<N> C, const Geo G, const EnsArgs A) {
   constexpr int n = N + 1, KC = EnsCfg<N>::KC, NT = EnsCfg<N>::NT;
   constexpr int THREADS = EnsCfg<N, ens_fwd_warps<N>()>::THREADS;
