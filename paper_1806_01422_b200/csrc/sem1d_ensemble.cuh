@@ -1084,14 +1084,12 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
     // and form z_{i-1} in the same pass -- two barriers per stage
 #pragma unroll
     for (int i = S - 1; i >= 0; --i) {
-      constexpr bool Z0 = false;
       if (LD && i == S - 1)
         ring_jact<N, WMT, decltype(bget), false, TILE_ILV != 0, true, true>(C, Gt, Uarr(i), slam, xfer, bget, mnu, warp,
                                                                          lane, kv, TB::b(S - 1));
       else
         ring_jact<N, WMT, decltype(bget), false, TILE_ILV != 0, true>(C, Gt, Uarr(i), LD ? Uarr(i + 1) : sz, xfer, bget,
                                                                    mnu, warp, lane, kv);
-      (void)Z0;
       double* zdst = LD ? Uarr(i) : sz;         // LD: U_i is dead once its J^T has run
 #pragma unroll
       for (int q = 0; q < WMT; ++q) {
