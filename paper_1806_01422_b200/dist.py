@@ -84,7 +84,9 @@ class HaloExchange:
         self.p, self.group = part, group
 
     def refresh(self, fields):
-        """Fill the ghost nodes of every extended field in ``fields`` (batched)."""
+        """Fill the ghost nodes of every extended field in ``fields``: one batched P2P round
+        whose messages go straight from each field's owned edge slice into the neighbour's
+        ghost slice (contiguous views, no pack / unpack kernels)."""
         import torch
         import torch.distributed as dist
         p = self.p
@@ -92,10 +94,6 @@ class HaloExchange:
             return
         N = p.N
         o0, no = p.own0, p.n_own
-        k = len(fields)
-        ops = []
-        send_l = send_r = recv_l = recv_r = None
-        dev = fields[0].device
         L = p.gl * N                       # left ghost nodes I receive
         R = p.gr * N + (0 if p.zone else 1)  # right ghost nodes I receive
         # what the neighbours receive from me: every rank that has a left (right)
@@ -103,23 +101,25 @@ class HaloExchange:
         # zone*N in ghost-zone mode -- so the sizes are the neighbours', not mine
         to_left = p.zone * N if p.zone else N + 1
         to_right = p.zone * N if p.zone else 2 * N
-        if p.left is not None:      # my first nodes -> left neighbour's right ghost
-            send_l = torch.stack([f[o0:o0 + to_left] for f in fields]).contiguous()
-            recv_l = torch.empty((k, L), dtype=torch.float64, device=dev)
-        if p.right is not None:     # my last nodes -> right neighbour's left ghost
-            send_r = torch.stack([f[o0 + no - to_right:o0 + no] for f in fields]).contiguous()
-            recv_r = torch.empty((k, R), dtype=torch.float64, device=dev)
-        # fixed order (send_left, send_right, recv_right, recv_left) pairs the messages
-        # correctly even when left and right neighbour are the same rank (P = 2)
-        if send_l is not None:
-            ops.append(dist.P2POp(dist.isend, send_l, p.left, self.group, tag=1))
-        if send_r is not None:
-            ops.append(dist.P2POp(dist.isend, send_r, p.right, self.group, tag=2))
-        if recv_r is not None:
-            ops.append(dist.P2POp(dist.irecv, recv_r, p.right, self.group, tag=1))
-        if recv_l is not None:
-            ops.append(dist.P2POp(dist.irecv, recv_l, p.left, self.group, tag=2))
-        staged = dev.type == "cuda" and dist.get_backend(self.group) == "gloo"
+        # per field: send left, send right, receive right, receive left.  NCCL pairs the
+        # messages between two ranks in issue order (also when left and right neighbour are
+        # the same rank, P = 2); gloo pairs them by tag (2i: sent leftwards, 2i+1: rightwards)
+        ops, recvs = [], []
+        for i, f in enumerate(fields):
+            if p.left is not None:
+                ops.append(dist.P2POp(dist.isend, f[o0:o0 + to_left], p.left, self.group, tag=2 * i))
+            if p.right is not None:
+                ops.append(dist.P2POp(dist.isend, f[o0 + no - to_right:o0 + no], p.right, self.group,
+                                      tag=2 * i + 1))
+            if p.right is not None:
+                dst = f[o0 + no:o0 + no + R]
+                ops.append(dist.P2POp(dist.irecv, dst, p.right, self.group, tag=2 * i))
+                recvs.append(dst)
+            if p.left is not None:
+                dst = f[0:L]
+                ops.append(dist.P2POp(dist.irecv, dst, p.left, self.group, tag=2 * i + 1))
+                recvs.append(dst)
+        staged = fields[0].device.type == "cuda" and dist.get_backend(self.group) == "gloo"
         if staged:   # gloo moves CPU tensors only: stage through host memory
             ops = [dist.P2POp(o.op, o.tensor.cpu() if o.op is dist.isend else
                               torch.empty(o.tensor.shape, dtype=o.tensor.dtype), o.peer, self.group,
@@ -128,17 +128,8 @@ class HaloExchange:
         for r in dist.batch_isend_irecv(ops):
             r.wait()
         if staged:
-            k_r = 0
-            if recv_r is not None:
-                recv_r.copy_(recv_cpu[k_r])
-                k_r += 1
-            if recv_l is not None:
-                recv_l.copy_(recv_cpu[k_r])
-        for i, f in enumerate(fields):
-            if recv_l is not None:
-                f[0:L] = recv_l[i]
-            if recv_r is not None:
-                f[o0 + no:o0 + no + R] = recv_r[i]
+            for dst, src in zip(recvs, recv_cpu):
+                dst.copy_(src)
 
 
 def shard_grid(global_grid, part):
