@@ -88,16 +88,25 @@ cudaError_t ensure_frag(const sem1d_plan* p) {
     const int NT = n / 8, KC = n / 4;
     const double* K = p->packed.data();
     const double* Dw = K + n * n;
-    std::vector<double> h((size_t)3 * NT * KC * 32);
-    for (int mat = 0; mat < 3; ++mat)
+    // [K, Dw, Dw^T] as bfrag_perm, then [K, Dw] with the output row's -nu M^-1_i / M^-1_i folded
+    // in (bfrag_pre; periodic rings, interface rows take pattern entry 0)
+    const double* minv = p->minv.data();
+    std::vector<double> h((size_t)5 * NT * KC * 32);
+    for (int mat = 0; mat < 5; ++mat)
       for (int nt = 0; nt < NT; ++nt)
         for (int kc = 0; kc < KC; ++kc)
           for (int l = 0; l < 32; ++l) {
             const int c = 8 * nt + (l >> 2);
             const int i = 4 * (2 * (c >> 3) + (c & 1)) + ((c >> 1) & 3);
             const int j = 4 * kc + (l & 3);
-            h[(((size_t)mat * NT + nt) * KC + kc) * 32 + l] =
-                mat == 0 ? K[i * n + j] : (mat == 1 ? Dw[i * n + j] : Dw[j * n + i]);
+            const int m = mat < 3 ? mat : mat - 3;
+            double b = m == 0 ? K[i * n + j] : (m == 1 ? Dw[i * n + j] : Dw[j * n + i]);
+            if (mat >= 3) {
+              const double mi = minv[(i == 0 || i == p->N) ? 0 : i];
+              volatile double sc = (mat == 3) ? (-p->nu) * mi : mi;   // one rounding, as on the device
+              b = b * sc;
+            }
+            h[(((size_t)mat * NT + nt) * KC + kc) * 32 + l] = b;
           }
     double* d = nullptr;
     cudaError_t e = cudaMalloc(&d, sizeof(double) * h.size());

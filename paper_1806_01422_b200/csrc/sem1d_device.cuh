@@ -1000,10 +1000,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-template <int N, int OP>
+// PRE (F on periodic rings): the K / Dw fragments carry -nu M^-1_i / M^-1_i of the output row,
+// so kx and du are already scaled and the row is M^-1-scaled F
+template <int N, int OP, bool PRE = false>
 __device__ __forceinline__ double combine_rows(double kx, double du, double qq, double ui,
                                                double wi, double mnu) {
-  if (OP == OP_RHS) return __dsub_rn(__dmul_rn(kx, mnu), __dmul_rn(ui, du));
+  if (OP == OP_RHS) return PRE ? __dsub_rn(kx, __dmul_rn(ui, du)) : __dsub_rn(__dmul_rn(kx, mnu), __dmul_rn(ui, du));
   if (OP == OP_JAC)
     return __dsub_rn(__dsub_rn(__dmul_rn(kx, mnu), __dmul_rn(wi, du)), __dmul_rn(ui, qq));
   return __dsub_rn(__dsub_rn(__dmul_rn(kx, mnu), __dmul_rn(wi, du)), qq);
@@ -1017,7 +1019,7 @@ struct MTileOut {
   double r[N / 8 + 1][2];
 };
 
-template <int N, int OP, bool EDGE, class BGet>
+template <int N, int OP, bool EDGE, class BGet, bool PRE = false>
 __device__ __forceinline__ void mtile_compute(const Consts<N>& C, const Geo& G, const double* su,
                                               const double* sw, int base, int64_t eg,
                                               const double* minv_a, const double (*minv_p)[2],
@@ -1058,7 +1060,7 @@ __device__ __forceinline__ void mtile_compute(const Consts<N>& C, const Geo& G, 
       double wi = 0.0;
       if (OP == OP_JAC) wi = aw[kcp];
       if (OP == OP_JACT) wi = aw[kcp];   // already zm = mask(z M^-1)
-      r[nt][h] = combine_rows<N, OP>(h ? k1 : k0, h ? p1 : p0, h ? q1 : q0, ui, wi, mnu);
+      r[nt][h] = combine_rows<N, OP, PRE>(h ? k1 : k0, h ? p1 : p0, h ? q1 : q0, ui, wi, mnu);
     }
   }
 }
@@ -1068,6 +1070,11 @@ __device__ __forceinline__ void mtile_compute(const Consts<N>& C, const Geo& G, 
 #endif
 // n = 32: output n-tiles per accumulation group in mtile_compute_multi (A/B on config 3:
 // 1 / 2 / 4 -> J^T 90.0 / 88.3 / 88.0 us, F and J flat within 0.3%; 4 slowed J to 75.8 us)
+// F on periodic rings: -nu M^-1 / M^-1 folded into the K / Dw fragments (2 FP64 multiplies per
+// node fewer on the pipe the DMMAs share)
+#ifndef WS_PRE_F
+#define WS_PRE_F 1
+#endif
 #ifndef WS_NTG
 #define WS_NTG 2
 #endif
@@ -1092,7 +1099,7 @@ __device__ __forceinline__ int ws_left_row(int rr) {
 // Q m-tiles of one warp at once (elements wbase/weg + ws_le(q, rr)): the loops over the output
 // n-tiles and k-chunks are outermost, so each B fragment -- read from shared memory when
 // the n x n matrices do not fit the register file (n = 32) -- feeds Q DMMAs instead of one.
-template <int N, int OP, bool EDGE, int Q, bool ILV, class BGet>
+template <int N, int OP, bool EDGE, int Q, bool ILV, class BGet, bool PRE = false>
 __device__ __forceinline__ void mtile_compute_multi(const Consts<N>& C, const Geo& G, const double* su,
                                                     const double* sw, int wbase, int64_t weg, int rr,
                                                     const double* minv_a, double mnu, int kq, BGet bget,
@@ -1155,7 +1162,7 @@ __device__ __forceinline__ void mtile_compute_multi(const Consts<N>& C, const Ge
         for (int h = 0; h < 2; ++h) {
           const int kcp = 2 * (nt0 + g) + h;
           const double wi = (OP == OP_RHS) ? 0.0 : aw[q][kcp];
-          r[q][nt0 + g][h] = combine_rows<N, OP>(k[g][q][h], p[g][q][h], qq[g][q][h], au[q][kcp], wi, mnu);
+          r[q][nt0 + g][h] = combine_rows<N, OP, PRE>(k[g][q][h], p[g][q][h], qq[g][q][h], au[q][kcp], wi, mnu);
         }
   }
 }
@@ -1284,6 +1291,11 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
   // B fragments: a coalesced copy of the plan's device table (bfrag_perm order; J^T's Dw^T
   // table follows Dw's), else built from kernel-parameter space (lane-divergent reads: 13% of
   // the stall samples of the config-3 F kernel)
+  // F on a periodic ring reads the prescaled fragments (second part of the plan's table)
+  // (plain applies only: the RK-stage epilogue keeps the reference's association, which the
+  // adaptive Kutta-3 error estimate -- a cancellation at the tolerance level -- is sensitive to)
+  const bool pre = WS_PRE_F && OP == OP_RHS && EPI == EPI_STORE && periodic && frag != nullptr;
+  if (pre) frag += 3 * NT * KC * 32;
   if (W::B_IN_SMEM) {
     constexpr int TOT = NMAT * NT * KC * 32, PER = (TOT + W::THREADS - 1) / W::THREADS;
     if (frag) {                    // every load in flight before the first store
@@ -1372,6 +1384,9 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
         ws_fin_t du_ = 0, dw_ = 0;
         if (!periodic && (tl == 0 || tl == tiles_per_ring - 1))
           mtile_compute<N, OP, true>(C, G, su, sw, wq * WE * N, ehw, minv_a, minv_p, mnu, kq, bget, du_, dw_, r);
+        else if (pre)
+          mtile_compute<N, OP, false, decltype(bget), true>(C, G, su, sw, wq * WE * N, ehw, minv_a, minv_p, mnu, kq,
+                                                            bget, du_, dw_, r);
         else
           mtile_compute<N, OP, false>(C, G, su, sw, wq * WE * N, ehw, minv_a, minv_p, mnu, kq, bget, du_, dw_, r);
         if (kq == 3) hrow[s * W::CW + wq] = (!periodic && eh < 0) ? 0.0 : r[NT - 1][1];
@@ -1406,22 +1421,23 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
       if (lane == 0) bulk_wait_read<OUTB - 1>();   // the store out of this buffer has drained
       __syncwarp();
       double carry = 0.0;
-      auto body = [&](auto edge_tag) {
+      auto body = [&](auto edge_tag, auto pre_tag) {
         constexpr bool EDGE = decltype(edge_tag)::value;
+        constexpr bool PRE = decltype(pre_tag)::value;
         constexpr bool MULTI = W::B_IN_SMEM && (WMT > 1);
         // interleaved rows: A/B (config 2 / 3) F 86.5 -> 85.3 us, J 111.9 -> 111.0 (n = 8);
         // F 59.9 -> 55.4, J 77.9 -> 73.8 (n = 32); J^T at n = 8 measured slower (126.9 vs 112.2)
         constexpr bool ILVW = WS_ILV && (WMT == 2 || WMT == 4) && !(OP == OP_JACT && N == 7);
         double rq[WMT][NT][2];
         if constexpr (MULTI) {
-          mtile_compute_multi<N, OP, EDGE, WMT, ILVW>(C, G, su, sw, (wel0 + 1) * N, e0 + wel0, rr, minv_a,
-                                                      mnu, kq, bget, fin_u, fin_w, rq);
+          mtile_compute_multi<N, OP, EDGE, WMT, ILVW, decltype(bget), PRE>(C, G, su, sw, (wel0 + 1) * N, e0 + wel0, rr,
+                                                                          minv_a, mnu, kq, bget, fin_u, fin_w, rq);
         } else {
 #pragma unroll
           for (int q = 0; q < WMT; ++q) {
             const int le = ws_le<WMT, ILVW>(q, rr);
-            mtile_compute<N, OP, EDGE>(C, G, su, sw, (wel0 + le + 1) * N, e0 + wel0 + le, minv_a, minv_p, mnu, kq,
-                                       bget, fin_u, fin_w, rq[q]);
+            mtile_compute<N, OP, EDGE, decltype(bget), PRE>(C, G, su, sw, (wel0 + le + 1) * N, e0 + wel0 + le, minv_a,
+                                                            minv_p, mnu, kq, bget, fin_u, fin_w, rq[q]);
           }
         }
         // interface value of element le's node 0 (v = left row N + own row 0, or row 0 alone
@@ -1433,7 +1449,7 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
             if (EDGE && eg == 0) {
               if (OP != OP_JACT) v = __dmul_rn(v, C.minv[N]);
               v = __dmul_rn(v, 0.0);
-            } else if (OP != OP_JACT) {
+            } else if (OP != OP_JACT && !PRE) {
               v = __dmul_rn(v, minv_if);
             }
           }
@@ -1452,7 +1468,7 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
             for (int h = 0; h < 2; ++h) {
               const int i = 4 * (2 * nt + h) + kq;     // permuted row (= A column)
               if (live && i != 0 && i != N)
-                wout[le * N + i] = (OP == OP_JACT) ? r[nt][h] : __dmul_rn(r[nt][h], minv_a[2 * nt + h]);
+                wout[le * N + i] = (OP == OP_JACT || PRE) ? r[nt][h] : __dmul_rn(r[nt][h], minv_a[2 * nt + h]);
             }
           if constexpr (!ILVW) {
             const double row0 = r[0][0];              // valid in lanes kq == 0
@@ -1480,8 +1496,9 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
           }
         }
       };
-      if (edge) body(std::integral_constant<bool, true>{});
-      else body(std::integral_constant<bool, false>{});
+      if (edge) body(std::integral_constant<bool, true>{}, std::integral_constant<bool, false>{});
+      else if (OP == OP_RHS && pre) body(std::integral_constant<bool, false>{}, std::integral_constant<bool, OP == OP_RHS>{});
+      else body(std::integral_constant<bool, false>{}, std::integral_constant<bool, false>{});
       // first interface node of the warp: needs the halo row from the producer
       while (!mbar_try_wait(&halo[s], (it / STAGES) & 1)) {
       }
@@ -1491,7 +1508,7 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
         if (!periodic && eg == 0) {
           if (OP != OP_JACT) v = __dmul_rn(v, C.minv[N]);
           v = __dmul_rn(v, 0.0);
-        } else if (OP != OP_JACT) {
+        } else if (OP != OP_JACT && !pre) {
           v = __dmul_rn(v, minv_if);
         }
         wout[0] = v;
