@@ -21,11 +21,15 @@
  *                         timeloop.py:133-186, adjoint.py:64-69 (see below)
  *
  * Conventions (mirror the reference contract, ops.py:216-230):
- *  - every array is fp64 in DEVICE memory owned by the caller; nothing is
- *    allocated inside a compute call; inputs are never written;
+ *  - every array is fp64 in DEVICE memory owned by the caller; inputs are never
+ *    written; nothing is allocated inside a compute call except, once per plan
+ *    with N+1 % 8 == 0, the tensor-core B-fragment table on its first apply
+ *    (freed by sem1d_plan_destroy);
  *  - fields are `batch` consecutive vectors of `ndof` doubles
  *    (ndof = E*N periodic, E*N+1 homogeneous Dirichlet, grid.py:61-63);
  *  - calls are stream ordered (`stream` is a cudaStream_t, NULL = legacy default);
+ *    the applies and whole-step kernels use programmatic dependent launch and
+ *    wait (griddepcontrol.wait) before reading any global input;
  *  - non-finite inputs do not abort the kernel: they OR a bit into *flag
  *    (device int), which the host maps to NumericFailure / StepFailure;
  *  - return value: 0 ok, SEM1D_EINVAL bad argument, SEM1D_ECUDA launch error
