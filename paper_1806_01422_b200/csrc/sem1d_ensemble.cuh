@@ -472,13 +472,17 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
   const int pad = (ndof + 2 + 1) & ~1;
   using TB = TabC<SCH>;                       // compile-time tableau: stage loops unroll
   constexpr int S = TB::s;
+  // z of stage i-1 goes into the dead stage-state slab U_i and the first transposed stage reads
+  // b_{s-1} lam from the lam slab, so the slab a z buffer took holds the NEXT step's trajectory
+  // state, prefetched by one bulk copy while this step runs
   double* su = smem;                          // u_n (= U_0)
-  double* sUs = su + pad;                     // U_1 .. U_{S-1}: S-1 arrays
+  double* spre = su + pad;                    // u_{n-1} in flight
+  double* sUs = spre + pad;                   // U_1 .. U_{S-1}: S-1 arrays
   double* sk = sUs + 3 * pad;                 // k_0 (RK3 recompute) / an older l (RK3 chain)
-  double* sz = sk + pad;                      // zm for the current J^T
-  double* slam = sz + pad;                    // lam (owner-only)
+  double* slam = sk + pad;                    // lam (owner-only, + wrap mirror)
   double* xfer = slam + pad;
-  double* sB = xfer + 32;                     // B-fragment table (ens_adj_bsm), per lane
+  uint64_t* pbar = reinterpret_cast<uint64_t*>(xfer + 32);
+  double* sB = xfer + 34;                     // B-fragment table (ens_adj_bsm), per lane
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kq = lane & 3, rr = lane >> 2;
   const int64_t b = blockIdx.x, nb = gridDim.x;
@@ -530,16 +534,41 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
   const int mt_total = (int)G.E / 8;
   const double* lin = A.lam_in + b * G.ndof;
   for (int k = tid; k < ndof; k += THREADS) slam[k] = lin[k];
+  if (tid == 0) slam[ndof] = lin[0];
   unsigned fin = 0u;
   double kv[WMT_MAX][KC], lnext[WMT_MAX][KC], lacc[WMT_MAX][KC];
+  // trajectory states arrive by bulk copy when a state is a 16-byte multiple (every row of the
+  // step-major trajectory is then 16-byte aligned)
+  const bool bulk = ((ndof * 8) & 15) == 0;
+  const uint32_t sbytes = (uint32_t)(ndof * 8);
+  auto traj_row = [&](int step) { return A.traj + ((int64_t)step * nb + b) * G.ndof; };
+  if (tid == 0) {
+    mbar_init(pbar, 1);
+    fence_mbar_init();
+    if (bulk && A.nsteps > 0) {
+      mbar_expect_tx(pbar, sbytes);
+      bulk_g2s(su, traj_row(A.nsteps - 1), sbytes, pbar);
+    }
+  }
+  uint32_t pphase = 0;
 
   for (int step = A.nsteps - 1; step >= 0; --step) {
     const double dt = A.dts[step];
-    const double* un = A.traj + ((int64_t)step * nb + b) * G.ndof;
+    const double* un = traj_row(step);
     __syncthreads();   // previous step's readers of su / sUs are done
-    for (int k = tid; k < ndof; k += THREADS) su[k] = un[k];
-    if (tid == 0) su[ndof] = un[0];
+    if (bulk) {
+      while (!mbar_try_wait(pbar, pphase)) {
+      }
+      pphase ^= 1u;
+    } else {
+      for (int k = tid; k < ndof; k += THREADS) su[k] = un[k];
+    }
+    if (tid == 0) su[ndof] = bulk ? su[0] : un[0];
     __syncthreads();
+    if (bulk && step > 0 && tid == 0) {   // u_{n-1} into the buffer u_{n+1} left
+      mbar_expect_tx(pbar, sbytes);
+      bulk_g2s(spre, traj_row(step - 1), sbytes, pbar);
+    }
     // ---- stage states U_1..U_{S-1} (timeloop.rk3_stages, adjoint.py:56)
 #pragma unroll
     for (int i = 0; i + 1 < S; ++i) {
@@ -592,16 +621,19 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
         const int g = ring_elem<WMT_MAX, ILV>(warp, q, rr) * N + j;
         const double z = zval(S - 1, g, q, kc);
         fin |= nonfinite_bit(z);
-        sz[g] = z;
-        if (g == 0) sz[ndof] = z;
       }
     }
-    __syncthreads();
-    // per stage: J^T apply (its internal barrier ends every read of sz), then accumulate
-    // l_i and form z_{i-1} in one pass -- two barriers per stage
+    // per stage: J^T apply (its internal barrier ends every read of its z and U_i), then
+    // accumulate l_i and form z_{i-1} (into the dead U_i) in one pass -- two barriers per stage
 #pragma unroll
     for (int i = S - 1; i >= 0; --i) {
-      ring_jact<N, WMT_MAX, decltype(bget), true, ILV, true>(C, G, Uarr(i), sz, xfer, bget, mnu, warp, lane, kv);
+      if (i == S - 1)
+        ring_jact<N, WMT_MAX, decltype(bget), true, ILV, true, true>(C, G, Uarr(i), slam, xfer, bget, mnu, warp, lane,
+                                                                   kv, TB::b(S - 1));
+      else
+        ring_jact<N, WMT_MAX, decltype(bget), true, ILV, true>(C, G, Uarr(i), Uarr(i + 1), xfer, bget, mnu, warp, lane,
+                                                             kv);
+      double* zdst = Uarr(i);
 #pragma unroll
       for (int q = 0; q < WMT_MAX; ++q) {
         const int mt = warp * WMT_MAX + q;
@@ -616,16 +648,23 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
           if (i + 1 < S && S == 3) sk[g] = lnext[q][kc];   // RK3: keep l_{i+1} for z_{i-1}
           lnext[q][kc] = l;
           if (i == 0) {
-            slam[g] = __dadd_rn(slam[g], lacc[q][kc]);
+            const double lv = __dadd_rn(slam[g], lacc[q][kc]);
+            slam[g] = lv;
+            if (g == 0) slam[ndof] = lv;
           } else {
             const double z = zval(i - 1, g, q, kc);
             fin |= nonfinite_bit(z);
-            sz[g] = z;
-            if (g == 0) sz[ndof] = z;
+            zdst[g] = z;
+            if (g == 0) zdst[ndof] = z;
           }
         }
       }
       __syncthreads();
+    }
+    if (bulk) {                                // swap the trajectory buffers
+      double* t = su;
+      su = spre;
+      spre = t;
     }
   }
   double* lo = A.lam_out + b * G.ndof;
@@ -636,7 +675,7 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
 template <int N>
 constexpr size_t ens_adj_smem_bytes(int ndof) {
   constexpr size_t frag = ens_adj_bsm<N>() ? 5 * EnsCfg<N>::NT * EnsCfg<N>::KC * 32 : 0;
-  return sizeof(double) * (7 * (size_t)((ndof + 2 + 1) & ~1) + 32 + frag);
+  return sizeof(double) * (7 * (size_t)((ndof + 2 + 1) & ~1) + 34 + frag);
 }
 
 // ============================================================================
