@@ -708,7 +708,7 @@ constexpr size_t ens_adj_smem_bytes(int ndof) {
 #define TILE_WA16 8
 #endif
 #ifndef TILE_WL8
-#define TILE_WL8 4
+#define TILE_WL8 8      // stored-stage adjoint at n = 8: 8 warps x 2 m-tiles, 3 CTAs/SM (0.445 vs 0.472 ms at 4 x 2 x 6)
 #endif
 #ifndef TILE_WMTL8
 #define TILE_WMTL8 2
@@ -783,7 +783,7 @@ __device__ __forceinline__ void tile_issue_n(const TileLoad& L, int LEN, const d
 template <int N>
 constexpr int tile_minb() { return (N + 1) == 8 ? TILE_MINB8 : 1; }
 #ifndef TILE_ADJ_LD_MINB8
-#define TILE_ADJ_LD_MINB8 6
+#define TILE_ADJ_LD_MINB8 3
 #endif
 template <int N, int MODE = 0>
 constexpr int tile_adj_minb() { return (N + 1) == 8 ? (MODE == 1 ? TILE_ADJ_LD_MINB8 : TILE_ADJ_MINB8) : 1; }
