@@ -696,13 +696,13 @@ constexpr size_t ens_adj_smem_bytes(int ndof) {
 #define TILE_WMT8 4
 #endif
 #ifndef TILE_WA8
-#define TILE_WA8 8      // recompute adjoint at n = 8: 8 warps x 2 m-tiles (0.653 vs 0.682 ms at 4 x 4)
+#define TILE_WA8 8      // recompute adjoint at n = 8: 8 warps x 4 m-tiles, 7 slabs, 2 CTAs/SM (0.624 ms; 0.649 at 8 x 2 x 3)
 #endif
 #ifndef TILE_WF8
 #define TILE_WF8 8
 #endif
 #ifndef TILE_WMTA8
-#define TILE_WMTA8 2
+#define TILE_WMTA8 4
 #endif
 #ifndef TILE_WA16
 #define TILE_WA16 8
@@ -714,7 +714,7 @@ constexpr size_t ens_adj_smem_bytes(int ndof) {
 #define TILE_WMTL8 2
 #endif
 #ifndef TILE_ADJ_MINB8
-#define TILE_ADJ_MINB8 3
+#define TILE_ADJ_MINB8 2
 #endif
 
 struct TileStepArgs {
@@ -951,13 +951,12 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
   constexpr bool LD = MODE == 1;
   using TB = TabC<SCH>;                       // compile-time tableau: stage loops unroll
   constexpr int S = TB::s;
-  // LD: z of stage i-1 goes into the (dead) stage-state slab U_i and the first stage reads
+  // z of stage i-1 goes into the (dead) stage-state slab U_i and the first stage reads
   // b_{s-1} lam from the lam slab, so there is no z slab; k (Kutta-3's older l) only for s = 3
-  // -- 10 slabs for RK4, 6 CTAs/SM
+  // -- RK4: 10 slabs with stored stages, 7 with recompute
   double* sUs = sbl + 2 * PAD;
   double* sk = sUs + (LD ? 6 : 3) * PAD;
-  double* sz = sk + ((LD && S != 3) ? 0 : PAD);
-  double* xfer = LD ? sz : sz + PAD;
+  double* xfer = sk + (S == 3 ? PAD : 0);
   uint64_t* bar = reinterpret_cast<uint64_t*>(xfer + 32);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int kq = lane & 3, rr = lane >> 2;
@@ -1112,24 +1111,19 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
         const int g = e * N + j;
         const double z = zval(S - 1, g, q, kc);
         if (e >= H && e < H + T) fin |= nonfinite_bit(z);
-        if (!LD) sz[g] = z;
       }
-    }
-    if (!LD) {
-      if (tid == 0) sz[TE * N] = 0.0;         // last node of the open chain (ghost margin)
-      __syncthreads();
     }
     // per stage: J^T apply (its internal barrier ends every read of sz), then accumulate l_i
     // and form z_{i-1} in the same pass -- two barriers per stage
 #pragma unroll
     for (int i = S - 1; i >= 0; --i) {
-      if (LD && i == S - 1)
+      if (i == S - 1)
         ring_jact<N, WMT, decltype(bget), false, TILE_ILV != 0, true, true>(C, Gt, Uarr(i), slam, xfer, bget, mnu, warp,
                                                                          lane, kv, TB::b(S - 1));
       else
-        ring_jact<N, WMT, decltype(bget), false, TILE_ILV != 0, true>(C, Gt, Uarr(i), LD ? Uarr(i + 1) : sz, xfer, bget,
-                                                                   mnu, warp, lane, kv);
-      double* zdst = LD ? Uarr(i) : sz;         // LD: U_i is dead once its J^T has run
+        ring_jact<N, WMT, decltype(bget), false, TILE_ILV != 0, true>(C, Gt, Uarr(i), Uarr(i + 1), xfer, bget, mnu, warp,
+                                                                   lane, kv);
+      double* zdst = Uarr(i);                   // U_i is dead once its J^T has run
 #pragma unroll
       for (int q = 0; q < WMT; ++q) {
         const int e = ring_elem<WMT, TILE_ILV != 0>(warp, q, rr);
@@ -1151,7 +1145,7 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
           }
         }
       }
-      if (LD && i > 0 && tid == 0) zdst[TE * N] = 0.0;   // last node of the open chain
+      if (i > 0 && tid == 0) zdst[TE * N] = 0.0;   // last node of the open chain
       __syncthreads();
     }
     const int64_t e_out0 = (int64_t)t * T;
@@ -1167,9 +1161,9 @@ struct TileCfg {
   // forward: TE = 256 elements for N = 7 (8 warps x 4 m-tiles, 2 CTAs per SM: the second
   // CTA's DMMA fills the first one's barrier waits; A/B 0.48 vs 0.54 ms per RK4 step at
   // 16 x 4 x 1), 128 for N = 15/23 (N = 15: 8 warps x 2 interleaved m-tiles), 64 for N = 31;
-  // adjoint: 128 for N = 7 (8 warps x 2 m-tiles, 3 CTAs per SM; with the compile-time
-  // tableaux 0.653 ms vs 0.682 at 4 x 4 x 3 and 0.735 at 4 x 2), 128 / 64 otherwise (nine
-  // slabs must fit the shared memory of the resident CTAs)
+  // adjoint: 256 for N = 7 (8 warps x 4 m-tiles, 2 CTAs per SM with the 7-slab layout:
+  // 0.624 ms vs 0.649 at 8 x 2 x 3, 0.682 at 4 x 4 x 3), 128 / 64 otherwise (the slabs must
+  // fit the shared memory of the resident CTAs)
   static constexpr int W = (N + 1) == 32 ? 8 : ((N + 1) == 8 ? TILE_WF8 : ((N + 1) == 16 ? TILE_WF16 : TILE_WF24));
   // adjoint warps: 8 x 2 m-tiles for N = 15/23 (at 16 warps the 128-register cap made the
   // compiler re-read the B fragments from kernel-parameter space with lane-divergent
@@ -1188,7 +1182,13 @@ struct TileCfg {
   static constexpr int PAD_A = ((TE_A * N + 1 + 2) + 1) & ~1;
   static constexpr size_t fwd_smem = sizeof(double) * (4 * (size_t)PAD_F + 32) + 2 * sizeof(uint64_t);
   static constexpr size_t BFRAG = ((N + 1) == 32) ? sizeof(double) * 5 * ((N + 1) / 8) * ((N + 1) / 4) * 32 + 16 : 0;
-  static constexpr size_t adj_smem = sizeof(double) * (9 * (size_t)PAD_A + 32) + 2 * sizeof(uint64_t) + BFRAG;
+  // recompute mode: u, lam double-buffered + U_1..U_3 (+ k for Kutta-3); the bound covers every
+  // scheme, adj_smem_s<SCH> is the launch size
+  static constexpr size_t adj_smem = sizeof(double) * (8 * (size_t)PAD_A + 32) + 2 * sizeof(uint64_t) + BFRAG;
+  template <int SCH>
+  static constexpr size_t adj_smem_s() {
+    return sizeof(double) * ((SCH == 1 ? 8 : 7) * (size_t)PAD_A + 32) + 2 * sizeof(uint64_t) + BFRAG;
+  }
   // adjoint step reading the stored stage states at the W_L x WMT_L shape: u, lam, U_1..U_3
   // double-buffered (+ k for Kutta-3); z lives in the dead U slabs, so RK4 needs 10 slabs
   // (6 CTAs/SM) -- the bound below (11) covers every scheme

@@ -330,7 +330,8 @@ cudaError_t launch_tile_sch(const PlanView& p, int kind, const TileStepArgs& a, 
       return launch_tile_one<N, tile_adj_kernel<N, TC::W_L, TC::WMT_L, SCH, 1>>(p, a, 32 * TC::W_L, sm, sm, s);
     }
   }
-  return launch_tile_one<N, tile_adj_kernel<N, TC::W_A, TC::WMT_A, SCH, 0>>(p, a, 32 * TC::W_A, TC::adj_smem, TC::adj_smem, s);
+  constexpr size_t sma = TC::template adj_smem_s<SCH>();
+  return launch_tile_one<N, tile_adj_kernel<N, TC::W_A, TC::WMT_A, SCH, 0>>(p, a, 32 * TC::W_A, sma, sma, s);
 }
 
 // Temporally blocked RK step / adjoint step for large periodic rings (batch 1).
