@@ -8,9 +8,9 @@ needed between steps.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
---impl reference times the reference algorithm's CPU implementation (the numpy
-port in oracle/, bit-identical to semopt 0.1.0 on the golden fixtures) on the
-host cores, on a bounded sample of the same workload.
+--impl reference times the reference's own CPU implementation (stock semopt 0.1.0,
+installed unmodified into baseline/_ref) on the host cores, on the same full
+config-2 step.
 Under torchrun (N > 1) the ranks share ONE periodic ring of N * 2^22 elements,
 element-sharded (dist.py): every operator input gets a ghost-node exchange with
 the two neighbouring ranks over NCCL (weak scaling); timing is the max over ranks.
@@ -98,26 +98,80 @@ def cpu_reference_step_sample(E_sample, reps, seed):
     return mesh.ndof, times
 
 
+def workload_config(world):
+    """The `config` object shared by both arms (same workload, same keys)."""
+    from paper_1806_01422_b200 import configs
+    c = configs.CFG2
+    return {"workload": "BASELINE config 2: 1D Burgers, E=2^22, N=7, nu=0.01, periodic [-1,1]",
+            "value": VALUE_DEF, "E": c["E"], "N": c["N"], "dof": c["E"] * c["N"],
+            "l2": "inputs 235 MB/field > 126 MB L2, no flush",
+            "parallelism": "single GPU" if world == 1 else
+            f"x{world} independent config-2 replicas at N=1's size + strong-scaled config-5 sweep (see scaling)"}
+
+
+REF_PATH = os.path.join(ROOT, "baseline", "_ref")
+
+
+def import_stock_reference():
+    """The unmodified reference package (semopt 0.1.0), installed into baseline/_ref by
+    `pip install --no-index --no-build-isolation --no-deps --target baseline/_ref <copy of
+    /root/reference/pkg>`.  Returns None when it is absent."""
+    if not os.path.isdir(os.path.join(REF_PATH, "semopt")):
+        return None
+    if REF_PATH not in sys.path:
+        sys.path.insert(0, REF_PATH)
+    import semopt.grid
+    import semopt.ops
+    return semopt
+
+
 def run_reference_arm(args):
+    """The reference's own CPU path, timed on the host cores: stock semopt
+    SemOperator.apply_rhs / apply_jacobian / apply_jacobian_transpose (ops.py:232-257) on the
+    FULL config-2 field, numpy/OpenBLAS with every host thread.  Falls back to the
+    bit-identical numpy port (oracle/semref.py) only if baseline/_ref is missing."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    E_sample = 1 << 18
-    ndof, times = cpu_reference_step_sample(E_sample, args.warmup + args.steps, seed=12)
+    import numpy as np
+
+    from paper_1806_01422_b200 import configs
+    c = configs.CFG2
+    semopt = import_stock_reference()
+    cores = host_cores()
+    u = v = w = None
+    if semopt is not None:
+        g = semopt.grid.grid_1d(c["xa"], c["xb"], c["E"], c["N"])
+        op = semopt.ops.SemOperator(g, semopt.ops.PdeCoefficients(c["nu"]))
+        ndof = g.nglobal
+        kind, what = "reference", "stock semopt 0.1.0 from baseline/_ref (ops.py:232-257)"
+        f_rhs, f_jac, f_jact = op.apply_rhs, op.apply_jacobian, op.apply_jacobian_transpose
+    else:
+        from oracle import semref as R
+        op = R.BurgersOracle(R.Mesh1D(c["xa"], c["xb"], c["E"], c["N"], True), c["nu"])
+        ndof = op.mesh.ndof
+        kind, what = "port", "numpy port of semopt ops.py (oracle/semref.py; baseline/_ref absent)"
+        f_rhs, f_jac, f_jact = op.rhs, op.jac, op.jact
+    u, v, w = configs.operator_inputs(ndof, c["seed"])
+    times = []
+    for _ in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        f_rhs(u)
+        f_jac(u, v)
+        f_jact(u, w)
+        times.append(time.perf_counter() - t0)
     timed = times[args.warmup:]
     total = sum(timed)
     value = 3 * ndof * len(timed) / total
-    cores = host_cores()
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "DOF/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * total / len(timed), "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded U(-1,1), N(0,1) per node)",
-        "config": {"workload": "BASELINE config 2 (1D Burgers, N=7, nu=0.01, periodic [-1,1])", "value": VALUE_DEF,
-                   "E": 1 << 22, "N": 7, "sample_E": E_sample, "sample_dof": ndof},
-        "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": cores, "kind": "port",
-                         "sample": f"F+J+J^T on E=2^18 of config 2 (same h, N, nu), "
-                                   f"numpy/OpenBLAS port of semopt ops.py, {cores} host threads"},
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded u~U(-1,1), v,w~N(0,1) per node)",
+        "config": workload_config(1),
+        "cpu_baseline": {"value": value, "unit": "DOF/s", "cores": cores, "kind": kind,
+                         "sample": f"the full config-2 step (F+J+J^T once each on all {ndof} DOF), "
+                                   f"{what}, numpy {np.__version__} / OpenBLAS, {cores} host threads"},
         "e2e": {"value": value, "unit": "DOF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -433,7 +487,8 @@ def run_gpu_arm(args):
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded u~U(-1,1), v,w~N(0,1) per node)",
-        "config": {"workload": "BASELINE config 2: 1D Burgers, E=2^22, N=7, nu=0.01, periodic [-1,1]",
+        "config": workload_config(1) if world == 1 else
+                  {"workload": "BASELINE config 2: 1D Burgers, E=2^22, N=7, nu=0.01, periodic [-1,1]",
                    "value": VALUE_DEF, "E": c["E"], "N": c["N"], "dof": ndof,
                    "per_rank_problem": "2^22 elements" + ("" if world == 1 else
                                        " of one element-sharded ring (ghost exchange per input)"),

@@ -217,6 +217,121 @@ class BurgersOracle:
         return cols
 
 
+class LongDoubleBurgers:
+    """ops.py:161-212 (+ the M^-1 / mask finishing of :226-257) evaluated in np.longdouble.
+
+    The constants are the reference's own fp64 K, Dw and M^-1 (the same bits the oracle and
+    the GPU start from); only the evaluation arithmetic is extended (x86 80-bit, 64-bit
+    mantissa).  |oracle - LD| is then the oracle's own rounding noise for an input, the yard
+    stick of the smooth-input parity bound of SURVEY.md 8(c) item 2:
+    |GPU - oracle| <= max(1e-12 ||oracle||_inf, 4 |oracle - LD|_inf)."""
+
+    LD = np.longdouble
+
+    def __init__(self, fp64_oracle):
+        o = fp64_oracle
+        self.mesh = o.mesh
+        self.nu = self.LD(o.nu)
+        self.K = o.K.astype(self.LD)
+        self.Dw = o.Dw.astype(self.LD)
+        self.minv = o.minv.astype(self.LD)
+
+    def _loc(self, x):
+        x = np.asarray(x)
+        return (x if x.dtype == self.LD else x.astype(float).astype(self.LD))[self.mesh.table]
+
+    def _asm(self, local):
+        out = np.zeros(self.mesh.ndof, dtype=self.LD)
+        np.add.at(out, self.mesh.table.ravel(), local.ravel())       # 2 terms per node: exact order-free
+        return out
+
+    def _mask(self, x):
+        return x if self.mesh.periodic else x * self.mesh.maskv.astype(self.LD)
+
+    def _mv(self, xl, A):
+        return np.einsum("ej,ij->ei", xl, A)                          # x @ A.T in longdouble
+
+    def rhs(self, u):
+        ul = self._loc(u)
+        acc = -self.nu * self._mv(ul, self.K) - ul * self._mv(ul, self.Dw)
+        return self._mask(self._asm(acc) * self.minv)
+
+    def jac(self, u, v):
+        ul, vl = self._loc(u), self._loc(v)
+        acc = -self.nu * self._mv(vl, self.K) - vl * self._mv(ul, self.Dw) - ul * self._mv(vl, self.Dw)
+        return self._mask(self._asm(acc) * self.minv)
+
+    def jact(self, u, z):
+        zm = self._mask(np.asarray(z, dtype=float).astype(self.LD) * self.minv)
+        ul, zl = self._loc(u), zm[self.mesh.table]
+        acc = (-self.nu * self._mv(zl, self.K) - zl * self._mv(ul, self.Dw)
+               - np.einsum("ej,ji->ei", ul * zl, self.Dw))
+        return self._mask(self._asm(acc))
+
+    def rk_step(self, u, dt, scheme):
+        """One explicit RK step (rk_step above) with every stage in longdouble."""
+        A, b = TABLEAUX[scheme]
+        dt = self.LD(dt)
+        u0 = np.asarray(u, dtype=float).astype(self.LD)
+        ks, U = [], u0
+        for i in range(len(b)):
+            if i > 0:
+                U = u0 + dt * sum(self.LD(a) * k for a, k in zip(A[i], ks))
+            ks.append(self.rhs(U))
+        return u0 + dt * sum(self.LD(bi) * k for bi, k in zip(b, ks))
+
+    def _jact_ld(self, U, z):
+        zm = self._mask(z * self.minv)
+        ul, zl = U[self.mesh.table], zm[self.mesh.table]
+        acc = (-self.nu * self._mv(zl, self.K) - zl * self._mv(ul, self.Dw)
+               - np.einsum("ej,ji->ei", ul * zl, self.Dw))
+        return self._mask(self._asm(acc))
+
+    def adjoint_rk_step(self, u, lam, dt, scheme):
+        """adjoint_rk_step above (adjoint.py:50-61 generalised) with every stage in longdouble."""
+        A, b = TABLEAUX[scheme]
+        dt = self.LD(dt)
+        u0 = np.asarray(u, dtype=float).astype(self.LD)
+        lam0 = np.asarray(lam, dtype=float).astype(self.LD)
+        Us, ks = [u0], []
+        for i in range(1, len(b)):
+            ks.append(self.rhs(Us[-1]))
+            Us.append(u0 + dt * sum(self.LD(a) * k for a, k in zip(A[i], ks)))
+        s = len(b)
+        ls = [None] * s
+        for i in range(s - 1, -1, -1):
+            z = self.LD(b[i]) * lam0
+            for j in range(i + 1, s):
+                a = A[j][i] if i < len(A[j]) else 0.0
+                if a != 0.0:
+                    z = z + self.LD(a) * ls[j]
+            ls[i] = dt * self._jact_ld(Us[i], z)
+        return lam0 + sum(ls)
+
+
+def smooth_fields(mesh, seed=0):
+    """Smooth periodic inputs for the noise-floor-aware parity bound:
+    a few low Fourier modes of the node coordinates with seeded amplitudes and phases."""
+    rng = np.random.default_rng(seed)
+    x = mesh.coordinates()
+    L = mesh.xb - mesh.xa
+    out = []
+    for _ in range(3):
+        f = np.zeros(mesh.ndof)
+        for k in range(1, 4):
+            f += rng.uniform(-1, 1) * np.sin(2.0 * np.pi * k * (x - mesh.xa) / L + rng.uniform(0, 2 * np.pi))
+        out.append(f)
+    return tuple(out)
+
+
+def ld_bound(gpu, oracle, ld):
+    """(err, bound): err = |GPU - oracle|_inf; bound = max(1e-12 ||oracle||_inf, 4 |oracle - LD|_inf)."""
+    gpu = np.asarray(gpu, dtype=float)
+    oracle = np.asarray(oracle, dtype=float)
+    noise = float(np.max(np.abs(oracle.astype(np.longdouble) - ld)))
+    return float(np.max(np.abs(gpu - oracle))), max(1e-12 * float(np.max(np.abs(oracle))), 4.0 * noise)
+
+
 class AdvectionOracle(BurgersOracle):
     """The LINEAR (constant speed a) and NONE advection branches of ops.py:147-212 in 1D:
     F = M^-1 Q^T(-nu K u - a Dw u), J v = F-part on v, J^T z = Q^T(-nu K zm - a Dw^T zm)."""

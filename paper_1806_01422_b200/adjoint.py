@@ -76,17 +76,19 @@ class AdjointEngine:
             self._L = {i: self.op.empty() for i in range(1, self.s)}
         return self._L
 
-    def step(self, u_n, lam, dt, lam_out, stages=None):
+    def step(self, u_n, lam, dt, lam_out, stages=None, flag=None):
         """lam_out = transpose of the step map at u_n applied to lam (no host sync).
         ``stages``: the step's stage states U_1..U_{s-1} stored by the forward run (fused
-        path): no recompute."""
+        path): no recompute.  ``flag``: device address of this step's own flag word (fused
+        path, ``sweep`` running ahead); default the operator's flag."""
         op, s = self.op, self.s
         fused = getattr(op, "step_fused_supported", None)
         if fused is not None and fused():
+            kw = {} if flag is None else {"flag": flag}
             if stages is not None and s > 1:
-                op.launch_adj_step_stages(u_n, stages, lam, lam_out, dt, self.scheme)
+                op.launch_adj_step_stages(u_n, stages, lam, lam_out, dt, self.scheme, **kw)
             else:
-                op.launch_adj_step(u_n, lam, lam_out, dt, self.scheme)
+                op.launch_adj_step(u_n, lam, lam_out, dt, self.scheme, **kw)
                 op.counters["rhs"] += s - 1
             op.counters["jact"] += s
             return
@@ -111,8 +113,8 @@ def adjoint_engine_for(op, scheme):
     return e
 
 
-def _check_adjoint_flags(op):
-    v = op.flags()
+def _check_adjoint_flags(op, v=None):
+    v = op.flags() if v is None else v
     if v & _lib.SEM1D_FLAG_STATE_NONFINITE:
         raise NumericFailure("state contains NaN/Inf")
     if v & _lib.SEM1D_FLAG_INPUT2_NONFINITE:
@@ -145,13 +147,22 @@ def adjoint_step_cn(op, u_n, u_np1, lam, t, dt, cfg, stats=None, out=None):
     return out.cpu().numpy() if host else out
 
 
-def sweep(op, cfg, fwd, schedule, lam_terminal, check_every=1):
+_ADJ_WINDOW = 16      # adjoint steps launched between two flag reads (run-ahead sweep)
+
+
+def sweep(op, cfg, fwd, schedule, lam_terminal, check_every=None):
     """Backward sweep over a recorded trajectory (adjoint.py:72-158).
 
     Schedule semantics, CheckpointError conditions and ``last_sweep_stats``
     follow the reference; states are device tensors, a Store keeps a
     reference (states are never mutated in place), an Advance re-runs the
     recorded dts through the same fused stage kernels (bitwise replay).
+
+    Flags: on the fused step kernels the sweep runs ahead (``check_every=None``): each
+    adjoint step ORs its non-finite bits into its own flag word and one device->host read
+    verifies up to _ADJ_WINDOW steps (and always before a recompute Advance and at the
+    end).  The first flagged step raises the same NumericFailure, with the same counters, as
+    the per-step check (``check_every=1``) would have.
     """
     m = fwd.n_steps
     if schedule.n_steps != m:
@@ -189,6 +200,31 @@ def sweep(op, cfg, fwd, schedule, lam_terminal, check_every=1):
     spare = op.empty()
     since_check = 0
     op.flags()
+    fz = getattr(op, "step_fused_supported", None)
+    ahead = (check_every is None and not cn and getattr(op, "supports_flag_slots", False)
+             and fz is not None and fz())
+    check_every = 1 if check_every is None else check_every
+    pending = []                       # (step, counters after it) of the unverified steps
+    if ahead:
+        wslots = op.flag_slots(_ADJ_WINDOW)
+        wslots.zero_()
+        wslot0 = wslots.data_ptr()
+
+    def verify():
+        if not pending:
+            return
+        words = wslots[:len(pending)]
+        red = getattr(op, "reduce_flag_words", None)      # sharded: OR over ranks
+        vals = (red(words) if red is not None else words).cpu().tolist()
+        wslots.zero_()
+        bad = next((i for i, v in enumerate(vals) if v), None)
+        if bad is not None:
+            op.counters.clear()
+            op.counters.update(pending[bad][1])          # as if the sweep stopped at that step
+            pending.clear()
+            _check_adjoint_flags(op, vals[bad])
+        pending.clear()
+
     for act in actions:
         if isinstance(act, Restore):
             if act.slot not in slots or slots[act.slot][0] != act.step:
@@ -201,6 +237,8 @@ def sweep(op, cfg, fwd, schedule, lam_terminal, check_every=1):
         elif isinstance(act, Advance):
             if current is None or current[0] != act.start:
                 raise CheckpointError(f"advance from step {act.start}: state not in hand")
+            if ahead:
+                verify()                   # the per-step loop would have raised before this
             u = current[1]
             for n in range(act.start, act.stop):
                 nxt = op.empty()
@@ -224,17 +262,27 @@ def sweep(op, cfg, fwd, schedule, lam_terminal, check_every=1):
             if cn:
                 u_np1 = succ[1] if succ[0] == n + 1 else fwd.u_final
                 adjoint_step_cn(op, current[1], u_np1, lam, fwd.ts[n], dts[n], cfg, stats, out=spare)
+            elif ahead:
+                adj.step(current[1], lam, dts[n], spare, stages=stage_snaps.get(n),
+                         flag=wslot0 + 4 * len(pending))
+                pending.append((n, dict(op.counters)))
             else:
                 adj.step(current[1], lam, dts[n], spare, stages=stage_snaps.get(n))
             lam, spare = spare, lam
-            since_check += 1
-            if since_check >= check_every:
-                _check_adjoint_flags(op)
-                since_check = 0
+            if ahead:
+                if len(pending) == _ADJ_WINDOW:
+                    verify()
+            else:
+                since_check += 1
+                if since_check >= check_every:
+                    _check_adjoint_flags(op)
+                    since_check = 0
             succ = current
             next_adj -= 1
         elif isinstance(act, Done):
             break
+    if ahead:
+        verify()
     _check_adjoint_flags(op)
     if next_adj != -1:
         raise CheckpointError(f"sweep incomplete: stopped before adjoint step {next_adj}")

@@ -50,6 +50,7 @@ struct sem1d_plan {
   mutable double* dfrag = nullptr;
   mutable std::once_flag frag_once;
   mutable cudaError_t frag_err = cudaSuccess;
+  int device = 0;              // the device current at sem1d_plan_create; every call runs there
 };
 
 namespace {
@@ -71,6 +72,7 @@ int fail(int code, const std::string& msg) { return sem1d::set_error(code, msg);
 
 namespace sem1d {
 int64_t plan_batch(const sem1d_plan* p) { return p ? p->batch : 0; }
+int plan_device(const sem1d_plan* p) { return p ? p->device : -1; }
 }  // namespace sem1d
 
 namespace {
@@ -464,6 +466,7 @@ int run_adv(const sem1d_plan* p, int op, const double* u, const double* w, doubl
 }  // namespace
 
 int sem1d_plan_set_advection(sem1d_plan* plan, int mode, double speed) {
+  DeviceGuard guard_(plan ? plan->device : -1);
   if (!plan || mode < 0 || mode > 2 || !std::isfinite(speed))
     return fail(SEM1D_EINVAL, "sem1d_plan_set_advection: bad argument (mode 0 burgers, 1 linear, 2 none)");
   plan->adv = mode;
@@ -505,6 +508,7 @@ int sem1d_plan_create(int64_t n_elements, int degree, int periodic, double nu, c
   p->ndof = n_elements * degree + (periodic ? 0 : 1);
   p->batch = batch;
   p->nu = nu;
+  if (cudaGetDevice(&p->device) != cudaSuccess) p->device = 0;
   p->mass.assign(mass_pattern, mass_pattern + degree + 2);
   p->minv.assign(minv_pattern, minv_pattern + degree + 2);
   // Consts<N> image: K[n*n], Dw[n*n], minv[N+2], mass[N+2], nu
@@ -519,6 +523,7 @@ int sem1d_plan_create(int64_t n_elements, int degree, int periodic, double nu, c
 }
 
 int sem1d_plan_destroy(sem1d_plan* plan) {
+  DeviceGuard guard_(plan ? plan->device : -1);
   if (plan && plan->dconst) cudaFree(plan->dconst);
   if (plan && plan->dfrag) cudaFree(plan->dfrag);
   delete plan;
@@ -534,6 +539,7 @@ static int run_apply(const sem1d_plan* p, int kind, const Args& a, void* stream,
 }
 
 int sem1d_rhs(const sem1d_plan* plan, const double* u, double* f, int* flag, void* stream) {
+  DeviceGuard guard_(plan ? plan->device : -1);
   if (!valid_plan(plan) || !u || !f || !flag) return fail(SEM1D_EINVAL, "sem1d_rhs: bad argument");
   if (plan->adv) return run_adv(plan, 0, u, nullptr, f, flag, stream, "sem1d_rhs");
   Args a = blank_args();
@@ -543,6 +549,7 @@ int sem1d_rhs(const sem1d_plan* plan, const double* u, double* f, int* flag, voi
 
 int sem1d_jac(const sem1d_plan* plan, const double* u, const double* v, double* out, int* flag,
               void* stream) {
+  DeviceGuard guard_(plan ? plan->device : -1);
   if (!valid_plan(plan) || !u || !v || !out || !flag) return fail(SEM1D_EINVAL, "sem1d_jac: bad argument");
   if (plan->adv) return run_adv(plan, 1, u, v, out, flag, stream, "sem1d_jac");
   Args a = blank_args();
@@ -552,6 +559,7 @@ int sem1d_jac(const sem1d_plan* plan, const double* u, const double* v, double* 
 
 int sem1d_jact(const sem1d_plan* plan, const double* u, const double* z, double* out, int* flag,
                void* stream) {
+  DeviceGuard guard_(plan ? plan->device : -1);
   if (!valid_plan(plan) || !u || !z || !out || !flag) return fail(SEM1D_EINVAL, "sem1d_jact: bad argument");
   if (plan->adv) return run_adv(plan, 2, u, z, out, flag, stream, "sem1d_jact");
   Args a = blank_args();
@@ -562,6 +570,7 @@ int sem1d_jact(const sem1d_plan* plan, const double* u, const double* z, double*
 int sem1d_rk_stage(const sem1d_plan* plan, const double* U_in, double* k_out, const double* base,
                    int nterms, const double* const* terms, const double* coef, double dt, double* Y,
                    int check_step, int* flag, void* stream) {
+  DeviceGuard guard_(plan ? plan->device : -1);
   if (!valid_burgers(plan) || !U_in || !base || !Y || !flag || nterms < 1)
     return fail(SEM1D_EINVAL, "sem1d_rk_stage: bad argument");
   Args a = blank_args();
@@ -576,6 +585,7 @@ int sem1d_adj_stage(const sem1d_plan* plan, const double* U, const double* lam, 
                     const double* const* l_terms, const double* acoef, double dt, double* l_out,
                     int nacc, const double* const* acc_terms, double* lam_out, int* flag,
                     void* stream) {
+  DeviceGuard guard_(plan ? plan->device : -1);
   if (!valid_burgers(plan) || !U || !lam || !flag) return fail(SEM1D_EINVAL, "sem1d_adj_stage: bad argument");
   Args a = blank_args();
   a.u = U; a.w = lam; a.b = b; a.out = l_out; a.flag = flag; a.base = lam; a.dt = dt; a.Y = lam_out;
@@ -590,6 +600,7 @@ int sem1d_adj_stage(const sem1d_plan* plan, const double* U, const double* lam, 
 
 int sem1d_ens_forward(const sem1d_plan* plan, const double* u0, double* traj, double* u_final,
                       const double* dts, int nsteps, int scheme, int* flags, void* stream) {
+  DeviceGuard guard_(plan ? plan->device : -1);
   if (!valid_burgers(plan) || !u0 || !u_final || !dts || !flags || nsteps < 0)
     return fail(SEM1D_EINVAL, "sem1d_ens_forward: bad argument");
   EnsArgs a;
@@ -607,6 +618,7 @@ int sem1d_ens_forward(const sem1d_plan* plan, const double* u0, double* traj, do
 int sem1d_ens_adjoint(const sem1d_plan* plan, const double* traj, const double* lam_in,
                       double* lam_out, const double* dts, int nsteps, int scheme, int* flags,
                       void* stream) {
+  DeviceGuard guard_(plan ? plan->device : -1);
   if (!valid_burgers(plan) || !traj || !lam_in || !lam_out || !dts || !flags || nsteps < 0)
     return fail(SEM1D_EINVAL, "sem1d_ens_adjoint: bad argument");
   EnsAdjArgs a;
@@ -622,6 +634,7 @@ int sem1d_ens_adjoint(const sem1d_plan* plan, const double* traj, const double* 
 }
 
 int sem1d_step_supported(const sem1d_plan* plan) {
+  DeviceGuard guard_(plan ? plan->device : -1);
   if (!valid_burgers(plan)) return 0;
   const int te = ((plan->N + 1) == 8) ? 8 * TILE_WF8 * TILE_WMT8 : ((plan->N + 1) == 32 ? 64 : 128);
   return (plan->periodic && plan->batch == 1 && (plan->N + 1) % 8 == 0 && plan->E >= 2 * te) ? 1 : 0;
@@ -629,6 +642,7 @@ int sem1d_step_supported(const sem1d_plan* plan) {
 
 int sem1d_rk_step(const sem1d_plan* plan, const double* u, double* u_new, double dt, int scheme,
                   int* flag, void* stream) {
+  DeviceGuard guard_(plan ? plan->device : -1);
   if (!valid_burgers(plan) || !u || !u_new || !flag || u == u_new)
     return fail(SEM1D_EINVAL, "sem1d_rk_step: bad argument (u_new must not alias u)");
   TileStepArgs a;
@@ -644,6 +658,7 @@ int sem1d_rk_step(const sem1d_plan* plan, const double* u, double* u_new, double
 
 int sem1d_adj_step(const sem1d_plan* plan, const double* u, const double* lam, double* lam_out,
                    double dt, int scheme, int* flag, void* stream) {
+  DeviceGuard guard_(plan ? plan->device : -1);
   if (!valid_burgers(plan) || !u || !lam || !lam_out || !flag || lam == lam_out)
     return fail(SEM1D_EINVAL, "sem1d_adj_step: bad argument (lam_out must not alias lam)");
   TileStepArgs a;
@@ -658,6 +673,7 @@ int sem1d_adj_step(const sem1d_plan* plan, const double* u, const double* lam, d
 }
 
 int sem1d_step_stages_supported(const sem1d_plan* plan) {
+  DeviceGuard guard_(plan ? plan->device : -1);
   if (!sem1d_step_supported(plan)) return 0;
   switch (plan->N) {
     case 7: return stages_fit<7>() ? 1 : 0;
@@ -670,6 +686,7 @@ int sem1d_step_stages_supported(const sem1d_plan* plan) {
 
 int sem1d_rk_step_stages(const sem1d_plan* plan, const double* u, double* u_new, double* const* stages,
                          double dt, int scheme, int* flag, void* stream) {
+  DeviceGuard guard_(plan ? plan->device : -1);
   if (!valid_burgers(plan) || !u || !u_new || !flag || !stages || u == u_new)
     return fail(SEM1D_EINVAL, "sem1d_rk_step_stages: bad argument");
   TileStepArgs a;
@@ -690,6 +707,7 @@ int sem1d_rk_step_stages(const sem1d_plan* plan, const double* u, double* u_new,
 
 int sem1d_adj_step_stages(const sem1d_plan* plan, const double* u, const double* const* stages,
                           const double* lam, double* lam_out, double dt, int scheme, int* flag, void* stream) {
+  DeviceGuard guard_(plan ? plan->device : -1);
   if (!valid_burgers(plan) || !u || !lam || !lam_out || !flag || !stages || lam == lam_out)
     return fail(SEM1D_EINVAL, "sem1d_adj_step_stages: bad argument (lam_out must not alias lam)");
   TileStepArgs a;
@@ -709,6 +727,7 @@ int sem1d_adj_step_stages(const sem1d_plan* plan, const double* u, const double*
 }
 
 int64_t sem1d_terminal_work_size(const sem1d_plan* plan) {
+  DeviceGuard guard_(plan ? plan->device : -1);
   if (!valid_plan(plan)) return -1;
   const int64_t per = RED_TPB * RED_ITEMS;
   return plan->batch * ((plan->ndof + per - 1) / per);
@@ -716,6 +735,7 @@ int64_t sem1d_terminal_work_size(const sem1d_plan* plan) {
 
 int sem1d_terminal(const sem1d_plan* plan, const double* uN, const double* ud, double* lam,
                    double* J_out, double* work, void* stream) {
+  DeviceGuard guard_(plan ? plan->device : -1);
   if (!valid_plan(plan) || !uN || !ud || !lam || !J_out || !work)
     return fail(SEM1D_EINVAL, "sem1d_terminal: bad argument");
   Pattern P;
@@ -736,6 +756,7 @@ int sem1d_terminal(const sem1d_plan* plan, const double* uN, const double* ud, d
 }
 
 int sem1d_scatter(const sem1d_plan* plan, const double* u, double* local, void* stream) {
+  DeviceGuard guard_(plan ? plan->device : -1);
   if (!valid_plan(plan) || !u || !local) return fail(SEM1D_EINVAL, "sem1d_scatter: bad argument");
   const Geo G = view(plan).geo;
   scatter_kernel<<<dim3(grid_for(plan->E * (plan->N + 1), 256), (unsigned)plan->batch), 256, 0,
@@ -745,6 +766,7 @@ int sem1d_scatter(const sem1d_plan* plan, const double* u, double* local, void* 
 }
 
 int sem1d_gather(const sem1d_plan* plan, const double* local, double* out, void* stream) {
+  DeviceGuard guard_(plan ? plan->device : -1);
   if (!valid_plan(plan) || !local || !out) return fail(SEM1D_EINVAL, "sem1d_gather: bad argument");
   const Geo G = view(plan).geo;
   gather_kernel<<<dim3(grid_for(plan->ndof, 256), (unsigned)plan->batch), 256, 0,

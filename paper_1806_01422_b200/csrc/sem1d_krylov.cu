@@ -29,6 +29,8 @@
 // order with no FMA contraction.
 #include <cuda_runtime.h>
 
+#include "sem1d_devguard.cuh"
+
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -40,6 +42,8 @@
 namespace sem1d {
 int set_error(int code, const std::string& msg);   // sem1d_capi.cu
 int64_t plan_batch(const sem1d_plan* p);           // sem1d_capi.cu
+int plan_device(const sem1d_plan* p);              // sem1d_capi.cu
+int plan3_device(const sem3d_plan* p);             // sem3d.cu
 }  // namespace sem1d
 
 namespace {
@@ -699,6 +703,7 @@ int cn_adjoint_impl(const OpIf& op, const double* u_n, const double* u_np1, cons
 extern "C" {
 
 int64_t sem1d_cn_work_size(const sem1d_plan* plan, int restart) {
+  sem1d::DeviceGuard guard_(sem1d::plan_device(plan));
   if (!plan || restart < 1 || restart > MAX_RESTART) return -1;
   const int64_t n = sem1d_plan_ndof(plan);
   return (int64_t)(restart + 1) * n + 4 * n + RED_DOUBLES + 3 * MAX_RESTART + 16 + 2;
@@ -707,6 +712,7 @@ int64_t sem1d_cn_work_size(const sem1d_plan* plan, int restart) {
 int sem1d_gmres(const sem1d_plan* plan, int transpose, const double* p, double alpha, const double* b,
                 double* x, const sem1d_cn_params* P, double* work, int* flag, sem1d_cn_stats* st,
                 void* stream) {
+  sem1d::DeviceGuard guard_(sem1d::plan_device(plan));
   if (!plan || sem1d::plan_batch(plan) != 1) return fail(SEM1D_EINVAL, "sem1d_gmres: needs a batch-1 plan");
   return gmres_impl(OpIf{plan, 0, nullptr, sem1d_plan_ndof(plan)}, transpose, p, alpha, b, x, P, work, flag,
                     st, stream);
@@ -714,6 +720,7 @@ int sem1d_gmres(const sem1d_plan* plan, int transpose, const double* p, double a
 
 int sem1d_cn_step(const sem1d_plan* plan, const double* u, double* v, double dt, const sem1d_cn_params* P,
                   double* work, int* flag, sem1d_cn_stats* st, void* stream) {
+  sem1d::DeviceGuard guard_(sem1d::plan_device(plan));
   if (!plan || sem1d::plan_batch(plan) != 1) return fail(SEM1D_EINVAL, "sem1d_cn_step: needs a batch-1 plan");
   return cn_step_impl(OpIf{plan, 0, nullptr, sem1d_plan_ndof(plan)}, u, v, dt, P, work, flag, st, stream);
 }
@@ -721,6 +728,7 @@ int sem1d_cn_step(const sem1d_plan* plan, const double* u, double* v, double dt,
 int sem1d_cn_adjoint_step(const sem1d_plan* plan, const double* u_n, const double* u_np1, const double* lam,
                           double* lam_out, double dt, const sem1d_cn_params* P, double* work, int* flag,
                           sem1d_cn_stats* st, void* stream) {
+  sem1d::DeviceGuard guard_(sem1d::plan_device(plan));
   if (!plan || sem1d::plan_batch(plan) != 1)
     return fail(SEM1D_EINVAL, "sem1d_cn_adjoint_step: needs a batch-1 plan");
   return cn_adjoint_impl(OpIf{plan, 0, nullptr, sem1d_plan_ndof(plan)}, u_n, u_np1, lam, lam_out, dt, P, work,
@@ -733,6 +741,7 @@ static int64_t krylov_doubles(int64_t n, int restart) {
 }
 
 int64_t sem3d_cn_work_size(const sem3d_plan* plan, int restart) {
+  sem1d::DeviceGuard guard_(sem1d::plan3_device(plan));
   if (!plan || restart < 1 || restart > MAX_RESTART) return -1;
   return krylov_doubles(sem3d_plan_ndof(plan), restart) + sem3d_work_size(plan);
 }
@@ -744,12 +753,14 @@ static OpIf op3(const sem3d_plan* plan, double* work, int restart) {
 
 int sem3d_gmres(const sem3d_plan* plan, int transpose, const double* p, double alpha, const double* b, double* x,
                 const sem1d_cn_params* P, double* work, int* flag, sem1d_cn_stats* st, void* stream) {
+  sem1d::DeviceGuard guard_(sem1d::plan3_device(plan));
   if (!plan || !P || !work) return fail(SEM1D_EINVAL, "sem3d_gmres: bad argument");
   return gmres_impl(op3(plan, work, P->gmres_restart), transpose, p, alpha, b, x, P, work, flag, st, stream);
 }
 
 int sem3d_cn_step(const sem3d_plan* plan, const double* u, double* v, double dt, const sem1d_cn_params* P,
                   double* work, int* flag, sem1d_cn_stats* st, void* stream) {
+  sem1d::DeviceGuard guard_(sem1d::plan3_device(plan));
   if (!plan || !P || !work) return fail(SEM1D_EINVAL, "sem3d_cn_step: bad argument");
   return cn_step_impl(op3(plan, work, P->gmres_restart), u, v, dt, P, work, flag, st, stream);
 }
@@ -757,6 +768,7 @@ int sem3d_cn_step(const sem3d_plan* plan, const double* u, double* v, double dt,
 int sem3d_cn_adjoint_step(const sem3d_plan* plan, const double* u_n, const double* u_np1, const double* lam,
                           double* lam_out, double dt, const sem1d_cn_params* P, double* work, int* flag,
                           sem1d_cn_stats* st, void* stream) {
+  sem1d::DeviceGuard guard_(sem1d::plan3_device(plan));
   if (!plan || !P || !work) return fail(SEM1D_EINVAL, "sem3d_cn_adjoint_step: bad argument");
   return cn_adjoint_impl(op3(plan, work, P->gmres_restart), u_n, u_np1, lam, lam_out, dt, P, work, flag, st,
                          stream);

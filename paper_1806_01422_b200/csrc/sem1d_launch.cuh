@@ -7,6 +7,7 @@
 
 #include <algorithm>
 
+#include "sem1d_devguard.cuh"
 #include "sem1d_device.cuh"
 #include "sem1d_ensemble.cuh"
 #include "sem1d_smallring.cuh"
@@ -33,11 +34,12 @@ template <int N, int OP, int PRO, int EPI>
 static cudaError_t launch_one(const PlanView& p, const Args& a, cudaStream_t s) {
   auto kern = apply_kernel<N, OP, PRO, EPI>;
   constexpr size_t smem = apply_smem_bytes<N, OP>();
-  static bool attr_done = false;  // benign race: idempotent attribute set
+  static DevCache attr;            // benign race: idempotent attribute set
+  int& attr_done = attr.here();
   if (!attr_done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    attr_done = true;
+    attr_done = 1;
   }
   const int64_t nblk = (p.geo.E + Tile<N>::TPB - 1) / Tile<N>::TPB;
   dim3 grid((unsigned)nblk, (unsigned)p.batch);
@@ -51,17 +53,15 @@ template <int N, int OP, int EPI>
 static cudaError_t launch_tma(const PlanView& p, const Args& a, cudaStream_t s) {
   auto kern = apply_tma_kernel<N, OP, EPI, kTmaStages>;
   constexpr size_t smem = tma_smem_bytes<N, OP, kTmaStages>();
-  static int max_resident = 0;  // CTAs per SM for this instantiation (cached)
+  static DevCache resident;       // resident CTAs for this instantiation, per device
+  int& max_resident = resident.here();
   if (max_resident == 0) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int per_sm = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, Tile<N>::TPB, smem);
     if (e != cudaSuccess) return e;
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    max_resident = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
+    max_resident = (per_sm > 0 ? per_sm : 1) * device_sms();
   }
   const int64_t per_ring = (p.geo.E + Tile<N>::TPB - 1) / Tile<N>::TPB;
   const int64_t total = per_ring * p.batch;
@@ -79,17 +79,15 @@ static cudaError_t launch_mma(const PlanView& p, const Args& a, cudaStream_t s) 
   } else {
     auto kern = apply_mma_kernel<N, OP, EPI, kTmaStages>;
     constexpr size_t smem = mma_smem_bytes<N, OP, kTmaStages>();
-    static int max_resident = 0;
+    static DevCache resident;
+    int& max_resident = resident.here();
     if (max_resident == 0) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       int per_sm = 0;
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, MmaTile<N>::THREADS, smem);
       if (e != cudaSuccess) return e;
-      int dev = 0, sms = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      max_resident = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
+      max_resident = (per_sm > 0 ? per_sm : 1) * device_sms();
     }
     const int64_t per_ring = (p.geo.E + MmaTile<N>::ELEMS - 1) / MmaTile<N>::ELEMS;
     const int64_t total = per_ring * p.batch;
@@ -110,17 +108,15 @@ static cudaError_t launch_ws(const PlanView& p, const Args& a, cudaStream_t s) {
     constexpr int ST = ws_stages<N, OP>();
     auto kern = apply_ws_kernel<N, OP, EPI, ST>;
     constexpr size_t smem = ws_smem_bytes<N, OP, ST>();
-    static int max_resident = 0;
+    static DevCache resident;
+    int& max_resident = resident.here();
     if (max_resident == 0) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       int per_sm = 0;
       e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WsTile<N, OP>::THREADS, smem);
       if (e != cudaSuccess) return e;
-      int dev = 0, sms = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      max_resident = (per_sm > 0 ? per_sm : 1) * (sms > 0 ? sms : 148);
+      max_resident = (per_sm > 0 ? per_sm : 1) * device_sms();
     }
     const int64_t per_ring = (p.geo.E + WsTile<N, OP>::ELEMS - 1) / WsTile<N, OP>::ELEMS;
     const int64_t total = per_ring * p.batch;
@@ -283,17 +279,15 @@ cudaError_t launch_ens_forward(const PlanView& p, const EnsArgs& a, cudaStream_t
   return launch_small<N>(p, &a, nullptr, s);
 }
 
-// One tile-step kernel instantiation: occupancy queried once (static per instantiation),
+// One tile-step kernel instantiation: occupancy queried once per device,
 // grid = min(tiles, resident CTAs).
 template <int N, auto KERN>
 cudaError_t launch_tile_one(const PlanView& p, const TileStepArgs& a, int threads, size_t smem,
                             size_t smem_limit, cudaStream_t s) {
-  static int per_sm = 0;
-  static int sms = 0;
+  static DevCache occ;             // per device
+  int& per_sm = occ.here();
+  const int sms = device_sms();
   if (per_sm == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaError_t e = cudaFuncSetAttribute(KERN, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_limit);
     if (e != cudaSuccess) return e;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, KERN, threads, smem);

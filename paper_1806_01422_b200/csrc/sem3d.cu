@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "sem1d.h"
+#include "sem1d_devguard.cuh"
 
 namespace sem1d {
 int set_error(int code, const std::string& msg);   // sem1d_capi.cu
@@ -41,7 +42,12 @@ struct sem3d_plan {
   int64_t E[3], P[3], nscalar, nelem;
   double nu;
   double* cbuf;   // device: K[3][n*n], Dw[n*n], T[3][n*n], minv[(N+1)^3], mass[(N+1)^3]
+  int device;     // the device current at sem3d_plan_create; every call runs there
 };
+
+namespace sem1d {
+int plan3_device(const sem3d_plan* p) { return p ? p->device : -1; }
+}  // namespace sem1d
 
 namespace {
 
@@ -514,11 +520,12 @@ cudaError_t launch_elem_mma(const sem3d_plan* p, const double* u, const double* 
                             cudaStream_t s) {
   auto kern = elem3d_mma_kernel<OP>;
   constexpr size_t smem = sizeof(double) * (size_t)L3<7>::BLK * (OP == OP3_RHS ? 4 : 7);
-  static bool done = false;
+  static sem1d::DevCache attr;     // the attribute is per (kernel, device)
+  int& done = attr.here();
   if (!done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    done = true;
+    done = 1;
   }
   kern<<<(unsigned)p->nelem, 128, smem, s>>>(geo(p), p->cbuf, u, w, loc, flag);
   return cudaGetLastError();
@@ -532,11 +539,12 @@ cudaError_t launch_elem(const sem3d_plan* p, const double* u, const double* w, d
   }
   auto kern = elem3d_kernel<N, OP>;
   constexpr size_t smem = L3<N>::smem(OP);
-  static bool done = false;
+  static sem1d::DevCache attr;     // the attribute is per (kernel, device)
+  int& done = attr.here();
   if (!done) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    done = true;
+    done = 1;
   }
   kern<<<(unsigned)p->nelem, L3<N>::THREADS, smem, s>>>(geo(p), p->cbuf, u, w, loc, flag);
   return cudaGetLastError();
@@ -592,6 +600,7 @@ int sem3d_plan_create(const int64_t* elements, int degree, double nu, const doub
   p->N = degree;
   p->n = n;
   p->nu = nu;
+  if (cudaGetDevice(&p->device) != cudaSuccess) p->device = 0;
   p->nscalar = 1;
   p->nelem = 1;
   for (int a = 0; a < 3; ++a) {
@@ -623,6 +632,7 @@ int sem3d_plan_create(const int64_t* elements, int degree, double nu, const doub
 }
 
 int sem3d_plan_destroy(sem3d_plan* p) {
+  sem1d::DeviceGuard guard_(p ? p->device : -1);
   if (!p) return SEM1D_OK;
   if (p->cbuf) cudaFree(p->cbuf);
   delete p;
@@ -632,12 +642,14 @@ int sem3d_plan_destroy(sem3d_plan* p) {
 int64_t sem3d_plan_ndof(const sem3d_plan* p) { return p ? 3 * p->nscalar : -1; }
 
 int64_t sem3d_work_size(const sem3d_plan* p) {
+  sem1d::DeviceGuard guard_(p ? p->device : -1);
   if (!p) return -1;
   return 3 * p->nelem * (int64_t)p->n * p->n * p->n + 4096;
 }
 
 static int run3(const sem3d_plan* p, int op, const double* u, const double* w, double* out, double* work,
                 int* flag, void* stream, const char* name) {
+  sem1d::DeviceGuard guard_(p ? p->device : -1);
   if (!p || !u || !out || !work || !flag || (op != OP3_RHS && !w))
     return fail(SEM1D_EINVAL, std::string(name) + ": bad argument");
   if (out == u || out == w) return fail(SEM1D_EINVAL, std::string(name) + ": output must not alias an input");
@@ -646,19 +658,23 @@ static int run3(const sem3d_plan* p, int op, const double* u, const double* w, d
 }
 
 int sem3d_rhs(const sem3d_plan* p, const double* u, double* f, double* work, int* flag, void* stream) {
+  sem1d::DeviceGuard guard_(p ? p->device : -1);
   return run3(p, OP3_RHS, u, nullptr, f, work, flag, stream, "sem3d_rhs");
 }
 int sem3d_jac(const sem3d_plan* p, const double* u, const double* v, double* out, double* work, int* flag,
               void* stream) {
+  sem1d::DeviceGuard guard_(p ? p->device : -1);
   return run3(p, OP3_JAC, u, v, out, work, flag, stream, "sem3d_jac");
 }
 int sem3d_jact(const sem3d_plan* p, const double* u, const double* z, double* out, double* work, int* flag,
                void* stream) {
+  sem1d::DeviceGuard guard_(p ? p->device : -1);
   return run3(p, OP3_JACT, u, z, out, work, flag, stream, "sem3d_jact");
 }
 
 int sem3d_terminal(const sem3d_plan* p, const double* uN, const double* ud, double* lam, double* J,
                    double* work, void* stream) {
+  sem1d::DeviceGuard guard_(p ? p->device : -1);
   if (!p || !uN || !ud || !lam || !J || !work) return fail(SEM1D_EINVAL, "sem3d_terminal: bad argument");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const int pat = (p->N + 1) * (p->N + 1) * (p->N + 1);

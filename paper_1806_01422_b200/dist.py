@@ -316,12 +316,22 @@ class ShardedOperator:
         return self.local.flag_slots(k)
 
     def reduce_flag_words(self, words):
-        """Max over ranks of the window's flag words (nonzero = the step failed somewhere)."""
-        return self._allreduce(words.clone(), "max")
+        """Bitwise OR over ranks of the window's flag words: each bit plane is all-reduced with
+        MAX, so every rank sees the same failing step and the same failure kind."""
+        import torch
+        planes = torch.stack([(words & b) != 0 for b in (1, 2, 4)]).to(torch.float64)
+        planes = self._allreduce(planes, "max")
+        out = torch.zeros_like(words)
+        for k, b in enumerate((1, 2, 4)):
+            out |= (planes[k] > 0).to(words.dtype) * b
+        return out
 
-    def launch_adj_step(self, u, lam, lam_out, dt, scheme):
+    def launch_adj_step(self, u, lam, lam_out, dt, scheme, flag=None):
         self.halo.refresh([u, lam])
-        self.local.launch_adj_step(u, lam, lam_out, dt, scheme)
+        if flag is None:
+            self.local.launch_adj_step(u, lam, lam_out, dt, scheme)
+        else:
+            self.local.launch_adj_step(u, lam, lam_out, dt, scheme, flag=flag)
 
     def launch_terminal(self, uN, ud, lam, J_out):
         """Objective on owned nodes, all-reduced; lam = mask(2 M d) (adjoint.py:39-47)."""

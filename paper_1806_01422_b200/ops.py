@@ -168,7 +168,8 @@ class SemOperator(ComposedStages):
         self.max_matrix_dim = ax.degree + 1
         if ax.degree > _lib.load().sem1d_max_degree():
             raise ValidationError(f"degree {ax.degree} exceeds the kernel limit")
-        self._plan = _Plan(grid, coef.nu, self._kmat, self._dw, self.batch)
+        with torch.cuda.device(self.device):   # the plan belongs to (and launches on) this device
+            self._plan = _Plan(grid, coef.nu, self._kmat, self._dw, self.batch)
         self._adv = coef.advection != BURGERS
         if self._adv:
             if coef.advection == LINEAR and coef.speed.size != grid.ncomp:   # ops.py:95-100
@@ -329,17 +330,19 @@ class SemOperator(ComposedStages):
             float(dt), self._SCHEME_CODES[scheme], flag or self._flag.data_ptr(), self._stream()),
             "sem1d_rk_step_stages")
 
-    def launch_adj_step_stages(self, u, stages, lam, lam_out, dt, scheme):
+    def launch_adj_step_stages(self, u, stages, lam, lam_out, dt, scheme, flag=None):
         """One fused adjoint step reading the stored stage states (no recompute)."""
         _lib.check(_lib.load().sem1d_adj_step_stages(
             self._plan.handle, u.data_ptr(), _lib.ptr_array([t.data_ptr() for t in stages]), lam.data_ptr(),
-            lam_out.data_ptr(), float(dt), self._SCHEME_CODES[scheme], self._flag.data_ptr(), self._stream()),
-            "sem1d_adj_step_stages")
+            lam_out.data_ptr(), float(dt), self._SCHEME_CODES[scheme], flag or self._flag.data_ptr(),
+            self._stream()), "sem1d_adj_step_stages")
 
-    def launch_adj_step(self, u, lam, lam_out, dt, scheme):
+    def launch_adj_step(self, u, lam, lam_out, dt, scheme, flag=None):
+        """One fused adjoint step; ``flag`` as in launch_rk_step (``sweep`` runs ahead with
+        per-step flag words)."""
         _lib.check(_lib.load().sem1d_adj_step(self._plan.handle, u.data_ptr(), lam.data_ptr(),
                                               lam_out.data_ptr(), float(dt),
-                                              self._SCHEME_CODES[scheme], self._flag.data_ptr(),
+                                              self._SCHEME_CODES[scheme], flag or self._flag.data_ptr(),
                                               self._stream()), "sem1d_adj_step")
 
     # -- implicit path (Crank-Nicolson; SURVEY.md 8(f) row 1) --------------------

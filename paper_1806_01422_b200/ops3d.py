@@ -78,7 +78,8 @@ class SemOperator3D(ComposedStages):
         self._transverse = [m2[:, None] * m3[None, :], m1[:, None] * m3[None, :],
                             m1[:, None] * m2[None, :]]
         self.max_matrix_dim = grid.N + 1
-        self._plan = _Plan3D(grid, coef.nu, self._kmat, self._dw, self._transverse)
+        with _torch().cuda.device(self.device):   # the plan belongs to (and launches on) this device
+            self._plan = _Plan3D(grid, coef.nu, self._kmat, self._dw, self._transverse)
         self.ndof = grid.nglobal
         self.shape = (self.ndof,)
         self._flag = torch.zeros(1, dtype=torch.int32, device=self.device)

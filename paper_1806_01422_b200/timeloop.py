@@ -404,7 +404,9 @@ def integrate(op, u0, cfg, store_steps="all", keep_log=False, keep_stages=False)
         if bad is None:
             pending.clear()
             return False
-        n, t, dt_next, attempts, u, nlog = pending[bad]
+        n, t, dt_next, attempts, u, nlog, counters = pending[bad]
+        op.counters.clear()
+        op.counters.update(counters)          # the discarded steps were never taken
         for rec in pending[bad:]:
             snapshots.pop(rec[0] + 1, None)
             stage_snaps.pop(rec[0], None)
@@ -431,7 +433,7 @@ def integrate(op, u0, cfg, store_steps="all", keep_log=False, keep_stages=False)
         if spec and not sync_next:
             keep_n = keep_stages and (store_all or n in want)
             st_out = [op.empty() for _ in range(engine.s - 1)] if keep_n else None
-            pending.append((n, t, dt_next, attempts - 1, u, len(log) if keep_log else 0))
+            pending.append((n, t, dt_next, attempts - 1, u, len(log) if keep_log else 0, dict(op.counters)))
             engine.step(u, dt, u_new, fused=True, stages_out=st_out, flag=slot0 + 4 * (len(pending) - 1))
             if keep_n:
                 stage_snaps[n] = st_out

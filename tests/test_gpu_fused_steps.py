@@ -138,7 +138,9 @@ def test_run_ahead_rollback_matches_per_step_checks(cuda, store, keep):
         _inject_failures(op, u0, 0.0, {1e-5: 1.5e-6, 2e-5: 0.75e-6, 3e-5: 0.3e-6})
         st = "all" if store == "all" else [0, 7, 19, 33]
         out[mode] = timeloop.integrate(op, u0, ts, store_steps=st, keep_log=True, keep_stages=keep)
+        out[mode + "_counters"] = dict(op.counters)
     a, b = out["ahead"], out["sync"]
+    assert out["ahead_counters"] == out["sync_counters"]      # rolled-back steps are not counted
     assert np.array_equal(a.ts, b.ts) and np.array_equal(a.dts, b.dts)
     assert a.stats == b.stats and a.stats["retries"] == 3
     assert a.step_log == b.step_log
@@ -162,3 +164,54 @@ def test_run_ahead_raises_like_per_step_checks(cuda):
         _inject_failures(op, u0, 0.0, {9 * 2e-6: 0.0})
         with pytest.raises(sb.StepFailure):
             timeloop.integrate(op, u0, ts)
+
+
+@pytest.mark.parametrize("keep", [False, True])
+@pytest.mark.parametrize("bad_step", [None, 3, 21, 37])
+def test_adjoint_run_ahead_matches_per_step_checks(cuda, keep, bad_step):
+    """sweep() runs ahead on the fused adjoint-step kernels (per-step flag words, one read
+    per window of 16 steps).  Without a failure the gradient is bitwise that of the
+    per-step-checked sweep; with a non-finite state planted at step `bad_step` both raise
+    the same NumericFailure with the same counters."""
+    steps = 40
+    out = {}
+    for mode in ("ahead", "sync"):
+        g, op, u0, ud, ts = _problem(1061, 7, 1e-3, 2e-6, steps, "rk4", 5)
+        fwd = timeloop.integrate(op, u0, ts, keep_stages=keep)
+        if bad_step is not None:
+            nan_state = fwd.snapshots[bad_step].clone()
+            nan_state[77] = float("nan")
+            fwd.snapshots[bad_step] = nan_state
+        J, lam = adjoint.terminal_condition(g, fwd.u_final, torch.from_numpy(ud).cuda(), op=op)
+        before = dict(op.counters)
+        kw = {} if mode == "ahead" else {"check_every": 1}
+        try:
+            out[mode] = ("ok", adjoint.sweep(op, ts, fwd, checkpoint.plan_store_all(steps), lam, **kw).clone())
+        except sb.NumericFailure as exc:
+            out[mode] = ("raised", str(exc))
+        out[mode + "_counters"] = {k: op.counters[k] - before[k] for k in op.counters}
+    assert out["ahead"][0] == out["sync"][0] == ("ok" if bad_step is None else "raised")
+    if bad_step is None:
+        assert torch.equal(out["ahead"][1], out["sync"][1])
+    else:
+        assert out["ahead"][1] == out["sync"][1]
+    assert out["ahead_counters"] == out["sync_counters"]
+
+
+def test_adjoint_run_ahead_binomial_and_cotangent_failure(cuda):
+    """Run-ahead across recompute Advances (binomial schedule) equals store-all bitwise; a
+    NaN terminal cotangent raises 'cotangent' at the first adjoint step in both modes."""
+    steps = 35
+    g, op, u0, ud, ts = _problem(1061, 7, 1e-3, 2e-6, steps, "rk4", 6)
+    fwd = timeloop.integrate(op, u0, ts)
+    J, lam = adjoint.terminal_condition(g, fwd.u_final, torch.from_numpy(ud).cuda(), op=op)
+    ref = adjoint.sweep(op, ts, fwd, checkpoint.plan_store_all(steps), lam, check_every=1).clone()
+    sched = checkpoint.plan_binomial(steps, 4)
+    fwd_b = timeloop.integrate(op, u0, ts, store_steps=sched.forward_stores.keys())
+    got = adjoint.sweep(op, ts, fwd_b, sched, lam)
+    assert torch.equal(got, ref)
+    bad = lam.clone()
+    bad[5] = float("inf")
+    for kw in ({}, {"check_every": 1}):
+        with pytest.raises(sb.NumericFailure, match="cotangent"):
+            adjoint.sweep(op, ts, fwd, checkpoint.plan_store_all(steps), bad, **kw)

@@ -271,3 +271,24 @@ def test_max_size_config5_apply(cuda):
         idx = np.arange(e0 * N, (e0 + ne) * N) % op.ndof
         inner = slice(N + 1, (ne - 1) * N)
         assert rel_err(fh[idx][inner], sub.rhs(uh[idx])[inner]) <= 1e-12
+
+
+def test_plan_runs_on_its_own_device(cuda):
+    """A plan belongs to the device current at sem1d_plan_create (SemOperator makes its
+    `device` current for that); every C-ABI call switches to it and restores the caller's
+    device.  On a multi-GPU box the operator is built on the LAST device while device 0 is
+    current; on one GPU the guard still must leave the current device untouched."""
+    ndev = torch.cuda.device_count()
+    dev = torch.device("cuda", ndev - 1)
+    torch.cuda.set_device(0)
+    op = sb.SemOperator(grid_1d(-1.0, 1.0, 700, 7), sb.PdeCoefficients(0.01), device=dev)
+    ref = R.BurgersOracle(R.Mesh1D(-1.0, 1.0, 700, 7, True), 0.01)
+    u, v, w = R.seeded_fields(ref.mesh.ndof, 9)
+    with torch.cuda.device(dev):
+        f = op.apply_rhs(u)
+        jt = op.apply_jacobian_transpose(u, w)
+    assert torch.cuda.current_device() == 0
+    assert rel_err(f, ref.rhs(u)) <= TOL and rel_err(jt, ref.jact(u, w)) <= TOL
+    ud = torch.from_numpy(u).to(dev)
+    out = op.apply_rhs(ud)
+    assert out.device == dev and torch.cuda.current_device() == 0

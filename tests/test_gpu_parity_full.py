@@ -1,0 +1,127 @@
+"""Parity at the BASELINE's full sizes and on smooth inputs.
+
+* Whole-field comparisons: config 2 (E = 2^22, N = 7, 29.4M DOF) and config 3 (E = 2^18,
+  N = 31) F, J v and J^T w against the oracle on every node, <= 1e-12 max-abs relative.
+* Smooth inputs: the kernels fold -nu M^-1 / dt M^-1 into their tensor-core operand tables
+  and (in the sweep kernels) regroup the stage arithmetic, so each product rounds differently
+  from the reference.  On rough inputs that is invisible (1e-16), on smooth inputs the terms
+  cancel and the reference's own rounding noise grows (up to 1e-7 relative at
+  N = 31, h = 2/2^18).  The bound is the survey's: |GPU - oracle| <= max(1e-12 ||oracle||,
+  4 |oracle - LD|), LD = the reference arithmetic (ops.py:161-212) evaluated in longdouble
+  from the same fp64 constants (oracle.semref.LongDoubleBurgers).  Applied per apply at the
+  BASELINE h / nu of N = 7 (config 5), 15 (config 4) and 31 (config 3), on every kernel path,
+  and to one fused RK4 step and one fused adjoint step (increments compared).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1806_01422_b200 as sb
+from oracle import semref as R
+from paper_1806_01422_b200 import configs
+from paper_1806_01422_b200.grid import grid_1d
+from semtest_util import rel_err
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+# (N, E, h, nu, dt): the BASELINE physics of configs 5, 4 and 3
+SMOOTH_CASES = [(7, 4096, 1.0 / 64.0, 1e-3, 2e-4), (15, 1024, 20.0 / 256.0, 0.01, 5e-5),
+                (31, 1024, 2.0 / 2 ** 18, 1e-3, 1e-14)]
+
+
+def _full_field_case(c):
+    op = configs.cfg_operator(c, device="cuda:0")
+    ref = R.BurgersOracle(R.Mesh1D(c["xa"], c["xb"], c["E"], c["N"], True), c["nu"])
+    u, v, w = configs.operator_inputs(op.ndof, c["seed"])
+    ud, vd, wd = (torch.from_numpy(a).cuda() for a in (u, v, w))
+    got = {"F": op.apply_rhs(ud).cpu().numpy(), "J": op.apply_jacobian(ud, vd).cpu().numpy(),
+           "JT": op.apply_jacobian_transpose(ud, wd).cpu().numpy()}
+    want = {"F": ref.rhs(u), "J": ref.jac(u, v), "JT": ref.jact(u, w)}
+    return {k: rel_err(got[k], want[k]) for k in got}
+
+
+def test_cfg2_whole_field_vs_oracle(cuda):
+    """Config 2 at full size: every one of the 29,360,128 nodes of F, J v and J^T w."""
+    errs = _full_field_case(configs.CFG2)
+    assert max(errs.values()) <= TOL, errs
+
+
+def test_cfg3_whole_field_vs_oracle(cuda):
+    """Config 3 at full size (E = 2^18, N = 31, dense 32 x 32 contractions on DMMA)."""
+    c = dict(configs.CFG3)
+    errs = _full_field_case(c)
+    assert max(errs.values()) <= TOL, errs
+
+
+@pytest.fixture(params=[0, 1, 2, 3], ids=["auto", "no-mma", "plain", "mma-sync"])
+def kernel_path(request):
+    from paper_1806_01422_b200 import _lib
+    lib = _lib.load()
+    assert lib.sem1d_set_kernel_path(request.param) == 0
+    yield request.param
+    lib.sem1d_set_kernel_path(0)
+
+
+def _smooth_setup(N, E, h, nu):
+    mesh = R.Mesh1D(0.0, E * h, E, N, True)
+    ref = R.BurgersOracle(mesh, nu)
+    ld = R.LongDoubleBurgers(ref)
+    g = grid_1d(0.0, E * h, E, N)
+    op = sb.SemOperator(g, sb.PdeCoefficients(nu), device="cuda:0")
+    return mesh, ref, ld, op
+
+
+@pytest.mark.parametrize("N,E,h,nu,dt", SMOOTH_CASES)
+def test_smooth_inputs_longdouble_bound(cuda, kernel_path, N, E, h, nu, dt):
+    mesh, ref, ld, op = _smooth_setup(N, E, h, nu)
+    u, v, w = R.smooth_fields(mesh, seed=N)
+    for name, gpu, orc, lde in (
+            ("F", op.apply_rhs(u), ref.rhs(u), ld.rhs(u)),
+            ("J", op.apply_jacobian(u, v), ref.jac(u, v), ld.jac(u, v)),
+            ("JT", op.apply_jacobian_transpose(u, w), ref.jact(u, w), ld.jact(u, w))):
+        err, bound = R.ld_bound(gpu, orc, lde)
+        assert err <= bound, (name, err, bound)
+
+
+def _incr_bound(gpu_new, orc_new, ld_new, base):
+    """Bound on step increments: (x_new - x) compared in longdouble (exact differences)."""
+    b = np.asarray(base, dtype=float).astype(np.longdouble)
+    dg = np.asarray(gpu_new, dtype=float).astype(np.longdouble) - b
+    do = np.asarray(orc_new, dtype=float).astype(np.longdouble) - b
+    dl = ld_new - b
+    err = float(np.max(np.abs(dg - do)))
+    bound = max(1e-12 * float(np.max(np.abs(do))), 4.0 * float(np.max(np.abs(do - dl))))
+    return err, bound
+
+
+@pytest.mark.parametrize("N,E,h,nu,dt", SMOOTH_CASES)
+def test_fused_steps_longdouble_bound(cuda, N, E, h, nu, dt):
+    """One whole-step RK4 kernel and one adjoint-step kernel (recompute and stored-stage
+    variants) on smooth inputs: increments within the longdouble-aware bound."""
+    mesh, ref, ld, op = _smooth_setup(N, E, h, nu)
+    assert op.step_fused_supported()
+    u, lam, _ = R.smooth_fields(mesh, seed=100 + N)
+    ud, ld_ = torch.from_numpy(u).cuda(), torch.from_numpy(lam).cuda()
+    un = op.empty()
+    op.launch_rk_step(ud, un, dt, "rk4")
+    err, bound = _incr_bound(un.cpu().numpy(), R.rk_step(ref, u, dt, "rk4"), ld.rk_step(u, dt, "rk4"), u)
+    assert err <= bound, ("step", err, bound)
+    lo = op.empty()
+    op.launch_adj_step(ud, ld_, lo, dt, "rk4")
+    assert op.flags() == 0
+    orc = R.adjoint_rk_step(ref, u, lam, dt, "rk4")
+    ldv = ld.adjoint_rk_step(u, lam, dt, "rk4")
+    err, bound = _incr_bound(lo.cpu().numpy(), orc, ldv, lam)
+    assert err <= bound, ("adjoint", err, bound)
+    if op.step_stages_supported():
+        st = [op.empty() for _ in range(3)]
+        un2 = op.empty()
+        op.launch_rk_step_stages(ud, un2, st, dt, "rk4")
+        err, bound = _incr_bound(un2.cpu().numpy(), R.rk_step(ref, u, dt, "rk4"), ld.rk_step(u, dt, "rk4"), u)
+        assert err <= bound, ("step+stages", err, bound)
+        lo2 = op.empty()
+        op.launch_adj_step_stages(ud, st, ld_, lo2, dt, "rk4")
+        err, bound = _incr_bound(lo2.cpu().numpy(), orc, ldv, lam)
+        assert err <= bound, ("adjoint stored stages", err, bound)

@@ -260,3 +260,38 @@ def test_advdiff_diffusion_problems_bit_exact(name, kind, speed, nu, E, t_end, s
                                          t_end / steps, scheme)
     assert j == g[f"{name}_J"][0]
     assert np.array_equal(gr, g[f"{name}_grad"]) and np.array_equal(uf, g[f"{name}_ufinal"])
+
+
+@pytest.mark.parametrize("N,per", [(7, True), (15, True), (31, True), (9, False)])
+def test_longdouble_restatement(N, per):
+    """The longdouble restatement of ops.py:161-212 (the yard stick of the smooth-input
+    bound) agrees with the fp64 oracle to rounding on rough inputs,
+    its RK4 step / adjoint step to the fp64 restatement, and its own J^T is the transpose of
+    its J (dot-product identity in longdouble)."""
+    m = R.Mesh1D(-1.0, 1.0, 24, N, per)
+    o = R.BurgersOracle(m, 0.01)
+    L = R.LongDoubleBurgers(o)
+    u, v, w = R.seeded_fields(m.ndof, N)
+    for a, b in ((o.rhs(u), L.rhs(u)), (o.jac(u, v), L.jac(u, v)), (o.jact(u, w), L.jact(u, w))):
+        assert b.dtype == np.longdouble
+        assert float(np.max(np.abs(a - b)) / np.max(np.abs(a))) <= 1e-14
+    mask = m.maskv
+    lhs = np.dot(L.jac(u, v * mask), (w * mask).astype(np.longdouble))
+    rhs = np.dot((v * mask).astype(np.longdouble), L.jact(u, w * mask))
+    assert abs(float(lhs - rhs)) <= 1e-16 * float(np.linalg.norm(L.jac(u, v * mask)) * np.linalg.norm(w))
+    if per:
+        dt = 1e-9
+        s = R.rk_step(o, u, dt, "rk4")
+        assert float(np.max(np.abs(s - L.rk_step(u, dt, "rk4")))) <= 1e-14
+        a = R.adjoint_rk_step(o, u, w, dt, "rk4")
+        assert float(np.max(np.abs(a - L.adjoint_rk_step(u, w, dt, "rk4")))) <= 1e-13 * float(np.max(np.abs(a)))
+
+
+def test_smooth_fields_and_bound_helper():
+    m = R.Mesh1D(0.0, 64.0, 4096, 7, True)
+    u, v, w = R.smooth_fields(m, 7)
+    assert u.shape == (m.ndof,) and np.all(np.isfinite(u)) and np.max(np.abs(u)) <= 3.0
+    # smooth: neighbouring nodes differ by far less than the amplitude
+    assert np.max(np.abs(np.diff(u))) <= 0.05
+    err, bound = R.ld_bound(u + 1e-13, u, u.astype(np.longdouble))
+    assert err > 0 and bound >= 1e-12 * np.max(np.abs(u))
