@@ -66,6 +66,9 @@ int sem1d_version(void);
  *     plain tiled kernel), 1 = never a tensor-core kernel, 2 = plain tiled
  *     kernel only, 3 = the CTA-synchronous tensor-core kernel (A/B reference). */
 int sem1d_set_kernel_path(int path);
+/* Tile-step kernels for A/B runs: 0 = auto (register-resident kernels for N = 7),
+ * 1 = the shared-memory tile kernels for every degree. */
+int sem1d_set_tile_variant(int variant);
 const char* sem1d_last_error(void);
 int sem1d_max_degree(void);
 
@@ -172,6 +175,13 @@ int sem1d_rk_step(const sem1d_plan* plan, const double* u, double* u_new, double
                   int* flag, void* stream);
 int sem1d_adj_step(const sem1d_plan* plan, const double* u, const double* lam, double* lam_out,
                    double dt, int scheme, int* flag, void* stream);
+/* One step (timeloop.py:111-130) with a choice of checks; stages may be NULL.  check = 1 is
+ * sem1d_rk_step / sem1d_rk_step_stages.  check = 0 tests only the new state: a non-finite
+ * stage input then shows as SEM1D_FLAG_STEP_NONFINITE (NaN/Inf reach the new state through
+ * every b_i != 0), so a caller that must tell NumericFailure from StepFailure re-runs a
+ * flagged step with check = 1 -- bitwise the same state (integrate's run-ahead does). */
+int sem1d_rk_step_ex(const sem1d_plan* plan, const double* u, double* u_new, double* const* stages,
+                     double dt, int scheme, int check, int* flag, void* stream);
 
 /* Terminal condition (adjoint.py:33-47): d = uN - ud, lam = mask(2 M d),
  * J_out[b] = d^T M d per batch member (deterministic two-level reduction;

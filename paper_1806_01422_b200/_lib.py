@@ -47,6 +47,7 @@ class CnStats(ctypes.Structure):
 SIGNATURES = {
     "sem1d_version": (c_int, []),
     "sem1d_set_kernel_path": (c_int, [c_int]),
+    "sem1d_set_tile_variant": (c_int, [c_int]),
     "sem1d_last_error": (ctypes.c_char_p, []),
     "sem1d_max_degree": (c_int, []),
     "sem1d_plan_create": (c_int, [c_int64, c_int, c_int, c_double, c_void_p, c_void_p, c_void_p,
@@ -72,6 +73,8 @@ SIGNATURES = {
     "sem1d_adj_step_stages": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int,
                                       c_void_p, c_void_p]),
     "sem1d_rk_step": (c_int, [c_void_p, c_void_p, c_void_p, c_double, c_int, c_void_p, c_void_p]),
+    "sem1d_rk_step_ex": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int, c_int, c_void_p,
+                                 c_void_p]),
     "sem1d_adj_step": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int, c_void_p,
                                c_void_p]),
     "sem1d_terminal_work_size": (c_int64, [c_void_p]),

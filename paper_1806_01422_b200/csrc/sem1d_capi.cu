@@ -32,6 +32,8 @@ SEM_DECL(30) SEM_DECL(31) SEM_DECL(32)
 namespace sem1d {
 static int g_path_override = 0;
 int sem1d_path_override() { return g_path_override; }
+static int g_tile_variant = 0;
+int sem1d_tile_variant() { return g_tile_variant; }
 }  // namespace sem1d
 
 struct sem1d_plan {
@@ -371,6 +373,13 @@ int sem1d_set_kernel_path(int path) {
   return SEM1D_OK;
 }
 const char* sem1d_last_error(void) { return g_err.c_str(); }
+
+int sem1d_set_tile_variant(int variant) {
+  if (variant < 0 || variant > 2)
+    return fail(SEM1D_EINVAL, "sem1d_set_tile_variant: 0 (auto), 1 (shared-memory tiles), 2 (N = 7 forward at 128-element tiles)");
+  g_tile_variant = variant;
+  return SEM1D_OK;
+}
 int sem1d_max_degree(void) { return SEM1D_MAX_DEGREE; }
 
 // ---- LINEAR / NONE advection (ops.py:147-212 branches) --------------------------------
@@ -648,7 +657,7 @@ int sem1d_rk_step(const sem1d_plan* plan, const double* u, double* u_new, double
   TileStepArgs a;
   std::memset(&a, 0, sizeof(a));
   if (!make_tableau(scheme, a.tab)) return fail(SEM1D_EINVAL, "sem1d_rk_step: unknown scheme");
-  a.u = u; a.out = u_new; a.flag = flag; a.dt = dt;
+  a.u = u; a.out = u_new; a.flag = flag; a.dt = dt; a.check = 1;
   cudaError_t e = dispatch_tile(plan, 0, a, static_cast<cudaStream_t>(stream));
   if (e == cudaErrorNotSupported)
     return fail(SEM1D_EINVAL, "sem1d_rk_step: needs a periodic batch-1 ring, N+1 in {8,16,24,32}, E >= 2 tiles");
@@ -664,11 +673,34 @@ int sem1d_adj_step(const sem1d_plan* plan, const double* u, const double* lam, d
   TileStepArgs a;
   std::memset(&a, 0, sizeof(a));
   if (!make_tableau(scheme, a.tab)) return fail(SEM1D_EINVAL, "sem1d_adj_step: unknown scheme");
-  a.u = u; a.lam = lam; a.out = lam_out; a.flag = flag; a.dt = dt;
+  a.u = u; a.lam = lam; a.out = lam_out; a.flag = flag; a.dt = dt; a.check = 1;
   cudaError_t e = dispatch_tile(plan, 1, a, static_cast<cudaStream_t>(stream));
   if (e == cudaErrorNotSupported)
     return fail(SEM1D_EINVAL, "sem1d_adj_step: needs a periodic batch-1 ring, N+1 in {8,16,24,32}, E >= 2 tiles");
   if (e != cudaSuccess) return cuda_fail(e, "sem1d_adj_step");
+  return SEM1D_OK;
+}
+
+int sem1d_rk_step_ex(const sem1d_plan* plan, const double* u, double* u_new, double* const* stages,
+                     double dt, int scheme, int check, int* flag, void* stream) {
+  DeviceGuard guard_(plan ? plan->device : -1);
+  if (!valid_burgers(plan) || !u || !u_new || !flag || u == u_new)
+    return fail(SEM1D_EINVAL, "sem1d_rk_step_ex: bad argument (u_new must not alias u)");
+  TileStepArgs a;
+  std::memset(&a, 0, sizeof(a));
+  if (!make_tableau(scheme, a.tab)) return fail(SEM1D_EINVAL, "sem1d_rk_step_ex: unknown scheme");
+  if (stages) {
+    if (a.tab.s < 2) return fail(SEM1D_EINVAL, "sem1d_rk_step_ex: a one-stage scheme has no stage states");
+    for (int i = 0; i + 1 < a.tab.s; ++i) {
+      if (!stages[i]) return fail(SEM1D_EINVAL, "sem1d_rk_step_ex: NULL stage buffer");
+      a.stages[i] = stages[i];
+    }
+  }
+  a.u = u; a.out = u_new; a.flag = flag; a.dt = dt; a.check = check ? 1 : 0;
+  cudaError_t e = dispatch_tile(plan, 0, a, static_cast<cudaStream_t>(stream));
+  if (e == cudaErrorNotSupported)
+    return fail(SEM1D_EINVAL, "sem1d_rk_step_ex: needs a periodic batch-1 ring, N+1 in {8,16,24,32}, E >= 2 tiles");
+  if (e != cudaSuccess) return cuda_fail(e, "sem1d_rk_step_ex");
   return SEM1D_OK;
 }
 
@@ -697,7 +729,7 @@ int sem1d_rk_step_stages(const sem1d_plan* plan, const double* u, double* u_new,
     if (!stages[i]) return fail(SEM1D_EINVAL, "sem1d_rk_step_stages: NULL stage buffer");
     a.stages[i] = stages[i];
   }
-  a.u = u; a.out = u_new; a.flag = flag; a.dt = dt;
+  a.u = u; a.out = u_new; a.flag = flag; a.dt = dt; a.check = 1;
   cudaError_t e = dispatch_tile(plan, 0, a, static_cast<cudaStream_t>(stream));
   if (e == cudaErrorNotSupported)
     return fail(SEM1D_EINVAL, "sem1d_rk_step_stages: needs a periodic batch-1 ring, N+1 in {8,16,24,32}");
@@ -718,7 +750,7 @@ int sem1d_adj_step_stages(const sem1d_plan* plan, const double* u, const double*
     if (!stages[i]) return fail(SEM1D_EINVAL, "sem1d_adj_step_stages: NULL stage buffer");
     a.stin[i] = stages[i];
   }
-  a.u = u; a.lam = lam; a.out = lam_out; a.flag = flag; a.dt = dt;
+  a.u = u; a.lam = lam; a.out = lam_out; a.flag = flag; a.dt = dt; a.check = 1;
   cudaError_t e = dispatch_tile(plan, 1, a, static_cast<cudaStream_t>(stream));
   if (e == cudaErrorNotSupported)
     return fail(SEM1D_EINVAL, "sem1d_adj_step_stages: needs a periodic batch-1 ring, N+1 in {8,16,24,32}");

@@ -728,6 +728,8 @@ struct TileStepArgs {
   Tableau tab;
   double* stages[3];      // forward: also write the stage states U_1..U_{s-1} (NULL: don't)
   const double* stin[3];  // adjoint: read U_1..U_{s-1} instead of recomputing them (NULL: recompute)
+  int check;              // 1: classify non-finite stage inputs (STATE bit); 0: outputs only
+                          // (register-resident N = 7 kernels; the others always classify)
 };
 
 // Tile loader shared by the step kernels: interior tiles arrive by one bulk

@@ -11,6 +11,7 @@
 #include "sem1d_device.cuh"
 #include "sem1d_ensemble.cuh"
 #include "sem1d_smallring.cuh"
+#include "sem1d_tilerf.cuh"
 
 namespace sem1d {
 
@@ -18,6 +19,9 @@ namespace sem1d {
 // tensor-core kernel, else TMA/DFMA, else plain), 1 = no tensor-core path,
 // 2 = plain kernel only, 3 = the first (CTA-synchronous) tensor-core kernel.
 int sem1d_path_override();
+// Tile-step kernel variant for A/B measurements and tests: 0 = auto (register-resident
+// N = 7 kernels), 1 = the shared-memory tile kernels for every degree
+int sem1d_tile_variant();
 
 #ifndef WS_PDL
 #define WS_PDL 1
@@ -309,9 +313,28 @@ cudaError_t launch_tile_one(const PlanView& p, const TileStepArgs& a, int thread
   return cudaLaunchKernelEx(&cfg, KERN, *static_cast<const Consts<N>*>(p.consts), p.geo, a);
 }
 
+// register-resident N = 7 forward step (sem1d_tilerf.cuh)
+template <int SCH, int WMT, int MINB>
+cudaError_t launch_tile_rf(const PlanView& p, const TileStepArgs& a, cudaStream_t s) {
+  constexpr size_t sm = RfCfg<WMT>::smem;
+  constexpr int th = 32 * RfCfg<WMT>::W;
+  if (a.stages[0])
+    return a.check ? launch_tile_one<7, tile_step_rf_kernel<SCH, true, true, WMT, MINB>>(p, a, th, sm, sm, s)
+                   : launch_tile_one<7, tile_step_rf_kernel<SCH, true, false, WMT, MINB>>(p, a, th, sm, sm, s);
+  return a.check ? launch_tile_one<7, tile_step_rf_kernel<SCH, false, true, WMT, MINB>>(p, a, th, sm, sm, s)
+                 : launch_tile_one<7, tile_step_rf_kernel<SCH, false, false, WMT, MINB>>(p, a, th, sm, sm, s);
+}
+
 template <int N, int SCH>
 cudaError_t launch_tile_sch(const PlanView& p, int kind, const TileStepArgs& a, cudaStream_t s) {
   using TC = TileCfg<N>;
+  if constexpr (N == 7) {
+    const int var = sem1d_tile_variant();
+    if (kind == 0 && var != 1) {
+      if (var == 2) return launch_tile_rf<SCH, 2, 3>(p, a, s);
+      return launch_tile_rf<SCH, 4, 2>(p, a, s);
+    }
+  }
   if (kind == 0) {
     if (a.stages[0]) return launch_tile_one<N, tile_step_kernel<N, TC::W, TC::WMT_F, SCH, 1>>(p, a, 32 * TC::W, TC::fwd_smem, TC::fwd_smem, s);
     return launch_tile_one<N, tile_step_kernel<N, TC::W, TC::WMT_F, SCH, 0>>(p, a, 32 * TC::W, TC::fwd_smem, TC::fwd_smem, s);
@@ -341,7 +364,10 @@ cudaError_t launch_tile_step(const PlanView& p, int kind, TileStepArgs a, cudaSt
     // ghost elements: s per side for a step (one per stage), 2s-1 for an adjoint step that
     // recomputes its stages, s when the forward stored them
     a.H = (kind == 0 || a.stin[0]) ? a.tab.s : 2 * a.tab.s - 1;
-    const int T = (kind == 0 ? TC::TE_F : (a.stin[0] ? TC::TE_L : TC::TE_A)) - 2 * a.H;
+    int te_f = TC::TE_F;
+    if constexpr (N == 7)
+      if (sem1d_tile_variant() == 2) te_f = RfCfg<2>::TE;
+    const int T = (kind == 0 ? te_f : (a.stin[0] ? TC::TE_L : TC::TE_A)) - 2 * a.H;
     a.ntiles = (int)((p.geo.E + T - 1) / T);
     switch (a.tab.s) {
       case 1: return launch_tile_sch<N, 0>(p, kind, a, s);

@@ -301,11 +301,13 @@ class SemOperator(ComposedStages):
 
     def launch_rk_step(self, u, u_new, dt, scheme, flag=None):
         """One fused step; ``flag``: device address of the int32 flag word to OR into
-        (default the operator's own -- ``integrate`` passes per-step slots when it runs ahead)."""
-        _lib.check(_lib.load().sem1d_rk_step(self._plan.handle, u.data_ptr(), u_new.data_ptr(),
-                                             float(dt), self._SCHEME_CODES[scheme],
-                                             flag or self._flag.data_ptr(), self._stream()),
-                   "sem1d_rk_step")
+        (default the operator's own -- ``integrate`` passes per-step slots when it runs ahead,
+        and then the step checks only its new state: a flagged step is re-run with the full
+        classification before any exception is raised, sem1d_rk_step_ex)."""
+        _lib.check(_lib.load().sem1d_rk_step_ex(self._plan.handle, u.data_ptr(), u_new.data_ptr(), None,
+                                                float(dt), self._SCHEME_CODES[scheme], 0 if flag else 1,
+                                                flag or self._flag.data_ptr(), self._stream()),
+                   "sem1d_rk_step_ex")
 
     supports_flag_slots = True
 
@@ -324,11 +326,12 @@ class SemOperator(ComposedStages):
         return self._stages_ok and self.step_fused_supported()
 
     def launch_rk_step_stages(self, u, u_new, stages, dt, scheme, flag=None):
-        """One fused step that also writes the stage states U_1..U_{s-1} into `stages`."""
-        _lib.check(_lib.load().sem1d_rk_step_stages(
+        """One fused step that also writes the stage states U_1..U_{s-1} into `stages`
+        (checks as in launch_rk_step)."""
+        _lib.check(_lib.load().sem1d_rk_step_ex(
             self._plan.handle, u.data_ptr(), u_new.data_ptr(), _lib.ptr_array([t.data_ptr() for t in stages]),
-            float(dt), self._SCHEME_CODES[scheme], flag or self._flag.data_ptr(), self._stream()),
-            "sem1d_rk_step_stages")
+            float(dt), self._SCHEME_CODES[scheme], 0 if flag else 1, flag or self._flag.data_ptr(),
+            self._stream()), "sem1d_rk_step_ex")
 
     def launch_adj_step_stages(self, u, stages, lam, lam_out, dt, scheme, flag=None):
         """One fused adjoint step reading the stored stage states (no recompute)."""
