@@ -325,6 +325,27 @@ cudaError_t launch_tile_rf(const PlanView& p, const TileStepArgs& a, cudaStream_
                  : launch_tile_one<7, tile_step_rf_kernel<SCH, false, false, WMT, MINB>>(p, a, th, sm, sm, s);
 }
 
+template <int SCH, bool LD, int WMT, int MINB>
+cudaError_t launch_tile_adj_rf(const PlanView& p, const TileStepArgs& a, cudaStream_t s) {
+  constexpr size_t sm = RfAdjCfg<WMT>::template smem<LD>();
+  return launch_tile_one<7, tile_adj_rf_kernel<SCH, LD, WMT, MINB>>(p, a, 32 * RfAdjCfg<WMT>::W, sm, sm, s);
+}
+
+// elements per tile of the kernel launch_tile_sch picks (kind 0 forward, 1 adjoint)
+template <int N>
+int tile_elems(int kind, bool ld) {
+  using TC = TileCfg<N>;
+  if constexpr (N == 7) {
+    const int var = sem1d_tile_variant();
+    if (var != 1) {
+      if (kind == 0) return var == 2 ? RfCfg<2>::TE : RfCfg<4>::TE;
+      if (ld) return var == 2 ? RfAdjCfg<2>::TE : RfAdjCfg<3>::TE;
+      return RfAdjCfg<4>::TE;
+    }
+  }
+  return kind == 0 ? TC::TE_F : (ld ? TC::TE_L : TC::TE_A);
+}
+
 template <int N, int SCH>
 cudaError_t launch_tile_sch(const PlanView& p, int kind, const TileStepArgs& a, cudaStream_t s) {
   using TC = TileCfg<N>;
@@ -333,6 +354,14 @@ cudaError_t launch_tile_sch(const PlanView& p, int kind, const TileStepArgs& a, 
     if (kind == 0 && var != 1) {
       if (var == 2) return launch_tile_rf<SCH, 2, 3>(p, a, s);
       return launch_tile_rf<SCH, 4, 2>(p, a, s);
+    }
+    if (kind == 1 && var != 1) {
+      if (a.stin[0]) {
+        if constexpr (SCH == 0) return cudaErrorNotSupported;
+        else if (var == 2) return launch_tile_adj_rf<SCH, true, 2, 3>(p, a, s);
+        else return launch_tile_adj_rf<SCH, true, 3, 2>(p, a, s);
+      }
+      return launch_tile_adj_rf<SCH, false, 4, 2>(p, a, s);
     }
   }
   if (kind == 0) {
@@ -364,10 +393,7 @@ cudaError_t launch_tile_step(const PlanView& p, int kind, TileStepArgs a, cudaSt
     // ghost elements: s per side for a step (one per stage), 2s-1 for an adjoint step that
     // recomputes its stages, s when the forward stored them
     a.H = (kind == 0 || a.stin[0]) ? a.tab.s : 2 * a.tab.s - 1;
-    int te_f = TC::TE_F;
-    if constexpr (N == 7)
-      if (sem1d_tile_variant() == 2) te_f = RfCfg<2>::TE;
-    const int T = (kind == 0 ? te_f : (a.stin[0] ? TC::TE_L : TC::TE_A)) - 2 * a.H;
+    const int T = tile_elems<N>(kind, a.stin[0] != nullptr) - 2 * a.H;
     a.ntiles = (int)((p.geo.E + T - 1) / T);
     switch (a.tab.s) {
       case 1: return launch_tile_sch<N, 0>(p, kind, a, s);

@@ -51,6 +51,9 @@ namespace sem1d {
 #ifndef RF_NOSTORE
 #define RF_NOSTORE 0
 #endif
+#ifndef RF_NOCHK
+#define RF_NOCHK 0          // timing experiment: no non-finite checks in the adjoint step
+#endif
 // RF_BULKOUT: results leave through shared memory and one bulk store per warp (the owned
 // node range of its 32 elements is contiguous in HBM) instead of 8 scattered 32-byte
 // register stores per lane
@@ -329,6 +332,370 @@ __global__ void __launch_bounds__(32 * RfCfg<WMT>::W, MINB)
   }
   if (RF_BULKOUT && lane == 0) bulk_wait_all();  // every bulk store has left shared memory
   const unsigned bits = (bad_state ? SEM1D_FLAG_STATE_NONFINITE : 0u) | (bad_out ? SEM1D_FLAG_STEP_NONFINITE : 0u);
+  const unsigned any = __reduce_or_sync(0xffffffffu, bits);
+  if (lane == 0 && any) atomicOr(A.flag, (int)any);
+}
+
+// ============================================================================
+// Register-resident adjoint step for N = 7 (the transpose of tile_step_rf_kernel's step,
+// adjoint.py:54-61 generalised to the tableau):
+//   l_i = dt J^T(U_i) (b_i lam + sum_{j>i} a_ji l_j),   lam_n = lam + l_{s-1} + ... + l_0.
+// Same lane layout, reflected fragments and pairwise warp exchanges as the forward kernel.
+// LD = 0: the stage states are recomputed (forward stages 0..s-2, H = 2s-1 ghost elements per
+// side); U_1..U_{s-2} wait in a per-lane shared-memory slot, U_{s-1} stays in registers.
+// LD = 1: U_1..U_{s-1} arrive with the tile (stored by the forward step, H = s).
+// J^T fragments fold dt and M^-1 (bfrag_adj values; Dw^T negated), so one accumulator
+// chain gives term1 - term3 of ops.py:195-212 and l = fma(-z, dt M^-1 Dw u, C).
+// Checks (the reference's per-call ones): a non-finite stage state sets the STATE bit, a
+// non-finite stage input z the INPUT2 ("cotangent") bit.
+// ============================================================================
+// The adjoint kernel runs the stage recurrence on w_i = z_i / b_i and l'_i = l_i / b_i:
+//   w_i = lam + sum_{j>i} (a_ji b_j / b_i) l'_j,   l'_i = dt J^T(U_i) w_i,   lam_n = lam + sum b_i l'_i,
+// which saves the b_i * lam multiply of every node and stage (w_{s-1} = lam).  The ratios are
+// exact binary fractions for the three tableaux: RK4 1/2, 1/2, 1; Kutta-3 1/2, 2, -1.
+template <int SCH>
+struct TabW {
+  __host__ __device__ static constexpr double c(int i, int j) {   // coefficient of l'_j in w_i
+    return SCH == 2 ? ((i == 2 && j == 3) ? 0.5 : (i == 1 && j == 2) ? 0.5 : (i == 0 && j == 1) ? 1.0 : 0.0)
+         : SCH == 1 ? ((i == 1 && j == 2) ? 0.5 : (i == 0 && j == 1) ? 2.0 : (i == 0 && j == 2) ? -1.0 : 0.0)
+                    : 0.0;
+  }
+};
+
+// exponent bits of a double if it may raise a flag (owned node), else 0: max-accumulated,
+// the result is non-finite iff it reaches 0x7ff00000 (two integer ops per checked value)
+__device__ __forceinline__ unsigned expbits(double x, unsigned mask) {
+  return (unsigned)__double2hiint(x) & mask;
+}
+
+template <int WMT_ = 4>
+struct RfAdjCfg {
+  static constexpr int N = 7, W = 8, WMT = WMT_, TE = 8 * W * WMT;
+  static constexpr int LEN = TE * N + 1;
+  static constexpr int PAD = ((LEN + 2) + 1) & ~1;
+  static constexpr int SLOT = W * 32 * WMT * 2;   // doubles of one per-lane stage slot
+  // slabs [2 buffers][u, lam (, U_1..U_3)] + per-lane slots (recompute) + exchange + barriers
+  template <bool LD>
+  static constexpr size_t smem() {
+    return sizeof(double) * ((size_t)2 * (LD ? 5 : 2) * PAD + (LD ? 0 : 2 * (size_t)SLOT) + 32) +
+           4 * sizeof(uint64_t);
+  }
+};
+
+__device__ __forceinline__ double bfrag_rf_adj(const Consts<7>& C, int mat, int kc, int lane, double dt) {
+  const int c = lane >> 2, k = lane & 3;
+  const int i = (c & 1) ? 7 - (c >> 1) : (c >> 1);
+  const int j = kc == 0 ? k : 7 - k;
+  const double mi = C.minv[(i == 0 || i == 7) ? 0 : i];
+  const double mj = C.minv[(j == 0 || j == 7) ? 0 : j];
+  if (mat == 0) return __dmul_rn(C.K[i * 8 + j], __dmul_rn(__dmul_rn(-C.nu, dt), mj));
+  if (mat == 1) return __dmul_rn(C.Dw[i * 8 + j], __dmul_rn(dt, mi));
+  return -__dmul_rn(C.Dw[j * 8 + i], __dmul_rn(dt, mj));
+}
+
+__device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+template <int SCH, bool LD, int WMT, int MINB>
+__global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
+    tile_adj_rf_kernel(const __grid_constant__ Consts<7> C, const Geo G, const TileStepArgs A) {
+  using CF = RfAdjCfg<WMT>;
+  constexpr int N = 7, W = CF::W, TE = CF::TE, LEN = CF::LEN, PAD = CF::PAD, SLOT = CF::SLOT;
+  using TB = TabC<SCH>;
+  constexpr int S = TB::s, H = LD ? S : 2 * S - 1, T = TE - 2 * H;
+  constexpr int NSLAB = LD ? S + 1 : 2;       // u, lam (, U_1..U_{s-1})
+  constexpr int SB = LD ? 5 : 2;              // slabs per buffer in the layout
+  extern __shared__ __align__(16) double smem[];
+  double* sslab = smem;                       // [2][SB][PAD]
+  double* sst = sslab + 2 * SB * PAD;         // [2][SLOT] recompute: U_1, U_2 per lane
+  double* xF = sst + (LD ? 0 : 2 * SLOT);     // [16]
+  double* xU = xF + 16;                       // [16]
+  uint64_t* full = reinterpret_cast<uint64_t*>(xU + 16);
+  uint64_t* empty = full + 2;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int kq = lane & 3, rr = lane >> 2;
+  const int e_lane = 8 * WMT * w + WMT * rr;
+  const int64_t ndof = G.ndof;
+  const double dt = A.dt;
+  double bk[2], bd[2], jk[2], jd[2], jt[2];
+#pragma unroll
+  for (int kc = 0; kc < 2; ++kc) {
+    bk[kc] = bfrag_rf(C, 0, kc, lane);
+    bd[kc] = bfrag_rf(C, 1, kc, lane);
+    jk[kc] = bfrag_rf_adj(C, 0, kc, lane, dt);
+    jd[kc] = bfrag_rf_adj(C, 1, kc, lane, dt);
+    jt[kc] = bfrag_rf_adj(C, 2, kc, lane, dt);
+  }
+  if (tid == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(&empty[0], W);
+    mbar_init(&empty[1], W);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  griddep_launch_dependents();
+  griddep_wait();
+  auto issue = [&](const TileLoad& Lx, int x) {
+    const double* srcs[5] = {A.u, A.lam, A.stin[0], A.stin[1], A.stin[2]};
+    double* base = sslab + x * SB * PAD;
+    double* dsts[5] = {base, base + PAD, base + 2 * PAD, base + 3 * PAD, base + 4 * PAD};
+    tile_issue_n(Lx, LEN, srcs, dsts, &full[x], NSLAB);
+  };
+  uint32_t fphase = 0u, ephase = 0u, pend = 0u;
+  int want = -1;                               // tid 0: tile whose prefetch waits for a free buffer
+  if (tid == 0 && blockIdx.x < A.ntiles) {
+    const TileLoad L = tile_load_plan(blockIdx.x, T, H, N, LEN, ndof);
+    if (L.bulk) {
+      issue(L, 0);
+      pend |= 1u;
+    }
+  }
+  // tid 0: issue the pending prefetch of tile `want` into buffer x once that buffer's
+  // readers (the tile before) are done: polled without blocking at every stage, forced
+  // (blocking) at the start of tile `want` itself
+  auto try_prefetch = [&](int x, bool block) {
+    if (tid != 0 || want < 0) return;
+    if (pend & (1u << x)) {
+      if (block) {
+        while (!mbar_try_wait(&empty[x], (ephase >> x) & 1u)) {
+        }
+      } else if (!mbar_test_wait(&empty[x], (ephase >> x) & 1u)) {
+        return;
+      }
+      ephase ^= 1u << x;
+      pend &= ~(1u << x);
+    }
+    issue(tile_load_plan(want, T, H, N, LEN, ndof), x);
+    pend |= 1u << x;
+    want = -1;
+  };
+  unsigned fstate = 0u, fz = 0u;
+  int it = 0;
+  for (int t = blockIdx.x; t < A.ntiles; t += gridDim.x, ++it) {
+    const int b = it & 1;
+    const TileLoad L = tile_load_plan(t, T, H, N, LEN, ndof);
+    // this lane's values of slab s (m-tile q, slot h) at sl[s * PAD + q * N + (h ? 7 - kq : kq)]
+    const double* sl = sslab + b * SB * PAD + L.sh + e_lane * N;
+    auto val = [&](int sidx, int q, int h) -> double { return sl[sidx * PAD + q * N + (h == 0 ? kq : 7 - kq)]; };
+    if (!L.bulk) {
+      // the tile wraps around the ring end (at most two per launch): the CTA fills the
+      // buffer itself; the barrier also means every warp is done with its previous tiles
+      __syncthreads();
+      double* dst = sslab + b * SB * PAD;
+      for (int k = tid; k < LEN; k += 32 * W) {
+        int64_t g = L.g0 + k;
+        while (g >= ndof) g -= ndof;
+        dst[k] = __ldg(A.u + g);
+        dst[PAD + k] = __ldg(A.lam + g);
+        if (LD)
+          for (int i = 1; i < S; ++i) dst[(1 + i) * PAD + k] = __ldg(A.stin[i - 1] + g);
+      }
+      __syncthreads();
+    }
+    if (tid == 0 && want == t) try_prefetch(b, true);   // this tile's load is still owed
+    if (L.bulk) {
+      while (!mbar_try_wait(&full[b], (fphase >> b) & 1u)) {
+      }
+      fphase ^= 1u << b;
+    }
+    if (tid == 0 && t + (int)gridDim.x < A.ntiles) {
+      want = tile_load_plan(t + gridDim.x, T, H, N, LEN, ndof).bulk ? t + (int)gridDim.x : -1;
+      try_prefetch(b ^ 1, false);
+    }
+    const int64_t e_base = (int64_t)t * T - H;
+    bool own[WMT];
+    unsigned msk[WMT][2];                        // check masks: owned node, not the node-7 replica
+#pragma unroll
+    for (int q = 0; q < WMT; ++q) {
+      const int e = e_lane + q;
+      own[q] = e >= H && e < H + T && e_base + e < G.E;
+      msk[q][0] = (!RF_NOCHK && own[q]) ? 0x7ff00000u : 0u;
+      msk[q][1] = (!RF_NOCHK && own[q] && kq != 0) ? 0x7ff00000u : 0u;
+    }
+    double U[WMT][2], F[WMT][2];
+    double k0[(SCH == 1) ? WMT : 1][2];
+    // pairwise exchange of a stage result R: interface sum (row 7 of e-1 into row 0 of e),
+    // then, after `mid` updated m-tile 0 and `rest` the others, the node-7 replica refresh
+    // of `Rn` (barriers run in every stage: see the forward kernel)
+    auto exchange = [&](double (&R)[WMT][2], auto&& mid, auto&& rest, double (&Rn)[WMT][2], bool refresh) {
+      double left = __shfl_up_sync(0xffffffffu, R[WMT - 1][1], 4);
+      if (w > 0) {
+        nbar_sync(RfCfg<4>::BAR_F + w - 1, 64);
+        if (lane == 0) left = xF[w - 1];
+      } else if (lane == 0) {
+        left = 0.0;
+      }
+      if (kq == 0) {
+#pragma unroll
+        for (int q = WMT - 1; q > 0; --q) R[q][0] = __dadd_rn(R[q - 1][1], R[q][0]);
+        R[0][0] = __dadd_rn(left, R[0][0]);
+      }
+      mid();
+      double right = __shfl_down_sync(0xffffffffu, Rn[0][0], 4);
+      if (w > 0) {
+        if (refresh && lane == 0) xU[w] = Rn[0][0];
+        nbar_arrive(RfCfg<4>::BAR_U + w - 1, 64);
+      }
+      rest();
+      if (w < W - 1) {
+        nbar_sync(RfCfg<4>::BAR_U + w, 64);
+        if (lane == 28) right = xU[w + 1];
+      }
+      if (refresh && kq == 0) {
+#pragma unroll
+        for (int q = 0; q + 1 < WMT; ++q) Rn[q][1] = Rn[q + 1][0];
+        Rn[WMT - 1][1] = right;
+      }
+    };
+    auto publish_F = [&](const double (&R)[WMT][2]) {
+      if (w < W - 1) {
+        if (lane == 28) xF[w] = R[WMT - 1][1];
+        nbar_arrive(RfCfg<4>::BAR_F + w, 64);
+      }
+    };
+    // ---- forward recompute of U_1..U_{s-1} (LD = 0) ----
+    if constexpr (!LD) {
+#pragma unroll
+      for (int q = 0; q < WMT; ++q)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) U[q][h] = val(0, q, h);
+#pragma unroll
+      for (int st = 0; st + 1 < S; ++st) {
+#pragma unroll
+        for (int q = 0; q < WMT; ++q)
+          fstate = max(fstate, max(expbits(U[q][0], msk[q][0]), expbits(U[q][1], msk[q][1])));
+        auto mtile_F = [&](int q) {
+          double ka = 0.0, kb = 0.0, da = 0.0, db = 0.0;
+          dmma884(ka, kb, U[q][0], bk[0]);
+          dmma884(da, db, U[q][0], bd[0]);
+          dmma884(ka, kb, U[q][1], bk[1]);
+          dmma884(da, db, U[q][1], bd[1]);
+          F[q][0] = __fma_rn(-U[q][0], da, ka);
+          F[q][1] = __fma_rn(-U[q][1], db, kb);
+        };
+        mtile_F(WMT - 1);
+        publish_F(F);
+#pragma unroll
+        for (int q = 0; q + 1 < WMT; ++q) mtile_F(q);
+        try_prefetch(b ^ 1, false);
+        const double c1 = __dmul_rn(dt, TB::a(st + 1, st));
+        auto upd = [&](int q) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const double k = F[q][h];
+            if (TB::nterm(st + 1) == 1) {
+              U[q][h] = __fma_rn(c1, k, val(0, q, h));
+            } else {
+              const double s2 = __fma_rn(TB::a(st + 1, st), k, __dmul_rn(TB::a(st + 1, 0), k0[q][h]));
+              U[q][h] = __fma_rn(dt, s2, val(0, q, h));
+            }
+            if (SCH == 1 && st == 0) k0[q][h] = k;
+          }
+        };
+        exchange(F, [&] { upd(0); },
+                 [&] {
+#pragma unroll
+                   for (int q = 1; q < WMT; ++q) upd(q);
+                 },
+                 U, true);
+        if (st + 2 < S) {                       // U_{st+1} waits in its per-lane slot
+          double* slot = sst + st * SLOT;
+#pragma unroll
+          for (int q = 0; q < WMT; ++q)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) slot[((w * WMT + q) * 2 + h) * 32 + lane] = U[q][h];
+        }
+      }
+    }
+    // ---- backward: stage-adjoint recurrence ----
+    double ln[WMT][2], lacc[WMT][2], l2[(SCH == 1) ? WMT : 1][2];   // l'_{i+1}, sum b l', l'_2
+    using TW = TabW<SCH>;
+#pragma unroll
+    for (int i = S - 1; i >= 0; --i) {
+      // stage state U_i
+      if (LD || i + 1 < S || S == 1) {            // (recompute: U_{s-1} is still in registers)
+#pragma unroll
+        for (int q = 0; q < WMT; ++q)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (i == 0) U[q][h] = val(0, q, h);
+            else if (LD) U[q][h] = val(1 + i, q, h);
+            else U[q][h] = sst[(i - 1) * SLOT + ((w * WMT + q) * 2 + h) * 32 + lane];
+          }
+      }
+      if (LD || i == S - 1) {                    // U_0..U_{s-2} were checked as stage inputs
+#pragma unroll
+        for (int q = 0; q < WMT; ++q)
+          fstate = max(fstate, max(expbits(U[q][0], msk[q][0]), expbits(U[q][1], msk[q][1])));
+      }
+      double Lr[WMT][2];                         // l'_i (element rows, then assembled)
+      auto mtile_L = [&](int q) {
+        double z[2], y[2];                       // z = w_i here
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double zz = val(1, q, h);
+          if (i + 1 < S && TW::c(i, i + 1) != 0.0) zz = __fma_rn(TW::c(i, i + 1), ln[q][h], zz);
+          if (SCH == 1 && i == 0) zz = __fma_rn(TW::c(0, 2), l2[q][h], zz);
+          z[h] = zz;
+          y[h] = __dmul_rn(U[q][h], zz);
+        }
+        if (i + 1 < S) fz = max(fz, max(expbits(z[0], msk[q][0]), expbits(z[1], msk[q][1])));
+        double ca = 0.0, cb = 0.0, da = 0.0, db = 0.0;
+        dmma884(ca, cb, z[0], jk[0]);
+        dmma884(da, db, U[q][0], jd[0]);
+        dmma884(ca, cb, z[1], jk[1]);
+        dmma884(da, db, U[q][1], jd[1]);
+        dmma884(ca, cb, y[0], jt[0]);
+        dmma884(ca, cb, y[1], jt[1]);
+        Lr[q][0] = __fma_rn(-z[0], da, ca);
+        Lr[q][1] = __fma_rn(-z[1], db, cb);
+      };
+      if (i == S - 1) {                          // w_{s-1} = lam: the cotangent input check
+#pragma unroll
+        for (int q = 0; q < WMT; ++q) fz = max(fz, max(expbits(val(1, q, 0), msk[q][0]), expbits(val(1, q, 1), msk[q][1])));
+      }
+      mtile_L(WMT - 1);
+      publish_F(Lr);
+#pragma unroll
+      for (int q = 0; q + 1 < WMT; ++q) mtile_L(q);
+      try_prefetch(b ^ 1, false);
+      auto acc_q = [&](int q) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          lacc[q][h] = (i == S - 1) ? __dmul_rn(TB::b(i), Lr[q][h]) : __fma_rn(TB::b(i), Lr[q][h], lacc[q][h]);
+          if (SCH == 1 && i == 1) l2[q][h] = ln[q][h];
+          ln[q][h] = Lr[q][h];
+        }
+      };
+      exchange(Lr, [&] { acc_q(0); },
+               [&] {
+#pragma unroll
+                 for (int q = 1; q < WMT; ++q) acc_q(q);
+               },
+               ln, i > 0);
+    }
+    // lam_n = lam + (b_{s-1} l'_{s-1} + ... + b_0 l'_0), owned nodes
+#pragma unroll
+    for (int q = 0; q < WMT; ++q) {
+      if (!own[q]) continue;
+      const int64_t g = (e_base + e_lane + q) * N;
+      A.out[g + kq] = __dadd_rn(val(1, q, 0), lacc[q][0]);
+      if (kq != 0) A.out[g + 7 - kq] = __dadd_rn(val(1, q, 1), lacc[q][1]);
+    }
+    __syncwarp();
+    if (L.bulk && lane == 0) mbar_arrive(&empty[b]);   // this warp is done with the tile's slabs
+  }
+  const unsigned bits = (fstate == 0x7ff00000u ? SEM1D_FLAG_STATE_NONFINITE : 0u) |
+                        (fz == 0x7ff00000u ? SEM1D_FLAG_INPUT2_NONFINITE : 0u);
   const unsigned any = __reduce_or_sync(0xffffffffu, bits);
   if (lane == 0 && any) atomicOr(A.flag, (int)any);
 }
