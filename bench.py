@@ -51,6 +51,9 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-sweep", action="store_true")
+    p.add_argument("--sweep-steps", type=int, default=64)
+    p.add_argument("--no-cfg5", action="store_true")
+    p.add_argument("--cfg5-steps", type=int, default=8)
     # test-only: exercise the sharded path with every rank on cuda:0 and a gloo exchange
     # (safe on one GPU: no kernel waits on another rank)
     p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"])
@@ -353,6 +356,161 @@ def sweep_ratio(op, torch, steps=8):
                        if getattr(op, "step_fused_supported", lambda: False)() else "per-stage"}
 
 
+FP64_PEAK_TFS = 36.98   # measured DMMA m8n8k4 f64 peak on this pool's B200 (profiles/r1_dmma_chains.jsonl)
+# whole-step kernels, per DOF of the ring: FP64 work (reference flop counts)
+# and algorithmic HBM bytes (each input read once, each output written once)
+STEP_BYTES = {"fwd": 16, "fwd_st": 40, "adj": 24, "adj_st": 48}
+
+
+def step_flops(kind, N=7):
+    f, j = flop_per_dof(N, "F"), flop_per_dof(N, "J")
+    return {"fwd": 4 * f, "fwd_st": 4 * f, "adj": 3 * f + 4 * j, "adj_st": 4 * j}[kind]
+
+
+def roofline_entry(us, flops_per_dof, bytes_per_dof, dof, hbm_gbs):
+    t_flop = flops_per_dof * dof / (FP64_PEAK_TFS * 1e12) * 1e6
+    t_byte = bytes_per_dof * dof / (hbm_gbs * 1e9) * 1e6
+    bound = "fp64" if t_flop >= t_byte else "hbm"
+    return {"us": us, "fp64_tflops": flops_per_dof * dof / (us * 1e-6) / 1e12,
+            "achieved_gbs": bytes_per_dof * dof / (us * 1e-6) / 1e9, "bound": bound,
+            "roofline_us": max(t_flop, t_byte), "frac": max(t_flop, t_byte) / us}
+
+
+def tile_kernel_times(op, torch, hbm_gbs, reps=20):
+    """The RK4 whole-step kernels on the config-2 field, CUDA events around `reps`
+    back-to-back launches on the launching stream: forward step (run-ahead form), forward
+    step writing its stage states, adjoint step with stage recompute, adjoint step reading
+    the stored stages.  Roofline = the slower of FP64 work at the measured DMMA peak and
+    algorithmic bytes at the measured HBM bandwidth."""
+    if not getattr(op, "step_fused_supported", lambda: False)():
+        return None
+    u = torch.sin(torch.linspace(0, 50, op.ndof, dtype=torch.float64, device=op.device))
+    lam = torch.cos(torch.linspace(0, 50, op.ndof, dtype=torch.float64, device=op.device))
+    o = op.empty()
+    st = [op.empty() for _ in range(3)]
+    slot = op.flag_slots(1)
+    dt = 1e-14
+    runs = {"fwd": lambda: op.launch_rk_step(u, o, dt, "rk4", flag=slot.data_ptr()),
+            "fwd_st": lambda: op.launch_rk_step_stages(u, o, st, dt, "rk4"),
+            "adj": lambda: op.launch_adj_step(u, lam, o, dt, "rk4"),
+            "adj_st": lambda: op.launch_adj_step_stages(u, st, lam, o, dt, "rk4")}
+    out = {}
+    for k, fn in runs.items():
+        for _ in range(3):
+            fn()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            fn()
+        b.record()
+        torch.cuda.synchronize()
+        us = 1e3 * a.elapsed_time(b) / reps
+        out[k] = roofline_entry(us, step_flops(k), STEP_BYTES[k], op.ndof, hbm_gbs)
+    if op.flags() or int(slot[0]):
+        raise RuntimeError("non-finite flag in the tile-kernel timing")
+    del u, lam, o, st
+    return out
+
+
+def cfg3_ops(torch, dev, reps=20):
+    """BASELINE config 3 (E = 2^18, N = 31, nu = 1e-3): F, J v, J^T w per launch (CUDA events
+    around each launch); FP64-bound -- fraction of the measured DMMA peak."""
+    from paper_1806_01422_b200 import configs
+    c = configs.CFG3
+    op = configs.cfg_operator(c, device=dev)
+    u, v, w = configs.operator_inputs(op.ndof, c["seed"])
+    ud, vd, wd = (torch.from_numpy(a).to(dev) for a in (u, v, w))
+    o = op.empty()
+    runs = {"F": lambda: op.launch_rhs(ud, o), "J": lambda: op.launch_jac(ud, vd, o),
+            "JT": lambda: op.launch_jact(ud, wd, o)}
+    out = {}
+    for k, fn in runs.items():
+        for _ in range(3):
+            fn()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * reps)]
+        for r in range(reps):
+            ev[2 * r].record()
+            fn()
+            ev[2 * r + 1].record()
+        torch.cuda.synchronize()
+        us = 1e3 * sum(ev[2 * r].elapsed_time(ev[2 * r + 1]) for r in range(reps)) / reps
+        ev[0].record()                          # back to back (PDL overlap kept), events at the ends
+        for r in range(reps):
+            fn()
+        ev[1].record()
+        torch.cuda.synchronize()
+        us_b2b = 1e3 * ev[0].elapsed_time(ev[1]) / reps
+        fl = flop_per_dof(c["N"], "F" if k == "F" else "J") * op.ndof
+        out[k] = {"us": us, "fp64_tflops": fl / (us * 1e-6) / 1e12,
+                  "frac_of_dmma_peak": fl / (us * 1e-6) / 1e12 / FP64_PEAK_TFS,
+                  "us_back_to_back": us_b2b, "frac_back_to_back": fl / (us_b2b * 1e-6) / 1e12 / FP64_PEAK_TFS}
+    if op.flags():
+        raise RuntimeError("non-finite flag in config 3")
+    return {"workload": "BASELINE config 3: E=2^18, N=31, nu=1e-3, periodic [-1,1]", "dof": op.ndof,
+            "fp64_peak_tflops": FP64_PEAK_TFS, "per_op": out}
+
+
+def cfg5_sweep(torch, dist, world, rank, dev, steps, backend="nccl"):
+    """BASELINE config 5's ring (E = 2^25, N = 7, h = 1/64, nu = 1e-3, 234,881,024 DOF),
+    strong-scaled: the same global ring at every N, `steps` fused RK4 forward steps then
+    `steps` fused adjoint steps (stage recompute, as the binomial-checkpointed gradient runs
+    them), dt = 2e-4, smooth 32-mode u0.  Sharded (N > 1): contiguous element blocks, 8-element
+    ghost zones, one NCCL halo exchange per step overlapped with the interior tiles.
+    Times on the device (CUDA events), max over ranks."""
+    from paper_1806_01422_b200 import configs
+    from paper_1806_01422_b200 import dist as sd
+    from paper_1806_01422_b200.grid import grid_1d
+    from paper_1806_01422_b200.ops import PdeCoefficients, SemOperator
+    c = configs.CFG5
+    E = c["E"]
+    g = grid_1d(0.0, E * c["h"], E, c["N"])
+    if world == 1:
+        op = SemOperator(g, PdeCoefficients(c["nu"]), device=dev)
+        u0 = configs.fourier_field_device(g, c["modes"], c["seed"], dev) / 8.0
+        lam0 = configs.fourier_field_device(g, c["modes"], c["seed"] + 1, dev)
+    else:
+        op = sd.ShardedOperator(g, PdeCoefficients(c["nu"]), rank, world, device=dev)
+        sl = slice(op.part.g_lo, op.part.g_lo + op.part.n_own)
+        u0 = op.field((configs.fourier_field_device(g, c["modes"], c["seed"], dev) / 8.0)[sl].contiguous())[0]
+        lam0 = op.field(configs.fourier_field_device(g, c["modes"], c["seed"] + 1, dev)[sl].contiguous())[0]
+    dt = c["dt"]
+    states = [u0] + [op.empty() for _ in range(steps)]
+    lam = [lam0.clone(), op.empty()]
+
+    def run(k):
+        for i in range(k):
+            op.launch_rk_step(states[i], states[i + 1], dt, "rk4")
+        f1 = torch.cuda.Event(enable_timing=True)
+        f1.record()
+        for i in range(k - 1, -1, -1):
+            op.launch_adj_step(states[i], lam[0], lam[1], dt, "rk4")
+            lam.reverse()
+        return f1
+
+    run(1)                                       # warm-up (allocations, first launches)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    mid = run(steps)
+    z.record()
+    torch.cuda.synchronize()
+    t = [a.elapsed_time(mid), mid.elapsed_time(z)]
+    if world > 1:
+        tt = torch.tensor(t, device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = tt.tolist()
+    if op.flags():
+        raise RuntimeError("non-finite flag in the config-5 sweep")
+    dof = E * c["N"]
+    del states, lam, u0, lam0
+    return {"n_gpus": world, "E": E, "dof": dof, "steps": steps, "forward_ms": t[0], "adjoint_ms": t[1],
+            "ms_per_step_pair": (t[0] + t[1]) / steps,
+            "dof_steps_per_s": 2 * dof * steps / ((t[0] + t[1]) * 1e-3),
+            "forward_dof_per_s": dof * steps / (t[0] * 1e-3), "adjoint_dof_per_s": dof * steps / (t[1] * 1e-3)}
+
+
 def run_gpu_arm(args):
     import numpy as np
     import torch
@@ -365,7 +523,11 @@ def run_gpu_arm(args):
         local = 0
     if world > 1:
         torch.cuda.set_device(local)
+        if args.dist_backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")      # communicator ranks in the log
         dist.init_process_group(args.dist_backend)
+        print(f"[bench] rank {rank}/{world} local_rank {local} device {torch.cuda.get_device_name(local)} "
+              f"backend {dist.get_backend()}", file=sys.stderr, flush=True)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     c = configs.CFG2
@@ -453,9 +615,40 @@ def run_gpu_arm(args):
     if op.flags():
         raise RuntimeError("non-finite flag raised in e2e")
 
-    sweep = None
+    sweep = tiles = cfg3 = dropin = None
     if not args.no_sweep and world == 1:
-        sweep = sweep_ratio(op, torch)
+        sweep = sweep_ratio(op, torch, steps=args.sweep_steps)
+        tiles = tile_kernel_times(op, torch, load_peaks()[0])
+        # the drop-in as a semopt user calls it: numpy in, numpy out, three serial applies
+        hu, hv, hw = u, v, w
+        op.apply_rhs(hu)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(3):
+            op.apply_rhs(hu)
+            op.apply_jacobian(hu, hv)
+            op.apply_jacobian_transpose(hu, hw)
+        dms = 1e3 * (time.perf_counter() - t0) / 3
+        dropin = {"value": 3 * ndof / (dms * 1e-3), "unit": "DOF/s", "ms_per_step": dms,
+                  "h2d_bytes_per_step": 5 * 8 * ndof, "d2h_bytes_per_step": 3 * 8 * ndof,
+                  "path": "SemOperator.apply_rhs / apply_jacobian / apply_jacobian_transpose on numpy "
+                          "arrays (what stock semopt code calls): pageable copies, serial"}
+        cfg3 = cfg3_ops(torch, dev)
+    # BASELINE config 5 strong-scaled: at N > 1 rank 0 first times the same ring alone
+    strong = None
+    if not args.no_cfg5:
+        t1 = None
+        if world > 1:
+            if rank == 0:
+                t1 = cfg5_sweep(torch, dist, 1, 0, dev, args.cfg5_steps)
+            dist.barrier()
+        strong = cfg5_sweep(torch, dist, world, rank, dev, args.cfg5_steps, args.dist_backend)
+        if t1 is not None:
+            strong["n1_reference"] = t1
+            strong["efficiency_vs_n1"] = t1["ms_per_step_pair"] / (world * strong["ms_per_step_pair"])
+        strong["note"] = ("strong scaling: the same 2^25-element ring at every N; N = 1's time is "
+                          "measured by rank 0 alone in the same job")
+        torch.cuda.empty_cache()
 
     if rank != 0:
         if world > 1:
@@ -512,6 +705,12 @@ def run_gpu_arm(args):
                 "path": ("SemOperator.apply_host: pinned host fields streamed in element chunks, "
                          "H2D / kernels / D2H overlapped on three streams") if streaming else
                         "SemOperator.apply_* on pinned host->device copies, results copied back"},
+        "tile_kernels": tiles and {"field": "config-2 ring (E=2^22, N=7), RK4, events around 20 "
+                                            "back-to-back launches", "fp64_peak_tflops": FP64_PEAK_TFS,
+                                   "bytes_per_dof": STEP_BYTES, **tiles},
+        "cfg3": cfg3,
+        "strong_scaling_cfg5": strong,
+        "e2e_dropin": dropin,
         "gpu_launches": 3 * args.steps,
         "clocks": clk.summary(),
     }

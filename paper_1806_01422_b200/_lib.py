@@ -73,8 +73,11 @@ SIGNATURES = {
     "sem1d_adj_step_stages": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int,
                                       c_void_p, c_void_p]),
     "sem1d_rk_step": (c_int, [c_void_p, c_void_p, c_void_p, c_double, c_int, c_void_p, c_void_p]),
-    "sem1d_rk_step_ex": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int, c_int, c_void_p,
-                                 c_void_p]),
+    "sem1d_rk_step_ex": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int, c_int, c_int, c_int,
+                                 c_void_p, c_void_p]),
+    "sem1d_adj_step_ex": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int, c_int, c_int,
+                                  c_void_p, c_void_p]),
+    "sem1d_step_tiling": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     "sem1d_adj_step": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int, c_void_p,
                                c_void_p]),
     "sem1d_terminal_work_size": (c_int64, [c_void_p]),

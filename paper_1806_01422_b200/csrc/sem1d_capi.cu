@@ -682,7 +682,7 @@ int sem1d_adj_step(const sem1d_plan* plan, const double* u, const double* lam, d
 }
 
 int sem1d_rk_step_ex(const sem1d_plan* plan, const double* u, double* u_new, double* const* stages,
-                     double dt, int scheme, int check, int* flag, void* stream) {
+                     double dt, int scheme, int check, int tile_lo, int tile_cnt, int* flag, void* stream) {
   DeviceGuard guard_(plan ? plan->device : -1);
   if (!valid_burgers(plan) || !u || !u_new || !flag || u == u_new)
     return fail(SEM1D_EINVAL, "sem1d_rk_step_ex: bad argument (u_new must not alias u)");
@@ -697,11 +697,59 @@ int sem1d_rk_step_ex(const sem1d_plan* plan, const double* u, double* u_new, dou
     }
   }
   a.u = u; a.out = u_new; a.flag = flag; a.dt = dt; a.check = check ? 1 : 0;
+  a.tile_lo = tile_lo; a.tile_cnt = tile_cnt;
   cudaError_t e = dispatch_tile(plan, 0, a, static_cast<cudaStream_t>(stream));
   if (e == cudaErrorNotSupported)
     return fail(SEM1D_EINVAL, "sem1d_rk_step_ex: needs a periodic batch-1 ring, N+1 in {8,16,24,32}, E >= 2 tiles");
+  if (e == cudaErrorInvalidValue)
+    return fail(SEM1D_EINVAL, "sem1d_rk_step_ex: bad tile range (ranges need N = 7)");
   if (e != cudaSuccess) return cuda_fail(e, "sem1d_rk_step_ex");
   return SEM1D_OK;
+}
+
+int sem1d_adj_step_ex(const sem1d_plan* plan, const double* u, const double* const* stages, const double* lam,
+                      double* lam_out, double dt, int scheme, int tile_lo, int tile_cnt, int* flag, void* stream) {
+  DeviceGuard guard_(plan ? plan->device : -1);
+  if (!valid_burgers(plan) || !u || !lam || !lam_out || !flag || lam == lam_out)
+    return fail(SEM1D_EINVAL, "sem1d_adj_step_ex: bad argument (lam_out must not alias lam)");
+  TileStepArgs a;
+  std::memset(&a, 0, sizeof(a));
+  if (!make_tableau(scheme, a.tab)) return fail(SEM1D_EINVAL, "sem1d_adj_step_ex: unknown scheme");
+  if (stages) {
+    if (a.tab.s < 2) return fail(SEM1D_EINVAL, "sem1d_adj_step_ex: a one-stage scheme has no stage states");
+    for (int i = 0; i + 1 < a.tab.s; ++i) {
+      if (!stages[i]) return fail(SEM1D_EINVAL, "sem1d_adj_step_ex: NULL stage buffer");
+      a.stin[i] = stages[i];
+    }
+  }
+  a.u = u; a.lam = lam; a.out = lam_out; a.flag = flag; a.dt = dt; a.check = 1;
+  a.tile_lo = tile_lo; a.tile_cnt = tile_cnt;
+  cudaError_t e = dispatch_tile(plan, 1, a, static_cast<cudaStream_t>(stream));
+  if (e == cudaErrorNotSupported)
+    return fail(SEM1D_EINVAL, "sem1d_adj_step_ex: needs a periodic batch-1 ring, N+1 in {8,16,24,32}, E >= 2 tiles");
+  if (e == cudaErrorInvalidValue)
+    return fail(SEM1D_EINVAL, "sem1d_adj_step_ex: bad tile range (ranges need N = 7)");
+  if (e != cudaSuccess) return cuda_fail(e, "sem1d_adj_step_ex");
+  return SEM1D_OK;
+}
+
+int sem1d_step_tiling(const sem1d_plan* plan, int kind, int stored, int scheme, int* ntiles, int* owned,
+                      int* ghost) {
+  DeviceGuard guard_(plan ? plan->device : -1);
+  Tableau tab;
+  if (!valid_burgers(plan) || !ntiles || !owned || !ghost || (kind != 0 && kind != 1) || !make_tableau(scheme, tab))
+    return fail(SEM1D_EINVAL, "sem1d_step_tiling: bad argument");
+  if (!sem1d_step_supported(plan)) return fail(SEM1D_EINVAL, "sem1d_step_tiling: no whole-step kernels for this plan");
+  const PlanView v = view(plan);
+  cudaError_t e = cudaErrorNotSupported;
+  switch (plan->N) {
+    case 7: e = tile_layout<7>(v, kind, stored != 0, tab.s, ntiles, owned, ghost); break;
+    case 15: e = tile_layout<15>(v, kind, stored != 0, tab.s, ntiles, owned, ghost); break;
+    case 23: e = tile_layout<23>(v, kind, stored != 0, tab.s, ntiles, owned, ghost); break;
+    case 31: e = tile_layout<31>(v, kind, stored != 0, tab.s, ntiles, owned, ghost); break;
+    default: break;
+  }
+  return e == cudaSuccess ? SEM1D_OK : fail(SEM1D_EINVAL, "sem1d_step_tiling: no whole-step kernels for this plan");
 }
 
 int sem1d_step_stages_supported(const sem1d_plan* plan) {

@@ -730,6 +730,8 @@ struct TileStepArgs {
   const double* stin[3];  // adjoint: read U_1..U_{s-1} instead of recomputing them (NULL: recompute)
   int check;              // 1: classify non-finite stage inputs (STATE bit); 0: outputs only
                           // (register-resident N = 7 kernels; the others always classify)
+  int tile_lo, tile_cnt;  // N = 7 kernels: run ring tiles (tile_lo + k) mod ntiles, k < tile_cnt
+                          // (tile_cnt 0: every tile); the other kernels need tile_cnt 0
 };
 
 // Tile loader shared by the step kernels: interior tiles arrive by one bulk

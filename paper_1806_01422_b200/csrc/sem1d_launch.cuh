@@ -297,7 +297,7 @@ cudaError_t launch_tile_one(const PlanView& p, const TileStepArgs& a, int thread
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, KERN, threads, smem);
     if (per_sm < 1) per_sm = 1;
   }
-  const int grid = (int)std::min<int64_t>(a.ntiles, (int64_t)per_sm * sms);
+  const int grid = (int)std::min<int64_t>(a.tile_cnt > 0 ? a.tile_cnt : a.ntiles, (int64_t)per_sm * sms);
   // programmatic dependent launch (consecutive steps of a sweep): the prologue overlaps the
   // previous step's drain; the kernel's griddep_wait() precedes its data path
   cudaLaunchConfig_t cfg = {};
@@ -344,6 +344,21 @@ int tile_elems(int kind, bool ld) {
     }
   }
   return kind == 0 ? TC::TE_F : (ld ? TC::TE_L : TC::TE_A);
+}
+
+// tiling of a step launch: tiles, owned elements per tile, ghost elements per side
+template <int N>
+cudaError_t tile_layout(const PlanView& p, int kind, bool ld, int s, int* ntiles, int* owned, int* ghost) {
+  if constexpr ((N + 1) % 8 != 0) {
+    return cudaErrorNotSupported;
+  } else {
+    const int H = (kind == 0 || ld) ? s : 2 * s - 1;
+    const int T = tile_elems<N>(kind, ld) - 2 * H;
+    *ntiles = (int)((p.geo.E + T - 1) / T);
+    *owned = T;
+    *ghost = H;
+    return cudaSuccess;
+  }
 }
 
 template <int N, int SCH>
@@ -395,6 +410,10 @@ cudaError_t launch_tile_step(const PlanView& p, int kind, TileStepArgs a, cudaSt
     a.H = (kind == 0 || a.stin[0]) ? a.tab.s : 2 * a.tab.s - 1;
     const int T = tile_elems<N>(kind, a.stin[0] != nullptr) - 2 * a.H;
     a.ntiles = (int)((p.geo.E + T - 1) / T);
+    bool rf = false;
+    if constexpr (N == 7) rf = sem1d_tile_variant() != 1;
+    if (a.tile_cnt != 0 && (!rf || a.tile_lo < 0 || a.tile_lo >= a.ntiles || a.tile_cnt < 0 || a.tile_cnt > a.ntiles))
+      return cudaErrorInvalidValue;
     switch (a.tab.s) {
       case 1: return launch_tile_sch<N, 0>(p, kind, a, s);
       case 3: return launch_tile_sch<N, 1>(p, kind, a, s);

@@ -134,8 +134,12 @@ __global__ void __launch_bounds__(32 * RfCfg<WMT>::W, MINB)
   // empty[x]: all W warps have read it (tracked by the issuing thread: pend = a bulk tile
   // was issued into x and its readers' arrivals are still owed)
   uint32_t fphase = 0u, ephase = 0u, pend = 0u;
-  if (tid == 0 && blockIdx.x < A.ntiles) {
-    const TileLoad L = tile_load_plan(blockIdx.x, T, H, N, LEN, ndof);
+  // tiles k = 0..cnt-1 of the launch are ring tiles (tile_lo + k) mod ntiles (a sharded
+  // step launches its interior tiles while the ghost exchange runs, then the edge tiles)
+  const int cnt = A.tile_cnt > 0 ? A.tile_cnt : A.ntiles;
+  auto tile_of = [&](int k) { return (A.tile_lo + k) % A.ntiles; };
+  if (tid == 0 && (int)blockIdx.x < cnt) {
+    const TileLoad L = tile_load_plan(tile_of(blockIdx.x), T, H, N, LEN, ndof);
     if (L.bulk) {
       tile_issue(L, LEN, A.u, sbuf, &full[0], 1, nullptr, nullptr);
       pend |= 1u;
@@ -143,7 +147,8 @@ __global__ void __launch_bounds__(32 * RfCfg<WMT>::W, MINB)
   }
   unsigned bad_state = 0u, bad_out = 0u;
   int it = 0;
-  for (int t = blockIdx.x; t < A.ntiles; t += gridDim.x, ++it) {
+  for (int k = blockIdx.x; k < cnt; k += gridDim.x, ++it) {
+    const int t = tile_of(k);
     const int b = it & 1;
     const TileLoad L = tile_load_plan(t, T, H, N, LEN, ndof);
     double u0[WMT][2], U[WMT][2], acc[WMT][2], F[WMT][2];
@@ -171,8 +176,8 @@ __global__ void __launch_bounds__(32 * RfCfg<WMT>::W, MINB)
       }
     }
     // prefetch the next tile into the other buffer once every warp has read its last tile
-    if (tid == 0 && t + (int)gridDim.x < A.ntiles) {
-      const TileLoad Ln = tile_load_plan(t + gridDim.x, T, H, N, LEN, ndof);
+    if (tid == 0 && k + (int)gridDim.x < cnt) {
+      const TileLoad Ln = tile_load_plan(tile_of(k + gridDim.x), T, H, N, LEN, ndof);
       if (Ln.bulk) {
         const int x = b ^ 1;
         if (pend & (1u << x)) {
@@ -451,9 +456,11 @@ __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
     tile_issue_n(Lx, LEN, srcs, dsts, &full[x], NSLAB);
   };
   uint32_t fphase = 0u, ephase = 0u, pend = 0u;
-  int want = -1;                               // tid 0: tile whose prefetch waits for a free buffer
-  if (tid == 0 && blockIdx.x < A.ntiles) {
-    const TileLoad L = tile_load_plan(blockIdx.x, T, H, N, LEN, ndof);
+  int want = -1;                               // tid 0: launch tile k whose prefetch waits for a buffer
+  const int cnt = A.tile_cnt > 0 ? A.tile_cnt : A.ntiles;
+  auto tile_of = [&](int k) { return (A.tile_lo + k) % A.ntiles; };
+  if (tid == 0 && (int)blockIdx.x < cnt) {
+    const TileLoad L = tile_load_plan(tile_of(blockIdx.x), T, H, N, LEN, ndof);
     if (L.bulk) {
       issue(L, 0);
       pend |= 1u;
@@ -474,13 +481,14 @@ __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
       ephase ^= 1u << x;
       pend &= ~(1u << x);
     }
-    issue(tile_load_plan(want, T, H, N, LEN, ndof), x);
+    issue(tile_load_plan(tile_of(want), T, H, N, LEN, ndof), x);
     pend |= 1u << x;
     want = -1;
   };
   unsigned fstate = 0u, fz = 0u;
   int it = 0;
-  for (int t = blockIdx.x; t < A.ntiles; t += gridDim.x, ++it) {
+  for (int k = blockIdx.x; k < cnt; k += gridDim.x, ++it) {
+    const int t = tile_of(k);
     const int b = it & 1;
     const TileLoad L = tile_load_plan(t, T, H, N, LEN, ndof);
     // this lane's values of slab s (m-tile q, slot h) at sl[s * PAD + q * N + (h ? 7 - kq : kq)]
@@ -501,14 +509,14 @@ __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
       }
       __syncthreads();
     }
-    if (tid == 0 && want == t) try_prefetch(b, true);   // this tile's load is still owed
+    if (tid == 0 && want == k) try_prefetch(b, true);   // this tile's load is still owed
     if (L.bulk) {
       while (!mbar_try_wait(&full[b], (fphase >> b) & 1u)) {
       }
       fphase ^= 1u << b;
     }
-    if (tid == 0 && t + (int)gridDim.x < A.ntiles) {
-      want = tile_load_plan(t + gridDim.x, T, H, N, LEN, ndof).bulk ? t + (int)gridDim.x : -1;
+    if (tid == 0 && k + (int)gridDim.x < cnt) {
+      want = tile_load_plan(tile_of(k + gridDim.x), T, H, N, LEN, ndof).bulk ? k + (int)gridDim.x : -1;
       try_prefetch(b ^ 1, false);
     }
     const int64_t e_base = (int64_t)t * T - H;

@@ -87,11 +87,30 @@ class HaloExchange:
         """Fill the ghost nodes of every extended field in ``fields``: one batched P2P round
         whose messages go straight from each field's owned edge slice into the neighbour's
         ghost slice (contiguous views, no pack / unpack kernels)."""
+        self.start(fields).finish()
+
+    class _Pending:
+        def __init__(self, works=(), copies=()):
+            self.works, self.copies = list(works), list(copies)
+
+        def finish(self):
+            """NCCL: the current stream waits for the exchange (no host sync); gloo: the
+            staged receives land in the ghost slices."""
+            for r in self.works:
+                r.wait()
+            for dst, src in self.copies:
+                dst.copy_(src)
+            self.works, self.copies = [], []
+
+    def start(self, fields):
+        """Post the exchange of ``fields`` and return a handle whose ``finish()`` makes the
+        current stream wait for it: kernels launched in between (the interior tiles of a
+        step, which read no ghost node) overlap the transfer."""
         import torch
         import torch.distributed as dist
         p = self.p
         if p.P == 1 or not fields:
-            return
+            return self._Pending()
         N = p.N
         o0, no = p.own0, p.n_own
         L = p.gl * N                       # left ghost nodes I receive
@@ -125,11 +144,12 @@ class HaloExchange:
                               torch.empty(o.tensor.shape, dtype=o.tensor.dtype), o.peer, self.group,
                               tag=o.tag) for o in ops]
             recv_cpu = [o.tensor for o in ops if o.op is dist.irecv]
-        for r in dist.batch_isend_irecv(ops):
-            r.wait()
-        if staged:
-            for dst, src in zip(recvs, recv_cpu):
-                dst.copy_(src)
+        works = dist.batch_isend_irecv(ops)
+        if staged:                    # host-side transfers: complete them now
+            for r in works:
+                r.wait()
+            return self._Pending(copies=list(zip(recvs, recv_cpu)))
+        return self._Pending(works=works)
 
 
 def shard_grid(global_grid, part):
@@ -299,12 +319,40 @@ class ShardedOperator:
         f = getattr(self.local, "step_fused_supported", None)
         return bool(self.part.zone >= 7 and f is not None and f())
 
+    def _tile_split(self, kind, scheme):
+        """(interior, edge) tile ranges (first, count) of a whole-step launch on the extended
+        chain: interior tiles read no ghost element, so they run while the exchange is in
+        flight (None: no split -- not the N = 7 kernels, or too few tiles)."""
+        key = (kind, scheme)
+        cache = self.__dict__.setdefault("_splits", {})
+        if key in cache:
+            return cache[key]
+        split = None
+        f = getattr(self.local, "step_tiling", None)
+        if f is not None and self.part.zone and self.part.N == 7 and getattr(self, "overlap", True):
+            try:
+                nt, T, H = f(kind, False, scheme)
+            except Exception:
+                nt = 0
+            z, Ee = self.part.zone, self.part.E_ext
+            inner = [t for t in range(nt) if t * T - H >= z and (t + 1) * T + H <= Ee - z]
+            if inner and inner == list(range(inner[0], inner[-1] + 1)) and len(inner) < nt:
+                ta, tb = inner[0], inner[-1] + 1
+                split = ((ta, tb - ta), (tb % nt, nt - tb + ta))
+        cache[key] = split
+        return split
+
     def launch_rk_step(self, u, u_new, dt, scheme, flag=None):
-        self.halo.refresh([u])
-        if flag is None:
-            self.local.launch_rk_step(u, u_new, dt, scheme)
-        else:
-            self.local.launch_rk_step(u, u_new, dt, scheme, flag=flag)
+        kw = {} if flag is None else {"flag": flag}
+        split = self._tile_split(0, scheme)
+        if split is None:
+            self.halo.refresh([u])
+            self.local.launch_rk_step(u, u_new, dt, scheme, **kw)
+            return
+        pending = self.halo.start([u])          # ghosts of u in flight ...
+        self.local.launch_rk_step(u, u_new, dt, scheme, tiles=split[0], **kw)   # ... interior tiles
+        pending.finish()
+        self.local.launch_rk_step(u, u_new, dt, scheme, tiles=split[1], **kw)   # edge tiles
 
     # run-ahead integrate (timeloop.integrate): per-step flag words of the local operator,
     # verified with one all-reduce per window so every rank rolls back at the same step
@@ -327,11 +375,16 @@ class ShardedOperator:
         return out
 
     def launch_adj_step(self, u, lam, lam_out, dt, scheme, flag=None):
-        self.halo.refresh([u, lam])
-        if flag is None:
-            self.local.launch_adj_step(u, lam, lam_out, dt, scheme)
-        else:
-            self.local.launch_adj_step(u, lam, lam_out, dt, scheme, flag=flag)
+        kw = {} if flag is None else {"flag": flag}
+        split = self._tile_split(1, scheme)
+        if split is None:
+            self.halo.refresh([u, lam])
+            self.local.launch_adj_step(u, lam, lam_out, dt, scheme, **kw)
+            return
+        pending = self.halo.start([u, lam])
+        self.local.launch_adj_step(u, lam, lam_out, dt, scheme, tiles=split[0], **kw)
+        pending.finish()
+        self.local.launch_adj_step(u, lam, lam_out, dt, scheme, tiles=split[1], **kw)
 
     def launch_terminal(self, uN, ud, lam, J_out):
         """Objective on owned nodes, all-reduced; lam = mask(2 M d) (adjoint.py:39-47)."""

@@ -299,15 +299,26 @@ class SemOperator(ComposedStages):
             self._step_ok = bool(_lib.load().sem1d_step_supported(self._plan.handle)) and not self._adv
         return self._step_ok and getattr(self, "use_fused_steps", True)
 
-    def launch_rk_step(self, u, u_new, dt, scheme, flag=None):
+    def launch_rk_step(self, u, u_new, dt, scheme, flag=None, tiles=None):
         """One fused step; ``flag``: device address of the int32 flag word to OR into
         (default the operator's own -- ``integrate`` passes per-step slots when it runs ahead,
         and then the step checks only its new state: a flagged step is re-run with the full
-        classification before any exception is raised, sem1d_rk_step_ex)."""
+        classification before any exception is raised, sem1d_rk_step_ex).  ``tiles``:
+        (first, count) ring tiles of the launch (N = 7; default all, see step_tiling)."""
+        lo, cnt = tiles or (0, 0)
         _lib.check(_lib.load().sem1d_rk_step_ex(self._plan.handle, u.data_ptr(), u_new.data_ptr(), None,
                                                 float(dt), self._SCHEME_CODES[scheme], 0 if flag else 1,
-                                                flag or self._flag.data_ptr(), self._stream()),
-                   "sem1d_rk_step_ex")
+                                                int(lo), int(cnt), flag or self._flag.data_ptr(),
+                                                self._stream()), "sem1d_rk_step_ex")
+
+    def step_tiling(self, kind, stored, scheme):
+        """(ntiles, owned elements per tile, ghost elements per side) of a whole-step launch
+        (kind 0 forward, 1 adjoint): tile t reads elements [t*owned - ghost, (t+1)*owned + ghost)."""
+        out = [_lib.ctypes.c_int() for _ in range(3)]
+        _lib.check(_lib.load().sem1d_step_tiling(self._plan.handle, int(kind), 1 if stored else 0,
+                                                 self._SCHEME_CODES[scheme], *[_lib.ctypes.byref(o) for o in out]),
+                   "sem1d_step_tiling")
+        return tuple(o.value for o in out)
 
     supports_flag_slots = True
 
@@ -325,28 +336,31 @@ class SemOperator(ComposedStages):
             self._stages_ok = bool(_lib.load().sem1d_step_stages_supported(self._plan.handle)) and not self._adv
         return self._stages_ok and self.step_fused_supported()
 
-    def launch_rk_step_stages(self, u, u_new, stages, dt, scheme, flag=None):
+    def launch_rk_step_stages(self, u, u_new, stages, dt, scheme, flag=None, tiles=None):
         """One fused step that also writes the stage states U_1..U_{s-1} into `stages`
-        (checks as in launch_rk_step)."""
+        (checks and tiles as in launch_rk_step)."""
+        lo, cnt = tiles or (0, 0)
         _lib.check(_lib.load().sem1d_rk_step_ex(
             self._plan.handle, u.data_ptr(), u_new.data_ptr(), _lib.ptr_array([t.data_ptr() for t in stages]),
-            float(dt), self._SCHEME_CODES[scheme], 0 if flag else 1, flag or self._flag.data_ptr(),
-            self._stream()), "sem1d_rk_step_ex")
+            float(dt), self._SCHEME_CODES[scheme], 0 if flag else 1, int(lo), int(cnt),
+            flag or self._flag.data_ptr(), self._stream()), "sem1d_rk_step_ex")
 
-    def launch_adj_step_stages(self, u, stages, lam, lam_out, dt, scheme, flag=None):
+    def launch_adj_step_stages(self, u, stages, lam, lam_out, dt, scheme, flag=None, tiles=None):
         """One fused adjoint step reading the stored stage states (no recompute)."""
-        _lib.check(_lib.load().sem1d_adj_step_stages(
+        lo, cnt = tiles or (0, 0)
+        _lib.check(_lib.load().sem1d_adj_step_ex(
             self._plan.handle, u.data_ptr(), _lib.ptr_array([t.data_ptr() for t in stages]), lam.data_ptr(),
-            lam_out.data_ptr(), float(dt), self._SCHEME_CODES[scheme], flag or self._flag.data_ptr(),
-            self._stream()), "sem1d_adj_step_stages")
+            lam_out.data_ptr(), float(dt), self._SCHEME_CODES[scheme], int(lo), int(cnt),
+            flag or self._flag.data_ptr(), self._stream()), "sem1d_adj_step_ex")
 
-    def launch_adj_step(self, u, lam, lam_out, dt, scheme, flag=None):
+    def launch_adj_step(self, u, lam, lam_out, dt, scheme, flag=None, tiles=None):
         """One fused adjoint step; ``flag`` as in launch_rk_step (``sweep`` runs ahead with
-        per-step flag words)."""
-        _lib.check(_lib.load().sem1d_adj_step(self._plan.handle, u.data_ptr(), lam.data_ptr(),
-                                              lam_out.data_ptr(), float(dt),
-                                              self._SCHEME_CODES[scheme], flag or self._flag.data_ptr(),
-                                              self._stream()), "sem1d_adj_step")
+        per-step flag words), ``tiles`` as in launch_rk_step."""
+        lo, cnt = tiles or (0, 0)
+        _lib.check(_lib.load().sem1d_adj_step_ex(self._plan.handle, u.data_ptr(), None, lam.data_ptr(),
+                                                 lam_out.data_ptr(), float(dt), self._SCHEME_CODES[scheme],
+                                                 int(lo), int(cnt), flag or self._flag.data_ptr(),
+                                                 self._stream()), "sem1d_adj_step_ex")
 
     # -- implicit path (Crank-Nicolson; SURVEY.md 8(f) row 1) --------------------
 

@@ -116,3 +116,41 @@ def test_partition_covers_every_node_once():
             assert p.ext_ndof == p.E_ext * N + 1
             assert (p.left is None) == (not per and r == 0) or P == 1
         assert owned == list(range(E * N + (0 if per else 1)))
+
+
+def test_sharded_tile_split_covers_every_tile_once():
+    """ShardedOperator._tile_split: the interior launch (run while the ghost exchange is in
+    flight) reads no ghost element; interior + edge launches cover every ring tile once."""
+    from paper_1806_01422_b200 import dist as sd
+    from paper_1806_01422_b200.grid import grid_1d
+
+    class FakeLocal:
+        device = "cpu"
+        counters = {}
+        max_matrix_dim = 8
+
+        def __init__(self, g, c):
+            self.g = g
+
+        def step_tiling(self, kind, stored, scheme):
+            H = 4 if kind == 0 else 7
+            T = 256 - 2 * H
+            E = self.g.axis.elements
+            return (E + T - 1) // T, T, H
+
+    for E, P in ((1 << 14, 2), (1 << 14, 8), (3000, 3)):
+        g = grid_1d(0.0, 1.0, E, 7)
+        for rank in range(P):
+            op = sd.ShardedOperator(g, None, rank, P, local_factory=FakeLocal)
+            for kind in (0, 1):
+                split = op._tile_split(kind, "rk4")
+                nt, T, H = op.local.step_tiling(kind, False, "rk4")
+                assert split is not None
+                (a0, ac), (b0, bc) = split
+                assert ac + bc == nt
+                tiles = [(a0 + k) % nt for k in range(ac)] + [(b0 + k) % nt for k in range(bc)]
+                assert sorted(tiles) == list(range(nt))
+                z, Ee = op.part.zone, op.part.E_ext
+                for k in range(ac):
+                    t = a0 + k
+                    assert t * T - H >= z and (t + 1) * T + H <= Ee - z

@@ -103,7 +103,7 @@ def test_bench_two_ranks_json_line(cuda, tmp_path):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(root, "bench.py"),
            "--gpus", "2", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--no-sweep",
-           "--same-device", "--dist-backend", "gloo"]
+           "--cfg5-steps", "2", "--same-device", "--dist-backend", "gloo"]
     out = subprocess.run(cmd, cwd=root, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
@@ -111,6 +111,9 @@ def test_bench_two_ranks_json_line(cuda, tmp_path):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
     assert "sharded" in d["config"]["parallelism"]
+    st = d["strong_scaling_cfg5"]          # config 5's ring strong-scaled over the 2 ranks
+    assert st["n_gpus"] == 2 and st["dof"] == 7 * 2 ** 25 and st["n1_reference"]["n_gpus"] == 1
+    assert st["efficiency_vs_n1"] > 0 and st["forward_ms"] > 0 and st["adjoint_ms"] > 0
 
 
 def test_sharded_evaluate_two_ranks_matches_single(cuda):
