@@ -69,23 +69,31 @@ def fourier_fields(grid, batch, n_modes, seed):
     return amps @ np.sin(phase)
 
 
-def fourier_field_device(grid, n_modes, seed, device):
+def fourier_field_device(grid, n_modes, seed, device, band=None):
     """One seeded smooth Fourier field sum_k a_k sin(2 pi k (x - xa) / L), a_k ~ U(-1, 1),
     evaluated on the device from the closed-form node coordinates (config 5 sizes make
-    the host outer product of fourier_fields prohibitive)."""
+    the host outer product of fourier_fields prohibitive).  ``band`` = (kmin, kmax): the n_modes
+    angular wavenumbers are drawn uniformly from that band instead (rounded to periodic
+    modes of the ring), so the fields have structure on the element scale, where viscosity
+    acts within a config-5 horizon."""
     import torch
     ax = grid.axis
     rng = np.random.default_rng(seed)
     amps = rng.uniform(-1.0, 1.0, n_modes)
+    if band is not None:
+        kappa = rng.uniform(band[0], band[1], n_modes)
+        modes = np.maximum(1.0, np.round(kappa * ax.length / (2.0 * np.pi)))
+    else:
+        modes = np.arange(1, n_modes + 1, dtype=float)
     N, E = ax.degree, ax.elements
-    xi = torch.as_tensor(grid.bases[0].nodes[:N], device=device)
+    xi = torch.as_tensor(np.array(grid.bases[0].nodes[:N]), device=device)
     e = torch.arange(E, dtype=torch.float64, device=device)
     x = (e[:, None] * grid.h + grid.h * (xi[None, :] + 1.0) / 2.0).reshape(-1)
     if not grid.periodic:
         x = torch.cat([x, torch.tensor([E * grid.h], dtype=torch.float64, device=device)])
     out = torch.zeros_like(x)
-    for k in range(1, n_modes + 1):
-        out += float(amps[k - 1]) * torch.sin((2.0 * np.pi * k / ax.length) * x)
+    for a, m in zip(amps, modes):
+        out += float(a) * torch.sin((2.0 * np.pi * float(m) / ax.length) * x)
     return out
 
 
@@ -113,9 +121,11 @@ def cfg4_problem(B=None, steps=None, scheme="rk4", device=None, seed=CFG4["seed"
                                u_guess=u0)
 
 
-def cfg5_problem(E=None, steps=None, slots=None, device=None, seed=CFG5["seed"]):
+def cfg5_problem(E=None, steps=None, slots=None, device=None, seed=CFG5["seed"], band=None, amp=1.0 / 8.0):
     """BASELINE config 5 (single-GPU form): periodic ring of E elements (h = 1/64, N = 7,
-    nu = 1e-3); u0 = 32-mode smooth Fourier field, target = forward run of a perturbed u0."""
+    nu = 1e-3); u0 = 32-mode smooth Fourier field, target = forward run of a perturbed u0.
+    ``band``: wavenumber band of the modes (fourier_field_device); ``amp``: scale of u0 (the
+    perturbation is amp / 5)."""
     import torch
     c = CFG5
     E = c["E"] if E is None else E
@@ -124,8 +134,8 @@ def cfg5_problem(E=None, steps=None, slots=None, device=None, seed=CFG5["seed"])
     grid = grid_1d(0.0, E * c["h"], E, c["N"], PERIODIC)
     op = SemOperator(grid, PdeCoefficients(c["nu"]), device=device)
     ts = timeloop.TsConfig(scheme="rk4", t0=0.0, t_end=steps * c["dt"], dt=c["dt"])
-    u0_t = fourier_field_device(grid, c["modes"], seed, op.device) / 8.0
-    pert = fourier_field_device(grid, c["modes"], seed + 77, op.device) / 40.0
+    u0_t = fourier_field_device(grid, c["modes"], seed, op.device, band) * amp
+    pert = fourier_field_device(grid, c["modes"], seed + 77, op.device, band) * (amp / 5.0)
     target = timeloop.integrate(op, u0_t + pert, ts, store_steps=None).u_final
     del pert
     return AssimilationProblem(name="cfg5", grid=grid, op=op, ts=ts, u_target=target,

@@ -137,7 +137,10 @@ __global__ void __launch_bounds__(32 * RfCfg<WMT>::W, MINB)
   // tiles k = 0..cnt-1 of the launch are ring tiles (tile_lo + k) mod ntiles (a sharded
   // step launches its interior tiles while the ghost exchange runs, then the edge tiles)
   const int cnt = A.tile_cnt > 0 ? A.tile_cnt : A.ntiles;
-  auto tile_of = [&](int k) { return (A.tile_lo + k) % A.ntiles; };
+  auto tile_of = [&](int k) {
+    const int t = A.tile_lo + k;                // < 2 ntiles
+    return t >= A.ntiles ? t - A.ntiles : t;
+  };
   if (tid == 0 && (int)blockIdx.x < cnt) {
     const TileLoad L = tile_load_plan(tile_of(blockIdx.x), T, H, N, LEN, ndof);
     if (L.bulk) {
@@ -458,7 +461,10 @@ __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
   uint32_t fphase = 0u, ephase = 0u, pend = 0u;
   int want = -1;                               // tid 0: launch tile k whose prefetch waits for a buffer
   const int cnt = A.tile_cnt > 0 ? A.tile_cnt : A.ntiles;
-  auto tile_of = [&](int k) { return (A.tile_lo + k) % A.ntiles; };
+  auto tile_of = [&](int k) {
+    const int t = A.tile_lo + k;                // < 2 ntiles
+    return t >= A.ntiles ? t - A.ntiles : t;
+  };
   if (tid == 0 && (int)blockIdx.x < cnt) {
     const TileLoad L = tile_load_plan(tile_of(blockIdx.x), T, H, N, LEN, ndof);
     if (L.bulk) {

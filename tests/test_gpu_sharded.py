@@ -127,7 +127,7 @@ def test_sharded_evaluate_two_ranks_matches_single(cuda):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     tool = os.path.join(root, "tools", "bench_cfg5.py")
-    args = ["16384", "24", "4", "1"]
+    args = ["--E", "16384", "--steps", "24", "--slots", "4", "--iters", "2", "--band", "80,160", "--amp", "0.015625"]
     one = subprocess.run([sys.executable, tool] + args, cwd=root, capture_output=True, text=True,
                          timeout=600)
     assert one.returncode == 0, one.stderr[-2000:]
