@@ -325,10 +325,10 @@ cudaError_t launch_tile_rf(const PlanView& p, const TileStepArgs& a, cudaStream_
                  : launch_tile_one<7, tile_step_rf_kernel<SCH, false, false, WMT, MINB>>(p, a, th, sm, sm, s);
 }
 
-template <int SCH, bool LD, int WMT, int MINB>
+template <int SCH, bool LD, int WMT, int MINB, bool DR = false>
 cudaError_t launch_tile_adj_rf(const PlanView& p, const TileStepArgs& a, cudaStream_t s) {
-  constexpr size_t sm = RfAdjCfg<WMT>::template smem<LD>();
-  return launch_tile_one<7, tile_adj_rf_kernel<SCH, LD, WMT, MINB>>(p, a, 32 * RfAdjCfg<WMT>::W, sm, sm, s);
+  constexpr size_t sm = RfAdjCfg<WMT>::template smem<LD, DR>();
+  return launch_tile_one<7, tile_adj_rf_kernel<SCH, LD, WMT, MINB, DR>>(p, a, 32 * RfAdjCfg<WMT>::W, sm, sm, s);
 }
 
 // elements per tile of the kernel launch_tile_sch picks (kind 0 forward, 1 adjoint)
@@ -340,7 +340,7 @@ int tile_elems(int kind, bool ld) {
     if (var != 1) {
       if (kind == 0) return var == 2 ? RfCfg<2>::TE : RfCfg<4>::TE;
       if (ld) return var == 2 ? RfAdjCfg<2>::TE : RfAdjCfg<3>::TE;
-      return RfAdjCfg<4>::TE;
+      return var == 2 ? RfAdjCfg<4>::TE : RfAdjCfg<3>::TE;
     }
   }
   return kind == 0 ? TC::TE_F : (ld ? TC::TE_L : TC::TE_A);
@@ -376,7 +376,8 @@ cudaError_t launch_tile_sch(const PlanView& p, int kind, const TileStepArgs& a, 
         else if (var == 2) return launch_tile_adj_rf<SCH, true, 2, 3>(p, a, s);
         else return launch_tile_adj_rf<SCH, true, 3, 2>(p, a, s);
       }
-      return launch_tile_adj_rf<SCH, false, 4, 2>(p, a, s);
+      if (var == 2) return launch_tile_adj_rf<SCH, false, 4, 2>(p, a, s);
+      return launch_tile_adj_rf<SCH, false, 3, 2, true>(p, a, s);
     }
   }
   if (kind == 0) {

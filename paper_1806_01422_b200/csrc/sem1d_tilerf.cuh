@@ -383,22 +383,27 @@ struct RfAdjCfg {
   static constexpr int PAD = ((LEN + 2) + 1) & ~1;
   static constexpr int SLOT = W * 32 * WMT * 2;   // doubles of one per-lane stage slot
   // slabs [2 buffers][u, lam (, U_1..U_3)] + per-lane slots (recompute) + exchange + barriers
-  template <bool LD>
+  // recompute mode: U_1, U_2 and (DR) the stage recompute's M^-1 Dw U_i, i = 0..2, per lane
+  template <bool LD, bool DR = false>
   static constexpr size_t smem() {
-    return sizeof(double) * ((size_t)2 * (LD ? 5 : 2) * PAD + (LD ? 0 : 2 * (size_t)SLOT) + 32) +
+    return sizeof(double) * ((size_t)2 * (LD ? 5 : 2) * PAD + (LD ? 0 : (DR ? 5 : 2) * (size_t)SLOT) + 32) +
            4 * sizeof(uint64_t);
   }
 };
 
+// J^T fragments without dt (the stage recurrence's coefficients carry it): K column j by
+// -nu M^-1_j, Dw^T column j by -M^-1_j; the z o (Dw u) term uses the forward kernel's
+// M^-1-row-scaled Dw fragment (bfrag_rf mat 1), whose output the stage recompute already has
 __device__ __forceinline__ double bfrag_rf_adj(const Consts<7>& C, int mat, int kc, int lane, double dt) {
   const int c = lane >> 2, k = lane & 3;
   const int i = (c & 1) ? 7 - (c >> 1) : (c >> 1);
   const int j = kc == 0 ? k : 7 - k;
   const double mi = C.minv[(i == 0 || i == 7) ? 0 : i];
   const double mj = C.minv[(j == 0 || j == 7) ? 0 : j];
-  if (mat == 0) return __dmul_rn(C.K[i * 8 + j], __dmul_rn(__dmul_rn(-C.nu, dt), mj));
-  if (mat == 1) return __dmul_rn(C.Dw[i * 8 + j], __dmul_rn(dt, mi));
-  return -__dmul_rn(C.Dw[j * 8 + i], __dmul_rn(dt, mj));
+  (void)dt;
+  (void)mi;
+  if (mat == 0) return __dmul_rn(C.K[i * 8 + j], __dmul_rn(-C.nu, mj));
+  return -__dmul_rn(C.Dw[j * 8 + i], mj);
 }
 
 __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
@@ -412,7 +417,9 @@ __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
   return ok != 0;
 }
 
-template <int SCH, bool LD, int WMT, int MINB>
+// DR (recompute mode): J^T(U_i), i < s-1, reuses M^-1 Dw U_i from the stage recompute
+// (two of its six DMMAs per m-tile), kept in per-lane shared-memory slots
+template <int SCH, bool LD, int WMT, int MINB, bool DR = false>
 __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
     tile_adj_rf_kernel(const __grid_constant__ Consts<7> C, const Geo G, const TileStepArgs A) {
   using CF = RfAdjCfg<WMT>;
@@ -424,7 +431,8 @@ __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
   extern __shared__ __align__(16) double smem[];
   double* sslab = smem;                       // [2][SB][PAD]
   double* sst = sslab + 2 * SB * PAD;         // [2][SLOT] recompute: U_1, U_2 per lane
-  double* xF = sst + (LD ? 0 : 2 * SLOT);     // [16]
+  double* sdw = sst + 2 * SLOT;               // [3][SLOT] DR: M^-1 Dw U_0..U_2 per lane
+  double* xF = sst + (LD ? 0 : (DR ? 5 : 2) * SLOT);   // [16]
   double* xU = xF + 16;                       // [16]
   uint64_t* full = reinterpret_cast<uint64_t*>(xU + 16);
   uint64_t* empty = full + 2;
@@ -433,13 +441,12 @@ __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
   const int e_lane = 8 * WMT * w + WMT * rr;
   const int64_t ndof = G.ndof;
   const double dt = A.dt;
-  double bk[2], bd[2], jk[2], jd[2], jt[2];
+  double bk[2], bd[2], jk[2], jt[2];
 #pragma unroll
   for (int kc = 0; kc < 2; ++kc) {
     bk[kc] = bfrag_rf(C, 0, kc, lane);
     bd[kc] = bfrag_rf(C, 1, kc, lane);
     jk[kc] = bfrag_rf_adj(C, 0, kc, lane, dt);
-    jd[kc] = bfrag_rf_adj(C, 1, kc, lane, dt);
     jt[kc] = bfrag_rf_adj(C, 2, kc, lane, dt);
   }
   if (tid == 0) {
@@ -595,6 +602,10 @@ __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
           dmma884(da, db, U[q][1], bd[1]);
           F[q][0] = __fma_rn(-U[q][0], da, ka);
           F[q][1] = __fma_rn(-U[q][1], db, kb);
+          if (DR) {                               // M^-1 Dw U_st for J^T(U_st)
+            sdw[st * SLOT + ((w * WMT + q) * 2 + 0) * 32 + lane] = da;
+            sdw[st * SLOT + ((w * WMT + q) * 2 + 1) * 32 + lane] = db;
+          }
         };
         mtile_F(WMT - 1);
         publish_F(F);
@@ -651,23 +662,32 @@ __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
         for (int q = 0; q < WMT; ++q)
           fstate = max(fstate, max(expbits(U[q][0], msk[q][0]), expbits(U[q][1], msk[q][1])));
       }
-      double Lr[WMT][2];                         // l'_i (element rows, then assembled)
+      double Lr[WMT][2];                         // l'_i / dt (element rows, then assembled)
+      // dt rides on the recurrence's coefficients: w_i = lam + c dt l'', lam_n = lam + b dt l''
+      const double cdt1 = (i + 1 < S) ? __dmul_rn(TW::c(i, i + 1), dt) : 0.0;
+      const double cdt2 = (SCH == 1 && i == 0) ? __dmul_rn(TW::c(0, 2), dt) : 0.0;
+      const double bdt = __dmul_rn(TB::b(i), dt);
       auto mtile_L = [&](int q) {
         double z[2], y[2];                       // z = w_i here
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           double zz = val(1, q, h);
-          if (i + 1 < S && TW::c(i, i + 1) != 0.0) zz = __fma_rn(TW::c(i, i + 1), ln[q][h], zz);
-          if (SCH == 1 && i == 0) zz = __fma_rn(TW::c(0, 2), l2[q][h], zz);
+          if (i + 1 < S && TW::c(i, i + 1) != 0.0) zz = __fma_rn(cdt1, ln[q][h], zz);
+          if (SCH == 1 && i == 0) zz = __fma_rn(cdt2, l2[q][h], zz);
           z[h] = zz;
           y[h] = __dmul_rn(U[q][h], zz);
         }
         if (i + 1 < S) fz = max(fz, max(expbits(z[0], msk[q][0]), expbits(z[1], msk[q][1])));
         double ca = 0.0, cb = 0.0, da = 0.0, db = 0.0;
         dmma884(ca, cb, z[0], jk[0]);
-        dmma884(da, db, U[q][0], jd[0]);
+        if (DR && !LD && i + 1 < S) {            // reuse the stage recompute's M^-1 Dw U_i
+          da = sdw[i * SLOT + ((w * WMT + q) * 2 + 0) * 32 + lane];
+          db = sdw[i * SLOT + ((w * WMT + q) * 2 + 1) * 32 + lane];
+        } else {
+          dmma884(da, db, U[q][0], bd[0]);
+          dmma884(da, db, U[q][1], bd[1]);
+        }
         dmma884(ca, cb, z[1], jk[1]);
-        dmma884(da, db, U[q][1], jd[1]);
         dmma884(ca, cb, y[0], jt[0]);
         dmma884(ca, cb, y[1], jt[1]);
         Lr[q][0] = __fma_rn(-z[0], da, ca);
@@ -685,7 +705,7 @@ __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
       auto acc_q = [&](int q) {
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          lacc[q][h] = (i == S - 1) ? __dmul_rn(TB::b(i), Lr[q][h]) : __fma_rn(TB::b(i), Lr[q][h], lacc[q][h]);
+          lacc[q][h] = (i == S - 1) ? __dmul_rn(bdt, Lr[q][h]) : __fma_rn(bdt, Lr[q][h], lacc[q][h]);
           if (SCH == 1 && i == 1) l2[q][h] = ln[q][h];
           ln[q][h] = Lr[q][h];
         }
