@@ -158,9 +158,9 @@ __device__ __forceinline__ void ring_rhs(const Consts<N>& C, const Geo& G, const
         dmma884(k0, k1, au[kc], bget(0, nt, kc));
         dmma884(p0, p1, au[kc], bget(1, nt, kc));
       }
-      if (PRE) {
-        r[nt][0] = __dsub_rn(k0, __dmul_rn(au[2 * nt], p0));
-        r[nt][1] = __dsub_rn(k1, __dmul_rn(au[2 * nt + 1], p1));
+      if (PRE) {                        // one DFMA: the FP64 pipe is shared with the DMMAs
+        r[nt][0] = __fma_rn(-au[2 * nt], p0, k0);
+        r[nt][1] = __fma_rn(-au[2 * nt + 1], p1, k1);
       } else {
         r[nt][0] = __dsub_rn(__dmul_rn(k0, mnu), __dmul_rn(au[2 * nt], p0));
         r[nt][1] = __dsub_rn(__dmul_rn(k1, mnu), __dmul_rn(au[2 * nt + 1], p1));
@@ -233,7 +233,7 @@ __device__ __forceinline__ double bfrag_adj(const Consts<N>& C, int mat, int nt,
   const double b = bfrag_perm<N>(C, mat, nt, kc, lane);
   if (mat == 0) return __dmul_rn(b, __dmul_rn(__dmul_rn(-C.nu, dt), mj));
   if (mat == 1) return __dmul_rn(b, __dmul_rn(dt, mi));
-  return __dmul_rn(b, __dmul_rn(dt, mj));
+  return -__dmul_rn(b, __dmul_rn(dt, mj));     // negated: accumulates into the K chain
 }
 
 // Compile-time Butcher tableaux of the sweep kernels (same values as make_tableau:
@@ -330,27 +330,27 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_fwd_warps<N>()>::THREADS, ((N + 
           if (j == N) continue;               // node N belongs to the next element
           const int g = e * N + j;
           const double kk = kv[q][kc];
-          // acc = b0 k0 + b1 k1 + ... left to right (timeloop.py:127)
-          const double term = __dmul_rn(TB::b(i), kk);
-          acc[q][kc] = (i == 0) ? term : __dadd_rn(acc[q][kc], term);
+          // acc = b0 k0 + b1 k1 + ... left to right (timeloop.py:127), fused multiply-adds
+          // (the FP64 pipe is shared with the DMMAs: 3 instead of 7 operations per node)
+          acc[q][kc] = (i == 0) ? __dmul_rn(TB::b(i), kk) : __fma_rn(TB::b(i), kk, acc[q][kc]);
           if (i + 1 < TB::s) {
             double y;
             if (TB::nterm(i + 1) == 1) {
               // single term: u + (dt * a) * k  (timeloop.py:114)
-              y = __dadd_rn(su[g], __dmul_rn(__dmul_rn(dt, TB::a(i + 1, i)), kk));
+              y = __fma_rn(__dmul_rn(dt, TB::a(i + 1, i)), kk, su[g]);
             } else {
               // u + dt * (a0 k0 + a1 k1)  (timeloop.py:116)
               double sacc = __dmul_rn(TB::a(i + 1, 0), (i == 0) ? kk : sk[g]);
 #pragma unroll
               for (int jj = 1; jj <= i; ++jj)
-                sacc = __dadd_rn(sacc, __dmul_rn(TB::a(i + 1, jj), (jj == i) ? kk : sk[g]));
-              y = __dadd_rn(su[g], __dmul_rn(dt, sacc));
+                sacc = __fma_rn(TB::a(i + 1, jj), (jj == i) ? kk : sk[g], sacc);
+              y = __fma_rn(dt, sacc, su[g]);
             }
             sU[g] = y;
             if (g == 0) sU[ndof] = y;
             if (i == 0 && TB::keep(0)) sk[g] = kk;
           } else {
-            const double un = __dadd_rn(su[g], __dmul_rn(dt, acc[q][kc]));
+            const double un = __fma_rn(dt, acc[q][kc], su[g]);
             bad_step |= nonfinite_bit(un) != 0u;
             su[g] = un;
             if (g == 0) su[ndof] = un;
@@ -409,10 +409,16 @@ __device__ __forceinline__ void ring_jact(const Consts<N>& C, const Geo& G, cons
       for (int kc = 0; kc < KC; ++kc) {
         dmma884(k0, k1, az[kc], bget(0, nt, kc));   // K zm
         dmma884(p0, p1, au[kc], bget(1, nt, kc));   // Dw u
-        dmma884(t0, t1, at[kc], bget(2, nt, kc));   // Dw^T (u o zm)
+        if (PREJ) dmma884(k0, k1, at[kc], bget(2, nt, kc));   // - Dw^T (u o zm) into the K chain
+        else dmma884(t0, t1, at[kc], bget(2, nt, kc));        // Dw^T (u o zm)
       }
-      r[nt][0] = __dsub_rn(__dsub_rn(PREJ ? k0 : __dmul_rn(k0, mnu), __dmul_rn(az[2 * nt], p0)), t0);
-      r[nt][1] = __dsub_rn(__dsub_rn(PREJ ? k1 : __dmul_rn(k1, mnu), __dmul_rn(az[2 * nt + 1], p1)), t1);
+      if (PREJ) {                    // one DFMA per value (FP64 pipe shared with the DMMAs)
+        r[nt][0] = __fma_rn(-az[2 * nt], p0, k0);
+        r[nt][1] = __fma_rn(-az[2 * nt + 1], p1, k1);
+      } else {
+        r[nt][0] = __dsub_rn(__dsub_rn(__dmul_rn(k0, mnu), __dmul_rn(az[2 * nt], p0)), t0);
+        r[nt][1] = __dsub_rn(__dsub_rn(__dmul_rn(k1, mnu), __dmul_rn(az[2 * nt + 1], p1)), t1);
+      }
     }
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt)
@@ -587,13 +593,13 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
           const double kk = kv[q][kc];
           double y;
           if (TB::nterm(i + 1) == 1) {
-            y = __dadd_rn(su[g], __dmul_rn(__dmul_rn(dt, TB::a(i + 1, i)), kk));
+            y = __fma_rn(__dmul_rn(dt, TB::a(i + 1, i)), kk, su[g]);
           } else {
             double sacc = __dmul_rn(TB::a(i + 1, 0), (i == 0) ? kk : sk[g]);
 #pragma unroll
             for (int jj = 1; jj <= i; ++jj)
-              sacc = __dadd_rn(sacc, __dmul_rn(TB::a(i + 1, jj), (jj == i) ? kk : sk[g]));
-            y = __dadd_rn(su[g], __dmul_rn(dt, sacc));
+              sacc = __fma_rn(TB::a(i + 1, jj), (jj == i) ? kk : sk[g], sacc);
+            y = __fma_rn(dt, sacc, su[g]);
           }
           dst[g] = y;
           if (g == 0) dst[ndof] = y;
@@ -604,10 +610,11 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
     }
     // ---- stage-adjoint chain, i = S-1 .. 0 (M^-1 and -nu ride on the J^T fragments, so z
     // enters unscaled); z_i = b_i lam + a_{i+1,i} l_{i+1} + a_{i+2,i} l_{i+2} (adjoint.py:58-60)
+    // lnext / sk hold l / dt (the ring J^T output): dt rides on the coefficients
     auto zval = [&](int i, int g, int q, int kc) -> double {
       double z = __dmul_rn(TB::b(i), slam[g]);
-      if (i + 1 < S && TB::a(i + 1, i) != 0.0) z = __dadd_rn(z, __dmul_rn(TB::a(i + 1, i), lnext[q][kc]));
-      if (i + 2 < S && TB::a(i + 2, i) != 0.0) z = __dadd_rn(z, __dmul_rn(TB::a(i + 2, i), sk[g]));
+      if (i + 1 < S && TB::a(i + 1, i) != 0.0) z = __fma_rn(__dmul_rn(TB::a(i + 1, i), dt), lnext[q][kc], z);
+      if (i + 2 < S && TB::a(i + 2, i) != 0.0) z = __fma_rn(__dmul_rn(TB::a(i + 2, i), dt), sk[g], z);
       return z;
     };
 #pragma unroll
@@ -643,12 +650,12 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
           const int j = 4 * kc + kq;
           if (j == N) continue;
           const int g = ring_elem<WMT_MAX, ILV>(warp, q, rr) * N + j;
-          const double l = __dmul_rn(dt, kv[q][kc]);
+          const double l = kv[q][kc];                       // l_i / dt
           lacc[q][kc] = (i == S - 1) ? l : __dadd_rn(lacc[q][kc], l);
           if (i + 1 < S && S == 3) sk[g] = lnext[q][kc];   // RK3: keep l_{i+1} for z_{i-1}
           lnext[q][kc] = l;
           if (i == 0) {
-            const double lv = __dadd_rn(slam[g], lacc[q][kc]);
+            const double lv = __fma_rn(dt, lacc[q][kc], slam[g]);
             slam[g] = lv;
             if (g == 0) slam[ndof] = lv;
           } else {
@@ -892,23 +899,22 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
           if (j == N) continue;
           const int g = e * N + j;
           const double kk = kv[q][kc];
-          const double term = __dmul_rn(tb, kk);
-          acc[q][kc] = (st == 0) ? term : __dadd_rn(acc[q][kc], term);
+          acc[q][kc] = (st == 0) ? __dmul_rn(tb, kk) : __fma_rn(tb, kk, acc[q][kc]);
           if (!last) {
             double y;
             if (one) {
-              y = __dadd_rn(su[g], __dmul_rn(c1, kk));
+              y = __fma_rn(c1, kk, su[g]);
             } else {
               double sacc = __dmul_rn(TB::a(st + 1, 0), (st == 0) ? kk : sk[g]);
 #pragma unroll
               for (int jj = 1; jj <= st; ++jj)
-                sacc = __dadd_rn(sacc, __dmul_rn(TB::a(st + 1, jj), (jj == st) ? kk : sk[g]));
-              y = __dadd_rn(su[g], __dmul_rn(A.dt, sacc));
+                sacc = __fma_rn(TB::a(st + 1, jj), (jj == st) ? kk : sk[g], sacc);
+              y = __fma_rn(A.dt, sacc, su[g]);
             }
             sU[g] = y;
             if (st == 0 && TB::keep(0)) sk[g] = kk;
           } else {
-            const double un = __dadd_rn(su[g], __dmul_rn(A.dt, acc[q][kc]));
+            const double un = __fma_rn(A.dt, acc[q][kc], su[g]);
             if (e >= H && e < H + T) bad |= !isfinite(un);
             sU[g] = un;                         // every warp is past its last read of sU
           }
@@ -1086,13 +1092,13 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
           const double kk = kv[q][kc];
           double y;
           if (TB::nterm(i + 1) == 1) {
-            y = __dadd_rn(su[g], __dmul_rn(__dmul_rn(A.dt, TB::a(i + 1, i)), kk));
+            y = __fma_rn(__dmul_rn(A.dt, TB::a(i + 1, i)), kk, su[g]);
           } else {
             double sacc = __dmul_rn(TB::a(i + 1, 0), (i == 0) ? kk : sk[g]);
 #pragma unroll
             for (int jj = 1; jj <= i; ++jj)
-              sacc = __dadd_rn(sacc, __dmul_rn(TB::a(i + 1, jj), (jj == i) ? kk : sk[g]));
-            y = __dadd_rn(su[g], __dmul_rn(A.dt, sacc));
+              sacc = __fma_rn(TB::a(i + 1, jj), (jj == i) ? kk : sk[g], sacc);
+            y = __fma_rn(A.dt, sacc, su[g]);
           }
           dst[g] = y;
           if (i == 0 && TB::keep(0)) sk[g] = kk;
@@ -1104,8 +1110,8 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
     // with l_{i+1} in lnext and (Kutta-3) l_{i+2} in sk
     auto zval = [&](int i, int g, int q, int kc) -> double {
       double z = __dmul_rn(TB::b(i), slam[g]);
-      if (i + 1 < S && TB::a(i + 1, i) != 0.0) z = __dadd_rn(z, __dmul_rn(TB::a(i + 1, i), lnext[q][kc]));
-      if (i + 2 < S && TB::a(i + 2, i) != 0.0) z = __dadd_rn(z, __dmul_rn(TB::a(i + 2, i), sk[g]));
+      if (i + 1 < S && TB::a(i + 1, i) != 0.0) z = __fma_rn(TB::a(i + 1, i), lnext[q][kc], z);
+      if (i + 2 < S && TB::a(i + 2, i) != 0.0) z = __fma_rn(TB::a(i + 2, i), sk[g], z);
       return z;
     };
 #pragma unroll
