@@ -71,3 +71,13 @@ def test_product_never_imports_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in re.sub(r"#.*|\"\"\".*?\"\"\"", "", txt, flags=re.S), f
+
+
+def test_integration_binding_is_the_documented_one():
+    """INTEGRATION.md reproduces integration/semopt_b200.py verbatim (the executed drop-in,
+    tests/test_gpu_dropin.py), so the document cannot drift from the tested binding."""
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = open(os.path.join(root, "integration", "semopt_b200.py")).read()
+    doc = open(os.path.join(root, "INTEGRATION.md")).read()
+    assert code.strip() in doc
