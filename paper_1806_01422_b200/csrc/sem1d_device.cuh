@@ -917,15 +917,24 @@ typedef double ws_fin_t;
 #endif
 // n = 32: consumer warps per operator (A/B, config 3): 8 warps x 2 interleaved m-tiles with
 // each shared-memory B fragment feeding both (mtile_compute_multi): F / J 55.4 / 73.8 us
-// (63.0 / 82.3 at 16 x 1), J^T 90.1 us (97.4 at 16 x 1, which spilled at the 96-register cap)
+// (63.0 / 82.3 at 16 x 1), J^T 90.1 us (97.4 at 16 x 1, which spilled at the 96-register cap).
+// J and J^T (round 2): 4 warps x 2 m-tiles on 64-element tiles at 2 CTAs/SM, so the two
+// CTAs of an SM run their DMMA and epilogue phases independently: J 67.2 -> 66.4 us,
+// J^T 69.7 -> 67.0 us; F measured 47.5 either way (and 48.5 at 3 CTAs/SM).
 #ifndef WS_CW32
 #define WS_CW32 8
 #endif
+#ifndef WS_CW32_J
+#define WS_CW32_J 4
+#endif
 #ifndef WS_CW32_JT
-#define WS_CW32_JT 8
+#define WS_CW32_JT 4
 #endif
 #ifndef WS_ELEMS32
 #define WS_ELEMS32 128
+#endif
+#ifndef WS_ELEMS32_J
+#define WS_ELEMS32_J 64
 #endif
 
 // Occupancy per operator (A/B-measured on config 2, profiles/r1_ab_occupancy.json):
@@ -947,9 +956,18 @@ typedef double ws_fin_t;
 template <int OP>
 constexpr int ws_outb() { return OP == OP_RHS ? WS_OUTB_F : WS_OUTB_J; }
 
-template <int N, int OP>
+#ifndef WS_MINB32
+#define WS_MINB32 2
+#endif
+#ifndef WS_MINB32_F
+#define WS_MINB32_F 1
+#endif
+// NZ >= 0: the adjoint-stage variant (J^T with the z = b lam + sum_j a_j l_j prologue and
+// the l / lam_out epilogue, adjoint.py:54-61) reading NZ l_j slabs besides U and lam
+template <int N, int OP, int NZ = -1>
 constexpr int ws_minb() {
-  return ((N + 1) > 16) ? 1 : ((N + 1) == 16 ? 2 : (OP == OP_RHS ? WS_MINB_F8 : WS_MINB_J8));
+  if constexpr (NZ >= 0) return ((N + 1) == 32 && NZ > 0) ? 1 : 2;
+  return ((N + 1) > 16) ? (OP == OP_RHS ? WS_MINB32_F : WS_MINB32) : ((N + 1) == 16 ? 2 : (OP == OP_RHS ? WS_MINB_F8 : WS_MINB_J8));
 }
 
 // ws-kernel B fragments with permuted output columns: DMMA output column
@@ -970,14 +988,20 @@ __device__ __forceinline__ double bfrag_perm(const Consts<N>& C, int mat, int nt
 #ifndef WS_ELEMS8_J
 #define WS_ELEMS8_J WS_ELEMS8
 #endif
-template <int N, int OP = OP_RHS>
+template <int N, int OP = OP_RHS, int NZ = -1>
 struct WsTile {
   static constexpr int n = N + 1;
+  static constexpr bool ADJ = NZ >= 0;
+  // inputs staged per tile: u; v / z / lam; the adjoint stage's NZ l_j fields
+  static constexpr int NIN = (OP == OP_RHS) ? 1 : 2 + (ADJ ? NZ : 0);
   // consumer warps: n = 32 per operator (see WS_CW32 above), else 8
-  static constexpr int CW = (n == 32) ? (OP == OP_JACT ? WS_CW32_JT : WS_CW32) : 8;
+  static constexpr int CW = (n == 32) ? (ADJ ? 4 : (OP == OP_JACT ? WS_CW32_JT : (OP == OP_JAC ? WS_CW32_J : WS_CW32))) : 8;
   static constexpr int THREADS = 32 * (CW + 1);
+  // the adjoint stage stages up to 4 inputs: half-size tiles keep 2 CTAs/SM at n = 8 and 16
   static constexpr int ELEMS =
-      (n == 8) ? (OP == OP_RHS ? WS_ELEMS8 : WS_ELEMS8_J) : (n == 32 ? WS_ELEMS32 : MmaTile<N>::ELEMS);
+      ADJ ? (n == 8 ? 128 : 64)
+          : (n == 8) ? (OP == OP_RHS ? WS_ELEMS8 : WS_ELEMS8_J)
+                     : (n == 32 ? (OP == OP_RHS ? WS_ELEMS32 : WS_ELEMS32_J) : MmaTile<N>::ELEMS);
   static constexpr int WE = ELEMS / CW;                          // elements per consumer warp
   static constexpr int WMT = WE / 8;                             // m-tiles per warp
   static constexpr int NT = n / 8, KC = n / 4;
@@ -1011,6 +1035,24 @@ __device__ __forceinline__ double combine_rows(double kx, double du, double qq, 
   return __dsub_rn(__dsub_rn(__dmul_rn(kx, mnu), __dmul_rn(wi, du)), qq);
 }
 
+// Second input of the ws kernel as the consumers read it: the staged v / z slab (a plain
+// pointer), or for the adjoint stage (NZ >= 0) z of adjoint.py:58-60 formed at fragment-load
+// time from the staged lam and l_j slabs, in the reference's order:
+// z = ((b lam + a_0 l_0) + a_1 l_1) + ...
+template <int NZ>
+struct WSrc {
+  const double* w;
+  const double* l[NZ > 0 ? NZ : 1];
+  double b;
+  double a[NZ > 0 ? NZ : 1];
+  __device__ __forceinline__ double operator[](int i) const {
+    double z = __dmul_rn(b, w[i]);
+#pragma unroll
+    for (int j = 0; j < NZ; ++j) z = __dadd_rn(z, __dmul_rn(a[j], l[j][i]));
+    return z;
+  }
+};
+
 // One DMMA m-tile: 8 elements (A rows) x n rows, pointwise-combined.  Lane
 // (rr, kq) ends with rows i = 8nt + 2kq + h of element rr in r[nt][h].
 // EDGE = tile touches a Dirichlet end (masking / special M^-1 entries).
@@ -1019,9 +1061,11 @@ struct MTileOut {
   double r[N / 8 + 1][2];
 };
 
-template <int N, int OP, bool EDGE, class BGet, bool PRE = false>
+// LAST: only the last output n-tile (rows 4(2NT-2+h)+kq, which hold row N): the producer's
+// halo rows of the ws kernel need nothing else (n = 32: 16 of F's 64 DMMAs per halo m-tile)
+template <int N, int OP, bool EDGE, class BGet, bool PRE = false, bool LAST = false, class WS = const double*>
 __device__ __forceinline__ void mtile_compute(const Consts<N>& C, const Geo& G, const double* su,
-                                              const double* sw, int base, int64_t eg,
+                                              const WS& sw, int base, int64_t eg,
                                               const double* minv_a, const double (*minv_p)[2],
                                               double mnu, int kq, BGet bget, ws_fin_t& fin_u,
                                               ws_fin_t& fin_w, double (&r)[(N + 1) / 8][2]) {
@@ -1043,7 +1087,7 @@ __device__ __forceinline__ void mtile_compute(const Consts<N>& C, const Geo& G, 
     }
   }
 #pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
+  for (int nt = LAST ? NT - 1 : 0; nt < NT; ++nt) {
     double k0 = 0.0, k1 = 0.0, p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
 #pragma unroll
     for (int kc = 0; kc < KC; ++kc) {
@@ -1099,9 +1143,9 @@ __device__ __forceinline__ int ws_left_row(int rr) {
 // Q m-tiles of one warp at once (elements wbase/weg + ws_le(q, rr)): the loops over the output
 // n-tiles and k-chunks are outermost, so each B fragment -- read from shared memory when
 // the n x n matrices do not fit the register file (n = 32) -- feeds Q DMMAs instead of one.
-template <int N, int OP, bool EDGE, int Q, bool ILV, class BGet, bool PRE = false>
+template <int N, int OP, bool EDGE, int Q, bool ILV, class BGet, bool PRE = false, class WS = const double*>
 __device__ __forceinline__ void mtile_compute_multi(const Consts<N>& C, const Geo& G, const double* su,
-                                                    const double* sw, int wbase, int64_t weg, int rr,
+                                                    const WS& sw, int wbase, int64_t weg, int rr,
                                                     const double* minv_a, double mnu, int kq, BGet bget,
                                                     ws_fin_t& fin_u, ws_fin_t& fin_w,
                                                     double (&r)[Q][(N + 1) / 8][2]) {
@@ -1167,13 +1211,16 @@ __device__ __forceinline__ void mtile_compute_multi(const Consts<N>& C, const Ge
   }
 }
 
-template <int N, int OP, int EPI, int STAGES>
-__global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
+// NZ >= 0 (OP_JACT, EPI_ADJ): one adjoint stage, adjoint.py:54-61 (see WSrc and the EPI_ADJ
+// epilogue below); the same arithmetic and association as apply_kernel<N, OP_JACT, PRO_ADJ, EPI_ADJ>
+template <int N, int OP, int EPI, int STAGES, int NZ = -1>
+__global__ void __launch_bounds__(WsTile<N, OP, NZ>::THREADS, ws_minb<N, OP, NZ>())
     apply_ws_kernel(const __grid_constant__ Consts<N> C, const Geo G, const Args A,
                     const int tiles_per_ring, const int total_tiles, const double* __restrict__ frag) {
-  using W = WsTile<N, OP>;
+  using W = WsTile<N, OP, NZ>;
+  static_assert(!W::ADJ || (OP == OP_JACT && EPI == EPI_ADJ), "adjoint stage = J^T with the EPI_ADJ epilogue");
   constexpr int ELEMS = W::ELEMS, WE = W::WE, WMT = W::WMT, NT = W::NT, KC = W::KC;
-  constexpr int NIN = (OP == OP_RHS) ? 1 : 2;
+  constexpr int NIN = W::NIN;
   constexpr int NMAT = (OP == OP_JACT) ? 3 : 2;
   constexpr int SA = W::SLAB_ALLOC;
   extern __shared__ __align__(16) double smem[];
@@ -1221,10 +1268,14 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
       if (ahi < alo) ahi = alo;
     }
     const int k0 = (int)(alo - g0), k1 = (int)(ahi - g0);
-    double* dst0 = stage_buf + (s * NIN + 0) * SA + sh;
-    double* dst1 = stage_buf + (s * NIN + 1) * SA + sh;
-    const double* src0 = A.u + bofs;
-    const double* src1 = (NIN == 2) ? A.w + bofs : nullptr;
+    // inputs: u; v / z / lam; the adjoint stage's l_j
+    double* dst[NIN];
+    const double* src[NIN];
+#pragma unroll
+    for (int i = 0; i < NIN; ++i) {
+      dst[i] = stage_buf + (s * NIN + i) * SA + sh;
+      src[i] = (i == 0 ? A.u : (i == 1 ? A.w : A.zin.ptr[i - 2])) + bofs;
+    }
     auto scalar_piece = [&](int kb, int ke) {
       for (int k = kb + lane; k < ke; k += 32) {
         int64_t g = g0 + k;
@@ -1234,24 +1285,41 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
         } else if (g >= G.ndof) {
           g -= G.ndof;
         }
-        dst0[k] = valid ? __ldg(src0 + g) : 0.0;
-        if (NIN == 2) dst1[k] = valid ? __ldg(src1 + g) : 0.0;
+#pragma unroll
+        for (int i = 0; i < NIN; ++i) dst[i][k] = valid ? __ldg(src[i] + g) : 0.0;
       }
     };
     if (k0 > 0) scalar_piece(0, k0);
     if (k1 < cnt) scalar_piece(k1, cnt);
     for (int k = cnt + lane; k < (ELEMS + 1) * N + 1; k += 32) {  // ragged tile: finite pad
-      dst0[k] = 0.0;
-      if (NIN == 2) dst1[k] = 0.0;
+#pragma unroll
+      for (int i = 0; i < NIN; ++i) dst[i][k] = 0.0;
     }
     __syncwarp();
     if (lane == 0) {
       const uint32_t bytes = (uint32_t)((ahi - alo) * 8);
       mbar_expect_tx(&full[s], NIN * bytes);
       if (bytes > 0) {
-        bulk_g2s(dst0 + k0, src0 + alo, bytes, &full[s]);
-        if (NIN == 2) bulk_g2s(dst1 + k0, src1 + alo, bytes, &full[s]);
+#pragma unroll
+        for (int i = 0; i < NIN; ++i) bulk_g2s(dst[i] + k0, src[i] + alo, bytes, &full[s]);
       }
+    }
+  };
+  // the consumers' second input for stage s (slab pointer, or the adjoint stage's z)
+  auto wsrc = [&](int s, int sh) {
+    const double* w = stage_buf + (s * NIN + 1) * SA + sh;
+    if constexpr (W::ADJ) {
+      WSrc<NZ> r;
+      r.w = w;
+      r.b = A.b;
+#pragma unroll
+      for (int j = 0; j < (NZ > 0 ? NZ : 1); ++j) {
+        r.l[j] = stage_buf + (s * NIN + 2 + (j < NZ ? j : 0)) * SA + sh;
+        r.a[j] = A.zin.coef[j];
+      }
+      return r;
+    } else {
+      return w;
     }
   };
   int issued = 0;  // tiles issued so far (iteration index of the next load)
@@ -1372,24 +1440,28 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
       const int64_t e0 = (int64_t)tl * ELEMS;
       const int sh = (int)((bofs + (e0 - 1) * N) & 1);
       const double* su = stage_buf + (s * NIN + 0) * SA + sh;
-      const double* sw = stage_buf + (s * NIN + 1) * SA + sh;
+      const auto sw = wsrc(s, sh);
       while (!mbar_try_wait(&full[s], (it / STAGES) & 1)) {
       }
 #pragma unroll 1
-      for (int hm = 0; hm < W::CW / 8; ++hm) {      // one halo m-tile per 8 consumer warps
-        const int wq = hm * 8 + rr;                 // consumer warp whose left neighbour this is
+      for (int hm = 0; hm < (W::CW + 7) / 8; ++hm) {  // one halo m-tile per 8 consumer warps
+        // consumer warp whose left neighbour this is (rows past the last warp repeat it)
+        const int wq = min(hm * 8 + rr, W::CW - 1);
         const int64_t eh = e0 + wq * WE - 1;
         const int64_t ehw = (eh < 0) ? G.E - 1 : eh;
         double r[NT][2];
         ws_fin_t du_ = 0, dw_ = 0;
+        using BG = decltype(bget);
         if (!periodic && (tl == 0 || tl == tiles_per_ring - 1))
-          mtile_compute<N, OP, true>(C, G, su, sw, wq * WE * N, ehw, minv_a, minv_p, mnu, kq, bget, du_, dw_, r);
+          mtile_compute<N, OP, true, BG, false, true>(C, G, su, sw, wq * WE * N, ehw, minv_a, minv_p, mnu, kq, bget,
+                                                      du_, dw_, r);
         else if (pre)
-          mtile_compute<N, OP, false, decltype(bget), true>(C, G, su, sw, wq * WE * N, ehw, minv_a, minv_p, mnu, kq,
-                                                            bget, du_, dw_, r);
+          mtile_compute<N, OP, false, BG, true, true>(C, G, su, sw, wq * WE * N, ehw, minv_a, minv_p, mnu, kq, bget,
+                                                      du_, dw_, r);
         else
-          mtile_compute<N, OP, false>(C, G, su, sw, wq * WE * N, ehw, minv_a, minv_p, mnu, kq, bget, du_, dw_, r);
-        if (kq == 3) hrow[s * W::CW + wq] = (!periodic && eh < 0) ? 0.0 : r[NT - 1][1];
+          mtile_compute<N, OP, false, BG, false, true>(C, G, su, sw, wq * WE * N, ehw, minv_a, minv_p, mnu, kq, bget,
+                                                       du_, dw_, r);
+        if (kq == 3 && hm * 8 + rr < W::CW) hrow[s * W::CW + wq] = (!periodic && eh < 0) ? 0.0 : r[NT - 1][1];
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&halo[s]);
@@ -1411,7 +1483,7 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
     const int sh = (int)((bofs + (e0 - 1) * N) & 1);
     const bool edge = !periodic && (tl == 0 || tl == tiles_per_ring - 1);
     const double* su = stage_buf + (s * NIN + 0) * SA + sh;
-    const double* sw = stage_buf + (s * NIN + 1) * SA + sh;
+    const auto sw = wsrc(s, sh);
     const int wel0 = warp * WE;
     const int wnel = min(WE, nel - wel0);
     double* wout = ostage + (it % OUTB) * W::OUT + warp * WE * N;   // this warp's node staging
@@ -1436,7 +1508,7 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
 #pragma unroll
           for (int q = 0; q < WMT; ++q) {
             const int le = ws_le<WMT, ILVW>(q, rr);
-            mtile_compute<N, OP, EDGE, decltype(bget), PRE>(C, G, su, sw, (wel0 + le + 1) * N, e0 + wel0 + le, minv_a,
+            mtile_compute<N, OP, EDGE, decltype(bget), PRE, false>(C, G, su, sw, (wel0 + le + 1) * N, e0 + wel0 + le, minv_a,
                                                             minv_p, mnu, kq, bget, fin_u, fin_w, rq[q]);
           }
         }
@@ -1537,6 +1609,16 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
           const int64_t ga = gw + k;
           if (EPI == EPI_STORE) {
             A.out[ga] = v;
+          } else if (EPI == EPI_ADJ) {
+            const double l = __dmul_rn(A.dt, v);  // l = dt * J^T(U) z   (adjoint.py:58-60)
+            if (A.out) A.out[ga] = l;
+            if (A.Y) {
+              // lam + l_0 + l_1 + ...                          (adjoint.py:61)
+              double acc = __ldg(A.base + ga);
+              for (int j = 0; j < A.epi.n; ++j)
+                acc = __dadd_rn(acc, A.epi.ptr[j] ? __ldg(A.epi.ptr[j] + ga) : l);
+              A.Y[ga] = acc;
+            }
           } else {  // EPI_RK: base + dt * combination (timeloop.py:114-127)
             if (A.out) A.out[ga] = v;
             double yv;
@@ -1579,22 +1661,23 @@ __global__ void __launch_bounds__(WsTile<N, OP>::THREADS, ws_minb<N, OP>())
 // Pipeline depth: enough stages that ~100 KB of slab loads can be in flight per
 // CTA (two CTAs per SM for n <= 16), since HBM at ~1.5 us loaded latency needs
 // >= 64 KB outstanding per SM (Little's law).
-template <int N, int OP>
+template <int N, int OP, int NZ = -1>
 constexpr int ws_stages() {
-  using W = WsTile<N, OP>;
-  constexpr int NIN = (OP == OP_RHS) ? 1 : 2;
+  using W = WsTile<N, OP, NZ>;
+  constexpr int NIN = W::NIN;
   // shared-memory budget that keeps ws_minb CTAs resident (227 KB per SM)
-  constexpr int mb = ws_minb<N, OP>();
+  constexpr int mb = ws_minb<N, OP, NZ>();
   constexpr int budget = (mb == 1 ? 180 : (mb == 2 ? 104 : (mb == 3 ? 72 : (mb == 4 ? 54 : 44)))) * 1024;
   constexpr int per = NIN * W::SLAB_ALLOC * 8;
-  constexpr int st = (budget - ws_outb<OP>() * W::OUT * 8 - (W::B_IN_SMEM ? 3 * W::NT * W::KC * 32 * 8 : 0)) / per;
+  constexpr int NMAT = (OP == OP_JACT) ? 3 : 2;
+  constexpr int st = (budget - ws_outb<OP>() * W::OUT * 8 - (W::B_IN_SMEM ? NMAT * W::NT * W::KC * 32 * 8 : 0)) / per;
   return st < 2 ? 2 : (st > 8 ? 8 : st);
 }
 
-template <int N, int OP, int STAGES>
+template <int N, int OP, int STAGES, int NZ = -1>
 constexpr size_t ws_smem_bytes() {
-  using W = WsTile<N, OP>;
-  constexpr int NIN = (OP == OP_RHS) ? 1 : 2;
+  using W = WsTile<N, OP, NZ>;
+  constexpr int NIN = W::NIN;
   constexpr int NMAT = (OP == OP_JACT) ? 3 : 2;
   return sizeof(double) * ((size_t)STAGES * NIN * W::SLAB_ALLOC + ws_outb<OP>() * W::OUT + STAGES * W::CW +
                            (W::B_IN_SMEM ? NMAT * W::NT * W::KC * 32 : 0)) +

@@ -104,25 +104,26 @@ static cudaError_t launch_mma(const PlanView& p, const Args& a, cudaStream_t s) 
 }
 
 
-template <int N, int OP, int EPI>
+template <int N, int OP, int EPI, int NZ = -1>
 static cudaError_t launch_ws(const PlanView& p, const Args& a, cudaStream_t s) {
   if constexpr ((N + 1) % 8 != 0) {
     return cudaErrorInvalidValue;
   } else {
-    constexpr int ST = ws_stages<N, OP>();
-    auto kern = apply_ws_kernel<N, OP, EPI, ST>;
-    constexpr size_t smem = ws_smem_bytes<N, OP, ST>();
+    using W = WsTile<N, OP, NZ>;
+    constexpr int ST = ws_stages<N, OP, NZ>();
+    auto kern = apply_ws_kernel<N, OP, EPI, ST, NZ>;
+    constexpr size_t smem = ws_smem_bytes<N, OP, ST, NZ>();
     static DevCache resident;
     int& max_resident = resident.here();
     if (max_resident == 0) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       int per_sm = 0;
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WsTile<N, OP>::THREADS, smem);
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, W::THREADS, smem);
       if (e != cudaSuccess) return e;
       max_resident = (per_sm > 0 ? per_sm : 1) * device_sms();
     }
-    const int64_t per_ring = (p.geo.E + WsTile<N, OP>::ELEMS - 1) / WsTile<N, OP>::ELEMS;
+    const int64_t per_ring = (p.geo.E + W::ELEMS - 1) / W::ELEMS;
     const int64_t total = per_ring * p.batch;
     if (total > 0x7fffffffLL) return cudaErrorInvalidValue;
     const int grid = (int)(total < max_resident ? total : max_resident);
@@ -130,7 +131,7 @@ static cudaError_t launch_ws(const PlanView& p, const Args& a, cudaStream_t s) {
     // previous kernel's drain; the producer's griddep_wait() orders the data path after it
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(WsTile<N, OP>::THREADS);
+    cfg.blockDim = dim3(W::THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -172,6 +173,14 @@ cudaError_t launch_apply(const PlanView& p, int kind, const Args& a, cudaStream_
         case 1: return launch_ws<N, OP_JAC, EPI_STORE>(p, a, s);
         case 2: return launch_ws<N, OP_JACT, EPI_STORE>(p, a, s);
         default: return launch_ws<N, OP_RHS, EPI_RK>(p, a, s);
+      }
+    }
+    // adjoint stage: z = b lam + up to two a_j l_j terms (RK4 needs one, Kutta-3 two)
+    if (kind == 4 && sem1d_path_override() == 0 && a.zin.n <= 2) {
+      switch (a.zin.n) {
+        case 0: return launch_ws<N, OP_JACT, EPI_ADJ, 0>(p, a, s);
+        case 1: return launch_ws<N, OP_JACT, EPI_ADJ, 1>(p, a, s);
+        default: return launch_ws<N, OP_JACT, EPI_ADJ, 2>(p, a, s);
       }
     }
     if (kind <= 3 && use_mma<N>(p) && sem1d_path_override() == 3) {
