@@ -632,7 +632,8 @@ def run_gpu_arm(args):
         dropin = {"value": 3 * ndof / (dms * 1e-3), "unit": "DOF/s", "ms_per_step": dms,
                   "h2d_bytes_per_step": 5 * 8 * ndof, "d2h_bytes_per_step": 3 * 8 * ndof,
                   "path": "SemOperator.apply_rhs / apply_jacobian / apply_jacobian_transpose on numpy "
-                          "arrays (what stock semopt code calls): pageable copies, serial"}
+                          "arrays (what stock semopt code calls): serial applies; numpy inputs stream through a "
+                          "ring of pinned chunks, results come back into pinned numpy arrays"}
         cfg3 = cfg3_ops(torch, dev)
     # BASELINE config 5 strong-scaled: at N > 1 rank 0 first times the same ring alone
     strong = None

@@ -1119,6 +1119,11 @@ __device__ __forceinline__ void mtile_compute(const Consts<N>& C, const Geo& G, 
 #ifndef WS_PRE_F
 #define WS_PRE_F 1
 #endif
+// round 2 (config 3, 64-element J / J^T tiles): 4 n-tiles per group for F and J^T
+// (47.27 -> 47.0 us, 67.0 -> 66.1 us), 2 for J (66.4 against 67.15 at 4)
+#ifndef WS_NTG_FT
+#define WS_NTG_FT 4
+#endif
 #ifndef WS_NTG
 #define WS_NTG 2
 #endif
@@ -1174,7 +1179,8 @@ __device__ __forceinline__ void mtile_compute_multi(const Consts<N>& C, const Ge
   }
   // NTG output n-tiles at a time: NTG x Q x (2 or 3) independent accumulator chains per warp
   // hide the DMMA -> DMMA latency of the k-chunk chains
-  constexpr int NTG = (NT % WS_NTG == 0) ? WS_NTG : 1;
+  constexpr int NTGW = (OP == OP_JAC) ? WS_NTG : WS_NTG_FT;
+  constexpr int NTG = (NT % NTGW == 0) ? NTGW : 1;
 #pragma unroll
   for (int nt0 = 0; nt0 < NT; nt0 += NTG) {
     double k[NTG][Q][2], p[NTG][Q][2], qq[NTG][Q][2];

@@ -101,6 +101,72 @@ def _stream_handle(device):
     return torch.cuda.current_stream(device).cuda_stream
 
 
+# numpy fields on the drop-in path (a semopt user's apply_rhs(u) with u a numpy array).
+# Pageable copies run at a few GB/s and the fresh result array page-faults on first touch,
+# so large fields move through pinned memory instead: inputs stream through a ring of
+# pinned chunks (the CPU copy of chunk k+1 overlaps the DMA of chunk k), results are read
+# back into pinned arrays from torch's caching host allocator (reused once the caller drops
+# them), handed to the caller as numpy views.
+_STAGE_MIN_BYTES = 1 << 20
+_STAGE_CHUNK = 1 << 21           # doubles per pinned chunk (16 MB)
+_STAGE_SLOTS = 3
+
+
+class _HostStaging:
+    def __init__(self):
+        self.bufs = None
+        self.events = [None] * _STAGE_SLOTS
+
+    def h2d(self, src, dst):
+        """dst (device) <- src (pageable CPU tensor), on dst's current stream."""
+        torch = _torch()
+        if self.bufs is None:
+            self.bufs = [torch.empty(_STAGE_CHUNK, dtype=torch.float64, pin_memory=True)
+                         for _ in range(_STAGE_SLOTS)]
+        s, d = src.reshape(-1), dst.reshape(-1)
+        stream = torch.cuda.current_stream(dst.device)
+        n = s.numel()
+        for k, off in enumerate(range(0, n, _STAGE_CHUNK)):
+            b = k % _STAGE_SLOTS
+            if self.events[b] is not None:
+                self.events[b].synchronize()          # the DMA out of this slot has drained
+            m = min(_STAGE_CHUNK, n - off)
+            buf = self.bufs[b][:m]
+            buf.copy_(s[off:off + m])
+            d[off:off + m].copy_(buf, non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            self.events[b] = ev
+
+
+_staging = None
+
+
+def host_to_device(x, device):
+    """A host field (numpy / CPU tensor) as a contiguous fp64 tensor on ``device``."""
+    global _staging
+    torch = _torch()
+    t = torch.as_tensor(x).contiguous()
+    if t.numel() * 8 < _STAGE_MIN_BYTES or t.dtype != torch.float64 or t.is_pinned():
+        return t.to(device, non_blocking=False)
+    if _staging is None:
+        _staging = _HostStaging()
+    out = torch.empty(t.shape, dtype=torch.float64, device=device)
+    _staging.h2d(t, out)
+    return out
+
+
+def device_to_host(t):
+    """A device result as a numpy array (pinned, read back in one DMA, for large fields)."""
+    torch = _torch()
+    if t.numel() * 8 < _STAGE_MIN_BYTES:
+        return t.cpu().numpy()
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+    h.copy_(t, non_blocking=True)
+    torch.cuda.current_stream(t.device).synchronize()
+    return h.numpy()
+
+
 class _Plan:
     """Owns one sem1d_plan* (C ABI)."""
 
@@ -199,7 +265,7 @@ class SemOperator(ComposedStages):
         if t.dtype != torch.float64:
             raise ValidationError(f"{name} must be float64, got {t.dtype}")
         if t.device != self.device:
-            t = t.to(self.device, non_blocking=False)
+            t = host_to_device(t, self.device) if t.device.type == "cpu" else t.to(self.device)
         return t.contiguous(), host
 
     def empty(self):
@@ -231,7 +297,7 @@ class SemOperator(ComposedStages):
 
     @staticmethod
     def _out(t, host):
-        return t.cpu().numpy() if host else t
+        return device_to_host(t) if host else t
 
     # -- raw launches (no validation, no sync): used by the engines -------------
 

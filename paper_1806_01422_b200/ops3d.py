@@ -20,7 +20,7 @@ import numpy as np
 from . import _lib
 from .errors import NumericFailure, ValidationError
 from .grid import Grid3D
-from .ops import BURGERS, ComposedStages, _stream_handle, _torch
+from .ops import BURGERS, ComposedStages, _stream_handle, _torch, device_to_host, host_to_device
 
 
 class _Plan3D:
@@ -100,7 +100,7 @@ class SemOperator3D(ComposedStages):
         if t.dtype != torch.float64:
             raise ValidationError(f"{name} must be float64, got {t.dtype}")
         if t.device != self.device:
-            t = t.to(self.device)
+            t = host_to_device(t, self.device) if t.device.type == "cpu" else t.to(self.device)
         return t.contiguous(), host
 
     def empty(self):
@@ -210,7 +210,7 @@ class SemOperator3D(ComposedStages):
         out = self.empty()
         launch(*ts, out)
         self.raise_for_flags((names[0], names[-1]))
-        return out.cpu().numpy() if host else out
+        return device_to_host(out) if host else out
 
     def apply_rhs(self, u):
         """f(u) = M^-1 gather(P_e(scatter(u))) (ops.py:232-236)."""

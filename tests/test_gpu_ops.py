@@ -292,3 +292,26 @@ def test_plan_runs_on_its_own_device(cuda):
     ud = torch.from_numpy(u).to(dev)
     out = op.apply_rhs(ud)
     assert out.device == dev and torch.cuda.current_device() == 0
+
+
+def test_numpy_fields_through_pinned_staging(cuda):
+    """Large numpy fields take the pinned-staging path (chunked H2D, pinned result arrays):
+    bitwise the same results as device tensors, fresh writable arrays per call, and the
+    same validation errors."""
+    op = _op(-1.0, 1.0, 1 << 20, 7, True, 0.01)          # 7.3M DOF: 59 MB, several chunks
+    u, v, w = R.seeded_fields(op.ndof, 11)
+    ud, vd, wd = (torch.from_numpy(a).cuda() for a in (u, v, w))
+    for host, dev in ((op.apply_rhs(u), op.apply_rhs(ud)),
+                      (op.apply_jacobian(u, v), op.apply_jacobian(ud, vd)),
+                      (op.apply_jacobian_transpose(u, w), op.apply_jacobian_transpose(ud, wd))):
+        assert isinstance(host, np.ndarray) and host.dtype == np.float64 and host.flags.writeable
+        assert np.array_equal(host, dev.cpu().numpy())
+    a, b = op.apply_rhs(u), op.apply_rhs(u)
+    assert a is not b and not np.shares_memory(a, b)
+    a[:] = 0.0
+    assert np.array_equal(b, op.apply_rhs(ud).cpu().numpy())
+    # a strided / float32 view goes through np.asarray like before
+    assert np.array_equal(op.apply_rhs(np.asfortranarray(u.astype(np.float32)).astype(np.float64)),
+                          op.apply_rhs(torch.from_numpy(u.astype(np.float32).astype(np.float64)).cuda()).cpu().numpy())
+    with pytest.raises(sb.ValidationError):
+        op.apply_rhs(u[:-1])

@@ -1,4 +1,4 @@
-"""F / J / J^T time vs ring size (N = 7): separates the fixed per-launch cost
+"""F / J / J^T time vs ring size (config 2, N = 7, or config 3, N = 31: size_sweep.py 3): separates the fixed per-launch cost
 (prologue, last-wave tail) from the steady-state bandwidth.  Also times a plain
 torch copy of the same bytes for the ceiling at each size."""
 import json
@@ -23,9 +23,11 @@ def timed(fn, reps=30):
     return 1e3 * s.elapsed_time(e) / reps
 
 
-def main():
-    for lg in (18, 19, 20, 21, 22, 23, 24):
-        c = dict(configs.CFG2, E=1 << lg)
+def main(cfg="2"):
+    base = {"2": configs.CFG2, "3": configs.CFG3}[cfg]
+    lgs = (18, 19, 20, 21, 22, 23, 24) if cfg == "2" else (15, 16, 17, 18, 19, 20, 21)
+    for lg in lgs:
+        c = dict(base, E=1 << lg)
         op = configs.cfg_operator(c, device="cuda:0")
         u, v, w = configs.operator_inputs(op.ndof, c["seed"])
         ud, vd, wd = (torch.from_numpy(a).cuda() for a in (u, v, w))
@@ -40,4 +42,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(*sys.argv[1:])
