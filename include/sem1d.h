@@ -67,7 +67,8 @@ int sem1d_version(void);
  *     kernel only, 3 = the CTA-synchronous tensor-core kernel (A/B reference). */
 int sem1d_set_kernel_path(int path);
 /* Tile-step kernels for A/B runs: 0 = auto (register-resident kernels for N = 7),
- * 1 = the shared-memory tile kernels for every degree. */
+ * 1 = the shared-memory tile kernels for every degree (and the shared-memory ensemble
+ * forward sweep at N = 15). */
 int sem1d_set_tile_variant(int variant);
 const char* sem1d_last_error(void);
 int sem1d_max_degree(void);

@@ -12,6 +12,7 @@
 #include "sem1d_ensemble.cuh"
 #include "sem1d_smallring.cuh"
 #include "sem1d_tilerf.cuh"
+#include "sem1d_ensrf.cuh"
 
 namespace sem1d {
 
@@ -278,6 +279,18 @@ cudaError_t launch_ens_forward(const PlanView& p, const EnsArgs& a, cudaStream_t
     const size_t smem = ens_smem_bytes<N>((int)p.geo.ndof);
     if (p.geo.periodic && p.geo.E % 8 == 0 && p.geo.E / 8 <= W * WMT && smem <= 220 * 1024 &&
         p.geo.E * (N + 1) > 1024) {
+      if constexpr (N == 15) {
+        // register-resident sweep (sem1d_ensrf.cuh): rings of 32..256 elements, 32 | E
+        if (ENS_RF && p.geo.E % 32 == 0 && sem1d_tile_variant() != 1) {
+          const size_t sm = EnsRf::smem((int)p.geo.ndof, a.tab.s == 3);
+          auto kr = a.tab.s == 4 ? ens_forward_rf_kernel<2> : a.tab.s == 3 ? ens_forward_rf_kernel<1>
+                                                                           : ens_forward_rf_kernel<0>;
+          cudaError_t e = cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+          if (e != cudaSuccess) return e;
+          kr<<<(unsigned)p.batch, EnsRf::THREADS, sm, s>>>(*static_cast<const Consts<N>*>(p.consts), p.geo, a);
+          return cudaGetLastError();
+        }
+      }
       const bool ilv = ENS_ILV && p.geo.E % (8 * WMT) == 0;
       auto kern = a.tab.s == 4 ? (ilv ? ens_forward_kernel<N, WMT, true, 2> : ens_forward_kernel<N, WMT, false, 2>)
                 : a.tab.s == 3 ? (ilv ? ens_forward_kernel<N, WMT, true, 1> : ens_forward_kernel<N, WMT, false, 1>)

@@ -125,3 +125,31 @@ def test_cfg4_full_scale_gradients_vs_oracle(cuda):
         assert rel_err(g[b], g_ref) <= 1e-9
     del prob, J, g
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("scheme", ["rk4", "rk3", "euler"])
+@pytest.mark.parametrize("E", [256, 32, 96, 160])
+def test_register_resident_ensemble_forward_bitwise(cuda, scheme, E):
+    """N = 15 rings with 32 | E run the register-resident forward sweep (sem1d_ensrf.cuh):
+    trajectory, final state and flag words bit-identical to the shared-memory kernel
+    (sem1d_set_tile_variant(1)) -- same arithmetic and association."""
+    from paper_1806_01422_b200 import _lib
+    B, steps, dt = 7, 30, 5e-5
+    grid = grid_1d(0.0, 20.0, E, 15)
+    op = sb.SemOperator(grid, sb.PdeCoefficients(0.01), device="cuda:0", batch=B)
+    u0 = configs.fourier_fields(grid, B, 4, seed=E)
+    u0[3] *= 1e140                                  # one failing problem: same flag words
+    ts = sb.TsConfig(scheme=scheme, t0=0.0, t_end=steps * dt, dt=dt)
+    lib = _lib.load()
+    runs = []
+    for variant in (0, 1):
+        assert lib.sem1d_set_tile_variant(variant) == 0
+        try:
+            runs.append(timeloop.integrate_ensemble(op, u0, ts))
+        finally:
+            lib.sem1d_set_tile_variant(0)
+    a, b = runs
+    ok = [i for i in range(B) if i != 3]            # (NaN payloads may differ: compare finite runs)
+    assert torch.equal(a.trajectory[:, ok], b.trajectory[:, ok]) and torch.equal(a.u_final[ok], b.u_final[ok])
+    assert a.stats["failed"] == b.stats["failed"] == [3]
+    assert not bool(torch.isfinite(a.u_final[3]).all()) and not bool(torch.isfinite(b.u_final[3]).all())
