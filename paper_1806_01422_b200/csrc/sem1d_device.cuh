@@ -1610,38 +1610,80 @@ __global__ void __launch_bounds__(WsTile<N, OP, NZ>::THREADS, ws_minb<N, OP, NZ>
           bulk_commit();
         }
       } else {
-        for (int k = lane; k < cnt_w; k += 32) {
-          const double v = wout[k];
-          const int64_t ga = gw + k;
+        // four nodes per lane at a time: every global read of a chunk (base, terms) is in
+        // flight before its arithmetic, instead of one dependent round trip per node (the
+        // stores of a chunk may alias the next chunk's inputs, so chunks stay ordered)
+        constexpr int U4 = 4;
+        for (int kb = lane; kb < cnt_w; kb += 32 * U4) {
+          double v[U4], x[U4];
+          bool live[U4];
+#pragma unroll
+          for (int r = 0; r < U4; ++r) {
+            live[r] = kb + 32 * r < cnt_w;
+            v[r] = live[r] ? wout[kb + 32 * r] : 0.0;
+          }
           if (EPI == EPI_STORE) {
-            A.out[ga] = v;
+#pragma unroll
+            for (int r = 0; r < U4; ++r)
+              if (live[r]) A.out[gw + kb + 32 * r] = v[r];
           } else if (EPI == EPI_ADJ) {
-            const double l = __dmul_rn(A.dt, v);  // l = dt * J^T(U) z   (adjoint.py:58-60)
-            if (A.out) A.out[ga] = l;
+            double l[U4];
+#pragma unroll
+            for (int r = 0; r < U4; ++r) l[r] = __dmul_rn(A.dt, v[r]);  // l = dt * J^T(U) z (adjoint.py:58-60)
             if (A.Y) {
               // lam + l_0 + l_1 + ...                          (adjoint.py:61)
-              double acc = __ldg(A.base + ga);
-              for (int j = 0; j < A.epi.n; ++j)
-                acc = __dadd_rn(acc, A.epi.ptr[j] ? __ldg(A.epi.ptr[j] + ga) : l);
-              A.Y[ga] = acc;
+#pragma unroll
+              for (int r = 0; r < U4; ++r) x[r] = live[r] ? __ldg(A.base + gw + kb + 32 * r) : 0.0;
+              for (int j = 0; j < A.epi.n; ++j) {
+                const double* pj = A.epi.ptr[j];
+                double t[U4];
+#pragma unroll
+                for (int r = 0; r < U4; ++r) t[r] = (pj && live[r]) ? __ldg(pj + gw + kb + 32 * r) : l[r];
+#pragma unroll
+                for (int r = 0; r < U4; ++r) x[r] = __dadd_rn(x[r], t[r]);
+              }
+            }
+#pragma unroll
+            for (int r = 0; r < U4; ++r) {
+              if (!live[r]) continue;
+              if (A.out) A.out[gw + kb + 32 * r] = l[r];
+              if (A.Y) A.Y[gw + kb + 32 * r] = x[r];
             }
           } else {  // EPI_RK: base + dt * combination (timeloop.py:114-127)
-            if (A.out) A.out[ga] = v;
-            double yv;
+            double bv[U4];
+#pragma unroll
+            for (int r = 0; r < U4; ++r) bv[r] = live[r] ? __ldg(A.base + gw + kb + 32 * r) : 0.0;
             if (A.epi.n == 1) {
-              const double kk = A.epi.ptr[0] ? __ldg(A.epi.ptr[0] + ga) : v;
-              yv = __dadd_rn(__ldg(A.base + ga), __dmul_rn(__dmul_rn(A.dt, A.epi.coef[0]), kk));
+              const double* p0 = A.epi.ptr[0];
+#pragma unroll
+              for (int r = 0; r < U4; ++r) x[r] = (p0 && live[r]) ? __ldg(p0 + gw + kb + 32 * r) : v[r];
+              const double c = __dmul_rn(A.dt, A.epi.coef[0]);
+#pragma unroll
+              for (int r = 0; r < U4; ++r) x[r] = __dadd_rn(bv[r], __dmul_rn(c, x[r]));
             } else {
-              double sacc = 0.0;
+#pragma unroll
+              for (int r = 0; r < U4; ++r) x[r] = 0.0;
               for (int j = 0; j < A.epi.n; ++j) {
-                const double kk = A.epi.ptr[j] ? __ldg(A.epi.ptr[j] + ga) : v;
-                const double term = __dmul_rn(A.epi.coef[j], kk);
-                sacc = (j == 0) ? term : __dadd_rn(sacc, term);
+                const double* pj = A.epi.ptr[j];
+                double t[U4];
+#pragma unroll
+                for (int r = 0; r < U4; ++r) t[r] = (pj && live[r]) ? __ldg(pj + gw + kb + 32 * r) : v[r];
+#pragma unroll
+                for (int r = 0; r < U4; ++r) {
+                  const double term = __dmul_rn(A.epi.coef[j], t[r]);
+                  x[r] = (j == 0) ? term : __dadd_rn(x[r], term);
+                }
               }
-              yv = __dadd_rn(__ldg(A.base + ga), __dmul_rn(A.dt, sacc));
+#pragma unroll
+              for (int r = 0; r < U4; ++r) x[r] = __dadd_rn(bv[r], __dmul_rn(A.dt, x[r]));
             }
-            if (A.check) bad_y |= nonfinite(yv);
-            A.Y[ga] = yv;
+#pragma unroll
+            for (int r = 0; r < U4; ++r) {
+              if (!live[r]) continue;
+              if (A.out) A.out[gw + kb + 32 * r] = v[r];
+              if (A.check) bad_y |= nonfinite(x[r]);
+              A.Y[gw + kb + 32 * r] = x[r];
+            }
           }
         }
         __syncwarp();
