@@ -375,8 +375,9 @@ int sem1d_set_kernel_path(int path) {
 const char* sem1d_last_error(void) { return g_err.c_str(); }
 
 int sem1d_set_tile_variant(int variant) {
-  if (variant < 0 || variant > 2)
-    return fail(SEM1D_EINVAL, "sem1d_set_tile_variant: 0 (auto), 1 (shared-memory tiles), 2 (N = 7 forward at 128-element tiles)");
+  if (variant < 0 || variant > 3)
+    return fail(SEM1D_EINVAL, "sem1d_set_tile_variant: 0 (auto), 1 (shared-memory tiles), 2 (N = 7 forward at "
+                              "128-element tiles), 3 (N = 7 forward at 192-element tiles)");
   g_tile_variant = variant;
   return SEM1D_OK;
 }

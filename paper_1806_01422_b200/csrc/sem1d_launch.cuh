@@ -335,7 +335,10 @@ cudaError_t launch_tile_one(const PlanView& p, const TileStepArgs& a, int thread
   return cudaLaunchKernelEx(&cfg, KERN, *static_cast<const Consts<N>*>(p.consts), p.geo, a);
 }
 
-// register-resident N = 7 forward step (sem1d_tilerf.cuh)
+// register-resident N = 7 forward step (sem1d_tilerf.cuh); variant 3: 192-element tiles
+#ifndef TILE_RF3_MINB
+#define TILE_RF3_MINB 3
+#endif
 template <int SCH, int WMT, int MINB>
 cudaError_t launch_tile_rf(const PlanView& p, const TileStepArgs& a, cudaStream_t s) {
   constexpr size_t sm = RfCfg<WMT>::smem;
@@ -360,7 +363,7 @@ int tile_elems(int kind, bool ld) {
   if constexpr (N == 7) {
     const int var = sem1d_tile_variant();
     if (var != 1) {
-      if (kind == 0) return var == 2 ? RfCfg<2>::TE : RfCfg<4>::TE;
+      if (kind == 0) return var == 2 ? RfCfg<2>::TE : (var == 3 ? RfCfg<3>::TE : RfCfg<4>::TE);
       if (ld) return var == 2 ? RfAdjCfg<2>::TE : RfAdjCfg<3>::TE;
       return var == 2 ? RfAdjCfg<4>::TE : RfAdjCfg<3>::TE;
     }
@@ -390,6 +393,7 @@ cudaError_t launch_tile_sch(const PlanView& p, int kind, const TileStepArgs& a, 
     const int var = sem1d_tile_variant();
     if (kind == 0 && var != 1) {
       if (var == 2) return launch_tile_rf<SCH, 2, 3>(p, a, s);
+      if (var == 3) return launch_tile_rf<SCH, 3, TILE_RF3_MINB>(p, a, s);
       return launch_tile_rf<SCH, 4, 2>(p, a, s);
     }
     if (kind == 1 && var != 1) {
