@@ -15,6 +15,8 @@ There is no CPU fallback: without the library or a GPU the constructor raises.
 
 from __future__ import annotations
 
+import threading
+
 import numpy as np
 
 from . import _lib
@@ -116,9 +118,14 @@ class _HostStaging:
     def __init__(self):
         self.bufs = None
         self.events = [None] * _STAGE_SLOTS
+        self.lock = threading.Lock()      # one ring per process; callers may be concurrent
 
     def h2d(self, src, dst):
         """dst (device) <- src (pageable CPU tensor), on dst's current stream."""
+        with self.lock:
+            self._h2d(src, dst)
+
+    def _h2d(self, src, dst):
         torch = _torch()
         if self.bufs is None:
             self.bufs = [torch.empty(_STAGE_CHUNK, dtype=torch.float64, pin_memory=True)
@@ -139,18 +146,15 @@ class _HostStaging:
             self.events[b] = ev
 
 
-_staging = None
+_staging = _HostStaging()
 
 
 def host_to_device(x, device):
     """A host field (numpy / CPU tensor) as a contiguous fp64 tensor on ``device``."""
-    global _staging
     torch = _torch()
     t = torch.as_tensor(x).contiguous()
     if t.numel() * 8 < _STAGE_MIN_BYTES or t.dtype != torch.float64 or t.is_pinned():
         return t.to(device, non_blocking=False)
-    if _staging is None:
-        _staging = _HostStaging()
     out = torch.empty(t.shape, dtype=torch.float64, device=device)
     _staging.h2d(t, out)
     return out

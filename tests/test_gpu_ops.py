@@ -315,3 +315,28 @@ def test_numpy_fields_through_pinned_staging(cuda):
                           op.apply_rhs(torch.from_numpy(u.astype(np.float32).astype(np.float64)).cuda()).cpu().numpy())
     with pytest.raises(sb.ValidationError):
         op.apply_rhs(u[:-1])
+
+
+def test_numpy_staging_concurrent_callers(cuda):
+    """The pinned staging ring is shared by the process: concurrent drop-in callers
+    (ops.py:86-88 allows concurrent calls) still get their own inputs' results."""
+    import threading
+    op = _op(-1.0, 1.0, 1 << 18, 7, True, 0.01)
+    fields = [R.seeded_fields(op.ndof, s)[0] for s in range(4)]
+    want = [op.apply_rhs(torch.from_numpy(f).cuda()).cpu().numpy() for f in fields]
+    got, errs = [None] * 4, []
+
+    def run(i):
+        try:
+            for _ in range(3):
+                got[i] = op.apply_rhs(fields[i])
+        except Exception as e:   # pragma: no cover - surfaced below
+            errs.append(e)
+    ts = [threading.Thread(target=run, args=(i,)) for i in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs
+    for i in range(4):
+        assert np.array_equal(got[i], want[i]), i
