@@ -325,62 +325,74 @@ __global__ void __launch_bounds__(128) elem3d_mma_kernel(const Geo3 G, const dou
   if (bad_u || bad_w)
     atomicOr(flag, (bad_u ? SEM1D_FLAG_STATE_NONFINITE : 0) | (bad_w ? SEM1D_FLAG_INPUT2_NONFINITE : 0));
   __syncthreads();
+  // Phases unrolled (compile-time axis: every shared-memory offset is a per-thread base plus
+  // an immediate).  The pencil's transverse weight t scales the A fragment and -nu rides on
+  // the K fragment, so an output is one DFMA (F) instead of four multiplies and a subtract:
+  //   F:   K'(t u_i) - u_ax D(t u_i)                 (K' = -nu K)
+  //   J:   K'(t w_i) - w_ax D(t u_i) - u_ax D(t w_i)
+  //   J^T: K'(t z_i) - D^T(t u_ax z_i) [- sum_j z_j D(t u_j) on the axis ax == ci]
+  // (the same terms and order as elem3d_kernel, rounded differently: 1e-13 apart)
+  double bKn[3][2];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int kc = 0; kc < 2; ++kc) bKn[a][kc] = __dmul_rn(G.mnu, bK[a][kc]);
+#pragma unroll
   for (int ci = 0; ci < 3; ++ci) {
     const double* Ui = sU + ci * B;
     const double* Wi = sW + ci * B;
+#pragma unroll
     for (int ax = 0; ax < 3; ++ax) {
 #pragma unroll
       for (int tt = 0; tt < 2; ++tt) {
         const int pt = 2 * warp + tt;                 // pencil tile: pencils (a = pt, b = 0..7)
+        // offset of position p along the axis of the lane's pencil (pt, r)
+        const int ob = ax == 0 ? pt * L::SJ + r : (ax == 1 ? pt * L::SI + r : pt * L::SI + r * L::SJ);
+        const int st = ax == 0 ? L::SI : (ax == 1 ? L::SJ : 1);
         const double t = tw[ax][tt];
         double xu[2], xw[2];
 #pragma unroll
         for (int kc = 0; kc < 2; ++kc) {
-          const int o = off<N>(ax, pt, r, 4 * kc + kq);
-          xu[kc] = Ui[o];
-          if (OP != OP3_RHS) xw[kc] = Wi[o];
+          const int o = ob + (4 * kc + kq) * st;
+          xu[kc] = __dmul_rn(t, Ui[o]);
+          if (OP != OP3_RHS) xw[kc] = __dmul_rn(t, Wi[o]);
         }
-        // contribution of this axis at the lane's two output nodes (i = 2kq + h):
-        //   F:   -nu K x_i - u_ax (D u_i)            J: -nu K w_i - w_ax (D u_i) - u_ax (D w_i)
-        //   J^T: -nu K z_i - D^T(u_ax z_i) [- sum_j z_j (D u_j) on the axis ax == ci]
         double c[2];
         if (OP == OP3_RHS) {
           double k0 = 0.0, k1 = 0.0, d0 = 0.0, d1 = 0.0;
 #pragma unroll
           for (int kc = 0; kc < 2; ++kc) {
-            dmma8(k0, k1, xu[kc], bK[ax][kc]);
+            dmma8(k0, k1, xu[kc], bKn[ax][kc]);
             dmma8(d0, d1, xu[kc], bD[kc]);
           }
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int o = off<N>(ax, pt, r, 2 * kq + h);
-            c[h] = __dsub_rn(__dmul_rn(__dmul_rn(h ? k1 : k0, t), G.mnu),
-                             __dmul_rn(sU[ax * B + o], __dmul_rn(h ? d1 : d0, t)));
+            const int o = ob + (2 * kq + h) * st;
+            c[h] = __fma_rn(-sU[ax * B + o], h ? d1 : d0, h ? k1 : k0);
           }
         } else if (OP == OP3_JAC) {
           double k0 = 0.0, k1 = 0.0, p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
 #pragma unroll
           for (int kc = 0; kc < 2; ++kc) {
-            dmma8(k0, k1, xw[kc], bK[ax][kc]);
+            dmma8(k0, k1, xw[kc], bKn[ax][kc]);
             dmma8(p0, p1, xu[kc], bD[kc]);
             dmma8(q0, q1, xw[kc], bD[kc]);
           }
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int o = off<N>(ax, pt, r, 2 * kq + h);
-            double v = __dmul_rn(__dmul_rn(h ? k1 : k0, t), G.mnu);
-            v = __dsub_rn(v, __dmul_rn(sW[ax * B + o], __dmul_rn(h ? p1 : p0, t)));
-            c[h] = __dsub_rn(v, __dmul_rn(sU[ax * B + o], __dmul_rn(h ? q1 : q0, t)));
+            const int o = ob + (2 * kq + h) * st;
+            const double v = __fma_rn(-sW[ax * B + o], h ? p1 : p0, h ? k1 : k0);
+            c[h] = __fma_rn(-sU[ax * B + o], h ? q1 : q0, v);
           }
         } else {
           const double* Ua = sU + ax * B;
           double xt[2];
 #pragma unroll
-          for (int kc = 0; kc < 2; ++kc) xt[kc] = __dmul_rn(Ua[off<N>(ax, pt, r, 4 * kc + kq)], xw[kc]);
+          for (int kc = 0; kc < 2; ++kc) xt[kc] = __dmul_rn(Ua[ob + (4 * kc + kq) * st], xw[kc]);
           double k0 = 0.0, k1 = 0.0, t0 = 0.0, t1 = 0.0;
 #pragma unroll
           for (int kc = 0; kc < 2; ++kc) {
-            dmma8(k0, k1, xw[kc], bK[ax][kc]);
+            dmma8(k0, k1, xw[kc], bKn[ax][kc]);
             dmma8(t0, t1, xt[kc], bDt[kc]);
           }
           double ej[3][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
@@ -388,25 +400,25 @@ __global__ void __launch_bounds__(128) elem3d_mma_kernel(const Geo3 G, const dou
           if (own) {
 #pragma unroll
             for (int kc = 0; kc < 2; ++kc) {
-              const int o = off<N>(ax, pt, r, 4 * kc + kq);
+              const int o = ob + (4 * kc + kq) * st;
 #pragma unroll
-              for (int jj = 0; jj < 3; ++jj) dmma8(ej[jj][0], ej[jj][1], sU[jj * B + o], bD[kc]);
+              for (int jj = 0; jj < 3; ++jj) dmma8(ej[jj][0], ej[jj][1], __dmul_rn(t, sU[jj * B + o]), bD[kc]);
             }
           }
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            const int o = off<N>(ax, pt, r, 2 * kq + h);
-            double v = __dsub_rn(__dmul_rn(__dmul_rn(h ? k1 : k0, t), G.mnu), __dmul_rn(h ? t1 : t0, t));
+            const int o = ob + (2 * kq + h) * st;
+            double v = __dsub_rn(h ? k1 : k0, h ? t1 : t0);
             if (own) {
 #pragma unroll
-              for (int jj = 0; jj < 3; ++jj) v = __dsub_rn(v, __dmul_rn(sW[jj * B + o], __dmul_rn(ej[jj][h], t)));
+              for (int jj = 0; jj < 3; ++jj) v = __fma_rn(-sW[jj * B + o], ej[jj][h], v);
             }
             c[h] = v;
           }
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          const int o = off<N>(ax, pt, r, 2 * kq + h);
+          const int o = ob + (2 * kq + h) * st;
           ACC[o] = (ax == 0) ? c[h] : __dadd_rn(ACC[o], c[h]);
         }
       }
