@@ -1614,6 +1614,9 @@ __global__ void __launch_bounds__(WsTile<N, OP, NZ>::THREADS, ws_minb<N, OP, NZ>
         // flight before its arithmetic, instead of one dependent round trip per node (the
         // stores of a chunk may alias the next chunk's inputs, so chunks stay ordered)
         constexpr int U4 = 4;
+        if constexpr (EPI == EPI_STORE) {            // unaligned warp range of a plain apply
+          for (int k = lane; k < cnt_w; k += 32) A.out[gw + k] = wout[k];
+        } else
         for (int kb = lane; kb < cnt_w; kb += 32 * U4) {
           double v[U4], x[U4];
           bool live[U4];
