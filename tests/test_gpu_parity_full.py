@@ -1,7 +1,8 @@
 """Parity at the BASELINE's full sizes and on smooth inputs.
 
-* Whole-field comparisons: config 2 (E = 2^22, N = 7, 29.4M DOF) and config 3 (E = 2^18,
-  N = 31) F, J v and J^T w against the oracle on every node, <= 1e-12 max-abs relative.
+* Whole-field comparisons: config 2 (E = 2^22, N = 7, 29.4M DOF), config 3 (E = 2^18,
+  N = 31) and config 5's ring (E = 2^25, N = 7, 235M DOF) F, J v and J^T w against the oracle
+  on every node, <= 1e-12 max-abs relative.
 * Smooth inputs: the kernels fold -nu M^-1 / dt M^-1 into their tensor-core operand tables
   and (in the sweep kernels) regroup the stage arithmetic, so each product rounds differently
   from the reference.  On rough inputs that is invisible (1e-16), on smooth inputs the terms
@@ -51,6 +52,15 @@ def test_cfg2_whole_field_vs_oracle(cuda):
 def test_cfg3_whole_field_vs_oracle(cuda):
     """Config 3 at full size (E = 2^18, N = 31, dense 32 x 32 contractions on DMMA)."""
     c = dict(configs.CFG3)
+    errs = _full_field_case(c)
+    assert max(errs.values()) <= TOL, errs
+
+
+def test_cfg5_whole_field_vs_oracle(cuda):
+    """Config 5's ring at full size (E = 2^25, N = 7, h = 1/64, nu = 1e-3: 234,881,024 nodes),
+    every node of F, J v and J^T w on the BASELINE's rough inputs."""
+    c5 = configs.CFG5
+    c = dict(xa=0.0, xb=c5["E"] * c5["h"], E=c5["E"], N=c5["N"], nu=c5["nu"], seed=c5["seed"])
     errs = _full_field_case(c)
     assert max(errs.values()) <= TOL, errs
 
