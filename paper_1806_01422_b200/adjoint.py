@@ -296,11 +296,13 @@ def gradient(op, cfg, fwd, schedule, u_ref):
     return j, sweep(op, cfg, fwd, schedule, lam)
 
 
-def ensemble_sweep(op, cfg, fwd, lam_terminal):
+def ensemble_sweep(op, cfg, fwd, lam_terminal, defer_checks=False):
     """Backward sweep of a batch of rings over a trajectory from
     ``timeloop.integrate_ensemble`` -- one CTA per ring, every step in shared memory
     (sem1d_ens_adjoint).  Same recurrence as :func:`sweep` with store-all; the stage
-    adjoints are accumulated as lam + (l_s + ... + l_1) instead of ((lam + l_1) + ...)."""
+    adjoints are accumulated as lam + (l_s + ... + l_1) instead of ((lam + l_1) + ...).
+    ``defer_checks``: returns (gradient, per-problem flag words on the device) without a
+    host sync; the caller raises NumericFailure("cotangent ...") for a nonzero word."""
     import torch
     traj = getattr(fwd, "trajectory", None)
     if traj is None:
@@ -310,10 +312,12 @@ def ensemble_sweep(op, cfg, fwd, lam_terminal):
     flags = torch.zeros(op.batch, dtype=torch.int32, device=op.device)
     op.launch_ens_adjoint(traj, lam_in.contiguous(), lam_out, fwd.dts_device, fwd.n_steps,
                           cfg.scheme, flags)
-    if int(flags.max()):
+    if not defer_checks and int(flags.max()):
         raise NumericFailure("cotangent contains NaN/Inf")
     s = len(TABLEAUX[cfg.scheme][1])
     op.counters["rhs"] += (s - 1) * fwd.n_steps
     op.counters["jact"] += s * fwd.n_steps
     op.last_sweep_stats = {"newton_iters": 0, "gmres_iters": 0, "recomputed": 0}
+    if defer_checks:
+        return lam_out, flags
     return lam_out.cpu().numpy() if host else lam_out

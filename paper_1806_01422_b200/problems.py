@@ -81,18 +81,15 @@ class AssimilationProblem:
             fwd = timeloop.integrate(self.op, u0_dev, self.ts, store_steps=None)
             return self._finish(fwd, self.schedule_for(fwd.n_steps), u0, host)
         m = timeloop.count_steps(self.ts)
-        sched = self.schedule_for(m)
         fwd = None
         if (self.use_ensemble and self.checkpoint_slots is None and self.ts.scheme != "cn"
                 and hasattr(self.op, "launch_ens_forward")
                 and timeloop.ring_resident_supported(self.op)):
             # the ring fits one CTA: whole forward sweep in one launch, trajectory in HBM
-            fwd = timeloop.integrate_ensemble(self.op, u0_dev, self.ts)
-            if fwd.stats["failed"]:
-                if self.op.batch > 1:
-                    from .errors import StepFailure
-                    raise StepFailure(f"non-finite state in problems {fwd.stats['failed'][:8]}")
-                fwd = None   # re-run stepwise: exact reference retry / exception semantics
+            out = self._evaluate_ring_resident(u0_dev, host)
+            if out is not None:
+                return out
+        sched = self.schedule_for(m)
         if fwd is None:
             keep = False
             if self.checkpoint_slots is None and timeloop.stages_supported(self.op, self.ts):
@@ -108,6 +105,50 @@ class AssimilationProblem:
         if fwd.n_steps != m:  # a StepFailure retry changed the time grid
             sched = self.schedule_for(fwd.n_steps)
         return self._finish(fwd, sched, u0, host)
+
+    def _evaluate_ring_resident(self, u0_dev, host):
+        """Forward sweep, terminal seed and backward sweep of ring-resident problems launched
+        back to back; every check of the gradient (initial state, per-problem step flags,
+        cotangent flags) comes back with J in ONE device->host transfer.  Raises and counts
+        exactly as the checked sequence integrate_ensemble / terminal_condition /
+        ensemble_sweep would; returns None when a batch-1 forward failed, so that evaluate
+        re-runs it stepwise with the reference's retry semantics."""
+        import torch
+        from .errors import NumericFailure, StepFailure
+        op, B = self.op, self.op.batch
+        before = dict(op.counters)
+        fwd = timeloop.integrate_ensemble(op, u0_dev, self.ts, defer_checks=True)
+        after_fwd = dict(op.counters)
+        lam = op.empty()
+        J = torch.empty(B, dtype=torch.float64, device=op.device)
+        op.launch_terminal(fwd.u_final, self.target(), lam, J)
+        g, aflags = adjoint.ensemble_sweep(op, self.ts, fwd, lam, defer_checks=True)
+        f64 = torch.float64
+        parts = [fwd.initial_ok_device.to(f64).reshape(1), fwd.flags_device.to(f64), aflags.to(f64), J]
+        if host:
+            parts.append(g.reshape(-1))
+        pk = torch.cat(parts).cpu().numpy()          # the one host sync of this gradient
+        if pk[0] == 0.0:
+            op.counters.clear()
+            op.counters.update(before)
+            raise NumericFailure("initial state contains NaN/Inf")
+        failed = [int(i) for i in np.nonzero(pk[1:1 + B])[0]]
+        fwd.stats["failed"] = failed
+        if failed:
+            op.counters.clear()
+            op.counters.update(after_fwd)           # the forward ran, the sweep did not
+            if B > 1:
+                raise StepFailure(f"non-finite state in problems {failed[:8]}")
+            return None
+        if np.any(pk[1 + B:1 + 2 * B] != 0.0):
+            op.counters.clear()
+            op.counters.update(after_fwd)
+            raise NumericFailure("cotangent contains NaN/Inf")
+        self.last_forward = fwd
+        j = float(pk[1 + 2 * B]) if B == 1 else J
+        if host:
+            g = pk[1 + 3 * B:].reshape(tuple(g.shape)).copy()
+        return j, g
 
     def _finish(self, fwd, sched, u0, host):
         """terminal seed + backward sweep (problems.py:196-199)."""

@@ -534,19 +534,40 @@ def ring_resident_supported(op):
     return bool(op.grid.periodic and n % 8 == 0 and E % 8 == 0 and E <= 256)
 
 
-def integrate_ensemble(op, u0, cfg, store_trajectory=True):
+def _dts_device(op, cfg):
+    """The fixed-dt sequence on the host and on the device, cached per operator and
+    time grid (the ring-resident sweeps of small problems are latency-bound)."""
+    import torch
+    key = (cfg.t0, cfg.t_end, cfg.dt, cfg.max_steps)
+    cache = op.__dict__.setdefault("_dts_cache", {})
+    hit = cache.get(key)
+    if hit is None:
+        dts = fixed_step_sizes(cfg)
+        hit = (dts, torch.tensor(dts, dtype=torch.float64, device=op.device))
+        if len(cache) > 16:
+            cache.clear()
+        cache[key] = hit
+    return hit
+
+
+def integrate_ensemble(op, u0, cfg, store_trajectory=True, defer_checks=False):
     """Forward sweep of a batch of independent rings, one CTA per ring, every step in
     shared memory (sem1d_ens_forward).  Same dt sequence and step arithmetic as
     :func:`integrate`; a problem whose state goes non-finite is reported in
-    ``stats["failed"]`` (the batched sweep does not retry with halved dt)."""
+    ``stats["failed"]`` (the batched sweep does not retry with halved dt).
+    ``defer_checks``: no host sync here -- the result carries ``flags_device`` and
+    ``initial_ok_device`` and ``stats["failed"]`` is None until the caller reads them
+    (``AssimilationProblem.evaluate`` reads every check of a gradient in one transfer)."""
     import torch
     _require_explicit(cfg)
     u, _ = op.field(u0, "initial state")
-    if not op._isfinite_all(u):
+    init_ok = None
+    if defer_checks:
+        init_ok = torch.isfinite(u).all()
+    elif not op._isfinite_all(u):
         raise NumericFailure("initial state contains NaN/Inf")
-    dts = fixed_step_sizes(cfg)
+    dts, dts_dev = _dts_device(op, cfg)
     m = len(dts)
-    dts_dev = torch.tensor(dts, dtype=torch.float64, device=op.device)
     traj = None
     if store_trajectory:
         traj = torch.empty((m + 1,) + tuple(u.shape), dtype=torch.float64, device=op.device)
@@ -554,8 +575,10 @@ def integrate_ensemble(op, u0, cfg, store_trajectory=True):
     flags = torch.zeros(op.batch, dtype=torch.int32, device=op.device)
     op.launch_ens_forward(u.contiguous(), traj, u_final, dts_dev, m, cfg.scheme, flags)
     op.counters["rhs"] += len(TABLEAUX[cfg.scheme][1]) * m
-    fl = flags.cpu()
-    failed = [int(i) for i in torch.nonzero(fl).flatten()]
+    failed = None
+    if not defer_checks:
+        fl = flags.cpu()
+        failed = [int(i) for i in torch.nonzero(fl).flatten()]
     snapshots = {n: traj[n] for n in range(m + 1)} if traj is not None else {0: u.clone()}
     ts = np.concatenate([[cfg.t0], cfg.t0 + np.cumsum(dts)]) if m else np.asarray([cfg.t0])
     if m:
@@ -565,4 +588,6 @@ def integrate_ensemble(op, u0, cfg, store_trajectory=True):
                         stats=stats)
     res.trajectory = traj          # (m+1, batch, ndof) step-major, for ensemble_sweep
     res.dts_device = dts_dev
+    res.flags_device = flags
+    res.initial_ok_device = init_ok
     return res
