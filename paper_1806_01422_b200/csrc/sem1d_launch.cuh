@@ -228,20 +228,22 @@ static cudaError_t launch_small(const PlanView& p, const EnsArgs* fa, const EnsA
   SmallGeo sg;
   sg.E = (int)p.geo.E; sg.N = N; sg.ndof = (int)p.geo.ndof; sg.periodic = p.geo.periodic;
   const Consts<N>& C = *static_cast<const Consts<N>*>(p.consts);
+  const int ts = fa ? fa->tab.s : aa->tab.s;     // compile-time tableau (TabC) per scheme
+  if (ts != 1 && ts != 3 && ts != 4) return cudaErrorInvalidValue;
   if (fa) {
     const size_t smem = small_fwd_smem(N, sg.ndof, sg.E);
     if (smem > 220 * 1024) return cudaErrorNotSupported;
-    cudaError_t e = cudaFuncSetAttribute(small_forward_kernel<N>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto kern = ts == 4 ? small_forward_kernel<N, 2> : (ts == 3 ? small_forward_kernel<N, 1> : small_forward_kernel<N, 0>);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    small_forward_kernel<N><<<(unsigned)p.batch, (unsigned)threads, smem, s>>>(C, sg, *fa);
+    kern<<<(unsigned)p.batch, (unsigned)threads, smem, s>>>(C, sg, *fa);
   } else {
     const size_t smem = small_adj_smem(N, sg.ndof, sg.E);
     if (smem > 220 * 1024) return cudaErrorNotSupported;
-    cudaError_t e = cudaFuncSetAttribute(small_adjoint_kernel<N>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    auto kern = ts == 4 ? small_adjoint_kernel<N, 2> : (ts == 3 ? small_adjoint_kernel<N, 1> : small_adjoint_kernel<N, 0>);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    small_adjoint_kernel<N><<<(unsigned)p.batch, (unsigned)threads, smem, s>>>(C, sg, *aa);
+    kern<<<(unsigned)p.batch, (unsigned)threads, smem, s>>>(C, sg, *aa);
   }
   return cudaGetLastError();
 }

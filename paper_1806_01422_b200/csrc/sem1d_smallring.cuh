@@ -80,10 +80,13 @@ __device__ __forceinline__ void small_pattern(const Consts<N>& C, const SmallGeo
   }
 }
 
-template <int N>
+// SCH: compile-time tableau (TabC: 0 Euler, 1 Kutta-3, 2 RK4) -- the stage loops unroll and
+// the coefficients become immediates; same values and association as the runtime tableau
+template <int N, int SCH>
 __global__ void __launch_bounds__(1024, 1)
     small_forward_kernel(const __grid_constant__ Consts<N> C, const SmallGeo G, const EnsArgs A) {
   constexpr int n = N + 1;
+  using TB = TabC<SCH>;
   extern __shared__ __align__(16) double smem[];
   const int ndof = G.ndof;
   double* sK = smem;
@@ -111,7 +114,8 @@ __global__ void __launch_bounds__(1024, 1)
   __syncthreads();
   for (int step = 0; step < A.nsteps; ++step) {
     const double dt = A.dts[step];
-    for (int st = 0; st < A.tab.s; ++st) {
+#pragma unroll
+    for (int st = 0; st < TB::s; ++st) {
       const double* src = (st == 0) ? su : sU;
       if (e < G.E) {
         if (owns) fin = fma(src[g], 0.0, fin);
@@ -121,16 +125,17 @@ __global__ void __launch_bounds__(1024, 1)
       if (owns) {
         double kk = __dmul_rn(small_assemble<N>(G, srow, e, i), minv);
         if (masked) kk = __dmul_rn(kk, 0.0);
-        const double term = __dmul_rn(A.tab.b[st], kk);
+        const double term = __dmul_rn(TB::b(st), kk);
         acc = (st == 0) ? term : __dadd_rn(acc, term);
-        if (st + 1 < A.tab.s) {
+        if (st + 1 < TB::s) {
           double y;
-          if (A.tab.nterm[st + 1] == 1) {
-            y = __dadd_rn(su[g], __dmul_rn(__dmul_rn(dt, A.tab.a[st + 1][st]), kk));
+          if (TB::nterm(st + 1) == 1) {
+            y = __dadd_rn(su[g], __dmul_rn(__dmul_rn(dt, TB::a(st + 1, st)), kk));
           } else {
-            double sacc = __dmul_rn(A.tab.a[st + 1][0], (st == 0) ? kk : kkeep);
+            double sacc = __dmul_rn(TB::a(st + 1, 0), (st == 0) ? kk : kkeep);
+#pragma unroll
             for (int jj = 1; jj <= st; ++jj)
-              sacc = __dadd_rn(sacc, __dmul_rn(A.tab.a[st + 1][jj], (jj == st) ? kk : kkeep));
+              sacc = __dadd_rn(sacc, __dmul_rn(TB::a(st + 1, jj), (jj == st) ? kk : kkeep));
             y = __dadd_rn(su[g], __dmul_rn(dt, sacc));
           }
           sU[g] = y;
@@ -152,10 +157,11 @@ __global__ void __launch_bounds__(1024, 1)
     atomicOr(&A.flags[b], (fin != fin ? SEM1D_FLAG_STATE_NONFINITE : 0) | (bad ? SEM1D_FLAG_STEP_NONFINITE : 0));
 }
 
-template <int N>
+template <int N, int SCH>
 __global__ void __launch_bounds__(1024, 1)
     small_adjoint_kernel(const __grid_constant__ Consts<N> C, const SmallGeo G, const EnsAdjArgs A) {
   constexpr int n = N + 1;
+  using TB = TabC<SCH>;
   extern __shared__ __align__(16) double smem[];
   const int ndof = G.ndof, pad = ndof + 2;
   double* sK = smem;
@@ -167,7 +173,7 @@ __global__ void __launch_bounds__(1024, 1)
   const int e = tid / n, i = tid - (tid / n) * n;
   const int64_t b = blockIdx.x, nb = gridDim.x;
   const double mnu = -C.nu;
-  const int S = A.tab.s;
+  constexpr int S = TB::s;
   for (int k = tid; k < n * n; k += blockDim.x) { sK[k] = C.K[k]; sDw[k] = C.Dw[k]; }
   int g = 0;
   const bool owns = small_owned(G, e, i, g);
@@ -176,17 +182,21 @@ __global__ void __launch_bounds__(1024, 1)
   if (owns) small_pattern<N>(C, G, g, minv, masked);
   double lam = owns ? A.lam_in[b * ndof + g] : 0.0;
   double fin = 0.0;
+  // this thread's trajectory value of the next step, loaded one step ahead
+  auto traj_at = [&](int step) { return A.traj[((int64_t)step * nb + b) * ndof + g]; };
+  double unext = (owns && A.nsteps > 0) ? traj_at(A.nsteps - 1) : 0.0;
   __syncthreads();
   for (int step = A.nsteps - 1; step >= 0; --step) {
     const double dt = A.dts[step];
-    const double* un = A.traj + ((int64_t)step * nb + b) * ndof;
     if (owns) {
-      sUs[g] = un[g];
-      if (g == 0 && G.periodic) sUs[ndof] = un[g];
+      sUs[g] = unext;
+      if (g == 0 && G.periodic) sUs[ndof] = unext;
+      if (step > 0) unext = traj_at(step - 1);
     }
     __syncthreads();
     // stage states U_1..U_{S-1} (timeloop.rk3_stages)
     double kkeep = 0.0;
+#pragma unroll
     for (int st = 0; st + 1 < S; ++st) {
       const double* src = sUs + st * pad;
       if (e < G.E) srow[tid] = small_row<N, OP_RHS>(sK, sDw, src, nullptr, e, i, mnu);
@@ -195,12 +205,13 @@ __global__ void __launch_bounds__(1024, 1)
         double kk = __dmul_rn(small_assemble<N>(G, srow, e, i), minv);
         if (masked) kk = __dmul_rn(kk, 0.0);
         double y;
-        if (A.tab.nterm[st + 1] == 1) {
-          y = __dadd_rn(sUs[g], __dmul_rn(__dmul_rn(dt, A.tab.a[st + 1][st]), kk));
+        if (TB::nterm(st + 1) == 1) {
+          y = __dadd_rn(sUs[g], __dmul_rn(__dmul_rn(dt, TB::a(st + 1, st)), kk));
         } else {
-          double sacc = __dmul_rn(A.tab.a[st + 1][0], (st == 0) ? kk : kkeep);
+          double sacc = __dmul_rn(TB::a(st + 1, 0), (st == 0) ? kk : kkeep);
+#pragma unroll
           for (int jj = 1; jj <= st; ++jj)
-            sacc = __dadd_rn(sacc, __dmul_rn(A.tab.a[st + 1][jj], (jj == st) ? kk : kkeep));
+            sacc = __dadd_rn(sacc, __dmul_rn(TB::a(st + 1, jj), (jj == st) ? kk : kkeep));
           y = __dadd_rn(sUs[g], __dmul_rn(dt, sacc));
         }
         double* dst = sUs + (st + 1) * pad;
@@ -212,11 +223,13 @@ __global__ void __launch_bounds__(1024, 1)
     }
     // stage-adjoint chain i = S-1..0 (adjoint.py:58-61), lam' = ((lam + l_0) + l_1) + ...
     double l[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
     for (int st = S - 1; st >= 0; --st) {
       if (owns) {
-        double z = __dmul_rn(A.tab.b[st], lam);
+        double z = __dmul_rn(TB::b(st), lam);
+#pragma unroll
         for (int jj = st + 1; jj < S; ++jj)
-          if (A.tab.a[jj][st] != 0.0) z = __dadd_rn(z, __dmul_rn(A.tab.a[jj][st], l[jj]));
+          if (TB::a(jj, st) != 0.0) z = __dadd_rn(z, __dmul_rn(TB::a(jj, st), l[jj]));
         fin = fma(z, 0.0, fin);
         double zm = __dmul_rn(z, minv);
         if (masked) zm = __dmul_rn(zm, 0.0);
@@ -235,6 +248,7 @@ __global__ void __launch_bounds__(1024, 1)
     }
     if (owns) {
       double acc = lam;
+#pragma unroll
       for (int st = 0; st < S; ++st) acc = __dadd_rn(acc, l[st]);
       lam = acc;
     }
