@@ -81,11 +81,13 @@ constexpr int kEnsAdjWarps = 8;
 #define ENS_ILV 1       // ensemble kernels: interleaved rows when E is a multiple of 8*WMT
 #endif
 #ifndef ENS_ADJ_W16
-#define ENS_ADJ_W16 0
+#define ENS_ADJ_W16 1
 #endif
-// backward-sweep warps: 8 (x 4 interleaved m-tiles at n = 16, B fragments in registers:
-// cfg4 adjoint 764 ms); ENS_ADJ_W16 = 16 warps x 2 with the B fragments in a shared-memory
-// table (ens_adj_bsm; 804 ms: the 128-register cap spills)
+// backward-sweep warps at n = 16: 16 x 2 interleaved m-tiles with the B fragments in a
+// shared-memory table (ens_adj_bsm).  Round 1 measured it slower (804 vs 764 ms, the
+// 128-register cap spilled); after round 2's kernel changes it is faster: config-4 adjoint
+// 443.3 -> 431.0 ms (8 warps x 4 with register B fragments: 253 registers, 2 warps per
+// sub-partition)
 template <int N>
 constexpr int ens_adj_warps() { return (ENS_ADJ_W16 && (N + 1) == 16) ? 16 : kEnsAdjWarps; }
 template <int N>
