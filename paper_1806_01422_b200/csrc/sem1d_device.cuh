@@ -942,8 +942,12 @@ typedef double ws_fin_t;
 #ifndef WS_MINB_F8
 #define WS_MINB_F8 3
 #endif
+// round 2: J at 2 CTAs/SM (deeper pipeline: 106.4 -> 103.9 us); J^T stays at 3 (109.2 at 2)
 #ifndef WS_MINB_J8
-#define WS_MINB_J8 3
+#define WS_MINB_J8 2
+#endif
+#ifndef WS_MINB_JT8
+#define WS_MINB_JT8 3
 #endif
 // output staging buffers: 2 lets a warp compute tile t+1 while the bulk store of
 // tile t still reads its staging (F has the shared memory to spare)
@@ -967,7 +971,8 @@ constexpr int ws_outb() { return OP == OP_RHS ? WS_OUTB_F : WS_OUTB_J; }
 template <int N, int OP, int NZ = -1>
 constexpr int ws_minb() {
   if constexpr (NZ >= 0) return ((N + 1) == 32 && NZ > 0) ? 1 : 2;
-  return ((N + 1) > 16) ? (OP == OP_RHS ? WS_MINB32_F : WS_MINB32) : ((N + 1) == 16 ? 2 : (OP == OP_RHS ? WS_MINB_F8 : WS_MINB_J8));
+  return ((N + 1) > 16) ? (OP == OP_RHS ? WS_MINB32_F : WS_MINB32)
+                        : ((N + 1) == 16 ? 2 : (OP == OP_RHS ? WS_MINB_F8 : (OP == OP_JAC ? WS_MINB_J8 : WS_MINB_JT8)));
 }
 
 // ws-kernel B fragments with permuted output columns: DMMA output column
