@@ -1117,6 +1117,11 @@ __device__ __forceinline__ void mtile_compute(const Consts<N>& C, const Geo& G, 
 #ifndef WS_ILV
 #define WS_ILV 1
 #endif
+// J^T at n = 8 on interleaved rows too (round 2: 107.1 -> 106.6 us; round 1 had measured it
+// slower, 126.9 vs 112.2, before the fragment table and the other kernel changes)
+#ifndef WS_ILV_JT7
+#define WS_ILV_JT7 1
+#endif
 // n = 32: output n-tiles per accumulation group in mtile_compute_multi (A/B on config 3:
 // 1 / 2 / 4 -> J^T 90.0 / 88.3 / 88.0 us, F and J flat within 0.3%; 4 slowed J to 75.8 us)
 // F on periodic rings: -nu M^-1 / M^-1 folded into the K / Dw fragments (2 FP64 multiplies per
@@ -1510,7 +1515,7 @@ __global__ void __launch_bounds__(WsTile<N, OP, NZ>::THREADS, ws_minb<N, OP, NZ>
         constexpr bool MULTI = W::B_IN_SMEM && (WMT > 1);
         // interleaved rows: A/B (config 2 / 3) F 86.5 -> 85.3 us, J 111.9 -> 111.0 (n = 8);
         // F 59.9 -> 55.4, J 77.9 -> 73.8 (n = 32); J^T at n = 8 measured slower (126.9 vs 112.2)
-        constexpr bool ILVW = WS_ILV && (WMT == 2 || WMT == 4) && !(OP == OP_JACT && N == 7);
+        constexpr bool ILVW = WS_ILV && (WMT == 2 || WMT == 4) && !(OP == OP_JACT && N == 7 && !WS_ILV_JT7);
         double rq[WMT][NT][2];
         if constexpr (MULTI) {
           mtile_compute_multi<N, OP, EDGE, WMT, ILVW, decltype(bget), PRE>(C, G, su, sw, (wel0 + 1) * N, e0 + wel0, rr,
