@@ -912,8 +912,9 @@ typedef double ws_fin_t;
 #define WS_FIN_BAD(acc) ((acc) != (acc))
 #endif
 
+// round 2: F on 512-element tiles at 2 CTAs/SM (77.5 -> 76.9 us); J / J^T keep 256
 #ifndef WS_ELEMS8
-#define WS_ELEMS8 256
+#define WS_ELEMS8 512
 #endif
 // n = 32: consumer warps per operator (A/B, config 3): 8 warps x 2 interleaved m-tiles with
 // each shared-memory B fragment feeding both (mtile_compute_multi): F / J 55.4 / 73.8 us
@@ -940,7 +941,7 @@ typedef double ws_fin_t;
 // Occupancy per operator (A/B-measured on config 2, profiles/r1_ab_occupancy.json):
 // F (one input) runs best at 4 CTAs/SM, J and J^T at 3.
 #ifndef WS_MINB_F8
-#define WS_MINB_F8 3
+#define WS_MINB_F8 2
 #endif
 // round 2: J at 2 CTAs/SM (deeper pipeline: 106.4 -> 103.9 us); J^T stays at 3 (109.2 at 2)
 #ifndef WS_MINB_J8
@@ -991,7 +992,7 @@ __device__ __forceinline__ double bfrag_perm(const Consts<N>& C, int mat, int nt
 }
 
 #ifndef WS_ELEMS8_J
-#define WS_ELEMS8_J WS_ELEMS8
+#define WS_ELEMS8_J 256
 #endif
 template <int N, int OP = OP_RHS, int NZ = -1>
 struct WsTile {
