@@ -938,12 +938,13 @@ typedef double ws_fin_t;
 #define WS_ELEMS32_J 64
 #endif
 
-// Occupancy per operator (A/B-measured on config 2, profiles/r1_ab_occupancy.json):
-// F (one input) runs best at 4 CTAs/SM, J and J^T at 3.
+// Occupancy per operator at n = 8, A/B-measured on config 2 (round 1:
+// profiles/r1_ab_occupancy.json; re-measured in round 2, profiles/r2_ws_ab_cfg2.jsonl):
+// F on 512-element tiles at 2 CTAs/SM, J at 2 (deeper pipeline: 106.4 -> 103.9 us), J^T at 3
+// (109.2 us at 2)
 #ifndef WS_MINB_F8
 #define WS_MINB_F8 2
 #endif
-// round 2: J at 2 CTAs/SM (deeper pipeline: 106.4 -> 103.9 us); J^T stays at 3 (109.2 at 2)
 #ifndef WS_MINB_J8
 #define WS_MINB_J8 2
 #endif
