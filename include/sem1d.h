@@ -68,7 +68,8 @@ int sem1d_version(void);
 int sem1d_set_kernel_path(int path);
 /* Tile-step kernels for A/B runs: 0 = auto (register-resident kernels for N = 7),
  * 1 = the shared-memory tile kernels for every degree (and the shared-memory ensemble
- * forward sweep at N = 15). */
+ * forward sweep at N = 15), 2 = N = 7 register-resident steps on 128-element tiles,
+ * 3 = the N = 7 register-resident forward step on 192-element tiles at 3 CTAs/SM. */
 int sem1d_set_tile_variant(int variant);
 const char* sem1d_last_error(void);
 int sem1d_max_degree(void);
