@@ -505,10 +505,13 @@ def cfg5_sweep(torch, dist, world, rank, dev, steps, backend="nccl"):
     dt = c["dt"]
     states = [u0] + [op.empty() for _ in range(steps)]
     lam = [lam0.clone(), op.empty()]
+    # the forward steps in the form the gradient's run-ahead integrate launches them: each
+    # step ORs into a flag word and checks only its new state (timeloop.integrate)
+    slot = op.flag_slots(1)
 
     def run(k):
         for i in range(k):
-            op.launch_rk_step(states[i], states[i + 1], dt, "rk4")
+            op.launch_rk_step(states[i], states[i + 1], dt, "rk4", flag=slot.data_ptr())
         f1 = torch.cuda.Event(enable_timing=True)
         f1.record()
         for i in range(k - 1, -1, -1):
@@ -530,7 +533,7 @@ def cfg5_sweep(torch, dist, world, rank, dev, steps, backend="nccl"):
         tt = torch.tensor(t, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t = tt.tolist()
-    if op.flags():
+    if op.flags() or int(slot[0]):
         raise RuntimeError("non-finite flag in the config-5 sweep")
     dof = E * c["N"]
     del states, lam, u0, lam0
