@@ -390,10 +390,12 @@ def tile_kernel_times(op, torch, hbm_gbs, reps=20):
     st = [op.empty() for _ in range(3)]
     slot = op.flag_slots(1)
     dt = 1e-14
+    # every kernel in the form the run-ahead integrate / sweep launches it (per-step flag word,
+    # outputs-only check; a flagged step is re-run with the classifying check)
     runs = {"fwd": lambda: op.launch_rk_step(u, o, dt, "rk4", flag=slot.data_ptr()),
-            "fwd_st": lambda: op.launch_rk_step_stages(u, o, st, dt, "rk4"),
-            "adj": lambda: op.launch_adj_step(u, lam, o, dt, "rk4"),
-            "adj_st": lambda: op.launch_adj_step_stages(u, st, lam, o, dt, "rk4")}
+            "fwd_st": lambda: op.launch_rk_step_stages(u, o, st, dt, "rk4", flag=slot.data_ptr()),
+            "adj": lambda: op.launch_adj_step(u, lam, o, dt, "rk4", flag=slot.data_ptr()),
+            "adj_st": lambda: op.launch_adj_step_stages(u, st, lam, o, dt, "rk4", flag=slot.data_ptr())}
     out = {}
     for k, fn in runs.items():
         for _ in range(3):
@@ -515,7 +517,7 @@ def cfg5_sweep(torch, dist, world, rank, dev, steps, backend="nccl"):
         f1 = torch.cuda.Event(enable_timing=True)
         f1.record()
         for i in range(k - 1, -1, -1):
-            op.launch_adj_step(states[i], lam[0], lam[1], dt, "rk4")
+            op.launch_adj_step(states[i], lam[0], lam[1], dt, "rk4", flag=slot.data_ptr())
             lam.reverse()
         return f1
 

@@ -184,13 +184,20 @@ int sem1d_adj_step(const sem1d_plan* plan, const double* u, const double* lam, d
  * flagged step with check = 1 -- bitwise the same state (integrate's run-ahead does). */
 int sem1d_rk_step_ex(const sem1d_plan* plan, const double* u, double* u_new, double* const* stages,
                      double dt, int scheme, int check, int tile_lo, int tile_cnt, int* flag, void* stream);
-/* The adjoint step (adjoint.py:54-61) with stored stages (may be NULL: recompute) and a tile
- * range.  Ranges (N = 7 kernels): the launch covers ring tiles (tile_lo + k) mod ntiles,
+/* The adjoint step (adjoint.py:54-61) with stored stages (may be NULL: recompute), a choice
+ * of checks and a tile range.  check = 1 is sem1d_adj_step / sem1d_adj_step_stages: stage
+ * states and cotangents are classified (SEM1D_FLAG_STATE_NONFINITE / _INPUT2_NONFINITE).
+ * check = 0 (N = 7 kernels; the others always classify) tests only lam_out: a non-finite
+ * stage state or cotangent then shows as SEM1D_FLAG_STEP_NONFINITE (it reaches lam_out through
+ * every stage term), and a caller that must raise the reference's exception re-runs the
+ * flagged step with check = 1 (bitwise the same lam_out; the sweep's run-ahead does).
+ * Ranges (N = 7 kernels): the launch covers ring tiles (tile_lo + k) mod ntiles,
  * k < tile_cnt (tile_cnt 0 = all).  A sharded step runs the tiles that read no ghost element
  * while the ghost exchange is in flight, then the rest; sem1d_step_tiling gives the layout:
  * tile t reads elements [t*owned - ghost, (t+1)*owned + ghost) of the ring. */
 int sem1d_adj_step_ex(const sem1d_plan* plan, const double* u, const double* const* stages, const double* lam,
-                      double* lam_out, double dt, int scheme, int tile_lo, int tile_cnt, int* flag, void* stream);
+                      double* lam_out, double dt, int scheme, int check, int tile_lo, int tile_cnt, int* flag,
+                      void* stream);
 int sem1d_step_tiling(const sem1d_plan* plan, int kind, int stored, int scheme, int* ntiles, int* owned,
                       int* ghost);
 

@@ -76,7 +76,7 @@ SIGNATURES = {
     "sem1d_rk_step_ex": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int, c_int, c_int, c_int,
                                  c_void_p, c_void_p]),
     "sem1d_adj_step_ex": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int, c_int, c_int,
-                                  c_void_p, c_void_p]),
+                                  c_int, c_void_p, c_void_p]),
     "sem1d_step_tiling": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_void_p]),
     "sem1d_adj_step": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int, c_void_p,
                                c_void_p]),

@@ -148,6 +148,7 @@ def adjoint_step_cn(op, u_n, u_np1, lam, t, dt, cfg, stats=None, out=None):
 
 
 _ADJ_WINDOW = 16      # adjoint steps launched between two flag reads (run-ahead sweep)
+_ADJ_WINDOW_BYTES = 8e9   # cotangents a run-ahead window keeps alive for a classifying re-run
 
 
 def sweep(op, cfg, fwd, schedule, lam_terminal, check_every=None):
@@ -159,10 +160,12 @@ def sweep(op, cfg, fwd, schedule, lam_terminal, check_every=None):
     recorded dts through the same fused stage kernels (bitwise replay).
 
     Flags: on the fused step kernels the sweep runs ahead (``check_every=None``): each
-    adjoint step ORs its non-finite bits into its own flag word and one device->host read
-    verifies up to _ADJ_WINDOW steps (and always before a recompute Advance and at the
-    end).  The first flagged step raises the same NumericFailure, with the same counters, as
-    the per-step check (``check_every=1``) would have.
+    adjoint step tests only its output cotangent and ORs the result into its own flag word,
+    and one device->host read verifies up to _ADJ_WINDOW steps (and always before a
+    recompute Advance and at the end).  A flagged step is re-run from its kept inputs with
+    the classifying check (state / cotangent, as the reference's per-call checks), bitwise
+    the same output; the first step that classifies raises the same NumericFailure, with the
+    same counters, as the per-step check (``check_every=1``) would have.
     """
     m = fwd.n_steps
     if schedule.n_steps != m:
@@ -204,11 +207,17 @@ def sweep(op, cfg, fwd, schedule, lam_terminal, check_every=None):
     ahead = (check_every is None and not cn and getattr(op, "supports_flag_slots", False)
              and fz is not None and fz())
     check_every = 1 if check_every is None else check_every
-    pending = []                       # (step, counters after it) of the unverified steps
+    # unverified steps: (step, counters after it, u_n, lam_{n+1}, stages, dt) -- the inputs
+    # stay alive until the window is verified, for the classifying re-run of a flagged step
+    pending = []
+    window = _ADJ_WINDOW
     if ahead:
-        wslots = op.flag_slots(_ADJ_WINDOW)
+        field = max(1, op.ndof * getattr(op, "batch", 1) * 8)
+        window = max(1, min(_ADJ_WINDOW, int(_ADJ_WINDOW_BYTES // field)))
+        wslots = op.flag_slots(window)
         wslots.zero_()
         wslot0 = wslots.data_ptr()
+    classify = _lib.SEM1D_FLAG_STATE_NONFINITE | _lib.SEM1D_FLAG_INPUT2_NONFINITE
 
     def verify():
         if not pending:
@@ -217,12 +226,26 @@ def sweep(op, cfg, fwd, schedule, lam_terminal, check_every=None):
         red = getattr(op, "reduce_flag_words", None)      # sharded: OR over ranks
         vals = (red(words) if red is not None else words).cpu().tolist()
         wslots.zero_()
-        bad = next((i for i, v in enumerate(vals) if v), None)
-        if bad is not None:
-            op.counters.clear()
-            op.counters.update(pending[bad][1])          # as if the sweep stopped at that step
-            pending.clear()
-            _check_adjoint_flags(op, vals[bad])
+        for j, v in enumerate(vals):
+            if not v:
+                continue
+            n, after, u_j, lam_j, st_j, dt_j = pending[j]
+            if not v & classify:
+                # outputs-only flag: re-run the step with the classifying check (the op's own
+                # flag word; sharded ranks all take this branch: the words were OR-reduced)
+                saved = dict(op.counters)
+                op.flags()
+                adj.step(u_j, lam_j, dt_j, op.empty(), stages=st_j)
+                v = op.flags()
+                op.counters.clear()
+                op.counters.update(saved)
+            if v & classify:
+                op.counters.clear()
+                op.counters.update(after)                # as if the sweep stopped at that step
+                pending.clear()
+                _check_adjoint_flags(op, v)
+            # an output that overflowed from finite inputs: the reference raises only when a
+            # later step reads it as its cotangent, which that step's re-run classifies
         pending.clear()
 
     for act in actions:
@@ -263,14 +286,15 @@ def sweep(op, cfg, fwd, schedule, lam_terminal, check_every=None):
                 u_np1 = succ[1] if succ[0] == n + 1 else fwd.u_final
                 adjoint_step_cn(op, current[1], u_np1, lam, fwd.ts[n], dts[n], cfg, stats, out=spare)
             elif ahead:
+                spare = op.empty()                       # lam stays alive while the step is pending
                 adj.step(current[1], lam, dts[n], spare, stages=stage_snaps.get(n),
                          flag=wslot0 + 4 * len(pending))
-                pending.append((n, dict(op.counters)))
+                pending.append((n, dict(op.counters), current[1], lam, stage_snaps.get(n), dts[n]))
             else:
                 adj.step(current[1], lam, dts[n], spare, stages=stage_snaps.get(n))
             lam, spare = spare, lam
             if ahead:
-                if len(pending) == _ADJ_WINDOW:
+                if len(pending) == window:
                     verify()
             else:
                 since_check += 1

@@ -709,7 +709,8 @@ int sem1d_rk_step_ex(const sem1d_plan* plan, const double* u, double* u_new, dou
 }
 
 int sem1d_adj_step_ex(const sem1d_plan* plan, const double* u, const double* const* stages, const double* lam,
-                      double* lam_out, double dt, int scheme, int tile_lo, int tile_cnt, int* flag, void* stream) {
+                      double* lam_out, double dt, int scheme, int check, int tile_lo, int tile_cnt, int* flag,
+                      void* stream) {
   DeviceGuard guard_(plan ? plan->device : -1);
   if (!valid_burgers(plan) || !u || !lam || !lam_out || !flag || lam == lam_out)
     return fail(SEM1D_EINVAL, "sem1d_adj_step_ex: bad argument (lam_out must not alias lam)");
@@ -723,7 +724,7 @@ int sem1d_adj_step_ex(const sem1d_plan* plan, const double* u, const double* con
       a.stin[i] = stages[i];
     }
   }
-  a.u = u; a.lam = lam; a.out = lam_out; a.flag = flag; a.dt = dt; a.check = 1;
+  a.u = u; a.lam = lam; a.out = lam_out; a.flag = flag; a.dt = dt; a.check = check ? 1 : 0;
   a.tile_lo = tile_lo; a.tile_cnt = tile_cnt;
   cudaError_t e = dispatch_tile(plan, 1, a, static_cast<cudaStream_t>(stream));
   if (e == cudaErrorNotSupported)

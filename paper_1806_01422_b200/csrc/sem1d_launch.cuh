@@ -355,7 +355,9 @@ cudaError_t launch_tile_rf(const PlanView& p, const TileStepArgs& a, cudaStream_
 template <int SCH, bool LD, int WMT, int MINB, bool DR = false>
 cudaError_t launch_tile_adj_rf(const PlanView& p, const TileStepArgs& a, cudaStream_t s) {
   constexpr size_t sm = RfAdjCfg<WMT>::template smem<LD, DR>();
-  return launch_tile_one<7, tile_adj_rf_kernel<SCH, LD, WMT, MINB, DR>>(p, a, 32 * RfAdjCfg<WMT>::W, sm, sm, s);
+  if (!a.check)   // run-ahead form: outputs-only check (classifying re-run by the caller)
+    return launch_tile_one<7, tile_adj_rf_kernel<SCH, LD, WMT, MINB, DR, false>>(p, a, 32 * RfAdjCfg<WMT>::W, sm, sm, s);
+  return launch_tile_one<7, tile_adj_rf_kernel<SCH, LD, WMT, MINB, DR, true>>(p, a, 32 * RfAdjCfg<WMT>::W, sm, sm, s);
 }
 
 // elements per tile of the kernel launch_tile_sch picks (kind 0 forward, 1 adjoint)

@@ -418,8 +418,13 @@ __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // DR (recompute mode): J^T(U_i), i < s-1, reuses M^-1 Dw U_i from the stage recompute
-// (two of its six DMMAs per m-tile), kept in per-lane shared-memory slots
-template <int SCH, bool LD, int WMT, int MINB, bool DR = false>
+// (two of its six DMMAs per m-tile), kept in per-lane shared-memory slots.
+// CHK = false (the sweep's run-ahead, check = 0): only the owned outputs lam_n are tested
+// (SEM1D_FLAG_STEP_NONFINITE).  A non-finite stage state or cotangent reaches lam_n at its
+// element's nodes through every stage term (products with U and w, every b_i != 0), so the
+// run-ahead re-runs a flagged step with CHK = true, which classifies its inputs as the
+// reference's per-call checks do (state / cotangent bits) and gives bitwise the same lam_n.
+template <int SCH, bool LD, int WMT, int MINB, bool DR = false, bool CHK = true>
 __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
     tile_adj_rf_kernel(const __grid_constant__ Consts<7> C, const Geo G, const TileStepArgs A) {
   using CF = RfAdjCfg<WMT>;
@@ -498,7 +503,7 @@ __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
     pend |= 1u << x;
     want = -1;
   };
-  unsigned fstate = 0u, fz = 0u;
+  unsigned fstate = 0u, fz = 0u, fout = 0u;
   int it = 0;
   for (int k = blockIdx.x; k < cnt; k += gridDim.x, ++it) {
     const int t = tile_of(k);
@@ -593,7 +598,7 @@ __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
       for (int st = 0; st + 1 < S; ++st) {
 #pragma unroll
         for (int q = 0; q < WMT; ++q)
-          fstate = max(fstate, max(expbits(U[q][0], msk[q][0]), expbits(U[q][1], msk[q][1])));
+          if (CHK) fstate = max(fstate, max(expbits(U[q][0], msk[q][0]), expbits(U[q][1], msk[q][1])));
         auto mtile_F = [&](int q) {
           double ka = 0.0, kb = 0.0, da = 0.0, db = 0.0;
           dmma884(ka, kb, U[q][0], bk[0]);
@@ -660,7 +665,7 @@ __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
       if (LD || i == S - 1) {                    // U_0..U_{s-2} were checked as stage inputs
 #pragma unroll
         for (int q = 0; q < WMT; ++q)
-          fstate = max(fstate, max(expbits(U[q][0], msk[q][0]), expbits(U[q][1], msk[q][1])));
+          if (CHK) fstate = max(fstate, max(expbits(U[q][0], msk[q][0]), expbits(U[q][1], msk[q][1])));
       }
       double Lr[WMT][2];                         // l'_i / dt (element rows, then assembled)
       // dt rides on the recurrence's coefficients: w_i = lam + c dt l'', lam_n = lam + b dt l''
@@ -677,7 +682,7 @@ __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
           z[h] = zz;
           y[h] = __dmul_rn(U[q][h], zz);
         }
-        if (i + 1 < S) fz = max(fz, max(expbits(z[0], msk[q][0]), expbits(z[1], msk[q][1])));
+        if (CHK && i + 1 < S) fz = max(fz, max(expbits(z[0], msk[q][0]), expbits(z[1], msk[q][1])));
         double ca = 0.0, cb = 0.0, da = 0.0, db = 0.0;
         dmma884(ca, cb, z[0], jk[0]);
         if (DR && !LD && i + 1 < S) {            // reuse the stage recompute's M^-1 Dw U_i
@@ -693,7 +698,7 @@ __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
         Lr[q][0] = __fma_rn(-z[0], da, ca);
         Lr[q][1] = __fma_rn(-z[1], db, cb);
       };
-      if (i == S - 1) {                          // w_{s-1} = lam: the cotangent input check
+      if (CHK && i == S - 1) {                   // w_{s-1} = lam: the cotangent input check
 #pragma unroll
         for (int q = 0; q < WMT; ++q) fz = max(fz, max(expbits(val(1, q, 0), msk[q][0]), expbits(val(1, q, 1), msk[q][1])));
       }
@@ -720,16 +725,19 @@ __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
     // lam_n = lam + (b_{s-1} l'_{s-1} + ... + b_0 l'_0), owned nodes
 #pragma unroll
     for (int q = 0; q < WMT; ++q) {
+      const double o0 = __dadd_rn(val(1, q, 0), lacc[q][0]), o1 = __dadd_rn(val(1, q, 1), lacc[q][1]);
+      if (!CHK) fout = max(fout, max(expbits(o0, msk[q][0]), expbits(o1, msk[q][1])));
       if (!own[q]) continue;
       const int64_t g = (e_base + e_lane + q) * N;
-      A.out[g + kq] = __dadd_rn(val(1, q, 0), lacc[q][0]);
-      if (kq != 0) A.out[g + 7 - kq] = __dadd_rn(val(1, q, 1), lacc[q][1]);
+      A.out[g + kq] = o0;
+      if (kq != 0) A.out[g + 7 - kq] = o1;
     }
     __syncwarp();
     if (L.bulk && lane == 0) mbar_arrive(&empty[b]);   // this warp is done with the tile's slabs
   }
   const unsigned bits = (fstate == 0x7ff00000u ? SEM1D_FLAG_STATE_NONFINITE : 0u) |
-                        (fz == 0x7ff00000u ? SEM1D_FLAG_INPUT2_NONFINITE : 0u);
+                        (fz == 0x7ff00000u ? SEM1D_FLAG_INPUT2_NONFINITE : 0u) |
+                        (fout == 0x7ff00000u ? SEM1D_FLAG_STEP_NONFINITE : 0u);
   const unsigned any = __reduce_or_sync(0xffffffffu, bits);
   if (lane == 0 && any) atomicOr(A.flag, (int)any);
 }

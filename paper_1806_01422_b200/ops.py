@@ -416,21 +416,25 @@ class SemOperator(ComposedStages):
             flag or self._flag.data_ptr(), self._stream()), "sem1d_rk_step_ex")
 
     def launch_adj_step_stages(self, u, stages, lam, lam_out, dt, scheme, flag=None, tiles=None):
-        """One fused adjoint step reading the stored stage states (no recompute)."""
+        """One fused adjoint step reading the stored stage states (no recompute); checks as in
+        launch_adj_step."""
         lo, cnt = tiles or (0, 0)
         _lib.check(_lib.load().sem1d_adj_step_ex(
             self._plan.handle, u.data_ptr(), _lib.ptr_array([t.data_ptr() for t in stages]), lam.data_ptr(),
-            lam_out.data_ptr(), float(dt), self._SCHEME_CODES[scheme], int(lo), int(cnt),
+            lam_out.data_ptr(), float(dt), self._SCHEME_CODES[scheme], 0 if flag else 1, int(lo), int(cnt),
             flag or self._flag.data_ptr(), self._stream()), "sem1d_adj_step_ex")
 
     def launch_adj_step(self, u, lam, lam_out, dt, scheme, flag=None, tiles=None):
-        """One fused adjoint step; ``flag`` as in launch_rk_step (``sweep`` runs ahead with
-        per-step flag words), ``tiles`` as in launch_rk_step."""
+        """One fused adjoint step; ``flag`` as in launch_rk_step: with a per-step flag word
+        (``sweep`` running ahead) the step tests only its output lam_out and the sweep re-runs a
+        flagged step with the classifying check (sem1d_adj_step_ex); ``tiles`` as in
+        launch_rk_step."""
         lo, cnt = tiles or (0, 0)
         _lib.check(_lib.load().sem1d_adj_step_ex(self._plan.handle, u.data_ptr(), None, lam.data_ptr(),
                                                  lam_out.data_ptr(), float(dt), self._SCHEME_CODES[scheme],
-                                                 int(lo), int(cnt), flag or self._flag.data_ptr(),
-                                                 self._stream()), "sem1d_adj_step_ex")
+                                                 0 if flag else 1, int(lo), int(cnt),
+                                                 flag or self._flag.data_ptr(), self._stream()),
+                   "sem1d_adj_step_ex")
 
     # -- implicit path (Crank-Nicolson; SURVEY.md 8(f) row 1) --------------------
 
