@@ -437,8 +437,8 @@ __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
   double* sslab = smem;                       // [2][SB][PAD]
   double* sst = sslab + 2 * SB * PAD;         // [2][SLOT] recompute: U_1, U_2 per lane
   double* sdw = sst + 2 * SLOT;               // [3][SLOT] DR: M^-1 Dw U_0..U_2 per lane
-  double* xF = sst + (LD ? 0 : (DR ? 5 : 2) * SLOT);   // [16]
-  double* xU = xF + 16;                       // [16]
+  double* xF = sst + (LD ? 0 : (DR ? 5 : 2) * SLOT);   // [2][8] raw row 7 of each warp's last element
+  double* xU = xF + 16;                       // [2][8] raw row 0 of each warp's first element
   uint64_t* full = reinterpret_cast<uint64_t*>(xU + 16);
   uint64_t* empty = full + 2;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -549,42 +549,55 @@ __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
     }
     double U[WMT][2], F[WMT][2];
     double k0[(SCH == 1) ? WMT : 1][2];
-    // pairwise exchange of a stage result R: interface sum (row 7 of e-1 into row 0 of e),
-    // then, after `mid` updated m-tile 0 and `rest` the others, the node-7 replica refresh
-    // of `Rn` (barriers run in every stage: see the forward kernel)
-    auto exchange = [&](double (&R)[WMT][2], auto&& mid, auto&& rest, double (&Rn)[WMT][2], bool refresh) {
+    // Pairwise exchange of a stage result R, ONE round per stage: each warp publishes the raw
+    // row 7 of its last element (to the right) and the raw row 0 of its first (to the left),
+    // and every interface sum (row 7 of e-1 + row 0 of e) is formed by BOTH lanes that hold
+    // the node -- the owner of node 0 of e and the node-7 replica of e-1 -- from the same two
+    // raw rows in the same order, so the replica is bitwise the owner's value and no second
+    // exchange of updated states is needed.  upd(q) then advances m-tile q (refresh: the
+    // replica rows take the full interface value).  Barrier order per warp: arrive BAR_F+w
+    // (publish_F), sync BAR_F+w-1, arrive BAR_U+w-1, sync BAR_U+w -- a warp passes its sync
+    // on BAR_U+w only after w+1 passed its sync on BAR_F+w, so no barrier generation takes two
+    // arrivals of one warp; the slots are double-buffered by exchange parity.
+    int xpar = 0;
+    auto exchange = [&](double (&R)[WMT][2], auto&& upd, bool refresh) {
       double left = __shfl_up_sync(0xffffffffu, R[WMT - 1][1], 4);
+      double rawr = __shfl_down_sync(0xffffffffu, R[0][0], 4);
       if (w > 0) {
         nbar_sync(RfCfg<4>::BAR_F + w - 1, 64);
-        if (lane == 0) left = xF[w - 1];
+        if (lane == 0) left = xF[xpar * 8 + w - 1];
+        if (lane == 0) xU[xpar * 8 + w] = R[0][0];
+        if (!RF_BAR_NA) __syncwarp();
+        nbar_arrive(RfCfg<4>::BAR_U + w - 1, 64);
       } else if (lane == 0) {
         left = 0.0;
       }
       if (kq == 0) {
+        double rp[WMT];
+#pragma unroll
+        for (int q = 0; q + 1 < WMT; ++q) rp[q] = __dadd_rn(R[q][1], R[q + 1][0]);
 #pragma unroll
         for (int q = WMT - 1; q > 0; --q) R[q][0] = __dadd_rn(R[q - 1][1], R[q][0]);
         R[0][0] = __dadd_rn(left, R[0][0]);
+        if (refresh) {
+#pragma unroll
+          for (int q = 0; q + 1 < WMT; ++q) R[q][1] = rp[q];
+        }
       }
-      mid();
-      double right = __shfl_down_sync(0xffffffffu, Rn[0][0], 4);
-      if (w > 0) {
-        if (refresh && lane == 0) xU[w] = Rn[0][0];
-        nbar_arrive(RfCfg<4>::BAR_U + w - 1, 64);
-      }
-      rest();
+#pragma unroll
+      for (int q = 0; q + 1 < WMT; ++q) upd(q);
       if (w < W - 1) {
         nbar_sync(RfCfg<4>::BAR_U + w, 64);
-        if (lane == 28) right = xU[w + 1];
+        if (lane == 28) rawr = xU[xpar * 8 + w + 1];
       }
-      if (refresh && kq == 0) {
-#pragma unroll
-        for (int q = 0; q + 1 < WMT; ++q) Rn[q][1] = Rn[q + 1][0];
-        Rn[WMT - 1][1] = right;
-      }
+      if (refresh && kq == 0) R[WMT - 1][1] = __dadd_rn(R[WMT - 1][1], rawr);
+      upd(WMT - 1);
+      xpar ^= 1;
     };
     auto publish_F = [&](const double (&R)[WMT][2]) {
       if (w < W - 1) {
-        if (lane == 28) xF[w] = R[WMT - 1][1];
+        if (lane == 28) xF[xpar * 8 + w] = R[WMT - 1][1];
+        if (!RF_BAR_NA) __syncwarp();
         nbar_arrive(RfCfg<4>::BAR_F + w, 64);
       }
     };
@@ -631,12 +644,7 @@ __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
             if (SCH == 1 && st == 0) k0[q][h] = k;
           }
         };
-        exchange(F, [&] { upd(0); },
-                 [&] {
-#pragma unroll
-                   for (int q = 1; q < WMT; ++q) upd(q);
-                 },
-                 U, true);
+        exchange(F, upd, true);
         if (st + 2 < S) {                       // U_{st+1} waits in its per-lane slot
           double* slot = sst + st * SLOT;
 #pragma unroll
@@ -715,12 +723,7 @@ __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
           ln[q][h] = Lr[q][h];
         }
       };
-      exchange(Lr, [&] { acc_q(0); },
-               [&] {
-#pragma unroll
-                 for (int q = 1; q < WMT; ++q) acc_q(q);
-               },
-               ln, i > 0);
+      exchange(Lr, acc_q, i > 0);
     }
     // lam_n = lam + (b_{s-1} l'_{s-1} + ... + b_0 l'_0), owned nodes
 #pragma unroll
