@@ -51,6 +51,11 @@ namespace sem1d {
 #ifndef RF_NOSTORE
 #define RF_NOSTORE 0
 #endif
+// RF_FWD_X1: the forward step's exchanges in the single-round form of the adjoint step
+// (1; A/B against the two-round form, 0)
+#ifndef RF_FWD_X1
+#define RF_FWD_X1 1
+#endif
 #ifndef RF_NOCHK
 #define RF_NOCHK 0          // timing experiment: no non-finite checks in the adjoint step
 #endif
@@ -105,8 +110,8 @@ __global__ void __launch_bounds__(32 * RfCfg<WMT>::W, MINB)
   extern __shared__ __align__(16) double smem[];
   double* sbuf = smem;                        // [2][PAD] tile loads
   double* sout = sbuf + 2 * PAD;              // [2][PAD] output staging (bulk stores)
-  double* xF = sout + 2 * PAD;                // [16] row 7 of each warp's last element
-  double* xU = xF + 16;                       // [16] node 0 of each warp's first element
+  double* xF = sout + 2 * PAD;                // [2][8] raw row 7 of each warp's last element
+  double* xU = xF + 16;                       // [2][8] raw row 0 of each warp's first element
   uint64_t* full = reinterpret_cast<uint64_t*>(xU + 16);
   uint64_t* empty = full + 2;
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -149,6 +154,7 @@ __global__ void __launch_bounds__(32 * RfCfg<WMT>::W, MINB)
     }
   }
   unsigned bad_state = 0u, bad_out = 0u;
+  int xpar = 0;                               // exchange-slot parity (one flip per stage)
   int it = 0;
   for (int k = blockIdx.x; k < cnt; k += gridDim.x, ++it) {
     const int t = tile_of(k);
@@ -283,54 +289,108 @@ __global__ void __launch_bounds__(32 * RfCfg<WMT>::W, MINB)
           }
         }
       };
-      // (1) the warp's last m-tile first: its row 7 is what the right warp waits for
-      mtile_F(WMT - 1);
-      double left = __shfl_up_sync(0xffffffffu, F[WMT - 1][1], 4);
-      if (w < W - 1) {
-        if (lane == 28) xF[w] = F[WMT - 1][1];
-        if (!RF_BAR_NA) __syncwarp();
-        nbar_arrive(CF::BAR_F + w, 64);
-      }
-      // (2) the other m-tiles
+      // the run-ahead form (no checks, no stage stores) keeps the two-round exchange: the
+      // single round measured 208.0 against 206.8 us there, 213.7 against 226.8 us with the
+      // checks and 268.8 against 271.5 us storing the stages (tools/tile_ab.py)
+      if constexpr (!(RF_FWD_X1 && (CHK || STG))) {
+        // (1) the warp's last m-tile first: its row 7 is what the right warp waits for
+        mtile_F(WMT - 1);
+        double left = __shfl_up_sync(0xffffffffu, F[WMT - 1][1], 4);
+        if (w < W - 1) {
+          if (lane == 28) xF[w] = F[WMT - 1][1];
+          if (!RF_BAR_NA) __syncwarp();
+          nbar_arrive(CF::BAR_F + w, 64);
+        }
+        // (2) the other m-tiles
 #pragma unroll
-      for (int q = 0; q + 1 < WMT; ++q) mtile_F(q);
-      // (3) interface node 0 of element e: + row 7 of element e-1 (lane kq = 0 holds both)
-      if (w > 0) {
-        nbar_sync(CF::BAR_F + w - 1, 64);
-        if (lane == 0) left = xF[w - 1];
-      } else if (lane == 0) {
-        left = 0.0;                             // tile edge: ghost element, left incomplete
-      }
-      if (kq == 0) {
-#pragma unroll
-        for (int q = WMT - 1; q > 0; --q) F[q][0] = __dadd_rn(F[q - 1][1], F[q][0]);
-        F[0][0] = __dadd_rn(left, F[0][0]);
-      }
-      // (4) stage update, m-tile 0 first: its node 0 is what the left warp waits for.  The
-      // pairwise barriers also run after the last stage: warp w may arrive on BAR_F + w of the
-      // next stage only after warp w+1 has passed this stage's sync on it (otherwise two of
-      // w's arrivals could complete one barrier generation)
-      update(0);
-      double right = __shfl_down_sync(0xffffffffu, U[0][0], 4);
-      if (w > 0) {
-        if (!last && lane == 0) xU[w] = U[0][0];
-        if (!RF_BAR_NA) __syncwarp();
-        nbar_arrive(CF::BAR_U + w - 1, 64);
-      }
-#pragma unroll
-      for (int q = 1; q < WMT; ++q) update(q);
-      // (5) refresh the node-7 replica of lane kq = 0: node 0 of the right neighbour
-      if (w < W - 1) {
-        nbar_sync(CF::BAR_U + w, 64);
-        if (lane == 28) right = xU[w + 1];
-      }
-      if (!last) {
+        for (int q = 0; q + 1 < WMT; ++q) mtile_F(q);
+        // (3) interface node 0 of element e: + row 7 of element e-1 (lane kq = 0 holds both)
+        if (w > 0) {
+          nbar_sync(CF::BAR_F + w - 1, 64);
+          if (lane == 0) left = xF[w - 1];
+        } else if (lane == 0) {
+          left = 0.0;                             // tile edge: ghost element, left incomplete
+        }
         if (kq == 0) {
 #pragma unroll
-          for (int q = 0; q + 1 < WMT; ++q) U[q][1] = U[q + 1][0];
-          U[WMT - 1][1] = right;
+          for (int q = WMT - 1; q > 0; --q) F[q][0] = __dadd_rn(F[q - 1][1], F[q][0]);
+          F[0][0] = __dadd_rn(left, F[0][0]);
         }
-        if (STG) put(U, A.stages[st]);            // stage state U_{st+1}, owned nodes
+        // (4) stage update, m-tile 0 first: its node 0 is what the left warp waits for.  The
+        // pairwise barriers also run after the last stage: warp w may arrive on BAR_F + w of the
+        // next stage only after warp w+1 has passed this stage's sync on it (otherwise two of
+        // w's arrivals could complete one barrier generation)
+        update(0);
+        double right = __shfl_down_sync(0xffffffffu, U[0][0], 4);
+        if (w > 0) {
+          if (!last && lane == 0) xU[w] = U[0][0];
+          if (!RF_BAR_NA) __syncwarp();
+          nbar_arrive(CF::BAR_U + w - 1, 64);
+        }
+#pragma unroll
+        for (int q = 1; q < WMT; ++q) update(q);
+        // (5) refresh the node-7 replica of lane kq = 0: node 0 of the right neighbour
+        if (w < W - 1) {
+          nbar_sync(CF::BAR_U + w, 64);
+          if (lane == 28) right = xU[w + 1];
+        }
+        if (!last) {
+          if (kq == 0) {
+#pragma unroll
+            for (int q = 0; q + 1 < WMT; ++q) U[q][1] = U[q + 1][0];
+            U[WMT - 1][1] = right;
+          }
+          if (STG) put(U, A.stages[st]);            // stage state U_{st+1}, owned nodes
+        }
+      } else {
+        // (1) the warp's last m-tile first: its raw row 7 is what the right warp waits for
+        mtile_F(WMT - 1);
+        double left = __shfl_up_sync(0xffffffffu, F[WMT - 1][1], 4);
+        if (w < W - 1) {
+          if (lane == 28) xF[xpar * 8 + w] = F[WMT - 1][1];
+          if (!RF_BAR_NA) __syncwarp();
+          nbar_arrive(CF::BAR_F + w, 64);
+        }
+        // (2) the other m-tiles
+#pragma unroll
+        for (int q = 0; q + 1 < WMT; ++q) mtile_F(q);
+        // (3) ONE pairwise exchange per stage (as in tile_adj_rf_kernel): raw row 7 of the left
+        // warp's last element, raw row 0 of the right warp's first; the interface sum of
+        // elements e-1 | e (row 7 + row 0, raw, in this order) is formed both by the owner of
+        // node 0 of e and by the node-7 replica of e-1, so the replica's next stage state is
+        // bitwise the owner's and no exchange of updated states is needed.  Barrier order:
+        // arrive BAR_F+w, sync BAR_F+w-1, arrive BAR_U+w-1, sync BAR_U+w (no warp can arrive
+        // twice on one barrier generation); slots double-buffered by stage parity.
+        double rawr = __shfl_down_sync(0xffffffffu, F[0][0], 4);
+        if (w > 0) {
+          nbar_sync(CF::BAR_F + w - 1, 64);
+          if (lane == 0) left = xF[xpar * 8 + w - 1];
+          if (lane == 0) xU[xpar * 8 + w] = F[0][0];
+          if (!RF_BAR_NA) __syncwarp();
+          nbar_arrive(CF::BAR_U + w - 1, 64);
+        } else if (lane == 0) {
+          left = 0.0;                             // tile edge: ghost element, left incomplete
+        }
+        if (kq == 0) {
+#pragma unroll
+          for (int q = WMT - 1; q > 0; --q) F[q][0] = __dadd_rn(F[q - 1][1], F[q][0]);
+          F[0][0] = __dadd_rn(left, F[0][0]);
+          if (!last) {                            // replicas inside the lane: the same sums
+#pragma unroll
+            for (int q = 0; q + 1 < WMT; ++q) F[q][1] = F[q + 1][0];
+          }
+        }
+        // (4) stage update; the last m-tile's replica needs the right warp's raw row 0
+#pragma unroll
+        for (int q = 0; q + 1 < WMT; ++q) update(q);
+        if (w < W - 1) {
+          nbar_sync(CF::BAR_U + w, 64);
+          if (lane == 28) rawr = xU[xpar * 8 + w + 1];
+        }
+        if (!last && kq == 0) F[WMT - 1][1] = __dadd_rn(F[WMT - 1][1], rawr);
+        update(WMT - 1);
+        xpar ^= 1;
+        if (!last && STG) put(U, A.stages[st]);   // stage state U_{st+1}, owned nodes
       }
     }
 #pragma unroll
@@ -573,15 +633,12 @@ __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
         left = 0.0;
       }
       if (kq == 0) {
-        double rp[WMT];
-#pragma unroll
-        for (int q = 0; q + 1 < WMT; ++q) rp[q] = __dadd_rn(R[q][1], R[q + 1][0]);
 #pragma unroll
         for (int q = WMT - 1; q > 0; --q) R[q][0] = __dadd_rn(R[q - 1][1], R[q][0]);
         R[0][0] = __dadd_rn(left, R[0][0]);
-        if (refresh) {
+        if (refresh) {                          // replicas inside the lane: the same sums
 #pragma unroll
-          for (int q = 0; q + 1 < WMT; ++q) R[q][1] = rp[q];
+          for (int q = 0; q + 1 < WMT; ++q) R[q][1] = R[q + 1][0];
         }
       }
 #pragma unroll
