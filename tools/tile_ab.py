@@ -39,6 +39,7 @@ for variant in [int(v) for v in (sys.argv[2].split(",") if len(sys.argv) > 2 els
          "fwd_us": t(lambda: op.launch_rk_step(u, o, dt, "rk4")),
          "fwd_fast_us": t(lambda: op.launch_rk_step(u, o, dt, "rk4", flag=slots.data_ptr())),
          "fwd_st_us": t(lambda: op.launch_rk_step_stages(u, o, st, dt, "rk4")),
+         "fwd_st_fast_us": t(lambda: op.launch_rk_step_stages(u, o, st, dt, "rk4", flag=slots.data_ptr())),
          "adj_us": t(lambda: op.launch_adj_step(u, lam, o, dt, "rk4")),
          "adj_fast_us": t(lambda: op.launch_adj_step(u, lam, o, dt, "rk4", flag=slots.data_ptr())),
          "adj_st_fast_us": t(lambda: op.launch_adj_step_stages(u, st, lam, o, dt, "rk4", flag=slots.data_ptr())),
