@@ -151,6 +151,14 @@ int sem1d_ens_forward(const sem1d_plan* plan, const double* u0, double* traj, do
 int sem1d_ens_adjoint(const sem1d_plan* plan, const double* traj, const double* lam_in,
                       double* lam_out, const double* dts, int nsteps, int scheme, int* flags,
                       void* stream);
+/* The same sweep with a choice of checks.  check = 1 is sem1d_ens_adjoint: every stage's
+ * cotangent is classified (SEM1D_FLAG_INPUT2_NONFINITE).  check = 0 tests only lam_out
+ * (SEM1D_FLAG_STEP_NONFINITE; a non-finite cotangent anywhere in the sweep reaches lam_out
+ * through the J^T terms): a caller re-runs a flagged problem set with check = 1 to tell a
+ * non-finite cotangent (the reference's NumericFailure) from a final overflow. */
+int sem1d_ens_adjoint_ex(const sem1d_plan* plan, const double* traj, const double* lam_in,
+                         double* lam_out, const double* dts, int nsteps, int scheme, int check,
+                         int* flags, void* stream);
 
 /* Temporally blocked steps for large periodic rings (batch 1, N+1 in
  * {8,16,24,32}, at least two 256/128-element tiles): ONE launch per explicit

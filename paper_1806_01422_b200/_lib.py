@@ -66,6 +66,8 @@ SIGNATURES = {
                                   c_void_p, c_void_p]),
     "sem1d_ens_adjoint": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int,
                                   c_void_p, c_void_p]),
+    "sem1d_ens_adjoint_ex": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_int, c_int,
+                                     c_void_p, c_void_p]),
     "sem1d_step_supported": (c_int, [c_void_p]),
     "sem1d_step_stages_supported": (c_int, [c_void_p]),
     "sem1d_rk_step_stages": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int, c_void_p,

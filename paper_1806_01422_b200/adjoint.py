@@ -104,6 +104,26 @@ class AdjointEngine:
         op.counters["jact"] += s
 
 
+def resolve_ensemble_flags(op, cfg, fwd, lam_terminal, word):
+    """An outputs-only ensemble sweep flagged a problem: classify it with a re-run of the
+    sweep under the per-stage cotangent checks (counters untouched) and raise the reference's
+    NumericFailure if a cotangent was non-finite; a flag from an overflow of the final
+    gradient alone returns (the reference raises only when a later apply reads it)."""
+    import torch
+    word = int(word)
+    if not word & _lib.SEM1D_FLAG_INPUT2_NONFINITE:
+        saved = dict(op.counters)
+        lam_in, _ = op.field(lam_terminal, "cotangent")
+        flags = torch.zeros(op.batch, dtype=torch.int32, device=op.device)
+        op.launch_ens_adjoint(fwd.trajectory, lam_in.contiguous(), op.empty(), fwd.dts_device, fwd.n_steps,
+                              cfg.scheme, flags, check=True)
+        word = int(flags.max())
+        op.counters.clear()
+        op.counters.update(saved)
+    if word & _lib.SEM1D_FLAG_INPUT2_NONFINITE:
+        raise NumericFailure("cotangent contains NaN/Inf")
+
+
 def adjoint_engine_for(op, scheme):
     cache = op.__dict__.setdefault("_adj_engines", {})
     e = cache.get(scheme)
@@ -320,13 +340,16 @@ def gradient(op, cfg, fwd, schedule, u_ref):
     return j, sweep(op, cfg, fwd, schedule, lam)
 
 
-def ensemble_sweep(op, cfg, fwd, lam_terminal, defer_checks=False):
+def ensemble_sweep(op, cfg, fwd, lam_terminal, defer_checks=False, check=False):
     """Backward sweep of a batch of rings over a trajectory from
     ``timeloop.integrate_ensemble`` -- one CTA per ring, every step in shared memory
     (sem1d_ens_adjoint).  Same recurrence as :func:`sweep` with store-all; the stage
     adjoints are accumulated as lam + (l_s + ... + l_1) instead of ((lam + l_1) + ...).
-    ``defer_checks``: returns (gradient, per-problem flag words on the device) without a
-    host sync; the caller raises NumericFailure("cotangent ...") for a nonzero word."""
+    The sweep tests only its outputs; a flagged sweep is re-run with the classifying check
+    (``check=True``, every stage's cotangent) and raises NumericFailure("cotangent ...") only
+    if a cotangent was non-finite -- a final overflow alone is returned, as the reference's
+    sweep would.  ``defer_checks``: returns (gradient, per-problem flag words on the device)
+    without a host sync; the caller resolves them (:func:`resolve_ensemble_flags`)."""
     import torch
     traj = getattr(fwd, "trajectory", None)
     if traj is None:
@@ -335,9 +358,9 @@ def ensemble_sweep(op, cfg, fwd, lam_terminal, defer_checks=False):
     lam_out = op.empty()
     flags = torch.zeros(op.batch, dtype=torch.int32, device=op.device)
     op.launch_ens_adjoint(traj, lam_in.contiguous(), lam_out, fwd.dts_device, fwd.n_steps,
-                          cfg.scheme, flags)
+                          cfg.scheme, flags, check=check)
     if not defer_checks and int(flags.max()):
-        raise NumericFailure("cotangent contains NaN/Inf")
+        resolve_ensemble_flags(op, cfg, fwd, lam_in, flags.max())
     s = len(TABLEAUX[cfg.scheme][1])
     op.counters["rhs"] += (s - 1) * fwd.n_steps
     op.counters["jact"] += s * fwd.n_steps

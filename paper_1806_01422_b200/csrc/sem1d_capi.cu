@@ -628,6 +628,12 @@ int sem1d_ens_forward(const sem1d_plan* plan, const double* u0, double* traj, do
 int sem1d_ens_adjoint(const sem1d_plan* plan, const double* traj, const double* lam_in,
                       double* lam_out, const double* dts, int nsteps, int scheme, int* flags,
                       void* stream) {
+  return sem1d_ens_adjoint_ex(plan, traj, lam_in, lam_out, dts, nsteps, scheme, 1, flags, stream);
+}
+
+int sem1d_ens_adjoint_ex(const sem1d_plan* plan, const double* traj, const double* lam_in,
+                         double* lam_out, const double* dts, int nsteps, int scheme, int check,
+                         int* flags, void* stream) {
   DeviceGuard guard_(plan ? plan->device : -1);
   if (!valid_burgers(plan) || !traj || !lam_in || !lam_out || !dts || !flags || nsteps < 0)
     return fail(SEM1D_EINVAL, "sem1d_ens_adjoint: bad argument");
@@ -635,6 +641,7 @@ int sem1d_ens_adjoint(const sem1d_plan* plan, const double* traj, const double* 
   std::memset(&a, 0, sizeof(a));
   if (!make_tableau(scheme, a.tab)) return fail(SEM1D_EINVAL, "sem1d_ens_adjoint: unknown scheme");
   a.traj = traj; a.lam_in = lam_in; a.lam_out = lam_out; a.dts = dts; a.nsteps = nsteps; a.flags = flags;
+  a.check = check ? 1 : 0;
   cudaError_t e = dispatch_ens_adjoint(plan, a, static_cast<cudaStream_t>(stream));
   if (e == cudaErrorNotSupported)
     return fail(SEM1D_EINVAL, "sem1d_ens_adjoint: ring too large for one CTA (needs E*(N+1) <= 1024, "

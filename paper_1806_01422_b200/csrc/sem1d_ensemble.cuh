@@ -23,6 +23,9 @@ namespace sem1d {
 #ifndef TILE_PRE
 #define TILE_PRE 1
 #endif
+#ifndef ENS_ADJ_NOCHK
+#define ENS_ADJ_NOCHK 0   // timing experiment only: no cotangent checks in the ensemble adjoint
+#endif
 #ifndef SEM1D_FIN_INT
 #define SEM1D_FIN_INT 1
 #endif
@@ -464,13 +467,15 @@ struct EnsAdjArgs {
   int nsteps;
   int* flags;
   Tableau tab;
+  int check;              // 1: classify every stage's cotangent (INPUT2 bit); 0: test only lam_out
+                          // (STEP bit; the caller re-runs a flagged sweep with check = 1)
 };
 
 // Backward sweep of one ring per CTA (adjoint.py:54-61 generalised, every step in
 // shared memory): stage states recomputed from the stored u_n (s-1 F applies), then
 // l_i = dt J^T(U_i)(b_i lam + sum_{j>i} a_ji l_j) for i = s-1..0 and
 // lam <- lam + (l_{s-1} + ... + l_0).
-template <int N, int WMT_MAX, bool ILV, int SCH>
+template <int N, int WMT_MAX, bool ILV, int SCH, bool CHK = true>
 __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
     ens_adjoint_kernel(const __grid_constant__ Consts<N> C, const Geo G, const EnsAdjArgs A) {
   constexpr int KC = EnsCfg<N>::KC, NT = EnsCfg<N>::NT;
@@ -622,7 +627,7 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
 #pragma unroll
     for (int q = 0; q < WMT_MAX; ++q) {
       const int mt = warp * WMT_MAX + q;
-      if (mt >= mt_total) break;
+      if (ENS_ADJ_NOCHK || !CHK || mt >= mt_total) break;
 #pragma unroll
       for (int kc = 0; kc < KC; ++kc) {
         const int j = 4 * kc + kq;
@@ -662,7 +667,7 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
             if (g == 0) slam[ndof] = lv;
           } else {
             const double z = zval(i - 1, g, q, kc);
-            fin |= nonfinite_bit(z);
+            if (!ENS_ADJ_NOCHK && CHK) fin |= nonfinite_bit(z);
             zdst[g] = z;
             if (g == 0) zdst[ndof] = z;
           }
@@ -677,8 +682,13 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
     }
   }
   double* lo = A.lam_out + b * G.ndof;
-  for (int k = tid; k < ndof; k += THREADS) lo[k] = slam[k];
-  if (fin) atomicOr(&A.flags[b], SEM1D_FLAG_INPUT2_NONFINITE);
+  unsigned bad_out = 0u;
+  for (int k = tid; k < ndof; k += THREADS) {
+    lo[k] = slam[k];
+    if (!CHK) bad_out |= nonfinite_bit(slam[k]);
+  }
+  if (fin || bad_out)
+    atomicOr(&A.flags[b], (fin ? SEM1D_FLAG_INPUT2_NONFINITE : 0) | (bad_out ? SEM1D_FLAG_STEP_NONFINITE : 0));
 }
 
 template <int N>

@@ -259,9 +259,14 @@ cudaError_t launch_ens_adjoint(const PlanView& p, const EnsAdjArgs& a, cudaStrea
     if (p.geo.periodic && p.geo.E % 8 == 0 && p.geo.E / 8 <= W * WMT && smem <= 227 * 1024 &&
         p.geo.E * (N + 1) > 1024) {
       const bool ilv = ENS_ILV && p.geo.E % (8 * WMT) == 0;
-      auto kern = a.tab.s == 4 ? (ilv ? ens_adjoint_kernel<N, WMT, true, 2> : ens_adjoint_kernel<N, WMT, false, 2>)
-                : a.tab.s == 3 ? (ilv ? ens_adjoint_kernel<N, WMT, true, 1> : ens_adjoint_kernel<N, WMT, false, 1>)
-                               : (ilv ? ens_adjoint_kernel<N, WMT, true, 0> : ens_adjoint_kernel<N, WMT, false, 0>);
+      // a.check = 0: outputs-only form (the caller re-runs a flagged sweep with check = 1)
+      auto pick = [&](auto chk) {
+        constexpr bool K = decltype(chk)::value;
+        return a.tab.s == 4 ? (ilv ? ens_adjoint_kernel<N, WMT, true, 2, K> : ens_adjoint_kernel<N, WMT, false, 2, K>)
+             : a.tab.s == 3 ? (ilv ? ens_adjoint_kernel<N, WMT, true, 1, K> : ens_adjoint_kernel<N, WMT, false, 1, K>)
+                            : (ilv ? ens_adjoint_kernel<N, WMT, true, 0, K> : ens_adjoint_kernel<N, WMT, false, 0, K>);
+      };
+      auto kern = a.check ? pick(std::true_type{}) : pick(std::false_type{});
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
       kern<<<(unsigned)p.batch, EnsCfg<N, W>::THREADS, smem, s>>>(

@@ -354,12 +354,14 @@ class SemOperator(ComposedStages):
             u_final.data_ptr(), dts_dev.data_ptr(), int(nsteps), code, flags.data_ptr(),
             self._stream()), "sem1d_ens_forward")
 
-    def launch_ens_adjoint(self, traj, lam_in, lam_out, dts_dev, nsteps, scheme, flags):
+    def launch_ens_adjoint(self, traj, lam_in, lam_out, dts_dev, nsteps, scheme, flags, check=True):
+        """check=False: only lam_out is tested (SEM1D_FLAG_STEP_NONFINITE); a caller re-runs a
+        flagged sweep with check=True to classify non-finite cotangents (sem1d_ens_adjoint_ex)."""
         code = {"euler": 0, "rk3": 1, "rk4": 2}[scheme]
-        _lib.check(_lib.load().sem1d_ens_adjoint(
+        _lib.check(_lib.load().sem1d_ens_adjoint_ex(
             self._plan.handle, traj.data_ptr(), lam_in.data_ptr(), lam_out.data_ptr(),
-            dts_dev.data_ptr(), int(nsteps), code, flags.data_ptr(), self._stream()),
-            "sem1d_ens_adjoint")
+            dts_dev.data_ptr(), int(nsteps), code, 1 if check else 0, flags.data_ptr(), self._stream()),
+            "sem1d_ens_adjoint_ex")
 
     _SCHEME_CODES = {"euler": 0, "rk3": 1, "rk4": 2}
 

@@ -140,10 +140,14 @@ class AssimilationProblem:
             if B > 1:
                 raise StepFailure(f"non-finite state in problems {failed[:8]}")
             return None
-        if np.any(pk[1 + B:1 + 2 * B] != 0.0):
-            op.counters.clear()
-            op.counters.update(after_fwd)
-            raise NumericFailure("cotangent contains NaN/Inf")
+        aw = pk[1 + B:1 + 2 * B]
+        if np.any(aw != 0.0):
+            try:   # the outputs-only sweep flagged: classify, as ensemble_sweep does
+                adjoint.resolve_ensemble_flags(op, self.ts, fwd, lam, int(max(aw)))
+            except NumericFailure:
+                op.counters.clear()
+                op.counters.update(after_fwd)
+                raise
         self.last_forward = fwd
         j = float(pk[1 + 2 * B]) if B == 1 else J
         if host:
