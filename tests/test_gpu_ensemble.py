@@ -153,3 +153,28 @@ def test_register_resident_ensemble_forward_bitwise(cuda, scheme, E):
     assert torch.equal(a.trajectory[:, ok], b.trajectory[:, ok]) and torch.equal(a.u_final[ok], b.u_final[ok])
     assert a.stats["failed"] == b.stats["failed"] == [3]
     assert not bool(torch.isfinite(a.u_final[3]).all()) and not bool(torch.isfinite(b.u_final[3]).all())
+
+
+def test_ensemble_adjoint_outputs_only_check_classifies(cuda):
+    """The ring-resident adjoint (N = 15) tests only its outputs; a flagged sweep is re-run with
+    the per-stage cotangent checks, so a non-finite cotangent still raises NumericFailure with
+    unchanged counters, and the gradient of a clean batch equals the classifying kernel's."""
+    import torch
+    from paper_1806_01422_b200 import adjoint
+    grid = grid_1d(0.0, 20.0, 256, 15)
+    op = sb.SemOperator(grid, sb.PdeCoefficients(0.01), device="cuda:0", batch=3)
+    u0 = configs.fourier_fields(grid, 3, 4, seed=9)
+    ts = sb.TsConfig(scheme="rk4", t0=0.0, t_end=20 * 5e-5, dt=5e-5)
+    fwd = timeloop.integrate_ensemble(op, u0, ts)
+    lam = torch.from_numpy(configs.fourier_fields(grid, 3, 4, seed=10)).cuda()
+    g = adjoint.ensemble_sweep(op, ts, fwd, lam)
+    flags = torch.zeros(3, dtype=torch.int32, device="cuda")
+    g1 = op.empty()
+    op.launch_ens_adjoint(fwd.trajectory, lam, g1, fwd.dts_device, fwd.n_steps, "rk4", flags, check=True)
+    assert torch.equal(g, g1) and int(flags.max()) == 0
+    bad = lam.clone()
+    bad[1, 17] = float("nan")
+    before = dict(op.counters)
+    with pytest.raises(sb.NumericFailure, match="cotangent"):
+        adjoint.ensemble_sweep(op, ts, fwd, bad)
+    assert op.counters == before
