@@ -98,6 +98,49 @@ __device__ __forceinline__ double bfrag_rf(const Consts<7>& C, int mat, int kc, 
   return mat == 0 ? __dmul_rn(C.K[i * 8 + j], __dmul_rn(-C.nu, mi)) : __dmul_rn(C.Dw[i * 8 + j], mi);
 }
 
+// RF_EO: F's two contractions on the reflection (even/odd) split.  The GLL nodes and weights
+// are symmetric about the element midpoint, so K' = -nu M^-1 K is centrosymmetric
+// (K'[7-i][7-j] = K'[i][j]) and Dw' = M^-1 Dw anti-centrosymmetric (Dw'[7-i][7-j] = -Dw'[i][j]);
+// with s_j = u_j + u_{7-j}, d_j = u_j - u_{7-j} (j < 4):
+//   (K'u)_i = (Ke s)_i + (Ko d)_i,  (K'u)_{7-i} = (Ke s)_i - (Ko d)_i,
+//   (Dw'u)_i = (De s)_i + (Do d)_i, (Dw'u)_{7-i} = (Do d)_i - (De s)_i,
+// four 4x4 blocks.  K and Dw share the input u, so ONE DMMA m8n8k4 on s gives Ke s and De s
+// (output columns 2i and 2i+1) and one on d gives Ko d and Do d: 2 DMMAs per m-tile instead of
+// 4, for 6 extra FP64 adds (the DMMA costs 16 sub-partition cycles of the FP64 datapath that
+// DADD/DFMA share, a DADD 2).  The blocks are formed from both halves of the matrices
+// (symmetrised: the host matrices are centrosymmetric to about one ulp only).
+#ifndef RF_EO
+#define RF_EO 1
+#endif
+__device__ __forceinline__ double bfrag_eo(const Consts<7>& C, int par, int lane) {
+  const int c = lane >> 2, j = lane & 3, i = c >> 1;
+  auto mi = [&](int r) { return C.minv[(r == 0 || r == 7) ? 0 : r]; };
+  double a, b;
+  if ((c & 1) == 0) {                           // K' blocks
+    auto kp = [&](int r, int s) { return __dmul_rn(C.K[r * 8 + s], __dmul_rn(-C.nu, mi(r))); };
+    a = __dadd_rn(kp(i, j), kp(7 - i, 7 - j));
+    b = __dadd_rn(kp(i, 7 - j), kp(7 - i, j));
+  } else {                                      // Dw' blocks
+    auto dp = [&](int r, int s) { return __dmul_rn(C.Dw[r * 8 + s], mi(r)); };
+    a = __dsub_rn(dp(i, j), dp(7 - i, 7 - j));
+    b = __dsub_rn(dp(i, 7 - j), dp(7 - i, j));
+  }
+  return 0.25 * (par == 0 ? __dadd_rn(a, b) : __dsub_rn(a, b));
+}
+// F at nodes kq / 7-kq of the lane's element from its two node values (RF_EO split); dw0/dw1
+// receive Dw'u at the two nodes
+__device__ __forceinline__ void f_eo(double u0, double u1, double be, double bo, double& f0, double& f1,
+                                     double& dw0, double& dw1) {
+  const double s = __dadd_rn(u0, u1), d = __dsub_rn(u0, u1);
+  double p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
+  dmma884(p0, p1, s, be);                       // (Ke s)_kq, (De s)_kq
+  dmma884(q0, q1, d, bo);                       // (Ko d)_kq, (Do d)_kq
+  dw0 = __dadd_rn(p1, q1);
+  dw1 = __dsub_rn(q1, p1);
+  f0 = __fma_rn(-u0, dw0, __dadd_rn(p0, q0));
+  f1 = __fma_rn(-u1, dw1, __dsub_rn(p0, q0));
+}
+
 // SCH: compile-time tableau (TabC); STG: also store U_1..U_{s-1}; CHK: classify stage inputs;
 // WMT: m-tiles (8 elements each) per warp; MINB: resident CTAs per SM
 template <int SCH, bool STG, bool CHK, int WMT, int MINB>
@@ -121,8 +164,8 @@ __global__ void __launch_bounds__(32 * RfCfg<WMT>::W, MINB)
   double bk[2], bd[2];
 #pragma unroll
   for (int kc = 0; kc < 2; ++kc) {
-    bk[kc] = bfrag_rf(C, 0, kc, lane);
-    bd[kc] = bfrag_rf(C, 1, kc, lane);
+    bk[kc] = RF_EO ? bfrag_eo(C, kc, lane) : bfrag_rf(C, 0, kc, lane);
+    bd[kc] = RF_EO ? 0.0 : bfrag_rf(C, 1, kc, lane);
   }
   const double dt = A.dt;
   if (tid == 0) {
@@ -253,6 +296,11 @@ __global__ void __launch_bounds__(32 * RfCfg<WMT>::W, MINB)
       }
     };
     auto mtile_F = [&](int q) {
+      if (RF_EO) {
+        double d0, d1;
+        f_eo(U[q][0], U[q][1], bk[0], bk[1], F[q][0], F[q][1], d0, d1);
+        return;
+      }
       double ka = 0.0, kb = 0.0, da = 0.0, db = 0.0;
       dmma884(ka, kb, U[q][0], bk[0]);
       dmma884(da, db, U[q][0], bd[0]);
@@ -509,7 +557,7 @@ __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
   double bk[2], bd[2], jk[2], jt[2];
 #pragma unroll
   for (int kc = 0; kc < 2; ++kc) {
-    bk[kc] = bfrag_rf(C, 0, kc, lane);
+    bk[kc] = RF_EO ? bfrag_eo(C, kc, lane) : bfrag_rf(C, 0, kc, lane);   // (RF_EO: the s / d blocks)
     bd[kc] = bfrag_rf(C, 1, kc, lane);
     jk[kc] = bfrag_rf_adj(C, 0, kc, lane, dt);
     jt[kc] = bfrag_rf_adj(C, 2, kc, lane, dt);
@@ -670,13 +718,18 @@ __global__ void __launch_bounds__(32 * RfAdjCfg<WMT>::W, MINB)
         for (int q = 0; q < WMT; ++q)
           if (CHK) fstate = max(fstate, max(expbits(U[q][0], msk[q][0]), expbits(U[q][1], msk[q][1])));
         auto mtile_F = [&](int q) {
-          double ka = 0.0, kb = 0.0, da = 0.0, db = 0.0;
-          dmma884(ka, kb, U[q][0], bk[0]);
-          dmma884(da, db, U[q][0], bd[0]);
-          dmma884(ka, kb, U[q][1], bk[1]);
-          dmma884(da, db, U[q][1], bd[1]);
-          F[q][0] = __fma_rn(-U[q][0], da, ka);
-          F[q][1] = __fma_rn(-U[q][1], db, kb);
+          double da = 0.0, db = 0.0;
+          if (RF_EO) {
+            f_eo(U[q][0], U[q][1], bk[0], bk[1], F[q][0], F[q][1], da, db);
+          } else {
+            double ka = 0.0, kb = 0.0;
+            dmma884(ka, kb, U[q][0], bk[0]);
+            dmma884(da, db, U[q][0], bd[0]);
+            dmma884(ka, kb, U[q][1], bk[1]);
+            dmma884(da, db, U[q][1], bd[1]);
+            F[q][0] = __fma_rn(-U[q][0], da, ka);
+            F[q][1] = __fma_rn(-U[q][1], db, kb);
+          }
           if (DR) {                               // M^-1 Dw U_st for J^T(U_st)
             sdw[st * SLOT + ((w * WMT + q) * 2 + 0) * 32 + lane] = da;
             sdw[st * SLOT + ((w * WMT + q) * 2 + 1) * 32 + lane] = db;
