@@ -83,6 +83,13 @@ int cuda_fail(cudaError_t e, const char* where) {
   return fail(SEM1D_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
+// bfrag_eo_value<N> for the two degrees that use it (N + 1 a multiple of 16, N <= 32)
+double eo_value(int N, const double* K, const double* Dw, const double* minv, double nu, int sec, int nt,
+                int kc, int l) {
+  return N == 15 ? sem1d::bfrag_eo_value<15>(K, Dw, minv, nu, sec, nt, kc, l)
+                 : sem1d::bfrag_eo_value<31>(K, Dw, minv, nu, sec, nt, kc, l);
+}
+
 // Host image of bfrag_perm (sem1d_device.cuh) for every (mat, nt, kc, lane): a permutation of
 // K / Dw entries, so the device table is bit-identical to the in-kernel construction.
 cudaError_t ensure_frag(const sem1d_plan* p) {
@@ -112,6 +119,19 @@ cudaError_t ensure_frag(const sem1d_plan* p) {
             }
             h[(((size_t)mat * NT + nt) * KC + kc) * 32 + l] = b;
           }
+    // n % 16 == 0: the reflection-split (WS_EO) sections follow, [Ke, Ko, De, Do, Te, To] and the
+    // prescaled [Ke', Ko', De', Do'], each [n/16][n/8][32] (bfrag_eo_value, sem1d_device.cuh)
+    if (n % 16 == 0) {
+      const int NT2 = NT / 2, KC2 = KC / 2;
+      const size_t base = h.size();
+      h.resize(base + (size_t)10 * NT2 * KC2 * 32);
+      for (int sec = 0; sec < 10; ++sec)
+        for (int nt = 0; nt < NT2; ++nt)
+          for (int kc = 0; kc < KC2; ++kc)
+            for (int l = 0; l < 32; ++l)
+              h[base + (((size_t)sec * NT2 + nt) * KC2 + kc) * 32 + l] =
+                  eo_value(p->N, K, Dw, minv, p->nu, sec, nt, kc, l);
+    }
     double* d = nullptr;
     cudaError_t e = cudaMalloc(&d, sizeof(double) * h.size());
     if (e == cudaSuccess) e = cudaMemcpy(d, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice);

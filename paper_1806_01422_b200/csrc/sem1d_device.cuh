@@ -968,11 +968,30 @@ constexpr int ws_outb() { return OP == OP_RHS ? WS_OUTB_F : WS_OUTB_J; }
 #ifndef WS_MINB32_F
 #define WS_MINB32_F 1
 #endif
+// WS_EO (see the comment at bfrag_eo_value): the plain applies at n % 16 == 0 on the reflection
+// split.  F at n = 32 then has half the DMMAs per tile and fewer live registers, and runs 64-element
+// tiles on 4 consumer warps at 3 CTAs/SM (128 registers; config 3: 35.5 us at 1 CTA/SM x 8 warps,
+// 34.5 at 2 x 4, 32.3 at 3 x 4)
+#ifndef WS_EO
+#define WS_EO 1
+#endif
+template <int N, int EPI, int NZ>
+constexpr bool ws_eo() { return WS_EO && (N + 1) % 16 == 0 && EPI == EPI_STORE && NZ < 0; }
+#ifndef WS_MINB32_F_EO
+#define WS_MINB32_F_EO 3
+#endif
+#ifndef WS_CW32_EO
+#define WS_CW32_EO 4
+#endif
+#ifndef WS_ELEMS32_EO
+#define WS_ELEMS32_EO 64
+#endif
 // NZ >= 0: the adjoint-stage variant (J^T with the z = b lam + sum_j a_j l_j prologue and
 // the l / lam_out epilogue, adjoint.py:54-61) reading NZ l_j slabs besides U and lam
-template <int N, int OP, int NZ = -1>
+template <int N, int OP, int NZ = -1, bool EO = false>
 constexpr int ws_minb() {
   if constexpr (NZ >= 0) return ((N + 1) == 32 && NZ > 0) ? 1 : 2;
+  if constexpr (EO && (N + 1) == 32 && OP == OP_RHS) return WS_MINB32_F_EO;
   return ((N + 1) > 16) ? (OP == OP_RHS ? WS_MINB32_F : WS_MINB32)
                         : ((N + 1) == 16 ? 2 : (OP == OP_RHS ? WS_MINB_F8 : (OP == OP_JAC ? WS_MINB_J8 : WS_MINB_JT8)));
 }
@@ -992,23 +1011,89 @@ __device__ __forceinline__ double bfrag_perm(const Consts<N>& C, int mat, int nt
   return C.Dw[j * n + i];
 }
 
+// WS_EO: the plain applies at n % 16 == 0 (N = 15, 31: config 3) on the reflection (even/odd)
+// split of K, Dw and Dw^T.  GLL nodes and weights are symmetric about the element midpoint, so
+// K is centrosymmetric (K[N-i][N-j] = K[i][j]) and Dw, Dw^T anti-centrosymmetric.  With
+// s_j = x_j + x_{N-j}, d_j = x_j - x_{N-j} (j < n/2) every n x n product becomes two
+// (n/2) x (n/2) products on the half-length vectors,
+//   (M x)_i = (Me s)_i + (Mo d)_i,  (M x)_{N-i} = +-((Me s)_i - (Mo d)_i)   (+ K, - Dw / Dw^T),
+// i.e. n^2/32 DMMA m8n8k4 per product instead of n^2/16 -- these kernels are bound by the
+// FP64 datapath the DMMAs occupy, not by HBM -- for n/4 + n/4 extra FP64 adds per lane.  The
+// half blocks are at least one 8-column n-tile wide for n >= 16, so no DMMA column is wasted
+// (n = 8 has 4-wide blocks: only F, whose two matrices share their input, gains there, see
+// sem1d_tilerf.cuh).  Lane (rr, kq) holds node pairs (j, N - j), j = 4kc + kq, kc < n/8, and
+// receives output rows i and N - i for the same set: rows 0 and N both sit in lane kq = 0.
+// Sections of the fragment table: [Ke, Ko, De, Do, Te, To] and, for F on periodic rings,
+// [Ke', Ko', De', Do'] with -nu M^-1_i / M^-1_i folded into row i (T = Dw^T).  The blocks are
+// formed from both halves of each matrix (the host matrices are centrosymmetric to about one
+// ulp only).  RK-stage and adjoint-stage launches keep the full-matrix fragments: their
+// epilogues promise the reference's association (the adaptive Kutta-3 error estimate is a
+// cancellation at the tolerance level).
+
+// sec: 0..5 = Ke, Ko, De, Do, Te, To; 6..9 = the prescaled Ke', Ko', De', Do'
+template <int N>
+__host__ __device__ inline double bfrag_eo_value(const double* K, const double* Dw, const double* minv, double nu,
+                                                 int sec, int nt, int kc, int lane) {
+  constexpr int n = N + 1;
+  const bool pre = sec >= 6;
+  const int mat = pre ? sec - 6 : sec;
+  const int m = mat >> 1, par = mat & 1;
+  const int c = 8 * nt + (lane >> 2);
+  const int i = 4 * (2 * (c >> 3) + (c & 1)) + ((c >> 1) & 3);   // output row, < n/2
+  const int j = 4 * kc + (lane & 3);                             // input node, < n/2
+  // every product / sum rounded once (no FMA contraction), on the host and on the device alike
+#ifdef __CUDA_ARCH__
+#define EO_MUL(x, y) __dmul_rn((x), (y))
+#define EO_ADD(x, y) __dadd_rn((x), (y))
+#define EO_SUB(x, y) __dsub_rn((x), (y))
+#else
+  auto vol = [](double v) { volatile double t = v; return t; };
+#define EO_MUL(x, y) vol((x) * (y))
+#define EO_ADD(x, y) vol((x) + (y))
+#define EO_SUB(x, y) vol((x) - (y))
+#endif
+  auto M = [&](int r, int s) -> double {
+    double b = m == 0 ? K[r * n + s] : (m == 1 ? Dw[r * n + s] : Dw[s * n + r]);
+    if (pre) {
+      const double mi = minv[(r == 0 || r == N) ? 0 : r];
+      const double sc = (m == 0) ? EO_MUL(-nu, mi) : mi;         // one rounding, as bfrag_pre
+      b = EO_MUL(b, sc);
+    }
+    return b;
+  };
+  double a, b;
+  if (m == 0) {
+    a = EO_ADD(M(i, j), M(N - i, N - j));
+    b = EO_ADD(M(i, N - j), M(N - i, j));
+  } else {
+    a = EO_SUB(M(i, j), M(N - i, N - j));
+    b = EO_SUB(M(i, N - j), M(N - i, j));
+  }
+  const double t = par == 0 ? EO_ADD(a, b) : EO_SUB(a, b);
+#undef EO_MUL
+#undef EO_ADD
+#undef EO_SUB
+  return 0.25 * t;
+}
+
 #ifndef WS_ELEMS8_J
 #define WS_ELEMS8_J 256
 #endif
-template <int N, int OP = OP_RHS, int NZ = -1>
+template <int N, int OP = OP_RHS, int NZ = -1, bool EO = false>
 struct WsTile {
   static constexpr int n = N + 1;
   static constexpr bool ADJ = NZ >= 0;
   // inputs staged per tile: u; v / z / lam; the adjoint stage's NZ l_j fields
   static constexpr int NIN = (OP == OP_RHS) ? 1 : 2 + (ADJ ? NZ : 0);
   // consumer warps: n = 32 per operator (see WS_CW32 above), else 8
-  static constexpr int CW = (n == 32) ? (ADJ ? 4 : (OP == OP_JACT ? WS_CW32_JT : (OP == OP_JAC ? WS_CW32_J : WS_CW32))) : 8;
+  static constexpr int CW =
+      (n == 32) ? (ADJ ? 4 : (OP == OP_JACT ? WS_CW32_JT : (OP == OP_JAC ? WS_CW32_J : (EO ? WS_CW32_EO : WS_CW32)))) : 8;
   static constexpr int THREADS = 32 * (CW + 1);
   // the adjoint stage stages up to 4 inputs: half-size tiles keep 2 CTAs/SM at n = 8 and 16
   static constexpr int ELEMS =
       ADJ ? (n == 8 ? 128 : 64)
           : (n == 8) ? (OP == OP_RHS ? WS_ELEMS8 : WS_ELEMS8_J)
-                     : (n == 32 ? (OP == OP_RHS ? WS_ELEMS32 : WS_ELEMS32_J) : MmaTile<N>::ELEMS);
+                     : (n == 32 ? (OP == OP_RHS ? (EO ? WS_ELEMS32_EO : WS_ELEMS32) : WS_ELEMS32_J) : MmaTile<N>::ELEMS);
   static constexpr int WE = ELEMS / CW;                          // elements per consumer warp
   static constexpr int WMT = WE / 8;                             // m-tiles per warp
   static constexpr int NT = n / 8, KC = n / 4;
@@ -1229,17 +1314,175 @@ __device__ __forceinline__ void mtile_compute_multi(const Consts<N>& C, const Ge
   }
 }
 
+// WS_EO form of mtile_compute / mtile_compute_multi (n % 16 == 0): Q m-tiles at once on the
+// half-length sum / difference vectors.  base[q] = slab index of node 0 of the lane's element
+// in m-tile q, eg[q] its global element.  Output: r[q][nt][h] is row 4(2nt + h) + kq for
+// nt < NT/2 and row N - (4(2(nt - NT/2) + h) + kq) above (ws_row_eo).  minv_lo / minv_hi:
+// M^-1 at nodes 4kc + kq and N - (4kc + kq).  LAST: only the n-tile that holds row N.
+#ifndef WS_EO_NTG
+#define WS_EO_NTG 1
+#endif
+// bit OP set: that operator takes its m-tiles one at a time even with the fragments in shared
+// memory (register pressure: 6 half-length vectors and 6 accumulator pairs per m-tile for J^T)
+#ifndef WS_EO_Q1
+#define WS_EO_Q1 7
+#endif
+// A/B only: J^T in two DMMA passes per n-tile group (K zm + Dw^T (u o zm) first, then Dw u on
+// sums and differences formed after the first pass, four half-length vectors live instead of
+// six).  Config 3: 58.6 us against 48.8 in one pass -- two short phases per m-tile leave the
+// FP64 datapath idle more often than the one-pass form's spills cost.
+#ifndef WS_EO_JT2P
+#define WS_EO_JT2P 0
+#endif
+template <int N, int OP, bool EDGE, int Q, class BGet, bool PRE, bool LAST, class WS>
+__device__ __forceinline__ void mtile_compute_eo(const Consts<N>& C, const Geo& G, const double* su, const WS& sw,
+                                                 const int (&base)[Q], const int64_t (&eg)[Q],
+                                                 const double* minv_lo, const double* minv_hi, double mnu,
+                                                 int kq, BGet bget, ws_fin_t& fin_u, ws_fin_t& fin_w,
+                                                 double (&r)[Q][(N + 1) / 8][2]) {
+  constexpr int n = N + 1, NT2 = n / 16, H = n / 8;
+  constexpr int HX = (OP != OP_RHS) ? H : 1, HT = (OP == OP_JACT) ? H : 1;
+  constexpr bool TWOPASS = WS_EO_JT2P && OP == OP_JACT;
+  double us[Q][H], ud[Q][H], xs[Q][HX], xd[Q][HX], ts[Q][HT], td[Q][HT];
+  // the second input at node j of m-tile q as the contraction sees it (J^T: masked z M^-1)
+  auto second = [&](int q, int kc, bool hi, bool acc) -> double {
+    const int j = hi ? N - (4 * kc + kq) : 4 * kc + kq;
+    double w = sw[base[q] + j];
+    if (acc) WS_FIN_ACC(fin_w, w);
+    if (OP == OP_JACT) {
+      const bool eslow = EDGE && (eg[q] == 0 || eg[q] == G.E - 1);
+      w = eslow ? jt_scale<N>(C, w, j, eg[q], G) : __dmul_rn(w, hi ? minv_hi[kc] : minv_lo[kc]);
+    }
+    return w;
+  };
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+#pragma unroll
+    for (int kc = 0; kc < H; ++kc) {
+      const int j = 4 * kc + kq;
+      const double a0 = su[base[q] + j], a1 = su[base[q] + N - j];
+      WS_FIN_ACC(fin_u, a0);
+      WS_FIN_ACC(fin_u, a1);
+      if (!TWOPASS) {
+        us[q][kc] = __dadd_rn(a0, a1);
+        ud[q][kc] = __dsub_rn(a0, a1);
+      }
+      if (OP != OP_RHS) {
+        const double w0 = second(q, kc, false, true), w1 = second(q, kc, true, true);
+        xs[q][kc] = __dadd_rn(w0, w1);
+        xd[q][kc] = __dsub_rn(w0, w1);
+        if (OP == OP_JACT) {
+          const double t0 = __dmul_rn(a0, w0), t1 = __dmul_rn(a1, w1);
+          ts[q][kc] = __dadd_rn(t0, t1);
+          td[q][kc] = __dsub_rn(t0, t1);
+        }
+      }
+    }
+  }
+  constexpr int NTG = (!LAST && NT2 % WS_EO_NTG == 0) ? WS_EO_NTG : 1;
+#pragma unroll
+  for (int nt0 = 0; nt0 < (LAST ? 1 : NT2); nt0 += NTG) {
+    // even (s) and odd (d) parts of K x, Dw u and Dw v / Dw^T (u o zm): 4 or 6 independent
+    // accumulator chains per m-tile and n-tile
+    double ke[NTG][Q][2], ko[NTG][Q][2], pe[NTG][Q][2], po[NTG][Q][2], qe[NTG][Q][2], qo[NTG][Q][2];
+#pragma unroll
+    for (int g = 0; g < NTG; ++g)
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) ke[g][q][h] = ko[g][q][h] = pe[g][q][h] = po[g][q][h] = qe[g][q][h] = qo[g][q][h] = 0.0;
+#pragma unroll
+    for (int kc = 0; kc < H; ++kc) {
+#pragma unroll
+      for (int g = 0; g < NTG; ++g) {
+        const int nt = nt0 + g;
+        const double bke = bget(0, nt, kc), bko = bget(1, nt, kc), bde = bget(2, nt, kc), bdo = bget(3, nt, kc);
+        const double bte = (OP == OP_JACT) ? bget(4, nt, kc) : 0.0, bto = (OP == OP_JACT) ? bget(5, nt, kc) : 0.0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+          dmma884(ke[g][q][0], ke[g][q][1], (OP == OP_RHS) ? us[q][kc] : xs[q][kc], bke);
+          dmma884(ko[g][q][0], ko[g][q][1], (OP == OP_RHS) ? ud[q][kc] : xd[q][kc], bko);
+          if (!TWOPASS) {
+            dmma884(pe[g][q][0], pe[g][q][1], us[q][kc], bde);
+            dmma884(po[g][q][0], po[g][q][1], ud[q][kc], bdo);
+          }
+          if (OP == OP_JAC) {
+            dmma884(qe[g][q][0], qe[g][q][1], xs[q][kc], bde);
+            dmma884(qo[g][q][0], qo[g][q][1], xd[q][kc], bdo);
+          }
+          if (OP == OP_JACT) {
+            dmma884(qe[g][q][0], qe[g][q][1], ts[q][kc], bte);
+            dmma884(qo[g][q][0], qo[g][q][1], td[q][kc], bto);
+          }
+        }
+      }
+    }
+    if (TWOPASS) {
+      if (nt0 == 0) {
+#pragma unroll
+        for (int q = 0; q < Q; ++q)
+#pragma unroll
+          for (int kc = 0; kc < H; ++kc) {
+            const int j = 4 * kc + kq;
+            const double a0 = su[base[q] + j], a1 = su[base[q] + N - j];
+            us[q][kc] = __dadd_rn(a0, a1);
+            ud[q][kc] = __dsub_rn(a0, a1);
+          }
+      }
+#pragma unroll
+      for (int kc = 0; kc < H; ++kc)
+#pragma unroll
+        for (int g = 0; g < NTG; ++g) {
+          const double bde = bget(2, nt0 + g, kc), bdo = bget(3, nt0 + g, kc);
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+            dmma884(pe[g][q][0], pe[g][q][1], us[q][kc], bde);
+            dmma884(po[g][q][0], po[g][q][1], ud[q][kc], bdo);
+          }
+        }
+    }
+#pragma unroll
+    for (int g = 0; g < NTG; ++g)
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int kcp = 2 * (nt0 + g) + h;       // output rows 4kcp + kq and N - (4kcp + kq)
+          // pointwise factors come back from the staged slabs (cheaper than 4 n registers per m-tile)
+          const double u0 = su[base[q] + 4 * kcp + kq], u1 = su[base[q] + N - (4 * kcp + kq)];
+          const double w0 = (OP == OP_RHS) ? 0.0 : second(q, kcp, false, false);
+          const double w1 = (OP == OP_RHS) ? 0.0 : second(q, kcp, true, false);
+          const double k0 = __dadd_rn(ke[g][q][h], ko[g][q][h]), k1 = __dsub_rn(ke[g][q][h], ko[g][q][h]);
+          const double p0 = __dadd_rn(pe[g][q][h], po[g][q][h]), p1 = __dsub_rn(po[g][q][h], pe[g][q][h]);
+          const double q0 = __dadd_rn(qe[g][q][h], qo[g][q][h]), q1 = __dsub_rn(qo[g][q][h], qe[g][q][h]);
+          r[q][nt0 + g][h] = combine_rows<N, OP, PRE>(k0, p0, q0, u0, w0, mnu);
+          r[q][NT2 + nt0 + g][h] = combine_rows<N, OP, PRE>(k1, p1, q1, u1, w1, mnu);
+        }
+  }
+}
+// row held in r[.][nt][h] by lane kq in the WS_EO layout
+template <int N>
+__device__ __forceinline__ int ws_row_eo(int nt, int h, int kq) {
+  constexpr int NT2 = (N + 1) / 16;
+  return nt < NT2 ? 4 * (2 * nt + h) + kq : N - (4 * (2 * (nt - NT2) + h) + kq);
+}
+
 // NZ >= 0 (OP_JACT, EPI_ADJ): one adjoint stage, adjoint.py:54-61 (see WSrc and the EPI_ADJ
 // epilogue below); the same arithmetic and association as apply_kernel<N, OP_JACT, PRO_ADJ, EPI_ADJ>
 template <int N, int OP, int EPI, int STAGES, int NZ = -1>
-__global__ void __launch_bounds__(WsTile<N, OP, NZ>::THREADS, ws_minb<N, OP, NZ>())
+__global__ void __launch_bounds__(WsTile<N, OP, NZ, ws_eo<N, EPI, NZ>()>::THREADS, ws_minb<N, OP, NZ, ws_eo<N, EPI, NZ>()>())
     apply_ws_kernel(const __grid_constant__ Consts<N> C, const Geo G, const Args A,
                     const int tiles_per_ring, const int total_tiles, const double* __restrict__ frag) {
-  using W = WsTile<N, OP, NZ>;
+  using W = WsTile<N, OP, NZ, ws_eo<N, EPI, NZ>()>;
   static_assert(!W::ADJ || (OP == OP_JACT && EPI == EPI_ADJ), "adjoint stage = J^T with the EPI_ADJ epilogue");
   constexpr int ELEMS = W::ELEMS, WE = W::WE, WMT = W::WMT, NT = W::NT, KC = W::KC;
   constexpr int NIN = W::NIN;
   constexpr int NMAT = (OP == OP_JACT) ? 3 : 2;
+  // WS_EO: half-size blocks, [Ke, Ko, De, Do (, Te, To)][NT/2][KC/2][32]; rows 0 and N in lane kq = 0
+  constexpr bool EO = ws_eo<N, EPI, NZ>();
+  constexpr int NMAT_EO = (OP == OP_JACT) ? 6 : 4, NT2 = NT / 2, KC2 = KC / 2;
+  constexpr int BTOT = EO ? NMAT_EO * NT2 * KC2 * 32 : NMAT * NT * KC * 32;   // B fragments of this kernel
+  constexpr int RN_NT = EO ? NT2 : NT - 1, RN_H = EO ? 0 : 1, RN_KQ = EO ? 0 : 3;   // where row N lands
   constexpr int SA = W::SLAB_ALLOC;
   extern __shared__ __align__(16) double smem[];
   double* stage_buf = smem;                                   // [STAGES][NIN][SA]
@@ -1247,7 +1490,7 @@ __global__ void __launch_bounds__(WsTile<N, OP, NZ>::THREADS, ws_minb<N, OP, NZ>
   double* ostage = smem + STAGES * NIN * SA;                  // [OUTB][OUT]
   double* hrow = ostage + OUTB * W::OUT;                      // [STAGES][CW] warp halo rows
   double* bsm = hrow + STAGES * W::CW;                        // B fragments (n = 32)
-  uint64_t* full = reinterpret_cast<uint64_t*>(bsm + (W::B_IN_SMEM ? NMAT * NT * KC * 32 : 0));
+  uint64_t* full = reinterpret_cast<uint64_t*>(bsm + (W::B_IN_SMEM ? BTOT : 0));
   uint64_t* empty = full + STAGES;
   uint64_t* halo = empty + STAGES;
   const int tid = threadIdx.x;
@@ -1381,9 +1624,13 @@ __global__ void __launch_bounds__(WsTile<N, OP, NZ>::THREADS, ws_minb<N, OP, NZ>
   // (plain applies only: the RK-stage epilogue keeps the reference's association, which the
   // adaptive Kutta-3 error estimate -- a cancellation at the tolerance level -- is sensitive to)
   const bool pre = WS_PRE_F && OP == OP_RHS && EPI == EPI_STORE && periodic && frag != nullptr;
-  if (pre) frag += 3 * NT * KC * 32;
+  if (EO) {
+    if (frag) frag += 5 * NT * KC * 32 + (pre ? 6 * NT2 * KC2 * 32 : 0);
+  } else if (pre) {
+    frag += 3 * NT * KC * 32;
+  }
   if (W::B_IN_SMEM) {
-    constexpr int TOT = NMAT * NT * KC * 32, PER = (TOT + W::THREADS - 1) / W::THREADS;
+    constexpr int TOT = BTOT, PER = (TOT + W::THREADS - 1) / W::THREADS;
     if (frag) {                    // every load in flight before the first store
       double t[PER];
 #pragma unroll
@@ -1400,16 +1647,32 @@ __global__ void __launch_bounds__(WsTile<N, OP, NZ>::THREADS, ws_minb<N, OP, NZ>
     for (int q = tid; q < TOT && !frag; q += W::THREADS) {
       {
         const int l = q & 31, r = q >> 5;
+        if constexpr (EO) {
+          const int kc = r % KC2, nt = (r / KC2) % NT2, mat = r / (KC2 * NT2);
+          bsm[q] = bfrag_eo_value<N>(C.K, C.Dw, C.minv, C.nu, mat + (pre ? 6 : 0), nt, kc, l);
+        } else {
         const int kc = r % KC, nt = (r / KC) % NT, mat = r / (KC * NT);
         bsm[q] = bfrag_perm<N>(C, mat, nt, kc, l);
+        }
       }
     }
   }
   __syncthreads();
 
   // per-lane constants (all warps): B fragments, M^-1 at fragment positions
-  double breg[W::B_IN_SMEM ? 1 : NMAT * NT * KC];
-  if (!W::B_IN_SMEM) {
+  double breg[W::B_IN_SMEM ? 1 : (EO ? NMAT_EO * NT2 * KC2 : NMAT * NT * KC)];
+  if (!W::B_IN_SMEM && EO) {
+#pragma unroll
+    for (int mat = 0; mat < NMAT_EO; ++mat)
+#pragma unroll
+      for (int nt = 0; nt < NT2; ++nt)
+#pragma unroll
+        for (int kc = 0; kc < KC2; ++kc)
+          breg[(mat * NT2 + nt) * KC2 + kc] =
+              frag ? __ldg(frag + ((mat * NT2 + nt) * KC2 + kc) * 32 + lane)
+                   : bfrag_eo_value<N>(C.K, C.Dw, C.minv, C.nu, mat + (pre ? 6 : 0), nt, kc, lane);
+  }
+  if (!W::B_IN_SMEM && !EO) {
 #pragma unroll
     for (int mat = 0; mat < NMAT; ++mat)
 #pragma unroll
@@ -1420,6 +1683,10 @@ __global__ void __launch_bounds__(WsTile<N, OP, NZ>::THREADS, ws_minb<N, OP, NZ>
               frag ? __ldg(frag + ((mat * NT + nt) * KC + kc) * 32 + lane) : bfrag_perm<N>(C, mat, nt, kc, lane);
   }
   auto bget = [&](int mat, int nt, int kc) -> double {
+    if (EO) {
+      if (W::B_IN_SMEM) return bsm[((mat * NT2 + nt) * KC2 + kc) * 32 + lane];
+      return breg[(mat * NT2 + nt) * KC2 + kc];
+    }
     if (W::B_IN_SMEM) return bsm[((mat * NT + nt) * KC + kc) * 32 + lane];
     return breg[(mat * NT + nt) * KC + kc];
   };
@@ -1439,6 +1706,21 @@ __global__ void __launch_bounds__(WsTile<N, OP, NZ>::THREADS, ws_minb<N, OP, NZ>
       const int i = 8 * nt + 2 * kq + h;
       minv_p[nt][h] = C.minv[(i == 0 || i == N) ? 0 : i];
     }
+  double minv_hi[KC2 > 0 ? KC2 : 1];                // WS_EO: M^-1 at the mirrored nodes N - (4kc + kq)
+#pragma unroll
+  for (int kc = 0; kc < KC2; ++kc) {
+    const int j = N - (4 * kc + kq);
+    minv_hi[kc] = C.minv[(j == 0 || j == N) ? 0 : j];
+  }
+  // row held in r[nt][h] by this lane, and M^-1 there
+  auto row_of = [&](int nt, int h) -> int {
+    if constexpr (EO) return ws_row_eo<N>(nt, h, kq);
+    else return 4 * (2 * nt + h) + kq;
+  };
+  auto minv_row = [&](int nt, int h) -> double {
+    if constexpr (EO) return nt < NT2 ? minv_a[2 * nt + h] : minv_hi[2 * (nt - NT2) + h];
+    else return minv_a[2 * nt + h];
+  };
   const double minv_if = C.minv[0];
   ws_fin_t fin_u = 0, fin_w = 0;
   bool bad_y = false;
@@ -1470,6 +1752,20 @@ __global__ void __launch_bounds__(WsTile<N, OP, NZ>::THREADS, ws_minb<N, OP, NZ>
         double r[NT][2];
         ws_fin_t du_ = 0, dw_ = 0;
         using BG = decltype(bget);
+        if constexpr (EO) {
+          const int hb[1] = {wq * WE * N};
+          const int64_t he[1] = {ehw};
+          using WSrcT = decltype(sw);
+          if (!periodic && (tl == 0 || tl == tiles_per_ring - 1))
+            mtile_compute_eo<N, OP, true, 1, BG, false, true, WSrcT>(C, G, su, sw, hb, he, minv_a, minv_hi, mnu, kq, bget,
+                                                                    du_, dw_, reinterpret_cast<double (&)[1][NT][2]>(r));
+          else if (pre)
+            mtile_compute_eo<N, OP, false, 1, BG, true, true, WSrcT>(C, G, su, sw, hb, he, minv_a, minv_hi, mnu, kq, bget,
+                                                                    du_, dw_, reinterpret_cast<double (&)[1][NT][2]>(r));
+          else
+            mtile_compute_eo<N, OP, false, 1, BG, false, true, WSrcT>(C, G, su, sw, hb, he, minv_a, minv_hi, mnu, kq, bget,
+                                                                     du_, dw_, reinterpret_cast<double (&)[1][NT][2]>(r));
+        } else
         if (!periodic && (tl == 0 || tl == tiles_per_ring - 1))
           mtile_compute<N, OP, true, BG, false, true>(C, G, su, sw, wq * WE * N, ehw, minv_a, minv_p, mnu, kq, bget,
                                                       du_, dw_, r);
@@ -1479,7 +1775,7 @@ __global__ void __launch_bounds__(WsTile<N, OP, NZ>::THREADS, ws_minb<N, OP, NZ>
         else
           mtile_compute<N, OP, false, BG, false, true>(C, G, su, sw, wq * WE * N, ehw, minv_a, minv_p, mnu, kq, bget,
                                                        du_, dw_, r);
-        if (kq == 3 && hm * 8 + rr < W::CW) hrow[s * W::CW + wq] = (!periodic && eh < 0) ? 0.0 : r[NT - 1][1];
+        if (kq == RN_KQ && hm * 8 + rr < W::CW) hrow[s * W::CW + wq] = (!periodic && eh < 0) ? 0.0 : r[RN_NT][RN_H];
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&halo[s]);
@@ -1519,7 +1815,25 @@ __global__ void __launch_bounds__(WsTile<N, OP, NZ>::THREADS, ws_minb<N, OP, NZ>
         // F 59.9 -> 55.4, J 77.9 -> 73.8 (n = 32); J^T at n = 8 measured slower (126.9 vs 112.2)
         constexpr bool ILVW = WS_ILV && (WMT == 2 || WMT == 4) && !(OP == OP_JACT && N == 7 && !WS_ILV_JT7);
         double rq[WMT][NT][2];
-        if constexpr (MULTI) {
+        if constexpr (EO) {
+          // Q m-tiles per call: all of the warp's with the fragments in shared memory (each
+          // fragment read feeds Q DMMAs), else one at a time
+          constexpr int QE = (MULTI && !(WS_EO_Q1 & (1 << OP))) ? WMT : 1;
+#pragma unroll
+          for (int q0 = 0; q0 < WMT; q0 += QE) {
+            int eb[QE];
+            int64_t ee[QE];
+#pragma unroll
+            for (int q = 0; q < QE; ++q) {
+              const int le = ws_le<WMT, ILVW>(q0 + q, rr);
+              eb[q] = (wel0 + le + 1) * N;
+              ee[q] = e0 + wel0 + le;
+            }
+            mtile_compute_eo<N, OP, EDGE, QE, decltype(bget), PRE, false, decltype(sw)>(
+                C, G, su, sw, eb, ee, minv_a, minv_hi, mnu, kq, bget, fin_u, fin_w,
+                reinterpret_cast<double (&)[QE][NT][2]>(rq[q0]));
+          }
+        } else if constexpr (MULTI) {
           mtile_compute_multi<N, OP, EDGE, WMT, ILVW, decltype(bget), PRE>(C, G, su, sw, (wel0 + 1) * N, e0 + wel0, rr,
                                                                           minv_a, mnu, kq, bget, fin_u, fin_w, rq);
         } else {
@@ -1556,20 +1870,20 @@ __global__ void __launch_bounds__(WsTile<N, OP, NZ>::THREADS, ws_minb<N, OP, NZ>
           for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              const int i = 4 * (2 * nt + h) + kq;     // permuted row (= A column)
+              const int i = row_of(nt, h);             // permuted row (= A column)
               if (live && i != 0 && i != N)
-                wout[le * N + i] = (OP == OP_JACT || PRE) ? r[nt][h] : __dmul_rn(r[nt][h], minv_a[2 * nt + h]);
+                wout[le * N + i] = (OP == OP_JACT || PRE) ? r[nt][h] : __dmul_rn(r[nt][h], minv_row(nt, h));
             }
           if constexpr (!ILVW) {
             const double row0 = r[0][0];              // valid in lanes kq == 0
-            const double rowN = r[NT - 1][1];         // valid in lanes kq == 3
-            double left = __shfl_up_sync(0xffffffffu, rowN, 1);
+            const double rowN = r[RN_NT][RN_H];       // valid in lanes kq == 3 (WS_EO: kq == 0)
+            double left = __shfl_up_sync(0xffffffffu, rowN, RN_KQ == 3 ? 1 : 4);
             if (rr == 0) left = carry;                // q == 0: patched after the halo arrives
-            carry = __shfl_sync(0xffffffffu, rowN, 31);
+            carry = __shfl_sync(0xffffffffu, rowN, 28 + RN_KQ);
             if (kq == 0 && live) put_row0(le, q == 0 && rr == 0, left, row0);
           }
-          if (EDGE && kq == 3 && live && eg == G.E - 1) {  // Dirichlet end node E*N
-            double v = r[NT - 1][1];
+          if (EDGE && kq == RN_KQ && live && eg == G.E - 1) {  // Dirichlet end node E*N
+            double v = r[RN_NT][RN_H];
             if (OP != OP_JACT) v = __dmul_rn(v, C.minv[N + 1]);
             wout[(le + 1) * N] = __dmul_rn(v, 0.0);
           }
@@ -1579,8 +1893,8 @@ __global__ void __launch_bounds__(WsTile<N, OP, NZ>::THREADS, ws_minb<N, OP, NZ>
           // of row ws_left_row(rr); (0, 0) is the warp's first element (halo)
 #pragma unroll
           for (int q = 0; q < WMT; ++q) {
-            const double left = q > 0 ? __shfl_down_sync(0xffffffffu, rq[q - 1][NT - 1][1], 3)
-                                      : __shfl_sync(0xffffffffu, rq[WMT - 1][NT - 1][1], 4 * ws_left_row<WMT>(rr) + 3);
+            const double left = q > 0 ? __shfl_down_sync(0xffffffffu, rq[q - 1][RN_NT][RN_H], RN_KQ)
+                                      : __shfl_sync(0xffffffffu, rq[WMT - 1][RN_NT][RN_H], 4 * ws_left_row<WMT>(rr) + RN_KQ);
             const int le = ws_le<WMT, ILVW>(q, rr);
             if (kq == 0 && le < wnel) put_row0(le, q == 0 && rr == 0, left, rq[q][0][0]);
           }
@@ -1724,26 +2038,32 @@ __global__ void __launch_bounds__(WsTile<N, OP, NZ>::THREADS, ws_minb<N, OP, NZ>
 // Pipeline depth: enough stages that ~100 KB of slab loads can be in flight per
 // CTA (two CTAs per SM for n <= 16), since HBM at ~1.5 us loaded latency needs
 // >= 64 KB outstanding per SM (Little's law).
-template <int N, int OP, int NZ = -1>
+// doubles of the kernel's shared-memory B-fragment table (EO: the reflection-split blocks)
+template <int N, int OP, int NZ, bool EO>
+constexpr int ws_bsm_doubles() {
+  using W = WsTile<N, OP, NZ, EO>;
+  if (!W::B_IN_SMEM) return 0;
+  return EO ? ((OP == OP_JACT) ? 6 : 4) * (W::NT / 2) * (W::KC / 2) * 32 : ((OP == OP_JACT) ? 3 : 2) * W::NT * W::KC * 32;
+}
+
+template <int N, int OP, int NZ = -1, bool EO = false>
 constexpr int ws_stages() {
-  using W = WsTile<N, OP, NZ>;
+  using W = WsTile<N, OP, NZ, EO>;
   constexpr int NIN = W::NIN;
   // shared-memory budget that keeps ws_minb CTAs resident (227 KB per SM)
-  constexpr int mb = ws_minb<N, OP, NZ>();
+  constexpr int mb = ws_minb<N, OP, NZ, EO>();
   constexpr int budget = (mb == 1 ? 180 : (mb == 2 ? 104 : (mb == 3 ? 72 : (mb == 4 ? 54 : 44)))) * 1024;
   constexpr int per = NIN * W::SLAB_ALLOC * 8;
-  constexpr int NMAT = (OP == OP_JACT) ? 3 : 2;
-  constexpr int st = (budget - ws_outb<OP>() * W::OUT * 8 - (W::B_IN_SMEM ? NMAT * W::NT * W::KC * 32 * 8 : 0)) / per;
+  constexpr int st = (budget - ws_outb<OP>() * W::OUT * 8 - ws_bsm_doubles<N, OP, NZ, EO>() * 8) / per;
   return st < 2 ? 2 : (st > 8 ? 8 : st);
 }
 
-template <int N, int OP, int STAGES, int NZ = -1>
+template <int N, int OP, int STAGES, int NZ = -1, bool EO = false>
 constexpr size_t ws_smem_bytes() {
-  using W = WsTile<N, OP, NZ>;
+  using W = WsTile<N, OP, NZ, EO>;
   constexpr int NIN = W::NIN;
-  constexpr int NMAT = (OP == OP_JACT) ? 3 : 2;
   return sizeof(double) * ((size_t)STAGES * NIN * W::SLAB_ALLOC + ws_outb<OP>() * W::OUT + STAGES * W::CW +
-                           (W::B_IN_SMEM ? NMAT * W::NT * W::KC * 32 : 0)) +
+                           ws_bsm_doubles<N, OP, NZ, EO>()) +
          sizeof(uint64_t) * 3 * STAGES;
 }
 

@@ -624,17 +624,19 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
       if (i + 2 < S && TB::a(i + 2, i) != 0.0) z = __fma_rn(__dmul_rn(TB::a(i + 2, i), dt), sk[g], z);
       return z;
     };
+    if constexpr (!ENS_ADJ_NOCHK && CHK) {
 #pragma unroll
-    for (int q = 0; q < WMT_MAX; ++q) {
-      const int mt = warp * WMT_MAX + q;
-      if (ENS_ADJ_NOCHK || !CHK || mt >= mt_total) break;
+      for (int q = 0; q < WMT_MAX; ++q) {
+        const int mt = warp * WMT_MAX + q;
+        if (mt >= mt_total) break;
 #pragma unroll
-      for (int kc = 0; kc < KC; ++kc) {
-        const int j = 4 * kc + kq;
-        if (j == N) continue;
-        const int g = ring_elem<WMT_MAX, ILV>(warp, q, rr) * N + j;
-        const double z = zval(S - 1, g, q, kc);
-        fin |= nonfinite_bit(z);
+        for (int kc = 0; kc < KC; ++kc) {
+          const int j = 4 * kc + kq;
+          if (j == N) continue;
+          const int g = ring_elem<WMT_MAX, ILV>(warp, q, rr) * N + j;
+          const double z = zval(S - 1, g, q, kc);
+          fin |= nonfinite_bit(z);
+        }
       }
     }
     // per stage: J^T apply (its internal barrier ends every read of its z and U_i), then

@@ -110,10 +110,11 @@ static cudaError_t launch_ws(const PlanView& p, const Args& a, cudaStream_t s) {
   if constexpr ((N + 1) % 8 != 0) {
     return cudaErrorInvalidValue;
   } else {
-    using W = WsTile<N, OP, NZ>;
-    constexpr int ST = ws_stages<N, OP, NZ>();
+    constexpr bool EO = ws_eo<N, EPI, NZ>();
+    using W = WsTile<N, OP, NZ, EO>;
+    constexpr int ST = ws_stages<N, OP, NZ, EO>();
     auto kern = apply_ws_kernel<N, OP, EPI, ST, NZ>;
-    constexpr size_t smem = ws_smem_bytes<N, OP, ST, NZ>();
+    constexpr size_t smem = ws_smem_bytes<N, OP, ST, NZ, EO>();
     static DevCache resident;
     int& max_resident = resident.here();
     if (max_resident == 0) {
