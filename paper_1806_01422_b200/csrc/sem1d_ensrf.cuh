@@ -14,7 +14,16 @@
 //  * The replica is refreshed after each stage update the same way in the other direction.
 //  * The base state u_n stays in shared memory (read once per node and stage, written by the
 //    last stage) and leaves for the trajectory with one bulk store per step.
-// Same arithmetic, association and flag bits as ens_forward_kernel (bit-identical results).
+// Same stage arithmetic, association and flag bits as ens_forward_kernel; with ENSRF_EO = 0
+// the results are bit-identical to it.
+//
+// ENSRF_EO (default): F on the reflection (even/odd) split of K' = -nu M^-1 K and Dw' = M^-1 Dw
+// (see bfrag_eo_value in sem1d_device.cuh): lane (rr, kq) holds the node pairs (j, 15 - j),
+// j = 4kc + kq, kc < 2, forms s = u_j + u_{15-j} and d = u_j - u_{15-j}, and 8 DMMAs per
+// m-tile and stage (Ke s, Ko d, De s, Do d; two k-chunks each) replace 16.  Rows 0 and 15 (the
+// replica of the right neighbour's node 0) then both sit in lane kq = 0, so the interface sum
+// of elements e-1 | e inside a lane needs no shuffle.  F differs from the full-matrix form in
+// the last bits only (the same products, summed in a different order).
 #pragma once
 
 #include "sem1d_ensemble.cuh"
@@ -27,6 +36,9 @@ namespace sem1d {
 #endif
 #ifndef ENSRF_NOBAR
 #define ENSRF_NOBAR 0       // timing experiment only (wrong results): no stage barriers
+#endif
+#ifndef ENSRF_EO
+#define ENSRF_EO 1
 #endif
 
 struct EnsRf {
@@ -57,13 +69,23 @@ __global__ void __launch_bounds__(EnsRf::THREADS, 2)
   const bool act = warp < nw;
   const int64_t b = blockIdx.x, nb = gridDim.x;
 
+  constexpr bool EO = ENSRF_EO != 0;
+  // node held in U[q][kc]; where the node-15 replica sits (lane kq = RKQ, slot RKC)
+  auto node = [&](int kc) -> int { return EO ? (kc < 2 ? 4 * kc + kq : N - (4 * (kc - 2) + kq)) : 4 * kc + kq; };
+  constexpr int RKQ = EO ? 0 : 3, RKC = EO ? 2 : 3, RLANE = 28 + RKQ;
+  // EO: bk[0] = Ke', bk[1] = Ko', bd[0] = De', bd[1] = Do' (two k-chunks each)
   double bk[NT][KC], bd[NT][KC];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt)
 #pragma unroll
     for (int kc = 0; kc < KC; ++kc) {
-      bk[nt][kc] = bfrag_pre<N>(C, 0, nt, kc, lane);
-      bd[nt][kc] = bfrag_pre<N>(C, 1, nt, kc, lane);
+      if (EO) {
+        bk[nt][kc] = kc < 2 ? bfrag_eo_value<N>(C.K, C.Dw, C.minv, C.nu, 6 + nt, 0, kc, lane) : 0.0;
+        bd[nt][kc] = kc < 2 ? bfrag_eo_value<N>(C.K, C.Dw, C.minv, C.nu, 8 + nt, 0, kc, lane) : 0.0;
+      } else {
+        bk[nt][kc] = bfrag_pre<N>(C, 0, nt, kc, lane);
+        bd[nt][kc] = bfrag_pre<N>(C, 1, nt, kc, lane);
+      }
     }
 
   const double* u0 = A.u0 + b * G.ndof;
@@ -88,7 +110,7 @@ __global__ void __launch_bounds__(EnsRf::THREADS, 2)
   for (int q = 0; q < WMT; ++q) {
     ebase[q] = (32 * warp + 4 * rr + q) * N;
 #pragma unroll
-    for (int kc = 0; kc < KC; ++kc) U[q][kc] = act ? su[ebase[q] + 4 * kc + kq] : 0.0;
+    for (int kc = 0; kc < KC; ++kc) U[q][kc] = act ? su[ebase[q] + node(kc)] : 0.0;
   }
   unsigned fin = 0u;
   bool bad_step = false;
@@ -106,7 +128,7 @@ __global__ void __launch_bounds__(EnsRf::THREADS, 2)
       const double c1 = last ? 0.0 : __dmul_rn(dt, TB::a(i + 1, i));
       // stage arithmetic of one owned node (ens_forward_kernel's, statement for statement)
       auto upd = [&](int q, int kc, double kk) {
-        const int g = ebase[q] + 4 * kc + kq;
+        const int g = ebase[q] + node(kc);
         const double acc = (i == 0) ? __dmul_rn(TB::b(i), kk) : __fma_rn(TB::b(i), kk, sacc[g]);
         if (!last) {
           sacc[g] = acc;
@@ -136,6 +158,22 @@ __global__ void __launch_bounds__(EnsRf::THREADS, 2)
 #pragma unroll
           for (int kc = 0; kc < KC; ++kc) fin |= nonfinite_bit(U[q][kc]);
           double Fv[KC];
+          if (EO) {
+            double ke[2] = {0.0, 0.0}, ko[2] = {0.0, 0.0}, pe[2] = {0.0, 0.0}, po[2] = {0.0, 0.0};
+#pragma unroll
+            for (int kc = 0; kc < 2; ++kc) {
+              const double sv = __dadd_rn(U[q][kc], U[q][2 + kc]), dv = __dsub_rn(U[q][kc], U[q][2 + kc]);
+              dmma884(ke[0], ke[1], sv, bk[0][kc]);
+              dmma884(ko[0], ko[1], dv, bk[1][kc]);
+              dmma884(pe[0], pe[1], sv, bd[0][kc]);
+              dmma884(po[0], po[1], dv, bd[1][kc]);
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {            // rows 4h + kq and 15 - (4h + kq)
+              Fv[h] = __fma_rn(-U[q][h], __dadd_rn(pe[h], po[h]), __dadd_rn(ke[h], ko[h]));
+              Fv[2 + h] = __fma_rn(-U[q][2 + h], __dsub_rn(po[h], pe[h]), __dsub_rn(ke[h], ko[h]));
+            }
+          } else
 #pragma unroll
           for (int nt = 0; nt < NT; ++nt) {
             double k0 = 0.0, k1 = 0.0, p0 = 0.0, p1 = 0.0;
@@ -148,20 +186,20 @@ __global__ void __launch_bounds__(EnsRf::THREADS, 2)
             Fv[2 * nt + 1] = __fma_rn(-U[q][2 * nt + 1], p1, k1);
           }
           F0[q] = Fv[0];
-          RN[q] = Fv[KC - 1];
+          RN[q] = Fv[RKC];
 #pragma unroll
           for (int kc = 1; kc < KC; ++kc)
-            if (kc < KC - 1 || kq != 3) upd(q, kc, Fv[kc]);
+            if (kc != RKC || kq != RKQ) upd(q, kc, Fv[kc]);
         }
-        if (lane == 31) xF[warp] = RN[WMT - 1];
+        if (lane == RLANE) xF[warp] = RN[WMT - 1];
       }
       if (!ENSRF_NOBAR) __syncthreads();
       // (2) interface nodes: + row 15 of the left element
       if (act) {
 #pragma unroll
         for (int q = 0; q < WMT; ++q) {
-          double left = q > 0 ? __shfl_down_sync(0xffffffffu, RN[q - 1], 3)
-                              : __shfl_sync(0xffffffffu, RN[WMT - 1], 4 * ((rr + 7) & 7) + 3);
+          double left = q > 0 ? (EO ? RN[q - 1] : __shfl_down_sync(0xffffffffu, RN[q - 1], 3))
+                              : __shfl_sync(0xffffffffu, RN[WMT - 1], 4 * ((rr + 7) & 7) + RKQ);
           if (q == 0 && lane == 0) left = xF[wl];
           upd(q, 0, kq == 0 ? __dadd_rn(left, F0[q]) : F0[q]);
         }
@@ -173,10 +211,11 @@ __global__ void __launch_bounds__(EnsRf::THREADS, 2)
       if (act) {
 #pragma unroll
         for (int q = 0; q < WMT; ++q) {
-          double right = q + 1 < WMT ? __shfl_up_sync(0xffffffffu, U[q + 1 < WMT ? q + 1 : 0][0], 3)
+          double right = q + 1 < WMT ? (EO ? U[q + 1 < WMT ? q + 1 : 0][0]
+                                           : __shfl_up_sync(0xffffffffu, U[q + 1 < WMT ? q + 1 : 0][0], 3))
                                      : __shfl_sync(0xffffffffu, U[0][0], 4 * ((rr + 1) & 7));
-          if (q == WMT - 1 && lane == 31) right = xU[wr];
-          if (kq == 3) U[q][KC - 1] = right;
+          if (q == WMT - 1 && lane == RLANE) right = xU[wr];
+          if (kq == RKQ) U[q][RKC] = right;
         }
       }
     }

@@ -129,10 +129,12 @@ def test_cfg4_full_scale_gradients_vs_oracle(cuda):
 
 @pytest.mark.parametrize("scheme", ["rk4", "rk3", "euler"])
 @pytest.mark.parametrize("E", [256, 32, 96, 160])
-def test_register_resident_ensemble_forward_bitwise(cuda, scheme, E):
+def test_register_resident_ensemble_forward_matches_shared_memory_kernel(cuda, scheme, E):
     """N = 15 rings with 32 | E run the register-resident forward sweep (sem1d_ensrf.cuh):
-    trajectory, final state and flag words bit-identical to the shared-memory kernel
-    (sem1d_set_tile_variant(1)) -- same arithmetic and association."""
+    same flag words as the shared-memory kernel (sem1d_set_tile_variant(1)) and the same
+    trajectory and final state to 1e-13 -- the stage arithmetic is the same, and F on the
+    reflection (even/odd) split sums the same products in a different order (built with
+    ENSRF_EO = 0 the two kernels are bit-identical)."""
     from paper_1806_01422_b200 import _lib
     B, steps, dt = 7, 30, 5e-5
     grid = grid_1d(0.0, 20.0, E, 15)
@@ -150,7 +152,9 @@ def test_register_resident_ensemble_forward_bitwise(cuda, scheme, E):
             lib.sem1d_set_tile_variant(0)
     a, b = runs
     ok = [i for i in range(B) if i != 3]            # (NaN payloads may differ: compare finite runs)
-    assert torch.equal(a.trajectory[:, ok], b.trajectory[:, ok]) and torch.equal(a.u_final[ok], b.u_final[ok])
+    scale = float(b.trajectory[:, ok].abs().max())
+    assert float((a.trajectory[:, ok] - b.trajectory[:, ok]).abs().max()) <= 1e-13 * scale
+    assert float((a.u_final[ok] - b.u_final[ok]).abs().max()) <= 1e-13 * scale
     assert a.stats["failed"] == b.stats["failed"] == [3]
     assert not bool(torch.isfinite(a.u_final[3]).all()) and not bool(torch.isfinite(b.u_final[3]).all())
 
