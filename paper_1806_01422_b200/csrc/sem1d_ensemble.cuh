@@ -23,6 +23,11 @@ namespace sem1d {
 #ifndef TILE_PRE
 #define TILE_PRE 1
 #endif
+// the ensemble adjoint at N = 15 on the reflection split (ring_rhs / ring_jact EO): 8 + 12 DMMAs
+// per m-tile for F + J^T instead of 16 + 24
+#ifndef ENS_ADJ_EO
+#define ENS_ADJ_EO 1
+#endif
 #ifndef ENS_ADJ_NOCHK
 #define ENS_ADJ_NOCHK 0   // timing experiment only: no cotangent checks in the ensemble adjoint
 #endif
@@ -119,11 +124,23 @@ __device__ __forceinline__ int ring_left_row(int rr) {
   else return rr > 0 ? rr - 1 : 0;
 }
 
+// Reflection (even/odd) split in the ring kernels (EO template flag of ring_rhs / ring_jact,
+// n % 16 == 0; see bfrag_eo_value in sem1d_device.cuh): lane (rr, kq) holds the node pairs
+// (j, N - j), j = 4kc + kq, kc < n/8.  Slot kc of a per-lane array is node ring_node(kc, kq);
+// rows 0 and N (the replica of the right neighbour's node 0) both sit in lane kq = 0.
+template <int N, bool EO>
+__device__ __forceinline__ int ring_node(int kc, int kq) {
+  constexpr int H = (N + 1) / 8;
+  if constexpr (EO) return kc < H ? 4 * kc + kq : N - (4 * (kc - H) + kq);
+  else return 4 * kc + kq;
+}
+
 // One operator application over the whole ring held in shared memory.
 // src: node values (ndof + 1 entries; entry ndof mirrors node 0 if periodic).
+// EO (PRE only): bget(0..3, nt, kc) = Ke', Ko', De', Do' blocks, nt < NT/2, kc < KC/2.
 // Output: kv[q][kc] = (M^-1-scaled) F at the nodes owned by this lane, for
 // m-tile q of this warp (node 4kc+kq of element 8*(warp + q*W) + rr ... see body).
-template <int N, int WMT_MAX, class BGet, bool WRAP = true, bool PRE = false, bool ILV = false>
+template <int N, int WMT_MAX, class BGet, bool WRAP = true, bool PRE = false, bool ILV = false, bool EO = false>
 __device__ __forceinline__ void ring_rhs(const Consts<N>& C, const Geo& G, const double* src,
                                          double* xfer, BGet bget, const double* minv_a,
                                          double mnu, int warp, int lane,
@@ -132,6 +149,8 @@ __device__ __forceinline__ void ring_rhs(const Consts<N>& C, const Geo& G, const
   // rings: one M^-1 per local row, the interface rows share M^-1_0), so the row value is
   // already the M^-1-scaled F: two FP64 ops per node fewer on the pipe the DMMAs use
   constexpr int KC = (N + 1) / 4, NT = (N + 1) / 8, W = EnsCfg<N>::W;
+  static_assert(!EO || (PRE && (N + 1) % 16 == 0), "reflection split: prescaled fragments, n % 16 == 0");
+  constexpr int RKQ = EO ? 0 : 3;             // lane (kq) that holds row N
   const int kq = lane & 3, rr = lane >> 2;
   const int E = (int)G.E;
   const int mt_total = E / 8;
@@ -144,6 +163,45 @@ __device__ __forceinline__ void ring_rhs(const Consts<N>& C, const Geo& G, const
     if (mt >= mt_total) break;
     const int e = ring_elem<WMT_MAX, ILV>(warp, q, rr);
     const int base = e * N;
+    if constexpr (EO) {
+      constexpr int H = KC / 2, NT2 = NT / 2;
+      double lo[H], hi[H], sv[H], dv[H];
+#pragma unroll
+      for (int kc = 0; kc < H; ++kc) {
+        lo[kc] = src[base + 4 * kc + kq];
+        hi[kc] = src[base + N - (4 * kc + kq)];
+        fin |= nonfinite_bit(lo[kc]) | nonfinite_bit(hi[kc]);
+        sv[kc] = __dadd_rn(lo[kc], hi[kc]);
+        dv[kc] = __dsub_rn(lo[kc], hi[kc]);
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT2; ++nt) {
+        double ke[2] = {0.0, 0.0}, ko[2] = {0.0, 0.0}, pe[2] = {0.0, 0.0}, po[2] = {0.0, 0.0};
+#pragma unroll
+        for (int kc = 0; kc < H; ++kc) {
+          dmma884(ke[0], ke[1], sv[kc], bget(0, nt, kc));
+          dmma884(ko[0], ko[1], dv[kc], bget(1, nt, kc));
+          dmma884(pe[0], pe[1], sv[kc], bget(2, nt, kc));
+          dmma884(po[0], po[1], dv[kc], bget(3, nt, kc));
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {           // rows 4(2nt + h) + kq and their mirrors
+          kv[q][2 * nt + h] = __fma_rn(-lo[2 * nt + h], __dadd_rn(pe[h], po[h]), __dadd_rn(ke[h], ko[h]));
+          kv[q][H + 2 * nt + h] = __fma_rn(-hi[2 * nt + h], __dsub_rn(po[h], pe[h]), __dsub_rn(ke[h], ko[h]));
+        }
+      }
+      const double row0 = kv[q][0], rowN = kv[q][H];   // both in lane kq = 0
+      if (ILV && WMT_MAX > 1) {
+        row0s[q] = row0;
+        rowNs[q] = rowN;
+      } else {
+        double left = __shfl_up_sync(0xffffffffu, rowN, 4);
+        if (rr == 0) left = carry;
+        carry = __shfl_sync(0xffffffffu, rowN, 28);
+        if (q == 0) row0_first = row0;
+        if (kq == 0) kv[q][0] = __dadd_rn(left, row0);
+      }
+    } else {
     double au[KC];
 #pragma unroll
     for (int kc = 0; kc < KC; ++kc) {
@@ -187,20 +245,21 @@ __device__ __forceinline__ void ring_rhs(const Consts<N>& C, const Geo& G, const
       if (q == 0) row0_first = row0;           // lane 0 patches it after the exchange
       if (kq == 0) kv[q][0] = PRE ? __dadd_rn(left, row0) : __dmul_rn(__dadd_rn(left, row0), minv_a[0]);
     }
+    }
   }
   if (ILV && WMT_MAX > 1 && warp * WMT_MAX < mt_total) {
     // left neighbour of (q, rr): (q-1, rr) in lane 4rr+3; of (0, rr): (WMT_MAX-1, ring_left_row)
 #pragma unroll
     for (int q = 0; q < WMT_MAX; ++q) {
-      const double left = q > 0 ? __shfl_down_sync(0xffffffffu, rowNs[q - 1], 3)
-                                : __shfl_sync(0xffffffffu, rowNs[WMT_MAX - 1], 4 * ring_left_row<WMT_MAX>(rr) + 3);
+      const double left = q > 0 ? __shfl_down_sync(0xffffffffu, rowNs[q - 1], RKQ)
+                                : __shfl_sync(0xffffffffu, rowNs[WMT_MAX - 1], 4 * ring_left_row<WMT_MAX>(rr) + RKQ);
       if (kq == 0 && (q > 0 || rr > 0))
         kv[q][0] = PRE ? __dadd_rn(left, row0s[q]) : __dmul_rn(__dadd_rn(left, row0s[q]), minv_a[0]);
     }
     carry = rowNs[WMT_MAX - 1];
     row0_first = row0s[0];
   }
-  if (lane == 31 && warp * WMT_MAX < mt_total) xfer[warp] = carry;   // row N of the warp's last element
+  if (lane == 28 + RKQ && warp * WMT_MAX < mt_total) xfer[warp] = carry;   // row N of the warp's last element
   __syncthreads();
   if (lane == 0 && warp * WMT_MAX < mt_total) {
     // left neighbour of the warp's first element: previous warp (ring wrap from the last;
@@ -239,6 +298,35 @@ __device__ __forceinline__ double bfrag_adj(const Consts<N>& C, int mat, int nt,
   if (mat == 0) return __dmul_rn(b, __dmul_rn(__dmul_rn(-C.nu, dt), mj));
   if (mat == 1) return __dmul_rn(b, __dmul_rn(dt, mi));
   return -__dmul_rn(b, __dmul_rn(dt, mj));     // negated: accumulates into the K chain
+}
+
+// Reflection-split blocks of the ring_jact<PREJ, EO> fragments with dt = 1 (the ensemble adjoint):
+// mat 0 / 1 = even / odd block of K'' = K diag(-nu M^-1) (centrosymmetric), mat 4 / 5 of
+// T'' = -Dw^T diag(M^-1) (anti-centrosymmetric); mat 2 / 3 = De' / Do' of Dw' = diag(M^-1) Dw,
+// the forward kernel's blocks (bfrag_eo_value sections 8, 9).  Formed from both halves of each
+// matrix, as bfrag_eo_value does.
+template <int N>
+__device__ __forceinline__ double bfrag_eo_adj(const Consts<N>& C, int mat, int nt, int kc, int lane) {
+  constexpr int n = N + 1;
+  if (mat == 2 || mat == 3) return bfrag_eo_value<N>(C.K, C.Dw, C.minv, C.nu, 6 + mat, nt, kc, lane);
+  const bool centro = mat < 2;
+  const int par = mat & 1;
+  const int c = 8 * nt + (lane >> 2);
+  const int i = 4 * (2 * (c >> 3) + (c & 1)) + ((c >> 1) & 3);
+  const int j = 4 * kc + (lane & 3);
+  auto M = [&](int r, int s) -> double {
+    const double ms = C.minv[(s == 0 || s == N) ? 0 : s];
+    return centro ? __dmul_rn(C.K[r * n + s], __dmul_rn(-C.nu, ms)) : -__dmul_rn(C.Dw[s * n + r], ms);
+  };
+  double a, b;
+  if (centro) {
+    a = __dadd_rn(M(i, j), M(N - i, N - j));
+    b = __dadd_rn(M(i, N - j), M(N - i, j));
+  } else {
+    a = __dsub_rn(M(i, j), M(N - i, N - j));
+    b = __dsub_rn(M(i, N - j), M(N - i, j));
+  }
+  return 0.25 * (par == 0 ? __dadd_rn(a, b) : __dsub_rn(a, b));
 }
 
 // Compile-time Butcher tableaux of the sweep kernels (same values as make_tableau:
@@ -384,12 +472,18 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_fwd_warps<N>()>::THREADS, ((N + 
 // dt * J^T(M^-1 z) (the M^-1 and dt products ride on the DMMAs)
 // ZS: the stage input is zs * zsrc (the first transposed stage reads b_{s-1} lam straight
 // from the lam slab)
-template <int N, int WMT_MAX, class BGet, bool WRAP = true, bool ILV = false, bool PREJ = false, bool ZS = false>
+// EO (PREJ only): bget(0..5, nt, kc) = K''e, K''o, De', Do', T''e, T''o blocks (bfrag_eo_adj);
+// the even K'' chain also takes T''o td and the odd one T''e ts, so that with A = K''e zs + T''o td
+// and B = K''o zd + T''e ts rows i and N - i of K''z + T''t are A + B and A - B
+template <int N, int WMT_MAX, class BGet, bool WRAP = true, bool ILV = false, bool PREJ = false, bool ZS = false,
+          bool EO = false>
 __device__ __forceinline__ void ring_jact(const Consts<N>& C, const Geo& G, const double* usrc,
                                           const double* zsrc, double* xfer, BGet bget,
                                           double mnu, int warp, int lane,
                                           double (&jv)[WMT_MAX][(N + 1) / 4], double zs = 1.0) {
   constexpr int KC = (N + 1) / 4, NT = (N + 1) / 8;
+  static_assert(!EO || (PREJ && (N + 1) % 16 == 0), "reflection split: prescaled fragments, n % 16 == 0");
+  constexpr int RKQ = EO ? 0 : 3;             // lane (kq) that holds row N
   const int kq = lane & 3, rr = lane >> 2;
   const int mt_total = (int)G.E / 8;
   double carry = 0.0, row0_first = 0.0;
@@ -399,6 +493,53 @@ __device__ __forceinline__ void ring_jact(const Consts<N>& C, const Geo& G, cons
     const int mt = warp * WMT_MAX + q;
     if (mt >= mt_total) break;
     const int base = ring_elem<WMT_MAX, ILV>(warp, q, rr) * N;
+    if constexpr (EO) {
+      constexpr int H = KC / 2, NT2 = NT / 2;
+      double zl[H], zh[H], us[H], ud[H], zs_[H], zd_[H], ts[H], td[H];
+#pragma unroll
+      for (int kc = 0; kc < H; ++kc) {
+        const int j0 = base + 4 * kc + kq, j1 = base + N - (4 * kc + kq);
+        const double u0 = usrc[j0], u1 = usrc[j1];
+        zl[kc] = ZS ? __dmul_rn(zs, zsrc[j0]) : zsrc[j0];
+        zh[kc] = ZS ? __dmul_rn(zs, zsrc[j1]) : zsrc[j1];
+        const double t0 = __dmul_rn(u0, zl[kc]), t1 = __dmul_rn(u1, zh[kc]);
+        us[kc] = __dadd_rn(u0, u1);
+        ud[kc] = __dsub_rn(u0, u1);
+        zs_[kc] = __dadd_rn(zl[kc], zh[kc]);
+        zd_[kc] = __dsub_rn(zl[kc], zh[kc]);
+        ts[kc] = __dadd_rn(t0, t1);
+        td[kc] = __dsub_rn(t0, t1);
+      }
+#pragma unroll
+      for (int nt = 0; nt < NT2; ++nt) {
+        double ca[2] = {0.0, 0.0}, cb[2] = {0.0, 0.0}, pe[2] = {0.0, 0.0}, po[2] = {0.0, 0.0};
+#pragma unroll
+        for (int kc = 0; kc < H; ++kc) {
+          dmma884(ca[0], ca[1], zs_[kc], bget(0, nt, kc));   // K''e zs
+          dmma884(cb[0], cb[1], zd_[kc], bget(1, nt, kc));   // K''o zd
+          dmma884(pe[0], pe[1], us[kc], bget(2, nt, kc));    // De' us
+          dmma884(po[0], po[1], ud[kc], bget(3, nt, kc));    // Do' ud
+          dmma884(cb[0], cb[1], ts[kc], bget(4, nt, kc));    // + T''e ts
+          dmma884(ca[0], ca[1], td[kc], bget(5, nt, kc));    // + T''o td
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          jv[q][2 * nt + h] = __fma_rn(-zl[2 * nt + h], __dadd_rn(pe[h], po[h]), __dadd_rn(ca[h], cb[h]));
+          jv[q][H + 2 * nt + h] = __fma_rn(-zh[2 * nt + h], __dsub_rn(po[h], pe[h]), __dsub_rn(ca[h], cb[h]));
+        }
+      }
+      const double row0 = jv[q][0], rowN = jv[q][H];   // both in lane kq = 0
+      if (ILV && WMT_MAX > 1) {
+        row0s[q] = row0;
+        rowNs[q] = rowN;
+      } else {
+        double left = __shfl_up_sync(0xffffffffu, rowN, 4);
+        if (rr == 0) left = carry;
+        carry = __shfl_sync(0xffffffffu, rowN, 28);
+        if (q == 0) row0_first = row0;
+        if (kq == 0) jv[q][0] = __dadd_rn(left, row0);
+      }
+    } else {
     double au[KC], az[KC], at[KC];
 #pragma unroll
     for (int kc = 0; kc < KC; ++kc) {
@@ -440,18 +581,19 @@ __device__ __forceinline__ void ring_jact(const Consts<N>& C, const Geo& G, cons
       if (q == 0) row0_first = row0;
       if (kq == 0) jv[q][0] = __dadd_rn(left, row0);
     }
+    }
   }
   if (ILV && WMT_MAX > 1 && warp * WMT_MAX < mt_total) {
 #pragma unroll
     for (int q = 0; q < WMT_MAX; ++q) {
-      const double left = q > 0 ? __shfl_down_sync(0xffffffffu, rowNs[q - 1], 3)
-                                : __shfl_sync(0xffffffffu, rowNs[WMT_MAX - 1], 4 * ring_left_row<WMT_MAX>(rr) + 3);
+      const double left = q > 0 ? __shfl_down_sync(0xffffffffu, rowNs[q - 1], RKQ)
+                                : __shfl_sync(0xffffffffu, rowNs[WMT_MAX - 1], 4 * ring_left_row<WMT_MAX>(rr) + RKQ);
       if (kq == 0 && (q > 0 || rr > 0)) jv[q][0] = __dadd_rn(left, row0s[q]);
     }
     carry = rowNs[WMT_MAX - 1];
     row0_first = row0s[0];
   }
-  if (lane == 31 && warp * WMT_MAX < mt_total) xfer[warp] = carry;
+  if (lane == 28 + RKQ && warp * WMT_MAX < mt_total) xfer[warp] = carry;
   __syncthreads();
   if (lane == 0 && warp * WMT_MAX < mt_total) {
     const int wl = (warp == 0) ? (WRAP ? (mt_total - 1) / WMT_MAX : -1) : warp - 1;
@@ -506,9 +648,18 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
   // laid out per lane (in registers the compiler re-reads them from parameter space
   // with lane-divergent indices)
   constexpr bool BSM = ens_adj_bsm<N>();
+  // reflection split (ring_node layout): N = 15 with the fragment table in shared memory
+  constexpr bool EO = ENS_ADJ_EO && N == 15 && BSM && TILE_PRE;
+  constexpr int NT2 = NT / 2, KH = KC / 2;
   double breg[BSM ? 1 : 3 * NT * KC];
   double bpre[(BSM || !TILE_PRE) ? 1 : 2 * NT * KC];
-  if constexpr (BSM) {
+  if constexpr (EO) {
+    // [K''e, K''o, De', Do', T''e, T''o, Ke', Ko'][NT/2][KC/2][32]
+    for (int q = tid; q < 8 * NT2 * KH * 32; q += THREADS) {
+      const int l = q & 31, f = q >> 5, kc = f % KH, nt = (f / KH) % NT2, mat = f / (KH * NT2);
+      sB[q] = mat < 6 ? bfrag_eo_adj<N>(C, mat, nt, kc, l) : bfrag_eo_value<N>(C.K, C.Dw, C.minv, C.nu, mat, nt, kc, l);
+    }
+  } else if constexpr (BSM) {
     for (int q = tid; q < 5 * NT * KC * 32; q += THREADS) {
       const int l = q & 31, f = q >> 5, kc = f % KC, nt = (f / KC) % NT, mat = f / (KC * NT);
       sB[q] = mat < 3 ? bfrag_adj<N>(C, mat, nt, kc, l, 1.0)
@@ -531,11 +682,13 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
     }
   }
   auto bget = [&](int mat, int nt, int kc) -> double {
-    if constexpr (BSM) return sB[((mat * NT + nt) * KC + kc) * 32 + lane];
+    if constexpr (EO) return sB[((mat * NT2 + nt) * KH + kc) * 32 + lane];
+    else if constexpr (BSM) return sB[((mat * NT + nt) * KC + kc) * 32 + lane];
     else return breg[(mat * NT + nt) * KC + kc];
   };
   auto bpget = [&](int mat, int nt, int kc) -> double {
-    if constexpr (BSM) return sB[(((mat + 3) * NT + nt) * KC + kc) * 32 + lane];
+    if constexpr (EO) return sB[(((mat < 2 ? 6 + mat : mat) * NT2 + nt) * KH + kc) * 32 + lane];
+    else if constexpr (BSM) return sB[(((mat + 3) * NT + nt) * KC + kc) * 32 + lane];
     else return TILE_PRE ? bpre[(mat * NT + nt) * KC + kc] : breg[(mat * NT + nt) * KC + kc];
   };
   double minv_a[KC];
@@ -585,7 +738,7 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
     // ---- stage states U_1..U_{S-1} (timeloop.rk3_stages, adjoint.py:56)
 #pragma unroll
     for (int i = 0; i + 1 < S; ++i) {
-      ring_rhs<N, WMT_MAX, decltype(bpget), true, TILE_PRE != 0, ILV>(C, G, Uarr(i), xfer, bpget, minv_a, mnu, warp,
+      ring_rhs<N, WMT_MAX, decltype(bpget), true, TILE_PRE != 0, ILV, EO>(C, G, Uarr(i), xfer, bpget, minv_a, mnu, warp,
                                                                 lane, kv, fin);
       double* dst = Uarr(i + 1);
 #pragma unroll
@@ -594,7 +747,7 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
         if (mt >= mt_total) break;
 #pragma unroll
         for (int kc = 0; kc < KC; ++kc) {
-          const int j = 4 * kc + kq;
+          const int j = ring_node<N, EO>(kc, kq);
           if (j == N) continue;
           const int g = ring_elem<WMT_MAX, ILV>(warp, q, rr) * N + j;
           const double kk = kv[q][kc];
@@ -631,7 +784,7 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
         if (mt >= mt_total) break;
 #pragma unroll
         for (int kc = 0; kc < KC; ++kc) {
-          const int j = 4 * kc + kq;
+          const int j = ring_node<N, EO>(kc, kq);
           if (j == N) continue;
           const int g = ring_elem<WMT_MAX, ILV>(warp, q, rr) * N + j;
           const double z = zval(S - 1, g, q, kc);
@@ -644,10 +797,10 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
 #pragma unroll
     for (int i = S - 1; i >= 0; --i) {
       if (i == S - 1)
-        ring_jact<N, WMT_MAX, decltype(bget), true, ILV, true, true>(C, G, Uarr(i), slam, xfer, bget, mnu, warp, lane,
+        ring_jact<N, WMT_MAX, decltype(bget), true, ILV, true, true, EO>(C, G, Uarr(i), slam, xfer, bget, mnu, warp, lane,
                                                                    kv, TB::b(S - 1));
       else
-        ring_jact<N, WMT_MAX, decltype(bget), true, ILV, true>(C, G, Uarr(i), Uarr(i + 1), xfer, bget, mnu, warp, lane,
+        ring_jact<N, WMT_MAX, decltype(bget), true, ILV, true, false, EO>(C, G, Uarr(i), Uarr(i + 1), xfer, bget, mnu, warp, lane,
                                                              kv);
       double* zdst = Uarr(i);
 #pragma unroll
@@ -656,7 +809,7 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_adj_warps<N>()>::THREADS, 1)
         if (mt >= mt_total) break;
 #pragma unroll
         for (int kc = 0; kc < KC; ++kc) {
-          const int j = 4 * kc + kq;
+          const int j = ring_node<N, EO>(kc, kq);
           if (j == N) continue;
           const int g = ring_elem<WMT_MAX, ILV>(warp, q, rr) * N + j;
           const double l = kv[q][kc];                       // l_i / dt
