@@ -28,6 +28,10 @@ namespace sem1d {
 #ifndef ENS_ADJ_EO
 #define ENS_ADJ_EO 1
 #endif
+// the shared-memory tile step / adjoint-step kernels (N = 15, 31) on the reflection split
+#ifndef TILE_EO
+#define TILE_EO 1
+#endif
 #ifndef ENS_ADJ_NOCHK
 #define ENS_ADJ_NOCHK 0   // timing experiment only: no cotangent checks in the ensemble adjoint
 #endif
@@ -300,26 +304,25 @@ __device__ __forceinline__ double bfrag_adj(const Consts<N>& C, int mat, int nt,
   return -__dmul_rn(b, __dmul_rn(dt, mj));     // negated: accumulates into the K chain
 }
 
-// Reflection-split blocks of the ring_jact<PREJ, EO> fragments with dt = 1 (the ensemble adjoint):
-// mat 0 / 1 = even / odd block of K'' = K diag(-nu M^-1) (centrosymmetric), mat 4 / 5 of
-// T'' = -Dw^T diag(M^-1) (anti-centrosymmetric); mat 2 / 3 = De' / Do' of Dw' = diag(M^-1) Dw,
-// the forward kernel's blocks (bfrag_eo_value sections 8, 9).  Formed from both halves of each
-// matrix, as bfrag_eo_value does.
+// Reflection-split blocks of the ring_jact<PREJ, EO> fragments (bfrag_adj's matrices; the ensemble
+// adjoint passes dt = 1): mat 0 / 1 = even / odd block of K'' = K diag(-nu dt M^-1) (centrosymmetric),
+// mat 2 / 3 of Dw'' = diag(dt M^-1) Dw and mat 4 / 5 of T'' = -Dw^T diag(dt M^-1) (both
+// anti-centrosymmetric).  Formed from both halves of each matrix, as bfrag_eo_value does.
 template <int N>
-__device__ __forceinline__ double bfrag_eo_adj(const Consts<N>& C, int mat, int nt, int kc, int lane) {
+__device__ __forceinline__ double bfrag_eo_adj(const Consts<N>& C, int mat, int nt, int kc, int lane, double dt = 1.0) {
   constexpr int n = N + 1;
-  if (mat == 2 || mat == 3) return bfrag_eo_value<N>(C.K, C.Dw, C.minv, C.nu, 6 + mat, nt, kc, lane);
-  const bool centro = mat < 2;
-  const int par = mat & 1;
+  const int m = mat >> 1, par = mat & 1;
   const int c = 8 * nt + (lane >> 2);
   const int i = 4 * (2 * (c >> 3) + (c & 1)) + ((c >> 1) & 3);
   const int j = 4 * kc + (lane & 3);
+  auto mv = [&](int r) -> double { return C.minv[(r == 0 || r == N) ? 0 : r]; };
   auto M = [&](int r, int s) -> double {
-    const double ms = C.minv[(s == 0 || s == N) ? 0 : s];
-    return centro ? __dmul_rn(C.K[r * n + s], __dmul_rn(-C.nu, ms)) : -__dmul_rn(C.Dw[s * n + r], ms);
+    if (m == 0) return __dmul_rn(C.K[r * n + s], __dmul_rn(__dmul_rn(-C.nu, dt), mv(s)));
+    if (m == 1) return __dmul_rn(C.Dw[r * n + s], __dmul_rn(dt, mv(r)));
+    return -__dmul_rn(C.Dw[s * n + r], __dmul_rn(dt, mv(s)));
   };
   double a, b;
-  if (centro) {
+  if (m == 0) {
     a = __dadd_rn(M(i, j), M(N - i, N - j));
     b = __dadd_rn(M(i, N - j), M(N - i, j));
   } else {
@@ -993,14 +996,30 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
   const double mnu = -C.nu;
   Geo Gt = G;
   Gt.E = TE;
-  double breg[2 * NT * KC];
+  // reflection split (ring_node layout, ring_rhs EO) for n % 16 == 0: Ke', Ko', De', Do' blocks
+  constexpr bool EO = TILE_EO && (N + 1) % 16 == 0 && TILE_PRE;
+  constexpr int NT2 = NT / 2, KH = KC / 2;
+  double breg[EO ? 4 * NT2 * KH : 2 * NT * KC];
+  if constexpr (EO) {
 #pragma unroll
-  for (int mat = 0; mat < 2; ++mat)
+    for (int mat = 0; mat < 4; ++mat)
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+      for (int nt = 0; nt < NT2; ++nt)
 #pragma unroll
-      for (int kc = 0; kc < KC; ++kc) breg[(mat * NT + nt) * KC + kc] = (TILE_PRE ? bfrag_pre<N>(C, mat, nt, kc, lane) : bfrag_perm<N>(C, mat, nt, kc, lane));
-  auto bget = [&](int mat, int nt, int kc) -> double { return breg[(mat * NT + nt) * KC + kc]; };
+        for (int kc = 0; kc < KH; ++kc)
+          breg[(mat * NT2 + nt) * KH + kc] = bfrag_eo_value<N>(C.K, C.Dw, C.minv, C.nu, 6 + mat, nt, kc, lane);
+  } else {
+#pragma unroll
+    for (int mat = 0; mat < 2; ++mat)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int kc = 0; kc < KC; ++kc) breg[(mat * NT + nt) * KC + kc] = (TILE_PRE ? bfrag_pre<N>(C, mat, nt, kc, lane) : bfrag_perm<N>(C, mat, nt, kc, lane));
+  }
+  auto bget = [&](int mat, int nt, int kc) -> double {
+    if constexpr (EO) return breg[(mat * NT2 + nt) * KH + kc];
+    else return breg[(mat * NT + nt) * KC + kc];
+  };
   double minv_a[KC];
 #pragma unroll
   for (int kc = 0; kc < KC; ++kc) {
@@ -1051,7 +1070,7 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
     for (int st = 0; st < TB::s; ++st) {
       if (STG && tid == 0) bulk_wait_read<0>();   // the previous stage's store has read sU
       const double* src = (st == 0) ? su : sU;
-      ring_rhs<N, WMT, decltype(bget), false, TILE_PRE != 0, TILE_ILV != 0>(C, Gt, src, xfer, bget, minv_a, mnu, warp, lane, kv,
+      ring_rhs<N, WMT, decltype(bget), false, TILE_PRE != 0, TILE_ILV != 0, EO>(C, Gt, src, xfer, bget, minv_a, mnu, warp, lane, kv,
                                                             fin);
       const double tb = TB::b(st);
       const bool last = (st + 1 == TB::s);
@@ -1062,7 +1081,7 @@ __global__ void __launch_bounds__(32 * W, tile_minb<N>())
         const int e = ring_elem<WMT, TILE_ILV != 0>(warp, q, rr);
 #pragma unroll
         for (int kc = 0; kc < KC; ++kc) {
-          const int j = 4 * kc + kq;
+          const int j = ring_node<N, EO>(kc, kq);
           if (j == N) continue;
           const int g = e * N + j;
           const double kk = kv[q][kc];
@@ -1161,10 +1180,33 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
   // per lane -- in registers the compiler re-reads them from kernel-parameter space with
   // lane-divergent indices (19x slower)
   constexpr bool BSM = (N + 1) == 32;
-  double breg[BSM ? 1 : 3 * NT * KC];
-  double bpre[(BSM || !TILE_PRE) ? 1 : 2 * NT * KC];
+  // reflection split (ring_node layout, ring_rhs / ring_jact EO) for n % 16 == 0:
+  // [K''e, K''o, Dw''e, Dw''o, T''e, T''o] with dt folded in, and the recompute's [Ke', Ko', De', Do']
+  constexpr bool EO = TILE_EO && (N + 1) % 16 == 0 && TILE_PRE;
+  constexpr int NT2 = NT / 2, KH = KC / 2;
+  double breg[BSM ? 1 : (EO ? 6 * NT2 * KH : 3 * NT * KC)];
+  double bpre[(BSM || !TILE_PRE) ? 1 : (EO ? 4 * NT2 * KH : 2 * NT * KC)];
   double* sB = bar_smem_end<N>(reinterpret_cast<double*>(bar + 2));
-  if constexpr (BSM) {
+  if constexpr (EO && BSM) {
+    for (int q = tid; q < 10 * NT2 * KH * 32; q += blockDim.x) {
+      const int l = q & 31, f = q >> 5, kc = f % KH, nt = (f / KH) % NT2, mat = f / (KH * NT2);
+      sB[q] = mat < 6 ? bfrag_eo_adj<N>(C, mat, nt, kc, l, A.dt) : bfrag_eo_value<N>(C.K, C.Dw, C.minv, C.nu, mat, nt, kc, l);
+    }
+  } else if constexpr (EO) {
+#pragma unroll
+    for (int mat = 0; mat < 6; ++mat)
+#pragma unroll
+      for (int nt = 0; nt < NT2; ++nt)
+#pragma unroll
+        for (int kc = 0; kc < KH; ++kc) breg[(mat * NT2 + nt) * KH + kc] = bfrag_eo_adj<N>(C, mat, nt, kc, lane, A.dt);
+#pragma unroll
+    for (int mat = 0; mat < 4; ++mat)
+#pragma unroll
+      for (int nt = 0; nt < NT2; ++nt)
+#pragma unroll
+        for (int kc = 0; kc < KH; ++kc)
+          bpre[(mat * NT2 + nt) * KH + kc] = bfrag_eo_value<N>(C.K, C.Dw, C.minv, C.nu, 6 + mat, nt, kc, lane);
+  } else if constexpr (BSM) {
     for (int q = tid; q < 5 * NT * KC * 32; q += blockDim.x) {
       const int l = q & 31, f = q >> 5, kc = f % KC, nt = (f / KC) % NT, mat = f / (KC * NT);
       sB[q] = mat < 3 ? bfrag_adj<N>(C, mat, nt, kc, l, A.dt)
@@ -1187,11 +1229,15 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
     }
   }
   auto bget = [&](int mat, int nt, int kc) -> double {
-    if constexpr (BSM) return sB[((mat * NT + nt) * KC + kc) * 32 + lane];
+    if constexpr (EO && BSM) return sB[((mat * NT2 + nt) * KH + kc) * 32 + lane];
+    else if constexpr (EO) return breg[(mat * NT2 + nt) * KH + kc];
+    else if constexpr (BSM) return sB[((mat * NT + nt) * KC + kc) * 32 + lane];
     else return breg[(mat * NT + nt) * KC + kc];
   };
   auto bpget = [&](int mat, int nt, int kc) -> double {
-    if constexpr (BSM) return sB[(((mat + 3) * NT + nt) * KC + kc) * 32 + lane];
+    if constexpr (EO && BSM) return sB[(((6 + mat) * NT2 + nt) * KH + kc) * 32 + lane];
+    else if constexpr (EO) return bpre[(mat * NT2 + nt) * KH + kc];
+    else if constexpr (BSM) return sB[(((mat + 3) * NT + nt) * KC + kc) * 32 + lane];
     else return TILE_PRE ? bpre[(mat * NT + nt) * KC + kc] : breg[(mat * NT + nt) * KC + kc];
   };
   double minv_a[KC];
@@ -1245,7 +1291,7 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
       for (int i = 1; i < S; ++i) Uarr(i)[LEN - 1] = su[LEN - 1];   // never-owned last node
 #pragma unroll
     for (int i = 0; i + 1 < S && !LD; ++i) {
-      ring_rhs<N, WMT, decltype(bpget), false, TILE_PRE != 0, TILE_ILV != 0>(C, Gt, Uarr(i), xfer, bpget, minv_a, mnu, warp, lane,
+      ring_rhs<N, WMT, decltype(bpget), false, TILE_PRE != 0, TILE_ILV != 0, EO>(C, Gt, Uarr(i), xfer, bpget, minv_a, mnu, warp, lane,
                                                               kv, fin);
       double* dst = Uarr(i + 1);
 #pragma unroll
@@ -1253,7 +1299,7 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
         const int e = ring_elem<WMT, TILE_ILV != 0>(warp, q, rr);
 #pragma unroll
         for (int kc = 0; kc < KC; ++kc) {
-          const int j = 4 * kc + kq;
+          const int j = ring_node<N, EO>(kc, kq);
           if (j == N) continue;
           const int g = e * N + j;
           const double kk = kv[q][kc];
@@ -1286,7 +1332,7 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
       const int e = ring_elem<WMT, TILE_ILV != 0>(warp, q, rr);
 #pragma unroll
       for (int kc = 0; kc < KC; ++kc) {
-        const int j = 4 * kc + kq;
+        const int j = ring_node<N, EO>(kc, kq);
         if (j == N) continue;
         const int g = e * N + j;
         const double z = zval(S - 1, g, q, kc);
@@ -1298,10 +1344,10 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
 #pragma unroll
     for (int i = S - 1; i >= 0; --i) {
       if (i == S - 1)
-        ring_jact<N, WMT, decltype(bget), false, TILE_ILV != 0, true, true>(C, Gt, Uarr(i), slam, xfer, bget, mnu, warp,
+        ring_jact<N, WMT, decltype(bget), false, TILE_ILV != 0, true, true, EO>(C, Gt, Uarr(i), slam, xfer, bget, mnu, warp,
                                                                          lane, kv, TB::b(S - 1));
       else
-        ring_jact<N, WMT, decltype(bget), false, TILE_ILV != 0, true>(C, Gt, Uarr(i), Uarr(i + 1), xfer, bget, mnu, warp,
+        ring_jact<N, WMT, decltype(bget), false, TILE_ILV != 0, true, false, EO>(C, Gt, Uarr(i), Uarr(i + 1), xfer, bget, mnu, warp,
                                                                    lane, kv);
       double* zdst = Uarr(i);                   // U_i is dead once its J^T has run
 #pragma unroll
@@ -1309,7 +1355,7 @@ __global__ void __launch_bounds__(32 * W, tile_adj_minb<N, MODE>())
         const int e = ring_elem<WMT, TILE_ILV != 0>(warp, q, rr);
 #pragma unroll
         for (int kc = 0; kc < KC; ++kc) {
-          const int j = 4 * kc + kq;
+          const int j = ring_node<N, EO>(kc, kq);
           if (j == N) continue;
           const int g = e * N + j;
           const double l = kv[q][kc];           // already dt * J^T(M^-1 z)
