@@ -119,13 +119,14 @@ cudaError_t ensure_frag(const sem1d_plan* p) {
             }
             h[(((size_t)mat * NT + nt) * KC + kc) * 32 + l] = b;
           }
-    // n % 16 == 0: the reflection-split (WS_EO) sections follow, [Ke, Ko, De, Do, Te, To] and the
-    // prescaled [Ke', Ko', De', Do'], each [n/16][n/8][32] (bfrag_eo_value, sem1d_device.cuh)
+    // n % 16 == 0: the reflection-split (WS_EO) sections follow, [Ke, Ko, De, Do, Te, To], the
+    // prescaled [Ke', Ko', De', Do'] and J^T's [K''e, K''o, De', Do', T''e, T''o], each
+    // [n/16][n/8][32] (bfrag_eo_value, sem1d_device.cuh)
     if (n % 16 == 0) {
       const int NT2 = NT / 2, KC2 = KC / 2;
       const size_t base = h.size();
-      h.resize(base + (size_t)10 * NT2 * KC2 * 32);
-      for (int sec = 0; sec < 10; ++sec)
+      h.resize(base + (size_t)16 * NT2 * KC2 * 32);
+      for (int sec = 0; sec < 16; ++sec)
         for (int nt = 0; nt < NT2; ++nt)
           for (int kc = 0; kc < KC2; ++kc)
             for (int l = 0; l < 32; ++l)

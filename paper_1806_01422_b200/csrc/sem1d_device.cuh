@@ -1030,13 +1030,18 @@ __device__ __forceinline__ double bfrag_perm(const Consts<N>& C, int mat, int nt
 // epilogues promise the reference's association (the adaptive Kutta-3 error estimate is a
 // cancellation at the tolerance level).
 
-// sec: 0..5 = Ke, Ko, De, Do, Te, To; 6..9 = the prescaled Ke', Ko', De', Do'
+// sec: 0..5 = Ke, Ko, De, Do, Te, To; 6..9 = the prescaled Ke', Ko', De', Do' (F and J on periodic
+// rings); 10..15 = J^T on periodic rings with M^-1 and -nu folded in, so z enters unscaled:
+// K''e, K''o of K diag(-nu M^-1), De', Do' again, T''e, T''o of -Dw^T diag(M^-1) (negated: its
+// products accumulate into the K'' chains)
 template <int N>
 __host__ __device__ inline double bfrag_eo_value(const double* K, const double* Dw, const double* minv, double nu,
                                                  int sec, int nt, int kc, int lane) {
   constexpr int n = N + 1;
+  const bool jt = sec >= 10;                     // column-scaled K'' / T'' (sec 12, 13: De', Do')
+  if (sec == 12 || sec == 13) sec -= 4;
   const bool pre = sec >= 6;
-  const int mat = pre ? sec - 6 : sec;
+  const int mat = jt && sec >= 10 ? sec - 10 : (pre ? sec - 6 : sec);
   const int m = mat >> 1, par = mat & 1;
   const int c = 8 * nt + (lane >> 2);
   const int i = 4 * (2 * (c >> 3) + (c & 1)) + ((c >> 1) & 3);   // output row, < n/2
@@ -1054,6 +1059,10 @@ __host__ __device__ inline double bfrag_eo_value(const double* K, const double* 
 #endif
   auto M = [&](int r, int s) -> double {
     double b = m == 0 ? K[r * n + s] : (m == 1 ? Dw[r * n + s] : Dw[s * n + r]);
+    if (jt && sec >= 10) {                       // K'' = K diag(-nu M^-1), T'' = -Dw^T diag(M^-1)
+      const double ms = minv[(s == 0 || s == N) ? 0 : s];
+      return m == 0 ? EO_MUL(b, EO_MUL(-nu, ms)) : -EO_MUL(b, ms);
+    }
     if (pre) {
       const double mi = minv[(r == 0 || r == N) ? 0 : r];
       const double sc = (m == 0) ? EO_MUL(-nu, mi) : mi;         // one rounding, as bfrag_pre
@@ -1322,6 +1331,13 @@ __device__ __forceinline__ void mtile_compute_multi(const Consts<N>& C, const Ge
 #ifndef WS_EO_NTG
 #define WS_EO_NTG 1
 #endif
+// J and J^T on periodic rings with the pointwise scalings on the fragments, as F has them
+// (WS_PRE_F): J = K'v - v o (Dw'u) - u o (Dw'v) is two DFMAs per row instead of three multiplies,
+// two subtractions and the M^-1 product; J^T takes z unscaled, K'' = K diag(-nu M^-1) and
+// T'' = -Dw^T diag(M^-1) accumulate into one pair of chains, and a row is one DFMA
+#ifndef WS_EO_PRE
+#define WS_EO_PRE 1
+#endif
 // bit OP set: that operator takes its m-tiles one at a time even with the fragments in shared
 // memory (register pressure: 6 half-length vectors and 6 accumulator pairs per m-tile for J^T)
 #ifndef WS_EO_Q1
@@ -1349,7 +1365,7 @@ __device__ __forceinline__ void mtile_compute_eo(const Consts<N>& C, const Geo& 
     const int j = hi ? N - (4 * kc + kq) : 4 * kc + kq;
     double w = sw[base[q] + j];
     if (acc) WS_FIN_ACC(fin_w, w);
-    if (OP == OP_JACT) {
+    if (OP == OP_JACT && !PRE) {                 // (PRE: M^-1 rides on the fragments)
       const bool eslow = EDGE && (eg[q] == 0 || eg[q] == G.E - 1);
       w = eslow ? jt_scale<N>(C, w, j, eg[q], G) : __dmul_rn(w, hi ? minv_hi[kc] : minv_lo[kc]);
     }
@@ -1410,7 +1426,12 @@ __device__ __forceinline__ void mtile_compute_eo(const Consts<N>& C, const Geo& 
             dmma884(qe[g][q][0], qe[g][q][1], xs[q][kc], bde);
             dmma884(qo[g][q][0], qo[g][q][1], xd[q][kc], bdo);
           }
-          if (OP == OP_JACT) {
+          if (OP == OP_JACT && PRE) {
+            // T'' is negated and its hi rows are O - E: with A = K''e zs + T''o td and
+            // B = K''o zd + T''e ts, rows i and N - i of K''z + T''t are A + B and A - B
+            dmma884(ko[g][q][0], ko[g][q][1], ts[q][kc], bte);
+            dmma884(ke[g][q][0], ke[g][q][1], td[q][kc], bto);
+          } else if (OP == OP_JACT) {
             dmma884(qe[g][q][0], qe[g][q][1], ts[q][kc], bte);
             dmma884(qo[g][q][0], qo[g][q][1], td[q][kc], bto);
           }
@@ -1454,9 +1475,19 @@ __device__ __forceinline__ void mtile_compute_eo(const Consts<N>& C, const Geo& 
           const double w1 = (OP == OP_RHS) ? 0.0 : second(q, kcp, true, false);
           const double k0 = __dadd_rn(ke[g][q][h], ko[g][q][h]), k1 = __dsub_rn(ke[g][q][h], ko[g][q][h]);
           const double p0 = __dadd_rn(pe[g][q][h], po[g][q][h]), p1 = __dsub_rn(po[g][q][h], pe[g][q][h]);
-          const double q0 = __dadd_rn(qe[g][q][h], qo[g][q][h]), q1 = __dsub_rn(qo[g][q][h], qe[g][q][h]);
-          r[q][nt0 + g][h] = combine_rows<N, OP, PRE>(k0, p0, q0, u0, w0, mnu);
-          r[q][NT2 + nt0 + g][h] = combine_rows<N, OP, PRE>(k1, p1, q1, u1, w1, mnu);
+          if (PRE && OP == OP_JACT) {            // K''z + T''t - z o (Dw'u): one DFMA per row
+            r[q][nt0 + g][h] = __fma_rn(-w0, p0, k0);
+            r[q][NT2 + nt0 + g][h] = __fma_rn(-w1, p1, k1);
+          } else {
+            const double q0 = __dadd_rn(qe[g][q][h], qo[g][q][h]), q1 = __dsub_rn(qo[g][q][h], qe[g][q][h]);
+            if (PRE && OP == OP_JAC) {           // K'v - v o (Dw'u) - u o (Dw'v): two DFMAs per row
+              r[q][nt0 + g][h] = __fma_rn(-u0, q0, __fma_rn(-w0, p0, k0));
+              r[q][NT2 + nt0 + g][h] = __fma_rn(-u1, q1, __fma_rn(-w1, p1, k1));
+            } else {
+              r[q][nt0 + g][h] = combine_rows<N, OP, PRE>(k0, p0, q0, u0, w0, mnu);
+              r[q][NT2 + nt0 + g][h] = combine_rows<N, OP, PRE>(k1, p1, q1, u1, w1, mnu);
+            }
+          }
         }
   }
 }
@@ -1623,9 +1654,11 @@ __global__ void __launch_bounds__(WsTile<N, OP, NZ, ws_eo<N, EPI, NZ>()>::THREAD
   // F on a periodic ring reads the prescaled fragments (second part of the plan's table)
   // (plain applies only: the RK-stage epilogue keeps the reference's association, which the
   // adaptive Kutta-3 error estimate -- a cancellation at the tolerance level -- is sensitive to)
-  const bool pre = WS_PRE_F && OP == OP_RHS && EPI == EPI_STORE && periodic && frag != nullptr;
+  // WS_EO: J and J^T too (sections 6..9 and 10..15 of the reflection-split table)
+  const bool pre = WS_PRE_F && (OP == OP_RHS || (EO && WS_EO_PRE)) && EPI == EPI_STORE && periodic && frag != nullptr;
+  constexpr int PRE_SEC = (OP == OP_JACT) ? 10 : 6;          // first prescaled section of this operator
   if (EO) {
-    if (frag) frag += 5 * NT * KC * 32 + (pre ? 6 * NT2 * KC2 * 32 : 0);
+    if (frag) frag += 5 * NT * KC * 32 + (pre ? PRE_SEC * NT2 * KC2 * 32 : 0);
   } else if (pre) {
     frag += 3 * NT * KC * 32;
   }
@@ -1649,7 +1682,7 @@ __global__ void __launch_bounds__(WsTile<N, OP, NZ, ws_eo<N, EPI, NZ>()>::THREAD
         const int l = q & 31, r = q >> 5;
         if constexpr (EO) {
           const int kc = r % KC2, nt = (r / KC2) % NT2, mat = r / (KC2 * NT2);
-          bsm[q] = bfrag_eo_value<N>(C.K, C.Dw, C.minv, C.nu, mat + (pre ? 6 : 0), nt, kc, l);
+          bsm[q] = bfrag_eo_value<N>(C.K, C.Dw, C.minv, C.nu, mat + (pre ? PRE_SEC : 0), nt, kc, l);
         } else {
         const int kc = r % KC, nt = (r / KC) % NT, mat = r / (KC * NT);
         bsm[q] = bfrag_perm<N>(C, mat, nt, kc, l);
@@ -1670,7 +1703,7 @@ __global__ void __launch_bounds__(WsTile<N, OP, NZ, ws_eo<N, EPI, NZ>()>::THREAD
         for (int kc = 0; kc < KC2; ++kc)
           breg[(mat * NT2 + nt) * KC2 + kc] =
               frag ? __ldg(frag + ((mat * NT2 + nt) * KC2 + kc) * 32 + lane)
-                   : bfrag_eo_value<N>(C.K, C.Dw, C.minv, C.nu, mat + (pre ? 6 : 0), nt, kc, lane);
+                   : bfrag_eo_value<N>(C.K, C.Dw, C.minv, C.nu, mat + (pre ? PRE_SEC : 0), nt, kc, lane);
   }
   if (!W::B_IN_SMEM && !EO) {
 #pragma unroll
@@ -1901,7 +1934,7 @@ __global__ void __launch_bounds__(WsTile<N, OP, NZ, ws_eo<N, EPI, NZ>()>::THREAD
         }
       };
       if (edge) body(std::integral_constant<bool, true>{}, std::integral_constant<bool, false>{});
-      else if (OP == OP_RHS && pre) body(std::integral_constant<bool, false>{}, std::integral_constant<bool, OP == OP_RHS>{});
+      else if (pre) body(std::integral_constant<bool, false>{}, std::integral_constant<bool, OP == OP_RHS || EO>{});
       else body(std::integral_constant<bool, false>{}, std::integral_constant<bool, false>{});
       // first interface node of the warp: needs the halo row from the producer
       while (!mbar_try_wait(&halo[s], (it / STAGES) & 1)) {

@@ -23,14 +23,15 @@ namespace sem1d {
 #ifndef TILE_PRE
 #define TILE_PRE 1
 #endif
+// the shared-memory ring / tile kernels (ens_forward_kernel, tile_step_kernel, tile_adj_kernel) at
+// n % 16 == 0 (N = 15, 31) on the reflection split (ring_rhs / ring_jact EO)
+#ifndef TILE_EO
+#define TILE_EO 1
+#endif
 // the ensemble adjoint at N = 15 on the reflection split (ring_rhs / ring_jact EO): 8 + 12 DMMAs
 // per m-tile for F + J^T instead of 16 + 24
 #ifndef ENS_ADJ_EO
 #define ENS_ADJ_EO 1
-#endif
-// the shared-memory tile step / adjoint-step kernels (N = 15, 31) on the reflection split
-#ifndef TILE_EO
-#define TILE_EO 1
 #endif
 #ifndef ENS_ADJ_NOCHK
 #define ENS_ADJ_NOCHK 0   // timing experiment only: no cotangent checks in the ensemble adjoint
@@ -378,14 +379,30 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_fwd_warps<N>()>::THREADS, ((N + 
   const double mnu = -C.nu;
   using TB = TabC<SCH>;                       // compile-time tableau: stage loop unrolls
 
-  double breg[2 * NT * KC];
+  // reflection split (ring_node layout, ring_rhs EO) for n % 16 == 0: Ke', Ko', De', Do' blocks
+  constexpr bool EO = TILE_EO && (N + 1) % 16 == 0 && TILE_PRE;
+  constexpr int NT2 = NT / 2, KH = KC / 2;
+  double breg[EO ? 4 * NT2 * KH : 2 * NT * KC];
+  if constexpr (EO) {
 #pragma unroll
-  for (int mat = 0; mat < 2; ++mat)
+    for (int mat = 0; mat < 4; ++mat)
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
+      for (int nt = 0; nt < NT2; ++nt)
 #pragma unroll
-      for (int kc = 0; kc < KC; ++kc) breg[(mat * NT + nt) * KC + kc] = (TILE_PRE ? bfrag_pre<N>(C, mat, nt, kc, lane) : bfrag_perm<N>(C, mat, nt, kc, lane));
-  auto bget = [&](int mat, int nt, int kc) -> double { return breg[(mat * NT + nt) * KC + kc]; };
+        for (int kc = 0; kc < KH; ++kc)
+          breg[(mat * NT2 + nt) * KH + kc] = bfrag_eo_value<N>(C.K, C.Dw, C.minv, C.nu, 6 + mat, nt, kc, lane);
+  } else {
+#pragma unroll
+    for (int mat = 0; mat < 2; ++mat)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+        for (int kc = 0; kc < KC; ++kc) breg[(mat * NT + nt) * KC + kc] = (TILE_PRE ? bfrag_pre<N>(C, mat, nt, kc, lane) : bfrag_perm<N>(C, mat, nt, kc, lane));
+  }
+  auto bget = [&](int mat, int nt, int kc) -> double {
+    if constexpr (EO) return breg[(mat * NT2 + nt) * KH + kc];
+    else return breg[(mat * NT + nt) * KC + kc];
+  };
   double minv_a[KC];
 #pragma unroll
   for (int kc = 0; kc < KC; ++kc) {
@@ -412,7 +429,7 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_fwd_warps<N>()>::THREADS, ((N + 
 #pragma unroll
     for (int i = 0; i < TB::s; ++i) {
       const double* src = (i == 0) ? su : sU;
-      ring_rhs<N, WMT_MAX, decltype(bget), true, TILE_PRE != 0, ILV>(C, G, src, xfer, bget, minv_a, mnu, warp, lane, kv,
+      ring_rhs<N, WMT_MAX, decltype(bget), true, TILE_PRE != 0, ILV, EO>(C, G, src, xfer, bget, minv_a, mnu, warp, lane, kv,
                                                                fin);
       // (ring_rhs ended with a barrier: every warp is done reading src)
 #pragma unroll
@@ -422,7 +439,7 @@ __global__ void __launch_bounds__(EnsCfg<N, ens_fwd_warps<N>()>::THREADS, ((N + 
         const int e = ring_elem<WMT_MAX, ILV>(warp, q, rr);
 #pragma unroll
         for (int kc = 0; kc < KC; ++kc) {
-          const int j = 4 * kc + kq;
+          const int j = ring_node<N, EO>(kc, kq);
           if (j == N) continue;               // node N belongs to the next element
           const int g = e * N + j;
           const double kk = kv[q][kc];
