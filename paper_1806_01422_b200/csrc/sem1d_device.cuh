@@ -25,6 +25,7 @@
 // coalesced stores.  The halo element's last row is recomputed by thread 0,
 // so CTAs never communicate and results are bitwise reproducible.
 #pragma once
+#include <cmath>
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -1030,6 +1031,63 @@ __device__ __forceinline__ double bfrag_perm(const Consts<N>& C, int mat, int nt
 // epilogues promise the reference's association (the adaptive Kutta-3 error estimate is a
 // cancellation at the tolerance level).
 
+// Double-double helpers for forming the half blocks.  A block entry is a signed sum of four
+// scaled matrix entries that may cancel; rounding each product and partial sum would perturb
+// the effective matrix by an ulp of its LARGEST mirrored entry, which on smooth inputs (where
+// K u cancels to a small result) costs as much accuracy as the contraction itself.  So the
+// four terms are formed as exact products (two_prod), summed in double-double, and rounded
+// once.  Only IEEE operations and FMA: the host table and the in-kernel construction agree
+// bit for bit.
+struct DD {
+  double hi, lo;
+};
+__host__ __device__ inline double dd_fma(double a, double b, double c) {
+#ifdef __CUDA_ARCH__
+  return __fma_rn(a, b, c);
+#else
+  return std::fma(a, b, c);
+#endif
+}
+__host__ __device__ inline double dd_add1(double a, double b) {
+#ifdef __CUDA_ARCH__
+  return __dadd_rn(a, b);
+#else
+  volatile double t = a + b;
+  return t;
+#endif
+}
+__host__ __device__ inline DD dd_two_sum(double a, double b) {
+  const double s = dd_add1(a, b), bb = dd_add1(s, -a);
+  return {s, dd_add1(dd_add1(a, -dd_add1(s, -bb)), dd_add1(b, -bb))};
+}
+__host__ __device__ inline DD dd_two_prod(double a, double b) {
+  const double p = dd_fma(a, b, 0.0);
+  return {p, dd_fma(a, b, -p)};
+}
+__host__ __device__ inline DD dd_add(DD x, DD y) {
+  DD s = dd_two_sum(x.hi, y.hi);
+  return dd_two_sum(s.hi, dd_add1(s.lo, dd_add1(x.lo, y.lo)));
+}
+__host__ __device__ inline DD dd_mul(DD x, double y) {
+  DD p = dd_two_prod(x.hi, y);
+  return dd_two_sum(p.hi, dd_add1(p.lo, dd_fma(x.lo, y, 0.0)));
+}
+__host__ __device__ inline DD dd_neg(DD x) { return {-x.hi, -x.lo}; }
+// even (par 0) / odd (par 1) half-block entry (i, j), i, j < n/2, of the matrix whose entries
+// term(r, s) returns (as double-doubles): centrosymmetric (centro) or anti-centrosymmetric;
+// formed from both halves, 1/4 ((M[i][j] +- M[N-i][N-j]) +- (M[i][N-j] +- M[N-i][j]))
+template <class Term>
+__host__ __device__ inline double eo_block_entry(Term term, bool centro, int par, int i, int j, int N) {
+  DD b = term(N - i, N - j), d = term(N - i, j);
+  if (!centro) {
+    b = dd_neg(b);
+    d = dd_neg(d);
+  }
+  const DD ab = dd_add(term(i, j), b), cd = dd_add(term(i, N - j), d);
+  const DD t = dd_add(ab, par == 0 ? cd : dd_neg(cd));
+  return 0.25 * dd_add1(t.hi, t.lo);
+}
+
 // sec: 0..5 = Ke, Ko, De, Do, Te, To; 6..9 = the prescaled Ke', Ko', De', Do' (F and J on periodic
 // rings); 10..15 = J^T on periodic rings with M^-1 and -nu folded in, so z enters unscaled:
 // K''e, K''o of K diag(-nu M^-1), De', Do' again, T''e, T''o of -Dw^T diag(M^-1) (negated: its
@@ -1038,51 +1096,22 @@ template <int N>
 __host__ __device__ inline double bfrag_eo_value(const double* K, const double* Dw, const double* minv, double nu,
                                                  int sec, int nt, int kc, int lane) {
   constexpr int n = N + 1;
-  const bool jt = sec >= 10;                     // column-scaled K'' / T'' (sec 12, 13: De', Do')
-  if (sec == 12 || sec == 13) sec -= 4;
-  const bool pre = sec >= 6;
-  const int mat = jt && sec >= 10 ? sec - 10 : (pre ? sec - 6 : sec);
+  const bool jt = sec >= 10 && sec != 12 && sec != 13;   // column-scaled K'' / T''
+  if (sec == 12 || sec == 13) sec -= 4;                  // De', Do'
+  const bool pre = !jt && sec >= 6;
+  const int mat = jt ? sec - 10 : (pre ? sec - 6 : sec);
   const int m = mat >> 1, par = mat & 1;
   const int c = 8 * nt + (lane >> 2);
   const int i = 4 * (2 * (c >> 3) + (c & 1)) + ((c >> 1) & 3);   // output row, < n/2
   const int j = 4 * kc + (lane & 3);                             // input node, < n/2
-  // every product / sum rounded once (no FMA contraction), on the host and on the device alike
-#ifdef __CUDA_ARCH__
-#define EO_MUL(x, y) __dmul_rn((x), (y))
-#define EO_ADD(x, y) __dadd_rn((x), (y))
-#define EO_SUB(x, y) __dsub_rn((x), (y))
-#else
-  auto vol = [](double v) { volatile double t = v; return t; };
-#define EO_MUL(x, y) vol((x) * (y))
-#define EO_ADD(x, y) vol((x) + (y))
-#define EO_SUB(x, y) vol((x) - (y))
-#endif
-  auto M = [&](int r, int s) -> double {
-    double b = m == 0 ? K[r * n + s] : (m == 1 ? Dw[r * n + s] : Dw[s * n + r]);
-    if (jt && sec >= 10) {                       // K'' = K diag(-nu M^-1), T'' = -Dw^T diag(M^-1)
-      const double ms = minv[(s == 0 || s == N) ? 0 : s];
-      return m == 0 ? EO_MUL(b, EO_MUL(-nu, ms)) : -EO_MUL(b, ms);
-    }
-    if (pre) {
-      const double mi = minv[(r == 0 || r == N) ? 0 : r];
-      const double sc = (m == 0) ? EO_MUL(-nu, mi) : mi;         // one rounding, as bfrag_pre
-      b = EO_MUL(b, sc);
-    }
-    return b;
+  auto mv = [&](int r) -> double { return minv[(r == 0 || r == N) ? 0 : r]; };
+  auto term = [&](int r, int s) -> DD {
+    const double b = m == 0 ? K[r * n + s] : (m == 1 ? Dw[r * n + s] : Dw[s * n + r]);
+    if (jt) return m == 0 ? dd_mul(dd_two_prod(-nu, mv(s)), b) : dd_neg(dd_two_prod(b, mv(s)));
+    if (pre) return m == 0 ? dd_mul(dd_two_prod(-nu, mv(r)), b) : dd_two_prod(b, mv(r));
+    return DD{b, 0.0};
   };
-  double a, b;
-  if (m == 0) {
-    a = EO_ADD(M(i, j), M(N - i, N - j));
-    b = EO_ADD(M(i, N - j), M(N - i, j));
-  } else {
-    a = EO_SUB(M(i, j), M(N - i, N - j));
-    b = EO_SUB(M(i, N - j), M(N - i, j));
-  }
-  const double t = par == 0 ? EO_ADD(a, b) : EO_SUB(a, b);
-#undef EO_MUL
-#undef EO_ADD
-#undef EO_SUB
-  return 0.25 * t;
+  return eo_block_entry(term, m == 0, par, i, j, N);
 }
 
 #ifndef WS_ELEMS8_J

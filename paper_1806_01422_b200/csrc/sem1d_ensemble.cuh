@@ -317,20 +317,13 @@ __device__ __forceinline__ double bfrag_eo_adj(const Consts<N>& C, int mat, int 
   const int i = 4 * (2 * (c >> 3) + (c & 1)) + ((c >> 1) & 3);
   const int j = 4 * kc + (lane & 3);
   auto mv = [&](int r) -> double { return C.minv[(r == 0 || r == N) ? 0 : r]; };
-  auto M = [&](int r, int s) -> double {
-    if (m == 0) return __dmul_rn(C.K[r * n + s], __dmul_rn(__dmul_rn(-C.nu, dt), mv(s)));
-    if (m == 1) return __dmul_rn(C.Dw[r * n + s], __dmul_rn(dt, mv(r)));
-    return -__dmul_rn(C.Dw[s * n + r], __dmul_rn(dt, mv(s)));
+  // exact products summed in double-double and rounded once (eo_block_entry)
+  auto term = [&](int r, int s) -> DD {
+    if (m == 0) return dd_mul(dd_mul(dd_two_prod(-C.nu, dt), mv(s)), C.K[r * n + s]);
+    if (m == 1) return dd_mul(dd_two_prod(dt, mv(r)), C.Dw[r * n + s]);
+    return dd_neg(dd_mul(dd_two_prod(dt, mv(s)), C.Dw[s * n + r]));
   };
-  double a, b;
-  if (m == 0) {
-    a = __dadd_rn(M(i, j), M(N - i, N - j));
-    b = __dadd_rn(M(i, N - j), M(N - i, j));
-  } else {
-    a = __dsub_rn(M(i, j), M(N - i, N - j));
-    b = __dsub_rn(M(i, N - j), M(N - i, j));
-  }
-  return 0.25 * (par == 0 ? __dadd_rn(a, b) : __dsub_rn(a, b));
+  return eo_block_entry(term, m == 0, par, i, j, N);
 }
 
 // Compile-time Butcher tableaux of the sweep kernels (same values as make_tableau:

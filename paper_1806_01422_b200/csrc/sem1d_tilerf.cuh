@@ -115,17 +115,13 @@ __device__ __forceinline__ double bfrag_rf(const Consts<7>& C, int mat, int kc, 
 __device__ __forceinline__ double bfrag_eo(const Consts<7>& C, int par, int lane) {
   const int c = lane >> 2, j = lane & 3, i = c >> 1;
   auto mi = [&](int r) { return C.minv[(r == 0 || r == 7) ? 0 : r]; };
-  double a, b;
+  // exact products summed in double-double and rounded once (eo_block_entry, sem1d_device.cuh)
   if ((c & 1) == 0) {                           // K' blocks
-    auto kp = [&](int r, int s) { return __dmul_rn(C.K[r * 8 + s], __dmul_rn(-C.nu, mi(r))); };
-    a = __dadd_rn(kp(i, j), kp(7 - i, 7 - j));
-    b = __dadd_rn(kp(i, 7 - j), kp(7 - i, j));
-  } else {                                      // Dw' blocks
-    auto dp = [&](int r, int s) { return __dmul_rn(C.Dw[r * 8 + s], mi(r)); };
-    a = __dsub_rn(dp(i, j), dp(7 - i, 7 - j));
-    b = __dsub_rn(dp(i, 7 - j), dp(7 - i, j));
+    auto kp = [&](int r, int s) -> DD { return dd_mul(dd_two_prod(-C.nu, mi(r)), C.K[r * 8 + s]); };
+    return eo_block_entry(kp, true, par, i, j, 7);
   }
-  return 0.25 * (par == 0 ? __dadd_rn(a, b) : __dsub_rn(a, b));
+  auto dp = [&](int r, int s) -> DD { return dd_two_prod(C.Dw[r * 8 + s], mi(r)); };   // Dw' blocks
+  return eo_block_entry(dp, false, par, i, j, 7);
 }
 // F at nodes kq / 7-kq of the lane's element from its two node values (RF_EO split); dw0/dw1
 // receive Dw'u at the two nodes

@@ -169,6 +169,36 @@ def test_lbfgs_quadratic_and_reference_log_shape():
     with pytest.raises(sb.LineSearchError):
         sb.line_search(lambda t: (0.0, 0.0, None), 0.0, 1.0)
 
+@pytest.mark.parametrize("n", [7, 15, 31])
+def test_reflection_symmetry_behind_the_split_kernels(n):
+    """The reflection (even/odd) split of the DMMA kernels (bfrag_eo_value in
+    csrc/sem1d_device.cuh) relies on K being centrosymmetric and Dw anti-centrosymmetric, which
+    holds for the reference's own matrices (ops.py:103-107) to a few ulp, and on the mass
+    pattern being symmetric.  The half blocks formed as the kernels form them (from both
+    halves of each matrix) reproduce the full products on the sums and differences of
+    mirrored nodes to rounding."""
+    g = golden("basis.npz")
+    K, Dw, w = g[f"K_{n}"], g[f"Dw_{n}"], g[f"weights_{n}"]
+    flip = lambda a: a[::-1, ::-1]
+    assert np.max(np.abs(K - flip(K))) <= 64 * np.finfo(float).eps * np.max(np.abs(K))
+    assert np.max(np.abs(Dw + flip(Dw))) <= 64 * np.finfo(float).eps * np.max(np.abs(Dw))
+    assert np.array_equal(w, w[::-1]) or np.max(np.abs(w - w[::-1])) <= 4 * np.finfo(float).eps
+    h = (n + 1) // 2
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal(n + 1)
+    s, d = x[:h] + x[::-1][:h], x[:h] - x[::-1][:h]
+    for M, centro in ((K, True), (Dw, False), (Dw.T.copy(), False)):
+        sg = 1.0 if centro else -1.0
+        a = M[:h, :h] + sg * flip(M)[:h, :h]                 # M[i][j] +- M[N-i][N-j]
+        b = M[:h, ::-1][:, :h] + sg * flip(M)[:h, ::-1][:, :h]   # M[i][N-j] +- M[N-i][j]
+        Me, Mo = 0.25 * (a + b), 0.25 * (a - b)
+        lo = Me @ s + Mo @ d
+        hi = sg * (Me @ s - Mo @ d)
+        y = M @ x
+        tol = 1e-13 * np.max(np.abs(M)) * np.max(np.abs(x)) * (n + 1)
+        assert np.max(np.abs(lo - y[:h])) <= tol and np.max(np.abs(hi - y[::-1][:h])) <= tol
+
+
 
 @pytest.mark.parametrize("k", [0, 1, 2])
 def test_grid3d_maps_bit_exact(k):
