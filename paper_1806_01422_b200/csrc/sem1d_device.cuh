@@ -976,8 +976,15 @@ constexpr int ws_outb() { return OP == OP_RHS ? WS_OUTB_F : WS_OUTB_J; }
 #ifndef WS_EO
 #define WS_EO 1
 #endif
+#ifndef WS_EO_ADJ
+#define WS_EO_ADJ 1
+#endif
 template <int N, int EPI, int NZ>
-constexpr bool ws_eo() { return WS_EO && (N + 1) % 16 == 0 && EPI == EPI_STORE && NZ < 0; }
+constexpr bool ws_eo() {
+  // plain applies, and (WS_EO_ADJ) the adjoint stage, whose J^T contraction is the plain one and
+  // whose recurrence epilogue keeps its association; the RK stage keeps the full matrices
+  return WS_EO && (N + 1) % 16 == 0 && ((EPI == EPI_STORE && NZ < 0) || (WS_EO_ADJ && EPI == EPI_ADJ && NZ >= 0));
+}
 #ifndef WS_MINB32_F_EO
 #define WS_MINB32_F_EO 3
 #endif
