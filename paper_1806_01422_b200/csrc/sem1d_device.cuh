@@ -935,9 +935,7 @@ typedef double ws_fin_t;
 #ifndef WS_ELEMS32
 #define WS_ELEMS32 128
 #endif
-#ifndef WS_ELEMS32_J
-#define WS_ELEMS32_J 64
-#endif
+// (J / J^T tiles at n = 32: 2 m-tiles per consumer warp, 16 * CW elements)
 
 // Occupancy per operator at n = 8, A/B-measured on config 2 (round 1:
 // profiles/r1_ab_occupancy.json; re-measured in round 2, profiles/r2_ws_ab_cfg2.jsonl):
@@ -1138,7 +1136,7 @@ struct WsTile {
   static constexpr int ELEMS =
       ADJ ? (n == 8 ? 128 : 64)
           : (n == 8) ? (OP == OP_RHS ? WS_ELEMS8 : WS_ELEMS8_J)
-                     : (n == 32 ? (OP == OP_RHS ? (EO ? WS_ELEMS32_EO : WS_ELEMS32) : WS_ELEMS32_J) : MmaTile<N>::ELEMS);
+                     : (n == 32 ? (OP == OP_RHS ? (EO ? WS_ELEMS32_EO : WS_ELEMS32) : 16 * CW) : MmaTile<N>::ELEMS);
   static constexpr int WE = ELEMS / CW;                          // elements per consumer warp
   static constexpr int WMT = WE / 8;                             // m-tiles per warp
   static constexpr int NT = n / 8, KC = n / 4;
