@@ -64,7 +64,13 @@ int sem1d_version(void);
  * 0 = automatic (warp-specialised FP64 tensor-core DMMA kernel for N+1 in
  *     {8,16,24,32}, else the TMA-pipelined DFMA kernel for odd N, else the
  *     plain tiled kernel), 1 = never a tensor-core kernel, 2 = plain tiled
- *     kernel only, 3 = the CTA-synchronous tensor-core kernel (A/B reference). */
+ *     kernel only, 3 = the CTA-synchronous tensor-core kernel (A/B reference).
+ * Arithmetic: for N+1 in {16, 32} the automatic path contracts on the reflection
+ * (even/odd) split of K, Dw and Dw^T (half blocks acting on sums and differences of
+ * mirrored nodes; the same products as ops.py:161-212 summed in a different order,
+ * within the 1e-12 per-apply tolerance and the smooth-input longdouble bound).  Paths 1
+ * and 2 keep the reference's summation order (bit-identical to its numpy result on the
+ * inputs tested). */
 int sem1d_set_kernel_path(int path);
 /* Tile-step kernels for A/B runs: 0 = auto (register-resident kernels for N = 7),
  * 1 = the shared-memory tile kernels for every degree (and the shared-memory ensemble
