@@ -99,6 +99,29 @@ def test_tile_edges(cuda, E):
         assert rel_err(op.apply_jacobian_transpose(u, w), ref.jact(u, w)) <= TOL
 
 
+@pytest.mark.parametrize("N", [15, 31])
+@pytest.mark.parametrize("E", [1, 2, 3, 5, 17])
+def test_tiny_rings_on_the_split_kernels(cuda, N, E):
+    """N = 15 / 31 take the reflection-split DMMA kernel at every ring size: rings smaller than
+    one m-tile, wrap-around of a one- or two-element periodic ring, both boundary kinds,
+    batches (rows 0 and N of an element sit in the same lane there)."""
+    for periodic in (True, False):
+        for B in (1, 3):
+            op = _op(0.0, 3.0, E, N, periodic, 0.02, batch=B)
+            ref = R.BurgersOracle(R.Mesh1D(0.0, 3.0, E, N, periodic), 0.02)
+            rng = np.random.default_rng(100 * N + E)
+            U = rng.uniform(-1, 1, (B, ref.mesh.ndof))
+            V = rng.standard_normal((B, ref.mesh.ndof))
+            F = op.apply_rhs(U if B > 1 else U[0])
+            JV = op.apply_jacobian(U if B > 1 else U[0], V if B > 1 else V[0])
+            JT = op.apply_jacobian_transpose(U if B > 1 else U[0], V if B > 1 else V[0])
+            for b in range(B):
+                f, jv, jt = (x[b] if B > 1 else x for x in (F, JV, JT))
+                assert rel_err(f, ref.rhs(U[b])) <= TOL
+                assert rel_err(jv, ref.jac(U[b], V[b])) <= TOL
+                assert rel_err(jt, ref.jact(U[b], V[b])) <= TOL
+
+
 def test_batched_operator_equals_per_problem(cuda):
     B, E, N = 5, 40, 15
     op = _op(0.0, 20.0, E, N, True, 0.01, batch=B)
