@@ -1422,9 +1422,9 @@ __device__ __forceinline__ void mtile_compute_eo(const Consts<N>& C, const Geo& 
         xs[q][kc] = __dadd_rn(w0, w1);
         xd[q][kc] = __dsub_rn(w0, w1);
         if (OP == OP_JACT) {
-          const double t0 = __dmul_rn(a0, w0), t1 = __dmul_rn(a1, w1);
-          ts[q][kc] = __dadd_rn(t0, t1);
-          td[q][kc] = __dsub_rn(t0, t1);
+          const double t1 = __dmul_rn(a1, w1);   // u o zm sums / differences: one product, two DFMAs
+          ts[q][kc] = __fma_rn(a0, w0, t1);
+          td[q][kc] = __fma_rn(a0, w0, -t1);
         }
       }
     }

@@ -515,13 +515,13 @@ __device__ __forceinline__ void ring_jact(const Consts<N>& C, const Geo& G, cons
         const double u0 = usrc[j0], u1 = usrc[j1];
         zl[kc] = ZS ? __dmul_rn(zs, zsrc[j0]) : zsrc[j0];
         zh[kc] = ZS ? __dmul_rn(zs, zsrc[j1]) : zsrc[j1];
-        const double t0 = __dmul_rn(u0, zl[kc]), t1 = __dmul_rn(u1, zh[kc]);
+        const double t1 = __dmul_rn(u1, zh[kc]);
         us[kc] = __dadd_rn(u0, u1);
         ud[kc] = __dsub_rn(u0, u1);
         zs_[kc] = __dadd_rn(zl[kc], zh[kc]);
         zd_[kc] = __dsub_rn(zl[kc], zh[kc]);
-        ts[kc] = __dadd_rn(t0, t1);
-        td[kc] = __dsub_rn(t0, t1);
+        ts[kc] = __fma_rn(u0, zl[kc], t1);        // u0 z0 + u1 z1 and u0 z0 - u1 z1: one product
+        td[kc] = __fma_rn(u0, zl[kc], -t1);       // and two DFMAs instead of two and two adds
       }
 #pragma unroll
       for (int nt = 0; nt < NT2; ++nt) {
