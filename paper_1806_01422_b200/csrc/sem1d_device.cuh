@@ -1509,7 +1509,10 @@ __device__ __forceinline__ void mtile_compute_eo(const Consts<N>& C, const Geo& 
           const double w1 = (OP == OP_RHS) ? 0.0 : second(q, kcp, true, false);
           const double k0 = __dadd_rn(ke[g][q][h], ko[g][q][h]), k1 = __dsub_rn(ke[g][q][h], ko[g][q][h]);
           const double p0 = __dadd_rn(pe[g][q][h], po[g][q][h]), p1 = __dsub_rn(po[g][q][h], pe[g][q][h]);
-          if (PRE && OP == OP_JACT) {            // K''z + T''t - z o (Dw'u): one DFMA per row
+          if (PRE && OP == OP_RHS) {             // K'u - u o (Dw'u): one DFMA per row
+            r[q][nt0 + g][h] = __fma_rn(-u0, p0, k0);
+            r[q][NT2 + nt0 + g][h] = __fma_rn(-u1, p1, k1);
+          } else if (PRE && OP == OP_JACT) {     // K''z + T''t - z o (Dw'u): one DFMA per row
             r[q][nt0 + g][h] = __fma_rn(-w0, p0, k0);
             r[q][NT2 + nt0 + g][h] = __fma_rn(-w1, p1, k1);
           } else {
