@@ -1372,6 +1372,19 @@ __device__ __forceinline__ void mtile_compute_multi(const Consts<N>& C, const Ge
 #ifndef WS_EO_PRE
 #define WS_EO_PRE 1
 #endif
+// A/B only (off): the producer warp's halo rows (row N of the element left of each consumer
+// warp) as dot products on the FP64 vector pipe instead of a halo m-tile of 16-24 DMMAs.  The
+// idea was that the producer warps of all resident CTAs share one SM sub-partition with two
+// consumer warps and lengthen its DMMA queue by 25%.  Measured on config 3 it loses, and the
+// times become unstable from launch to launch: F 35.8-36.2 us against 31.8, J 44-51.5 against
+// 47.9, J^T 53.7-55.6 against 47.0 -- vector FP64 work interleaved into the consumers' DMMA
+// phases on that sub-partition costs more than the DMMAs it replaces.
+#ifndef WS_EO_HALO
+#define WS_EO_HALO 0
+#endif
+#ifndef WS_PROD_SLEEP
+#define WS_PROD_SLEEP 0
+#endif
 // bit OP set: that operator takes its m-tiles one at a time even with the fragments in shared
 // memory (register pressure: 6 half-length vectors and 6 accumulator pairs per m-tile for J^T)
 #ifndef WS_EO_Q1
@@ -1558,7 +1571,8 @@ __global__ void __launch_bounds__(WsTile<N, OP, NZ, ws_eo<N, EPI, NZ>()>::THREAD
   double* ostage = smem + STAGES * NIN * SA;                  // [OUTB][OUT]
   double* hrow = ostage + OUTB * W::OUT;                      // [STAGES][CW] warp halo rows
   double* bsm = hrow + STAGES * W::CW;                        // B fragments (n = 32)
-  uint64_t* full = reinterpret_cast<uint64_t*>(bsm + (W::B_IN_SMEM ? BTOT : 0));
+  double* hal = bsm + (W::B_IN_SMEM ? BTOT : 0);              // WS_EO_HALO: 3 scaled matrix rows / columns N
+  uint64_t* full = reinterpret_cast<uint64_t*>(hal + (EO ? 3 * (N + 1) : 0));
   uint64_t* empty = full + STAGES;
   uint64_t* halo = empty + STAGES;
   const int tid = threadIdx.x;
@@ -1655,6 +1669,7 @@ __global__ void __launch_bounds__(WsTile<N, OP, NZ, ws_eo<N, EPI, NZ>()>::THREAD
   auto issue_next = [&](int T) {
     const int s = issued % STAGES;
     while (!mbar_try_wait(&empty[s], ((issued / STAGES) & 1) ^ 1)) {
+      if (WS_PROD_SLEEP) __nanosleep(WS_PROD_SLEEP);   // the producer shares its sub-partition with consumers
     }
     load_tile(T, s);
     ++issued;
@@ -1724,6 +1739,21 @@ __global__ void __launch_bounds__(WsTile<N, OP, NZ, ws_eo<N, EPI, NZ>()>::THREAD
         const int kc = r % KC, nt = (r / KC) % NT, mat = r / (KC * NT);
         bsm[q] = bfrag_perm<N>(C, mat, nt, kc, l);
         }
+      }
+    }
+  }
+  if constexpr (EO) {
+    // WS_EO_HALO: row N of the prescaled matrices (the producer's halo rows are three dot
+    // products per element on the FP64 vector pipe instead of 16-24 DMMAs)
+    if (WS_EO_HALO && pre) {
+      constexpr int n = N + 1;
+      const double m0 = C.minv[0];
+      for (int j = tid; j < n; j += W::THREADS) {
+        const double mj = C.minv[(j == 0 || j == N) ? 0 : j];
+        hal[j] = (OP == OP_JACT) ? __dmul_rn(C.K[N * n + j], __dmul_rn(-C.nu, mj))
+                                 : __dmul_rn(C.K[N * n + j], __dmul_rn(-C.nu, m0));
+        hal[n + j] = __dmul_rn(C.Dw[N * n + j], m0);
+        hal[2 * n + j] = -__dmul_rn(C.Dw[j * n + N], mj);
       }
     }
   }
@@ -1822,7 +1852,39 @@ __global__ void __launch_bounds__(WsTile<N, OP, NZ, ws_eo<N, EPI, NZ>()>::THREAD
         double r[NT][2];
         ws_fin_t du_ = 0, dw_ = 0;
         using BG = decltype(bget);
-        if constexpr (EO) {
+        if (EO && WS_EO_HALO && pre) {
+          // row N of element eh on the vector pipe: lane (rr, kq) sums the products of nodes
+          // j = kq, kq + 4, ..., the four partial sums meet by two butterfly shuffles
+          constexpr int n = N + 1;
+          const int hbase = wq * WE * N;
+          double kx = 0.0, du = 0.0, qq = 0.0;
+#pragma unroll
+          for (int m = 0; m < n / 4; ++m) {
+            const int j = 4 * m + kq;
+            const double uj = su[hbase + j];
+            du = __fma_rn(hal[n + j], uj, du);
+            if (OP == OP_RHS) {
+              kx = __fma_rn(hal[j], uj, kx);
+            } else {
+              const double wj = sw[hbase + j];
+              kx = __fma_rn(hal[j], wj, kx);
+              if (OP == OP_JAC) qq = __fma_rn(hal[n + j], wj, qq);
+              else kx = __fma_rn(hal[2 * n + j], __dmul_rn(uj, wj), kx);
+            }
+          }
+#pragma unroll
+          for (int x = 1; x <= 2; x <<= 1) {
+            kx = __dadd_rn(kx, __shfl_xor_sync(0xffffffffu, kx, x));
+            du = __dadd_rn(du, __shfl_xor_sync(0xffffffffu, du, x));
+            if (OP == OP_JAC) qq = __dadd_rn(qq, __shfl_xor_sync(0xffffffffu, qq, x));
+          }
+          const double uN = su[hbase + N];
+          double row;
+          if (OP == OP_RHS) row = __fma_rn(-uN, du, kx);
+          else if (OP == OP_JAC) row = __fma_rn(-uN, qq, __fma_rn(-sw[hbase + N], du, kx));
+          else row = __fma_rn(-sw[hbase + N], du, kx);
+          r[RN_NT][RN_H] = row;                      // (pre: periodic ring, every halo row exists)
+        } else if constexpr (EO) {
           const int hb[1] = {wq * WE * N};
           const int64_t he[1] = {ehw};
           using WSrcT = decltype(sw);
@@ -2133,7 +2195,7 @@ constexpr size_t ws_smem_bytes() {
   using W = WsTile<N, OP, NZ, EO>;
   constexpr int NIN = W::NIN;
   return sizeof(double) * ((size_t)STAGES * NIN * W::SLAB_ALLOC + ws_outb<OP>() * W::OUT + STAGES * W::CW +
-                           ws_bsm_doubles<N, OP, NZ, EO>()) +
+                           ws_bsm_doubles<N, OP, NZ, EO>() + (EO ? 3 * (N + 1) : 0)) +
          sizeof(uint64_t) * 3 * STAGES;
 }
 
