@@ -1,7 +1,7 @@
 """Randomised parity soak of the reflection-split kernels (N = 15, 31; plus N = 7 and 23 as the
 unsplit controls): random ring sizes, both boundary kinds, batches, F / J v / J^T w against the
 oracle at 1e-12, and one fused RK4 step + adjoint step per case where the fused kernels apply
-(1e-9).  python tools/soak_split.py [cases] [seed]"""
+(increments of the state and of the cotangent at 1e-9).  python tools/soak_split.py [cases] [seed]"""
 import json
 import os
 import sys
@@ -58,8 +58,10 @@ def main(cases=150, seed=0):
             op.launch_adj_step(ud, ld, lo, dt, "rk4")
             torch.cuda.synchronize()
             if op.flags() == 0:
-                es = rel(un.cpu().numpy(), R.rk_step(ref, u, dt, "rk4"))
-                ea = rel(lo.cpu().numpy(), R.adjoint_rk_step(ref, u, lam, dt, "rk4"))
+                # the INCREMENTS of the step and of the adjoint step (the states themselves move by
+                # ~dt and would hide an error in the stage arithmetic)
+                es = rel(un.cpu().numpy() - u, R.rk_step(ref, u, dt, "rk4") - u)
+                ea = rel(lo.cpu().numpy() - lam, R.adjoint_rk_step(ref, u, lam, dt, "rk4") - lam)
                 worst["step"], worst["adj"] = max(worst["step"], es), max(worst["adj"], ea)
                 if not es <= 1e-9:
                     fails.append((c, N, E, per, B, "step", es))
