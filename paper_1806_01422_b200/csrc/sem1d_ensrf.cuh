@@ -40,6 +40,9 @@ namespace sem1d {
 #ifndef ENSRF_EO
 #define ENSRF_EO 1
 #endif
+#ifndef ENSRF_MINB
+#define ENSRF_MINB 2       // rings (CTAs) per SM; 3 (80 registers, 72-128 B of spills): 138.7 ms against 128.0 on config 4
+#endif
 
 struct EnsRf {
   static constexpr int N = 15, KC = 4, NT = 2, WMT = 4, W = 8, THREADS = 32 * W;
@@ -50,7 +53,7 @@ struct EnsRf {
 };
 
 template <int SCH>
-__global__ void __launch_bounds__(EnsRf::THREADS, 2)
+__global__ void __launch_bounds__(EnsRf::THREADS, ENSRF_MINB)
     ens_forward_rf_kernel(const __grid_constant__ Consts<15> C, const Geo G, const EnsArgs A) {
   constexpr int N = EnsRf::N, KC = EnsRf::KC, NT = EnsRf::NT, WMT = EnsRf::WMT, W = EnsRf::W;
   using TB = TabC<SCH>;
